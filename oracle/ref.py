@@ -1,0 +1,179 @@
+"""ctypes binding of the UNMODIFIED reference library (oracle/_ref).
+
+TEST INFRASTRUCTURE ONLY. ``oracle/Makefile`` compiles the reference's own
+sources (/root/reference/proj/src) together with ``ref_capi.cpp`` into
+``oracle/_ref/libeigmod_ref.so``; this module calls its entry points with
+numpy buffers. Errors are re-raised with the reference's semantics:
+``ValueError`` for std::invalid_argument, ``RefNumericalError`` (carrying the
+stage) for eigmod::NumericalError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_ref", "libeigmod_ref.so")
+_lib = None
+
+
+class RefNumericalError(RuntimeError):
+    def __init__(self, msg: str):
+        super().__init__(msg)
+        m = re.match(r"\[(\w+)\]", msg)
+        self.stage = m.group(1) if m else ""
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not available():
+            raise FileNotFoundError(f"{LIB_PATH} not built (run `make -C oracle ref`)")
+        _lib = C.CDLL(LIB_PATH)
+        _lib.ref_default_tolerance.restype = C.c_double
+    return _lib
+
+
+_D = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+_I = lambda a: a.ctypes.data_as(C.POINTER(C.c_int))  # noqa: E731
+_L = lambda a: a.ctypes.data_as(C.POINTER(C.c_int64))  # noqa: E731
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _check(rc: int, buf) -> None:
+    if rc == 0:
+        return
+    msg = buf.value.decode(errors="replace")
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 2:
+        raise RefNumericalError(msg)
+    raise RuntimeError(msg)
+
+
+def set_parallel(on: bool) -> None:
+    lib().ref_set_parallel(1 if on else 0)
+
+
+def worker_count() -> int:
+    return lib().ref_worker_count()
+
+
+def random_instance(n: int, k: int, norm: float, seed: int):
+    """core.hpp:17-20 — the reference's own seeded instance (signs all +1)."""
+    q = np.empty((n, n)); lam = np.empty(n); km = np.empty((n, k))
+    buf = C.create_string_buffer(512)
+    _check(lib().ref_random_instance(C.c_int64(n), C.c_int64(k), C.c_double(norm),
+                                     C.c_uint64(seed), _D(q), _D(lam), _D(km), buf, 512), buf)
+    return q, lam, km
+
+
+def transform_update(q, lam, kmat, signs):
+    q, lam, kmat, signs = _f64(q), _f64(lam), _f64(kmat), _i32(signs)
+    n, k = kmat.shape
+    u = np.empty((n, k))
+    buf = C.create_string_buffer(512)
+    _check(lib().ref_transform_update(_D(q), _D(lam), _D(kmat), _I(signs), C.c_int64(n),
+                                      C.c_int64(k), _D(u), buf, 512), buf)
+    return u
+
+
+def secular_weights(lam, u, signs):
+    lam, u, signs = _f64(lam), _f64(u), _i32(signs)
+    n, k = u.shape
+    out = np.empty(n)
+    buf = C.create_string_buffer(512)
+    _check(lib().ref_secular_weights(_D(lam), _D(u), _I(signs), C.c_int64(n), C.c_int64(k),
+                                     _D(out), buf, 512), buf)
+    return out
+
+
+def deflate_problem(lam, u, signs):
+    """secular.cpp:278-340 → dict(poles, weights, pole_origin, unchanged, collided)."""
+    lam, u, signs = _f64(lam), _f64(u), _i32(signs)
+    n, k = u.shape
+    poles = np.empty(n); w = np.empty(n)
+    po = np.empty(n, np.int64); un = np.empty(n, np.int64); co = np.empty(n, np.int64)
+    cnt = np.zeros(3, np.int64)
+    buf = C.create_string_buffer(512)
+    _check(lib().ref_deflate_problem(_D(lam), _D(u), _I(signs), C.c_int64(n), C.c_int64(k),
+                                     _D(poles), _D(w), _L(po), _L(un), _L(co), _L(cnt), buf,
+                                     512), buf)
+    m, nu, nc = (int(x) for x in cnt)
+    return dict(poles=poles[:m].copy(), weights=w[:m].copy(), pole_origin=po[:m].copy(),
+                unchanged=un[:nu].copy(), collided=co[:nc].copy())
+
+
+def default_tolerance(lam, kmat, signs):
+    lam, kmat, signs = _f64(lam), _f64(kmat), _i32(signs)
+    n, k = kmat.shape
+    return lib().ref_default_tolerance(_D(lam), _D(kmat), _I(signs), C.c_int64(n), C.c_int64(k))
+
+
+def update_eigenvalues_full(q, lam, kmat, signs, tol, sturm=False):
+    """rootfind.hpp:51-53 → (values, roots, seconds)."""
+    q, lam, kmat, signs = _f64(q), _f64(lam), _f64(kmat), _i32(signs)
+    n, k = kmat.shape
+    vals = np.empty(n); roots = np.empty(n); nr = np.zeros(1, np.int64); sec = np.zeros(1)
+    buf = C.create_string_buffer(1024)
+    _check(lib().ref_update_eigenvalues_full(_D(q), _D(lam), _D(kmat), _I(signs), C.c_int64(n),
+                                             C.c_int64(k), C.c_double(tol), C.c_int(1 if sturm else 0),
+                                             _D(vals), _D(roots), _L(nr), _D(sec), buf, 1024), buf)
+    return vals, roots[: int(nr[0])].copy(), float(sec[0])
+
+
+def update_pairs(q, lam, kmat, signs, tol, reorthogonalize=False):
+    """update_eigenvalues_full + assemble_eigenvectors → (lambda', Q', (t_eig, t_vec))."""
+    q, lam, kmat, signs = _f64(q), _f64(lam), _f64(kmat), _i32(signs)
+    n, k = kmat.shape
+    lo = np.empty(n); qo = np.empty((n, n)); sec = np.zeros(2)
+    buf = C.create_string_buffer(1024)
+    _check(lib().ref_update_pairs(_D(q), _D(lam), _D(kmat), _I(signs), C.c_int64(n), C.c_int64(k),
+                                  C.c_double(tol), C.c_int(1 if reorthogonalize else 0), _D(lo),
+                                  _D(qo), _D(sec), buf, 1024), buf)
+    return lo, qo, (float(sec[0]), float(sec[1]))
+
+
+def update_decomposition(q, lam, kmat, signs, tol, reorthogonalize=False):
+    """eigvec.hpp:35-36 → (lambda', Q', residual_fro, ortho_err, wall_time)."""
+    q, lam, kmat, signs = _f64(q), _f64(lam), _f64(kmat), _i32(signs)
+    n, k = kmat.shape
+    lo = np.empty(n); qo = np.empty((n, n)); met = np.zeros(3)
+    buf = C.create_string_buffer(1024)
+    _check(lib().ref_update_decomposition(_D(q), _D(lam), _D(kmat), _I(signs), C.c_int64(n),
+                                          C.c_int64(k), C.c_double(tol),
+                                          C.c_int(1 if reorthogonalize else 0), _D(lo), _D(qo),
+                                          _D(met), buf, 1024), buf)
+    return lo, qo, float(met[0]), float(met[1]), float(met[2])
+
+
+def jacobi_eigenvalues(a):
+    a = _f64(a)
+    n = a.shape[0]
+    out = np.empty(n)
+    buf = C.create_string_buffer(512)
+    _check(lib().ref_jacobi_eigenvalues(_D(a), C.c_int64(n), _D(out), buf, 512), buf)
+    return out
+
+
+def eval_secular(poles, weights, x, leading=1.0):
+    poles, weights = _f64(poles), _f64(weights)
+    f = np.zeros(1)
+    buf = C.create_string_buffer(512)
+    _check(lib().ref_eval_secular(_D(poles), _D(weights), C.c_int64(len(poles)),
+                                  C.c_double(leading), C.c_double(x), _D(f), buf, 512), buf)
+    return float(f[0])

@@ -1,0 +1,240 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product library.
+//
+// extern "C" shim over the UNMODIFIED reference library (eigmod, compiled
+// from /root/reference/proj/src by oracle/Makefile into oracle/_ref/). It lets
+// the Python tests, the golden-vector generator and bench.py's CPU-baseline
+// leg call the reference's own entry points through ctypes:
+//   transform_update          proj/include/eigmod/secular.hpp:28
+//   secular_weights           proj/include/eigmod/secular.hpp:34
+//   deflate_problem           proj/include/eigmod/secular.hpp:69
+//   update_eigenvalues_full   proj/include/eigmod/rootfind.hpp:51-53
+//   assemble_eigenvectors     proj/include/eigmod/eigvec.hpp:29-31
+//   update_decomposition      proj/include/eigmod/eigvec.hpp:35-36
+//   random_instance           proj/include/eigmod/core.hpp:17-20
+//   jacobi_evd                proj/include/eigmod/baseline.hpp:15
+// Return codes follow the product C-ABI (include/eigmod_b200.h):
+// 0 ok, 1 std::invalid_argument, 2 NumericalError (stage in the message
+// buffer as "[stage] msg"), 4 any other exception.
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+
+#include "eigmod/baseline.hpp"
+#include "eigmod/core.hpp"
+#include "eigmod/eigvec.hpp"
+#include "eigmod/kernels.hpp"
+#include "eigmod/rootfind.hpp"
+#include "eigmod/secular.hpp"
+#include "eigmod/types.hpp"
+
+using namespace eigmod;
+
+namespace {
+
+void put_msg(char* buf, std::size_t len, const std::string& s) {
+  if (!buf || len == 0) return;
+  std::size_t m = s.size() < len - 1 ? s.size() : len - 1;
+  std::memcpy(buf, s.data(), m);
+  buf[m] = 0;
+}
+
+template <class F>
+int guarded(char* msg, std::size_t len, F&& f) {
+  try {
+    f();
+    put_msg(msg, len, "");
+    return 0;
+  } catch (const NumericalError& e) {
+    put_msg(msg, len, e.what());
+    return 2;
+  } catch (const std::invalid_argument& e) {
+    put_msg(msg, len, e.what());
+    return 1;
+  } catch (const std::exception& e) {
+    put_msg(msg, len, e.what());
+    return 4;
+  }
+}
+
+Matrix to_matrix(const double* p, std::int64_t r, std::int64_t c) {
+  Matrix m(static_cast<std::size_t>(r), static_cast<std::size_t>(c));
+  if (r * c) std::memcpy(m.data(), p, sizeof(double) * r * c);
+  return m;
+}
+
+SpectralDecomposition to_decomp(const double* q, const double* lambda, std::int64_t n) {
+  SpectralDecomposition d;
+  d.q = to_matrix(q, n, n);
+  d.lambda.assign(lambda, lambda + n);
+  return d;
+}
+
+LowRankUpdate to_update(const double* kmat, const int* signs, std::int64_t n, std::int64_t k) {
+  LowRankUpdate u;
+  u.kmat = to_matrix(kmat, n, k);
+  u.signs.assign(signs, signs + k);
+  return u;
+}
+
+TransformedUpdate to_tu(const double* u, const int* signs, std::int64_t n, std::int64_t k) {
+  TransformedUpdate tu;
+  tu.u = to_matrix(u, n, k);
+  tu.signs.assign(signs, signs + k);
+  return tu;
+}
+
+void copy_vec(const Vec& v, double* out) {
+  if (!v.empty()) std::memcpy(out, v.data(), sizeof(double) * v.size());
+}
+
+void copy_idx(const std::vector<std::size_t>& v, std::int64_t* out) {
+  for (std::size_t i = 0; i < v.size(); ++i) out[i] = static_cast<std::int64_t>(v[i]);
+}
+
+}  // namespace
+
+extern "C" {
+
+void ref_set_parallel(int on) { kernels::set_parallel(on != 0); }
+int ref_worker_count() { return kernels::worker_count(); }
+
+int ref_random_instance(std::int64_t n, std::int64_t k, double norm, std::uint64_t seed, double* q,
+                        double* lambda, double* kmat, char* msg, std::size_t len) {
+  return guarded(msg, len, [&] {
+    auto [d, u] = random_instance(n, k, norm, seed);
+    std::memcpy(q, d.q.data(), sizeof(double) * n * n);
+    copy_vec(d.lambda, lambda);
+    std::memcpy(kmat, u.kmat.data(), sizeof(double) * n * k);
+  });
+}
+
+int ref_transform_update(const double* q, const double* lambda, const double* kmat,
+                         const int* signs, std::int64_t n, std::int64_t k, double* u_out,
+                         char* msg, std::size_t len) {
+  return guarded(msg, len, [&] {
+    const TransformedUpdate tu =
+        transform_update(to_decomp(q, lambda, n), to_update(kmat, signs, n, k));
+    std::memcpy(u_out, tu.u.data(), sizeof(double) * n * k);
+  });
+}
+
+int ref_secular_weights(const double* lambda, const double* u, const int* signs, std::int64_t n,
+                        std::int64_t k, double* alpha_out, char* msg, std::size_t len) {
+  return guarded(msg, len, [&] {
+    const Vec lam(lambda, lambda + n);
+    copy_vec(secular_weights(lam, to_tu(u, signs, n, k)), alpha_out);
+  });
+}
+
+// Deflation record. Output arrays must hold n entries each; counts are
+// written to counts[0..2] = (npoles, nunchanged, ncollided).
+int ref_deflate_problem(const double* lambda, const double* u, const int* signs, std::int64_t n,
+                        std::int64_t k, double* poles, double* weights, std::int64_t* pole_origin,
+                        std::int64_t* unchanged, std::int64_t* collided, std::int64_t* counts,
+                        char* msg, std::size_t len) {
+  return guarded(msg, len, [&] {
+    const Vec lam(lambda, lambda + n);
+    const DeflatedProblem dp = deflate_problem(lam, to_tu(u, signs, n, k));
+    copy_vec(dp.coeffs.poles, poles);
+    copy_vec(dp.coeffs.weights, weights);
+    copy_idx(dp.pole_origin, pole_origin);
+    copy_idx(dp.unchanged, unchanged);
+    copy_idx(dp.collided, collided);
+    counts[0] = static_cast<std::int64_t>(dp.coeffs.size());
+    counts[1] = static_cast<std::int64_t>(dp.unchanged.size());
+    counts[2] = static_cast<std::int64_t>(dp.collided.size());
+  });
+}
+
+double ref_default_tolerance(const double* lambda, const double* kmat, const int* signs,
+                             std::int64_t n, std::int64_t k) {
+  const Vec lam(lambda, lambda + n);
+  return default_tolerance(lam, to_update(kmat, signs, n, k));
+}
+
+// Eigenvalue stage. values_out (n), roots_out (n), nroots_out (1).
+// stage_seconds receives the wall time of the call.
+int ref_update_eigenvalues_full(const double* q, const double* lambda, const double* kmat,
+                                const int* signs, std::int64_t n, std::int64_t k, double tol,
+                                int strategy, double* values_out, double* roots_out,
+                                std::int64_t* nroots_out, double* stage_seconds, char* msg,
+                                std::size_t len) {
+  return guarded(msg, len, [&] {
+    const auto d = to_decomp(q, lambda, n);
+    const auto u = to_update(kmat, signs, n, k);
+    const auto t0 = std::chrono::steady_clock::now();
+    const EigenvalueUpdate plan = update_eigenvalues_full(
+        d, u, tol, strategy ? LocateStrategy::sturm : LocateStrategy::automatic);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (stage_seconds) *stage_seconds = std::chrono::duration<double>(t1 - t0).count();
+    copy_vec(plan.values, values_out);
+    copy_vec(plan.roots, roots_out);
+    *nroots_out = static_cast<std::int64_t>(plan.roots.size());
+  });
+}
+
+// Both stages, timed separately (the bench.cpp:188-222 split):
+// stage_seconds[0] = update_eigenvalues_full, [1] = assemble_eigenvectors.
+int ref_update_pairs(const double* q, const double* lambda, const double* kmat, const int* signs,
+                     std::int64_t n, std::int64_t k, double tol, int reorthogonalize,
+                     double* lambda_out, double* q_out, double* stage_seconds, char* msg,
+                     std::size_t len) {
+  return guarded(msg, len, [&] {
+    const auto d = to_decomp(q, lambda, n);
+    const auto u = to_update(kmat, signs, n, k);
+    const auto t0 = std::chrono::steady_clock::now();
+    const EigenvalueUpdate plan = update_eigenvalues_full(d, u, tol);
+    const auto t1 = std::chrono::steady_clock::now();
+    const SpectralDecomposition out = assemble_eigenvectors(d, plan, reorthogonalize != 0);
+    const auto t2 = std::chrono::steady_clock::now();
+    if (stage_seconds) {
+      stage_seconds[0] = std::chrono::duration<double>(t1 - t0).count();
+      stage_seconds[1] = std::chrono::duration<double>(t2 - t1).count();
+    }
+    copy_vec(out.lambda, lambda_out);
+    std::memcpy(q_out, out.q.data(), sizeof(double) * n * n);
+  });
+}
+
+// Full update with the reference's own metrics (residual_fro, ortho_err,
+// wall_time) in metrics[0..2].
+int ref_update_decomposition(const double* q, const double* lambda, const double* kmat,
+                             const int* signs, std::int64_t n, std::int64_t k, double tol,
+                             int reorthogonalize, double* lambda_out, double* q_out,
+                             double* metrics, char* msg, std::size_t len) {
+  return guarded(msg, len, [&] {
+    const UpdateResult r = update_decomposition(to_decomp(q, lambda, n),
+                                                to_update(kmat, signs, n, k), tol,
+                                                reorthogonalize != 0);
+    copy_vec(r.decomposition.lambda, lambda_out);
+    std::memcpy(q_out, r.decomposition.q.data(), sizeof(double) * n * n);
+    metrics[0] = r.residual_fro;
+    metrics[1] = r.ortho_err;
+    metrics[2] = r.wall_time;
+  });
+}
+
+// Eigenvalues of the symmetric matrix a (n x n) by the reference's Jacobi
+// oracle (ascending).
+int ref_jacobi_eigenvalues(const double* a, std::int64_t n, double* out, char* msg,
+                           std::size_t len) {
+  return guarded(msg, len, [&] {
+    const SymmetricDense s = SymmetricDense::from(to_matrix(a, n, n));
+    copy_vec(jacobi_evd(s).lambda, out);
+  });
+}
+
+// Secular function of the deflated problem (secular.hpp:44-47).
+int ref_eval_secular(const double* poles, const double* weights, std::int64_t m, double leading,
+                     double x, double* f_out, char* msg, std::size_t len) {
+  return guarded(msg, len, [&] {
+    const SecularCoefficients c =
+        make_secular(Vec(poles, poles + m), Vec(weights, weights + m), leading);
+    *f_out = eval_secular(c, x);
+  });
+}
+
+}  // extern "C"
