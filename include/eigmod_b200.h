@@ -1,0 +1,144 @@
+/* eigmod_b200 — C ABI of the B200 (sm_100a) rank-k symmetric eigen-update.
+ *
+ * Drop-in boundary for the hot path of the reference library "eigmod"
+ * (/root/reference/proj/include/eigmod/*.hpp): given A = Q diag(lambda) Q^T
+ * and a signed rank-k update K J K^T, compute the updated eigenpairs of
+ * A' = A + K J K^T. All matrices are dense row-major float64 with the
+ * reference's layout (types.hpp:14-44: (i,j) -> data[i*cols + j]); Q's
+ * columns are eigenvectors, lambda ascending, signs J_r in {+1,-1}.
+ *
+ * Plain pointers and sizes only. Host-pointer entry points mirror the
+ * reference's C++ functions one to one (cited per function); the
+ * *_device entry points take device pointers and run on the context's
+ * stream (benchmark and multi-GPU drivers).
+ *
+ * Return codes (every function):
+ *   EIGMOD_B200_OK                0
+ *   EIGMOD_B200_INVALID_ARGUMENT  1  -> std::invalid_argument in the reference
+ *   EIGMOD_B200_NUMERICAL         2  -> eigmod::NumericalError(stage, msg)
+ *   EIGMOD_B200_CUDA              3  -> device / driver failure
+ * eigmod_b200_last_error / eigmod_b200_last_stage describe the last failure
+ * of a context. There is no CPU fallback: without a usable sm_100 device
+ * every call fails with EIGMOD_B200_CUDA.
+ */
+#ifndef EIGMOD_B200_H
+#define EIGMOD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EIGMOD_B200_OK 0
+#define EIGMOD_B200_INVALID_ARGUMENT 1
+#define EIGMOD_B200_NUMERICAL 2
+#define EIGMOD_B200_CUDA 3
+
+typedef struct eigmod_b200_ctx eigmod_b200_ctx;
+
+/* ---- context --------------------------------------------------------- */
+/* One context per device and host thread (workspaces and the stream are
+ * owned by it; calls on one context must not overlap). */
+int eigmod_b200_ctx_create(int device, eigmod_b200_ctx** out);
+void eigmod_b200_ctx_destroy(eigmod_b200_ctx* ctx);
+/* Run on an existing cudaStream_t (e.g. torch's current stream). NULL
+ * restores the context's own stream. */
+int eigmod_b200_ctx_set_stream(eigmod_b200_ctx* ctx, void* cuda_stream);
+/* Options: "run_rel" = near-equal-pole run threshold relative to
+ * max(1,max|lambda|) used by the solve (1e-10 exact mode, the default;
+ * 1e-12 = the reference's kPoleMergeRelGap, secular.hpp:66). */
+int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value);
+const char* eigmod_b200_last_error(const eigmod_b200_ctx* ctx);
+const char* eigmod_b200_last_stage(const eigmod_b200_ctx* ctx);
+/* stats[0] secular roots, [1] decoupled pairs, [2] collided roots,
+ * [3] total S(x) evaluations, [4] max evaluations of one root,
+ * [5] padded rank, [6] effective rank, [7] pole groups. */
+int eigmod_b200_stats(const eigmod_b200_ctx* ctx, double* stats8);
+/* Bytes of device workspace currently held by the context. */
+int64_t eigmod_b200_workspace_bytes(const eigmod_b200_ctx* ctx);
+
+/* ---- host-pointer drop-ins ------------------------------------------- */
+/* U = Q^T K (replaces transform_update, secular.hpp:28 / secular.cpp:155-161).
+ * q: n x n, kmat: n x k, u_out: n x k. */
+int eigmod_b200_transform_update(eigmod_b200_ctx* ctx, const double* q, const double* kmat,
+                                 int64_t n, int64_t k, double* u_out);
+
+/* Raw per-pole weights alpha_i = w_i^T adj(M_i) J w_i of a strictly
+ * increasing spectrum (replaces secular_weights, secular.hpp:34 /
+ * secular.cpp:206-217). u: n x k, alpha_out: n. */
+int eigmod_b200_secular_weights(eigmod_b200_ctx* ctx, const double* lambda, const double* u,
+                                const int* signs, int64_t n, int64_t k, double* alpha_out);
+
+/* Deflation record of the reference (replaces deflate_problem,
+ * secular.hpp:59-69 / secular.cpp:278-340): poles, weights, pole_origin,
+ * unchanged, collided each sized n by the caller; counts[0..2] =
+ * (npoles, nunchanged, ncollided). */
+int eigmod_b200_deflate_problem(eigmod_b200_ctx* ctx, const double* lambda, const double* u,
+                                const int* signs, int64_t n, int64_t k, double* poles,
+                                double* weights, int64_t* pole_origin, int64_t* unchanged,
+                                int64_t* collided, int64_t* counts);
+
+/* Eigenvalue stage (replaces update_eigenvalues_full, rootfind.hpp:51-53 /
+ * rootfind.cpp:381-472, for both the rank-2 and the general rank-k entry):
+ * values_out (n, ascending), roots_out (n; the first *nroots_out are the
+ * secular roots, ascending). u_out (n x k, may be NULL) receives U = Q^T K
+ * (kept columns first, *k_eff_out of them; keep_out (k, may be NULL) their
+ * indices). tol must be > 0; it is accepted for API compatibility (the
+ * solver converges to ~1 ulp regardless). */
+int eigmod_b200_update_eigenvalues(eigmod_b200_ctx* ctx, const double* q, const double* lambda,
+                                   const double* kmat, const int* signs, int64_t n, int64_t k,
+                                   double tol, double* values_out, double* roots_out,
+                                   int64_t* nroots_out, double* u_out, int64_t* k_eff_out,
+                                   int64_t* keep_out);
+
+/* Full update (replaces update_decomposition, eigvec.hpp:35-36 /
+ * eigvec.cpp:366-395, and the assemble_eigenvectors stage, eigvec.hpp:29-31):
+ * lambda_out (n, ascending) and q_out (n x n; column j the eigenvector of
+ * lambda_out[j], the reference's merge order and sign rule). wall_time_out
+ * (may be NULL) receives the seconds spent on the update itself. */
+int eigmod_b200_update_decomposition(eigmod_b200_ctx* ctx, const double* q, const double* lambda,
+                                     const double* kmat, const int* signs, int64_t n, int64_t k,
+                                     double tol, double* lambda_out, double* q_out,
+                                     double* wall_time_out);
+
+/* ---- device-pointer pipeline ----------------------------------------- */
+/* Whole update on device buffers (one GPU). */
+int eigmod_b200_update_decomposition_device(eigmod_b200_ctx* ctx, const double* d_q,
+                                            const double* d_lambda, const double* d_kmat,
+                                            const int* signs, int64_t n, int64_t k,
+                                            double* d_lambda_out, double* d_q_out);
+
+/* Staged form for root/column partitioning across GPUs (one process per
+ * GPU; the collectives between stages are the caller's):
+ *   1. project:  U rows [col_lo, col_hi) = (Q^T K)[col_lo:col_hi]  -> d_u_out
+ *                ((col_hi-col_lo) x kp, kp = padded rank from
+ *                eigmod_b200_padded_rank(k)); all-gather to n x kp.
+ *   2. plan:     deflation + reduced problem from the full U (every rank).
+ *   3. solve:    roots [j0, j1) of the reduced problem -> d_rec_out
+ *                ((j1-j0) x eigmod_b200_record_width(kp) doubles);
+ *                all-gather to nroots records.
+ *   4. finish:   columns [c0, c1) of Q' (d_q_out, leading dimension ldq)
+ *                and all n eigenvalues (d_lambda_out) from all records. */
+int eigmod_b200_padded_rank(int64_t k);
+int eigmod_b200_record_width(int kp);
+int eigmod_b200_project_device(eigmod_b200_ctx* ctx, const double* d_q, const double* d_kmat,
+                               int64_t n, int64_t k, int64_t col_lo, int64_t col_hi,
+                               double* d_u_out);
+int eigmod_b200_plan_device(eigmod_b200_ctx* ctx, const double* d_lambda, const double* d_u,
+                            const int* signs, int64_t n, int64_t k, int64_t* nroots_out);
+int eigmod_b200_solve_device(eigmod_b200_ctx* ctx, int64_t j0, int64_t j1, double* d_rec_out);
+int eigmod_b200_finish_device(eigmod_b200_ctx* ctx, const double* d_q, const double* d_rec_all,
+                              int64_t c0, int64_t c1, double* d_lambda_out, double* d_q_out,
+                              int64_t ldq);
+
+/* Plain FP64 GEMM on the DMMA path: C (m x nn, ldc) = A (m x kk) B^T
+ * (B nn x kk), all row-major device buffers (validation / benchmarks). */
+int eigmod_b200_gemm_nt_device(eigmod_b200_ctx* ctx, const double* d_a, const double* d_b,
+                               int64_t m, int64_t nn, int64_t kk, double* d_c, int64_t ldc);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EIGMOD_B200_H */

@@ -1,0 +1,362 @@
+"""ctypes binding of the C ABI in include/eigmod_b200.h (lib/libeigmod_b200.so).
+
+This is the Python host side of the drop-in boundary. It mirrors the
+reference's entry points (proj/include/eigmod/*.hpp) with the same names,
+argument meaning and error behaviour:
+
+  transform_update         secular.hpp:28        U = Q^T K
+  secular_weights          secular.hpp:34        per-pole weights alpha
+  deflate_problem          secular.hpp:69        deflation record
+  update_eigenvalues_full  rootfind.hpp:51-53    eigenvalue stage (rank-2 and rank-k)
+  update_eigenvalues       rootfind.hpp:58
+  update_decomposition     eigvec.hpp:35-36      eigenvalues + eigenvectors
+
+std::invalid_argument -> ValueError; eigmod::NumericalError -> NumericalError
+(with .stage); device failures -> DeviceError. There is no CPU fallback: if
+the shared library or a B200 is missing, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libeigmod_b200.so")
+
+_lib = None
+_lock = threading.Lock()
+
+
+class NumericalError(RuntimeError):
+    """eigmod::NumericalError (proj/include/eigmod/types.hpp:79-87)."""
+
+    def __init__(self, stage: str, msg: str):
+        super().__init__(msg)
+        self.stage = stage
+
+
+class DeviceError(RuntimeError):
+    """CUDA / device failure (no CPU fallback exists)."""
+
+
+_D = C.POINTER(C.c_double)
+_I32 = C.POINTER(C.c_int)
+_I64 = C.POINTER(C.c_int64)
+_VP = C.c_void_p
+
+
+def _declare(lib):
+    sig = {
+        "eigmod_b200_ctx_create": (C.c_int, [C.c_int, C.POINTER(_VP)]),
+        "eigmod_b200_ctx_destroy": (None, [_VP]),
+        "eigmod_b200_ctx_set_stream": (C.c_int, [_VP, _VP]),
+        "eigmod_b200_set_option": (C.c_int, [_VP, C.c_char_p, C.c_double]),
+        "eigmod_b200_last_error": (C.c_char_p, [_VP]),
+        "eigmod_b200_last_stage": (C.c_char_p, [_VP]),
+        "eigmod_b200_stats": (C.c_int, [_VP, _D]),
+        "eigmod_b200_workspace_bytes": (C.c_int64, [_VP]),
+        "eigmod_b200_transform_update": (C.c_int, [_VP, _D, _D, C.c_int64, C.c_int64, _D]),
+        "eigmod_b200_secular_weights": (C.c_int, [_VP, _D, _D, _I32, C.c_int64, C.c_int64, _D]),
+        "eigmod_b200_deflate_problem": (C.c_int, [_VP, _D, _D, _I32, C.c_int64, C.c_int64, _D, _D,
+                                                  _I64, _I64, _I64, _I64]),
+        "eigmod_b200_update_eigenvalues": (C.c_int, [_VP, _D, _D, _D, _I32, C.c_int64, C.c_int64,
+                                                     C.c_double, _D, _D, _I64, _D, _I64, _I64]),
+        "eigmod_b200_update_decomposition": (C.c_int, [_VP, _D, _D, _D, _I32, C.c_int64,
+                                                       C.c_int64, C.c_double, _D, _D, _D]),
+        "eigmod_b200_update_decomposition_device": (C.c_int, [_VP, _VP, _VP, _VP, _I32, C.c_int64,
+                                                              C.c_int64, _VP, _VP]),
+        "eigmod_b200_padded_rank": (C.c_int, [C.c_int64]),
+        "eigmod_b200_record_width": (C.c_int, [C.c_int]),
+        "eigmod_b200_project_device": (C.c_int, [_VP, _VP, _VP, C.c_int64, C.c_int64, C.c_int64,
+                                                 C.c_int64, _VP]),
+        "eigmod_b200_plan_device": (C.c_int, [_VP, _VP, _VP, _I32, C.c_int64, C.c_int64, _I64]),
+        "eigmod_b200_solve_device": (C.c_int, [_VP, C.c_int64, C.c_int64, _VP]),
+        "eigmod_b200_finish_device": (C.c_int, [_VP, _VP, _VP, C.c_int64, C.c_int64, _VP, _VP,
+                                                C.c_int64]),
+        "eigmod_b200_gemm_nt_device": (C.c_int, [_VP, _VP, _VP, C.c_int64, C.c_int64, C.c_int64,
+                                                 _VP, C.c_int64]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return sig
+
+
+EXPORTED = None
+
+
+def lib():
+    """Loads lib/libeigmod_b200.so; raises if it was not built."""
+    global _lib, EXPORTED
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise DeviceError(f"{LIB_PATH} missing: run __graft_entry__.build() "
+                                  "(python -m paper_1706_00773_b200.build)")
+            _lib = C.CDLL(LIB_PATH)
+            EXPORTED = sorted(_declare(_lib))
+    return _lib
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _dp(a):
+    return a.ctypes.data_as(_D)
+
+
+class Context:
+    """One device context (stream + workspaces); not thread-safe."""
+
+    def __init__(self, device: int = 0):
+        self._l = lib()
+        h = _VP()
+        rc = self._l.eigmod_b200_ctx_create(int(device), C.byref(h))
+        if rc != 0:
+            raise DeviceError(f"eigmod_b200_ctx_create(device={device}) failed (rc={rc}): "
+                              "no usable sm_100 GPU")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._l.eigmod_b200_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc: int):
+        if rc == 0:
+            return
+        msg = (self._l.eigmod_b200_last_error(self.h) or b"").decode()
+        stage = (self._l.eigmod_b200_last_stage(self.h) or b"").decode()
+        if rc == 1:
+            raise ValueError(msg)
+        if rc == 2:
+            raise NumericalError(stage, msg)
+        raise DeviceError(msg)
+
+    def set_stream(self, stream_ptr: int | None):
+        self.check(self._l.eigmod_b200_ctx_set_stream(self.h, _VP(stream_ptr or 0)))
+
+    def set_option(self, key: str, value: float):
+        self.check(self._l.eigmod_b200_set_option(self.h, key.encode(), C.c_double(value)))
+
+    def stats(self) -> dict:
+        s = np.zeros(8)
+        self.check(self._l.eigmod_b200_stats(self.h, _dp(s)))
+        keys = ["roots", "decoupled", "collided", "evals", "max_evals", "kp", "k_eff", "groups"]
+        return {k: float(v) for k, v in zip(keys, s)}
+
+    def workspace_bytes(self) -> int:
+        return int(self._l.eigmod_b200_workspace_bytes(self.h))
+
+
+_default: dict[int, Context] = {}
+
+
+def default_context(device: int = 0) -> Context:
+    ctx = _default.get(device)
+    if ctx is None:
+        ctx = _default[device] = Context(device)
+    return ctx
+
+
+# --------------------------------------------------------------- host API
+@dataclass
+class DeflatedProblem:
+    """secular.hpp:59-64."""
+
+    poles: np.ndarray
+    weights: np.ndarray
+    pole_origin: np.ndarray
+    unchanged: np.ndarray
+    collided: np.ndarray
+    leading: float = 1.0
+
+
+@dataclass
+class EigenvalueUpdate:
+    """rootfind.hpp:40-45."""
+
+    values: np.ndarray
+    roots: np.ndarray
+    problem: DeflatedProblem | None
+    u: np.ndarray                      # transformed U (zero columns dropped)
+    signs: np.ndarray
+    keep: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int64))
+
+
+@dataclass
+class UpdateResult:
+    """types.hpp:71-76 (residual_fro / ortho_err filled on request)."""
+
+    lam: np.ndarray
+    q: np.ndarray
+    residual_fro: float = float("nan")
+    ortho_err: float = float("nan")
+    wall_time: float = 0.0
+
+
+def transform_update(q, kmat, ctx: Context | None = None) -> np.ndarray:
+    ctx = ctx or default_context()
+    q, kmat = _f64(q), _f64(kmat)
+    if kmat.ndim != 2 or q.shape != (kmat.shape[0], kmat.shape[0]):
+        raise ValueError("transform_update: dimension mismatch")
+    n, k = kmat.shape
+    u = np.empty((n, k))
+    ctx.check(ctx._l.eigmod_b200_transform_update(ctx.h, _dp(q), _dp(kmat), n, k, _dp(u)))
+    return u
+
+
+def secular_weights(lam, u, signs, ctx: Context | None = None) -> np.ndarray:
+    ctx = ctx or default_context()
+    lam, u, signs = _f64(lam), _f64(u), _i32(signs)
+    n, k = u.shape
+    if k == 0:
+        raise ValueError("secular_weights: k = 0")
+    if lam.shape[0] != n or signs.shape[0] != k:
+        raise ValueError("secular_weights: dimension mismatch")
+    out = np.empty(n)
+    ctx.check(ctx._l.eigmod_b200_secular_weights(ctx.h, _dp(lam), _dp(u),
+                                                  signs.ctypes.data_as(_I32), n, k, _dp(out)))
+    return out
+
+
+def deflate_problem(lam, u, signs, ctx: Context | None = None) -> DeflatedProblem:
+    ctx = ctx or default_context()
+    lam, u, signs = _f64(lam), _f64(u), _i32(signs)
+    n, k = u.shape
+    if lam.shape[0] != n:
+        raise ValueError("deflate_problem: dimension mismatch")
+    poles, w = np.empty(n), np.empty(n)
+    po, un, co = (np.empty(n, np.int64) for _ in range(3))
+    cnt = np.zeros(3, np.int64)
+    ctx.check(ctx._l.eigmod_b200_deflate_problem(
+        ctx.h, _dp(lam), _dp(u), signs.ctypes.data_as(_I32), n, k, _dp(poles), _dp(w),
+        po.ctypes.data_as(_I64), un.ctypes.data_as(_I64), co.ctypes.data_as(_I64),
+        cnt.ctypes.data_as(_I64)))
+    m, nu, nc = (int(x) for x in cnt)
+    return DeflatedProblem(poles[:m].copy(), w[:m].copy(), po[:m].copy(), un[:nu].copy(),
+                           co[:nc].copy())
+
+
+def _check_update(q, lam, kmat, signs):
+    if kmat.ndim != 2 or lam.ndim != 1 or q.shape != (lam.shape[0], lam.shape[0]):
+        raise ValueError("LowRankUpdate: dimension mismatch")
+    if kmat.shape[0] != lam.shape[0]:
+        raise ValueError("LowRankUpdate: dimension mismatch")
+    if signs.shape[0] != kmat.shape[1]:
+        raise ValueError("LowRankUpdate: signs size")
+
+
+def update_eigenvalues_full(q, lam, kmat, signs, tol, with_problem=True,
+                            ctx: Context | None = None) -> EigenvalueUpdate:
+    ctx = ctx or default_context()
+    q, lam, kmat, signs = _f64(q), _f64(lam), _f64(kmat), _i32(signs)
+    _check_update(q, lam, kmat, signs)
+    n, k = kmat.shape
+    vals, roots = np.empty(n), np.empty(n)
+    nr, keff = np.zeros(1, np.int64), np.zeros(1, np.int64)
+    u = np.empty(n * k)
+    keep = np.zeros(k, np.int64)
+    ctx.check(ctx._l.eigmod_b200_update_eigenvalues(
+        ctx.h, _dp(q), _dp(lam), _dp(kmat), signs.ctypes.data_as(_I32), n, k, C.c_double(tol),
+        _dp(vals), _dp(roots), nr.ctypes.data_as(_I64), _dp(u), keff.ctypes.data_as(_I64),
+        keep.ctypes.data_as(_I64)))
+    ke = int(keff[0])
+    uk = u[: n * ke].reshape(n, ke).copy()
+    sg = signs[keep[:ke]].copy()
+    prob = None
+    if with_problem and ke > 0:
+        prob = deflate_problem(lam, uk, sg, ctx=ctx)
+    elif with_problem:
+        prob = DeflatedProblem(np.zeros(0), np.zeros(0), np.zeros(0, np.int64),
+                               np.arange(n, dtype=np.int64), np.zeros(0, np.int64))
+    return EigenvalueUpdate(vals, roots[: int(nr[0])].copy(), prob, uk, sg, keep[:ke].copy())
+
+
+def update_eigenvalues(q, lam, kmat, signs, tol, ctx: Context | None = None) -> np.ndarray:
+    return update_eigenvalues_full(q, lam, kmat, signs, tol, with_problem=False, ctx=ctx).values
+
+
+def update_decomposition(q, lam, kmat, signs, tol, metrics=False,
+                         ctx: Context | None = None) -> UpdateResult:
+    ctx = ctx or default_context()
+    q, lam, kmat, signs = _f64(q), _f64(lam), _f64(kmat), _i32(signs)
+    _check_update(q, lam, kmat, signs)
+    n, k = kmat.shape
+    lo = np.empty(n)
+    qo = np.empty((n, n))
+    wt = np.zeros(1)
+    ctx.check(ctx._l.eigmod_b200_update_decomposition(
+        ctx.h, _dp(q), _dp(lam), _dp(kmat), signs.ctypes.data_as(_I32), n, k, C.c_double(tol),
+        _dp(lo), _dp(qo), _dp(wt)))
+    res = UpdateResult(lo, qo, wall_time=float(wt[0]))
+    if metrics:  # eigvec.cpp:384-393 (validation only, outside the timed update)
+        target = q @ np.diag(lam) @ q.T + kmat @ np.diag(signs.astype(float)) @ kmat.T
+        target = 0.5 * (target + target.T)
+        got = qo @ np.diag(lo) @ qo.T
+        got = 0.5 * (got + got.T)
+        res.residual_fro = float(np.linalg.norm(got - target))
+        res.ortho_err = float(np.abs(qo.T @ qo - np.eye(n)).max())
+    return res
+
+
+def default_tolerance(lam, kmat) -> float:
+    """rootfind.cpp:306-312."""
+    scale = max(1.0, float(np.max(np.abs(lam))) if len(lam) else 1.0)
+    kn = float(np.linalg.norm(kmat))
+    return 1e-12 * max(scale, kn * kn)
+
+
+# --------------------------------------------------------- device (torch) API
+def _ptr(t):
+    return _VP(t.data_ptr())
+
+
+def padded_rank(k: int) -> int:
+    return int(lib().eigmod_b200_padded_rank(int(k)))
+
+
+def record_width(kp: int) -> int:
+    return int(lib().eigmod_b200_record_width(int(kp)))
+
+
+def update_decomposition_device(q, lam, kmat, signs, lam_out, q_out, ctx: Context | None = None):
+    """All-device update on torch CUDA float64 tensors (runs on torch's
+    current stream)."""
+    import torch
+
+    ctx = ctx or default_context(q.device.index or 0)
+    ctx.set_stream(torch.cuda.current_stream(q.device).cuda_stream)
+    sg = _i32(np.asarray(signs))
+    n, k = kmat.shape
+    ctx.check(ctx._l.eigmod_b200_update_decomposition_device(
+        ctx.h, _ptr(q), _ptr(lam), _ptr(kmat), sg.ctypes.data_as(_I32), n, k, _ptr(lam_out),
+        _ptr(q_out)))
+
+
+def gemm_nt_device(a, b, c, ctx: Context | None = None):
+    import torch
+
+    ctx = ctx or default_context(a.device.index or 0)
+    ctx.set_stream(torch.cuda.current_stream(a.device).cuda_stream)
+    m, kk = a.shape
+    nn = b.shape[0]
+    ctx.check(ctx._l.eigmod_b200_gemm_nt_device(ctx.h, _ptr(a), _ptr(b), m, nn, kk, _ptr(c),
+                                                 c.stride(0)))

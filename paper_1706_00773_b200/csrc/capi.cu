@@ -1,0 +1,593 @@
+// C ABI (include/eigmod_b200.h) over the sm_100a pipeline.
+//
+// Orchestration of one update on one device:
+//   K1 transform_update_dev   U = Q^T K            (deflate.cu)
+//      column drop            rootfind.cpp:318-340 (norms on device, decision on host)
+//   K2 build_plan_dev         runs, alpha, classification, reduced problem
+//   K3 solve_roots            all roots of the reduced problem (secular.cu)
+//   K4 merge/build_xt         column order + eigenvector rows (eigvec.cu)
+//   K5 back_transform_dev     Q' = Q X, norms and sign rule (gemm.cu)
+// Host work is limited to argument validation, a handful of scalar/size
+// read-backs between stages and the bookkeeping of the reference's output
+// lists; every O(n^2) or larger step runs on the GPU.
+#include <algorithm>
+#include <cfloat>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/eigmod_b200.h"
+#include "pipeline.cuh"
+
+using eigb::Error;
+
+struct eigmod_b200_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr, stream = nullptr;
+  int sms = 148;
+  eigb::DeviceScratch ws;
+  eigb::Plan plan;
+  bool have_plan = false;
+  eigb::RootRecords recs{};
+  double run_rel = eigb::kExactRunRelGap;
+  const double* lam = nullptr;  // lambda of the current plan (rank-0 copy)
+  std::string err, stage;
+};
+
+namespace {
+
+constexpr int kRecHead = 5;  // value, origin, delta, flags, evals
+
+void check_basic(int64_t n, int64_t k, const int* signs) {
+  // proj/src/core.cpp:89-97 (validate_update)
+  if (n < 1) throw Error(1, "", "LowRankUpdate: dimension mismatch");
+  if (k < 1 || k > n) throw Error(1, "", "LowRankUpdate: rank out of range");
+  if (k > eigb::kMaxRank) throw Error(1, "", "LowRankUpdate: rank above 32 is not supported");
+  if (signs)
+    for (int64_t r = 0; r < k; ++r)
+      if (signs[r] != 1 && signs[r] != -1)
+        throw Error(1, "", "LowRankUpdate: signs must be +1/-1");
+}
+
+void check_finite(const double* p, int64_t cnt, const char* what) {
+  for (int64_t i = 0; i < cnt; ++i)
+    if (!std::isfinite(p[i])) throw Error(1, "", std::string("LowRankUpdate: non-finite ") + what);
+}
+
+void check_ascending(const double* lam, int64_t n) {
+  // proj/src/secular.cpp:281-283, surfaced as NumericalError("deflate")
+  for (int64_t i = 0; i + 1 < n; ++i)
+    if (!(lam[i] <= lam[i + 1]))
+      throw Error(2, "deflate", "deflate_problem: eigenvalues not ascending");
+}
+
+template <class F>
+int guarded(eigmod_b200_ctx* ctx, F&& f) {
+  if (!ctx) return EIGMOD_B200_INVALID_ARGUMENT;
+  try {
+    EIGB_CUDA(cudaSetDevice(ctx->device));
+    f();
+    ctx->err.clear();
+    ctx->stage.clear();
+    return EIGMOD_B200_OK;
+  } catch (const Error& e) {
+    ctx->err = e.what();
+    ctx->stage = e.stage;
+    return e.code;
+  } catch (const std::exception& e) {
+    ctx->err = e.what();
+    ctx->stage = "cuda";
+    return EIGMOD_B200_CUDA;
+  }
+}
+
+// ---------------------------------------------------------------- stages
+void project(eigmod_b200_ctx* c, const double* q, const double* kmat, int64_t n, int64_t k,
+             int64_t lo, int64_t hi, double* u_out) {
+  const int kp = eigb::padded_rank(k);
+  eigb::transform_update_dev(q, kmat, n, (int)k, kp, lo, hi, u_out, c->ws, c->sms, c->stream);
+}
+
+void plan_from_u(eigmod_b200_ctx* c, const double* lam, const double* u, const int* signs,
+                 int64_t n, int64_t k, double run_rel) {
+  eigb::Plan& p = c->plan;
+  p = eigb::Plan{};
+  p.run_rel = run_rel;
+  c->lam = lam;
+  const int kp = eigb::padded_rank(k);
+  double* norms = c->ws.get_f64("cap_norms", k);
+  eigb::column_norms2_dev(u, n, kp, (int)k, norms, c->stream);
+  std::vector<double> nh(k);
+  EIGB_CUDA(cudaMemcpyAsync(nh.data(), norms, 8 * k, cudaMemcpyDeviceToHost, c->stream));
+  EIGB_CUDA(cudaStreamSynchronize(c->stream));
+  // proj/src/rootfind.cpp:318-340: drop columns with norm <= 1e-15 max(1, max)
+  double maxnorm = 0.0;
+  for (auto& v : nh) v = std::sqrt(v), maxnorm = std::max(maxnorm, v);
+  const double drop = eigb::kColumnDropRel * std::max(1.0, maxnorm);
+  for (int64_t j = 0; j < k; ++j)
+    if (nh[j] > drop) p.keep_h.push_back((int)j);
+  p.n = n;
+  p.k = (int)p.keep_h.size();
+  if (p.k == 0) {  // rootfind.cpp:394-399: nothing couples
+    p.kp = 0;
+    p.nred = 0;
+    p.ndec = n;
+    c->have_plan = true;
+    return;
+  }
+  p.kp = eigb::padded_rank(p.k);
+  p.u = c->ws.get_f64("pl_u", (size_t)n * p.kp);
+  int* keep_d = c->ws.get_i32("cap_keep", p.k);
+  EIGB_CUDA(cudaMemcpyAsync(keep_d, p.keep_h.data(), 4 * p.k, cudaMemcpyHostToDevice, c->stream));
+  eigb::repack_columns_dev(u, n, kp, keep_d, p.k, p.kp, p.u, c->stream);
+  p.sgn_h.clear();
+  p.m_neg = 0;
+  std::vector<int> sp(p.kp, 1);
+  for (int r = 0; r < p.k; ++r) {
+    sp[r] = signs[p.keep_h[r]];
+    p.sgn_h.push_back(sp[r]);
+    p.m_neg += sp[r] < 0;
+  }
+  p.sgn = c->ws.get_i32("pl_sgn", p.kp);
+  EIGB_CUDA(cudaMemcpyAsync(p.sgn, sp.data(), 4 * p.kp, cudaMemcpyHostToDevice, c->stream));
+  eigb::build_plan_dev(p, lam, n, run_rel, c->ws, c->stream);
+  c->have_plan = true;
+}
+
+eigb::RootRecords alloc_records(eigmod_b200_ctx* c) {
+  const int64_t nr = std::max<int64_t>(c->plan.nred, 1);
+  const int kp = std::max(c->plan.kp, 1);
+  eigb::RootRecords r;
+  r.value = c->ws.get_f64("rec_value", nr);
+  r.origin = c->ws.get_i64("rec_origin", nr);
+  r.delta = c->ws.get_f64("rec_delta", nr);
+  r.flags = c->ws.get_i32("rec_flags", nr);
+  r.evals = c->ws.get_i32("rec_evals", nr);
+  r.y = c->ws.get_f64("rec_y", (size_t)nr * kp);
+  return r;
+}
+
+__global__ void pack_records_kernel(eigb::RootRecords r, int64_t j0, int64_t cnt, int kp,
+                                    double* out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  const int64_t j = j0 + t;
+  double* o = out + t * (kRecHead + kp);
+  o[0] = r.value[j];
+  o[1] = (double)r.origin[j];
+  o[2] = r.delta[j];
+  o[3] = (double)r.flags[j];
+  o[4] = (double)r.evals[j];
+  for (int c = 0; c < kp; ++c) o[kRecHead + c] = r.y[j * kp + c];
+}
+
+__global__ void unpack_records_kernel(const double* in, int64_t cnt, int kp, eigb::RootRecords r) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cnt) return;
+  const double* o = in + j * (kRecHead + kp);
+  r.value[j] = o[0];
+  r.origin[j] = (int64_t)o[1];
+  r.delta[j] = o[2];
+  r.flags[j] = (int)o[3];
+  r.evals[j] = (int)o[4];
+  for (int c = 0; c < kp; ++c) r.y[j * kp + c] = o[kRecHead + c];
+}
+
+void solve(eigmod_b200_ctx* c, int64_t j0, int64_t j1) {
+  if (!c->have_plan) throw Error(1, "", "solve: no plan (call plan first)");
+  c->recs = alloc_records(c);
+  if (c->plan.nred == 0) return;
+  eigb::solve_roots(c->plan.view(), j0, j1, c->recs, c->ws, c->sms, c->stream);
+}
+
+__global__ void copy_block_kernel(const double* __restrict__ a, int64_t n, int64_t c0, int64_t nc,
+                                  double* __restrict__ out, int64_t ldo) {
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x)
+    for (int64_t j = threadIdx.x; j < nc; j += blockDim.x) out[i * ldo + j] = a[i * n + c0 + j];
+}
+
+void finish(eigmod_b200_ctx* c, const double* q, const double* lam_in, int64_t c0, int64_t c1,
+            double* lam_out, double* q_out, int64_t ldq) {
+  eigb::Plan& p = c->plan;
+  const int64_t n = p.n;
+  if (!lam_in) lam_in = c->lam;
+  if (p.k == 0) {  // unchanged pairs: lambda and Q copied exactly
+    if (lam_out)
+      EIGB_CUDA(cudaMemcpyAsync(lam_out, lam_in, 8 * n, cudaMemcpyDeviceToDevice, c->stream));
+    if (q_out && c1 > c0) {
+      copy_block_kernel<<<1024, 256, 0, c->stream>>>(q, n, c0, c1 - c0, q_out, ldq);
+      EIGB_LAUNCH_CHECK();
+    }
+    return;
+  }
+  eigb::Columns cols;
+  eigb::merge_columns_dev(p, c->recs, cols, c->ws, c->stream);
+  if (lam_out)
+    EIGB_CUDA(cudaMemcpyAsync(lam_out, cols.value, 8 * n, cudaMemcpyDeviceToDevice, c->stream));
+  if (!q_out || c1 <= c0) return;
+  double* colldir = c->ws.get_f64("colldir", (size_t)std::max<int64_t>(p.nred, 1) * (p.kp + 1));
+  int* collok = c->ws.get_i32("collok", std::max<int64_t>(p.nred, 1));
+  eigb::collision_vectors_dev(p, c->recs, colldir, collok, c->ws, c->stream);
+  const int64_t nc = c1 - c0;
+  double* xt = c->ws.get_f64("xt", (size_t)nc * n);
+  double* colscale = c->ws.get_f64("colscale", nc);
+  int* cmode = c->ws.get_i32("colmode", nc);
+  eigb::build_xt_dev(p, c->recs, cols, colldir, collok, c0, c1, xt, colscale, cmode, c->stream);
+  eigb::back_transform_dev(q, xt, n, nc, colscale, cmode, q_out, ldq, c->ws, c->stream);
+}
+
+void full_device(eigmod_b200_ctx* c, const double* q, const double* lam, const double* kmat,
+                 const int* signs, int64_t n, int64_t k, double* lam_out, double* q_out) {
+  const int kp = eigb::padded_rank(k);
+  double* u = c->ws.get_f64("cap_u_full", (size_t)n * kp);
+  project(c, q, kmat, n, k, 0, n, u);
+  plan_from_u(c, lam, u, signs, n, k, c->run_rel);
+  solve(c, 0, c->plan.nred);
+  finish(c, q, lam, 0, n, lam_out, q_out, n);
+}
+
+}  // namespace
+
+extern "C" {
+
+int eigmod_b200_ctx_create(int device, eigmod_b200_ctx** out) {
+  if (!out) return EIGMOD_B200_INVALID_ARGUMENT;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return EIGMOD_B200_CUDA;
+  if (device < 0 || device >= ndev) return EIGMOD_B200_INVALID_ARGUMENT;
+  auto* c = new eigmod_b200_ctx;
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return EIGMOD_B200_CUDA;
+  }
+  c->stream = c->own;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  if (major != 10) {  // sm_100a kernels only
+    cudaStreamDestroy(c->own);
+    delete c;
+    return EIGMOD_B200_CUDA;
+  }
+  *out = c;
+  return EIGMOD_B200_OK;
+}
+
+void eigmod_b200_ctx_destroy(eigmod_b200_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->ws.release();
+  cudaStreamDestroy(ctx->own);
+  delete ctx;
+}
+
+int eigmod_b200_ctx_set_stream(eigmod_b200_ctx* ctx, void* s) {
+  return guarded(ctx, [&] { ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own; });
+}
+
+int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) {
+  return guarded(ctx, [&] {
+    if (!key) throw Error(1, "", "set_option: null key");
+    if (std::string(key) == "run_rel") {
+      if (!(value > 0.0 && value < 1e-3)) throw Error(1, "", "set_option: run_rel out of range");
+      ctx->run_rel = value;
+    } else {
+      throw Error(1, "", std::string("set_option: unknown key ") + key);
+    }
+  });
+}
+
+const char* eigmod_b200_last_error(const eigmod_b200_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : "null context";
+}
+const char* eigmod_b200_last_stage(const eigmod_b200_ctx* ctx) {
+  return ctx ? ctx->stage.c_str() : "";
+}
+
+int eigmod_b200_stats(const eigmod_b200_ctx* cctx, double* s) {
+  auto* ctx = const_cast<eigmod_b200_ctx*>(cctx);
+  return guarded(ctx, [&] {
+    for (int i = 0; i < 8; ++i) s[i] = 0.0;
+    if (!ctx->have_plan) return;
+    const eigb::Plan& p = ctx->plan;
+    s[0] = (double)p.nred;
+    s[1] = (double)p.ndec;
+    s[5] = p.kp;
+    s[6] = p.k;
+    s[7] = (double)p.ng;
+    if (p.nred > 0 && ctx->recs.evals) {
+      std::vector<int> ev(p.nred), fl(p.nred);
+      EIGB_CUDA(cudaMemcpyAsync(ev.data(), ctx->recs.evals, 4 * p.nred, cudaMemcpyDeviceToHost, ctx->stream));
+      EIGB_CUDA(cudaMemcpyAsync(fl.data(), ctx->recs.flags, 4 * p.nred, cudaMemcpyDeviceToHost, ctx->stream));
+      EIGB_CUDA(cudaStreamSynchronize(ctx->stream));
+      double tot = 0, mx = 0, col = 0;
+      for (int64_t j = 0; j < p.nred; ++j) {
+        tot += ev[j];
+        mx = std::max(mx, (double)ev[j]);
+        col += (fl[j] & 1);
+      }
+      s[2] = col;
+      s[3] = tot;
+      s[4] = mx;
+    }
+  });
+}
+
+int64_t eigmod_b200_workspace_bytes(const eigmod_b200_ctx* ctx) {
+  return ctx ? (int64_t)ctx->ws.bytes() : 0;
+}
+
+int eigmod_b200_padded_rank(int64_t k) { return eigb::padded_rank(k); }
+int eigmod_b200_record_width(int kp) { return kRecHead + kp; }
+
+// ------------------------------------------------------- host drop-ins
+int eigmod_b200_transform_update(eigmod_b200_ctx* ctx, const double* q, const double* kmat,
+                                 int64_t n, int64_t k, double* u_out) {
+  return guarded(ctx, [&] {
+    if (!q || !kmat || !u_out) throw Error(1, "", "transform_update: null pointer");
+    check_basic(n, k, nullptr);
+    const int kp = eigb::padded_rank(k);
+    double* dq = ctx->ws.get_f64("h_q", (size_t)n * n);
+    double* dk = ctx->ws.get_f64("h_k", (size_t)n * k);
+    double* du = ctx->ws.get_f64("h_u", (size_t)n * kp);
+    EIGB_CUDA(cudaMemcpyAsync(dq, q, 8 * n * n, cudaMemcpyHostToDevice, ctx->stream));
+    EIGB_CUDA(cudaMemcpyAsync(dk, kmat, 8 * n * k, cudaMemcpyHostToDevice, ctx->stream));
+    project(ctx, dq, dk, n, k, 0, n, du);
+    std::vector<double> up((size_t)n * kp);
+    EIGB_CUDA(cudaMemcpyAsync(up.data(), du, 8 * n * kp, cudaMemcpyDeviceToHost, ctx->stream));
+    EIGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t c = 0; c < k; ++c) u_out[i * k + c] = up[i * kp + c];
+  });
+}
+
+int eigmod_b200_secular_weights(eigmod_b200_ctx* ctx, const double* lambda, const double* u,
+                                const int* signs, int64_t n, int64_t k, double* alpha_out) {
+  return guarded(ctx, [&] {
+    if (k < 1) throw Error(1, "", "secular_weights: k = 0");
+    check_basic(n, k, signs);
+    for (int64_t i = 0; i + 1 < n; ++i)
+      if (!(lambda[i] < lambda[i + 1]))
+        throw Error(1, "", "secular_weights: poles not strictly increasing");
+    for (int64_t i = 0; i < n; ++i)
+      if (!std::isfinite(lambda[i])) throw Error(1, "", "secular_weights: non-finite pole");
+    const int kp = eigb::padded_rank(k);
+    std::vector<double> up((size_t)n * kp, 0.0);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t c = 0; c < k; ++c) up[i * kp + c] = u[i * k + c];
+    std::vector<int64_t> gs(n), gl(n, 1);
+    for (int64_t i = 0; i < n; ++i) gs[i] = i;
+    std::vector<int> sp(kp, 1);
+    for (int64_t r = 0; r < k; ++r) sp[r] = signs[r];
+    double* du = ctx->ws.get_f64("sw_u", up.size());
+    double* dl = ctx->ws.get_f64("sw_l", n);
+    int64_t* dgs = ctx->ws.get_i64("sw_gs", n);
+    int64_t* dgl = ctx->ws.get_i64("sw_gl", n);
+    int* dsg = ctx->ws.get_i32("sw_sg", kp);
+    double* da = ctx->ws.get_f64("sw_a", n);
+    auto st = ctx->stream;
+    EIGB_CUDA(cudaMemcpyAsync(du, up.data(), 8 * up.size(), cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dl, lambda, 8 * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dgs, gs.data(), 8 * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dgl, gl.data(), 8 * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dsg, sp.data(), 4 * kp, cudaMemcpyHostToDevice, st));
+    eigb::group_weights(kp, dl, du, n, dgs, dgl, dl, n, dsg, (int)k, da, ctx->ws, st);
+    EIGB_CUDA(cudaMemcpyAsync(alpha_out, da, 8 * n, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int eigmod_b200_deflate_problem(eigmod_b200_ctx* ctx, const double* lambda, const double* u,
+                                const int* signs, int64_t n, int64_t k, double* poles,
+                                double* weights, int64_t* pole_origin, int64_t* unchanged,
+                                int64_t* collided, int64_t* counts) {
+  return guarded(ctx, [&] {
+    check_basic(n, k, signs);
+    for (int64_t i = 0; i + 1 < n; ++i)
+      if (!(lambda[i] <= lambda[i + 1]))
+        throw Error(1, "", "deflate_problem: eigenvalues not ascending");
+    const int kp = eigb::padded_rank(k);
+    std::vector<double> up((size_t)n * kp, 0.0);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t c = 0; c < k; ++c) up[i * kp + c] = u[i * k + c];
+    std::vector<int> sp(kp, 1);
+    int m_neg = 0;
+    for (int64_t r = 0; r < k; ++r) sp[r] = signs[r], m_neg += signs[r] < 0;
+    auto st = ctx->stream;
+    eigb::Plan p;
+    p.k = (int)k;
+    p.kp = kp;
+    p.m_neg = m_neg;
+    p.u = ctx->ws.get_f64("dp_u", up.size());
+    p.sgn = ctx->ws.get_i32("dp_sg", kp);
+    double* dl = ctx->ws.get_f64("dp_l", n);
+    EIGB_CUDA(cudaMemcpyAsync(p.u, up.data(), 8 * up.size(), cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(p.sgn, sp.data(), 4 * kp, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dl, lambda, 8 * n, cudaMemcpyHostToDevice, st));
+    // parity record: the reference's run threshold (secular.hpp:66)
+    eigb::build_plan_dev(p, dl, n, eigb::kPoleMergeRelGap, ctx->ws, st);
+    const int64_t ng = p.ng;
+    std::vector<int64_t> gs(ng), gl(ng);
+    std::vector<double> gv(ng), al(ng);
+    std::vector<int> kd(ng);
+    EIGB_CUDA(cudaMemcpyAsync(gs.data(), p.gstart, 8 * ng, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaMemcpyAsync(gl.data(), p.glen, 8 * ng, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaMemcpyAsync(gv.data(), p.gval, 8 * ng, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaMemcpyAsync(al.data(), p.alpha, 8 * ng, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaMemcpyAsync(kd.data(), p.kind, 4 * ng, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaStreamSynchronize(st));
+    int64_t np = 0, nu = 0, nc = 0;  // secular.cpp:316-337 output order
+    for (int64_t g = 0; g < ng; ++g) {
+      if (kd[g] == 1) {
+        for (int64_t i = gs[g]; i < gs[g] + gl[g]; ++i) unchanged[nu++] = i;
+        continue;
+      }
+      if (kd[g] == 2) {
+        collided[nc++] = gs[g];
+      } else {
+        poles[np] = gv[g];
+        weights[np] = al[g];
+        pole_origin[np] = gs[g];
+        ++np;
+      }
+      for (int64_t i = gs[g] + 1; i < gs[g] + gl[g]; ++i) unchanged[nu++] = i;
+    }
+    counts[0] = np;
+    counts[1] = nu;
+    counts[2] = nc;
+  });
+}
+
+int eigmod_b200_update_eigenvalues(eigmod_b200_ctx* ctx, const double* q, const double* lambda,
+                                   const double* kmat, const int* signs, int64_t n, int64_t k,
+                                   double tol, double* values_out, double* roots_out,
+                                   int64_t* nroots_out, double* u_out, int64_t* k_eff_out,
+                                   int64_t* keep_out) {
+  return guarded(ctx, [&] {
+    check_basic(n, k, signs);
+    check_finite(kmat, n * k, "K");
+    if (!(tol > 0.0)) throw Error(1, "", "update_eigenvalues: tol must be positive");
+    check_ascending(lambda, n);
+    auto st = ctx->stream;
+    const int kp = eigb::padded_rank(k);
+    double* dq = ctx->ws.get_f64("h_q", (size_t)n * n);
+    double* dl = ctx->ws.get_f64("h_l", n);
+    double* dk = ctx->ws.get_f64("h_k", (size_t)n * k);
+    double* du = ctx->ws.get_f64("h_u", (size_t)n * kp);
+    double* dlo = ctx->ws.get_f64("h_lo", n);
+    EIGB_CUDA(cudaMemcpyAsync(dq, q, 8 * n * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dl, lambda, 8 * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dk, kmat, 8 * n * k, cudaMemcpyHostToDevice, st));
+    project(ctx, dq, dk, n, k, 0, n, du);
+    plan_from_u(ctx, dl, du, signs, n, k, ctx->run_rel);
+    solve(ctx, 0, ctx->plan.nred);
+    finish(ctx, dq, dl, 0, 0, dlo, nullptr, n);
+    const eigb::Plan& p = ctx->plan;
+    EIGB_CUDA(cudaMemcpyAsync(values_out, dlo, 8 * n, cudaMemcpyDeviceToHost, st));
+    if (roots_out && p.nred > 0)
+      EIGB_CUDA(cudaMemcpyAsync(roots_out, ctx->recs.value, 8 * p.nred, cudaMemcpyDeviceToHost, st));
+    if (u_out && p.k > 0) {
+      std::vector<double> up((size_t)n * p.kp);
+      EIGB_CUDA(cudaMemcpyAsync(up.data(), p.u, 8 * up.size(), cudaMemcpyDeviceToHost, st));
+      EIGB_CUDA(cudaStreamSynchronize(st));
+      for (int64_t i = 0; i < n; ++i)
+        for (int c = 0; c < p.k; ++c) u_out[i * p.k + c] = up[i * p.kp + c];
+    }
+    EIGB_CUDA(cudaStreamSynchronize(st));
+    if (roots_out && p.nred > 1) std::sort(roots_out, roots_out + p.nred);
+    if (nroots_out) *nroots_out = p.nred;
+    if (k_eff_out) *k_eff_out = p.k;
+    if (keep_out)
+      for (int c = 0; c < p.k; ++c) keep_out[c] = p.keep_h[c];
+  });
+}
+
+int eigmod_b200_update_decomposition(eigmod_b200_ctx* ctx, const double* q, const double* lambda,
+                                     const double* kmat, const int* signs, int64_t n, int64_t k,
+                                     double tol, double* lambda_out, double* q_out,
+                                     double* wall_time_out) {
+  return guarded(ctx, [&] {
+    check_basic(n, k, signs);
+    check_finite(kmat, n * k, "K");
+    if (!(tol > 0.0)) throw Error(1, "", "update_eigenvalues: tol must be positive");
+    check_ascending(lambda, n);
+    auto st = ctx->stream;
+    const auto t0 = std::chrono::steady_clock::now();
+    double* dq = ctx->ws.get_f64("h_q", (size_t)n * n);
+    double* dl = ctx->ws.get_f64("h_l", n);
+    double* dk = ctx->ws.get_f64("h_k", (size_t)n * k);
+    double* dlo = ctx->ws.get_f64("h_lo", n);
+    double* dqo = ctx->ws.get_f64("h_qo", (size_t)n * n);
+    EIGB_CUDA(cudaMemcpyAsync(dq, q, 8 * n * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dl, lambda, 8 * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dk, kmat, 8 * n * k, cudaMemcpyHostToDevice, st));
+    full_device(ctx, dq, dl, dk, signs, n, k, dlo, dqo);
+    EIGB_CUDA(cudaMemcpyAsync(lambda_out, dlo, 8 * n, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaMemcpyAsync(q_out, dqo, 8 * n * n, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaStreamSynchronize(st));
+    if (wall_time_out)
+      *wall_time_out =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+// ------------------------------------------------------- device pipeline
+int eigmod_b200_update_decomposition_device(eigmod_b200_ctx* ctx, const double* d_q,
+                                            const double* d_lambda, const double* d_kmat,
+                                            const int* signs, int64_t n, int64_t k,
+                                            double* d_lambda_out, double* d_q_out) {
+  return guarded(ctx, [&] {
+    check_basic(n, k, signs);
+    full_device(ctx, d_q, d_lambda, d_kmat, signs, n, k, d_lambda_out, d_q_out);
+  });
+}
+
+int eigmod_b200_project_device(eigmod_b200_ctx* ctx, const double* d_q, const double* d_kmat,
+                               int64_t n, int64_t k, int64_t col_lo, int64_t col_hi,
+                               double* d_u_out) {
+  return guarded(ctx, [&] {
+    check_basic(n, k, nullptr);
+    if (col_lo < 0 || col_hi > n || col_hi < col_lo) throw Error(1, "", "project: bad range");
+    if (col_hi > col_lo) project(ctx, d_q, d_kmat, n, k, col_lo, col_hi, d_u_out);
+  });
+}
+
+int eigmod_b200_plan_device(eigmod_b200_ctx* ctx, const double* d_lambda, const double* d_u,
+                            const int* signs, int64_t n, int64_t k, int64_t* nroots_out) {
+  return guarded(ctx, [&] {
+    check_basic(n, k, signs);
+    plan_from_u(ctx, d_lambda, d_u, signs, n, k, ctx->run_rel);
+    ctx->recs = alloc_records(ctx);
+    if (nroots_out) *nroots_out = ctx->plan.nred;
+  });
+}
+
+int eigmod_b200_solve_device(eigmod_b200_ctx* ctx, int64_t j0, int64_t j1, double* d_rec_out) {
+  return guarded(ctx, [&] {
+    if (!ctx->have_plan) throw Error(1, "", "solve: no plan");
+    if (j0 < 0 || j1 > ctx->plan.nred || j1 < j0) throw Error(1, "", "solve: bad root range");
+    if (ctx->plan.nred == 0) return;
+    eigb::solve_roots(ctx->plan.view(), j0, j1, ctx->recs, ctx->ws, ctx->sms, ctx->stream);
+    if (d_rec_out && j1 > j0) {
+      pack_records_kernel<<<(unsigned)eigb::cdiv(j1 - j0, 128), 128, 0, ctx->stream>>>(
+          ctx->recs, j0, j1 - j0, ctx->plan.kp, d_rec_out);
+      EIGB_LAUNCH_CHECK();
+    }
+  });
+}
+
+int eigmod_b200_finish_device(eigmod_b200_ctx* ctx, const double* d_q, const double* d_rec_all,
+                              int64_t c0, int64_t c1, double* d_lambda_out, double* d_q_out,
+                              int64_t ldq) {
+  return guarded(ctx, [&] {
+    if (!ctx->have_plan) throw Error(1, "", "finish: no plan");
+    const eigb::Plan& p = ctx->plan;
+    if (c0 < 0 || c1 > p.n || c1 < c0) throw Error(1, "", "finish: bad column range");
+    if (d_rec_all && p.nred > 0) {
+      unpack_records_kernel<<<(unsigned)eigb::cdiv(p.nred, 128), 128, 0, ctx->stream>>>(
+          d_rec_all, p.nred, p.kp, ctx->recs);
+      EIGB_LAUNCH_CHECK();
+    }
+    // lambda is only needed for the rank-0 copy; the plan keeps no pointer to it
+    finish(ctx, d_q, nullptr, c0, c1, d_lambda_out, d_q_out, ldq);
+  });
+}
+
+int eigmod_b200_gemm_nt_device(eigmod_b200_ctx* ctx, const double* d_a, const double* d_b,
+                               int64_t m, int64_t nn, int64_t kk, double* d_c, int64_t ldc) {
+  return guarded(ctx, [&] {
+    double* ones = ctx->ws.get_f64("gemm_ones", nn);
+    std::vector<double> h(nn, 1.0);
+    EIGB_CUDA(cudaMemcpyAsync(ones, h.data(), 8 * nn, cudaMemcpyHostToDevice, ctx->stream));
+    EIGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    eigb::gemm_nt_dev(d_a, d_b, m, nn, kk, d_c, ldc, ones, nullptr, ctx->stream);
+  });
+}
+
+}  // extern "C"

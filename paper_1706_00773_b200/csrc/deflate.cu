@@ -1,0 +1,545 @@
+// K1 projection U = Q^T K and the deflation pre-pass (sm_100a).
+//
+// K1 (proj/src/secular.cpp:155-161 -> kernels.cpp:50-65): HBM-bound
+//   streaming pass over Q (row-major, n x n): thread t of a CTA owns two
+//   columns i of Q, reads Q[r, i] coalesced row by row, and accumulates
+//   U[i, :] += Q[r, i] * K[r, :] with K rows broadcast from shared memory.
+//   Rows are split across CTAs; the partial sums are reduced in a fixed
+//   order (deterministic, independent of the launch geometry per split).
+// Deflation (proj/src/secular.cpp:278-340): runs of near-equal poles
+//   (lambda[i] - lambda[i-1] < rel * max(1, max|lambda|)) with the run mean as
+//   representative, classification by the reference's alpha/row-mass rules,
+//   and the reduced problem the solver works on. Multi-member runs are
+//   compressed with a Householder QR of their U rows (exact mode):
+//   rows beyond the numerical rank decouple at the representative.
+#include "pipeline.cuh"
+
+#include <algorithm>
+#include <cfloat>
+
+namespace eigb {
+
+namespace {
+
+constexpr int kTfThreads = 128;
+constexpr int kTfCols = 2 * kTfThreads;
+constexpr int kTfRows = 32;
+
+template <int KP>
+__global__ void __launch_bounds__(kTfThreads) transform_partial_kernel(
+    const double* __restrict__ q, const double* __restrict__ kmat, int64_t n, int k,
+    int64_t rows_per_split, int64_t col_lo, int64_t col_hi, double* __restrict__ part) {
+  __shared__ __align__(16) double ks[kTfRows][KP];
+  const int64_t c0 = col_lo + (int64_t)blockIdx.x * kTfCols + threadIdx.x;
+  const int64_t c1 = c0 + kTfThreads;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t r1 = (r0 + rows_per_split < n) ? r0 + rows_per_split : n;
+  double a0[KP], a1[KP];
+#pragma unroll
+  for (int c = 0; c < KP; ++c) a0[c] = a1[c] = 0.0;
+  const bool v0 = c0 < col_hi, v1 = c1 < col_hi;
+  for (int64_t rr = r0; rr < r1; rr += kTfRows) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < kTfRows * KP; t += kTfThreads) {
+      const int r = t / KP, c = t % KP;
+      const int64_t row = rr + r;
+      ks[r][c] = (row < r1 && c < k) ? kmat[row * k + c] : 0.0;
+    }
+    __syncthreads();
+    const int cnt = (int)((r1 - rr < kTfRows) ? r1 - rr : kTfRows);
+#pragma unroll 4
+    for (int r = 0; r < cnt; ++r) {
+      const double q0 = v0 ? __ldcs(q + (rr + r) * n + c0) : 0.0;
+      const double q1 = v1 ? __ldcs(q + (rr + r) * n + c1) : 0.0;
+#pragma unroll
+      for (int c = 0; c < KP; ++c) {
+        a0[c] = fma(q0, ks[r][c], a0[c]);
+        a1[c] = fma(q1, ks[r][c], a1[c]);
+      }
+    }
+  }
+  const int64_t ncols = col_hi - col_lo;
+  double* out = part + (int64_t)blockIdx.y * ncols * KP;
+  if (v0)
+    for (int c = 0; c < KP; ++c) out[(c0 - col_lo) * KP + c] = a0[c];
+  if (v1)
+    for (int c = 0; c < KP; ++c) out[(c1 - col_lo) * KP + c] = a1[c];
+}
+
+__global__ void transform_reduce_kernel(const double* __restrict__ part, int64_t cnt, int splits,
+                                        double* __restrict__ u) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  double s = part[t];
+  for (int p = 1; p < splits; ++p) s += part[(int64_t)p * cnt + t];
+  u[t] = s;
+}
+
+template <int KP>
+void launch_transform(const double* q, const double* kmat, int64_t n, int k, int64_t col_lo,
+                      int64_t col_hi, double* u, DeviceScratch& ws, int sms, cudaStream_t st) {
+  const int64_t ncols = col_hi - col_lo;
+  const int64_t gx = cdiv(ncols, kTfCols);
+  int64_t splits = std::max<int64_t>(1, cdiv(4 * (int64_t)sms, gx));
+  splits = std::min<int64_t>(splits, cdiv(n, kTfRows));
+  const int64_t rps = cdiv(cdiv(n, splits), kTfRows) * kTfRows;
+  splits = cdiv(n, rps);
+  double* part = ws.get_f64("tf_part", (size_t)splits * ncols * KP);
+  dim3 grid((unsigned)gx, (unsigned)splits);
+  transform_partial_kernel<KP><<<grid, kTfThreads, 0, st>>>(q, kmat, n, k, rps, col_lo, col_hi, part);
+  EIGB_LAUNCH_CHECK();
+  const int64_t cnt = ncols * KP;
+  transform_reduce_kernel<<<(unsigned)cdiv(cnt, 256), 256, 0, st>>>(part, cnt, (int)splits, u);
+  EIGB_LAUNCH_CHECK();
+}
+
+// Column norms of U (first k columns), fixed-order block reduction.
+__global__ void colnorm_kernel(const double* __restrict__ u, int64_t n, int kp, int k,
+                               double* __restrict__ out) {
+  __shared__ double red[32];
+  const int c = blockIdx.x;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += u[i * kp + c] * u[i * kp + c];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    out[c] = t;
+  }
+}
+
+// Repack the kept columns (host-chosen) into a fresh padded [n][kp2] array.
+__global__ void repack_kernel(const double* __restrict__ u, int64_t n, int kp, const int* keep,
+                              int k2, int kp2, double* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * kp2) return;
+  const int64_t i = t / kp2;
+  const int c = (int)(t % kp2);
+  out[t] = (c < k2) ? u[i * kp + keep[c]] : 0.0;
+}
+
+// ---------------------------------------------------------------- runs
+// Single-CTA planning kernel: scale, run boundaries, groups, representatives.
+// groups are emitted in ascending order; rep_row[i] = representative of row i.
+constexpr int kPlanThreads = 1024;
+
+__device__ double block_max(double v, double* red) {
+  v = warp_max(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : -INFINITY;
+    t = warp_max(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// Deterministic block sum: per-thread strided partials, then fixed-order tree.
+__device__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    red[0] = t;
+  }
+  __syncthreads();
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// Exclusive scan of 0/1-ish int64 counts over n items by one CTA, in chunks.
+__device__ void block_exclusive_scan(const int64_t* in, int64_t* out, int64_t n, int64_t* total,
+                                     int64_t* sh) {
+  int64_t carry = 0;
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t v = (i < n) ? in[i] : 0;
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+      const int64_t t = (threadIdx.x >= (unsigned)off) ? sh[threadIdx.x - off] : 0;
+      __syncthreads();
+      sh[threadIdx.x] += t;
+      __syncthreads();
+    }
+    if (i < n) out[i] = carry + sh[threadIdx.x] - v;
+    const int64_t chunk = sh[blockDim.x - 1];
+    __syncthreads();
+    carry += chunk;
+  }
+  if (total) *total = carry;
+}
+
+__global__ void __launch_bounds__(kPlanThreads) runs_kernel(const double* __restrict__ lam,
+                                                            int64_t n, double rel,
+                                                            int64_t* __restrict__ flag,
+                                                            int64_t* __restrict__ gid,
+                                                            int64_t* __restrict__ gstart,
+                                                            int64_t* __restrict__ glen,
+                                                            double* __restrict__ gval,
+                                                            double* __restrict__ rep_row,
+                                                            int64_t* __restrict__ counts,
+                                                            double* __restrict__ scal) {
+  __shared__ double red[32];
+  __shared__ int64_t sh[kPlanThreads];
+  double m = 1.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, fabs(lam[i]));
+  const double scale = block_max(m, red);
+  const double gap = rel * scale;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+    flag[i] = (i == 0 || !(lam[i] - lam[i - 1] < gap)) ? 1 : 0;
+  __syncthreads();
+  __shared__ int64_t ng;
+  block_exclusive_scan(flag, gid, n, &ng, sh);
+  __syncthreads();
+  // gid is exclusive scan of starts; group of row i = gid[i] + flag[i] - 1
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t g = gid[i] + flag[i] - 1;
+    if (flag[i]) gstart[g] = i;
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) gid[i] = gid[i] + flag[i] - 1;
+  __syncthreads();
+  for (int64_t g = threadIdx.x; g < ng; g += blockDim.x) {
+    const int64_t s0 = gstart[g];
+    const int64_t s1 = (g + 1 < ng) ? gstart[g + 1] : n;
+    glen[g] = s1 - s0;
+    double s = 0.0;  // proj/src/secular.cpp:299-301 (sequential sum, then divide)
+    for (int64_t i = s0; i < s1; ++i) s += lam[i];
+    gval[g] = s / (double)(s1 - s0);
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) rep_row[i] = gval[gid[i]];
+  if (threadIdx.x == 0) {
+    counts[0] = ng;
+    scal[0] = scale;
+  }
+}
+
+// Classification (proj/src/secular.cpp:306-331): kind 0 survives, 1 unchanged
+// (all members decouple at their own value), 2 collided (value kept; in the
+// solve the row stays coupled and the root lands on the pole).
+__global__ void __launch_bounds__(kPlanThreads) classify_kernel(
+    const double* __restrict__ u, int64_t n, int kp, int k, const double* __restrict__ alpha,
+    const int64_t* __restrict__ gstart, const int64_t* __restrict__ glen, const int64_t* counts,
+    int* __restrict__ kind, double* __restrict__ scal) {
+  __shared__ double red[32];
+  const int64_t ng = counts[0];
+  double am = 0.0;
+  for (int64_t g = threadIdx.x; g < ng; g += blockDim.x) am += fabs(alpha[g]);
+  const double alpha_mass = block_sum(am, red);
+  double um = 0.0;
+  for (int64_t t = threadIdx.x; t < n * kp; t += blockDim.x) {
+    const int c = (int)(t % kp);
+    if (c < k) um += u[t] * u[t];
+  }
+  const double fn = sqrt(block_sum(um, red));
+  const double u_mass = fn * fn;
+  const double drop = kWeightDeflationRel * (1.0 + alpha_mass);
+  for (int64_t g = threadIdx.x; g < ng; g += blockDim.x) {
+    int kd = 0;
+    if (fabs(alpha[g]) <= drop) {
+      double row_mass = 0.0;
+      for (int64_t i = gstart[g]; i < gstart[g] + glen[g]; ++i)
+        for (int r = 0; r < k; ++r) row_mass += u[i * kp + r] * u[i * kp + r];
+      kd = (row_mass <= kRowMassRel * (1.0 + u_mass)) ? 1 : 2;
+    }
+    kind[g] = kd;
+  }
+  if (threadIdx.x == 0) {
+    scal[1] = alpha_mass;
+    scal[2] = u_mass;
+    scal[3] = fn;
+  }
+}
+
+// Householder QR of each multi-member run's rows (exact mode compression).
+// One thread per multi group (rare: near-equal poles only). Writes R (m x kp,
+// in place of a copy), H (m x m) and the numerical rank.
+__global__ void compress_kernel(const double* __restrict__ u, int kp, int k,
+                                const int64_t* __restrict__ gstart,
+                                const int64_t* __restrict__ glen, const int* __restrict__ kind,
+                                const int64_t* counts, const int64_t* __restrict__ hoff,
+                                const int64_t* __restrict__ roff, double* __restrict__ hbuf,
+                                double* __restrict__ rbuf, int64_t* __restrict__ rank,
+                                const double* __restrict__ scal) {
+  const int64_t ng = counts[0];
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  const int64_t m = glen[g];
+  if (m < 2 || kind[g] == 1) {
+    rank[g] = 0;
+    return;
+  }
+  double* H = hbuf + hoff[g];
+  double* B = rbuf + roff[g];
+  const int64_t s0 = gstart[g];
+  for (int64_t i = 0; i < m; ++i)
+    for (int c = 0; c < kp; ++c) B[i * kp + c] = u[(s0 + i) * kp + c];
+  for (int64_t i = 0; i < m * m; ++i) H[i] = 0.0;
+  for (int64_t i = 0; i < m; ++i) H[i * m + i] = 1.0;
+  const int64_t steps = m < k ? m : k;
+  for (int64_t c = 0; c < steps; ++c) {
+    double nrm = 0.0;
+    for (int64_t i = c; i < m; ++i) nrm += B[i * kp + c] * B[i * kp + c];
+    nrm = sqrt(nrm);
+    if (nrm == 0.0) continue;
+    const double al = B[c * kp + c] >= 0.0 ? -nrm : nrm;
+    double vn = 0.0;
+    // v stored temporarily in column c of B below the diagonal is not safe;
+    // recompute per use from (B[i][c] - (i==c ? al : 0)).
+    for (int64_t i = c; i < m; ++i) {
+      const double vi = B[i * kp + c] - (i == c ? al : 0.0);
+      vn += vi * vi;
+    }
+    if (vn == 0.0) continue;
+    const double beta = 2.0 / vn;
+    const double v_c = B[c * kp + c] - al;
+    // H <- (I - beta v v^T) H, B <- (I - beta v v^T) B; column c of B last.
+    for (int64_t j = 0; j < m; ++j) {
+      double s = v_c * H[c * m + j];
+      for (int64_t i = c + 1; i < m; ++i) s += B[i * kp + c] * H[i * m + j];
+      s *= beta;
+      H[c * m + j] -= s * v_c;
+      for (int64_t i = c + 1; i < m; ++i) H[i * m + j] -= s * B[i * kp + c];
+    }
+    for (int j = kp - 1; j >= (int)c; --j) {
+      double s = v_c * B[c * kp + j];
+      for (int64_t i = c + 1; i < m; ++i) s += B[i * kp + c] * B[i * kp + j];
+      s *= beta;
+      if (j == c) {
+        B[c * kp + c] -= s * v_c;  // = al
+        for (int64_t i = c + 1; i < m; ++i) B[i * kp + c] = 0.0;
+      } else {
+        B[c * kp + j] -= s * v_c;
+        for (int64_t i = c + 1; i < m; ++i) B[i * kp + j] -= s * B[i * kp + c];
+      }
+    }
+  }
+  // numerical rank: leading rows with norm above eps * ||U||_F
+  const double thr = DBL_EPSILON * scal[3];
+  int64_t r = 0;
+  for (int64_t t = 0; t < steps; ++t) {
+    double rn = 0.0;
+    for (int c = 0; c < kp; ++c) rn += B[t * kp + c] * B[t * kp + c];
+    if (sqrt(rn) > thr) r = t + 1;
+  }
+  rank[g] = r;
+}
+
+// Reduced-problem assembly (single CTA, scans over groups in order).
+//   reduced rows: singleton non-unchanged groups (their row), multi groups
+//   (their first rank[g] compressed rows at the representative);
+//   decoupled entries (ascending by construction): unchanged members at
+//   their own value (unit vectors), multi-group rows beyond the rank at the
+//   representative (rotation vectors).
+__global__ void __launch_bounds__(kPlanThreads) assemble_reduced_kernel(
+    const double* __restrict__ lam, const double* __restrict__ u, int64_t n, int kp,
+    const int64_t* __restrict__ gstart, const int64_t* __restrict__ glen,
+    const double* __restrict__ gval, const int* __restrict__ kind,
+    const int64_t* __restrict__ rank, const int64_t* __restrict__ roff,
+    const double* __restrict__ rbuf, int64_t* counts, int64_t* __restrict__ tmp_a,
+    int64_t* __restrict__ tmp_b, int64_t* __restrict__ off_red, int64_t* __restrict__ off_dec,
+    double* __restrict__ d, double* __restrict__ ur, int64_t* __restrict__ red_src,
+    double* __restrict__ dec_val, int64_t* __restrict__ dec_src, int64_t* __restrict__ orig_map) {
+  __shared__ int64_t sh[kPlanThreads];
+  const int64_t ng = counts[0];
+  for (int64_t g = threadIdx.x; g < ng; g += blockDim.x) {
+    const int64_t m = glen[g];
+    int64_t nr, nd;
+    if (kind[g] == 1) nr = 0, nd = m;
+    else if (m == 1) nr = 1, nd = 0;
+    else nr = rank[g], nd = m - rank[g];
+    tmp_a[g] = nr;
+    tmp_b[g] = nd;
+  }
+  __syncthreads();
+  __shared__ int64_t nred, ndec;
+  block_exclusive_scan(tmp_a, off_red, ng, &nred, sh);
+  __syncthreads();
+  block_exclusive_scan(tmp_b, off_dec, ng, &ndec, sh);
+  __syncthreads();
+  for (int64_t g = threadIdx.x; g < ng; g += blockDim.x) {
+    const int64_t m = glen[g], s0 = gstart[g];
+    int64_t pr = off_red[g], pd = off_dec[g];
+    if (kind[g] == 1) {
+      for (int64_t i = 0; i < m; ++i) {
+        dec_val[pd + i] = lam[s0 + i];
+        dec_src[pd + i] = s0 + i;            // unit vector e_(s0+i)
+        orig_map[s0 + i] = -1;               // decoupled coordinate
+      }
+    } else if (m == 1) {
+      d[pr] = lam[s0];
+      for (int c = 0; c < kp; ++c) ur[pr * kp + c] = u[s0 * kp + c];
+      red_src[pr] = s0;
+      orig_map[s0] = pr;
+    } else {
+      const int64_t r = rank[g];
+      const double* B = rbuf + roff[g];
+      for (int64_t t = 0; t < r; ++t) {
+        d[pr + t] = gval[g];
+        for (int c = 0; c < kp; ++c) ur[(pr + t) * kp + c] = B[t * kp + c];
+        red_src[pr + t] = -(g * 65536 + t) - 2;  // rotated row t of group g
+      }
+      for (int64_t t = r; t < m; ++t) {
+        dec_val[pd + t - r] = gval[g];
+        dec_src[pd + t - r] = -(g * 65536 + t) - 2;
+      }
+      for (int64_t i = 0; i < m; ++i) orig_map[s0 + i] = -2 - g;  // member of multi group g
+    }
+  }
+  if (threadIdx.x == 0) {
+    counts[1] = nred;
+    counts[2] = ndec;
+  }
+}
+
+__global__ void clips_kernel(const double* __restrict__ d, const double* __restrict__ ur,
+                             int64_t nr, int kp, int k, const int* __restrict__ sgn,
+                             double* __restrict__ scal) {
+  __shared__ double red[32];
+  double pos = 0.0, neg = 0.0, m = 1.0;
+  for (int64_t t = threadIdx.x; t < nr * kp; t += blockDim.x) {
+    const int c = (int)(t % kp);
+    if (c >= k) continue;
+    const double v = ur[t] * ur[t];
+    if (sgn[c] > 0) pos += v; else neg += v;
+  }
+  for (int64_t i = threadIdx.x; i < nr; i += blockDim.x) m = fmax(m, fabs(d[i]));
+  pos = block_sum(pos, red);
+  neg = block_sum(neg, red);
+  m = block_max(m, red);
+  if (threadIdx.x == 0) {
+    const double pad = 1e-9 * m;
+    scal[4] = (nr > 0) ? d[0] - neg * (1.0 + 1e-12) - pad : 0.0;
+    scal[5] = (nr > 0) ? d[nr - 1] + pos * (1.0 + 1e-12) + pad : 0.0;
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host side
+void transform_update_dev(const double* q, const double* kmat, int64_t n, int k, int kp,
+                          int64_t col_lo, int64_t col_hi, double* u, DeviceScratch& ws, int sms,
+                          cudaStream_t st) {
+  switch (kp) {
+    case 1: launch_transform<1>(q, kmat, n, k, col_lo, col_hi, u, ws, sms, st); break;
+    case 2: launch_transform<2>(q, kmat, n, k, col_lo, col_hi, u, ws, sms, st); break;
+    case 4: launch_transform<4>(q, kmat, n, k, col_lo, col_hi, u, ws, sms, st); break;
+    case 8: launch_transform<8>(q, kmat, n, k, col_lo, col_hi, u, ws, sms, st); break;
+    case 16: launch_transform<16>(q, kmat, n, k, col_lo, col_hi, u, ws, sms, st); break;
+    case 32: launch_transform<32>(q, kmat, n, k, col_lo, col_hi, u, ws, sms, st); break;
+    default: throw Error(1, "", "transform: unsupported padded rank");
+  }
+}
+
+void column_norms2_dev(const double* u, int64_t n, int kp, int k, double* out, cudaStream_t st) {
+  colnorm_kernel<<<k, 256, 0, st>>>(u, n, kp, k, out);
+  EIGB_LAUNCH_CHECK();
+}
+
+void repack_columns_dev(const double* u, int64_t n, int kp, const int* keep, int k2, int kp2,
+                        double* out, cudaStream_t st) {
+  repack_kernel<<<(unsigned)cdiv(n * kp2, 256), 256, 0, st>>>(u, n, kp, keep, k2, kp2, out);
+  EIGB_LAUNCH_CHECK();
+}
+
+void build_plan_dev(Plan& p, const double* lam, int64_t n, double run_rel, DeviceScratch& ws,
+                    cudaStream_t st) {
+  const int kp = p.kp, k = p.k;
+  p.n = n;
+  int64_t* flag = ws.get_i64("pl_flag", n);
+  p.gid = ws.get_i64("pl_gid", n);
+  p.gstart = ws.get_i64("pl_gstart", n);
+  p.glen = ws.get_i64("pl_glen", n);
+  p.gval = ws.get_f64("pl_gval", n);
+  p.rep_row = ws.get_f64("pl_rep_row", n);
+  p.counts = ws.get_i64("pl_counts", 8);
+  p.scal = ws.get_f64("pl_scal", 8);
+  runs_kernel<<<1, kPlanThreads, 0, st>>>(lam, n, run_rel, flag, p.gid, p.gstart, p.glen, p.gval,
+                                           p.rep_row, p.counts, p.scal);
+  EIGB_LAUNCH_CHECK();
+  int64_t ng = 0;
+  EIGB_CUDA(cudaMemcpyAsync(&ng, p.counts, 8, cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaStreamSynchronize(st));
+  p.ng = ng;
+  p.alpha = ws.get_f64("pl_alpha", ng);
+  group_weights(kp, p.rep_row, p.u, n, p.gstart, p.glen, p.gval, ng, p.sgn, k, p.alpha, ws, st);
+  p.kind = ws.get_i32("pl_kind", ng);
+  classify_kernel<<<1, kPlanThreads, 0, st>>>(p.u, n, kp, k, p.alpha, p.gstart, p.glen, p.counts,
+                                               p.kind, p.scal);
+  EIGB_LAUNCH_CHECK();
+
+  // multi-member runs: host-side offsets (lengths are needed for H/R storage)
+  std::vector<int64_t> glen_h(ng);
+  EIGB_CUDA(cudaMemcpyAsync(glen_h.data(), p.glen, 8 * ng, cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaStreamSynchronize(st));
+  std::vector<int64_t> hoff(ng), roff(ng);
+  int64_t hs = 0, rs = 0, nmulti = 0;
+  for (int64_t g = 0; g < ng; ++g) {
+    hoff[g] = hs;
+    roff[g] = rs;
+    if (glen_h[g] > 1) {
+      hs += glen_h[g] * glen_h[g];
+      rs += glen_h[g] * kp;
+      ++nmulti;
+    }
+  }
+  p.nmulti = nmulti;
+  p.hoff = ws.get_i64("pl_hoff", ng);
+  p.roff = ws.get_i64("pl_roff", ng);
+  p.hbuf = ws.get_f64("pl_hbuf", hs);
+  p.rbuf = ws.get_f64("pl_rbuf", rs);
+  p.rank = ws.get_i64("pl_rank", ng);
+  EIGB_CUDA(cudaMemcpyAsync(p.hoff, hoff.data(), 8 * ng, cudaMemcpyHostToDevice, st));
+  EIGB_CUDA(cudaMemcpyAsync(p.roff, roff.data(), 8 * ng, cudaMemcpyHostToDevice, st));
+  if (nmulti > 0) {
+    compress_kernel<<<(unsigned)cdiv(ng, 64), 64, 0, st>>>(p.u, kp, k, p.gstart, p.glen, p.kind,
+                                                         p.counts, p.hoff, p.roff, p.hbuf, p.rbuf,
+                                                         p.rank, p.scal);
+    EIGB_LAUNCH_CHECK();
+  } else {
+    EIGB_CUDA(cudaMemsetAsync(p.rank, 0, 8 * ng, st));
+  }
+  p.d = ws.get_f64("pl_d", n);
+  p.ur = ws.get_f64("pl_ur", (size_t)n * kp);
+  p.red_src = ws.get_i64("pl_red_src", n);
+  p.dec_val = ws.get_f64("pl_dec_val", n);
+  p.dec_src = ws.get_i64("pl_dec_src", n);
+  p.orig_map = ws.get_i64("pl_orig_map", n);
+  int64_t* ta = ws.get_i64("pl_tmpa", ng);
+  int64_t* tb = ws.get_i64("pl_tmpb", ng);
+  p.off_red = ws.get_i64("pl_off_red", ng);
+  p.off_dec = ws.get_i64("pl_off_dec", ng);
+  assemble_reduced_kernel<<<1, kPlanThreads, 0, st>>>(
+      lam, p.u, n, kp, p.gstart, p.glen, p.gval, p.kind, p.rank, p.roff, p.rbuf, p.counts, ta, tb,
+      p.off_red, p.off_dec, p.d, p.ur, p.red_src, p.dec_val, p.dec_src, p.orig_map);
+  EIGB_LAUNCH_CHECK();
+  int64_t cnt[3];
+  EIGB_CUDA(cudaMemcpyAsync(cnt, p.counts, 24, cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaStreamSynchronize(st));
+  p.nred = cnt[1];
+  p.ndec = cnt[2];
+  if (p.nred + p.ndec != n) throw Error(2, "merge", "reduced problem does not account for n pairs");
+  clips_kernel<<<1, kPlanThreads, 0, st>>>(p.d, p.ur, p.nred, kp, k, p.sgn, p.scal);
+  EIGB_LAUNCH_CHECK();
+  double sc[8];
+  EIGB_CUDA(cudaMemcpyAsync(sc, p.scal, 64, cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaStreamSynchronize(st));
+  p.scale = sc[0];
+  p.alpha_mass = sc[1];
+  p.u_mass = sc[2];
+  p.lo_clip = sc[4];
+  p.hi_clip = sc[5];
+}
+
+}  // namespace eigb

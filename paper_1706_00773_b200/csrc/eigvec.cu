@@ -1,0 +1,361 @@
+// K4: eigenvector columns X (stored transposed, Xt[c, :] = column c of the
+// in-basis eigenvector matrix) and the final column order (sm_100a).
+//
+// Column order (proj/src/eigvec.cpp:260-278): roots, then decoupled pairs,
+// stable-merged by value. Root columns follow the reference formula
+// w_s = (U y)_s / (lambda_s - lambda') (eigvec.cpp:133-153) with y the null
+// vector of S(lambda') from the solver and the difference formed in the
+// solver's shifted origin, (d_s - d_o) - delta; the norm is left to the
+// GEMM epilogue (column scale). Roots that sit on a pole use the reference's
+// bordered system (eigvec.cpp:75-119). Decoupled pairs are unit vectors
+// (unchanged, eigvec.cpp:288-291) or rows of a run's Householder rotation.
+// Xt is written row by row with coalesced stores: HBM-bound (8 n^2 bytes).
+#include "pipeline.cuh"
+
+#include <thrust/device_ptr.h>
+#include <thrust/execution_policy.h>
+#include <thrust/sequence.h>
+#include <thrust/sort.h>
+
+namespace eigb {
+
+namespace {
+
+__global__ void root_order_check_kernel(const double* v, int64_t n, int* bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i + 1 < n && v[i + 1] < v[i]) atomicOr(bad, 1);
+}
+
+__global__ void merge_kernel(const double* __restrict__ rv, const int64_t* __restrict__ rperm,
+                             int64_t nr, const double* __restrict__ dv,
+                             const int64_t* __restrict__ dsrc, int64_t nd,
+                             int* __restrict__ kind, int64_t* __restrict__ payload,
+                             double* __restrict__ value) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nr) {
+    const double x = rv[t];
+    const int64_t c = t + dev_n_less(dv, nd, x);  // roots precede equal decoupled values
+    kind[c] = 0;
+    payload[c] = rperm ? rperm[t] : t;
+    value[c] = x;
+  } else if (t < nr + nd) {
+    const int64_t e = t - nr;
+    const double x = dv[e];
+    const int64_t c = e + dev_n_leq(rv, nr, x);
+    kind[c] = dsrc[e] >= 0 ? 1 : 2;
+    payload[c] = e;
+    value[c] = x;
+  }
+}
+
+// Small symmetric Jacobi (eigvec.cpp:17-54 scheme) for the bordered system.
+__device__ void sym_evd_dev(double* a, int k, double* v) {
+  for (int i = 0; i < k * k; ++i) v[i] = 0.0;
+  for (int i = 0; i < k; ++i) v[i * k + i] = 1.0;
+  for (int sweep = 0; sweep < 80; ++sweep) {
+    double off = 0.0, amax = 0.0;
+    for (int p = 0; p < k; ++p)
+      for (int q = 0; q < k; ++q) {
+        if (p != q) off += a[p * k + q] * a[p * k + q];
+        amax = fmax(amax, fabs(a[p * k + q]));
+      }
+    if (off <= 1e-36 * amax * amax || off == 0.0) break;
+    for (int p = 0; p < k; ++p)
+      for (int q = p + 1; q < k; ++q) {
+        const double apq = a[p * k + q];
+        if (apq == 0.0) continue;
+        const double tau = (a[q * k + q] - a[p * k + p]) / (2.0 * apq);
+        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+        const double c = 1.0 / sqrt(1.0 + t * t), s = t * c;
+        for (int i = 0; i < k; ++i) {
+          const double aip = a[i * k + p], aiq = a[i * k + q];
+          a[i * k + p] = c * aip - s * aiq;
+          a[i * k + q] = s * aip + c * aiq;
+        }
+        for (int j = 0; j < k; ++j) {
+          const double apj = a[p * k + j], aqj = a[q * k + j];
+          a[p * k + j] = c * apj - s * aqj;
+          a[q * k + j] = s * apj + c * aqj;
+        }
+        a[p * k + q] = a[q * k + p] = 0.0;
+        for (int i = 0; i < k; ++i) {
+          const double vip = v[i * k + p], viq = v[i * k + q];
+          v[i * k + p] = c * vip - s * viq;
+          v[i * k + q] = s * vip + c * viq;
+        }
+      }
+  }
+}
+
+// Bordered systems for collided roots, 32 per CTA: the pole pass with
+// |d_s - pole| < gap excluded gives T; B = [[I + J T, -J w],[w^T, 0]];
+// null direction from B^T B (eigvec.cpp:157-185); residual check 1e-6.
+template <int KP>
+__global__ void __launch_bounds__(kPassThreads, 1) collision_kernel(
+    ReducedView rp, const int64_t* __restrict__ list, int64_t cnt, const int64_t* __restrict__ origin,
+    double gap, double* __restrict__ colldir, int* __restrict__ collok, double* __restrict__ scratch) {
+  using C = PassCfg<KP>;
+  extern __shared__ __align__(16) double smem[];
+  double* tiles = smem;
+  double* red = tiles + 2 * C::TILE_DOUBLES;
+  __shared__ double dob[32], delta[32], yy[32 * KP];
+  __shared__ int active[32], hit[32];
+  const int t = threadIdx.x;
+  const int64_t b0 = (int64_t)blockIdx.x * 32;
+  if (t < 32) {
+    const int64_t q = b0 + t;
+    active[t] = q < cnt;
+    dob[t] = 0.0;
+    delta[t] = (q < cnt) ? rp.d[origin[list[q]]] : 0.0;
+    hit[t] = 0;
+  }
+  __syncthreads();
+  PassSlots sl{dob, delta, yy, active, hit};
+  secular_pass<KP>(rp.d, rp.u, rp.n, sl, false, true, gap, tiles, red);
+  if (t < 32 && active[t]) {
+    const int64_t j = list[b0 + t];
+    const int64_t idx = origin[j];
+    const int k = rp.k, K1 = k + 1;
+    double* B = scratch + ((size_t)blockIdx.x * 32 + t) * 3 * (KP + 1) * (KP + 1);
+    double* BtB = B + K1 * K1;
+    double* V = BtB + K1 * K1;
+    const double* rb = red + t * (C::P + 1);
+    for (int r = 0; r < K1 * K1; ++r) B[r] = 0.0;
+    for (int r = 0; r < k; ++r)
+      for (int c = 0; c < k; ++c) {
+        const double tv = (r <= c) ? rb[C::pidx(r, c)] : rb[C::pidx(c, r)];
+        B[r * K1 + c] = (r == c ? 1.0 : 0.0) + (double)rp.sgn[r] * tv;
+      }
+    const double* wi = rp.u + idx * KP;
+    for (int r = 0; r < k; ++r) {
+      B[r * K1 + k] = -(double)rp.sgn[r] * wi[r];
+      B[k * K1 + r] = wi[r];
+    }
+    double fro = 0.0;
+    for (int i = 0; i < K1; ++i)
+      for (int jj = 0; jj < K1; ++jj) {
+        double s = 0.0;
+        for (int l = 0; l < K1; ++l) s += B[l * K1 + i] * B[l * K1 + jj];
+        BtB[i * K1 + jj] = s;
+        fro += B[i * K1 + jj] * B[i * K1 + jj];
+      }
+    sym_evd_dev(BtB, K1, V);
+    int imin = 0;
+    for (int r = 1; r < K1; ++r)
+      if (BtB[r * K1 + r] < BtB[imin * K1 + imin]) imin = r;
+    double nrm = 0.0;
+    for (int r = 0; r < K1; ++r) nrm += V[r * K1 + imin] * V[r * K1 + imin];
+    nrm = sqrt(nrm);
+    double res = 0.0;
+    for (int i = 0; i < K1; ++i) {
+      double mi = 0.0;
+      for (int l = 0; l < K1; ++l) mi += B[i * K1 + l] * V[l * K1 + imin] / nrm;
+      res += mi * mi;
+    }
+    const int ok = sqrt(res) <= 1e-6 * fmax(1.0, sqrt(fro));
+    // beta (k entries, zero pads) then xi = direction[k] at index KP
+    for (int r = 0; r < KP; ++r) colldir[j * (KP + 1) + r] = (r < k) ? V[r * K1 + imin] / nrm : 0.0;
+    colldir[j * (KP + 1) + KP] = V[k * K1 + imin] / nrm;
+    collok[j] = ok;
+  }
+}
+
+template <int KP>
+__device__ __forceinline__ double red_value(const ReducedView& rp, int64_t r, const double* yv,
+                                            double dob, double del, bool coll, int64_t o,
+                                            double pole, double gap, bool collok) {
+  const double* ui = rp.u + r * KP;
+  double t = 0.0;
+#pragma unroll
+  for (int c = 0; c < KP; ++c) t = fma(ui[c], yv[c], t);
+  if (!coll) return t / ((rp.d[r] - dob) - del);
+  if (!collok) return (r == o) ? 1.0 : 0.0;
+  const double g = rp.d[r] - pole;
+  if (fabs(g) < gap) return (r == o) ? yv[KP] : 0.0;
+  return -t / g;
+}
+
+constexpr int kXtThreads = 256;
+
+template <int KP>
+__global__ void __launch_bounds__(kXtThreads) xt_kernel(
+    ReducedView rp, int64_t n, const int* __restrict__ ckind, const int64_t* __restrict__ cpay,
+    const int64_t* __restrict__ origin, const double* __restrict__ delta,
+    const int* __restrict__ flags, const double* __restrict__ yall,
+    const double* __restrict__ colldir, const int* __restrict__ collok,
+    const int64_t* __restrict__ orig_map, const int64_t* __restrict__ dec_src,
+    const int64_t* __restrict__ gstart, const int64_t* __restrict__ glen,
+    const int64_t* __restrict__ hoff, const double* __restrict__ hbuf,
+    const int64_t* __restrict__ rank, const int64_t* __restrict__ off_red, double gap,
+    int64_t c0, double* __restrict__ xt, double* __restrict__ colscale, int* __restrict__ cmode) {
+  __shared__ double yv[KP + 1];
+  __shared__ double red[32];
+  const int64_t c = c0 + blockIdx.x;
+  double* row = xt + (int64_t)blockIdx.x * n;
+  const int kind = ckind[c];
+  if (kind != 0) {
+    const int64_t e = cpay[c];
+    const int64_t src = dec_src[e];
+    if (kind == 1) {
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) row[i] = (i == src) ? 1.0 : 0.0;
+    } else {
+      const int64_t code = -(src + 2);
+      const int64_t g = code / 65536, tt = code % 65536;
+      const int64_t s0 = gstart[g], m = glen[g];
+      const double* H = hbuf + hoff[g];
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+        row[i] = (i >= s0 && i < s0 + m) ? H[tt * m + (i - s0)] : 0.0;
+    }
+    if (threadIdx.x == 0) {
+      colscale[c - c0] = 1.0;
+      cmode[c - c0] = (kind == 2);
+    }
+    return;
+  }
+  const int64_t j = cpay[c];
+  const bool coll = (flags[j] & 1) != 0;
+  const int64_t o = origin[j];
+  const double dob = rp.d[o];
+  const double del = delta[j];
+  const bool cok = coll ? (collok[j] != 0) : true;
+  if (threadIdx.x <= KP) {
+    if (coll) yv[threadIdx.x] = colldir[j * (KP + 1) + threadIdx.x];
+    else yv[threadIdx.x] = (threadIdx.x < KP) ? yall[j * KP + threadIdx.x] : 0.0;
+  }
+  __syncthreads();
+  double ss = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t r = orig_map[i];
+    double x;
+    if (r >= 0) {
+      x = red_value<KP>(rp, r, yv, dob, del, coll, o, dob, gap, cok);
+    } else if (r == -1) {
+      x = 0.0;
+    } else {
+      const int64_t g = -2 - r;
+      const int64_t s0 = gstart[g], m = glen[g];
+      const double* H = hbuf + hoff[g];
+      x = 0.0;
+      for (int64_t tt = 0; tt < rank[g]; ++tt)
+        x += H[tt * m + (i - s0)] *
+             red_value<KP>(rp, off_red[g] + tt, yv, dob, del, coll, o, dob, gap, cok);
+    }
+    row[i] = x;
+    ss = fma(x, x, ss);
+  }
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tsum = 0.0;
+    for (int w = 0; w < kXtThreads / 32; ++w) tsum += red[w];
+    colscale[c - c0] = (tsum > 0.0) ? 1.0 / sqrt(tsum) : 1.0;
+    cmode[c - c0] = 1;
+  }
+}
+
+template <int KP>
+void launch_xt(const Plan& p, const RootRecords& roots, const Columns& cols, const double* colldir,
+               const int* collok, int64_t c0, int64_t c1, double* xt, double* colscale, int* cmode,
+               cudaStream_t st) {
+  const double gap = kPoleMergeRelGap * p.scale;
+  xt_kernel<KP><<<(unsigned)(c1 - c0), kXtThreads, 0, st>>>(
+      p.view(), p.n, cols.kind, cols.payload, roots.origin, roots.delta, roots.flags, roots.y,
+      colldir, collok, p.orig_map, p.dec_src, p.gstart, p.glen, p.hoff, p.hbuf, p.rank, p.off_red,
+      gap, c0, xt, colscale, cmode);
+  EIGB_LAUNCH_CHECK();
+}
+
+template <int KP>
+void launch_collisions(const Plan& p, const RootRecords& roots, const int64_t* list, int64_t cnt,
+                       double* colldir, int* collok, DeviceScratch& ws, cudaStream_t st) {
+  using C = PassCfg<KP>;
+  const int grid = (int)cdiv(cnt, 32);
+  double* scratch = ws.get_f64("coll_scratch", (size_t)grid * 32 * 3 * (KP + 1) * (KP + 1));
+  const size_t sm = sizeof(double) * (2 * C::TILE_DOUBLES + C::RED_DOUBLES);
+  EIGB_CUDA(cudaFuncSetAttribute(collision_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm));
+  collision_kernel<KP><<<grid, kPassThreads, sm, st>>>(p.view(), list, cnt, roots.origin,
+                                                       kPoleMergeRelGap * p.scale, colldir,
+                                                       collok, scratch);
+  EIGB_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+void merge_columns_dev(const Plan& p, const RootRecords& roots, Columns& cols, DeviceScratch& ws,
+                       cudaStream_t st) {
+  const int64_t nr = p.nred, nd = p.ndec, n = p.n;
+  cols.kind = ws.get_i32("col_kind", n);
+  cols.payload = ws.get_i64("col_payload", n);
+  cols.value = ws.get_f64("col_value", n);
+  const double* rv = roots.value;
+  const int64_t* perm = nullptr;
+  if (nr > 1) {
+    // Roots come out ascending from the count-certified brackets; ties within
+    // an ulp can swap, so verify and fall back to a stable device sort.
+    int* bad = ws.get_i32("merge_bad", 1);
+    EIGB_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+    root_order_check_kernel<<<(unsigned)cdiv(nr, 256), 256, 0, st>>>(rv, nr, bad);
+    EIGB_LAUNCH_CHECK();
+    int bad_h = 0;
+    EIGB_CUDA(cudaMemcpyAsync(&bad_h, bad, 4, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaStreamSynchronize(st));
+    if (bad_h) {
+      double* sv = ws.get_f64("merge_sorted", nr);
+      int64_t* pm = ws.get_i64("merge_perm", nr);
+      EIGB_CUDA(cudaMemcpyAsync(sv, rv, 8 * nr, cudaMemcpyDeviceToDevice, st));
+      thrust::sequence(thrust::cuda::par.on(st), thrust::device_ptr<int64_t>(pm),
+                       thrust::device_ptr<int64_t>(pm + nr));
+      thrust::stable_sort_by_key(thrust::cuda::par.on(st), thrust::device_ptr<double>(sv),
+                                 thrust::device_ptr<double>(sv + nr),
+                                 thrust::device_ptr<int64_t>(pm));
+      rv = sv;
+      perm = pm;
+    }
+  }
+  merge_kernel<<<(unsigned)cdiv(nr + nd, 256), 256, 0, st>>>(rv, perm, nr, p.dec_val, p.dec_src,
+                                                             nd, cols.kind, cols.payload,
+                                                             cols.value);
+  EIGB_LAUNCH_CHECK();
+}
+
+void collision_vectors_dev(const Plan& p, const RootRecords& roots, double* colldir, int* collok,
+                           DeviceScratch& ws, cudaStream_t st) {
+  const int64_t nr = p.nred;
+  if (nr == 0) return;
+  std::vector<int> fl(nr);
+  EIGB_CUDA(cudaMemcpyAsync(fl.data(), roots.flags, 4 * nr, cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaStreamSynchronize(st));
+  std::vector<int64_t> list;
+  for (int64_t j = 0; j < nr; ++j)
+    if (fl[j] & 1) list.push_back(j);
+  if (list.empty()) return;
+  int64_t* dl = ws.get_i64("coll_list", list.size());
+  EIGB_CUDA(cudaMemcpyAsync(dl, list.data(), 8 * list.size(), cudaMemcpyHostToDevice, st));
+  const int64_t cnt = (int64_t)list.size();
+  switch (p.kp) {
+    case 1: launch_collisions<1>(p, roots, dl, cnt, colldir, collok, ws, st); break;
+    case 2: launch_collisions<2>(p, roots, dl, cnt, colldir, collok, ws, st); break;
+    case 4: launch_collisions<4>(p, roots, dl, cnt, colldir, collok, ws, st); break;
+    case 8: launch_collisions<8>(p, roots, dl, cnt, colldir, collok, ws, st); break;
+    case 16: launch_collisions<16>(p, roots, dl, cnt, colldir, collok, ws, st); break;
+    case 32: launch_collisions<32>(p, roots, dl, cnt, colldir, collok, ws, st); break;
+  }
+}
+
+void build_xt_dev(const Plan& p, const RootRecords& roots, const Columns& cols,
+                  const double* colldir, const int* collok, int64_t c0, int64_t c1, double* xt,
+                  double* colscale, int* cmode, cudaStream_t st) {
+  if (c1 <= c0) return;
+  switch (p.kp) {
+    case 1: launch_xt<1>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, st); break;
+    case 2: launch_xt<2>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, st); break;
+    case 4: launch_xt<4>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, st); break;
+    case 8: launch_xt<8>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, st); break;
+    case 16: launch_xt<16>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, st); break;
+    case 32: launch_xt<32>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, st); break;
+  }
+}
+
+}  // namespace eigb

@@ -1,0 +1,74 @@
+// Device pipeline of the rank-k eigen-update: plan (projection + deflation),
+// root solve, column assembly and the Q X back-transform.
+#pragma once
+
+#include <vector>
+
+#include "secular.cuh"
+
+namespace eigb {
+
+// Everything derived from (lambda, U, J) before the root solve; lives in the
+// context's scratch buffers.
+struct Plan {
+  int64_t n = 0;
+  int k = 0, kp = 0, m_neg = 0;
+  std::vector<int> sgn_h;        // effective signs (kept columns)
+  std::vector<int> keep_h;       // kept column indices of the caller's K
+  double* u = nullptr;           // [n][kp] padded U (kept columns)
+  int* sgn = nullptr;            // [kp] device, pads +1
+  // runs / groups
+  int64_t ng = 0, nmulti = 0;
+  int64_t *gid = nullptr, *gstart = nullptr, *glen = nullptr, *counts = nullptr;
+  double *gval = nullptr, *rep_row = nullptr, *scal = nullptr, *alpha = nullptr;
+  int* kind = nullptr;
+  int64_t *hoff = nullptr, *roff = nullptr, *rank = nullptr;
+  double *hbuf = nullptr, *rbuf = nullptr;
+  // reduced problem
+  int64_t nred = 0, ndec = 0;
+  double *d = nullptr, *ur = nullptr, *dec_val = nullptr;
+  int64_t *red_src = nullptr, *dec_src = nullptr, *orig_map = nullptr, *off_red = nullptr,
+          *off_dec = nullptr;
+  double scale = 1.0, alpha_mass = 0.0, u_mass = 0.0, lo_clip = 0.0, hi_clip = 0.0;
+  double run_rel = kExactRunRelGap;
+
+  ReducedView view() const {
+    return ReducedView{d, ur, sgn, nred, k, kp, m_neg, lo_clip, hi_clip};
+  }
+};
+
+// Final column layout after the stable merge of roots and decoupled pairs.
+struct Columns {
+  int* kind = nullptr;        // 0 root, 1 unit vector, 2 run rotation vector
+  int64_t* payload = nullptr; // root j or decoupled entry e
+  double* value = nullptr;    // lambda' (ascending)
+};
+
+// deflate.cu
+void transform_update_dev(const double* q, const double* kmat, int64_t n, int k, int kp,
+                          int64_t col_lo, int64_t col_hi, double* u, DeviceScratch& ws, int sms,
+                          cudaStream_t st);
+void column_norms2_dev(const double* u, int64_t n, int kp, int k, double* out, cudaStream_t st);
+void repack_columns_dev(const double* u, int64_t n, int kp, const int* keep, int k2, int kp2,
+                        double* out, cudaStream_t st);
+void build_plan_dev(Plan& p, const double* lam, int64_t n, double run_rel, DeviceScratch& ws,
+                    cudaStream_t st);
+
+// eigvec.cu
+void merge_columns_dev(const Plan& p, const RootRecords& roots, Columns& cols, DeviceScratch& ws,
+                       cudaStream_t st);
+void collision_vectors_dev(const Plan& p, const RootRecords& roots, double* colldir,
+                           int* collok, DeviceScratch& ws, cudaStream_t st);
+void build_xt_dev(const Plan& p, const RootRecords& roots, const Columns& cols,
+                  const double* colldir, const int* collok, int64_t c0, int64_t c1, double* xt,
+                  double* colscale, int* colsign_mode, cudaStream_t st);
+
+// gemm.cu: C[:, c0:c1] = (A Xt^T) diag(scale) with the reference's sign rule
+// on columns whose mode is 1 (proj/src/eigvec.cpp:340-347).
+void back_transform_dev(const double* a, const double* xt, int64_t n, int64_t ncols,
+                        const double* colscale, const int* colsign_mode, double* c, int64_t ldc,
+                        DeviceScratch& ws, cudaStream_t st);
+void gemm_nt_dev(const double* a, const double* b, int64_t m, int64_t nn, int64_t kk, double* c,
+                 int64_t ldc, const double* colscale, double* tile_colmax, cudaStream_t st);
+
+}  // namespace eigb

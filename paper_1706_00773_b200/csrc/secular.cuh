@@ -1,0 +1,80 @@
+// Internal interfaces between the device stages of the eigen-update pipeline.
+#pragma once
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#ifdef __CUDACC__
+#include "secular_pass.cuh"
+#endif
+
+namespace eigb {
+
+// Named, grow-only device buffers owned by a context (one per device/stream).
+class DeviceScratch {
+ public:
+  ~DeviceScratch() { release(); }
+  void* get(const std::string& name, size_t bytes) {
+    auto it = bufs_.find(name);
+    if (it != bufs_.end() && it->second.second >= bytes) return it->second.first;
+    if (it != bufs_.end()) {
+      cudaFree(it->second.first);
+      bufs_.erase(it);
+    }
+    void* p = nullptr;
+    if (bytes == 0) bytes = 16;
+    EIGB_CUDA(cudaMalloc(&p, bytes));
+    bufs_[name] = {p, bytes};
+    return p;
+  }
+  double* get_f64(const std::string& n, size_t cnt) { return static_cast<double*>(get(n, cnt * 8)); }
+  int64_t* get_i64(const std::string& n, size_t cnt) { return static_cast<int64_t*>(get(n, cnt * 8)); }
+  int* get_i32(const std::string& n, size_t cnt) { return static_cast<int*>(get(n, cnt * 4)); }
+  void release() {
+    for (auto& kv : bufs_) cudaFree(kv.second.first);
+    bufs_.clear();
+  }
+  size_t bytes() const {
+    size_t s = 0;
+    for (auto& kv : bufs_) s += kv.second.second;
+    return s;
+  }
+
+ private:
+  std::map<std::string, std::pair<void*, size_t>> bufs_;
+};
+
+// The deflated ("reduced") secular problem the solver works on: poles d
+// (ascending, duplicates allowed after run compression) and rows u (padded to
+// kp columns), diag(d) + u J u^T.
+struct ReducedView {
+  const double* d;
+  const double* u;    // [n][kp]
+  const int* sgn;     // [kp] device, pads +1
+  int64_t n;
+  int k;              // effective rank (unpadded)
+  int kp;
+  int m_neg;          // number of -1 signs
+  double lo_clip, hi_clip;
+};
+
+// Per-root solver output (indexed by root j of the reduced problem).
+struct RootRecords {
+  double* value;   // root (double)
+  int64_t* origin; // reduced pole index o: root = d[o] + delta
+  double* delta;
+  int* flags;      // 1 collided (sits on pole o), 2 ulp bracket without isolation
+  int* evals;      // S(x) evaluations spent
+  double* y;       // [n][kp] unit null vector of S(root)
+};
+
+void solve_roots(const ReducedView& rp, int64_t j0, int64_t j1, const RootRecords& out,
+                 DeviceScratch& ws, int sms, cudaStream_t st);
+
+void group_weights(int kp, const double* rep, const double* u, int64_t n, const int64_t* gstart,
+                   const int64_t* glen, const double* gval, int64_t ng, const int* sgn, int k,
+                   double* alpha, DeviceScratch& ws, cudaStream_t st);
+
+}  // namespace eigb

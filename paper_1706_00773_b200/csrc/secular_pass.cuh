@@ -1,0 +1,516 @@
+// The secular "pole pass": for a batch of 32 evaluation points x_b (one per
+// lane, "slots") accumulate
+//     S_b = J + sum_i u_i u_i^T / (d_i - x_b)            (k x k, symmetric)
+//     g_b = sum_i (u_i . y_b)^2 / (d_i - x_b)^2        (= y_b^T S'(x_b) y_b)
+// over all poles i. This one contraction is the inner loop of
+//   * the deflation weights  (x_b = representative of pole group b; the
+//     excluded self term is the diff == 0 case; proj/src/secular.cpp:168-202),
+//   * the root solver        (inertia count + Newton),
+//   * the collision vectors  (proj/src/eigvec.cpp:75-119).
+//
+// Work split inside one CTA (NWARP = 8 warps): lane = slot, warp w handles
+// entry group (w % EG) of the packed upper triangle and pole split (w / EG).
+// Pole tiles (d_i and the padded row u_i) are staged in shared memory with
+// cp.async double buffering and read as warp-wide broadcasts, so every lane
+// spends its issue slots on DFMA: per pole and slot one MUFU.RCP64H + 4 DFMA
+// for 1/(d_i - x_b), then (KP - r) DFMA per row r of the entry group.
+#pragma once
+
+#include "common.cuh"
+
+namespace eigb {
+
+constexpr int kPassWarps = 8;
+constexpr int kPassThreads = kPassWarps * 32;
+constexpr int kPoleTile = 64;
+
+template <int KP>
+struct PassCfg {
+  static constexpr int P = KP * (KP + 1) / 2;
+  static constexpr int EG = (KP <= 8) ? 1 : (KP == 16 ? 2 : 8);
+  static constexpr int PS = kPassWarps / EG;
+  // Row range [row_lo(g), row_lo(g+1)) of entry group g: greedy split of the
+  // packed triangle into EG groups of about P/EG entries.
+  __host__ __device__ static constexpr int row_lo(int g) {
+    if (g <= 0) return 0;
+    if (g >= EG) return KP;
+    int acc = 0, r = 0;
+    while (r < KP && acc < (P * g + EG - 1) / EG) {
+      acc += KP - r;
+      ++r;
+    }
+    return r;
+  }
+  __host__ __device__ static constexpr int entries(int g) {
+    int e = 0;
+    for (int r = row_lo(g); r < row_lo(g + 1); ++r) e += KP - r;
+    return e;
+  }
+  // packed index of (r, c), r <= c
+  __host__ __device__ static constexpr int pidx(int r, int c) {
+    return r * KP - r * (r - 1) / 2 + (c - r);
+  }
+  static constexpr int SIGMA_GROUP = EG - 1;  // group that also accumulates g_b
+  // shared memory (doubles)
+  static constexpr int TILE_DOUBLES = kPoleTile * (KP + 1);
+  static constexpr int RED_DOUBLES = 32 * (P + 1);
+};
+
+// Per-slot evaluation point: x_b = dob[b] + delta[b]; the difference to pole i
+// is formed as (d_i - dob[b]) - delta[b] so a shifted origin keeps relative
+// accuracy near d_o. active[b] == 0 disables the slot (its terms are zero).
+struct PassSlots {
+  double* dob;     // [32]
+  double* delta;   // [32]
+  double* y;       // [32][KP]  direction for g_b
+  int* active;     // [32]
+  int* hit;        // [32]  set when some d_i - x_b == 0 (solver: pole hit)
+};
+
+template <int KP>
+__device__ __forceinline__ void load_pole_tile(double* tile, const double* __restrict__ d,
+                                               const double* __restrict__ u, int64_t i0,
+                                               int64_t n) {
+  // tile layout: [kPoleTile] d, then [kPoleTile][KP] rows. Rows beyond n are
+  // zero with d = NaN (NaN difference => term skipped).
+  double* td = tile;
+  double* tu = tile + kPoleTile;
+  const int tid = threadIdx.x;
+  const int64_t cnt = (n - i0) < kPoleTile ? (n - i0) : kPoleTile;
+  for (int t = tid; t < kPoleTile; t += kPassThreads) td[t] = (t < cnt) ? d[i0 + t] : __longlong_as_double(0x7ff8000000000000ll);
+  if (KP >= 2) {
+    constexpr int CH = KP / 2;  // 16-byte chunks per row
+    const double2* src = reinterpret_cast<const double2*>(u + i0 * KP);
+    double2* dst = reinterpret_cast<double2*>(tu);
+    for (int t = tid; t < kPoleTile * CH; t += kPassThreads) {
+      if (t < cnt * CH) {
+        const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst + t));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(src + t));
+      } else {
+        dst[t] = make_double2(0.0, 0.0);
+      }
+    }
+  } else {
+    for (int t = tid; t < kPoleTile; t += kPassThreads) tu[t] = (t < cnt) ? u[i0 + t] : 0.0;
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// Body of one warp: entry group G (compile time, so only its accumulators
+// are live), pole split p. All warps run the same tile loop, so every
+// __syncthreads() is reached the same number of times by the whole CTA.
+template <int KP, int G>
+__device__ __forceinline__ void pass_body(const double* __restrict__ d,
+                                          const double* __restrict__ u, int64_t n,
+                                          const PassSlots& slots, bool want_sigma,
+                                          bool exclude_zero, double excl_gap, double* tiles,
+                                          double* red, int p) {
+  using C = PassCfg<KP>;
+  constexpr int RLO = C::row_lo(G), RHI = C::row_lo(G + 1);
+  constexpr int E = C::entries(G);
+  constexpr int E0 = C::pidx(RLO, RLO);  // packed offset of the group's first entry
+  const int lane = threadIdx.x & 31;
+  const double dob = slots.dob[lane];
+  const double del = slots.delta[lane];
+  const bool act = slots.active[lane] != 0;
+  const bool sig = want_sigma && (G == C::SIGMA_GROUP);
+  double yv[KP];
+#pragma unroll
+  for (int c = 0; c < KP; ++c) yv[c] = sig ? slots.y[lane * KP + c] : 0.0;
+  double acc[E > 0 ? E : 1];
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc[e] = 0.0;
+  double gs = 0.0;
+  int hit = 0;
+
+  const int64_t ntiles = (n + kPoleTile - 1) / kPoleTile;
+  if (ntiles > 0) load_pole_tile<KP>(tiles, d, u, 0, n);
+  constexpr int per = kPoleTile / C::PS;
+  for (int64_t t = 0; t < ntiles; ++t) {
+    const double* cur = tiles + (t & 1) * C::TILE_DOUBLES;
+    if (t + 1 < ntiles) {
+      load_pole_tile<KP>(tiles + ((t + 1) & 1) * C::TILE_DOUBLES, d, u, (t + 1) * kPoleTile, n);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* td = cur;
+    const double* tu = cur + kPoleTile;
+#pragma unroll 2
+    for (int ii = 0; ii < per; ++ii) {
+      const int i = p * per + ii;
+      const double diff = (td[i] - dob) - del;
+      double D;
+      if (excl_gap > 0.0) {
+        D = (act && fabs(diff) >= excl_gap) ? rcp64(diff) : 0.0;
+      } else if (diff == 0.0) {
+        hit |= !exclude_zero;
+        D = 0.0;
+      } else {
+        D = (act && diff == diff) ? rcp64(diff) : 0.0;
+      }
+      double ur[KP];
+      if constexpr (KP >= 2) {
+#pragma unroll
+        for (int c = 0; c < KP; c += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(tu + i * KP + c);
+          ur[c] = v.x;
+          ur[c + 1] = v.y;
+        }
+      } else {
+        ur[0] = tu[i];
+      }
+#pragma unroll
+      for (int r = RLO; r < RHI; ++r) {
+        const double v = D * ur[r];
+#pragma unroll
+        for (int c = r; c < KP; ++c) acc[C::pidx(r, c) - E0] = fma(v, ur[c], acc[C::pidx(r, c) - E0]);
+      }
+      if (sig) {
+        double tt = 0.0;
+#pragma unroll
+        for (int c = 0; c < KP; ++c) tt = fma(ur[c], yv[c], tt);
+        const double td2 = tt * D;
+        gs = fma(td2, td2, gs);
+      }
+    }
+    __syncthreads();  // tile buffer reuse
+  }
+
+  // Deterministic reduction over pole splits: p = 0 writes, p = 1.. add in order.
+  constexpr int PP = C::P + 1;
+  for (int q = 0; q < C::PS; ++q) {
+    if (p == q) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if (q == 0) red[lane * PP + E0 + e] = acc[e];
+        else red[lane * PP + E0 + e] += acc[e];
+      }
+      if (G == C::SIGMA_GROUP) {
+        if (q == 0) red[lane * PP + C::P] = gs;
+        else red[lane * PP + C::P] += gs;
+      }
+    }
+    __syncthreads();
+  }
+  if (hit) atomicOr(&slots.hit[lane], 1);
+}
+
+// Runs the pass. On return (after __syncthreads) red[b * (P+1) + e] holds the
+// packed S_b (without J) and red[b*(P+1) + P] holds g_b, for every slot b.
+// `exclude_zero`: a zero difference drops the term (deflation weights)
+// instead of flagging a pole hit. `excl_gap` > 0 drops every pole with
+// |d_i - x_b| < excl_gap (bordered collision systems).
+template <int KP>
+__device__ void secular_pass(const double* __restrict__ d, const double* __restrict__ u, int64_t n,
+                             const PassSlots& slots, bool want_sigma, bool exclude_zero,
+                             double excl_gap, double* tiles /* 2 x TILE_DOUBLES */,
+                             double* red /* RED_DOUBLES */) {
+  using C = PassCfg<KP>;
+  const int warp = threadIdx.x >> 5;
+  const int g = warp % C::EG;
+  const int p = warp / C::EG;
+#define EIGB_PASS_CASE(GG)                                                                  \
+  case GG:                                                                                 \
+    if constexpr (GG < C::EG)                                                              \
+      pass_body<KP, GG>(d, u, n, slots, want_sigma, exclude_zero, excl_gap, tiles, red, p); \
+    break;
+  switch (g) {
+    EIGB_PASS_CASE(0)
+    EIGB_PASS_CASE(1)
+    EIGB_PASS_CASE(2)
+    EIGB_PASS_CASE(3)
+    EIGB_PASS_CASE(4)
+    EIGB_PASS_CASE(5)
+    EIGB_PASS_CASE(6)
+    EIGB_PASS_CASE(7)
+  }
+#undef EIGB_PASS_CASE
+  __syncthreads();
+}
+
+// ------------------------------------------------------------ small k x k
+// Bunch-Kaufman LDL^T (partial pivoting, alpha = (1+sqrt(17))/8) of the full
+// symmetric n x n matrix A (row-major, leading dimension ld), in place.
+// piv[k] encodes the interchange of step k (>= 0: 1x1 with row piv[k];
+// < 0: 2x2 block with row -piv[k]-1). Returns the number of negative
+// eigenvalues (inertia); *zero is set when an exactly zero pivot occurred.
+__host__ __device__ inline int bk_factor(double* A, int n, int ld, int* piv, int* zero) {
+  const double alpha = 0.6403882032022076;
+  int neg = 0;
+  *zero = 0;
+  int k = 0;
+  while (k < n) {
+    const double absakk = fabs(A[k * ld + k]);
+    int imax = k;
+    double colmax = 0.0;
+    for (int i = k + 1; i < n; ++i) {
+      const double v = fabs(A[i * ld + k]);
+      if (v > colmax) colmax = v, imax = i;
+    }
+    int kstep = 1, kp = k;
+    if (fmax(absakk, colmax) == 0.0) {
+      piv[k] = k;
+      *zero = 1;
+      ++k;
+      continue;
+    }
+    if (absakk >= alpha * colmax) {
+      kp = k;
+    } else {
+      double rowmax = 0.0;
+      for (int j = k; j < n; ++j)
+        if (j != imax) rowmax = fmax(rowmax, fabs(A[imax * ld + j]));
+      if (absakk >= alpha * colmax * (colmax / rowmax)) {
+        kp = k;
+      } else if (fabs(A[imax * ld + imax]) >= alpha * rowmax) {
+        kp = imax;
+      } else {
+        kp = imax;
+        kstep = 2;
+      }
+    }
+    const int kk = k + kstep - 1;
+    if (kp != kk) {  // symmetric interchange of kk and kp (whole rows/cols)
+      for (int j = 0; j < n; ++j) {
+        const double t = A[kk * ld + j];
+        A[kk * ld + j] = A[kp * ld + j];
+        A[kp * ld + j] = t;
+      }
+      for (int i = 0; i < n; ++i) {
+        const double t = A[i * ld + kk];
+        A[i * ld + kk] = A[i * ld + kp];
+        A[i * ld + kp] = t;
+      }
+    }
+    if (kstep == 1) {
+      const double dk = A[k * ld + k];
+      piv[k] = kp;
+      if (dk < 0.0) ++neg;
+      if (dk == 0.0) {
+        *zero = 1;
+      } else {
+        const double r1 = 1.0 / dk;
+        for (int i = k + 1; i < n; ++i) {
+          const double li = A[i * ld + k] * r1;
+          for (int j = k + 1; j <= i; ++j) A[i * ld + j] -= li * A[j * ld + k];
+        }
+        for (int i = k + 1; i < n; ++i) A[i * ld + k] *= r1;
+        for (int i = k + 1; i < n; ++i)
+          for (int j = k + 1; j < i; ++j) A[j * ld + i] = A[i * ld + j];
+      }
+    } else {
+      const double a = A[k * ld + k], b = A[(k + 1) * ld + k], c = A[(k + 1) * ld + k + 1];
+      const double det = a * c - b * b;
+      piv[k] = -kp - 1;
+      piv[k + 1] = -kp - 1;
+      if (det < 0.0) neg += 1;
+      else if (a + c < 0.0) neg += 2;
+      if (det == 0.0) {
+        *zero = 1;
+      } else {
+        const double id = 1.0 / det;
+        // D^-1 = id * [[c, -b], [-b, a]]
+        // rows in decreasing order: row i reads columns k, k+1 of rows j <= i
+        // before they are overwritten by their L entries
+        for (int i = n - 1; i >= k + 2; --i) {
+          const double x1 = A[i * ld + k], x2 = A[i * ld + k + 1];
+          const double w1 = (c * x1 - b * x2) * id;
+          const double w2 = (a * x2 - b * x1) * id;
+          for (int j = k + 2; j <= i; ++j)
+            A[i * ld + j] -= w1 * A[j * ld + k] + w2 * A[j * ld + k + 1];
+          A[i * ld + k] = w1;
+          A[i * ld + k + 1] = w2;
+        }
+        for (int i = k + 2; i < n; ++i)
+          for (int j = k + 2; j < i; ++j) A[j * ld + i] = A[i * ld + j];
+      }
+    }
+    k += kstep;
+  }
+  return neg;
+}
+
+// Solves A z = b with the factorization of bk_factor. bk_factor applies
+// every interchange to whole rows and columns (including the finished L
+// columns), so P A P^T = L D L^T with one permutation P: permute b, solve
+// L, D (1x1 / 2x2 blocks), L^T, permute back. Zero pivots are replaced by
+// `tiny` (inverse iteration on a singular matrix).
+__host__ __device__ inline void bk_solve(const double* A, int n, int ld, const int* piv, double* b,
+                                         double tiny) {
+  int k = 0;
+  while (k < n) {  // b <- P b (interchanges in factorization order)
+    if (piv[k] >= 0) {
+      const int kp = piv[k];
+      if (kp != k) { const double t = b[k]; b[k] = b[kp]; b[kp] = t; }
+      k += 1;
+    } else {
+      const int kp = -piv[k] - 1;
+      if (kp != k + 1) { const double t = b[k + 1]; b[k + 1] = b[kp]; b[kp] = t; }
+      k += 2;
+    }
+  }
+  k = 0;
+  while (k < n) {  // L y = b
+    if (piv[k] >= 0) {
+      for (int i = k + 1; i < n; ++i) b[i] -= A[i * ld + k] * b[k];
+      k += 1;
+    } else {
+      for (int i = k + 2; i < n; ++i) b[i] -= A[i * ld + k] * b[k] + A[i * ld + k + 1] * b[k + 1];
+      k += 2;
+    }
+  }
+  k = 0;
+  while (k < n) {  // D w = y
+    if (piv[k] >= 0) {
+      double dk = A[k * ld + k];
+      if (dk == 0.0) dk = tiny;
+      b[k] /= dk;
+      k += 1;
+    } else {
+      const double a = A[k * ld + k], bb = A[(k + 1) * ld + k], c = A[(k + 1) * ld + k + 1];
+      double det = a * c - bb * bb;
+      if (det == 0.0) det = tiny;
+      const double x1 = (c * b[k] - bb * b[k + 1]) / det;
+      const double x2 = (a * b[k + 1] - bb * b[k]) / det;
+      b[k] = x1;
+      b[k + 1] = x2;
+      k += 2;
+    }
+  }
+  k = n - 1;
+  while (k >= 0) {  // L^T z = w
+    if (piv[k] >= 0) {
+      for (int i = k + 1; i < n; ++i) b[k] -= A[i * ld + k] * b[i];
+      k -= 1;
+    } else {  // block (k-1, k)
+      for (int i = k + 1; i < n; ++i) {
+        b[k] -= A[i * ld + k] * b[i];
+        b[k - 1] -= A[i * ld + k - 1] * b[i];
+      }
+      k -= 2;
+    }
+  }
+  // z <- P^T z (interchanges in reverse order)
+  k = n - 1;
+  while (k >= 0) {
+    if (piv[k] >= 0) {
+      const int kp = piv[k];
+      if (kp != k) { const double t = b[k]; b[k] = b[kp]; b[kp] = t; }
+      k -= 1;
+    } else {
+      const int kp = -piv[k] - 1;  // second row of the block is k
+      if (kp != k) { const double t = b[k]; b[k] = b[kp]; b[kp] = t; }
+      k -= 2;
+    }
+  }
+}
+
+// proj/src/secular.cpp:14-38 (LU with partial pivoting, det on the fly).
+__device__ inline int lu_factor_dev(double* m, int k, int ld, int* piv, double* det) {
+  for (int i = 0; i < k; ++i) piv[i] = i;
+  *det = 1.0;
+  for (int col = 0; col < k; ++col) {
+    int best = col;
+    for (int i = col + 1; i < k; ++i)
+      if (fabs(m[i * ld + col]) > fabs(m[best * ld + col])) best = i;
+    if (best != col) {
+      for (int j = 0; j < k; ++j) {
+        const double t = m[col * ld + j];
+        m[col * ld + j] = m[best * ld + j];
+        m[best * ld + j] = t;
+      }
+      const int t = piv[col];
+      piv[col] = piv[best];
+      piv[best] = t;
+      *det = -*det;
+    }
+    const double pivot = m[col * ld + col];
+    *det *= pivot;
+    if (pivot == 0.0) return 0;
+    for (int i = col + 1; i < k; ++i) {
+      const double f = m[i * ld + col] / pivot;
+      m[i * ld + col] = f;
+      for (int j = col + 1; j < k; ++j) m[i * ld + j] -= f * m[col * ld + j];
+    }
+  }
+  return 1;
+}
+
+// Adjugate of the k x k matrix m (ld) into adj (ld), following
+// proj/src/secular.cpp:49-124: cofactors for k <= 3, LU det*inverse when
+// min pivot > 1e-8 max pivot, cofactor expansion with LU minors otherwise.
+// `scratch` holds at least 2*k*k doubles.
+__device__ inline void adjugate_dev(const double* m, int k, int ld, double* adj, double* scratch) {
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j) adj[i * ld + j] = 0.0;
+  if (k == 1) { adj[0] = 1.0; return; }
+#define MM(i, j) m[(i) * ld + (j)]
+  if (k == 2) {
+    adj[0] = MM(1, 1); adj[1] = -MM(0, 1); adj[ld] = -MM(1, 0); adj[ld + 1] = MM(0, 0);
+    return;
+  }
+  if (k == 3) {
+    adj[0 * ld + 0] = MM(1, 1) * MM(2, 2) - MM(1, 2) * MM(2, 1);
+    adj[0 * ld + 1] = MM(0, 2) * MM(2, 1) - MM(0, 1) * MM(2, 2);
+    adj[0 * ld + 2] = MM(0, 1) * MM(1, 2) - MM(0, 2) * MM(1, 1);
+    adj[1 * ld + 0] = MM(1, 2) * MM(2, 0) - MM(1, 0) * MM(2, 2);
+    adj[1 * ld + 1] = MM(0, 0) * MM(2, 2) - MM(0, 2) * MM(2, 0);
+    adj[1 * ld + 2] = MM(0, 2) * MM(1, 0) - MM(0, 0) * MM(1, 2);
+    adj[2 * ld + 0] = MM(1, 0) * MM(2, 1) - MM(1, 1) * MM(2, 0);
+    adj[2 * ld + 1] = MM(0, 1) * MM(2, 0) - MM(0, 0) * MM(2, 1);
+    adj[2 * ld + 2] = MM(0, 0) * MM(1, 1) - MM(0, 1) * MM(1, 0);
+    return;
+  }
+  double* lu = scratch;  // k x k, ld k
+  int piv[kMaxRank];
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j) lu[i * k + j] = MM(i, j);
+  double det, maxpiv = 0.0, minpiv = 0.0;
+  if (lu_factor_dev(lu, k, k, piv, &det)) {
+    maxpiv = fabs(lu[0]);
+    minpiv = maxpiv;
+    for (int i = 1; i < k; ++i) {
+      const double pv = fabs(lu[i * k + i]);
+      maxpiv = fmax(maxpiv, pv);
+      minpiv = fmin(minpiv, pv);
+    }
+  }
+  if (minpiv > 1e-8 * maxpiv) {
+    double x[kMaxRank];
+    for (int j = 0; j < k; ++j) {
+      for (int i = 0; i < k; ++i) x[i] = (piv[i] == j) ? det : 0.0;
+      for (int i = 1; i < k; ++i)
+        for (int l = 0; l < i; ++l) x[i] -= lu[i * k + l] * x[l];
+      for (int ii = k; ii-- > 0;) {
+        for (int l = ii + 1; l < k; ++l) x[ii] -= lu[ii * k + l] * x[l];
+        x[ii] /= lu[ii * k + ii];
+      }
+      for (int i = 0; i < k; ++i) adj[i * ld + j] = x[i];
+    }
+    return;
+  }
+  double* minor = scratch + k * k;
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j) {
+      int mr = 0;
+      for (int r = 0; r < k; ++r) {
+        if (r == i) continue;
+        int mc = 0;
+        for (int c = 0; c < k; ++c) {
+          if (c == j) continue;
+          minor[mr * (k - 1) + mc] = MM(r, c);
+          ++mc;
+        }
+        ++mr;
+      }
+      double dm;
+      int pv[kMaxRank];
+      lu_factor_dev(minor, k - 1, k - 1, pv, &dm);
+      adj[j * ld + i] = (((i + j) % 2) ? -1.0 : 1.0) * dm;
+    }
+#undef MM
+}
+
+}  // namespace eigb
