@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark: updated eigenpairs/sec (FP64) of the rank-k eigen-update.
+
+Workload (BASELINE.json configs[4], the n = 32768 configuration the scaling
+target is quoted on; it fits one B200): rank-16 update, n = 32768, FP64,
+Lambda ~ sort(U[-100,100]), K ~ N(0,1/n), alternating signs, Q random
+orthogonal (8.6 GB). One "step" = one full update (U = Q^T K, deflation, all
+n roots, eigenvector columns, Q' = Q X with the sign rule).
+
+  value  device throughput: n / step time, inputs resident in HBM, CUDA
+         events on the launching stream, max over ranks (inputs 8.6 GB >
+         L2, no flush needed).
+  e2e    the same update through the host-pointer C ABI
+         (eigmod_b200_update_decomposition) from pinned host memory: H2D of
+         Q, lambda, K and D2H of Q', lambda' inside the timed region.
+
+N > 1 (torchrun, one process per GPU, NCCL): Q is replicated (broadcast once
+before timing); each rank projects its slice of U and all-gathers it, plans
+redundantly, solves its slice of root indices and all-gathers the root
+records, then writes its column block of Q' (strong scaling: n fixed).
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref, the unmodified eigmod sources) on the host cores; see DESIGN.md.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "updated eigenpairs/sec (FP64, n,k) at 1/2/4/8 B200; % of FP64 roofline"
+UNIT = "eigenpairs/s"
+REF_SAMPLE_N = 2048
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--n", type=int, default=None, help="override n (smaller smoke runs)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------ CPU baseline
+def reference_sample(n=REF_SAMPLE_N, reps=1, warm=1):
+    """The unmodified reference (oracle/_ref) on the config-4 family at n =
+    2048, the largest size it completes reliably (it throws
+    at n >= 8192 and on 3/5 seeds at n = 4096). OpenMP on all host cores
+    (kernels::set_parallel(true), the reference's --parallel)."""
+    from oracle import ref
+    from paper_1706_00773_b200.instances import make_instance
+
+    q, lam, kmat, signs = make_instance(4, n=n, seed=11)
+    ref.set_parallel(True)
+    tol = ref.default_tolerance(lam, kmat, signs)
+    times = []
+    for i in range(warm + reps):
+        t0 = time.perf_counter()
+        ref.update_pairs(q, lam, kmat, signs, tol)
+        dt = time.perf_counter() - t0
+        if i >= warm:
+            times.append(dt)
+    cores = ref.worker_count()
+    return times, cores, n
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    times, cores, n = reference_sample(reps=args.steps, warm=args.warmup)
+    t = statistics.median(times)
+    v = n / t
+    line = {
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"config-4 family (rank-16, Lambda~U[-100,100], alternating "
+                               f"signs) at n={n}: bounded sample of the n=32768 workload",
+                   "n": n, "k": 16},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"reference update_eigenvalues_full + assemble_eigenvectors "
+                                   f"(oracle/_ref, OpenMP {cores} threads) at n={n}, median of "
+                                   f"{args.steps}"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- our arm
+def fp64_peak_measured(torch, dev):
+    """cuBLAS DGEMM 8192^3 (best of 3): the FP64 tensor roofline denominator
+    measured live (MEASURED_PEAKS.json has no FP64 entry)."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    torch.matmul(a, b)
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(3):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1706_00773_b200 import capi
+    from paper_1706_00773_b200.instances import CONFIGS, make_instance_torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = CONFIGS[args.config]
+    n = args.n or cfg["n"]
+    k = cfg["k"]
+    # instance: rank 0 generates, Q is replicated by NCCL broadcast (before timing)
+    if rank == 0:
+        q, lam, kmat, signs = make_instance_torch(args.config, n=n, device=dev)
+    else:
+        q = torch.empty((n, n), dtype=torch.float64, device=dev)
+        lam = torch.empty(n, dtype=torch.float64, device=dev)
+        kmat = torch.empty((n, k), dtype=torch.float64, device=dev)
+        signs = torch.tensor(cfg["signs"], dtype=torch.int32)
+    if world > 1:
+        for t in (q, lam, kmat):
+            dist.broadcast(t, 0)
+    signs_np = signs.numpy().astype(np.int32)
+    torch.cuda.synchronize()
+
+    ctx = capi.Context(local)
+    ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+    ctx.set_option("timing", 1.0)
+    lam_out = torch.empty(n, dtype=torch.float64, device=dev)
+
+    if world == 1:
+        q_out = torch.empty((n, n), dtype=torch.float64, device=dev)
+
+        def step():
+            capi.update_decomposition_device(q, lam, kmat, signs_np, lam_out, q_out, ctx=ctx)
+    else:
+        from paper_1706_00773_b200.sharded import ShardedUpdate
+
+        shard = ShardedUpdate(ctx, n, k, signs_np, rank, world, dev)
+        q_out = shard.alloc_output()
+
+        def step():
+            shard.run(q, lam, kmat, lam_out, q_out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ctx.stage_times(reset=True)
+    launches0 = capi.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = capi.launch_count() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    stages = ctx.stage_times()
+    stats = ctx.stats()
+
+    out = {}
+    if rank == 0:
+        value = n / (ms * 1e-3)
+        calls = max(1, stages["calls"])
+        gemm_ms = stages["k5_gemm"] / calls
+        cols = n if world == 1 else shard.ncols_local
+        gemm_flops = 2.0 * n * n * cols
+        peak = fp64_peak_measured(torch, dev)
+        achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+        solve_ms = stages["k3_solve"] / calls
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded; Q from a GPU QR of a Philox N(0,1) matrix)",
+            "config": {"workload": cfg["name"], "n": n, "k": k, "signs": list(cfg["signs"]),
+                       "parallelism": f"roots+columns x{world}",
+                       "l2": "inputs (8.6 GB Q) exceed L2; no flush"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "stage_ms": {kk: round(v / calls, 3) for kk, v in stages.items() if kk != "calls"},
+            "solver": {"roots": stats["roots"], "evals_per_root":
+                       stats["evals"] / max(1.0, stats["roots"]), "max_evals": stats["max_evals"]},
+            "roofline": {"kernel": "K5 dmma_gemm_nt_kernel (Q' = Q X, DMMA.8x8x4)",
+                         "bound": "tensor", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
+                         "peak_source": "cuBLAS DGEMM 8192^3 measured live in this run "
+                                        "(MEASURED_PEAKS.json has no FP64 entry; DMMA loop "
+                                        "ceiling 37.0, profiles/fp64_peaks_r01.json)",
+                         "algorithmic_flops_per_launch": gemm_flops,
+                         "traffic": None},
+        }
+        # CPU secular-solver roofline (K3): algorithmic flops per S evaluation
+        kp = int(stats["kp"]) or 1
+        fl_eval = n * (k * (k + 1) + 1)
+        out["roofline_k3"] = {
+            "bound": "fp64", "evals": stats["evals"],
+            "achieved": stats["evals"] * fl_eval / (solve_ms * 1e-3) / 1e12 if solve_ms else None,
+            "unit": "TFLOP/s", "note": f"n*(k(k+1)+1) flops per S(x) evaluation, kp={kp}"}
+    # ---- e2e through the host-pointer C ABI (single GPU)
+    if world == 1 and not args.no_e2e:
+        h_q = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        h_q.copy_(q)
+        h_lam = lam.cpu().numpy()
+        h_k = kmat.cpu().numpy()
+        h_qo = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        h_lo = np.empty(n)
+        del q_out
+        torch.cuda.empty_cache()
+        import ctypes as C
+
+        qp = C.cast(h_q.data_ptr(), capi._D)
+        qop = C.cast(h_qo.data_ptr(), capi._D)
+        ectx = capi.Context(local)
+        sg = np.ascontiguousarray(signs_np)
+
+        def e2e_step():
+            wt = np.zeros(1)
+            ectx.check(ectx._l.eigmod_b200_update_decomposition(
+                ectx.h, qp, capi._dp(np.ascontiguousarray(h_lam)), capi._dp(np.ascontiguousarray(h_k)),
+                sg.ctypes.data_as(capi._I32), n, k, C.c_double(1e-12), capi._dp(h_lo), qop,
+                capi._dp(wt)))
+            return wt[0]
+
+        for _ in range(max(1, min(args.warmup, 2))):
+            e2e_step()
+        ts = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            e2e_step()
+            ts.append(time.perf_counter() - t0)
+        te = statistics.mean(ts)
+        out["e2e"] = {"value": n / te, "unit": UNIT,
+                      "h2d_bytes_per_step": 8 * (n * n + n + n * k),
+                      "d2h_bytes_per_step": 8 * (n * n + n),
+                      "ms_per_step": te * 1e3,
+                      "path": "eigmod_b200_update_decomposition (host pointers, pinned)"}
+        ectx.close()
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        try:
+            times, cores, ns = reference_sample(reps=3, warm=1)
+            t = statistics.median(times)
+            out["cpu_baseline"] = {
+                "value": ns / t, "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"unmodified reference (oracle/_ref) update_eigenvalues_full + "
+                          f"assemble_eigenvectors, config-4 family at n={ns} (largest size it "
+                          f"completes; throws at n>=8192), OpenMP {cores} threads, median of 3"}
+        except Exception as e:  # the baseline is reported, never required
+            out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(),
+                                   "kind": "reference", "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -46,7 +46,8 @@ void eigmod_b200_ctx_destroy(eigmod_b200_ctx* ctx);
 /* Run on an existing cudaStream_t (e.g. torch's current stream). NULL
  * restores the context's own stream. */
 int eigmod_b200_ctx_set_stream(eigmod_b200_ctx* ctx, void* cuda_stream);
-/* Options: "run_rel" = near-equal-pole run threshold relative to
+/* Options: "timing" = 1 enables per-stage CUDA-event timing;
+ * "run_rel" = near-equal-pole run threshold relative to
  * max(1,max|lambda|) used by the solve (1e-10 exact mode, the default;
  * 1e-12 = the reference's kPoleMergeRelGap, secular.hpp:66). */
 int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value);
@@ -56,6 +57,14 @@ const char* eigmod_b200_last_stage(const eigmod_b200_ctx* ctx);
  * [3] total S(x) evaluations, [4] max evaluations of one root,
  * [5] padded rank, [6] effective rank, [7] pole groups. */
 int eigmod_b200_stats(const eigmod_b200_ctx* ctx, double* stats8);
+/* Cumulative per-stage device time (CUDA events on the context stream) of
+ * eigmod_b200_update_decomposition[_device] calls made with option
+ * "timing" = 1: ms8[0] K1 projection, [1] K2 deflation/plan, [2] K3 root
+ * solve, [3] K4 eigenvector columns, [4] K5 DMMA GEMM, [5] sign rule,
+ * [7] number of timed calls. reset != 0 clears the counters. */
+int eigmod_b200_stage_times(eigmod_b200_ctx* ctx, double* ms8, int reset);
+/* Kernels launched by this library since load (all contexts). */
+int64_t eigmod_b200_launch_count(void);
 /* Bytes of device workspace currently held by the context. */
 int64_t eigmod_b200_workspace_bytes(const eigmod_b200_ctx* ctx);
 

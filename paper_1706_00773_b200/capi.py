@@ -59,6 +59,8 @@ def _declare(lib):
         "eigmod_b200_last_stage": (C.c_char_p, [_VP]),
         "eigmod_b200_stats": (C.c_int, [_VP, _D]),
         "eigmod_b200_workspace_bytes": (C.c_int64, [_VP]),
+        "eigmod_b200_stage_times": (C.c_int, [_VP, _D, C.c_int]),
+        "eigmod_b200_launch_count": (C.c_int64, []),
         "eigmod_b200_transform_update": (C.c_int, [_VP, _D, _D, C.c_int64, C.c_int64, _D]),
         "eigmod_b200_secular_weights": (C.c_int, [_VP, _D, _D, _I32, C.c_int64, C.c_int64, _D]),
         "eigmod_b200_deflate_problem": (C.c_int, [_VP, _D, _D, _I32, C.c_int64, C.c_int64, _D, _D,
@@ -161,6 +163,15 @@ class Context:
         self.check(self._l.eigmod_b200_stats(self.h, _dp(s)))
         keys = ["roots", "decoupled", "collided", "evals", "max_evals", "kp", "k_eff", "groups"]
         return {k: float(v) for k, v in zip(keys, s)}
+
+    def stage_times(self, reset: bool = False) -> dict:
+        """Cumulative per-stage device ms (option "timing" must be on)."""
+        s = np.zeros(8)
+        self.check(self._l.eigmod_b200_stage_times(self.h, _dp(s), 1 if reset else 0))
+        keys = ["k1_project", "k2_plan", "k3_solve", "k4_columns", "k5_gemm", "sign_rule"]
+        out = {k: float(v) for k, v in zip(keys, s)}
+        out["calls"] = int(s[7])
+        return out
 
     def workspace_bytes(self) -> int:
         return int(self._l.eigmod_b200_workspace_bytes(self.h))
@@ -327,6 +338,11 @@ def default_tolerance(lam, kmat) -> float:
 # --------------------------------------------------------- device (torch) API
 def _ptr(t):
     return _VP(t.data_ptr())
+
+
+def launch_count() -> int:
+    """Kernels launched by libeigmod_b200.so in this process."""
+    return int(lib().eigmod_b200_launch_count())
 
 
 def padded_rank(k: int) -> int:

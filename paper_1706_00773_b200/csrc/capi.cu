@@ -11,6 +11,7 @@
 // read-backs between stages and the bookkeeping of the reference's output
 // lists; every O(n^2) or larger step runs on the GPU.
 #include <algorithm>
+#include <atomic>
 #include <cfloat>
 #include <chrono>
 #include <cmath>
@@ -34,7 +35,26 @@ struct eigmod_b200_ctx {
   double run_rel = eigb::kExactRunRelGap;
   const double* lam = nullptr;  // lambda of the current plan (rank-0 copy)
   std::string err, stage;
+  // per-stage CUDA-event timing (option "timing"): 0 K1 project, 1 K2 plan,
+  // 2 K3 solve, 3 K4 columns, 4 K5 GEMM, 5 sign rule
+  bool timing = false;
+  cudaEvent_t ev[8] = {};
+  double stage_ms[8] = {};
+  int64_t timed_calls = 0;
+  void mark(int i) {
+    if (!timing) return;
+    if (!ev[i]) EIGB_CUDA(cudaEventCreate(&ev[i]));
+    EIGB_CUDA(cudaEventRecord(ev[i], stream));
+  }
 };
+
+namespace eigb {
+namespace {
+std::atomic<int64_t> g_launches{0};
+}
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(); }
+}  // namespace eigb
 
 namespace {
 
@@ -215,17 +235,35 @@ void finish(eigmod_b200_ctx* c, const double* q, const double* lam_in, int64_t c
   double* colscale = c->ws.get_f64("colscale", nc);
   int* cmode = c->ws.get_i32("colmode", nc);
   eigb::build_xt_dev(p, c->recs, cols, colldir, collok, c0, c1, xt, colscale, cmode, c->stream);
-  eigb::back_transform_dev(q, xt, n, nc, colscale, cmode, q_out, ldq, c->ws, c->stream);
+  c->mark(4);
+  double* tcm = eigb::tile_colmax_buffer(n, nc, c->ws);
+  eigb::gemm_nt_dev(q, xt, n, nc, n, q_out, ldq, colscale, tcm, c->stream);
+  c->mark(5);
+  eigb::sign_rule_dev(tcm, n, nc, cmode, q_out, ldq, c->ws, c->stream);
+  c->mark(6);
 }
 
 void full_device(eigmod_b200_ctx* c, const double* q, const double* lam, const double* kmat,
                  const int* signs, int64_t n, int64_t k, double* lam_out, double* q_out) {
   const int kp = eigb::padded_rank(k);
   double* u = c->ws.get_f64("cap_u_full", (size_t)n * kp);
+  c->mark(0);
   project(c, q, kmat, n, k, 0, n, u);
+  c->mark(1);
   plan_from_u(c, lam, u, signs, n, k, c->run_rel);
+  c->mark(2);
   solve(c, 0, c->plan.nred);
+  c->mark(3);
   finish(c, q, lam, 0, n, lam_out, q_out, n);
+  if (c->timing && c->plan.k > 0) {
+    EIGB_CUDA(cudaEventSynchronize(c->ev[6]));
+    for (int i = 0; i < 6; ++i) {
+      float ms = 0.f;
+      EIGB_CUDA(cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]));
+      c->stage_ms[i] += ms;
+    }
+    c->timed_calls += 1;
+  }
 }
 
 }  // namespace
@@ -277,6 +315,8 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
     if (std::string(key) == "run_rel") {
       if (!(value > 0.0 && value < 1e-3)) throw Error(1, "", "set_option: run_rel out of range");
       ctx->run_rel = value;
+    } else if (std::string(key) == "timing") {
+      ctx->timing = value != 0.0;
     } else {
       throw Error(1, "", std::string("set_option: unknown key ") + key);
     }
@@ -322,6 +362,20 @@ int eigmod_b200_stats(const eigmod_b200_ctx* cctx, double* s) {
 int64_t eigmod_b200_workspace_bytes(const eigmod_b200_ctx* ctx) {
   return ctx ? (int64_t)ctx->ws.bytes() : 0;
 }
+
+int eigmod_b200_stage_times(eigmod_b200_ctx* ctx, double* ms8, int reset) {
+  return guarded(ctx, [&] {
+    for (int i = 0; i < 6; ++i) ms8[i] = ctx->stage_ms[i];
+    ms8[6] = 0.0;
+    ms8[7] = (double)ctx->timed_calls;
+    if (reset) {
+      for (double& v : ctx->stage_ms) v = 0.0;
+      ctx->timed_calls = 0;
+    }
+  });
+}
+
+int64_t eigmod_b200_launch_count(void) { return eigb::launch_count(); }
 
 int eigmod_b200_padded_rank(int64_t k) { return eigb::padded_rank(k); }
 int eigmod_b200_record_width(int kp) { return kRecHead + kp; }

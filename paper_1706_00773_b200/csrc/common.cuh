@@ -25,7 +25,12 @@ struct Error : std::runtime_error {
       throw ::eigb::Error(3, "cuda", std::string(#x) + ": " + cudaGetErrorString(e_));       \
   } while (0)
 
-#define EIGB_LAUNCH_CHECK() EIGB_CUDA(cudaGetLastError())
+void note_launch();
+#define EIGB_LAUNCH_CHECK()          \
+  do {                               \
+    EIGB_CUDA(cudaGetLastError());   \
+    ::eigb::note_launch();           \
+  } while (0)
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

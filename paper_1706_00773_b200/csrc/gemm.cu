@@ -16,6 +16,8 @@
 // sign rule (eigvec.cpp:340-347), which a second pass applies.
 #include "pipeline.cuh"
 
+#include <algorithm>
+
 namespace eigb {
 
 namespace {
@@ -245,22 +247,23 @@ void gemm_nt_dev(const double* a, const double* b, int64_t m, int64_t nn, int64_
   EIGB_LAUNCH_CHECK();
 }
 
-void back_transform_dev(const double* a, const double* xt, int64_t n, int64_t ncols,
-                        const double* colscale, const int* mode, double* c, int64_t ldc,
-                        DeviceScratch& ws, cudaStream_t st) {
+void sign_rule_dev(const double* tile_colmax, int64_t n, int64_t ncols, const int* mode, double* c,
+                   int64_t ldc, DeviceScratch& ws, cudaStream_t st) {
   if (ncols <= 0) return;
   const int64_t tiles_m = cdiv(n, BM);
-  double* tcm = ws.get_f64("gemm_tile_colmax", (size_t)tiles_m * ncols);
-  gemm_nt_dev(a, xt, n, ncols, n, c, ldc, colscale, tcm, st);
   double* flip = ws.get_f64("gemm_flip", ncols);
   int* any = ws.get_i32("gemm_any_flip", 1);
-  colsign_kernel<<<(unsigned)cdiv(ncols, 256), 256, 0, st>>>(tcm, tiles_m, ncols, mode, flip);
+  colsign_kernel<<<(unsigned)cdiv(ncols, 256), 256, 0, st>>>(tile_colmax, tiles_m, ncols, mode, flip);
   EIGB_LAUNCH_CHECK();
   EIGB_CUDA(cudaMemsetAsync(any, 0, 4, st));
   any_flip_kernel<<<(unsigned)cdiv(ncols, 256), 256, 0, st>>>(flip, ncols, any);
   EIGB_LAUNCH_CHECK();
   apply_sign_kernel<<<148 * 8, 256, 0, st>>>(c, n, ncols, ldc, flip, any);
   EIGB_LAUNCH_CHECK();
+}
+
+double* tile_colmax_buffer(int64_t n, int64_t ncols, DeviceScratch& ws) {
+  return ws.get_f64("gemm_tile_colmax", (size_t)cdiv(n, BM) * std::max<int64_t>(ncols, 1));
 }
 
 }  // namespace eigb

@@ -63,12 +63,18 @@ void build_xt_dev(const Plan& p, const RootRecords& roots, const Columns& cols,
                   const double* colldir, const int* collok, int64_t c0, int64_t c1, double* xt,
                   double* colscale, int* colsign_mode, cudaStream_t st);
 
-// gemm.cu: C[:, c0:c1] = (A Xt^T) diag(scale) with the reference's sign rule
-// on columns whose mode is 1 (proj/src/eigvec.cpp:340-347).
-void back_transform_dev(const double* a, const double* xt, int64_t n, int64_t ncols,
-                        const double* colscale, const int* colsign_mode, double* c, int64_t ldc,
-                        DeviceScratch& ws, cudaStream_t st);
+// gemm.cu: C[:, c0:c1] = (A Xt^T) diag(scale) on the DMMA pipe; the
+// epilogue leaves per-(row tile, column) signed maxima in tile_colmax, and
+// sign_rule_dev applies the reference's sign rule (proj/src/eigvec.cpp:340-347)
+// to the columns whose mode is 1.
 void gemm_nt_dev(const double* a, const double* b, int64_t m, int64_t nn, int64_t kk, double* c,
                  int64_t ldc, const double* colscale, double* tile_colmax, cudaStream_t st);
+double* tile_colmax_buffer(int64_t n, int64_t ncols, DeviceScratch& ws);
+void sign_rule_dev(const double* tile_colmax, int64_t n, int64_t ncols, const int* mode, double* c,
+                   int64_t ldc, DeviceScratch& ws, cudaStream_t st);
+
+// Kernel launches issued by this library (evidence for bench.py's
+// gpu_launches); incremented by EIGB_LAUNCH_CHECK.
+int64_t launch_count();
 
 }  // namespace eigb

@@ -1,0 +1,329 @@
+"""Parity of the sm_100a path (through the C ABI) with the oracle, the
+reference fixtures and LAPACK. Every test here needs a B200."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SEEDED = np.load(os.path.join(HERE, "golden", "ref_seeded.npz"))
+CASES = np.load(os.path.join(HERE, "golden", "ref_cases.npz"))
+
+
+def _cases(npz):
+    keys = sorted({k.split("__")[0] for k in npz.files})
+    return [(k, {f.split("__")[1]: npz[f] for f in npz.files if f.split("__")[0] == k}) for k in keys]
+
+
+SEEDED_CASES = _cases(SEEDED)
+RANDOM_CASES = _cases(CASES)
+IDS = [n for n, _ in SEEDED_CASES]
+
+
+def _aprime(q, lam, kmat, signs):
+    a = q @ np.diag(lam) @ q.T + kmat @ np.diag(np.asarray(signs, float)) @ kmat.T
+    return 0.5 * (a + a.T)
+
+
+@pytest.fixture(scope="module")
+def api(ctx):
+    from paper_1706_00773_b200 import capi
+
+    return capi
+
+
+# ----------------------------------------------------------- stages
+@pytest.mark.parametrize("name,c", SEEDED_CASES, ids=IDS)
+def test_transform_update(api, ctx, name, c):
+    u = api.transform_update(c["q"], c["kmat"], ctx=ctx)
+    scale = max(1.0, float(np.abs(c["u"]).max()))
+    assert np.abs(u - c["u"]).max() <= 1e-13 * scale
+
+
+@pytest.mark.parametrize("name,c", SEEDED_CASES, ids=IDS)
+def test_deflation_record_matches_reference(api, ctx, name, c):
+    d = api.deflate_problem(c["lam"], c["u"], c["signs"], ctx=ctx)
+    # decisions depend on input bits only (runs, row mass); alpha within rounding
+    assert np.array_equal(d.pole_origin, c["dp_pole_origin"])
+    assert np.array_equal(d.unchanged, c["dp_unchanged"])
+    assert np.array_equal(d.collided, c["dp_collided"])
+    assert np.array_equal(d.poles, c["dp_poles"])
+    w = c["dp_weights"]
+    if len(w):
+        scale = np.abs(w) + np.abs(w).sum() / len(w)
+        # the reference's own alpha is unstable on merged clusters (|alpha| ~ 1e64)
+        tau = 1e-9 if not name.startswith("c3") else 1e-6
+        assert np.all(np.abs(d.weights - w) <= tau * scale)
+
+
+def test_secular_weights_vs_oracle(api, ctx):
+    rng = np.random.default_rng(9)
+    for k in (1, 2, 3, 4, 5, 8, 16):
+        n = 60
+        lam = np.sort(rng.uniform(-2, 2, n))
+        u = rng.standard_normal((n, k)) / math.sqrt(n)
+        s = np.where(np.arange(k) % 2 == 0, 1, -1)
+        a_gpu = api.secular_weights(lam, u, s, ctx=ctx)
+        a_ref = port.secular_weights(lam, u, s)
+        scale = np.abs(a_ref) + np.abs(a_ref).sum() / n
+        assert np.all(np.abs(a_gpu - a_ref) <= 1e-10 * scale), k
+
+
+# ------------------------------------------------------ eigenpairs
+@pytest.mark.parametrize("name,c", SEEDED_CASES, ids=IDS)
+def test_update_decomposition_parity(api, ctx, name, c):
+    q, lam, kmat, s = c["q"], c["lam"], c["kmat"], c["signs"]
+    res = api.update_decomposition(q, lam, kmat, s, float(c["tol"]), ctx=ctx)
+    a = _aprime(q, lam, kmat, s)
+    ev = np.linalg.eigvalsh(a)
+    nrm = float(np.abs(ev).max())
+    n = len(lam)
+    lo, qo, _ = port.update(q, lam, kmat, s)
+    assert np.abs(res.lam - ev).max() <= 1e-10 * nrm          # north-star eigenvalue tol
+    assert np.abs(res.lam - lo).max() <= 1e-12 * nrm          # vs the oracle
+    assert np.abs(a @ res.q - res.q * res.lam[None, :]).max() <= 1e-10 * nrm
+    assert np.abs(res.q.T @ res.q - np.eye(n)).max() <= 1e-9
+    assert np.abs(res.q - qo).max() <= 1e-8                   # same columns, same signs
+    if str(c["eig_status"]) == "ok" and np.abs(c["values"] - ev).max() <= 1e-10 * nrm:
+        assert np.abs(res.lam - c["values"]).max() <= 1e-10 * nrm
+    if str(c["vec_status"]) == "ok":
+        assert np.abs(res.q - c["q_out"]).max() <= 1e-5       # reference vectors ~1e-7
+
+
+@pytest.mark.parametrize("name,c", RANDOM_CASES, ids=[n for n, _ in RANDOM_CASES])
+def test_reference_random_instances(api, ctx, name, c):
+    # tests/test_rootfind.cpp:163-178 and test_eigvec.cpp:133-183 instances
+    res = api.update_decomposition(c["q"], c["lam"], c["kmat"], c["signs"], float(c["tol"]),
+                                   ctx=ctx)
+    ev = np.linalg.eigvalsh(_aprime(c["q"], c["lam"], c["kmat"], c["signs"]))
+    assert np.abs(res.lam - ev).max() <= 1e-12 * max(1.0, float(np.abs(ev).max()))
+    if str(c["eig_status"]) == "ok":
+        assert np.abs(res.lam - c["values"]).max() <= 1e-9
+    if str(c["vec_status"]) == "ok":
+        assert np.abs(res.q - c["q_out"]).max() <= 1e-5
+
+
+def test_update_eigenvalues_full_fields(api, ctx):
+    name, c = SEEDED_CASES[0]
+    up = api.update_eigenvalues_full(c["q"], c["lam"], c["kmat"], c["signs"], 1e-12, ctx=ctx)
+    assert np.all(np.diff(up.values) >= 0)
+    assert 0 < len(up.roots) <= len(c["lam"]) and np.all(np.diff(up.roots) >= 0)
+    assert np.abs(up.u - c["u"]).max() <= 1e-13 * max(1.0, float(np.abs(c["u"]).max()))
+    assert np.array_equal(up.problem.pole_origin, c["dp_pole_origin"])
+
+
+# ---------------------------------------------------------- goldens
+R2 = math.sqrt(2.0)
+
+
+def test_golden_2x2(api, ctx):
+    # tests/test_eigvec.cpp:107-123, test_cli.cpp:62-63
+    res = api.update_decomposition(np.eye(2), [0.0, 1.0], [[1.0, 0.0], [1.0, 1.0]], [1, 1], 1e-14,
+                                   metrics=True, ctx=ctx)
+    assert abs(res.lam[0] - 0.58578643762690495) <= 1e-12 * 2
+    assert abs(res.lam[1] - 3.4142135623730951) <= 1e-12 * 4
+    lam = 2.0 - R2
+    nrm = math.sqrt(1.0 + (lam - 1.0) ** 2)
+    assert abs(res.q[0, 0] - 1.0 / nrm) <= 1e-12 and abs(res.q[1, 0] - (lam - 1.0) / nrm) <= 1e-12
+    assert res.residual_fro <= 1e-10 and res.ortho_err <= 1e-12
+
+
+def test_golden_k_zero_bit_exact(api, ctx):
+    # tests/test_eigvec.cpp:97-105
+    rng = np.random.default_rng(77)
+    q, _ = np.linalg.qr(rng.standard_normal((8, 8)))
+    lam = np.sort(rng.uniform(-1, 1, 8))
+    res = api.update_decomposition(q, lam, np.zeros((8, 2)), [1, 1], 1e-12, metrics=True, ctx=ctx)
+    assert np.array_equal(res.lam, lam) and np.array_equal(res.q, q)
+    assert res.residual_fro == 0.0 or res.residual_fro < 1e-15
+
+
+def test_golden_unchanged_rows_copy_columns_exactly(api, ctx):
+    # rows of U that vanish leave their eigenpairs untouched (secular.cpp:316-325,
+    # eigvec.cpp:288-291): the matching columns of Q' are exact copies.
+    rng = np.random.default_rng(4)
+    n = 12
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.sort(rng.uniform(-1, 1, n))
+    u = rng.standard_normal((n, 2))
+    u[[2, 7]] = 0.0
+    kmat = q @ u
+    u2 = q.T @ kmat
+    res = api.update_decomposition(q, lam, kmat, [1, -1], 1e-12, ctx=ctx)
+    for i in (2, 7):
+        if np.abs(u2[i]).max() == 0.0:
+            col = int(np.where(res.lam == lam[i])[0][0])
+            assert np.array_equal(res.q[:, col], q[:, i])
+
+
+def test_golden_rank1_collision(api, ctx):
+    # tests/test_rootfind.cpp:150-161
+    vals = api.update_eigenvalues(np.eye(2), [1.0, 2.0], [[1.0], [0.0]], [1], 1e-14, ctx=ctx)
+    assert np.allclose(vals, [2.0, 2.0], rtol=0, atol=2e-12)
+
+
+def test_golden_collided_vector(api, ctx):
+    # tests/test_eigvec.cpp:64-76
+    res = api.update_decomposition(np.eye(2), [0.0, 1.0], np.eye(2), [1, 1], 1e-14, ctx=ctx)
+    assert np.allclose(res.lam, [1.0, 2.0], atol=1e-14)
+    assert np.allclose(np.abs(res.q), np.eye(2), atol=1e-14)
+
+
+def test_golden_weights_and_deflation(api, ctx):
+    # tests/test_secular.cpp:97-126, 273-298
+    inv = 1.0 / R2
+    assert np.allclose(api.secular_weights([1.0, 2.0], [[inv], [inv]], [1], ctx=ctx), [0.5, 0.5],
+                       rtol=1e-13)
+    a = api.secular_weights([0.0, 1.0], np.eye(2), [1, 1], ctx=ctx)
+    assert abs(a[0] - 2.0) <= 2e-13 and abs(a[1]) <= 1e-15
+    assert np.allclose(api.secular_weights([0.0, 1.0], [[1.0, 0.0], [1.0, 1.0]], [1, 1], ctx=ctx),
+                       [2.0, 1.0], rtol=1e-13)
+    d = api.deflate_problem([0.0, 1.0, 2.0], [[0.0], [0.5], [0.0]], [1], ctx=ctx)
+    assert np.allclose(d.poles, [1.0]) and np.allclose(d.weights, [0.25])
+    assert list(d.unchanged) == [0, 2] and list(d.pole_origin) == [1]
+    d = api.deflate_problem([1.0, 1.0 + 1e-15, 2.0], [[1.0], [2.0], [1.0]], [1], ctx=ctx)
+    assert len(d.poles) == 2 and abs(d.weights[0] - 5.0) <= 5e-9 and len(d.unchanged) == 1
+
+
+def test_error_behaviour(api, ctx):
+    # std::invalid_argument (core.cpp:89-97, rootfind.cpp:384) / NumericalError("deflate")
+    with pytest.raises(ValueError):
+        api.update_decomposition(np.eye(2), [0.0, 1.0], np.eye(2), [1, 2], 1e-12, ctx=ctx)
+    with pytest.raises(ValueError):
+        api.update_decomposition(np.eye(2), [0.0, 1.0], np.ones((2, 3)), [1, 1, 1], 1e-12, ctx=ctx)
+    with pytest.raises(ValueError):
+        api.update_decomposition(np.eye(2), [0.0, 1.0], np.eye(2), [1, 1], 0.0, ctx=ctx)
+    with pytest.raises(ValueError):
+        api.update_decomposition(np.eye(2), [0.0, 1.0], [[np.nan, 0.0], [0.0, 1.0]], [1, 1], 1e-12,
+                                 ctx=ctx)
+    with pytest.raises(api.NumericalError) as e:
+        api.update_decomposition(np.eye(2), [1.0, 0.0], np.eye(2), [1, 1], 1e-12, ctx=ctx)
+    assert e.value.stage == "deflate"
+    with pytest.raises(ValueError):
+        api.secular_weights([1.0, 1.0], [[1.0], [0.0]], [1], ctx=ctx)
+
+
+def test_deterministic(api, ctx):
+    from paper_1706_00773_b200.instances import make_instance
+
+    q, lam, kmat, s = make_instance(4, n=384, seed=21)
+    r1 = api.update_decomposition(q, lam, kmat, s, 1e-12, ctx=ctx)
+    r2 = api.update_decomposition(q, lam, kmat, s, 1e-12, ctx=ctx)
+    assert np.array_equal(r1.lam, r2.lam) and np.array_equal(r1.q, r2.q)
+
+
+# ----------------------------------------------- staged (multi-GPU) path
+def test_staged_path_equals_one_shot(api, ctx):
+    """The root/column-partitioned data path, run as two virtual ranks on one
+    GPU one after the other (no cross-rank waits): same bits as one shot."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1706_00773_b200.instances import make_instance
+    from paper_1706_00773_b200.sharded import CudaBackend, split
+
+    q, lam, kmat, s = make_instance(2, n=700, seed=5)
+    dev = torch.device("cuda", 0)
+    tq, tl, tk = (torch.from_numpy(x).to(dev) for x in (q, lam, kmat))
+    n, k = kmat.shape
+    lo1 = torch.empty(n, dtype=torch.float64, device=dev)
+    qo1 = torch.empty((n, n), dtype=torch.float64, device=dev)
+    api.update_decomposition_device(tq, tl, tk, s, lo1, qo1, ctx=ctx)
+    ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+    be = CudaBackend(ctx, n, k, s)
+    world = 2
+    u_all = torch.zeros((split(n, world, 0)[2] * world, be.kp), dtype=torch.float64, device=dev)
+    for r in range(world):
+        a, b, ch = split(n, world, r)
+        part = torch.zeros((ch, be.kp), dtype=torch.float64, device=dev)
+        be.project(tq, tk, a, b, part)
+        u_all[r * ch: r * ch + (b - a)] = part[: b - a]
+    nred = be.plan(tl, u_all[:n])
+    recs = []
+    for r in range(world):
+        j0, j1, jc = split(nred, world, r)
+        part = torch.zeros((jc, be.width), dtype=torch.float64, device=dev)
+        be.solve(j0, j1, part)
+        recs.append(part[: j1 - j0])
+    rec_all = torch.cat(recs)
+    lo2 = torch.empty(n, dtype=torch.float64, device=dev)
+    qo2 = torch.empty((n, n), dtype=torch.float64, device=dev)
+    for r in range(world):
+        c0, c1, _ = split(n, world, r)
+        blk = torch.empty((n, c1 - c0), dtype=torch.float64, device=dev)
+        be.finish(tq, rec_all, c0, c1, lo2, blk)
+        qo2[:, c0:c1] = blk
+    torch.cuda.synchronize()
+    assert torch.equal(lo1, lo2)
+    assert torch.equal(qo1, qo2)
+
+
+# ------------------------------------------------- full-size configs
+def _device_checks(api, ctx, cfg, n=None, lapack=True, oracle_roots=64):
+    import torch
+
+    from paper_1706_00773_b200.instances import make_instance_torch
+
+    dev = torch.device("cuda", 0)
+    q, lam, kmat, signs = make_instance_torch(cfg, n=n, device=dev)
+    n, k = kmat.shape
+    lo = torch.empty(n, dtype=torch.float64, device=dev)
+    qo = torch.empty((n, n), dtype=torch.float64, device=dev)
+    api.update_decomposition_device(q, lam, kmat, signs.numpy(), lo, qo, ctx=ctx)
+    torch.cuda.synchronize()
+    st = ctx.stats()
+    sg = signs.to(dev, torch.float64)
+    # size-independent identities: trace and Frobenius norm of A'
+    u = q.T @ kmat
+    tr = float(lam.sum() + (sg * (kmat * kmat).sum(0)).sum())
+    assert abs(float(lo.sum()) - tr) <= 1e-10 * n * max(1.0, float(lam.abs().max()))
+    w = u * sg[None, :]
+    fro2 = float((lam * lam).sum() + 2.0 * (lam[:, None] * w * u).sum()
+                 + ((u.T @ u) * (sg[:, None] * sg[None, :]) * (u.T @ u)).sum())
+    assert abs(float((lo * lo).sum()) - fro2) <= 1e-10 * fro2
+    # residual A'Q' - Q'Lambda' = Q(Lambda(Q^T Q')) + K J (K^T Q') - Q' Lambda' and ortho
+    nrm = float(lo.abs().max())
+    qtq = q.T @ qo
+    r = q @ (lam[:, None] * qtq) + kmat @ (sg[:, None] * (kmat.T @ qo)) - qo * lo[None, :]
+    resid = float(r.abs().max()) / nrm
+    del r
+    ortho = float((qo.T @ qo - torch.eye(n, dtype=torch.float64, device=dev)).abs().max())
+    assert resid <= 1e-10, resid
+    assert ortho <= 1e-9, ortho
+    if lapack:
+        a = q @ (lam[:, None] * q.T) + kmat @ (sg[:, None] * kmat.T)
+        ev = torch.linalg.eigvalsh(0.5 * (a + a.T))
+        assert float((lo - ev).abs().max()) <= 1e-10 * nrm
+    if oracle_roots and st["decoupled"] == 0:
+        # exact per-root parity with the oracle at full size on a sample of roots
+        uu = u.cpu().numpy()
+        lh = lam.cpu().numpy()
+        js = np.linspace(0, n - 1, oracle_roots).astype(int)
+        lo_h = lo.cpu().numpy()
+        for j in js:
+            roots, _, _, _ = port.solve_roots(lh, uu, signs.numpy(), int(j), int(j) + 1)
+            assert abs(roots[0] - lo_h[j]) <= 1e-12 * nrm
+    return st, resid, ortho
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_config_full_size(api, ctx, cfg):
+    _device_checks(api, ctx, cfg)
+
+
+@pytest.mark.slow
+def test_config3_full_size_deflation(api, ctx):
+    st, _, _ = _device_checks(api, ctx, 3)
+    assert st["decoupled"] > 0
+
+
+@pytest.mark.slow
+def test_config4_full_size(api, ctx):
+    _device_checks(api, ctx, 4, lapack=False, oracle_roots=24)
