@@ -43,9 +43,11 @@ typedef struct eigmod_b200_ctx eigmod_b200_ctx;
  * owned by it; calls on one context must not overlap). */
 int eigmod_b200_ctx_create(int device, eigmod_b200_ctx** out);
 void eigmod_b200_ctx_destroy(eigmod_b200_ctx* ctx);
-/* Run on an existing cudaStream_t (e.g. torch's current stream). NULL
- * restores the context's own stream. */
+/* Run on an existing cudaStream_t (e.g. torch's current stream), taken
+ * verbatim: NULL selects the legacy default stream. */
 int eigmod_b200_ctx_set_stream(eigmod_b200_ctx* ctx, void* cuda_stream);
+/* Back to the context's own (non-blocking) stream, the default. */
+int eigmod_b200_ctx_use_own_stream(eigmod_b200_ctx* ctx);
 /* Options: "timing" = 1 enables per-stage CUDA-event timing;
  * "run_rel" = near-equal-pole run threshold relative to
  * max(1,max|lambda|) used by the solve (1e-10 exact mode, the default;

@@ -54,6 +54,7 @@ def _declare(lib):
         "eigmod_b200_ctx_create": (C.c_int, [C.c_int, C.POINTER(_VP)]),
         "eigmod_b200_ctx_destroy": (None, [_VP]),
         "eigmod_b200_ctx_set_stream": (C.c_int, [_VP, _VP]),
+        "eigmod_b200_ctx_use_own_stream": (C.c_int, [_VP]),
         "eigmod_b200_set_option": (C.c_int, [_VP, C.c_char_p, C.c_double]),
         "eigmod_b200_last_error": (C.c_char_p, [_VP]),
         "eigmod_b200_last_stage": (C.c_char_p, [_VP]),
@@ -153,7 +154,12 @@ class Context:
         raise DeviceError(msg)
 
     def set_stream(self, stream_ptr: int | None):
-        self.check(self._l.eigmod_b200_ctx_set_stream(self.h, _VP(stream_ptr or 0)))
+        """Run on this cudaStream_t handle (0 = legacy default stream);
+        None returns to the context's own stream."""
+        if stream_ptr is None:
+            self.check(self._l.eigmod_b200_ctx_use_own_stream(self.h))
+        else:
+            self.check(self._l.eigmod_b200_ctx_set_stream(self.h, _VP(int(stream_ptr))))
 
     def set_option(self, key: str, value: float):
         self.check(self._l.eigmod_b200_set_option(self.h, key.encode(), C.c_double(value)))

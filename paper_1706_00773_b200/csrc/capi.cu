@@ -33,6 +33,7 @@ struct eigmod_b200_ctx {
   bool have_plan = false;
   eigb::RootRecords recs{};
   double run_rel = eigb::kExactRunRelGap;
+  eigb::SolveOptions sopt;
   const double* lam = nullptr;  // lambda of the current plan (rank-0 copy)
   std::string err, stage;
   // per-stage CUDA-event timing (option "timing"): 0 K1 project, 1 K2 plan,
@@ -199,7 +200,7 @@ void solve(eigmod_b200_ctx* c, int64_t j0, int64_t j1) {
   if (!c->have_plan) throw Error(1, "", "solve: no plan (call plan first)");
   c->recs = alloc_records(c);
   if (c->plan.nred == 0) return;
-  eigb::solve_roots(c->plan.view(), j0, j1, c->recs, c->ws, c->sms, c->stream);
+  eigb::solve_roots(c->plan.view(), j0, j1, c->recs, c->sopt, c->ws, c->sms, c->stream);
 }
 
 __global__ void copy_block_kernel(const double* __restrict__ a, int64_t n, int64_t c0, int64_t nc,
@@ -306,7 +307,12 @@ void eigmod_b200_ctx_destroy(eigmod_b200_ctx* ctx) {
 }
 
 int eigmod_b200_ctx_set_stream(eigmod_b200_ctx* ctx, void* s) {
-  return guarded(ctx, [&] { ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own; });
+  // verbatim: NULL is the legacy default stream (torch's default stream)
+  return guarded(ctx, [&] { ctx->stream = static_cast<cudaStream_t>(s); });
+}
+
+int eigmod_b200_ctx_use_own_stream(eigmod_b200_ctx* ctx) {
+  return guarded(ctx, [&] { ctx->stream = ctx->own; });
 }
 
 int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) {
@@ -315,6 +321,11 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
     if (std::string(key) == "run_rel") {
       if (!(value > 0.0 && value < 1e-3)) throw Error(1, "", "set_option: run_rel out of range");
       ctx->run_rel = value;
+    } else if (std::string(key) == "step_tol") {
+      if (!(value > 0.0)) throw Error(1, "", "set_option: step_tol must be positive");
+      ctx->sopt.step_tol = value;
+    } else if (std::string(key) == "max_iters") {
+      ctx->sopt.max_iters = (int)value;
     } else if (std::string(key) == "timing") {
       ctx->timing = value != 0.0;
     } else {
@@ -607,7 +618,7 @@ int eigmod_b200_solve_device(eigmod_b200_ctx* ctx, int64_t j0, int64_t j1, doubl
     if (!ctx->have_plan) throw Error(1, "", "solve: no plan");
     if (j0 < 0 || j1 > ctx->plan.nred || j1 < j0) throw Error(1, "", "solve: bad root range");
     if (ctx->plan.nred == 0) return;
-    eigb::solve_roots(ctx->plan.view(), j0, j1, ctx->recs, ctx->ws, ctx->sms, ctx->stream);
+    eigb::solve_roots(ctx->plan.view(), j0, j1, ctx->recs, ctx->sopt, ctx->ws, ctx->sms, ctx->stream);
     if (d_rec_out && j1 > j0) {
       pack_records_kernel<<<(unsigned)eigb::cdiv(j1 - j0, 128), 128, 0, ctx->stream>>>(
           ctx->recs, j0, j1 - j0, ctx->plan.kp, d_rec_out);

@@ -27,7 +27,6 @@ namespace {
 
 constexpr int FLAG_COLLIDED = 1;   // bracket collapsed onto a pole
 constexpr int FLAG_UNISOLATED = 2; // ulp bracket without pole-free isolation
-constexpr int kMaxIters = 160;
 
 struct SolveSmem {
   double dob[32], delta[32], lo[32], hi[32], xlast[32], sig_last[32], gp_last[32], step_prev[32];
@@ -44,6 +43,8 @@ struct SolveArgs {
   double* scratch;  // gridDim.x * 32 * KP * KP
   int m_neg, p_pos;
   double lo_clip, hi_clip;
+  double step_tol;
+  int max_iters;
 };
 
 template <int KP>
@@ -111,7 +112,7 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
     const double cur = s.delta[b], lo = s.lo[b], hi = s.hi[b];
     double alt = nextafter(cur, hi);
     if (!(alt < hi)) alt = nextafter(cur, lo);
-    if (!(alt > lo && alt < hi) || s.iters[b] > kMaxIters) {
+    if (!(alt > lo && alt < hi) || s.iters[b] > a.max_iters) {
       if (s.phase[b] == 0) slot_finish_unisolated<KP>(s, y, b, a);
       else slot_finish<KP>(s, y, b, a, s.o[b], cur, s.dob[b] + cur, FLAG_UNISOLATED);
       return;
@@ -133,11 +134,17 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
   const int neg = bk_factor(F, KP, KP, piv, &zero);
   double z[KP];
   for (int c = 0; c < KP; ++c) z[c] = y[b * KP + c];
-  bk_solve(F, KP, KP, piv, z, 1e-290);
+  // an exactly zero pivot (x is a root to working precision) is replaced by a
+  // tiny multiple of the pivot scale, so inverse iteration still returns the
+  // null vector instead of overflowing
+  double pscale = 0.0;
+  for (int c = 0; c < KP; ++c) pscale = fmax(pscale, fabs(F[c * KP + c]));
+  const double tiny = 1e-4 * DBL_EPSILON * fmax(pscale, 1e-300);
+  bk_solve(F, KP, KP, piv, z, tiny);
   double zz = 0.0, zy = 0.0;
   for (int c = 0; c < KP; ++c) zz += z[c] * z[c], zy += z[c] * y[b * KP + c];
   double sigma = 0.0;
-  if (zz > 0.0 && zz < 1e300 && isfinite(zz)) {
+  if (zz > 0.0 && isfinite(zz)) {
     sigma = zy / zz;
     const double inv = rsqrt(zz);
     for (int c = 0; c < KP; ++c) y[b * KP + c] = z[c] * inv;
@@ -175,7 +182,7 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
       return;
     }
     const double xm = 0.5 * (lo + hi);
-    if (!(xm > lo && xm < hi) || s.iters[b] > kMaxIters) {
+    if (!(xm > lo && xm < hi) || s.iters[b] > a.max_iters) {
       slot_finish_unisolated<KP>(s, y, b, a);
       return;
     }
@@ -190,8 +197,19 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
   const double step = (gp > 0.0) ? -sigma / gp : NAN;
   const double w = hi - lo;
   const double tol = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi));
-  if ((fabs(step) <= 2.0 * DBL_EPSILON * fabs(dl)) || w <= tol || zero ||
-      s.iters[b] > kMaxIters) {
+  if ((fabs(step) <= a.step_tol * DBL_EPSILON * fabs(dl)) || w <= tol || zero ||
+      s.iters[b] > a.max_iters) {
+    // two more inverse-iteration steps on the same factorization: the
+    // eigenvector formula needs y to the accuracy of the root
+    for (int it = 0; it < 2; ++it) {
+      for (int c = 0; c < KP; ++c) z[c] = y[b * KP + c];
+      bk_solve(F, KP, KP, piv, z, tiny);
+      double z2 = 0.0;
+      for (int c = 0; c < KP; ++c) z2 += z[c] * z[c];
+      if (!(z2 > 0.0 && isfinite(z2))) break;
+      const double inv = rsqrt(z2);
+      for (int c = 0; c < KP; ++c) y[b * KP + c] = z[c] * inv;
+    }
     slot_finish<KP>(s, y, b, a, s.o[b], dl, s.dob[b] + dl, 0);
     return;
   }
@@ -316,7 +334,7 @@ size_t weights_smem_bytes() {
 
 template <int KP>
 void launch_solve(const ReducedView& rp, int64_t j0, int64_t j1, const RootRecords& out,
-                  DeviceScratch& ws, int sms, cudaStream_t st) {
+                  const SolveOptions& opt, DeviceScratch& ws, int sms, cudaStream_t st) {
   SolveArgs<KP> a;
   a.rp = rp;
   a.j_end = j1;
@@ -325,6 +343,8 @@ void launch_solve(const ReducedView& rp, int64_t j0, int64_t j1, const RootRecor
   a.p_pos = rp.k - rp.m_neg;
   a.lo_clip = rp.lo_clip;
   a.hi_clip = rp.hi_clip;
+  a.step_tol = opt.step_tol;
+  a.max_iters = opt.max_iters;
   const int64_t nroots = j1 - j0;
   const int grid = (int)std::min<int64_t>(sms, cdiv(nroots, 32));
   a.scratch = ws.get_f64("solve_scratch", (size_t)grid * 32 * KP * KP);
@@ -355,15 +375,15 @@ void launch_weights(const double* rep, const double* u, int64_t n, const int64_t
 }  // namespace
 
 void solve_roots(const ReducedView& rp, int64_t j0, int64_t j1, const RootRecords& out,
-                 DeviceScratch& ws, int sms, cudaStream_t st) {
+                 const SolveOptions& opt, DeviceScratch& ws, int sms, cudaStream_t st) {
   if (j1 <= j0) return;
   switch (rp.kp) {
-    case 1: launch_solve<1>(rp, j0, j1, out, ws, sms, st); break;
-    case 2: launch_solve<2>(rp, j0, j1, out, ws, sms, st); break;
-    case 4: launch_solve<4>(rp, j0, j1, out, ws, sms, st); break;
-    case 8: launch_solve<8>(rp, j0, j1, out, ws, sms, st); break;
-    case 16: launch_solve<16>(rp, j0, j1, out, ws, sms, st); break;
-    case 32: launch_solve<32>(rp, j0, j1, out, ws, sms, st); break;
+    case 1: launch_solve<1>(rp, j0, j1, out, opt, ws, sms, st); break;
+    case 2: launch_solve<2>(rp, j0, j1, out, opt, ws, sms, st); break;
+    case 4: launch_solve<4>(rp, j0, j1, out, opt, ws, sms, st); break;
+    case 8: launch_solve<8>(rp, j0, j1, out, opt, ws, sms, st); break;
+    case 16: launch_solve<16>(rp, j0, j1, out, opt, ws, sms, st); break;
+    case 32: launch_solve<32>(rp, j0, j1, out, opt, ws, sms, st); break;
     default: throw Error(1, "", "solve_roots: unsupported padded rank");
   }
 }

@@ -70,8 +70,16 @@ struct RootRecords {
   double* y;       // [n][kp] unit null vector of S(root)
 };
 
+// Phase-B stopping rule: the evaluated point is accepted once the Newton
+// correction is below step_tol * eps * |delta| (or the certified bracket is
+// within 2 ulps); max_iters caps the evaluations of one root.
+struct SolveOptions {
+  double step_tol = 0.5;
+  int max_iters = 160;
+};
+
 void solve_roots(const ReducedView& rp, int64_t j0, int64_t j1, const RootRecords& out,
-                 DeviceScratch& ws, int sms, cudaStream_t st);
+                 const SolveOptions& opt, DeviceScratch& ws, int sms, cudaStream_t st);
 
 void group_weights(int kp, const double* rep, const double* u, int64_t n, const int64_t* gstart,
                    const int64_t* glen, const double* gval, int64_t ng, const int* sgn, int k,
