@@ -200,7 +200,8 @@ void solve(eigmod_b200_ctx* c, int64_t j0, int64_t j1) {
   if (!c->have_plan) throw Error(1, "", "solve: no plan (call plan first)");
   c->recs = alloc_records(c);
   if (c->plan.nred == 0) return;
-  eigb::solve_roots(c->plan.view(), j0, j1, c->recs, c->sopt, c->ws, c->sms, c->stream);
+  eigb::solve_roots(c->plan.view(), c->plan.alpha_red_ok ? c->plan.alpha_red : nullptr, j0, j1,
+                    c->recs, c->sopt, c->ws, c->sms, c->stream);
 }
 
 __global__ void copy_block_kernel(const double* __restrict__ a, int64_t n, int64_t c0, int64_t nc,
@@ -326,6 +327,10 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
       ctx->sopt.step_tol = value;
     } else if (std::string(key) == "max_iters") {
       ctx->sopt.max_iters = (int)value;
+    } else if (std::string(key) == "sweep") {
+      ctx->sopt.sweep = value != 0.0;
+    } else if (std::string(key) == "fnewton") {
+      ctx->sopt.fnewton = value != 0.0;
     } else if (std::string(key) == "timing") {
       ctx->timing = value != 0.0;
     } else {
@@ -618,7 +623,8 @@ int eigmod_b200_solve_device(eigmod_b200_ctx* ctx, int64_t j0, int64_t j1, doubl
     if (!ctx->have_plan) throw Error(1, "", "solve: no plan");
     if (j0 < 0 || j1 > ctx->plan.nred || j1 < j0) throw Error(1, "", "solve: bad root range");
     if (ctx->plan.nred == 0) return;
-    eigb::solve_roots(ctx->plan.view(), j0, j1, ctx->recs, ctx->sopt, ctx->ws, ctx->sms, ctx->stream);
+    eigb::solve_roots(ctx->plan.view(), ctx->plan.alpha_red_ok ? ctx->plan.alpha_red : nullptr, j0,
+                      j1, ctx->recs, ctx->sopt, ctx->ws, ctx->sms, ctx->stream);
     if (d_rec_out && j1 > j0) {
       pack_records_kernel<<<(unsigned)eigb::cdiv(j1 - j0, 128), 128, 0, ctx->stream>>>(
           ctx->recs, j0, j1 - j0, ctx->plan.kp, d_rec_out);

@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(kPlanThreads) assemble_reduced_kernel(
     const int64_t* __restrict__ rank, const int64_t* __restrict__ roff,
     const double* __restrict__ rbuf, int64_t* counts, int64_t* __restrict__ tmp_a,
     int64_t* __restrict__ tmp_b, int64_t* __restrict__ off_red, int64_t* __restrict__ off_dec,
+    const double* __restrict__ alpha, double* __restrict__ alpha_red,
     double* __restrict__ d, double* __restrict__ ur, int64_t* __restrict__ red_src,
     double* __restrict__ dec_val, int64_t* __restrict__ dec_src, int64_t* __restrict__ orig_map) {
   __shared__ int64_t sh[kPlanThreads];
@@ -379,6 +380,7 @@ __global__ void __launch_bounds__(kPlanThreads) assemble_reduced_kernel(
       }
     } else if (m == 1) {
       d[pr] = lam[s0];
+      alpha_red[pr] = alpha[g];
       for (int c = 0; c < kp; ++c) ur[pr * kp + c] = u[s0 * kp + c];
       red_src[pr] = s0;
       orig_map[s0] = pr;
@@ -387,6 +389,7 @@ __global__ void __launch_bounds__(kPlanThreads) assemble_reduced_kernel(
       const double* B = rbuf + roff[g];
       for (int64_t t = 0; t < r; ++t) {
         d[pr + t] = gval[g];
+        alpha_red[pr + t] = 0.0;  // not a simple pole: f-Newton is disabled
         for (int c = 0; c < kp; ++c) ur[(pr + t) * kp + c] = B[t * kp + c];
         red_src[pr + t] = -(g * 65536 + t) - 2;  // rotated row t of group g
       }
@@ -511,6 +514,7 @@ void build_plan_dev(Plan& p, const double* lam, int64_t n, double run_rel, Devic
     EIGB_CUDA(cudaMemsetAsync(p.rank, 0, 8 * ng, st));
   }
   p.d = ws.get_f64("pl_d", n);
+  p.alpha_red = ws.get_f64("pl_alpha_red", n);
   p.ur = ws.get_f64("pl_ur", (size_t)n * kp);
   p.red_src = ws.get_i64("pl_red_src", n);
   p.dec_val = ws.get_f64("pl_dec_val", n);
@@ -522,13 +526,25 @@ void build_plan_dev(Plan& p, const double* lam, int64_t n, double run_rel, Devic
   p.off_dec = ws.get_i64("pl_off_dec", ng);
   assemble_reduced_kernel<<<1, kPlanThreads, 0, st>>>(
       lam, p.u, n, kp, p.gstart, p.glen, p.gval, p.kind, p.rank, p.roff, p.rbuf, p.counts, ta, tb,
-      p.off_red, p.off_dec, p.d, p.ur, p.red_src, p.dec_val, p.dec_src, p.orig_map);
+      p.off_red, p.off_dec, p.alpha, p.alpha_red, p.d, p.ur, p.red_src, p.dec_val, p.dec_src,
+      p.orig_map);
   EIGB_LAUNCH_CHECK();
   int64_t cnt[3];
   EIGB_CUDA(cudaMemcpyAsync(cnt, p.counts, 24, cudaMemcpyDeviceToHost, st));
   EIGB_CUDA(cudaStreamSynchronize(st));
   p.nred = cnt[1];
   p.ndec = cnt[2];
+  {  // rows of compressed runs are not simple poles of f
+    std::vector<int64_t> rk(ng), gl2(ng);
+    std::vector<int> kd(ng);
+    EIGB_CUDA(cudaMemcpyAsync(rk.data(), p.rank, 8 * ng, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaMemcpyAsync(kd.data(), p.kind, 4 * ng, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaStreamSynchronize(st));
+    bool ok = true;
+    for (int64_t g = 0; g < ng && ok; ++g)
+      if (glen_h[g] > 1 && kd[g] != 1 && rk[g] > 0) ok = false;
+    p.alpha_red_ok = ok;
+  }
   if (p.nred + p.ndec != n) throw Error(2, "merge", "reduced problem does not account for n pairs");
   clips_kernel<<<1, kPlanThreads, 0, st>>>(p.d, p.ur, p.nred, kp, k, p.sgn, p.scal);
   EIGB_LAUNCH_CHECK();

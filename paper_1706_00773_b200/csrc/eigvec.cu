@@ -96,9 +96,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) collision_kernel(
     double gap, double* __restrict__ colldir, int* __restrict__ collok, double* __restrict__ scratch) {
   using C = PassCfg<KP>;
   extern __shared__ __align__(16) double smem[];
-  double* tiles = smem;
-  double* red = tiles + 2 * C::TILE_DOUBLES;
-  __shared__ double dob[32], delta[32], yy[32 * KP];
+  __shared__ double dob[32], delta[32];
   __shared__ int active[32], hit[32];
   const int t = threadIdx.x;
   const int64_t b0 = (int64_t)blockIdx.x * 32;
@@ -110,8 +108,12 @@ __global__ void __launch_bounds__(kPassThreads, 1) collision_kernel(
     hit[t] = 0;
   }
   __syncthreads();
-  PassSlots sl{dob, delta, yy, active, hit};
-  secular_pass<KP>(rp.d, rp.u, rp.n, sl, false, true, gap, tiles, red);
+  PassSlots sl{dob, delta, nullptr, active, hit};
+  PassOpts o;
+  o.exclude_zero = true;
+  o.excl_gap = gap;
+  secular_pass<KP>(rp.d, rp.u, rp.n, sl, o, smem);
+  const double* red = pass_result<KP>(smem);
   if (t < 32 && active[t]) {
     const int64_t j = list[b0 + t];
     const int64_t idx = origin[j];
@@ -119,7 +121,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) collision_kernel(
     double* B = scratch + ((size_t)blockIdx.x * 32 + t) * 3 * (KP + 1) * (KP + 1);
     double* BtB = B + K1 * K1;
     double* V = BtB + K1 * K1;
-    const double* rb = red + t * (C::P + 1);
+    const double* rb = red + t * C::OUT;
     for (int r = 0; r < K1 * K1; ++r) B[r] = 0.0;
     for (int r = 0; r < k; ++r)
       for (int c = 0; c < k; ++c) {
@@ -272,7 +274,7 @@ void launch_collisions(const Plan& p, const RootRecords& roots, const int64_t* l
   using C = PassCfg<KP>;
   const int grid = (int)cdiv(cnt, 32);
   double* scratch = ws.get_f64("coll_scratch", (size_t)grid * 32 * 3 * (KP + 1) * (KP + 1));
-  const size_t sm = sizeof(double) * (2 * C::TILE_DOUBLES + C::RED_DOUBLES);
+  const size_t sm = sizeof(double) * C::SMEM_DOUBLES;
   EIGB_CUDA(cudaFuncSetAttribute(collision_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sm));
   collision_kernel<KP><<<grid, kPassThreads, sm, st>>>(p.view(), list, cnt, roots.origin,

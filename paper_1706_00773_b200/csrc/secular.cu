@@ -1,22 +1,28 @@
-// K2 deflation weights and K3 batched per-root solver (sm_100a).
+// K2 deflation weights, the count sweep and K3 batched per-root solver (sm_100a).
 //
 // K2 (proj/src/secular.cpp:168-202 group_weights): one pole pass per batch of
 //   32 pole groups evaluated at their representatives, then per group the
 //   reference's adjugate route (cofactors k <= 3, LU det*inverse, cofactor
 //   expansion fallback) on M_g = J S_g, alpha_g = sum_s w_s^T adj(M_g) J w_s.
-// K3 (replaces locate.cpp / sturm.cpp / rootfind.cpp:89-229, 342-377): a
-//   persistent kernel whose CTAs own 32 root slots each. Every iteration one
-//   pole pass evaluates S(x_b) = J + U^T (D - x_b)^-1 U for all slots; a
-//   Bunch-Kaufman LDL^T gives the inertia, hence the exact eigenvalue count
-//   #eig < x_b = #{d_i < x_b} + m - nu(S(x_b)), and one
-//   inverse-iteration step gives the eigenvalue sigma of S nearest zero with
-//   its vector y. Phase A bisects the count inside the Weyl window
-//   [d_{j-m}, d_{j+p}] (proj/src/locate.cpp:159-171) until root j is alone in
-//   a pole-free bracket; phase B runs Newton on sigma (sigma' = y^T S' y from
-//   the same pass) in the shifted origin x = d_o + delta, safeguarded by the
-//   count-certified bracket, to ~1 ulp of delta. A converged slot writes its
-//   root record (value, origin, delta, y) and takes the next root index from
-//   a global counter, so the batch stays full until the queue drains.
+//
+// Count sweep (replaces the location stage, proj/src/locate.cpp:65-252 and
+//   sturm.cpp): the exact eigenvalue count #eig < x = #{d_i < x} + m -
+//   nu(S(x)) (nu from a Bunch-Kaufman LDL^T of S) at the two
+//   points d_a -/+ theta * gap next to every pole. Between consecutive points
+//   the counts bracket every root; a bracket that holds one root and no pole
+//   is "isolated". Two S evaluations per root locate all n roots at once.
+//
+// K3 (replaces rootfind.cpp:89-229, 342-377): a persistent kernel whose CTAs
+//   own 32 root slots. Each slot starts from its sweep bracket; phase A
+//   bisects the count until the root is isolated, phase B works in the
+//   shifted origin x = d_o + delta (d_o the pole nearest the iterate) with a
+//   Newton step on g = -delta f(x) (f the scalar secular function with the K2
+//   residues; a pole of f at d_o becomes a line) until |step| < 1e-6 |delta|,
+//   then Newton on psi = -delta sigma (sigma the eigenvalue of S nearest zero,
+//   from inverse iteration; sigma' = y^T S' y from the same pass) to a few ulps
+//   of delta. Every step is confined to the count-certified bracket. A
+//   converged slot writes its root record (value, origin, delta, y) and takes
+//   the next root index from a global counter.
 #include "secular.cuh"
 
 #include <cfloat>
@@ -27,56 +33,197 @@ namespace {
 
 constexpr int FLAG_COLLIDED = 1;   // bracket collapsed onto a pole
 constexpr int FLAG_UNISOLATED = 2; // ulp bracket without pole-free isolation
+constexpr double kSweepTheta = 1e-3;
+constexpr double kFSwitchRel = 1e-6;  // f-Newton -> sigma-Newton
 
+// Sweep points: 2a -> d_a - theta*gap_left, 2a+1 -> d_a + theta*gap_right,
+// gaps to the nearest distinct neighbours (1 at the ends).
+__device__ __forceinline__ double sweep_point(const double* d, int64_t N, int64_t q) {
+  const int64_t a = q >> 1;
+  const double da = d[a];
+  if (q & 1) {
+    int64_t b = a + 1;
+    while (b < N && d[b] == da) ++b;
+    const double g = (b < N) ? d[b] - da : 1.0;
+    return da + kSweepTheta * g;
+  }
+  int64_t b = a - 1;
+  while (b >= 0 && d[b] == da) --b;
+  const double g = (b >= 0) ? da - d[b] : 1.0;
+  return da - kSweepTheta * g;
+}
+
+template <int KP>
+__device__ __forceinline__ void load_S(const double* rb, const int* sgn, int k, double* F, int es) {
+  using C = PassCfg<KP>;
+  for (int r = 0; r < KP; ++r)
+    for (int c = r; c < KP; ++c) {
+      double v = rb[C::pidx(r, c)];
+      if (r == c) v += (r < k) ? (double)sgn[r] : 1.0;
+      F[(r * KP + c) * es] = v;
+      F[(c * KP + r) * es] = v;
+    }
+}
+
+// ------------------------------------------------------------ sweep kernel
+template <int KP>
+__global__ void __launch_bounds__(kPassThreads, 1) count_sweep_kernel(ReducedView rp,
+                                                                      int* __restrict__ counts) {
+  using C = PassCfg<KP>;
+  extern __shared__ __align__(16) double smem[];
+  double* F = smem + C::SMEM_DOUBLES;  // interleaved [KP*KP][32]
+  __shared__ double dob[32], delta[32];
+  __shared__ int active[32], hit[32];
+  const int t = threadIdx.x;
+  const int64_t Q = 2 * rp.n;
+  const int64_t q0 = (int64_t)blockIdx.x * 32;
+  if (t < 32) {
+    const int64_t q = q0 + t;
+    active[t] = q < Q;
+    dob[t] = 0.0;
+    delta[t] = (q < Q) ? sweep_point(rp.d, rp.n, q) : 0.0;
+    hit[t] = 0;
+  }
+  __syncthreads();
+  PassSlots sl{dob, delta, nullptr, active, hit};
+  PassOpts o;
+  secular_pass<KP>(rp.d, rp.u, rp.n, sl, o, smem);
+  if (t < 32 && active[t]) {
+    const double* rb = pass_result<KP>(smem) + t * C::OUT;
+    load_S<KP>(rb, rp.sgn, rp.k, F + t, 32);
+    int piv[KP], zero;
+    const int neg = bk_factor(F + t, KP, KP, piv, &zero, 32);
+    const double x = delta[t];
+    // a hit (x on a pole, duplicates) gives an unusable point: -1
+    counts[q0 + t] = hit[t] ? -1 : (int)(dev_n_less(rp.d, rp.n, x) + rp.m_neg - neg);
+  }
+}
+
+// ------------------------------------------------------------ solver
 struct SolveSmem {
-  double dob[32], delta[32], lo[32], hi[32], xlast[32], sig_last[32], gp_last[32], step_prev[32];
+  double dob[32], delta[32], lo[32], hi[32], step_prev[32];
   int64_t j[32], o[32], below[32];
-  int active[32], hit[32], phase[32], lo_ok[32], hi_ok[32], iters[32];
+  int active[32], hit[32], phase[32], lo_ok[32], hi_ok[32], iters[32], itersA[32], fmode[32];
 };
 
 template <int KP>
 struct SolveArgs {
   ReducedView rp;
+  const double* alpha;     // residues of the reduced poles (nullptr: no f-Newton)
+  const int* counts;       // sweep counts [2N] (-1 = unusable point)
   int64_t j_end;
   unsigned long long* next_root;
   RootRecords out;
-  double* scratch;  // gridDim.x * 32 * KP * KP
   int m_neg, p_pos;
   double lo_clip, hi_clip;
   double step_tol;
   int max_iters;
 };
 
+// Sweep bracket of root j: the last usable sweep point with count <= j and
+// the first with count > j (outer clips count 0 and N).
 template <int KP>
-__device__ void slot_init(SolveSmem& s, double* y, int b, int64_t j, const SolveArgs<KP>& a) {
-  const int64_t N = a.rp.n;
-  s.j[b] = j;
-  s.lo[b] = (j - a.m_neg >= 0) ? a.rp.d[j - a.m_neg] : a.lo_clip;
-  s.hi[b] = (j + a.p_pos <= N - 1) ? a.rp.d[j + a.p_pos] : a.hi_clip;
-  s.lo_ok[b] = s.hi_ok[b] = 0;
-  s.phase[b] = 0;
-  s.iters[b] = 0;
-  s.hit[b] = 0;
-  s.step_prev[b] = 0.0;
-  s.dob[b] = 0.0;
-  s.delta[b] = 0.5 * (s.lo[b] + s.hi[b]);
-  s.active[b] = 1;
-  const double y0 = rsqrt((double)a.rp.k);
-  for (int c = 0; c < KP; ++c) y[b * KP + c] = (c < a.rp.k) ? y0 : 0.0;
+__device__ void sweep_bracket(const SolveArgs<KP>& a, int64_t j, double* lo, double* hi,
+                              int* lo_ok, int* hi_ok) {
+  const int64_t Q = 2 * a.rp.n;
+  int64_t L = 0, R = Q;  // first q with counts[q] > j (skipping -1 entries linearly)
+  while (L < R) {
+    const int64_t mid = (L + R) >> 1;
+    int64_t q = mid;
+    while (q < R && a.counts[q] < 0) ++q;
+    if (q == R) { R = mid; continue; }
+    if (a.counts[q] > j) R = mid; else L = q + 1;
+  }
+  // hi point: first usable q >= L
+  int64_t qh = L;
+  while (qh < Q && a.counts[qh] < 0) ++qh;
+  int64_t ql = L - 1;
+  while (ql >= 0 && a.counts[ql] < 0) --ql;
+  if (ql >= 0) {
+    *lo = sweep_point(a.rp.d, a.rp.n, ql);
+    *lo_ok = (a.counts[ql] == j);
+  } else {
+    *lo = a.lo_clip;
+    *lo_ok = (j == 0);
+  }
+  if (qh < Q) {
+    *hi = sweep_point(a.rp.d, a.rp.n, qh);
+    *hi_ok = (a.counts[qh] == j + 1);
+  } else {
+    *hi = a.hi_clip;
+    *hi_ok = (j + 1 == a.rp.n);
+  }
 }
 
 template <int KP>
-__device__ void slot_finish(SolveSmem& s, double* y, int b, const SolveArgs<KP>& a, int64_t o,
-                            double delta, double value, int flags) {
+__device__ void enter_phase_b(SolveSmem& s, int b, const SolveArgs<KP>& a, double xstart) {
+  const double* d = a.rp.d;
+  const int64_t N = a.rp.n;
+  const double lo = s.lo[b], hi = s.hi[b];
+  const int64_t pa = dev_n_leq(d, N, lo) - 1, pb = pa + 1;
+  int64_t o;
+  if (pa < 0) o = pb;
+  else if (pb >= N) o = pa;
+  else o = (xstart - d[pa] <= d[pb] - xstart) ? pa : pb;
+  const double dob = d[o];
+  s.o[b] = o;
+  s.below[b] = pa + 1;
+  s.dob[b] = dob;
+  s.lo[b] = lo - dob;
+  s.hi[b] = hi - dob;
+  s.phase[b] = 1;
+  s.itersA[b] = s.iters[b];
+  s.fmode[b] = (a.alpha != nullptr);
+  s.step_prev[b] = s.hi[b] - s.lo[b];
+  s.delta[b] = xstart - dob;
+}
+
+template <int KP>
+__device__ void slot_init(SolveSmem& s, double* y, int b, int64_t j, const SolveArgs<KP>& a) {
+  const double* d = a.rp.d;
+  const int64_t N = a.rp.n;
+  s.j[b] = j;
+  s.iters[b] = 0;
+  s.itersA[b] = 0;
+  s.hit[b] = 0;
+  s.phase[b] = 0;
+  s.active[b] = 1;
+  s.dob[b] = 0.0;
+  const double y0 = rsqrt((double)a.rp.k);
+  for (int c = 0; c < KP; ++c) y[b * KP + c] = (c < a.rp.k) ? y0 : 0.0;
+  double lo, hi;
+  int lok, hok;
+  if (a.counts) {
+    sweep_bracket<KP>(a, j, &lo, &hi, &lok, &hok);
+  } else {  // Weyl window (proj/src/locate.cpp:159-171)
+    lo = (j - a.m_neg >= 0) ? d[j - a.m_neg] : a.lo_clip;
+    hi = (j + a.p_pos <= N - 1) ? d[j + a.p_pos] : a.hi_clip;
+    lok = hok = 0;
+  }
+  s.lo[b] = lo;
+  s.hi[b] = hi;
+  s.lo_ok[b] = lok;
+  s.hi_ok[b] = hok;
+  if (lok && hok && dev_n_less(d, N, hi) == dev_n_leq(d, N, lo)) {
+    enter_phase_b<KP>(s, b, a, 0.5 * (lo + hi));
+  } else {
+    s.delta[b] = 0.5 * (lo + hi);
+  }
+}
+
+template <int KP>
+__device__ void slot_finish(SolveSmem& s, const double* y, int b, const SolveArgs<KP>& a,
+                            int64_t o, double delta, double value, int flags, double* ynext) {
   const int64_t j = s.j[b];
   a.out.value[j] = value;
   a.out.origin[j] = o;
   a.out.delta[j] = delta;
-  a.out.flags[j] = flags;
+  const int ia = s.phase[b] ? (s.itersA[b] < 255 ? s.itersA[b] : 255) : 255;
+  a.out.flags[j] = flags | (ia << 8);
   a.out.evals[j] = s.iters[b];
-  for (int c = 0; c < KP; ++c) a.out.y[j * KP + c] = y[b * KP + c];
+  for (int c = 0; c < KP; ++c) a.out.y[j * KP + c] = y[c];
   const unsigned long long nj = atomicAdd(a.next_root, 1ull);
-  if ((int64_t)nj < a.j_end) slot_init<KP>(s, y, b, (int64_t)nj, a);
+  if ((int64_t)nj < a.j_end) slot_init<KP>(s, ynext, b, (int64_t)nj, a);
   else s.active[b] = 0;
 }
 
@@ -87,21 +234,23 @@ __device__ void slot_finish_unisolated(SolveSmem& s, double* y, int b, const Sol
   const double* d = a.rp.d;
   const int64_t N = a.rp.n;
   const double lo = s.lo[b], hi = s.hi[b], mid = 0.5 * (lo + hi);
+  double yc[KP];
+  for (int c = 0; c < KP; ++c) yc[c] = y[b * KP + c];
   int64_t p = dev_n_less(d, N, lo);
   if (p < N && d[p] <= hi) {
     int64_t o = p;
     for (int64_t q = p + 1; q < N && d[q] <= hi; ++q)
       if (fabs(d[q] - mid) < fabs(d[o] - mid)) o = q;
-    slot_finish<KP>(s, y, b, a, o, 0.0, d[o], FLAG_COLLIDED);
+    slot_finish<KP>(s, yc, b, a, o, 0.0, d[o], FLAG_COLLIDED, y);
     return;
   }
   int64_t o = p < N ? p : N - 1;
   if (o > 0 && fabs(d[o - 1] - mid) < fabs(d[o] - mid)) o -= 1;
-  slot_finish<KP>(s, y, b, a, o, mid - d[o], mid, FLAG_UNISOLATED);
+  slot_finish<KP>(s, yc, b, a, o, mid - d[o], mid, FLAG_UNISOLATED, y);
 }
 
 template <int KP>
-__device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, double* F, int* piv,
+__device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, double* F, int es,
                           const SolveArgs<KP>& a) {
   using C = PassCfg<KP>;
   const double* d = a.rp.d;
@@ -113,72 +262,53 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
     double alt = nextafter(cur, hi);
     if (!(alt < hi)) alt = nextafter(cur, lo);
     if (!(alt > lo && alt < hi) || s.iters[b] > a.max_iters) {
-      if (s.phase[b] == 0) slot_finish_unisolated<KP>(s, y, b, a);
-      else slot_finish<KP>(s, y, b, a, s.o[b], cur, s.dob[b] + cur, FLAG_UNISOLATED);
+      if (s.phase[b] == 0) {
+        slot_finish_unisolated<KP>(s, y, b, a);
+      } else {
+        double yc[KP];
+        for (int c = 0; c < KP; ++c) yc[c] = y[b * KP + c];
+        slot_finish<KP>(s, yc, b, a, s.o[b], cur, s.dob[b] + cur, FLAG_UNISOLATED, y);
+      }
       return;
     }
     s.delta[b] = alt;
     return;
   }
-  // S = J + packed sum, full storage in F (ld KP)
-  const double* rb = red + b * (C::P + 1);
-  for (int r = 0; r < KP; ++r)
-    for (int c = r; c < KP; ++c) {
-      double v = rb[C::pidx(r, c)];
-      if (r == c) v += (r < a.rp.k) ? (double)a.rp.sgn[r] : 1.0;
-      F[r * KP + c] = v;
-      F[c * KP + r] = v;
-    }
-  const double gp = rb[C::P];
-  int zero = 0;
-  const int neg = bk_factor(F, KP, KP, piv, &zero);
-  double z[KP];
-  for (int c = 0; c < KP; ++c) z[c] = y[b * KP + c];
-  // an exactly zero pivot (x is a root to working precision) is replaced by a
-  // tiny multiple of the pivot scale, so inverse iteration still returns the
-  // null vector instead of overflowing
+  const double* rb = red + b * C::OUT;
+  load_S<KP>(rb, a.rp.sgn, a.rp.k, F, es);
+  const double gp = rb[C::IG];
+  const double fv = 1.0 + rb[C::IF], fpv = rb[C::IFP];
+  int piv[KP], zero = 0;
+  const int neg = bk_factor(F, KP, KP, piv, &zero, es);
   double pscale = 0.0;
-  for (int c = 0; c < KP; ++c) pscale = fmax(pscale, fabs(F[c * KP + c]));
+  for (int c = 0; c < KP; ++c) pscale = fmax(pscale, fabs(F[(c * KP + c) * es]));
+  // an exactly zero pivot (x is a root to working precision) is replaced by a
+  // tiny multiple of the pivot scale: inverse iteration then still returns
+  // the null vector instead of overflowing
   const double tiny = 1e-4 * DBL_EPSILON * fmax(pscale, 1e-300);
-  bk_solve(F, KP, KP, piv, z, tiny);
+  double yv[KP], z[KP];
+  for (int c = 0; c < KP; ++c) yv[c] = y[b * KP + c];
+  for (int c = 0; c < KP; ++c) z[c] = yv[c];
+  bk_solve(F, KP, KP, piv, z, tiny, es);
   double zz = 0.0, zy = 0.0;
-  for (int c = 0; c < KP; ++c) zz += z[c] * z[c], zy += z[c] * y[b * KP + c];
+  for (int c = 0; c < KP; ++c) zz += z[c] * z[c], zy += z[c] * yv[c];
   double sigma = 0.0;
   if (zz > 0.0 && isfinite(zz)) {
-    sigma = zy / zz;
+    sigma = zy / zz;  // Rayleigh quotient of S at z
     const double inv = rsqrt(zz);
-    for (int c = 0; c < KP; ++c) y[b * KP + c] = z[c] * inv;
+    for (int c = 0; c < KP; ++c) yv[c] = z[c] * inv;
   }
+  for (int c = 0; c < KP; ++c) y[b * KP + c] = yv[c];
   const int64_t j = s.j[b];
 
   if (s.phase[b] == 0) {
     const double x = s.delta[b];
-    const int64_t below = dev_n_less(d, N, x);
-    const int64_t cnt = below + a.m_neg - neg;
+    const int64_t cnt = dev_n_less(d, N, x) + a.m_neg - neg;
     if (cnt >= j + 1) { s.hi[b] = x; s.hi_ok[b] = (cnt == j + 1); }
     else { s.lo[b] = x; s.lo_ok[b] = (cnt == j); }
     const double lo = s.lo[b], hi = s.hi[b];
     if (s.lo_ok[b] && s.hi_ok[b] && dev_n_less(d, N, hi) == dev_n_leq(d, N, lo)) {
-      // isolated: shifted origin at the nearer bracketing pole
-      const int64_t pa = dev_n_leq(d, N, lo) - 1, pb = pa + 1;
-      const double mid = 0.5 * (lo + hi);
-      int64_t o;
-      if (pa < 0) o = pb;
-      else if (pb >= N) o = pa;
-      else o = (mid - d[pa] <= d[pb] - mid) ? pa : pb;
-      const double dob = d[o];
-      s.o[b] = o;
-      s.below[b] = pa + 1;
-      s.dob[b] = dob;
-      s.lo[b] = lo - dob;
-      s.hi[b] = hi - dob;
-      s.phase[b] = 1;
-      const double dl = x - dob;
-      const double step = (gp > 0.0) ? -sigma / gp : NAN;
-      double dn = dl + step;
-      if (!(dn > s.lo[b] && dn < s.hi[b])) dn = 0.5 * (s.lo[b] + s.hi[b]);
-      s.step_prev[b] = s.hi[b] - s.lo[b];
-      s.delta[b] = dn;
+      enter_phase_b<KP>(s, b, a, 0.5 * (lo + hi));
       return;
     }
     const double xm = 0.5 * (lo + hi);
@@ -189,59 +319,102 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
     s.delta[b] = xm;
     return;
   }
-  // phase B (delta domain)
+  // ---- phase B (delta domain)
   const double dl = s.delta[b];
   const int64_t cnt = s.below[b] + a.m_neg - neg;
   if (cnt >= j + 1) s.hi[b] = dl; else s.lo[b] = dl;
   const double lo = s.lo[b], hi = s.hi[b];
-  const double step = (gp > 0.0) ? -sigma / gp : NAN;
+  double step = NAN;
+  if (s.fmode[b]) {  // Newton on g = -delta f: g' = -f - delta f'
+    const double den = fv + dl * fpv;
+    step = (den != 0.0) ? -dl * fv / den : NAN;
+    if (!(fabs(step) > kFSwitchRel * fabs(dl))) s.fmode[b] = 0;  // f resolved: polish on S
+  }
+  if (!s.fmode[b]) {  // Newton on psi = -delta sigma: psi' = -sigma - delta sigma'
+    const double den = sigma + dl * gp;
+    step = (gp > 0.0 && den != 0.0) ? -dl * sigma / den : NAN;
+  }
   const double w = hi - lo;
   const double tol = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi));
-  if ((fabs(step) <= a.step_tol * DBL_EPSILON * fabs(dl)) || w <= tol || zero ||
-      s.iters[b] > a.max_iters) {
+  // converged: S-Newton correction below step_tol ulps, or stalled at the
+  // rounding floor of sigma (no longer shrinking while already tiny)
+  const bool sdone = !s.fmode[b] && ((fabs(step) <= a.step_tol * DBL_EPSILON * fabs(dl)) ||
+                                     (fabs(step) >= fabs(s.step_prev[b]) &&
+                                      fabs(step) <= 1e3 * DBL_EPSILON * fabs(dl)));
+  if (sdone || w <= tol || zero || s.iters[b] > a.max_iters) {
     // two more inverse-iteration steps on the same factorization: the
     // eigenvector formula needs y to the accuracy of the root
     for (int it = 0; it < 2; ++it) {
-      for (int c = 0; c < KP; ++c) z[c] = y[b * KP + c];
-      bk_solve(F, KP, KP, piv, z, tiny);
+      for (int c = 0; c < KP; ++c) z[c] = yv[c];
+      bk_solve(F, KP, KP, piv, z, tiny, es);
       double z2 = 0.0;
       for (int c = 0; c < KP; ++c) z2 += z[c] * z[c];
       if (!(z2 > 0.0 && isfinite(z2))) break;
       const double inv = rsqrt(z2);
-      for (int c = 0; c < KP; ++c) y[b * KP + c] = z[c] * inv;
+      for (int c = 0; c < KP; ++c) yv[c] = z[c] * inv;
     }
-    slot_finish<KP>(s, y, b, a, s.o[b], dl, s.dob[b] + dl, 0);
+    slot_finish<KP>(s, yv, b, a, s.o[b], dl, s.dob[b] + dl, 0, y);
     return;
   }
   double dn = dl + step;
-  if (!(dn > lo && dn < hi) || !(fabs(step) <= 0.5 * fabs(s.step_prev[b]))) {
+  // safeguard: bisect when the step leaves the certified bracket or stops
+  // shrinking
+  if (!(dn > lo && dn < hi) || !(fabs(step) < fabs(s.step_prev[b]))) {
     dn = 0.5 * (lo + hi);
     s.step_prev[b] = w;
   } else {
     s.step_prev[b] = step;
   }
+  // re-origin at the pole nearest the new iterate (keeps relative accuracy
+  // of delta when the root sits next to the far end of the interval)
+  const int64_t pa = s.below[b] - 1, pb = s.below[b];
+  if (pa >= 0 && pb < N) {
+    const double xn = s.dob[b] + dn;
+    const int64_t want = (xn - d[pa] <= d[pb] - xn) ? pa : pb;
+    if (want != s.o[b]) {
+      const double sh = s.dob[b] - d[want];
+      s.o[b] = want;
+      s.dob[b] = d[want];
+      s.lo[b] = lo + sh;
+      s.hi[b] = hi + sh;
+      dn = dn + sh;
+      if (!(dn > s.lo[b] && dn < s.hi[b])) dn = 0.5 * (s.lo[b] + s.hi[b]);
+    }
+  }
   s.delta[b] = dn;
 }
 
 template <int KP>
-__global__ void __launch_bounds__(kPassThreads, 1) solve_roots_kernel(SolveArgs<KP> a) {
+constexpr bool kFactorInSmem = (KP <= 16);
+
+template <int KP>
+__global__ void __launch_bounds__(kPassThreads, 1) solve_roots_kernel(SolveArgs<KP> a,
+                                                                      double* gscratch) {
   using C = PassCfg<KP>;
   extern __shared__ __align__(16) double smem[];
-  double* tiles = smem;
-  double* red = tiles + 2 * C::TILE_DOUBLES;
-  double* y = red + C::RED_DOUBLES;                       // [32][KP]
-  SolveSmem& s = *reinterpret_cast<SolveSmem*>(y + 32 * KP);
+  double* y = smem + C::SMEM_DOUBLES;                      // [32][KP]
+  double* Fs = y + 32 * KP;                                // [KP*KP][32] (KP <= 16)
+  SolveSmem& s = *reinterpret_cast<SolveSmem*>(Fs + (kFactorInSmem<KP> ? 32 * KP * KP : 0));
   __shared__ int any;
   const int t = threadIdx.x;
-  double* F = a.scratch + ((size_t)blockIdx.x * 32 + (t & 31)) * KP * KP;
-  int piv[KP];
-
+  double* F;
+  int es;
+  if constexpr (kFactorInSmem<KP>) {
+    F = Fs + (t & 31);
+    es = 32;
+  } else {
+    F = gscratch + ((size_t)blockIdx.x * 32 + (t & 31)) * KP * KP;
+    es = 1;
+  }
   if (t < 32) {
     const unsigned long long nj = atomicAdd(a.next_root, 1ull);
     if ((int64_t)nj < a.j_end) slot_init<KP>(s, y, t, (int64_t)nj, a);
     else s.active[t] = 0;
   }
   __syncthreads();
+  PassOpts o;
+  o.alpha = a.alpha;
+  o.want_sigma = true;
   for (;;) {
     if (t == 0) {
       int v = 0;
@@ -251,8 +424,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) solve_roots_kernel(SolveArgs<
     __syncthreads();
     if (!any) break;
     PassSlots sl{s.dob, s.delta, y, s.active, s.hit};
-    secular_pass<KP>(a.rp.d, a.rp.u, a.rp.n, sl, true, false, 0.0, tiles, red);
-    if (t < 32 && s.active[t]) slot_step<KP>(s, y, t, red, F, piv, a);
+    secular_pass<KP>(a.rp.d, a.rp.u, a.rp.n, sl, o, smem);
+    if (t < 32 && s.active[t]) slot_step<KP>(s, y, t, pass_result<KP>(smem), F, es, a);
     __syncthreads();
   }
 }
@@ -277,9 +450,7 @@ template <int KP>
 __global__ void __launch_bounds__(kPassThreads, 1) group_weights_kernel(WeightArgs<KP> a) {
   using C = PassCfg<KP>;
   extern __shared__ __align__(16) double smem[];
-  double* tiles = smem;
-  double* red = tiles + 2 * C::TILE_DOUBLES;
-  __shared__ double dob[32], delta[32], yy[32 * KP];
+  __shared__ double dob[32], delta[32];
   __shared__ int active[32], hit[32];
   const int t = threadIdx.x;
   const int64_t g0 = (int64_t)blockIdx.x * 32;
@@ -291,15 +462,17 @@ __global__ void __launch_bounds__(kPassThreads, 1) group_weights_kernel(WeightAr
     hit[t] = 0;
   }
   __syncthreads();
-  PassSlots sl{dob, delta, yy, active, hit};
-  secular_pass<KP>(a.rep, a.u, a.n, sl, false, true, 0.0, tiles, red);
+  PassSlots sl{dob, delta, nullptr, active, hit};
+  PassOpts o;
+  o.exclude_zero = true;
+  secular_pass<KP>(a.rep, a.u, a.n, sl, o, smem);
   if (t < 32 && active[t]) {
     const int64_t g = g0 + t;
     const int k = a.k;
     double* M = a.scratch + ((size_t)blockIdx.x * 32 + t) * 4 * KP * KP;
     double* adj = M + KP * KP;
     double* work = adj + KP * KP;
-    const double* rb = red + t * (C::P + 1);
+    const double* rb = pass_result<KP>(smem) + t * C::OUT;
     // M = I + J T (proj/src/secular.cpp:176-188): row r scaled by sign r.
     for (int r = 0; r < k; ++r)
       for (int c = 0; c < k; ++c) {
@@ -323,20 +496,28 @@ __global__ void __launch_bounds__(kPassThreads, 1) group_weights_kernel(WeightAr
 template <int KP>
 size_t solve_smem_bytes() {
   using C = PassCfg<KP>;
-  return sizeof(double) * (2 * C::TILE_DOUBLES + C::RED_DOUBLES + 32 * KP) + sizeof(SolveSmem);
+  return sizeof(double) * (C::SMEM_DOUBLES + 32 * KP + (kFactorInSmem<KP> ? 32 * KP * KP : 0)) +
+         sizeof(SolveSmem);
 }
 
 template <int KP>
-size_t weights_smem_bytes() {
+void launch_sweep(const ReducedView& rp, int* counts, cudaStream_t st) {
   using C = PassCfg<KP>;
-  return sizeof(double) * (2 * C::TILE_DOUBLES + C::RED_DOUBLES);
+  const size_t sm = sizeof(double) * (C::SMEM_DOUBLES + 32 * KP * KP);
+  EIGB_CUDA(cudaFuncSetAttribute(count_sweep_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm));
+  count_sweep_kernel<KP><<<(unsigned)cdiv(2 * rp.n, 32), kPassThreads, sm, st>>>(rp, counts);
+  EIGB_LAUNCH_CHECK();
 }
 
 template <int KP>
-void launch_solve(const ReducedView& rp, int64_t j0, int64_t j1, const RootRecords& out,
-                  const SolveOptions& opt, DeviceScratch& ws, int sms, cudaStream_t st) {
+void launch_solve(const ReducedView& rp, const double* alpha, const int* counts, int64_t j0,
+                  int64_t j1, const RootRecords& out, const SolveOptions& opt, DeviceScratch& ws,
+                  int sms, cudaStream_t st) {
   SolveArgs<KP> a;
   a.rp = rp;
+  a.alpha = alpha;
+  a.counts = counts;
   a.j_end = j1;
   a.out = out;
   a.m_neg = rp.m_neg;
@@ -347,14 +528,15 @@ void launch_solve(const ReducedView& rp, int64_t j0, int64_t j1, const RootRecor
   a.max_iters = opt.max_iters;
   const int64_t nroots = j1 - j0;
   const int grid = (int)std::min<int64_t>(sms, cdiv(nroots, 32));
-  a.scratch = ws.get_f64("solve_scratch", (size_t)grid * 32 * KP * KP);
+  double* gscratch = kFactorInSmem<KP> ? nullptr
+                                       : ws.get_f64("solve_scratch", (size_t)grid * 32 * KP * KP);
   a.next_root = reinterpret_cast<unsigned long long*>(ws.get_i64("solve_counter", 1));
   const unsigned long long start = (unsigned long long)j0;
   EIGB_CUDA(cudaMemcpyAsync(a.next_root, &start, sizeof(start), cudaMemcpyHostToDevice, st));
   const size_t sm = solve_smem_bytes<KP>();
   EIGB_CUDA(cudaFuncSetAttribute(solve_roots_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sm));
-  solve_roots_kernel<KP><<<grid, kPassThreads, sm, st>>>(a);
+  solve_roots_kernel<KP><<<grid, kPassThreads, sm, st>>>(a, gscratch);
   EIGB_LAUNCH_CHECK();
 }
 
@@ -362,10 +544,11 @@ template <int KP>
 void launch_weights(const double* rep, const double* u, int64_t n, const int64_t* gstart,
                     const int64_t* glen, const double* gval, int64_t ng, const int* sgn, int k,
                     double* alpha, DeviceScratch& ws, cudaStream_t st) {
+  using C = PassCfg<KP>;
   WeightArgs<KP> a{rep, u, n, gstart, glen, gval, ng, sgn, k, alpha, nullptr};
   const int grid = (int)cdiv(ng, 32);
   a.scratch = ws.get_f64("weights_scratch", (size_t)grid * 32 * 4 * KP * KP);
-  const size_t sm = weights_smem_bytes<KP>();
+  const size_t sm = sizeof(double) * C::SMEM_DOUBLES;
   EIGB_CUDA(cudaFuncSetAttribute(group_weights_kernel<KP>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   group_weights_kernel<KP><<<grid, kPassThreads, sm, st>>>(a);
@@ -374,18 +557,35 @@ void launch_weights(const double* rep, const double* u, int64_t n, const int64_t
 
 }  // namespace
 
-void solve_roots(const ReducedView& rp, int64_t j0, int64_t j1, const RootRecords& out,
-                 const SolveOptions& opt, DeviceScratch& ws, int sms, cudaStream_t st) {
+void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t j1,
+                 const RootRecords& out, const SolveOptions& opt, DeviceScratch& ws, int sms,
+                 cudaStream_t st) {
   if (j1 <= j0) return;
+  int* counts = nullptr;
+  if (opt.sweep) {
+    counts = ws.get_i32("sweep_counts", 2 * rp.n);
+    switch (rp.kp) {
+      case 1: launch_sweep<1>(rp, counts, st); break;
+      case 2: launch_sweep<2>(rp, counts, st); break;
+      case 4: launch_sweep<4>(rp, counts, st); break;
+      case 8: launch_sweep<8>(rp, counts, st); break;
+      case 16: launch_sweep<16>(rp, counts, st); break;
+      case 32: launch_sweep<32>(rp, counts, st); break;
+      default: throw Error(1, "", "solve_roots: unsupported padded rank");
+    }
+  }
+  if (!opt.fnewton) alpha = nullptr;
+#define EIGB_SOLVE(K) launch_solve<K>(rp, alpha, counts, j0, j1, out, opt, ws, sms, st)
   switch (rp.kp) {
-    case 1: launch_solve<1>(rp, j0, j1, out, opt, ws, sms, st); break;
-    case 2: launch_solve<2>(rp, j0, j1, out, opt, ws, sms, st); break;
-    case 4: launch_solve<4>(rp, j0, j1, out, opt, ws, sms, st); break;
-    case 8: launch_solve<8>(rp, j0, j1, out, opt, ws, sms, st); break;
-    case 16: launch_solve<16>(rp, j0, j1, out, opt, ws, sms, st); break;
-    case 32: launch_solve<32>(rp, j0, j1, out, opt, ws, sms, st); break;
+    case 1: EIGB_SOLVE(1); break;
+    case 2: EIGB_SOLVE(2); break;
+    case 4: EIGB_SOLVE(4); break;
+    case 8: EIGB_SOLVE(8); break;
+    case 16: EIGB_SOLVE(16); break;
+    case 32: EIGB_SOLVE(32); break;
     default: throw Error(1, "", "solve_roots: unsupported padded rank");
   }
+#undef EIGB_SOLVE
 }
 
 void group_weights(int kp, const double* rep, const double* u, int64_t n, const int64_t* gstart,

@@ -1,19 +1,26 @@
 // The secular "pole pass": for a batch of 32 evaluation points x_b (one per
-// lane, "slots") accumulate
-//     S_b = J + sum_i u_i u_i^T / (d_i - x_b)            (k x k, symmetric)
-//     g_b = sum_i (u_i . y_b)^2 / (d_i - x_b)^2        (= y_b^T S'(x_b) y_b)
-// over all poles i. This one contraction is the inner loop of
+// lane, "slots") accumulate, over all poles i with D_ib = 1/(d_i - x_b),
+//     S_b  = J + sum_i D_ib u_i u_i^T                    (k x k, symmetric)
+//     g_b  = sum_i (u_i . y_b)^2 D_ib^2                  (= y_b^T S'(x_b) y_b)
+//     f_b  = 1 + sum_i alpha_i D_ib,  f'_b = sum_i alpha_i D_ib^2
+// (f is the reference's scalar secular function, proj/src/secular.cpp:223-243,
+// with the residues alpha from K2). This contraction is the inner loop of
 //   * the deflation weights  (x_b = representative of pole group b; the
 //     excluded self term is the diff == 0 case; proj/src/secular.cpp:168-202),
-//   * the root solver        (inertia count + Newton),
+//   * the count sweep and the root solver,
 //   * the collision vectors  (proj/src/eigvec.cpp:75-119).
 //
-// Work split inside one CTA (NWARP = 8 warps): lane = slot, warp w handles
-// entry group (w % EG) of the packed upper triangle and pole split (w / EG).
-// Pole tiles (d_i and the padded row u_i) are staged in shared memory with
-// cp.async double buffering and read as warp-wide broadcasts, so every lane
-// spends its issue slots on DFMA: per pole and slot one MUFU.RCP64H + 4 DFMA
-// for 1/(d_i - x_b), then (KP - r) DFMA per row r of the entry group.
+// One CTA = 8 warps, lane = slot. Per tile of kPoleTile poles (staged in
+// shared memory by cp.async, double-buffered):
+//   D phase:   warp w takes poles w, w+8, ...; each lane forms its
+//              difference (d_i - dob_b) - delta_b (shifted origin), one
+//              MUFU.RCP64H + 4 DFMA reciprocal, writes D to shared memory and
+//              accumulates g_b, f_b, f'_b. Each reciprocal is computed once.
+//   FMA phase: warp w = (entry group g, pole split p) accumulates its share
+//              of the packed upper triangle: per pole one D load, the row u_i
+//              as warp-wide broadcasts, then (KP - r) DFMA per row r.
+// Entry groups are balanced (KP = 16: rows 0-4 = 70 entries, rows 5-15 =
+// 66), so no warp idles at the tile barriers.
 #pragma once
 
 #include "common.cuh"
@@ -50,10 +57,14 @@ struct PassCfg {
   __host__ __device__ static constexpr int pidx(int r, int c) {
     return r * KP - r * (r - 1) / 2 + (c - r);
   }
-  static constexpr int SIGMA_GROUP = EG - 1;  // group that also accumulates g_b
-  // shared memory (doubles)
-  static constexpr int TILE_DOUBLES = kPoleTile * (KP + 1);
-  static constexpr int RED_DOUBLES = 32 * (P + 1);
+  // reduced output per slot: P packed entries, then g, f, f'
+  static constexpr int OUT = P + 3;
+  static constexpr int IG = P, IF = P + 1, IFP = P + 2;
+  // shared memory (doubles): tile = d, alpha, u rows
+  static constexpr int TILE_DOUBLES = kPoleTile * (KP + 2);
+  static constexpr int DBUF_DOUBLES = kPoleTile * 32;
+  static constexpr int RED_DOUBLES = 32 * OUT;
+  static constexpr int SMEM_DOUBLES = 2 * TILE_DOUBLES + DBUF_DOUBLES + RED_DOUBLES;
 };
 
 // Per-slot evaluation point: x_b = dob[b] + delta[b]; the difference to pole i
@@ -67,18 +78,30 @@ struct PassSlots {
   int* hit;        // [32]  set when some d_i - x_b == 0 (solver: pole hit)
 };
 
+struct PassOpts {
+  const double* alpha = nullptr;  // residues for f (nullptr: f not needed)
+  bool want_sigma = false;        // accumulate g_b along y_b
+  bool exclude_zero = false;      // diff == 0 drops the term (no hit flag)
+  double excl_gap = 0.0;          // > 0: drop poles with |diff| < excl_gap
+};
+
 template <int KP>
 __device__ __forceinline__ void load_pole_tile(double* tile, const double* __restrict__ d,
+                                               const double* __restrict__ alpha,
                                                const double* __restrict__ u, int64_t i0,
                                                int64_t n) {
-  // tile layout: [kPoleTile] d, then [kPoleTile][KP] rows. Rows beyond n are
-  // zero with d = NaN (NaN difference => term skipped).
+  // tile layout: [T] d, [T] alpha, then [T][KP] rows. Rows beyond n are zero
+  // with d = NaN (NaN difference => term skipped).
   double* td = tile;
-  double* tu = tile + kPoleTile;
+  double* ta = tile + kPoleTile;
+  double* tu = tile + 2 * kPoleTile;
   const int tid = threadIdx.x;
   const int64_t cnt = (n - i0) < kPoleTile ? (n - i0) : kPoleTile;
-  for (int t = tid; t < kPoleTile; t += kPassThreads) td[t] = (t < cnt) ? d[i0 + t] : __longlong_as_double(0x7ff8000000000000ll);
-  if (KP >= 2) {
+  for (int t = tid; t < kPoleTile; t += kPassThreads) {
+    td[t] = (t < cnt) ? d[i0 + t] : __longlong_as_double(0x7ff8000000000000ll);
+    ta[t] = (t < cnt && alpha) ? alpha[i0 + t] : 0.0;
+  }
+  if constexpr (KP >= 2) {
     constexpr int CH = KP / 2;  // 16-byte chunks per row
     const double2* src = reinterpret_cast<const double2*>(u + i0 * KP);
     double2* dst = reinterpret_cast<double2*>(tu);
@@ -96,100 +119,138 @@ __device__ __forceinline__ void load_pole_tile(double* tile, const double* __res
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// Body of one warp: entry group G (compile time, so only its accumulators
-// are live), pole split p. All warps run the same tile loop, so every
-// __syncthreads() is reached the same number of times by the whole CTA.
+// FMA phase of entry group G on one tile (compile-time rows, so only this
+// group's accumulators are live).
 template <int KP, int G>
-__device__ __forceinline__ void pass_body(const double* __restrict__ d,
-                                          const double* __restrict__ u, int64_t n,
-                                          const PassSlots& slots, bool want_sigma,
-                                          bool exclude_zero, double excl_gap, double* tiles,
-                                          double* red, int p) {
+__device__ __forceinline__ void fma_tile(const double* __restrict__ tu, const double* __restrict__ db,
+                                         int p, int lane, double* acc) {
   using C = PassCfg<KP>;
   constexpr int RLO = C::row_lo(G), RHI = C::row_lo(G + 1);
+  constexpr int E0 = C::pidx(RLO, RLO);
+  constexpr int per = kPoleTile / C::PS;
+#pragma unroll 2
+  for (int ii = 0; ii < per; ++ii) {
+    const int i = p * per + ii;
+    const double D = db[i * 32 + lane];
+    double ur[KP];
+    if constexpr (KP >= 2) {
+#pragma unroll
+      for (int c = RLO & ~1; c < KP; c += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(tu + i * KP + c);
+        ur[c] = v.x;
+        ur[c + 1] = v.y;
+      }
+    } else {
+      ur[0] = tu[i];
+    }
+#pragma unroll
+    for (int r = RLO; r < RHI; ++r) {
+      const double v = D * ur[r];
+#pragma unroll
+      for (int c = r; c < KP; ++c) acc[C::pidx(r, c) - E0] = fma(v, ur[c], acc[C::pidx(r, c) - E0]);
+    }
+  }
+}
+
+template <int KP, int G>
+__device__ __forceinline__ void pass_body(const double* __restrict__ d, const double* __restrict__ u,
+                                          int64_t n, const PassSlots& slots, const PassOpts& o,
+                                          double* tiles, double* dbuf, double* red, int p) {
+  using C = PassCfg<KP>;
   constexpr int E = C::entries(G);
-  constexpr int E0 = C::pidx(RLO, RLO);  // packed offset of the group's first entry
+  constexpr int E0 = C::pidx(C::row_lo(G), C::row_lo(G));
   const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const double dob = slots.dob[lane];
   const double del = slots.delta[lane];
   const bool act = slots.active[lane] != 0;
-  const bool sig = want_sigma && (G == C::SIGMA_GROUP);
+  const bool sig = o.want_sigma;
+  const bool wf = o.alpha != nullptr;
   double yv[KP];
 #pragma unroll
   for (int c = 0; c < KP; ++c) yv[c] = sig ? slots.y[lane * KP + c] : 0.0;
   double acc[E > 0 ? E : 1];
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.0;
-  double gs = 0.0;
+  double gs = 0.0, fs = 0.0, fps = 0.0;
   int hit = 0;
 
   const int64_t ntiles = (n + kPoleTile - 1) / kPoleTile;
-  if (ntiles > 0) load_pole_tile<KP>(tiles, d, u, 0, n);
-  constexpr int per = kPoleTile / C::PS;
+  if (ntiles > 0) load_pole_tile<KP>(tiles, d, o.alpha, u, 0, n);
   for (int64_t t = 0; t < ntiles; ++t) {
     const double* cur = tiles + (t & 1) * C::TILE_DOUBLES;
-    if (t + 1 < ntiles) {
-      load_pole_tile<KP>(tiles + ((t + 1) & 1) * C::TILE_DOUBLES, d, u, (t + 1) * kPoleTile, n);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // tile t landed; previous FMA phase done with dbuf
+    if (t + 1 < ntiles)
+      load_pole_tile<KP>(tiles + ((t + 1) & 1) * C::TILE_DOUBLES, d, o.alpha, u,
+                         (t + 1) * kPoleTile, n);
     const double* td = cur;
-    const double* tu = cur + kPoleTile;
+    const double* ta = cur + kPoleTile;
+    const double* tu = cur + 2 * kPoleTile;
+    // ---- D phase
 #pragma unroll 2
-    for (int ii = 0; ii < per; ++ii) {
-      const int i = p * per + ii;
+    for (int i = warp; i < kPoleTile; i += kPassWarps) {
       const double diff = (td[i] - dob) - del;
       double D;
-      if (excl_gap > 0.0) {
-        D = (act && fabs(diff) >= excl_gap) ? rcp64(diff) : 0.0;
+      if (o.excl_gap > 0.0) {
+        D = (act && fabs(diff) >= o.excl_gap) ? rcp64(diff) : 0.0;
       } else if (diff == 0.0) {
-        hit |= !exclude_zero;
+        hit |= !o.exclude_zero;
         D = 0.0;
       } else {
         D = (act && diff == diff) ? rcp64(diff) : 0.0;
       }
-      double ur[KP];
-      if constexpr (KP >= 2) {
-#pragma unroll
-        for (int c = 0; c < KP; c += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(tu + i * KP + c);
-          ur[c] = v.x;
-          ur[c + 1] = v.y;
-        }
-      } else {
-        ur[0] = tu[i];
-      }
-#pragma unroll
-      for (int r = RLO; r < RHI; ++r) {
-        const double v = D * ur[r];
-#pragma unroll
-        for (int c = r; c < KP; ++c) acc[C::pidx(r, c) - E0] = fma(v, ur[c], acc[C::pidx(r, c) - E0]);
-      }
+      dbuf[i * 32 + lane] = D;
       if (sig) {
         double tt = 0.0;
+        if constexpr (KP >= 2) {
 #pragma unroll
-        for (int c = 0; c < KP; ++c) tt = fma(ur[c], yv[c], tt);
+          for (int c = 0; c < KP; c += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(tu + i * KP + c);
+            tt = fma(v.x, yv[c], tt);
+            tt = fma(v.y, yv[c + 1], tt);
+          }
+        } else {
+          tt = tu[i] * yv[0];
+        }
         const double td2 = tt * D;
         gs = fma(td2, td2, gs);
       }
+      if (wf) {
+        const double aD = ta[i] * D;
+        fs += aD;
+        fps = fma(aD, D, fps);
+      }
     }
-    __syncthreads();  // tile buffer reuse
+    __syncthreads();  // D of this tile visible
+    // ---- FMA phase
+    fma_tile<KP, G>(tu, dbuf, p, lane, acc);
   }
+  __syncthreads();
 
-  // Deterministic reduction over pole splits: p = 0 writes, p = 1.. add in order.
-  constexpr int PP = C::P + 1;
+  // Deterministic reduction: FMA partials over pole splits p = 0.. in order,
+  // D-phase partials (g, f, f') over warps 0..7 in order.
+  constexpr int OUT = C::OUT;
   for (int q = 0; q < C::PS; ++q) {
     if (p == q) {
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        if (q == 0) red[lane * PP + E0 + e] = acc[e];
-        else red[lane * PP + E0 + e] += acc[e];
+        if (q == 0) red[lane * OUT + E0 + e] = acc[e];
+        else red[lane * OUT + E0 + e] += acc[e];
       }
-      if (G == C::SIGMA_GROUP) {
-        if (q == 0) red[lane * PP + C::P] = gs;
-        else red[lane * PP + C::P] += gs;
+    }
+    __syncthreads();
+  }
+  for (int q = 0; q < kPassWarps; ++q) {
+    if (warp == q) {
+      if (q == 0) {
+        red[lane * OUT + C::IG] = gs;
+        red[lane * OUT + C::IF] = fs;
+        red[lane * OUT + C::IFP] = fps;
+      } else {
+        red[lane * OUT + C::IG] += gs;
+        red[lane * OUT + C::IF] += fs;
+        red[lane * OUT + C::IFP] += fps;
       }
     }
     __syncthreads();
@@ -197,24 +258,22 @@ __device__ __forceinline__ void pass_body(const double* __restrict__ d,
   if (hit) atomicOr(&slots.hit[lane], 1);
 }
 
-// Runs the pass. On return (after __syncthreads) red[b * (P+1) + e] holds the
-// packed S_b (without J) and red[b*(P+1) + P] holds g_b, for every slot b.
-// `exclude_zero`: a zero difference drops the term (deflation weights)
-// instead of flagging a pole hit. `excl_gap` > 0 drops every pole with
-// |d_i - x_b| < excl_gap (bordered collision systems).
+// Runs the pass. On return (after __syncthreads) red[b * OUT + e] holds the
+// packed S_b (without J) and red[b*OUT + P..P+2] = g_b, f_b - 1, f'_b.
+// smem: SMEM_DOUBLES doubles (tiles, D buffer, reduction).
 template <int KP>
 __device__ void secular_pass(const double* __restrict__ d, const double* __restrict__ u, int64_t n,
-                             const PassSlots& slots, bool want_sigma, bool exclude_zero,
-                             double excl_gap, double* tiles /* 2 x TILE_DOUBLES */,
-                             double* red /* RED_DOUBLES */) {
+                             const PassSlots& slots, const PassOpts& o, double* smem_pass) {
   using C = PassCfg<KP>;
+  double* tiles = smem_pass;
+  double* dbuf = tiles + 2 * C::TILE_DOUBLES;
+  double* red = dbuf + C::DBUF_DOUBLES;
   const int warp = threadIdx.x >> 5;
   const int g = warp % C::EG;
   const int p = warp / C::EG;
-#define EIGB_PASS_CASE(GG)                                                                  \
-  case GG:                                                                                 \
-    if constexpr (GG < C::EG)                                                              \
-      pass_body<KP, GG>(d, u, n, slots, want_sigma, exclude_zero, excl_gap, tiles, red, p); \
+#define EIGB_PASS_CASE(GG)                                                     \
+  case GG:                                                                    \
+    if constexpr (GG < C::EG) pass_body<KP, GG>(d, u, n, slots, o, tiles, dbuf, red, p); \
     break;
   switch (g) {
     EIGB_PASS_CASE(0)
@@ -230,23 +289,29 @@ __device__ void secular_pass(const double* __restrict__ d, const double* __restr
   __syncthreads();
 }
 
+template <int KP>
+__device__ __forceinline__ const double* pass_result(const double* smem_pass) {
+  using C = PassCfg<KP>;
+  return smem_pass + 2 * C::TILE_DOUBLES + C::DBUF_DOUBLES;
+}
+
 // ------------------------------------------------------------ small k x k
 // Bunch-Kaufman LDL^T (partial pivoting, alpha = (1+sqrt(17))/8) of the full
 // symmetric n x n matrix A (row-major, leading dimension ld), in place.
 // piv[k] encodes the interchange of step k (>= 0: 1x1 with row piv[k];
 // < 0: 2x2 block with row -piv[k]-1). Returns the number of negative
 // eigenvalues (inertia); *zero is set when an exactly zero pivot occurred.
-__host__ __device__ inline int bk_factor(double* A, int n, int ld, int* piv, int* zero) {
+__host__ __device__ inline int bk_factor(double* A, int n, int ld, int* piv, int* zero, int es = 1) {
   const double alpha = 0.6403882032022076;
   int neg = 0;
   *zero = 0;
   int k = 0;
   while (k < n) {
-    const double absakk = fabs(A[k * ld + k]);
+    const double absakk = fabs(A[(k * ld + k) * es]);
     int imax = k;
     double colmax = 0.0;
     for (int i = k + 1; i < n; ++i) {
-      const double v = fabs(A[i * ld + k]);
+      const double v = fabs(A[(i * ld + k) * es]);
       if (v > colmax) colmax = v, imax = i;
     }
     int kstep = 1, kp = k;
@@ -261,10 +326,10 @@ __host__ __device__ inline int bk_factor(double* A, int n, int ld, int* piv, int
     } else {
       double rowmax = 0.0;
       for (int j = k; j < n; ++j)
-        if (j != imax) rowmax = fmax(rowmax, fabs(A[imax * ld + j]));
+        if (j != imax) rowmax = fmax(rowmax, fabs(A[(imax * ld + j) * es]));
       if (absakk >= alpha * colmax * (colmax / rowmax)) {
         kp = k;
-      } else if (fabs(A[imax * ld + imax]) >= alpha * rowmax) {
+      } else if (fabs(A[(imax * ld + imax) * es]) >= alpha * rowmax) {
         kp = imax;
       } else {
         kp = imax;
@@ -274,18 +339,18 @@ __host__ __device__ inline int bk_factor(double* A, int n, int ld, int* piv, int
     const int kk = k + kstep - 1;
     if (kp != kk) {  // symmetric interchange of kk and kp (whole rows/cols)
       for (int j = 0; j < n; ++j) {
-        const double t = A[kk * ld + j];
-        A[kk * ld + j] = A[kp * ld + j];
-        A[kp * ld + j] = t;
+        const double t = A[(kk * ld + j) * es];
+        A[(kk * ld + j) * es] = A[(kp * ld + j) * es];
+        A[(kp * ld + j) * es] = t;
       }
       for (int i = 0; i < n; ++i) {
-        const double t = A[i * ld + kk];
-        A[i * ld + kk] = A[i * ld + kp];
-        A[i * ld + kp] = t;
+        const double t = A[(i * ld + kk) * es];
+        A[(i * ld + kk) * es] = A[(i * ld + kp) * es];
+        A[(i * ld + kp) * es] = t;
       }
     }
     if (kstep == 1) {
-      const double dk = A[k * ld + k];
+      const double dk = A[(k * ld + k) * es];
       piv[k] = kp;
       if (dk < 0.0) ++neg;
       if (dk == 0.0) {
@@ -293,15 +358,15 @@ __host__ __device__ inline int bk_factor(double* A, int n, int ld, int* piv, int
       } else {
         const double r1 = 1.0 / dk;
         for (int i = k + 1; i < n; ++i) {
-          const double li = A[i * ld + k] * r1;
-          for (int j = k + 1; j <= i; ++j) A[i * ld + j] -= li * A[j * ld + k];
+          const double li = A[(i * ld + k) * es] * r1;
+          for (int j = k + 1; j <= i; ++j) A[(i * ld + j) * es] -= li * A[(j * ld + k) * es];
         }
-        for (int i = k + 1; i < n; ++i) A[i * ld + k] *= r1;
+        for (int i = k + 1; i < n; ++i) A[(i * ld + k) * es] *= r1;
         for (int i = k + 1; i < n; ++i)
-          for (int j = k + 1; j < i; ++j) A[j * ld + i] = A[i * ld + j];
+          for (int j = k + 1; j < i; ++j) A[(j * ld + i) * es] = A[(i * ld + j) * es];
       }
     } else {
-      const double a = A[k * ld + k], b = A[(k + 1) * ld + k], c = A[(k + 1) * ld + k + 1];
+      const double a = A[(k * ld + k) * es], b = A[((k + 1) * ld + k) * es], c = A[((k + 1) * ld + k + 1) * es];
       const double det = a * c - b * b;
       piv[k] = -kp - 1;
       piv[k + 1] = -kp - 1;
@@ -315,16 +380,16 @@ __host__ __device__ inline int bk_factor(double* A, int n, int ld, int* piv, int
         // rows in decreasing order: row i reads columns k, k+1 of rows j <= i
         // before they are overwritten by their L entries
         for (int i = n - 1; i >= k + 2; --i) {
-          const double x1 = A[i * ld + k], x2 = A[i * ld + k + 1];
+          const double x1 = A[(i * ld + k) * es], x2 = A[(i * ld + k + 1) * es];
           const double w1 = (c * x1 - b * x2) * id;
           const double w2 = (a * x2 - b * x1) * id;
           for (int j = k + 2; j <= i; ++j)
-            A[i * ld + j] -= w1 * A[j * ld + k] + w2 * A[j * ld + k + 1];
-          A[i * ld + k] = w1;
-          A[i * ld + k + 1] = w2;
+            A[(i * ld + j) * es] -= w1 * A[(j * ld + k) * es] + w2 * A[(j * ld + k + 1) * es];
+          A[(i * ld + k) * es] = w1;
+          A[(i * ld + k + 1) * es] = w2;
         }
         for (int i = k + 2; i < n; ++i)
-          for (int j = k + 2; j < i; ++j) A[j * ld + i] = A[i * ld + j];
+          for (int j = k + 2; j < i; ++j) A[(j * ld + i) * es] = A[(i * ld + j) * es];
       }
     }
     k += kstep;
@@ -338,7 +403,7 @@ __host__ __device__ inline int bk_factor(double* A, int n, int ld, int* piv, int
 // L, D (1x1 / 2x2 blocks), L^T, permute back. Zero pivots are replaced by
 // `tiny` (inverse iteration on a singular matrix).
 __host__ __device__ inline void bk_solve(const double* A, int n, int ld, const int* piv, double* b,
-                                         double tiny) {
+                                         double tiny, int es = 1) {
   int k = 0;
   while (k < n) {  // b <- P b (interchanges in factorization order)
     if (piv[k] >= 0) {
@@ -354,22 +419,22 @@ __host__ __device__ inline void bk_solve(const double* A, int n, int ld, const i
   k = 0;
   while (k < n) {  // L y = b
     if (piv[k] >= 0) {
-      for (int i = k + 1; i < n; ++i) b[i] -= A[i * ld + k] * b[k];
+      for (int i = k + 1; i < n; ++i) b[i] -= A[(i * ld + k) * es] * b[k];
       k += 1;
     } else {
-      for (int i = k + 2; i < n; ++i) b[i] -= A[i * ld + k] * b[k] + A[i * ld + k + 1] * b[k + 1];
+      for (int i = k + 2; i < n; ++i) b[i] -= A[(i * ld + k) * es] * b[k] + A[(i * ld + k + 1) * es] * b[k + 1];
       k += 2;
     }
   }
   k = 0;
   while (k < n) {  // D w = y
     if (piv[k] >= 0) {
-      double dk = A[k * ld + k];
+      double dk = A[(k * ld + k) * es];
       if (dk == 0.0) dk = tiny;
       b[k] /= dk;
       k += 1;
     } else {
-      const double a = A[k * ld + k], bb = A[(k + 1) * ld + k], c = A[(k + 1) * ld + k + 1];
+      const double a = A[(k * ld + k) * es], bb = A[((k + 1) * ld + k) * es], c = A[((k + 1) * ld + k + 1) * es];
       double det = a * c - bb * bb;
       if (det == 0.0) det = tiny;
       const double x1 = (c * b[k] - bb * b[k + 1]) / det;
@@ -382,12 +447,12 @@ __host__ __device__ inline void bk_solve(const double* A, int n, int ld, const i
   k = n - 1;
   while (k >= 0) {  // L^T z = w
     if (piv[k] >= 0) {
-      for (int i = k + 1; i < n; ++i) b[k] -= A[i * ld + k] * b[i];
+      for (int i = k + 1; i < n; ++i) b[k] -= A[(i * ld + k) * es] * b[i];
       k -= 1;
     } else {  // block (k-1, k)
       for (int i = k + 1; i < n; ++i) {
-        b[k] -= A[i * ld + k] * b[i];
-        b[k - 1] -= A[i * ld + k - 1] * b[i];
+        b[k] -= A[(i * ld + k) * es] * b[i];
+        b[k - 1] -= A[(i * ld + k - 1) * es] * b[i];
       }
       k -= 2;
     }
