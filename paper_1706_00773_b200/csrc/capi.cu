@@ -236,7 +236,8 @@ void finish(eigmod_b200_ctx* c, const double* q, const double* lam_in, int64_t c
   double* xt = c->ws.get_f64("xt", (size_t)nc * n);
   double* colscale = c->ws.get_f64("colscale", nc);
   int* cmode = c->ws.get_i32("colmode", nc);
-  eigb::build_xt_dev(p, c->recs, cols, colldir, collok, c0, c1, xt, colscale, cmode, c->stream);
+  eigb::build_xt_dev(p, c->recs, cols, colldir, collok, c0, c1, xt, colscale, cmode, c->ws,
+                     c->stream);
   c->mark(4);
   double* tcm = eigb::tile_colmax_buffer(n, nc, c->ws);
   eigb::gemm_nt_dev(q, xt, n, nc, n, q_out, ldq, colscale, tcm, c->stream);

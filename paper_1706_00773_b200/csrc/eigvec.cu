@@ -162,25 +162,43 @@ __global__ void __launch_bounds__(kPassThreads, 1) collision_kernel(
   }
 }
 
+// Per-column parameters of a tile (shared memory).
 template <int KP>
-__device__ __forceinline__ double red_value(const ReducedView& rp, int64_t r, const double* yv,
-                                            double dob, double del, bool coll, int64_t o,
-                                            double pole, double gap, bool collok) {
-  const double* ui = rp.u + r * KP;
+struct XtCol {
+  int kind;      // 0 root, 1 unit, 2 rotation, -1 outside [c0, c1)
+  int mode;      // roots: 0 formula, 1 bordered (collided), 2 collided fallback e_o
+  int64_t o;     // roots: origin pole; unit: source index; rotation: group
+  int64_t t;     // rotation row
+  double dob, del;
+  double y[KP + 1];
+};
+
+// Value of reduced coordinate r for column parameters cp (eigvec.cpp:133-153
+// formula in the solver's shifted origin, or the bordered-system vector of
+// eigvec.cpp:75-119 for a root sitting on pole o).
+template <int KP>
+__device__ __forceinline__ double red_value(const ReducedView& rp, int64_t r, const double* ur,
+                                            const XtCol<KP>& cp, double gap) {
   double t = 0.0;
 #pragma unroll
-  for (int c = 0; c < KP; ++c) t = fma(ui[c], yv[c], t);
-  if (!coll) return t / ((rp.d[r] - dob) - del);
-  if (!collok) return (r == o) ? 1.0 : 0.0;
-  const double g = rp.d[r] - pole;
-  if (fabs(g) < gap) return (r == o) ? yv[KP] : 0.0;
+  for (int c = 0; c < KP; ++c) t = fma(ur[c], cp.y[c], t);
+  const double dr = rp.d[r];
+  if (cp.mode == 0) return t * rcp64((dr - cp.dob) - cp.del);
+  if (cp.mode == 2) return (r == cp.o) ? 1.0 : 0.0;
+  const double g = dr - cp.dob;
+  if (fabs(g) < gap) return (r == cp.o) ? cp.y[KP] : 0.0;
   return -t / g;
 }
 
 constexpr int kXtThreads = 256;
+constexpr int kXtCols = 16;
 
+// One CTA = 256 original indices x 16 columns. Each thread loads its row of U
+// once and produces 16 entries of Xt (coalesced stores along the row index);
+// squared norms are reduced per CTA and finished by xt_norm_kernel in a
+// fixed order (deterministic).
 template <int KP>
-__global__ void __launch_bounds__(kXtThreads) xt_kernel(
+__global__ void __launch_bounds__(kXtThreads) xt_tile_kernel(
     ReducedView rp, int64_t n, const int* __restrict__ ckind, const int64_t* __restrict__ cpay,
     const int64_t* __restrict__ origin, const double* __restrict__ delta,
     const int* __restrict__ flags, const double* __restrict__ yall,
@@ -189,82 +207,128 @@ __global__ void __launch_bounds__(kXtThreads) xt_kernel(
     const int64_t* __restrict__ gstart, const int64_t* __restrict__ glen,
     const int64_t* __restrict__ hoff, const double* __restrict__ hbuf,
     const int64_t* __restrict__ rank, const int64_t* __restrict__ off_red, double gap,
-    int64_t c0, double* __restrict__ xt, double* __restrict__ colscale, int* __restrict__ cmode) {
-  __shared__ double yv[KP + 1];
-  __shared__ double red[32];
-  const int64_t c = c0 + blockIdx.x;
-  double* row = xt + (int64_t)blockIdx.x * n;
-  const int kind = ckind[c];
-  if (kind != 0) {
-    const int64_t e = cpay[c];
-    const int64_t src = dec_src[e];
-    if (kind == 1) {
-      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) row[i] = (i == src) ? 1.0 : 0.0;
+    int64_t c0, int64_t c1, double* __restrict__ xt, double* __restrict__ part) {
+  __shared__ XtCol<KP> cols[kXtCols];
+  __shared__ double red[kXtThreads / 32][kXtCols];
+  const int64_t cb = c0 + (int64_t)blockIdx.y * kXtCols;
+  if (threadIdx.x < kXtCols) {
+    XtCol<KP>& cp = cols[threadIdx.x];
+    const int64_t c = cb + threadIdx.x;
+    if (c >= c1) {
+      cp.kind = -1;
     } else {
-      const int64_t code = -(src + 2);
-      const int64_t g = code / 65536, tt = code % 65536;
-      const int64_t s0 = gstart[g], m = glen[g];
-      const double* H = hbuf + hoff[g];
-      for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
-        row[i] = (i >= s0 && i < s0 + m) ? H[tt * m + (i - s0)] : 0.0;
+      cp.kind = ckind[c];
+      const int64_t pay = cpay[c];
+      if (cp.kind == 0) {
+        const int64_t j = pay;
+        cp.o = origin[j];
+        cp.dob = rp.d[cp.o];
+        cp.del = delta[j];
+        const bool coll = (flags[j] & 1) != 0;
+        cp.mode = coll ? (collok[j] ? 1 : 2) : 0;
+        for (int q = 0; q <= KP; ++q)
+          cp.y[q] = coll ? colldir[j * (KP + 1) + q] : (q < KP ? yall[j * KP + q] : 0.0);
+      } else {
+        const int64_t src = dec_src[pay];
+        if (cp.kind == 1) {
+          cp.o = src;
+        } else {
+          const int64_t code = -(src + 2);
+          cp.o = code / 65536;
+          cp.t = code % 65536;
+        }
+      }
     }
-    if (threadIdx.x == 0) {
-      colscale[c - c0] = 1.0;
-      cmode[c - c0] = (kind == 2);
-    }
-    return;
-  }
-  const int64_t j = cpay[c];
-  const bool coll = (flags[j] & 1) != 0;
-  const int64_t o = origin[j];
-  const double dob = rp.d[o];
-  const double del = delta[j];
-  const bool cok = coll ? (collok[j] != 0) : true;
-  if (threadIdx.x <= KP) {
-    if (coll) yv[threadIdx.x] = colldir[j * (KP + 1) + threadIdx.x];
-    else yv[threadIdx.x] = (threadIdx.x < KP) ? yall[j * KP + threadIdx.x] : 0.0;
   }
   __syncthreads();
-  double ss = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const int64_t r = orig_map[i];
-    double x;
-    if (r >= 0) {
-      x = red_value<KP>(rp, r, yv, dob, del, coll, o, dob, gap, cok);
-    } else if (r == -1) {
-      x = 0.0;
+  const int64_t i = (int64_t)blockIdx.x * kXtThreads + threadIdx.x;
+  const bool valid = i < n;
+  const int64_t r = valid ? orig_map[i] : -1;
+  double ur[KP];
+  if (r >= 0) {
+    if constexpr (KP >= 2) {
+#pragma unroll
+      for (int c = 0; c < KP; c += 2) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(rp.u + r * KP + c));
+        ur[c] = v.x;
+        ur[c + 1] = v.y;
+      }
     } else {
-      const int64_t g = -2 - r;
-      const int64_t s0 = gstart[g], m = glen[g];
-      const double* H = hbuf + hoff[g];
-      x = 0.0;
-      for (int64_t tt = 0; tt < rank[g]; ++tt)
-        x += H[tt * m + (i - s0)] *
-             red_value<KP>(rp, off_red[g] + tt, yv, dob, del, coll, o, dob, gap, cok);
+      ur[0] = rp.u[r];
     }
-    row[i] = x;
-    ss = fma(x, x, ss);
   }
-  ss = warp_sum(ss);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  double ss[kXtCols];
+#pragma unroll
+  for (int q = 0; q < kXtCols; ++q) {
+    const XtCol<KP>& cp = cols[q];
+    double x = 0.0;
+    if (cp.kind == 0) {
+      if (r >= 0) {
+        x = red_value<KP>(rp, r, ur, cp, gap);
+      } else if (r <= -2) {  // member of a compressed run: rotate back
+        const int64_t g = -2 - r;
+        const int64_t s0 = gstart[g], m = glen[g];
+        const double* H = hbuf + hoff[g];
+        for (int64_t tt = 0; tt < rank[g]; ++tt) {
+          const int64_t rr = off_red[g] + tt;
+          double uu[KP];
+#pragma unroll
+          for (int c = 0; c < KP; ++c) uu[c] = rp.u[rr * KP + c];
+          x += H[tt * m + (i - s0)] * red_value<KP>(rp, rr, uu, cp, gap);
+        }
+      }
+    } else if (cp.kind == 1) {
+      x = (i == cp.o) ? 1.0 : 0.0;
+    } else if (cp.kind == 2) {
+      const int64_t s0 = gstart[cp.o], m = glen[cp.o];
+      x = (i >= s0 && i < s0 + m) ? hbuf[hoff[cp.o] + cp.t * m + (i - s0)] : 0.0;
+    }
+    if (valid && cp.kind >= 0) __stcs(xt + (cb + q - c0) * n + i, x);
+    ss[q] = x * x;
+  }
+  // per-CTA column sums (fixed order: warp shuffles, then warps 0..7)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < kXtCols; ++q) {
+    const double v = warp_sum(ss[q]);
+    if (lane == 0) red[warp][q] = v;
+  }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < kXtCols) {
     double tsum = 0.0;
-    for (int w = 0; w < kXtThreads / 32; ++w) tsum += red[w];
-    colscale[c - c0] = (tsum > 0.0) ? 1.0 / sqrt(tsum) : 1.0;
-    cmode[c - c0] = 1;
+    for (int w = 0; w < kXtThreads / 32; ++w) tsum += red[w][threadIdx.x];
+    const int64_t c = cb + threadIdx.x;
+    if (c < c1) part[(c - c0) * gridDim.x + blockIdx.x] = tsum;
   }
+}
+
+__global__ void xt_norm_kernel(const double* __restrict__ part, int64_t nchunks, int64_t c0,
+                               int64_t c1, const int* __restrict__ ckind,
+                               double* __restrict__ colscale, int* __restrict__ cmode) {
+  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= c1) return;
+  const int kind = ckind[c];
+  double s = 0.0;
+  for (int64_t b = 0; b < nchunks; ++b) s += part[(c - c0) * nchunks + b];
+  colscale[c - c0] = (kind == 0 && s > 0.0) ? 1.0 / sqrt(s) : 1.0;
+  cmode[c - c0] = (kind != 1);  // sign rule on computed columns (eigvec.cpp:340-347)
 }
 
 template <int KP>
 void launch_xt(const Plan& p, const RootRecords& roots, const Columns& cols, const double* colldir,
                const int* collok, int64_t c0, int64_t c1, double* xt, double* colscale, int* cmode,
-               cudaStream_t st) {
+               DeviceScratch& ws, cudaStream_t st) {
   const double gap = kPoleMergeRelGap * p.scale;
-  xt_kernel<KP><<<(unsigned)(c1 - c0), kXtThreads, 0, st>>>(
+  const int64_t nchunks = cdiv(p.n, kXtThreads);
+  double* part = ws.get_f64("xt_part", (size_t)nchunks * (c1 - c0));
+  dim3 grid((unsigned)nchunks, (unsigned)cdiv(c1 - c0, kXtCols));
+  xt_tile_kernel<KP><<<grid, kXtThreads, 0, st>>>(
       p.view(), p.n, cols.kind, cols.payload, roots.origin, roots.delta, roots.flags, roots.y,
       colldir, collok, p.orig_map, p.dec_src, p.gstart, p.glen, p.hoff, p.hbuf, p.rank, p.off_red,
-      gap, c0, xt, colscale, cmode);
+      gap, c0, c1, xt, part);
+  EIGB_LAUNCH_CHECK();
+  xt_norm_kernel<<<(unsigned)cdiv(c1 - c0, 128), 128, 0, st>>>(part, nchunks, c0, c1, cols.kind,
+                                                               colscale, cmode);
   EIGB_LAUNCH_CHECK();
 }
 
@@ -348,15 +412,15 @@ void collision_vectors_dev(const Plan& p, const RootRecords& roots, double* coll
 
 void build_xt_dev(const Plan& p, const RootRecords& roots, const Columns& cols,
                   const double* colldir, const int* collok, int64_t c0, int64_t c1, double* xt,
-                  double* colscale, int* cmode, cudaStream_t st) {
+                  double* colscale, int* cmode, DeviceScratch& ws, cudaStream_t st) {
   if (c1 <= c0) return;
   switch (p.kp) {
-    case 1: launch_xt<1>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, st); break;
-    case 2: launch_xt<2>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, st); break;
-    case 4: launch_xt<4>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, st); break;
-    case 8: launch_xt<8>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, st); break;
-    case 16: launch_xt<16>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, st); break;
-    case 32: launch_xt<32>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, st); break;
+    case 1: launch_xt<1>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, ws, st); break;
+    case 2: launch_xt<2>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, ws, st); break;
+    case 4: launch_xt<4>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, ws, st); break;
+    case 8: launch_xt<8>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, ws, st); break;
+    case 16: launch_xt<16>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, ws, st); break;
+    case 32: launch_xt<32>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, ws, st); break;
   }
 }
 

@@ -17,6 +17,9 @@
 #include "pipeline.cuh"
 
 #include <algorithm>
+#include <climits>
+#include <cstdlib>
+#include <string>
 
 namespace eigb {
 
@@ -64,6 +67,79 @@ __device__ __forceinline__ void load_stage(double* st, const double* __restrict_
     const double* src = bytes ? b + gr * K + gk : b;
     cp_async16(sb + row * BK + 2 * (q ^ (row & 7)), src, bytes);
   }
+}
+
+// Epilogue shared by both kernels: column scale (eigenvector norms from K4),
+// row-major stores with leading dimension ldc, and per (row tile, column) the
+// signed entry of largest magnitude, first row on ties (eigvec.cpp:340-347).
+__device__ __forceinline__ void epilogue_store(double (&acc)[8][4][2], int64_t m, int64_t nn,
+                                               double* __restrict__ c, int64_t ldc,
+                                               const double* __restrict__ colscale, int64_t m0,
+                                               int64_t n0, int wm, int wn, int g, int t4,
+                                               double* colbest, int* colrow) {
+#pragma unroll
+  for (int nb = 0; nb < 4; ++nb) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int cl = wn * 32 + nb * 8 + 2 * t4 + e;
+      const int64_t cg = n0 + cl;
+      const double sc = (cg < nn) ? colscale[cg] : 0.0;
+      double best = 0.0;
+      int brow = 0x7fffffff;
+#pragma unroll
+      for (int mb = 0; mb < 8; ++mb) {
+        const int rl = wm * 64 + mb * 8 + g;
+        const double v = acc[mb][nb][e] * sc;
+        acc[mb][nb][e] = v;
+        if (m0 + rl < m && (fabs(v) > fabs(best) || (fabs(v) == fabs(best) && rl < brow))) {
+          best = v;
+          brow = rl;
+        }
+      }
+      // reduce over the 8 lanes sharing this column (g = 0..7)
+#pragma unroll
+      for (int o = 4; o <= 16; o <<= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int orow = __shfl_xor_sync(0xffffffffu, brow, o);
+        if (fabs(ob) > fabs(best) || (fabs(ob) == fabs(best) && orow < brow)) {
+          best = ob;
+          brow = orow;
+        }
+      }
+      if (g == 0) {
+        colbest[wm * BN + cl] = best;
+        colrow[wm * BN + cl] = brow;
+      }
+    }
+  }
+#pragma unroll
+  for (int mb = 0; mb < 8; ++mb) {
+    const int64_t row = m0 + wm * 64 + mb * 8 + g;
+    if (row >= m) continue;
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) {
+      const int64_t col = n0 + wn * 32 + nb * 8 + 2 * t4;
+      double* dst = c + row * ldc + col;
+      if (col + 1 < nn && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        *reinterpret_cast<double2*>(dst) = make_double2(acc[mb][nb][0], acc[mb][nb][1]);
+      } else {
+        if (col < nn) dst[0] = acc[mb][nb][0];
+        if (col + 1 < nn) dst[1] = acc[mb][nb][1];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void tile_colmax_write(double* __restrict__ tile_colmax, int64_t tm,
+                                                  int64_t nn, int64_t n0, int tid,
+                                                  const double* colbest, const int* colrow) {
+  const int64_t cg = n0 + tid;
+  if (cg >= nn) return;
+  const double b0 = colbest[tid], b1 = colbest[BN + tid];
+  const int r0 = colrow[tid], r1 = colrow[BN + tid];
+  double best = b0;
+  if (fabs(b1) > fabs(b0) || (fabs(b1) == fabs(b0) && r1 < r0)) best = b1;
+  tile_colmax[tm * nn + cg] = best;
 }
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -135,72 +211,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
 
   // ---- epilogue: scale, store, per-tile column max for the sign rule
-  double* colbest = smem;                 // [2][BN] signed value
+  double* colbest = smem;                               // [2][BN] signed value
   int* colrow = reinterpret_cast<int*>(smem + 2 * BN);  // [2][BN] row of best
-#pragma unroll
-  for (int nb = 0; nb < 4; ++nb) {
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int cl = wn * 32 + nb * 8 + 2 * t4 + e;
-      const int64_t cg = n0 + cl;
-      const double sc = (cg < nn) ? colscale[cg] : 0.0;
-      double best = 0.0;
-      int brow = 0x7fffffff;
-#pragma unroll
-      for (int mb = 0; mb < 8; ++mb) {
-        const int rl = wm * 64 + mb * 8 + g;
-        const double v = acc[mb][nb][e] * sc;
-        acc[mb][nb][e] = v;
-        if (m0 + rl < m && (fabs(v) > fabs(best) || (fabs(v) == fabs(best) && rl < brow))) {
-          best = v;
-          brow = rl;
-        }
-      }
-      // reduce over the 8 lanes sharing this column (g = 0..7)
-#pragma unroll
-      for (int o = 4; o <= 16; o <<= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int orow = __shfl_xor_sync(0xffffffffu, brow, o);
-        if (fabs(ob) > fabs(best) || (fabs(ob) == fabs(best) && orow < brow)) {
-          best = ob;
-          brow = orow;
-        }
-      }
-      if (g == 0) {
-        colbest[wm * BN + cl] = best;
-        colrow[wm * BN + cl] = brow;
-      }
-    }
-  }
-  // stores (row-major C with leading dimension ldc)
-#pragma unroll
-  for (int mb = 0; mb < 8; ++mb) {
-    const int64_t row = m0 + wm * 64 + mb * 8 + g;
-    if (row >= m) continue;
-#pragma unroll
-    for (int nb = 0; nb < 4; ++nb) {
-      const int64_t col = n0 + wn * 32 + nb * 8 + 2 * t4;
-      double* dst = c + row * ldc + col;
-      if (col + 1 < nn && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-        *reinterpret_cast<double2*>(dst) = make_double2(acc[mb][nb][0], acc[mb][nb][1]);
-      } else {
-        if (col < nn) dst[0] = acc[mb][nb][0];
-        if (col + 1 < nn) dst[1] = acc[mb][nb][1];
-      }
-    }
-  }
+  epilogue_store(acc, m, nn, c, ldc, colscale, m0, n0, wm, wn, g, t4, colbest, colrow);
   __syncthreads();
-  if (tile_colmax && tid < BN) {
-    const int64_t cg = n0 + tid;
-    if (cg < nn) {
-      double b0 = colbest[tid], b1 = colbest[BN + tid];
-      const int r0 = colrow[tid], r1 = colrow[BN + tid];
-      double best = b0;
-      if (fabs(b1) > fabs(b0) || (fabs(b1) == fabs(b0) && r1 < r0)) best = b1;
-      tile_colmax[tm * nn + cg] = best;
-    }
-  }
+  if (tile_colmax && tid < BN) tile_colmax_write(tile_colmax, tm, nn, n0, tid, colbest, colrow);
 }
+
+}  // namespace
+}  // namespace eigb
+
+#include "gemm_tma.cuh"
+
+namespace eigb {
+namespace {
 
 // Sign rule across row tiles: first tile holding the maximal |entry| decides.
 __global__ void colsign_kernel(const double* __restrict__ tile_colmax, int64_t tiles_m,
@@ -239,6 +263,22 @@ void gemm_nt_dev(const double* a, const double* b, int64_t m, int64_t nn, int64_
   if ((kk & 1) || (reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
     throw Error(1, "", "gemm: operands must be 16-byte aligned with an even inner dimension");
   const int64_t tiles = cdiv(m, BM) * cdiv(nn, BN);
+  static int use_tma = -1;  // EIGMOD_B200_GEMM=cpasync selects the cp.async kernel
+  if (use_tma < 0) {
+    const char* e = std::getenv("EIGMOD_B200_GEMM");
+    use_tma = !(e && std::string(e) == "cpasync");
+  }
+  CUtensorMap ma, mb;
+  if (use_tma && kk <= INT32_MAX && m <= INT32_MAX && nn <= INT32_MAX && make_map(&ma, a, m, kk) &&
+      make_map(&mb, b, nn, kk)) {
+    const size_t sm = sizeof(double) * TMA_STAGES * STAGE_DOUBLES + 2 * TMA_STAGES * 8 + 1024;
+    EIGB_CUDA(cudaFuncSetAttribute(dmma_gemm_nt_tma_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    dmma_gemm_nt_tma_kernel<<<(unsigned)tiles, TMA_THREADS, sm, st>>>(ma, mb, m, nn, kk, c, ldc,
+                                                                      colscale, tile_colmax);
+    EIGB_LAUNCH_CHECK();
+    return;
+  }
   const size_t sm = sizeof(double) * STAGES * STAGE_DOUBLES;
   EIGB_CUDA(cudaFuncSetAttribute(dmma_gemm_nt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sm));

@@ -1,0 +1,188 @@
+// TMA variant of the K5 DMMA GEMM (included by gemm.cu after its helpers).
+//
+// One elected thread issues cp.async.bulk.tensor (TMA, 128-byte swizzle =
+// the layout load_stage writes) into a 6-stage ring guarded by full/empty
+// mbarriers; all 8 warps wait only for "full", run the same DMMA fragment
+// schedule as the cp.async kernel and release the slot with one arrive per
+// warp. The refill of a slot is issued one k-tile after its release, so the
+// issuing thread rarely waits. No CTA-wide barrier in the main loop, no
+// per-thread copy instructions. (A dedicated producer warp would make the
+// CTA 288 threads, which caps registers at 168 and spills the accumulators.)
+// Out-of-range boxes are zero-filled by the TMA unit.
+#pragma once
+
+#include <cuda.h>
+
+namespace eigb {
+namespace {
+
+constexpr int TMA_STAGES = 6;
+constexpr int TMA_THREADS = GEMM_THREADS;
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];" ::"r"(d),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(b), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(TMA_THREADS, 1)
+    dmma_gemm_nt_tma_kernel(const __grid_constant__ CUtensorMap tma_a,
+                            const __grid_constant__ CUtensorMap tma_b, int64_t m, int64_t nn,
+                            int64_t K, double* __restrict__ c, int64_t ldc,
+                            const double* __restrict__ colscale, double* __restrict__ tile_colmax) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  double* smem = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TMA_STAGES * STAGE_DOUBLES);
+  uint64_t* empty = full + TMA_STAGES;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t tiles_m = cdiv_dev(m, BM), tiles_n = cdiv_dev(nn, BN);
+  const int64_t pid = blockIdx.x;
+  const int64_t group = 8;
+  const int64_t per_group = group * tiles_n;
+  const int64_t gidx = pid / per_group;
+  const int64_t first_m = gidx * group;
+  const int64_t gsize = (tiles_m - first_m) < group ? (tiles_m - first_m) : group;
+  const int64_t tm = first_m + (pid % per_group) % gsize;
+  const int64_t tn = (pid % per_group) / gsize;
+  const int64_t m0 = tm * BM, n0 = tn * BN;
+  const int64_t KT = (K + BK - 1) / BK;
+
+  if (tid == 0) {
+    for (int s = 0; s < TMA_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], GEMM_THREADS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  auto issue = [&](int64_t kt) {
+    const int s = (int)(kt % TMA_STAGES);
+    double* st = smem + s * STAGE_DOUBLES;
+    mbar_expect_tx(&full[s], STAGE_DOUBLES * 8);
+    tma_load_2d(st, &tma_a, &full[s], (int)(kt * BK), (int)m0);
+    tma_load_2d(st + BM * BK, &tma_b, &full[s], (int)(kt * BK), (int)n0);
+  };
+  if (tid == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
+    for (int64_t kt = 0; kt < TMA_STAGES && kt < KT; ++kt) issue(kt);
+  }
+
+  const int wm = warp >> 2, wn = warp & 3;
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int g = lane >> 2, t4 = lane & 3;
+  for (int64_t kt = 0; kt < KT; ++kt) {
+    // refill the slot released in the previous iteration
+    if (tid == 0 && kt >= 1 && kt - 1 + TMA_STAGES < KT) {
+      const int64_t pk = kt - 1;
+      mbar_wait(&empty[pk % TMA_STAGES], (unsigned)(pk / TMA_STAGES) & 1);
+      issue(pk + TMA_STAGES);
+    }
+    const int s = (int)(kt % TMA_STAGES);
+    mbar_wait(&full[s], (unsigned)(kt / TMA_STAGES) & 1);
+    const double* sa = smem + s * STAGE_DOUBLES;
+    const double* sb = sa + BM * BK;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = 2 * t4 + h;
+      double2 af[8], bf[4];
+#pragma unroll
+      for (int mb = 0; mb < 8; ++mb)
+        af[mb] = *reinterpret_cast<const double2*>(sa + (wm * 64 + mb * 8 + g) * BK + 2 * (q ^ g));
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb)
+        bf[nb] = *reinterpret_cast<const double2*>(sb + (wn * 32 + nb * 8 + g) * BK + 2 * (q ^ g));
+#pragma unroll
+      for (int mb = 0; mb < 8; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) dmma(acc[mb][nb][0], acc[mb][nb][1], af[mb].x, bf[nb].x);
+#pragma unroll
+      for (int mb = 0; mb < 8; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) dmma(acc[mb][nb][0], acc[mb][nb][1], af[mb].y, bf[nb].y);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ---- epilogue
+  __syncthreads();
+  double* colbest = smem;
+  int* colrow = reinterpret_cast<int*>(smem + 2 * BN);
+  epilogue_store(acc, m, nn, c, ldc, colscale, m0, n0, wm, wn, g, t4, colbest, colrow);
+  __syncthreads();
+  if (tile_colmax && tid < BN) tile_colmax_write(tile_colmax, tm, nn, n0, tid, colbest, colrow);
+}
+
+// Driver entry point for tensor-map encoding (no -lcuda at link time).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2D map of a row-major [rows][kk] FP64 matrix, box BK (k) x 128 (rows).
+bool make_map(CUtensorMap* map, const double* base, int64_t rows, int64_t kk) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)kk, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)kk * 8};
+  const cuuint32_t box[2] = {BK, 128};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+}  // namespace eigb

@@ -62,7 +62,7 @@ void collision_vectors_dev(const Plan& p, const RootRecords& roots, double* coll
                            int* collok, DeviceScratch& ws, cudaStream_t st);
 void build_xt_dev(const Plan& p, const RootRecords& roots, const Columns& cols,
                   const double* colldir, const int* collok, int64_t c0, int64_t c1, double* xt,
-                  double* colscale, int* colsign_mode, cudaStream_t st);
+                  double* colscale, int* colsign_mode, DeviceScratch& ws, cudaStream_t st);
 
 // gemm.cu: C[:, c0:c1] = (A Xt^T) diag(scale) on the DMMA pipe; the
 // epilogue leaves per-(row tile, column) signed maxima in tile_colmax, and
