@@ -67,6 +67,9 @@ int eigmod_b200_stats(const eigmod_b200_ctx* ctx, double* stats8);
 int eigmod_b200_stage_times(eigmod_b200_ctx* ctx, double* ms8, int reset);
 /* Kernels launched by this library since load (all contexts). */
 int64_t eigmod_b200_launch_count(void);
+/* Live FP64 ceilings of the context's device in TFLOP/s: out2[0] DMMA.8x8x4
+ * tensor-pipe loop, out2[1] DFMA loop (roofline denominators). */
+int eigmod_b200_fp64_peaks(eigmod_b200_ctx* ctx, double* out2);
 /* Bytes of device workspace currently held by the context. */
 int64_t eigmod_b200_workspace_bytes(const eigmod_b200_ctx* ctx);
 

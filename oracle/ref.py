@@ -177,3 +177,76 @@ def eval_secular(poles, weights, x, leading=1.0):
     _check(lib().ref_eval_secular(_D(poles), _D(weights), C.c_int64(len(poles)),
                                   C.c_double(leading), C.c_double(x), _D(f), buf, 512), buf)
     return float(f[0])
+
+
+# ---- per-eigenpair sampling of the reference at full size ----------------
+class _Handle:
+    def __init__(self, ptr, free):
+        self.ptr, self._free = ptr, free
+
+    def __del__(self):
+        try:
+            self._free(self.ptr)
+        except Exception:
+            pass
+
+
+def matrix(a):
+    """Persistent eigmod::Matrix copy of a (for repeated ref_gemm_nn calls)."""
+    a = _f64(a)
+    L = lib()
+    L.ref_matrix_new.restype = C.c_void_p
+    L.ref_matrix_free.argtypes = [C.c_void_p]
+    p = L.ref_matrix_new(_D(a), C.c_int64(a.shape[0]), C.c_int64(a.shape[1]))
+    return _Handle(p, L.ref_matrix_free)
+
+
+def gemm_nn(h, b):
+    """kernels::gemm_nn (the reference's Q X, kernels.cpp:32-48) on a handle."""
+    b = _f64(b)
+    rows = None
+    L = lib()
+    L.ref_gemm_nn.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_int64,
+                              C.POINTER(C.c_double), C.c_char_p, C.c_size_t]
+    out = np.empty((b.shape[0] if rows is None else rows, b.shape[1]))
+    buf = C.create_string_buffer(512)
+    _check(L.ref_gemm_nn(h.ptr, _D(b), C.c_int64(b.shape[1]), _D(out), buf, 512), buf)
+    return out
+
+
+def transformed(u, signs):
+    u, signs = _f64(u), _i32(signs)
+    L = lib()
+    L.ref_tu_new.restype = C.c_void_p
+    L.ref_tu_free.argtypes = [C.c_void_p]
+    p = L.ref_tu_new(_D(u), _I(signs), C.c_int64(u.shape[0]), C.c_int64(u.shape[1]))
+    return _Handle(p, L.ref_tu_free)
+
+
+def basis_vector(tu, lam, root):
+    """eigvec.cpp:133-153: null_problem + null_direction + resolvent."""
+    lam = _f64(lam)
+    n = lam.shape[0]
+    L = lib()
+    L.ref_basis_vector.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_int64, C.c_double,
+                                   C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_char_p,
+                                   C.c_size_t]
+    w = np.empty(n)
+    res = np.zeros(1)
+    buf = C.create_string_buffer(512)
+    _check(L.ref_basis_vector(tu.ptr, _D(lam), C.c_int64(n), C.c_double(root), _D(w), _D(res),
+                              buf, 512), buf)
+    return w, float(res[0])
+
+
+def dnc_solve(poles, weights, lo, hi, expected, tol):
+    """rootfind.cpp:89-229 on the bracket (lo, hi) holding `expected` roots."""
+    poles, weights = _f64(poles), _f64(weights)
+    L = lib()
+    out = np.empty(max(1, int(expected)))
+    nr = np.zeros(1, np.int64)
+    buf = C.create_string_buffer(1024)
+    _check(L.ref_dnc_solve(_D(poles), _D(weights), C.c_int64(len(poles)), C.c_double(lo),
+                           C.c_double(hi), C.c_int64(expected), C.c_double(tol), _D(out), _L(nr),
+                           buf, 1024), buf)
+    return out[: int(nr[0])].copy()

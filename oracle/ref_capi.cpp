@@ -16,6 +16,7 @@
 // 0 ok, 1 std::invalid_argument, 2 NumericalError (stage in the message
 // buffer as "[stage] msg"), 4 any other exception.
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -234,6 +235,72 @@ int ref_eval_secular(const double* poles, const double* weights, std::int64_t m,
     const SecularCoefficients c =
         make_secular(Vec(poles, poles + m), Vec(weights, weights + m), leading);
     *f_out = eval_secular(c, x);
+  });
+}
+
+}  // extern "C"
+
+// ---- handles for sampling the reference's per-eigenpair work at full size
+// (bench.py --impl reference): the reference's own kernels on persistent
+// operands, so each timed step only pays for the sampled work.
+extern "C" {
+
+void* ref_matrix_new(const double* data, std::int64_t rows, std::int64_t cols) {
+  return new Matrix(to_matrix(data, rows, cols));
+}
+void ref_matrix_free(void* h) { delete static_cast<Matrix*>(h); }
+
+// C = A * B with the reference's back-transform kernel (kernels.cpp:32-48,
+// called at eigvec.cpp:339). b: A.cols() x bcols, c_out: A.rows() x bcols.
+int ref_gemm_nn(void* a, const double* b, std::int64_t bcols, double* c_out, char* msg,
+                std::size_t len) {
+  return guarded(msg, len, [&] {
+    const Matrix& A = *static_cast<Matrix*>(a);
+    const Matrix B = to_matrix(b, static_cast<std::int64_t>(A.cols()), bcols);
+    const Matrix Cm = kernels::gemm_nn(A, B);
+    std::memcpy(c_out, Cm.data(), sizeof(double) * Cm.rows() * Cm.cols());
+  });
+}
+
+void* ref_tu_new(const double* u, const int* signs, std::int64_t n, std::int64_t k) {
+  return new TransformedUpdate(to_tu(u, signs, n, k));
+}
+void ref_tu_free(void* h) { delete static_cast<TransformedUpdate*>(h); }
+
+// One eigenvector of the reference's assembly (eigvec.cpp:133-153): the
+// null problem M(root) (eigvec.cpp:187-202), its null direction
+// (eigvec.cpp:157-185) and the resolvent w_s = (U beta)_s / (lambda_s - root).
+int ref_basis_vector(void* tu_h, const double* lambda, std::int64_t n, double root, double* w_out,
+                     double* resid_out, char* msg, std::size_t len) {
+  return guarded(msg, len, [&] {
+    const TransformedUpdate& tu = *static_cast<TransformedUpdate*>(tu_h);
+    const Vec lam(lambda, lambda + n);
+    const Matrix m = null_problem(tu, lam, root);
+    const NullDirection nd = null_direction(m);
+    const std::size_t k = tu.rank();
+    double norm2 = 0.0;
+    for (std::int64_t s = 0; s < n; ++s) {
+      double ub = 0.0;
+      for (std::size_t r = 0; r < k; ++r) ub += tu.u(s, r) * nd.direction[r];
+      w_out[s] = ub / (lambda[s] - root);
+      norm2 += w_out[s] * w_out[s];
+    }
+    const double inv = 1.0 / std::sqrt(norm2);
+    for (std::int64_t s = 0; s < n; ++s) w_out[s] *= inv;
+    *resid_out = nd.residual;
+  });
+}
+
+// The reference's bracket solver (rootfind.hpp:35-36 / rootfind.cpp:89-229)
+// on its secular function with the given poles and weights.
+int ref_dnc_solve(const double* poles, const double* weights, std::int64_t m, double lo, double hi,
+                  std::int64_t expected, double tol, double* roots_out, std::int64_t* nroots,
+                  char* msg, std::size_t len) {
+  return guarded(msg, len, [&] {
+    const SecularCoefficients c = make_secular(Vec(poles, poles + m), Vec(weights, weights + m), 1.0);
+    const Vec r = dnc_solve(c, RootBracket{lo, hi, static_cast<long>(expected)}, tol);
+    copy_vec(r, roots_out);
+    *nroots = static_cast<std::int64_t>(r.size());
   });
 }
 

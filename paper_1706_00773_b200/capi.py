@@ -62,6 +62,7 @@ def _declare(lib):
         "eigmod_b200_workspace_bytes": (C.c_int64, [_VP]),
         "eigmod_b200_stage_times": (C.c_int, [_VP, _D, C.c_int]),
         "eigmod_b200_launch_count": (C.c_int64, []),
+        "eigmod_b200_fp64_peaks": (C.c_int, [_VP, _D]),
         "eigmod_b200_transform_update": (C.c_int, [_VP, _D, _D, C.c_int64, C.c_int64, _D]),
         "eigmod_b200_secular_weights": (C.c_int, [_VP, _D, _D, _I32, C.c_int64, C.c_int64, _D]),
         "eigmod_b200_deflate_problem": (C.c_int, [_VP, _D, _D, _I32, C.c_int64, C.c_int64, _D, _D,
@@ -178,6 +179,12 @@ class Context:
         out = {k: float(v) for k, v in zip(keys, s)}
         out["calls"] = int(s[7])
         return out
+
+    def fp64_peaks(self) -> dict:
+        """Live FP64 ceilings (TFLOP/s) of this device: DMMA and DFMA loops."""
+        out = np.zeros(2)
+        self.check(self._l.eigmod_b200_fp64_peaks(self.h, _dp(out)))
+        return {"dmma_tflops": float(out[0]), "dfma_tflops": float(out[1])}
 
     def workspace_bytes(self) -> int:
         return int(self._l.eigmod_b200_workspace_bytes(self.h))

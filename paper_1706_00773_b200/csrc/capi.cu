@@ -394,6 +394,10 @@ int eigmod_b200_stage_times(eigmod_b200_ctx* ctx, double* ms8, int reset) {
 
 int64_t eigmod_b200_launch_count(void) { return eigb::launch_count(); }
 
+int eigmod_b200_fp64_peaks(eigmod_b200_ctx* ctx, double* out2) {
+  return guarded(ctx, [&] { eigb::fp64_peaks_dev(ctx->sms, &out2[0], &out2[1], ctx->ws, ctx->stream); });
+}
+
 int eigmod_b200_padded_rank(int64_t k) { return eigb::padded_rank(k); }
 int eigmod_b200_record_width(int kp) { return kRecHead + kp; }
 

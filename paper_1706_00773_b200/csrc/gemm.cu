@@ -307,3 +307,75 @@ double* tile_colmax_buffer(int64_t n, int64_t ncols, DeviceScratch& ws) {
 }
 
 }  // namespace eigb
+
+// ------------------------------------------------------------ FP64 ceilings
+// Loop kernels that saturate the DMMA tensor pipe and the DFMA pipe; bench.py
+// uses them as the live FP64 roofline denominators (MEASURED_PEAKS.json has
+// no FP64 entry).
+namespace eigb {
+namespace {
+
+__global__ void dmma_peak_kernel(double* out, int iters, double av, double bv) {
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  const double A = av + threadIdx.x, B = bv - threadIdx.x;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma(c[i][0], c[i][1], A, B);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.0) out[threadIdx.x] = s;
+}
+
+__global__ void dfma_peak_kernel(double* out, int iters, double a, double b) {
+  double acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = fma(acc[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += acc[i];
+  if (s == 12345.0) out[threadIdx.x] = s;
+}
+
+}  // namespace
+
+void fp64_peaks_dev(int sms, double* dmma_tflops, double* dfma_tflops, DeviceScratch& ws,
+                    cudaStream_t st) {
+  double* out = ws.get_f64("peak_out", 1024);
+  cudaEvent_t e0, e1;
+  EIGB_CUDA(cudaEventCreate(&e0));
+  EIGB_CUDA(cudaEventCreate(&e1));
+  const int iters = 20000;
+  auto timed = [&](auto launch) {
+    launch();
+    EIGB_LAUNCH_CHECK();
+    float best = 1e30f;
+    for (int r = 0; r < 3; ++r) {
+      EIGB_CUDA(cudaEventRecord(e0, st));
+      launch();
+      EIGB_CUDA(cudaEventRecord(e1, st));
+      EIGB_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      EIGB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      best = std::min(best, ms);
+    }
+    return (double)best;
+  };
+  const int bm = 8 * sms;
+  const double ms_m = timed([&] { dmma_peak_kernel<<<bm, 128, 0, st>>>(out, iters / 4, 1e-3, 2e-3); });
+  *dmma_tflops = 2.0 * 256 * 8 * (iters / 4) * 4.0 * bm / (ms_m * 1e-3) / 1e12;
+  const int bf = 8 * sms;
+  const double ms_f = timed([&] { dfma_peak_kernel<<<bf, 256, 0, st>>>(out, iters, 0.999, 1e-3); });
+  *dfma_tflops = 2.0 * 8 * iters * 256.0 * bf / (ms_f * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
+}  // namespace eigb

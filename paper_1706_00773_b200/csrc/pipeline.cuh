@@ -78,4 +78,8 @@ void sign_rule_dev(const double* tile_colmax, int64_t n, int64_t ncols, const in
 // gpu_launches); incremented by EIGB_LAUNCH_CHECK.
 int64_t launch_count();
 
+// Live FP64 ceilings (TFLOP/s): DMMA.8x8x4 loop and DFMA loop (gemm.cu).
+void fp64_peaks_dev(int sms, double* dmma_tflops, double* dfma_tflops, DeviceScratch& ws,
+                    cudaStream_t st);
+
 }  // namespace eigb
