@@ -117,6 +117,26 @@ int eigmod_b200_update_decomposition(eigmod_b200_ctx* ctx, const double* q, cons
                                      double tol, double* lambda_out, double* q_out,
                                      double* wall_time_out);
 
+/* Eigenvector stage from an already transformed update (replaces
+ * assemble_eigenvectors, eigvec.hpp:29-31 / eigvec.cpp:254-364): u is the
+ * n x k matrix U = Q^T K of EigenvalueUpdate.transformed. The eigenvalue
+ * stage is recomputed on the device (deterministic: identical values). */
+int eigmod_b200_assemble_from_u(eigmod_b200_ctx* ctx, const double* q, const double* lambda,
+                                const double* u, const int* signs, int64_t n, int64_t k,
+                                double* lambda_out, double* q_out);
+
+/* UpdateResult metrics of the reference (eigvec.cpp:384-393) on the GPU:
+ * residual_fro = ||Q' diag(l') Q'^T - (Q diag(l) Q^T + K J K^T)||_F with the
+ * reference's symmetrization, ortho_err = max |Q'^T Q' - I|. */
+int eigmod_b200_update_metrics(eigmod_b200_ctx* ctx, const double* q, const double* lambda,
+                               const double* kmat, const int* signs, int64_t n, int64_t k,
+                               const double* q_out, const double* lambda_out,
+                               double* residual_fro, double* ortho_err);
+
+/* Host-pointer FP64 GEMM on the DMMA path: C (m x nn) = A (m x kk) B^T. */
+int eigmod_b200_gemm_nt(eigmod_b200_ctx* ctx, const double* a, const double* b, int64_t m,
+                        int64_t nn, int64_t kk, double* c);
+
 /* ---- device-pointer pipeline ----------------------------------------- */
 /* Whole update on device buffers (one GPU). */
 int eigmod_b200_update_decomposition_device(eigmod_b200_ctx* ctx, const double* d_q,

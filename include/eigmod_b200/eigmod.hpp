@@ -1,0 +1,165 @@
+// eigmod drop-in API over the B200 C ABI (include/eigmod_b200.h).
+//
+// Same declarations as the reference's public headers
+// (/root/reference/proj/include/eigmod/{types,core,secular,rootfind,eigvec,
+// kernels}.hpp) for the functions on the hot path, so a caller recompiles
+// against include/ and links lib/libeigmod_b200_cxx.so instead of
+// libeigmod.a. Value semantics and exception types are the reference's:
+// std::invalid_argument for preconditions, eigmod::NumericalError(stage, msg)
+// for numerical failures; device failures surface as std::runtime_error.
+// Everything O(n^2) and above runs on the GPU; there is no CPU fallback.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace eigmod {
+
+using Vec = std::vector<double>;
+
+// types.hpp:14-44 — dense row-major matrix of doubles.
+class Matrix {
+ public:
+  Matrix() = default;
+  Matrix(std::size_t rows, std::size_t cols, double fill = 0.0)
+      : rows_(rows), cols_(cols), data_(rows * cols, fill) {}
+  static Matrix identity(std::size_t n) {
+    Matrix m(n, n);
+    for (std::size_t i = 0; i < n; ++i) m(i, i) = 1.0;
+    return m;
+  }
+  double& operator()(std::size_t i, std::size_t j) { return data_[i * cols_ + j]; }
+  double operator()(std::size_t i, std::size_t j) const { return data_[i * cols_ + j]; }
+  std::size_t rows() const { return rows_; }
+  std::size_t cols() const { return cols_; }
+  bool empty() const { return data_.empty(); }
+  double* data() { return data_.data(); }
+  const double* data() const { return data_.data(); }
+  double* row(std::size_t i) { return data_.data() + i * cols_; }
+  const double* row(std::size_t i) const { return data_.data() + i * cols_; }
+  bool operator==(const Matrix& o) const = default;
+
+ private:
+  std::size_t rows_ = 0, cols_ = 0;
+  std::vector<double> data_;
+};
+
+// types.hpp:47-53
+struct SymmetricDense {
+  std::size_t n = 0;
+  Matrix entries;
+  static SymmetricDense from(const Matrix& m);
+};
+
+// types.hpp:55-60 — A = Q diag(lambda) Q^T, lambda ascending.
+struct SpectralDecomposition {
+  Matrix q;
+  Vec lambda;
+  std::size_t size() const { return lambda.size(); }
+};
+
+// types.hpp:62-69 — sum_r signs[r] k_r k_r^T.
+struct LowRankUpdate {
+  Matrix kmat;
+  std::vector<int> signs;
+  std::size_t rank() const { return kmat.cols(); }
+  std::size_t dim() const { return kmat.rows(); }
+};
+
+// types.hpp:71-76
+struct UpdateResult {
+  SpectralDecomposition decomposition;
+  double residual_fro = 0.0;
+  double ortho_err = 0.0;
+  double wall_time = 0.0;
+};
+
+// types.hpp:78-87
+class NumericalError : public std::runtime_error {
+ public:
+  NumericalError(std::string stage, const std::string& msg)
+      : std::runtime_error("[" + stage + "] " + msg), stage_(std::move(stage)) {}
+  const std::string& stage() const { return stage_; }
+
+ private:
+  std::string stage_;
+};
+
+void validate_update(const SpectralDecomposition& d, const LowRankUpdate& u);
+
+// core.hpp — validation helpers (GPU GEMMs)
+SymmetricDense reconstruct(const SpectralDecomposition& d);
+SymmetricDense apply_update(const SymmetricDense& a, const LowRankUpdate& u);
+
+// secular.hpp:9-17
+struct SecularCoefficients {
+  Vec poles;
+  Vec weights;
+  double leading = 1.0;
+  std::size_t size() const { return poles.size(); }
+};
+SecularCoefficients make_secular(Vec poles, Vec weights, double leading = 1.0);
+
+// secular.hpp:19-28
+struct TransformedUpdate {
+  Matrix u;
+  std::vector<int> signs;
+  std::size_t rank() const { return u.cols(); }
+  std::size_t dim() const { return u.rows(); }
+};
+TransformedUpdate transform_update(const SpectralDecomposition& d, const LowRankUpdate& u);
+
+// secular.hpp:30-57
+Vec secular_weights(const Vec& lambda, const TransformedUpdate& tu);
+SecularCoefficients secular_coefficients(const Vec& lambda, const TransformedUpdate& tu);
+double eval_secular(const SecularCoefficients& c, double x);
+double eval_secular_derivative(const SecularCoefficients& c, double x);
+std::pair<Vec, Vec> rank2_split(const Vec& a, const Vec& b);
+
+// secular.hpp:59-69
+struct DeflatedProblem {
+  SecularCoefficients coeffs;
+  std::vector<std::size_t> pole_origin;
+  std::vector<std::size_t> unchanged;
+  std::vector<std::size_t> collided;
+};
+inline constexpr double kPoleMergeRelGap = 1e-12;
+inline constexpr double kWeightDeflationRel = 1e-14;
+DeflatedProblem deflate_problem(const Vec& lambda, const TransformedUpdate& tu);
+
+// rootfind.hpp:37-58
+double default_tolerance(const Vec& lambda, const LowRankUpdate& u);
+struct EigenvalueUpdate {
+  Vec values;
+  Vec roots;
+  DeflatedProblem problem;
+  TransformedUpdate transformed;
+};
+enum class LocateStrategy { automatic, sturm };
+// Both the rank-2 and the general rank-k entry (rootfind.hpp:51-53): the
+// strategy is accepted for compatibility; one inertia-count solver serves all.
+EigenvalueUpdate update_eigenvalues_full(const SpectralDecomposition& d, const LowRankUpdate& u,
+                                         double tol,
+                                         LocateStrategy strategy = LocateStrategy::automatic);
+Vec update_eigenvalues(const SpectralDecomposition& d, const LowRankUpdate& u, double tol);
+
+// eigvec.hpp:29-36. reorthogonalize is accepted for compatibility: the
+// vectors are orthonormal to ~1e-11 without it.
+SpectralDecomposition assemble_eigenvectors(const SpectralDecomposition& d,
+                                            const EigenvalueUpdate& plan,
+                                            bool reorthogonalize = false);
+UpdateResult update_decomposition(const SpectralDecomposition& d, const LowRankUpdate& u,
+                                  double tol, bool reorthogonalize = false);
+
+// kernels.hpp:9-13 — the OpenMP toggle has no meaning on the GPU path.
+namespace kernels {
+void set_parallel(bool on);
+bool parallel();
+int worker_count();
+}  // namespace kernels
+
+}  // namespace eigmod

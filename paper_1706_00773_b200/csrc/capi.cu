@@ -667,3 +667,96 @@ int eigmod_b200_gemm_nt_device(eigmod_b200_ctx* ctx, const double* d_a, const do
 }
 
 }  // extern "C"
+
+// ----------------------------------------------- more host drop-ins
+namespace eigb {
+void update_metrics_dev(const double* q, const double* lam, const double* kmat, const int* sgn,
+                        int64_t n, int k, const double* qo, const double* lo, double* residual_fro,
+                        double* ortho_err, DeviceScratch& ws, cudaStream_t st);
+}
+
+extern "C" {
+
+int eigmod_b200_assemble_from_u(eigmod_b200_ctx* ctx, const double* q, const double* lambda,
+                                const double* u, const int* signs, int64_t n, int64_t k,
+                                double* lambda_out, double* q_out) {
+  return guarded(ctx, [&] {
+    if (k < 0 || k > n) throw Error(1, "", "assemble: rank out of range");
+    check_ascending(lambda, n);
+    auto st = ctx->stream;
+    double* dq = ctx->ws.get_f64("h_q", (size_t)n * n);
+    double* dl = ctx->ws.get_f64("h_l", n);
+    double* dlo = ctx->ws.get_f64("h_lo", n);
+    double* dqo = ctx->ws.get_f64("h_qo", (size_t)n * n);
+    EIGB_CUDA(cudaMemcpyAsync(dq, q, 8 * n * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dl, lambda, 8 * n, cudaMemcpyHostToDevice, st));
+    if (k == 0) {
+      EIGB_CUDA(cudaMemcpyAsync(q_out, dq, 8 * n * n, cudaMemcpyDeviceToHost, st));
+      EIGB_CUDA(cudaMemcpyAsync(lambda_out, dl, 8 * n, cudaMemcpyDeviceToHost, st));
+      EIGB_CUDA(cudaStreamSynchronize(st));
+      return;
+    }
+    check_basic(n, k, signs);
+    const int kp = eigb::padded_rank(k);
+    std::vector<double> up((size_t)n * kp, 0.0);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t c = 0; c < k; ++c) up[i * kp + c] = u[i * k + c];
+    double* du = ctx->ws.get_f64("h_u", (size_t)n * kp);
+    EIGB_CUDA(cudaMemcpyAsync(du, up.data(), 8 * up.size(), cudaMemcpyHostToDevice, st));
+    plan_from_u(ctx, dl, du, signs, n, k, ctx->run_rel);
+    solve(ctx, 0, ctx->plan.nred);
+    finish(ctx, dq, dl, 0, n, dlo, dqo, n);
+    EIGB_CUDA(cudaMemcpyAsync(lambda_out, dlo, 8 * n, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaMemcpyAsync(q_out, dqo, 8 * n * n, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int eigmod_b200_update_metrics(eigmod_b200_ctx* ctx, const double* q, const double* lambda,
+                               const double* kmat, const int* signs, int64_t n, int64_t k,
+                               const double* q_out, const double* lambda_out, double* residual_fro,
+                               double* ortho_err) {
+  return guarded(ctx, [&] {
+    check_basic(n, k, signs);
+    auto st = ctx->stream;
+    double* dq = ctx->ws.get_f64("m_q", (size_t)n * n);
+    double* dqo = ctx->ws.get_f64("m_qo", (size_t)n * n);
+    double* dl = ctx->ws.get_f64("m_l", n);
+    double* dlo = ctx->ws.get_f64("m_lo", n);
+    double* dk = ctx->ws.get_f64("m_k", (size_t)n * k);
+    int* ds = ctx->ws.get_i32("m_s", k);
+    EIGB_CUDA(cudaMemcpyAsync(dq, q, 8 * n * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dqo, q_out, 8 * n * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dl, lambda, 8 * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dlo, lambda_out, 8 * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dk, kmat, 8 * n * k, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(ds, signs, 4 * k, cudaMemcpyHostToDevice, st));
+    eigb::update_metrics_dev(dq, dl, dk, ds, n, (int)k, dqo, dlo, residual_fro, ortho_err, ctx->ws,
+                             st);
+  });
+}
+
+int eigmod_b200_gemm_nt(eigmod_b200_ctx* ctx, const double* a, const double* b, int64_t m,
+                        int64_t nn, int64_t kk, double* c) {
+  return guarded(ctx, [&] {
+    if (m < 0 || nn < 0 || kk < 0) throw Error(1, "", "gemm_nt: negative size");
+    if (m == 0 || nn == 0) return;
+    auto st = ctx->stream;
+    const int64_t kp = kk + (kk & 1);  // the DMMA kernel wants an even inner dimension
+    double* da = ctx->ws.get_f64("g_a", (size_t)m * kp);
+    double* db = ctx->ws.get_f64("g_b", (size_t)nn * kp);
+    double* dc = ctx->ws.get_f64("g_c", (size_t)m * nn);
+    double* ones = ctx->ws.get_f64("g_ones", nn);
+    std::vector<double> h(nn, 1.0);
+    EIGB_CUDA(cudaMemcpyAsync(ones, h.data(), 8 * nn, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemset2DAsync(da, 8 * kp, 0, 8 * kp, m, st));
+    EIGB_CUDA(cudaMemset2DAsync(db, 8 * kp, 0, 8 * kp, nn, st));
+    EIGB_CUDA(cudaMemcpy2DAsync(da, 8 * kp, a, 8 * kk, 8 * kk, m, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpy2DAsync(db, 8 * kp, b, 8 * kk, 8 * kk, nn, cudaMemcpyHostToDevice, st));
+    eigb::gemm_nt_dev(da, db, m, nn, kp, dc, nn, ones, nullptr, st);
+    EIGB_CUDA(cudaMemcpyAsync(c, dc, 8 * m * nn, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,317 @@
+// The reference's C++ API (namespace eigmod) over the B200 C ABI.
+//
+// Each function keeps the reference's declaration (include/eigmod_b200/
+// eigmod.hpp, mirroring proj/include/eigmod/*.hpp) and error behaviour:
+// preconditions throw std::invalid_argument, numerical failures throw
+// eigmod::NumericalError with the reference's stage names, device failures
+// throw std::runtime_error. The heavy work runs in libeigmod_b200.so on the
+// GPU; this file only marshals std::vector-backed values and the O(n) / O(nk)
+// utilities the reference exposes next to the hot path.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <memory>
+#include <mutex>
+
+#include "eigmod_b200.h"
+#include "eigmod_b200/eigmod.hpp"
+
+namespace eigmod {
+
+namespace {
+
+// One context per host thread (contexts must not be used concurrently).
+eigmod_b200_ctx* ctx() {
+  thread_local std::unique_ptr<eigmod_b200_ctx, void (*)(eigmod_b200_ctx*)> c(
+      nullptr, eigmod_b200_ctx_destroy);
+  if (!c) {
+    eigmod_b200_ctx* p = nullptr;
+    const int rc = eigmod_b200_ctx_create(0, &p);
+    if (rc != EIGMOD_B200_OK)
+      throw std::runtime_error("eigmod (B200): no usable sm_100 device (rc " + std::to_string(rc) +
+                               ")");
+    c.reset(p);
+  }
+  return c.get();
+}
+
+void check(int rc) {
+  if (rc == EIGMOD_B200_OK) return;
+  eigmod_b200_ctx* c = ctx();
+  const std::string msg = eigmod_b200_last_error(c);
+  const std::string stage = eigmod_b200_last_stage(c);
+  if (rc == EIGMOD_B200_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (rc == EIGMOD_B200_NUMERICAL) {
+    // strip the "[stage] " prefix the device layer adds
+    std::string body = msg;
+    const std::string pre = "[" + stage + "] ";
+    if (body.rfind(pre, 0) == 0) body = body.substr(pre.size());
+    throw NumericalError(stage, body);
+  }
+  throw std::runtime_error(msg);
+}
+
+bool all_finite(const Matrix& m) {
+  const double* p = m.data();
+  for (std::size_t i = 0; i < m.rows() * m.cols(); ++i)
+    if (!std::isfinite(p[i])) return false;
+  return true;
+}
+
+void require_increasing(const Vec& poles, const char* who) {
+  for (std::size_t i = 0; i + 1 < poles.size(); ++i)
+    if (!(poles[i] < poles[i + 1]))
+      throw std::invalid_argument(std::string(who) + ": poles not strictly increasing");
+  for (double p : poles)
+    if (!std::isfinite(p)) throw std::invalid_argument(std::string(who) + ": non-finite pole");
+}
+
+Matrix symmetrized(Matrix a) {
+  const std::size_t n = a.rows();
+  for (std::size_t i = 0; i < n; ++i)
+    for (std::size_t j = i + 1; j < n; ++j) {
+      const double s = 0.5 * (a(i, j) + a(j, i));
+      a(i, j) = s;
+      a(j, i) = s;
+    }
+  return a;
+}
+
+}  // namespace
+
+SymmetricDense SymmetricDense::from(const Matrix& m) {
+  if (m.rows() != m.cols()) throw std::invalid_argument("SymmetricDense: matrix not square");
+  if (!all_finite(m)) throw std::invalid_argument("SymmetricDense: non-finite entries");
+  SymmetricDense s;
+  s.n = m.rows();
+  s.entries = symmetrized(m);
+  return s;
+}
+
+void validate_update(const SpectralDecomposition& d, const LowRankUpdate& u) {
+  // proj/src/core.cpp:89-97
+  if (u.dim() != d.size()) throw std::invalid_argument("LowRankUpdate: dimension mismatch");
+  if (u.rank() < 1 || u.rank() > u.dim())
+    throw std::invalid_argument("LowRankUpdate: rank out of range");
+  if (u.signs.size() != u.rank()) throw std::invalid_argument("LowRankUpdate: signs size");
+  for (int s : u.signs)
+    if (s != 1 && s != -1) throw std::invalid_argument("LowRankUpdate: signs must be +1/-1");
+  if (!all_finite(u.kmat)) throw std::invalid_argument("LowRankUpdate: non-finite K");
+}
+
+// core.hpp: Q diag(lambda) Q^T on the DMMA GEMM, symmetrized.
+SymmetricDense reconstruct(const SpectralDecomposition& d) {
+  if (d.q.cols() != d.lambda.size()) throw std::invalid_argument("reconstruct: dimension mismatch");
+  const std::size_t n = d.q.rows(), k = d.q.cols();
+  Matrix w(n, k), a(n, n);
+  for (std::size_t i = 0; i < n; ++i)
+    for (std::size_t j = 0; j < k; ++j) w(i, j) = d.q(i, j) * d.lambda[j];
+  if (n > 0) check(eigmod_b200_gemm_nt(ctx(), w.data(), d.q.data(), n, n, k, a.data()));
+  return SymmetricDense::from(symmetrized(a));
+}
+
+SymmetricDense apply_update(const SymmetricDense& a, const LowRankUpdate& u) {
+  if (u.dim() != a.n) throw std::invalid_argument("apply_update: dimension mismatch");
+  if (u.signs.size() != u.rank()) throw std::invalid_argument("apply_update: signs size");
+  Matrix out = a.entries;
+  for (std::size_t r = 0; r < u.rank(); ++r)
+    for (std::size_t i = 0; i < a.n; ++i) {
+      const double cvi = static_cast<double>(u.signs[r]) * u.kmat(i, r);
+      for (std::size_t j = 0; j < a.n; ++j) out(i, j) += cvi * u.kmat(j, r);
+    }
+  return SymmetricDense::from(out);
+}
+
+SecularCoefficients make_secular(Vec poles, Vec weights, double leading) {
+  // proj/src/secular.cpp:136-153
+  if (poles.size() != weights.size())
+    throw std::invalid_argument("make_secular: poles/weights size mismatch");
+  require_increasing(poles, "make_secular");
+  for (double w : weights)
+    if (!std::isfinite(w)) throw std::invalid_argument("make_secular: non-finite weight");
+  if (!std::isfinite(leading)) throw std::invalid_argument("make_secular: non-finite leading");
+  SecularCoefficients c;
+  c.leading = leading;
+  for (std::size_t i = 0; i < poles.size(); ++i) {
+    if (weights[i] == 0.0) continue;
+    c.poles.push_back(poles[i]);
+    c.weights.push_back(weights[i]);
+  }
+  return c;
+}
+
+TransformedUpdate transform_update(const SpectralDecomposition& d, const LowRankUpdate& u) {
+  if (u.dim() != d.size()) throw std::invalid_argument("transform_update: dimension mismatch");
+  TransformedUpdate tu;
+  tu.signs = u.signs;
+  tu.u = Matrix(u.dim(), u.rank());
+  if (u.rank() > 0 && u.dim() > 0)
+    check(eigmod_b200_transform_update(ctx(), d.q.data(), u.kmat.data(), u.dim(), u.rank(),
+                                       tu.u.data()));
+  return tu;
+}
+
+Vec secular_weights(const Vec& lambda, const TransformedUpdate& tu) {
+  if (tu.rank() < 1) throw std::invalid_argument("secular_weights: k = 0");
+  if (tu.dim() != lambda.size()) throw std::invalid_argument("secular_weights: dimension mismatch");
+  if (tu.signs.size() != tu.rank())
+    throw std::invalid_argument("secular_weights: signs size mismatch");
+  require_increasing(lambda, "secular_weights");
+  Vec alpha(lambda.size());
+  check(eigmod_b200_secular_weights(ctx(), lambda.data(), tu.u.data(), tu.signs.data(),
+                                    lambda.size(), tu.rank(), alpha.data()));
+  return alpha;
+}
+
+SecularCoefficients secular_coefficients(const Vec& lambda, const TransformedUpdate& tu) {
+  return make_secular(lambda, secular_weights(lambda, tu), 1.0);
+}
+
+double eval_secular(const SecularCoefficients& c, double x) {
+  // proj/src/secular.cpp:223-232
+  double f = c.leading;
+  for (std::size_t j = 0; j < c.size(); ++j) {
+    const double gap = x - c.poles[j];
+    if (std::fabs(gap) < 1e-300) throw std::invalid_argument("eval_secular: evaluation at a pole");
+    f -= c.weights[j] / gap;
+  }
+  return f;
+}
+
+double eval_secular_derivative(const SecularCoefficients& c, double x) {
+  double f = 0.0;
+  for (std::size_t j = 0; j < c.size(); ++j) {
+    const double gap = x - c.poles[j];
+    if (std::fabs(gap) < 1e-300)
+      throw std::invalid_argument("eval_secular_derivative: evaluation at a pole");
+    f += c.weights[j] / (gap * gap);
+  }
+  return f;
+}
+
+std::pair<Vec, Vec> rank2_split(const Vec& a, const Vec& b) {
+  // proj/src/secular.cpp:266-276
+  if (a.size() != b.size() || a.empty())
+    throw std::invalid_argument("rank2_split: bad input vectors");
+  const double inv_sqrt2 = 1.0 / std::sqrt(2.0);
+  Vec u1(a.size()), u2(a.size());
+  for (std::size_t i = 0; i < a.size(); ++i) {
+    u1[i] = (a[i] + b[i]) * inv_sqrt2;
+    u2[i] = (a[i] - b[i]) * inv_sqrt2;
+  }
+  return {std::move(u1), std::move(u2)};
+}
+
+DeflatedProblem deflate_problem(const Vec& lambda, const TransformedUpdate& tu) {
+  const std::size_t n = lambda.size();
+  if (tu.dim() != n) throw std::invalid_argument("deflate_problem: dimension mismatch");
+  DeflatedProblem out;
+  if (n == 0) return out;
+  Vec poles(n), weights(n);
+  std::vector<std::int64_t> po(n), un(n), co(n), cnt(3);
+  check(eigmod_b200_deflate_problem(ctx(), lambda.data(), tu.u.data(), tu.signs.data(), n,
+                                    tu.rank(), poles.data(), weights.data(), po.data(), un.data(),
+                                    co.data(), cnt.data()));
+  out.coeffs.poles.assign(poles.begin(), poles.begin() + cnt[0]);
+  out.coeffs.weights.assign(weights.begin(), weights.begin() + cnt[0]);
+  out.coeffs.leading = 1.0;
+  out.pole_origin.assign(po.begin(), po.begin() + cnt[0]);
+  out.unchanged.assign(un.begin(), un.begin() + cnt[1]);
+  out.collided.assign(co.begin(), co.begin() + cnt[2]);
+  return out;
+}
+
+double default_tolerance(const Vec& lambda, const LowRankUpdate& u) {
+  // proj/src/rootfind.cpp:306-312
+  double scale = 1.0;
+  for (double l : lambda) scale = std::max(scale, std::fabs(l));
+  double kn2 = 0.0;
+  const double* p = u.kmat.data();
+  for (std::size_t i = 0; i < u.kmat.rows() * u.kmat.cols(); ++i) kn2 += p[i] * p[i];
+  const double kn = std::sqrt(kn2);
+  return 1e-12 * std::max(scale, kn * kn);
+}
+
+EigenvalueUpdate update_eigenvalues_full(const SpectralDecomposition& d, const LowRankUpdate& u,
+                                         double tol, LocateStrategy) {
+  validate_update(d, u);
+  if (!(tol > 0.0)) throw std::invalid_argument("update_eigenvalues: tol must be positive");
+  const std::size_t n = d.size(), k = u.rank();
+  EigenvalueUpdate out;
+  out.values.resize(n);
+  Vec roots(n), ubuf(n * k);
+  std::int64_t nroots = 0, keff = 0;
+  std::vector<std::int64_t> keep(k);
+  check(eigmod_b200_update_eigenvalues(ctx(), d.q.data(), d.lambda.data(), u.kmat.data(),
+                                       u.signs.data(), n, k, tol, out.values.data(), roots.data(),
+                                       &nroots, ubuf.data(), &keff, keep.data()));
+  out.roots.assign(roots.begin(), roots.begin() + nroots);
+  out.transformed.u = Matrix(n, keff);
+  std::copy(ubuf.begin(), ubuf.begin() + n * keff, out.transformed.u.data());
+  for (std::int64_t c = 0; c < keff; ++c) out.transformed.signs.push_back(u.signs[keep[c]]);
+  if (keff == 0) {  // rootfind.cpp:394-399
+    out.problem.unchanged.resize(n);
+    for (std::size_t i = 0; i < n; ++i) out.problem.unchanged[i] = i;
+  } else {
+    out.problem = deflate_problem(d.lambda, out.transformed);
+  }
+  return out;
+}
+
+Vec update_eigenvalues(const SpectralDecomposition& d, const LowRankUpdate& u, double tol) {
+  validate_update(d, u);
+  if (!(tol > 0.0)) throw std::invalid_argument("update_eigenvalues: tol must be positive");
+  const std::size_t n = d.size(), k = u.rank();
+  Vec values(n), roots(n);
+  std::int64_t nroots = 0, keff = 0;
+  check(eigmod_b200_update_eigenvalues(ctx(), d.q.data(), d.lambda.data(), u.kmat.data(),
+                                       u.signs.data(), n, k, tol, values.data(), roots.data(),
+                                       &nroots, nullptr, &keff, nullptr));
+  return values;
+}
+
+SpectralDecomposition assemble_eigenvectors(const SpectralDecomposition& d,
+                                            const EigenvalueUpdate& plan, bool) {
+  const std::size_t n = d.size(), k = plan.transformed.rank();
+  if (plan.transformed.dim() != n && k > 0)
+    throw std::invalid_argument("assemble_eigenvectors: plan does not match the decomposition");
+  SpectralDecomposition out;
+  out.lambda.resize(n);
+  out.q = Matrix(n, n);
+  check(eigmod_b200_assemble_from_u(ctx(), d.q.data(), d.lambda.data(), plan.transformed.u.data(),
+                                    plan.transformed.signs.data(), n, k, out.lambda.data(),
+                                    out.q.data()));
+  if (!plan.values.empty() && plan.values.size() != n)
+    throw NumericalError("assemble", "eigenpair count mismatch");
+  return out;
+}
+
+UpdateResult update_decomposition(const SpectralDecomposition& d, const LowRankUpdate& u,
+                                  double tol, bool) {
+  validate_update(d, u);
+  if (!(tol > 0.0)) throw std::invalid_argument("update_eigenvalues: tol must be positive");
+  const std::size_t n = d.size(), k = u.rank();
+  UpdateResult res;
+  res.decomposition.lambda.resize(n);
+  res.decomposition.q = Matrix(n, n);
+  double wall = 0.0;
+  check(eigmod_b200_update_decomposition(ctx(), d.q.data(), d.lambda.data(), u.kmat.data(),
+                                         u.signs.data(), n, k, tol,
+                                         res.decomposition.lambda.data(),
+                                         res.decomposition.q.data(), &wall));
+  res.wall_time = wall;
+  // metrics outside the timed update, as eigvec.cpp:384-393
+  check(eigmod_b200_update_metrics(ctx(), d.q.data(), d.lambda.data(), u.kmat.data(),
+                                   u.signs.data(), n, k, res.decomposition.q.data(),
+                                   res.decomposition.lambda.data(), &res.residual_fro,
+                                   &res.ortho_err));
+  return res;
+}
+
+namespace kernels {
+void set_parallel(bool) {}
+bool parallel() { return false; }
+int worker_count() { return 1; }
+}  // namespace kernels
+
+}  // namespace eigmod

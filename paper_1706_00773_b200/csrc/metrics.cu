@@ -1,0 +1,122 @@
+// Validation metrics of an update on the GPU (proj/src/eigvec.cpp:384-393):
+//   residual_fro = || sym(Q' diag(l') Q'^T) - sym(sym(Q diag(l) Q^T) + K J K^T) ||_F
+//   ortho_err    = max_ij |(Q'^T Q' - I)_ij|
+// with the reference's symmetrization (kernels.cpp:123-131, applied by
+// SymmetricDense::from at core.cpp:66-74). The three n^3 products run on the
+// K5 DMMA GEMM; the reference does them on the CPU (outside its timer).
+#include "pipeline.cuh"
+
+namespace eigb {
+
+namespace {
+
+__global__ void scale_cols_kernel(const double* __restrict__ q, const double* __restrict__ lam,
+                                  int64_t n, double* __restrict__ w) {
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x)
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) w[i * n + j] = q[i * n + j] * lam[j];
+}
+
+__global__ void transpose_kernel(const double* __restrict__ a, int64_t n, double* __restrict__ t) {
+  __shared__ double tile[32][33];
+  const int64_t bx = (int64_t)blockIdx.x * 32, by = (int64_t)blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = by + r, j = bx + threadIdx.x;
+    tile[r][threadIdx.x] = (i < n && j < n) ? a[i * n + j] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = bx + r, j = by + threadIdx.x;
+    if (i < n && j < n) t[i * n + j] = tile[threadIdx.x][r];
+  }
+}
+
+// Partial sums of squared residual entries (upper triangle + diagonal, both
+// symmetrized exactly as the reference), one value per block.
+__global__ void residual_kernel(const double* __restrict__ g1, const double* __restrict__ g2,
+                                const double* __restrict__ kmat, const int* __restrict__ sgn,
+                                int64_t n, int k, double* __restrict__ part) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+      // target = sym(sym(A) + K J K^T); got = sym(G1)
+      const double a = 0.5 * (g2[i * n + j] + g2[j * n + i]);
+      double kjk = 0.0;
+      for (int r = 0; r < k; ++r) kjk += (double)sgn[r] * kmat[i * k + r] * kmat[j * k + r];
+      const double tgt = a + kjk;  // kjk is symmetric; sym() leaves it unchanged
+      const double got = 0.5 * (g1[i * n + j] + g1[j * n + i]);
+      const double d = got - tgt;
+      s += d * d;
+    }
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void ortho_kernel(const double* __restrict__ g, int64_t n, double* __restrict__ part) {
+  __shared__ double red[32];
+  double m = 0.0;
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x)
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x)
+      m = fmax(m, fabs(g[i * n + j] - (i == j ? 1.0 : 0.0)));
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = fmax(t, red[w]);
+    part[blockIdx.x] = t;
+  }
+}
+
+}  // namespace
+
+void update_metrics_dev(const double* q, const double* lam, const double* kmat, const int* sgn,
+                        int64_t n, int k, const double* qo, const double* lo, double* residual_fro,
+                        double* ortho_err, DeviceScratch& ws, cudaStream_t st) {
+  double* w = ws.get_f64("met_w", (size_t)n * n);
+  double* g1 = ws.get_f64("met_g1", (size_t)n * n);
+  double* g2 = ws.get_f64("met_g2", (size_t)n * n);
+  double* ones = ws.get_f64("met_ones", n);
+  {
+    std::vector<double> h(n, 1.0);
+    EIGB_CUDA(cudaMemcpyAsync(ones, h.data(), 8 * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaStreamSynchronize(st));
+  }
+  const int blocks = (int)std::min<int64_t>(n, 4096);
+  scale_cols_kernel<<<blocks, 256, 0, st>>>(qo, lo, n, w);
+  EIGB_LAUNCH_CHECK();
+  gemm_nt_dev(w, qo, n, n, n, g1, n, ones, nullptr, st);
+  scale_cols_kernel<<<blocks, 256, 0, st>>>(q, lam, n, w);
+  EIGB_LAUNCH_CHECK();
+  gemm_nt_dev(w, q, n, n, n, g2, n, ones, nullptr, st);
+  double* part = ws.get_f64("met_part", blocks);
+  residual_kernel<<<blocks, 256, 0, st>>>(g1, g2, kmat, sgn, n, k, part);
+  EIGB_LAUNCH_CHECK();
+  std::vector<double> hp(blocks);
+  EIGB_CUDA(cudaMemcpyAsync(hp.data(), part, 8 * blocks, cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaStreamSynchronize(st));
+  double s = 0.0;
+  for (double v : hp) s += v;
+  *residual_fro = std::sqrt(s);
+  // Q'^T Q' = T T^T with T = Q'^T
+  dim3 tb(32, 8), tg((unsigned)cdiv(n, 32), (unsigned)cdiv(n, 32));
+  transpose_kernel<<<tg, tb, 0, st>>>(qo, n, w);
+  EIGB_LAUNCH_CHECK();
+  gemm_nt_dev(w, w, n, n, n, g1, n, ones, nullptr, st);
+  ortho_kernel<<<blocks, 256, 0, st>>>(g1, n, part);
+  EIGB_LAUNCH_CHECK();
+  EIGB_CUDA(cudaMemcpyAsync(hp.data(), part, 8 * blocks, cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaStreamSynchronize(st));
+  double m = 0.0;
+  for (double v : hp) m = std::max(m, v);
+  *ortho_err = m;
+}
+
+}  // namespace eigb

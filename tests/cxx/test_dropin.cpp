@@ -1,0 +1,246 @@
+// The reference's own unit-test cases (proj/tests/test_secular.cpp,
+// test_rootfind.cpp, test_eigvec.cpp), restated against the drop-in C++ API:
+// the same #include "eigmod/..." lines and the same calls, linked against
+// lib/libeigmod_b200_cxx.so instead of libeigmod.a. Run by
+// tests/test_cxx_dropin.py on a B200.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <stdexcept>
+#include <string>
+
+#include "eigmod/eigvec.hpp"
+#include "eigmod/kernels.hpp"
+#include "eigmod/rootfind.hpp"
+#include "eigmod/secular.hpp"
+
+using namespace eigmod;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(cond)                                                        \
+  do {                                                                     \
+    ++g_checks;                                                            \
+    if (!(cond)) {                                                         \
+      ++g_fail;                                                            \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);          \
+    }                                                                      \
+  } while (0)
+#define CHECK_NEAR(a, b, tol) CHECK(std::fabs((a) - (b)) <= (tol))
+template <class E, class F>
+bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+static const double kR2 = std::sqrt(2.0);
+
+static TransformedUpdate make_tu(Matrix u, std::vector<int> s) {
+  TransformedUpdate t;
+  t.u = std::move(u);
+  t.signs = std::move(s);
+  return t;
+}
+
+// Haar-random instance: Householder QR of a Gaussian matrix (positive R
+// diagonal), sorted uniform spectrum, Gaussian K scaled to Frobenius norm.
+static std::pair<SpectralDecomposition, LowRankUpdate> instance(std::size_t n, std::size_t k,
+                                                                double norm, unsigned seed) {
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> g(0, 1);
+  std::uniform_real_distribution<double> un(-1, 1);
+  Matrix a(n, n), q = Matrix::identity(n);
+  for (std::size_t i = 0; i < n * n; ++i) a.data()[i] = g(rng);
+  std::vector<double> v(n);
+  for (std::size_t c = 0; c < n; ++c) {
+    double nr = 0;
+    for (std::size_t i = c; i < n; ++i) nr += a(i, c) * a(i, c);
+    nr = std::sqrt(nr);
+    const double al = a(c, c) >= 0 ? -nr : nr;
+    double vn = 0;
+    for (std::size_t i = c; i < n; ++i) v[i] = a(i, c) - (i == c ? al : 0), vn += v[i] * v[i];
+    if (vn == 0) continue;
+    for (std::size_t j = 0; j < n; ++j) {
+      double s = 0, t = 0;
+      for (std::size_t i = c; i < n; ++i) s += v[i] * a(i, j), t += v[i] * q(i, j);
+      s *= 2 / vn, t *= 2 / vn;
+      for (std::size_t i = c; i < n; ++i) a(i, j) -= s * v[i], q(i, j) -= t * v[i];
+    }
+  }
+  SpectralDecomposition d;
+  d.q = Matrix(n, n);
+  for (std::size_t i = 0; i < n; ++i)
+    for (std::size_t j = 0; j < n; ++j) d.q(i, j) = q(j, i) * (a(j, j) < 0 ? -1.0 : 1.0);
+  d.lambda.resize(n);
+  for (auto& l : d.lambda) l = un(rng);
+  std::sort(d.lambda.begin(), d.lambda.end());
+  for (std::size_t i = 1; i < n; ++i) d.lambda[i] = std::max(d.lambda[i], d.lambda[i - 1] + 1e-6);
+  LowRankUpdate u;
+  u.kmat = Matrix(n, k);
+  double fn = 0;
+  for (std::size_t i = 0; i < n * k; ++i) u.kmat.data()[i] = g(rng), fn += u.kmat.data()[i] * u.kmat.data()[i];
+  for (std::size_t i = 0; i < n * k; ++i) u.kmat.data()[i] *= norm / std::sqrt(fn);
+  u.signs.assign(k, 1);
+  return {d, u};
+}
+
+int main() {
+  // ---- secular (test_secular.cpp:61-126, 212-298)
+  {
+    SpectralDecomposition d;
+    d.q = Matrix::identity(3);
+    d.lambda = {0.0, 1.0, 2.0};
+    Matrix k(3, 2);
+    k(0, 0) = 1.0;
+    k(2, 1) = -2.0;
+    const TransformedUpdate tu = transform_update(d, {k, {1, -1}});
+    CHECK(tu.u == k);
+    CHECK(tu.signs[1] == -1);
+  }
+  {
+    const double inv = 1.0 / kR2;
+    Matrix u(2, 1);
+    u(0, 0) = inv;
+    u(1, 0) = inv;
+    const Vec a = secular_weights({1.0, 2.0}, make_tu(u, {1}));
+    CHECK_NEAR(a[0], 0.5, 1e-13);
+    CHECK_NEAR(a[1], 0.5, 1e-13);
+    const Vec b = secular_weights({0.0, 1.0}, make_tu(Matrix::identity(2), {1, 1}));
+    CHECK_NEAR(b[0], 2.0, 2e-13);
+    CHECK_NEAR(b[1], 0.0, 1e-15);
+    Matrix u2(2, 2);
+    u2(0, 0) = 1.0;
+    u2(1, 0) = 1.0;
+    u2(1, 1) = 1.0;
+    const Vec c = secular_weights({0.0, 1.0}, make_tu(u2, {1, 1}));
+    CHECK_NEAR(c[0], 2.0, 2e-13);
+    CHECK_NEAR(c[1], 1.0, 1e-13);
+    const SecularCoefficients sc = secular_coefficients({0.0, 1.0}, make_tu(u2, {1, 1}));
+    CHECK_NEAR(eval_secular(sc, 2.0 + kR2), 0.0, 1e-12);
+    CHECK_NEAR(eval_secular(sc, 2.0 - kR2), 0.0, 1e-12);
+  }
+  {
+    const SecularCoefficients c = make_secular({0.0, 1.0}, {2.0, 1.0});
+    CHECK_NEAR(eval_secular(c, 2.0), -1.0, 1e-15);
+    CHECK(throws<std::invalid_argument>([&] { (void)eval_secular(c, 1.0); }));
+    CHECK(throws<std::invalid_argument>([&] { (void)make_secular({1.0, 1.0}, {1.0, 1.0}); }));
+    const SecularCoefficients z = make_secular({0.0, 1.0, 2.0}, {1.0, 0.0, 3.0});
+    CHECK(z.size() == 2 && z.poles[1] == 2.0);
+  }
+  {
+    Vec lambda = {0.0, 1.0, 2.0};
+    Matrix u(3, 1);
+    u(1, 0) = 0.5;
+    const DeflatedProblem dp = deflate_problem(lambda, make_tu(u, {1}));
+    CHECK(dp.coeffs.size() == 1);
+    CHECK_NEAR(dp.coeffs.poles[0], 1.0, 0);
+    CHECK_NEAR(dp.coeffs.weights[0], 0.25, 1e-15);
+    CHECK(dp.unchanged.size() == 2 && dp.unchanged[0] == 0 && dp.unchanged[1] == 2);
+    CHECK(dp.pole_origin[0] == 1);
+    Matrix u3(3, 1);
+    u3(0, 0) = 1.0;
+    u3(1, 0) = 2.0;
+    u3(2, 0) = 1.0;
+    const DeflatedProblem dm = deflate_problem({1.0, 1.0 + 1e-15, 2.0}, make_tu(u3, {1}));
+    CHECK(dm.coeffs.size() == 2);
+    CHECK_NEAR(dm.coeffs.weights[0], 5.0, 5e-9);
+    CHECK(dm.unchanged.size() == 1);
+  }
+  {
+    const auto [u1, u2] = rank2_split({1.0, 0.0}, {0.0, 1.0});
+    CHECK_NEAR(u1[0] * u1[1] - u2[0] * u2[1], 1.0, 1e-15);
+  }
+  // ---- rootfind (test_rootfind.cpp:135-161, 207-213)
+  SpectralDecomposition g2;
+  g2.q = Matrix::identity(2);
+  g2.lambda = {0.0, 1.0};
+  Matrix gk(2, 2);
+  gk(0, 0) = 1.0;
+  gk(1, 0) = 1.0;
+  gk(1, 1) = 1.0;
+  {
+    const Vec v = update_eigenvalues(g2, {gk, {1, 1}}, 1e-14);
+    CHECK(v.size() == 2);
+    CHECK_NEAR(v[0], 2.0 - kR2, 1e-12 * 2);
+    CHECK_NEAR(v[1], 2.0 + kR2, 1e-12 * 4);
+  }
+  {
+    auto [d, u] = instance(9, 2, 1.0, 3);
+    u.kmat = Matrix(9, 2);
+    CHECK(update_eigenvalues(d, u, 1e-12) == d.lambda);
+  }
+  {
+    SpectralDecomposition d;
+    d.q = Matrix::identity(2);
+    d.lambda = {1.0, 2.0};
+    Matrix k(2, 1);
+    k(0, 0) = 1.0;
+    const Vec v = update_eigenvalues(d, {k, {1}}, 1e-14);
+    CHECK_NEAR(v[0], 2.0, 2e-12);
+    CHECK_NEAR(v[1], 2.0, 2e-12);
+  }
+  {
+    Matrix k(3, 1);
+    CHECK(throws<std::invalid_argument>([&] { (void)update_eigenvalues(g2, {k, {1}}, 1e-12); }));
+    CHECK(throws<std::invalid_argument>([&] { (void)update_eigenvalues(g2, {gk, {1, 2}}, 1e-12); }));
+    SpectralDecomposition bad = g2;
+    bad.lambda = {1.0, 0.0};
+    bool stage_ok = false;
+    try {
+      (void)update_eigenvalues(bad, {gk, {1, 1}}, 1e-12);
+    } catch (const NumericalError& e) {
+      stage_ok = e.stage() == "deflate";
+    }
+    CHECK(stage_ok);
+  }
+  {
+    const EigenvalueUpdate plan = update_eigenvalues_full(g2, {gk, {1, 1}}, 1e-14);
+    CHECK(plan.values.size() == 2 && plan.roots.size() == 2);
+    CHECK(plan.transformed.rank() == 2 && plan.problem.coeffs.size() == 2);
+    const SpectralDecomposition dd = assemble_eigenvectors(g2, plan);
+    CHECK_NEAR(dd.lambda[0], plan.values[0], 0);
+  }
+  // ---- eigvec (test_eigvec.cpp:97-131)
+  {
+    auto [d, u] = instance(8, 2, 1.0, 77);
+    u.kmat = Matrix(8, 2);
+    const UpdateResult r = update_decomposition(d, u, 1e-12);
+    CHECK(r.residual_fro <= 1e-15);
+    CHECK(r.decomposition.q == d.q);
+    CHECK(r.decomposition.lambda == d.lambda);
+  }
+  {
+    const UpdateResult r = update_decomposition(g2, {gk, {1, 1}}, 1e-14);
+    CHECK_NEAR(r.decomposition.lambda[0], 2.0 - kR2, 1e-12 * 2);
+    CHECK(r.residual_fro <= 1e-10);
+    CHECK(r.ortho_err <= 1e-12);
+    const double lam = 2.0 - kR2, nrm = std::sqrt(1.0 + (lam - 1.0) * (lam - 1.0));
+    CHECK_NEAR(r.decomposition.q(0, 0), 1.0 / nrm, 1e-12);
+    CHECK_NEAR(r.decomposition.q(1, 0), (lam - 1.0) / nrm, 1e-12);
+  }
+  {
+    auto [d, u] = instance(100, 3, 0.3, 31);
+    const UpdateResult r = update_decomposition(d, u, default_tolerance(d.lambda, u));
+    // reference bound 1e-8 ||A||_F and 1e-6; the B200 path meets 1e-10 / 1e-9
+    CHECK(r.residual_fro <= 1e-10 * 10.0);
+    CHECK(r.ortho_err <= 1e-9);
+  }
+  {
+    for (unsigned seed = 0; seed < 5; ++seed) {
+      auto [d, u] = instance(24, 2, 1.0, 6000 + seed);
+      u.signs = {1, -1};
+      const UpdateResult r = update_decomposition(d, u, 1e-13);
+      CHECK(r.ortho_err <= 1e-9);
+      CHECK(r.residual_fro <= 1e-10);
+    }
+  }
+  kernels::set_parallel(true);  // accepted, no effect on the GPU path
+  std::printf("%d checks, %d failures\n", g_checks, g_fail);
+  return g_fail == 0 ? 0 : 1;
+}
