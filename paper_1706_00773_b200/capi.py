@@ -71,6 +71,11 @@ def _declare(lib):
                                                      C.c_double, _D, _D, _I64, _D, _I64, _I64]),
         "eigmod_b200_update_decomposition": (C.c_int, [_VP, _D, _D, _D, _I32, C.c_int64,
                                                        C.c_int64, C.c_double, _D, _D, _D]),
+        "eigmod_b200_assemble_from_u": (C.c_int, [_VP, _D, _D, _D, _I32, C.c_int64, C.c_int64, _D,
+                                                  _D]),
+        "eigmod_b200_update_metrics": (C.c_int, [_VP, _D, _D, _D, _I32, C.c_int64, C.c_int64, _D,
+                                                 _D, _D, _D]),
+        "eigmod_b200_gemm_nt": (C.c_int, [_VP, _D, _D, C.c_int64, C.c_int64, C.c_int64, _D]),
         "eigmod_b200_update_decomposition_device": (C.c_int, [_VP, _VP, _VP, _VP, _I32, C.c_int64,
                                                               C.c_int64, _VP, _VP]),
         "eigmod_b200_padded_rank": (C.c_int, [C.c_int64]),
@@ -331,13 +336,12 @@ def update_decomposition(q, lam, kmat, signs, tol, metrics=False,
         ctx.h, _dp(q), _dp(lam), _dp(kmat), signs.ctypes.data_as(_I32), n, k, C.c_double(tol),
         _dp(lo), _dp(qo), _dp(wt)))
     res = UpdateResult(lo, qo, wall_time=float(wt[0]))
-    if metrics:  # eigvec.cpp:384-393 (validation only, outside the timed update)
-        target = q @ np.diag(lam) @ q.T + kmat @ np.diag(signs.astype(float)) @ kmat.T
-        target = 0.5 * (target + target.T)
-        got = qo @ np.diag(lo) @ qo.T
-        got = 0.5 * (got + got.T)
-        res.residual_fro = float(np.linalg.norm(got - target))
-        res.ortho_err = float(np.abs(qo.T @ qo - np.eye(n)).max())
+    if metrics:  # eigvec.cpp:384-393 (validation only, outside the timed update), on the GPU
+        rf, oe = np.zeros(1), np.zeros(1)
+        ctx.check(ctx._l.eigmod_b200_update_metrics(
+            ctx.h, _dp(q), _dp(lam), _dp(kmat), signs.ctypes.data_as(_I32), n, k, _dp(qo),
+            _dp(lo), _dp(rf), _dp(oe)))
+        res.residual_fro, res.ortho_err = float(rf[0]), float(oe[0])
     return res
 
 

@@ -1,0 +1,47 @@
+"""Summarise ncu captures (launch list + full-set reports) into profiles/."""
+import csv, collections, io, json, subprocess, sys
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if 'Kernel Name' in r][0]
+    h = rows[hi]; ki = h.index('Kernel Name'); vi = h.index('Metric Value'); ui = h.index('Metric Unit')
+    agg = collections.OrderedDict()
+    for r in rows[hi + 1:]:
+        if len(r) <= vi: continue
+        v = float(r[vi].replace(',', ''))
+        v = v / 1e6 if r[ui] == 'nsecond' else v / 1e3 if r[ui] == 'usecond' else v
+        name = r[ki].split('(')[0].replace('void ', '')
+        a = agg.setdefault(name, [0.0, 0]); a[0] += v; a[1] += 1
+    return agg
+
+KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
+        'sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active',
+        'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active',
+        'sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active',
+        'sm__throughput.avg.pct_of_peak_sustained_elapsed',
+        'gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed',
+        'dram__throughput.avg.pct_of_peak_sustained_elapsed',
+        'sm__warps_active.avg.pct_of_peak_sustained_active',
+        'launch__registers_per_thread', 'launch__grid_size', 'launch__block_size',
+        'smsp__issue_active.avg.pct_of_peak_sustained_active']
+
+def full(rep):
+    out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, units, v = rows[0], rows[1], rows[-1]
+    d = {'kernel': v[h.index('Kernel Name')][:80]}
+    for k in KEYS:
+        if k in h:
+            d[k] = v[h.index(k)] + (' ' + units[h.index(k)] if units[h.index(k)] else '')
+    return d
+
+if __name__ == '__main__':
+    res = {}
+    if sys.argv[1].endswith('.csv'):
+        agg = launches(sys.argv[1]); tot = sum(a[0] for a in agg.values())
+        res = {k: {'ms': round(v, 4), 'launches': c, 'share': round(v / tot, 4)} for k, (v, c) in
+               sorted(agg.items(), key=lambda x: -x[1][0])}
+    else:
+        for rep in sys.argv[1:]:
+            res[rep] = full(rep)
+    print(json.dumps(res, indent=1))
