@@ -35,6 +35,8 @@ struct eigmod_b200_ctx {
   double run_rel = eigb::kExactRunRelGap;
   eigb::SolveOptions sopt;
   const double* lam = nullptr;  // lambda of the current plan (rank-0 copy)
+  cudaStream_t copy = nullptr;   // D2H stream of the blocked host path
+  std::vector<cudaEvent_t> blk_ev;
   std::string err, stage;
   // per-stage CUDA-event timing (option "timing"): 0 K1 project, 1 K2 plan,
   // 2 K3 solve, 3 K4 columns, 4 K5 GEMM, 5 sign rule
@@ -210,8 +212,13 @@ __global__ void copy_block_kernel(const double* __restrict__ a, int64_t n, int64
     for (int64_t j = threadIdx.x; j < nc; j += blockDim.x) out[i * ldo + j] = a[i * n + c0 + j];
 }
 
+// host_q_out != nullptr (host-pointer entry points): the GEMM and the sign
+// rule run in column blocks and each finished block is copied to the host on
+// a second stream while the next block computes (the D2H of Q' overlaps the
+// back-transform; each block's signs are final when its GEMM ends).
 void finish(eigmod_b200_ctx* c, const double* q, const double* lam_in, int64_t c0, int64_t c1,
-            double* lam_out, double* q_out, int64_t ldq) {
+            double* lam_out, double* q_out, int64_t ldq, double* host_q_out = nullptr,
+            int64_t host_ld = 0) {
   eigb::Plan& p = c->plan;
   const int64_t n = p.n;
   if (!lam_in) lam_in = c->lam;
@@ -240,14 +247,44 @@ void finish(eigmod_b200_ctx* c, const double* q, const double* lam_in, int64_t c
                      c->stream);
   c->mark(4);
   double* tcm = eigb::tile_colmax_buffer(n, nc, c->ws);
-  eigb::gemm_nt_dev(q, xt, n, nc, n, q_out, ldq, colscale, tcm, c->stream);
+  if (!host_q_out) {
+    eigb::gemm_nt_dev(q, xt, n, nc, n, q_out, ldq, colscale, tcm, c->stream);
+    c->mark(5);
+    eigb::sign_rule_dev(tcm, n, nc, cmode, q_out, ldq, c->ws, c->stream);
+    c->mark(6);
+    return;
+  }
+  if (!c->copy) EIGB_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+  const int64_t nb = std::min<int64_t>(8, eigb::cdiv(nc, 128));
+  const int64_t wb = eigb::cdiv(eigb::cdiv(nc, nb), 128) * 128;
+  while ((int64_t)c->blk_ev.size() < nb) {
+    cudaEvent_t e;
+    EIGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->blk_ev.push_back(e);
+  }
+  // all blocks are enqueued before the first copy: a pageable destination
+  // makes cudaMemcpy2DAsync block the host, and the GPU must not wait on that
+  for (int64_t b = 0; b * wb < nc; ++b) {
+    const int64_t a0 = b * wb, w = std::min(wb, nc - a0);
+    double* cb = q_out + a0;
+    eigb::gemm_nt_dev(q, xt + a0 * n, n, w, n, cb, ldq, colscale + a0, tcm, c->stream);
+    eigb::sign_rule_dev(tcm, n, w, cmode + a0, cb, ldq, c->ws, c->stream);
+    EIGB_CUDA(cudaEventRecord(c->blk_ev[b], c->stream));
+  }
+  for (int64_t b = 0; b * wb < nc; ++b) {
+    const int64_t a0 = b * wb, w = std::min(wb, nc - a0);
+    EIGB_CUDA(cudaStreamWaitEvent(c->copy, c->blk_ev[b], 0));
+    EIGB_CUDA(cudaMemcpy2DAsync(host_q_out + (c0 + a0), 8 * host_ld, q_out + a0, 8 * ldq, 8 * w,
+                                n, cudaMemcpyDeviceToHost, c->copy));
+  }
   c->mark(5);
-  eigb::sign_rule_dev(tcm, n, nc, cmode, q_out, ldq, c->ws, c->stream);
   c->mark(6);
+  EIGB_CUDA(cudaStreamSynchronize(c->copy));
 }
 
 void full_device(eigmod_b200_ctx* c, const double* q, const double* lam, const double* kmat,
-                 const int* signs, int64_t n, int64_t k, double* lam_out, double* q_out) {
+                 const int* signs, int64_t n, int64_t k, double* lam_out, double* q_out,
+                 double* host_q_out = nullptr) {
   const int kp = eigb::padded_rank(k);
   double* u = c->ws.get_f64("cap_u_full", (size_t)n * kp);
   c->mark(0);
@@ -257,7 +294,7 @@ void full_device(eigmod_b200_ctx* c, const double* q, const double* lam, const d
   c->mark(2);
   solve(c, 0, c->plan.nred);
   c->mark(3);
-  finish(c, q, lam, 0, n, lam_out, q_out, n);
+  finish(c, q, lam, 0, n, lam_out, q_out, n, host_q_out, n);
   if (c->timing && c->plan.k > 0) {
     EIGB_CUDA(cudaEventSynchronize(c->ev[6]));
     for (int i = 0; i < 6; ++i) {
@@ -304,6 +341,8 @@ void eigmod_b200_ctx_destroy(eigmod_b200_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   ctx->ws.release();
+  if (ctx->copy) cudaStreamDestroy(ctx->copy);
+  for (auto e : ctx->blk_ev) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->own);
   delete ctx;
 }
@@ -582,9 +621,12 @@ int eigmod_b200_update_decomposition(eigmod_b200_ctx* ctx, const double* q, cons
     EIGB_CUDA(cudaMemcpyAsync(dq, q, 8 * n * n, cudaMemcpyHostToDevice, st));
     EIGB_CUDA(cudaMemcpyAsync(dl, lambda, 8 * n, cudaMemcpyHostToDevice, st));
     EIGB_CUDA(cudaMemcpyAsync(dk, kmat, 8 * n * k, cudaMemcpyHostToDevice, st));
-    full_device(ctx, dq, dl, dk, signs, n, k, dlo, dqo);
+    // Q' leaves in column blocks overlapped with the GEMM (finish); the rank-0
+    // case (plain copy of Q) has no GEMM to overlap with
+    full_device(ctx, dq, dl, dk, signs, n, k, dlo, dqo, q_out);
     EIGB_CUDA(cudaMemcpyAsync(lambda_out, dlo, 8 * n, cudaMemcpyDeviceToHost, st));
-    EIGB_CUDA(cudaMemcpyAsync(q_out, dqo, 8 * n * n, cudaMemcpyDeviceToHost, st));
+    if (ctx->plan.k == 0)
+      EIGB_CUDA(cudaMemcpyAsync(q_out, dqo, 8 * n * n, cudaMemcpyDeviceToHost, st));
     EIGB_CUDA(cudaStreamSynchronize(st));
     if (wall_time_out)
       *wall_time_out =
