@@ -371,6 +371,8 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
       ctx->sopt.sweep = value != 0.0;
     } else if (std::string(key) == "fnewton") {
       ctx->sopt.fnewton = value != 0.0;
+    } else if (std::string(key) == "cluster") {
+      ctx->sopt.cluster = (int)value;
     } else if (std::string(key) == "timing") {
       ctx->timing = value != 0.0;
     } else {

@@ -27,6 +27,8 @@
 
 #include <cfloat>
 
+#include <cooperative_groups.h>
+
 namespace eigb {
 
 namespace {
@@ -68,15 +70,16 @@ __device__ __forceinline__ void load_S(const double* rb, const int* sgn, int k, 
 // ------------------------------------------------------------ sweep kernel
 template <int KP>
 __global__ void __launch_bounds__(kPassThreads, 1) count_sweep_kernel(ReducedView rp,
-                                                                      int* __restrict__ counts) {
+                                                                      int* __restrict__ counts,
+                                                                      int64_t qbeg, int64_t qend) {
   using C = PassCfg<KP>;
   extern __shared__ __align__(16) double smem[];
   double* F = smem + C::SMEM_DOUBLES;  // interleaved [KP*KP][32]
   __shared__ double dob[32], delta[32];
   __shared__ int active[32], hit[32];
   const int t = threadIdx.x;
-  const int64_t Q = 2 * rp.n;
-  const int64_t q0 = (int64_t)blockIdx.x * 32;
+  const int64_t Q = qend;
+  const int64_t q0 = qbeg + (int64_t)blockIdx.x * 32;
   if (t < 32) {
     const int64_t q = q0 + t;
     active[t] = q < Q;
@@ -104,6 +107,7 @@ struct SolveSmem {
   double dob[32], delta[32], lo[32], hi[32], step_prev[32];
   int64_t j[32], o[32], below[32];
   int active[32], hit[32], phase[32], lo_ok[32], hi_ok[32], iters[32], itersA[32], fmode[32];
+  unsigned long long jnext[32];  // root handed out by cluster rank 0
 };
 
 template <int KP>
@@ -118,6 +122,8 @@ struct SolveArgs {
   double lo_clip, hi_clip;
   double step_tol;
   int max_iters;
+  int writer;  // writes root records (cluster rank 0)
+  int64_t qbeg, qend;  // swept point range
 };
 
 // Sweep bracket of root j: the last usable sweep point with count <= j and
@@ -125,8 +131,11 @@ struct SolveArgs {
 template <int KP>
 __device__ void sweep_bracket(const SolveArgs<KP>& a, int64_t j, double* lo, double* hi,
                               int* lo_ok, int* hi_ok) {
-  const int64_t Q = 2 * a.rp.n;
-  int64_t L = 0, R = Q;  // first q with counts[q] > j (skipping -1 entries linearly)
+  // the swept points are [qbeg, qend); outside them fall back to the Weyl
+  // window bound (proj/src/locate.cpp:159-171), uncertified
+  const int64_t N = a.rp.n;
+  const int64_t QB = a.qbeg, QE = a.qend;
+  int64_t L = QB, R = QE;  // first usable q with counts[q] > j
   while (L < R) {
     const int64_t mid = (L + R) >> 1;
     int64_t q = mid;
@@ -134,24 +143,29 @@ __device__ void sweep_bracket(const SolveArgs<KP>& a, int64_t j, double* lo, dou
     if (q == R) { R = mid; continue; }
     if (a.counts[q] > j) R = mid; else L = q + 1;
   }
-  // hi point: first usable q >= L
   int64_t qh = L;
-  while (qh < Q && a.counts[qh] < 0) ++qh;
+  while (qh < QE && a.counts[qh] < 0) ++qh;
   int64_t ql = L - 1;
-  while (ql >= 0 && a.counts[ql] < 0) --ql;
-  if (ql >= 0) {
-    *lo = sweep_point(a.rp.d, a.rp.n, ql);
+  while (ql >= QB && a.counts[ql] < 0) --ql;
+  if (ql >= QB) {
+    *lo = sweep_point(a.rp.d, N, ql);
     *lo_ok = (a.counts[ql] == j);
-  } else {
+  } else if (QB == 0) {
     *lo = a.lo_clip;
     *lo_ok = (j == 0);
-  }
-  if (qh < Q) {
-    *hi = sweep_point(a.rp.d, a.rp.n, qh);
-    *hi_ok = (a.counts[qh] == j + 1);
   } else {
+    *lo = (j - a.m_neg >= 0) ? a.rp.d[j - a.m_neg] : a.lo_clip;
+    *lo_ok = 0;
+  }
+  if (qh < QE) {
+    *hi = sweep_point(a.rp.d, N, qh);
+    *hi_ok = (a.counts[qh] == j + 1);
+  } else if (QE == 2 * N) {
     *hi = a.hi_clip;
-    *hi_ok = (j + 1 == a.rp.n);
+    *hi_ok = (j + 1 == N);
+  } else {
+    *hi = (j + a.p_pos <= N - 1) ? a.rp.d[j + a.p_pos] : a.hi_clip;
+    *hi_ok = 0;
   }
 }
 
@@ -215,16 +229,17 @@ template <int KP>
 __device__ void slot_finish(SolveSmem& s, const double* y, int b, const SolveArgs<KP>& a,
                             int64_t o, double delta, double value, int flags, double* ynext) {
   const int64_t j = s.j[b];
-  a.out.value[j] = value;
-  a.out.origin[j] = o;
-  a.out.delta[j] = delta;
-  const int ia = s.phase[b] ? (s.itersA[b] < 255 ? s.itersA[b] : 255) : 255;
-  a.out.flags[j] = flags | (ia << 8);
-  a.out.evals[j] = s.iters[b];
-  for (int c = 0; c < KP; ++c) a.out.y[j * KP + c] = y[c];
-  const unsigned long long nj = atomicAdd(a.next_root, 1ull);
-  if ((int64_t)nj < a.j_end) slot_init<KP>(s, ynext, b, (int64_t)nj, a);
-  else s.active[b] = 0;
+  if (a.writer) {  // cluster rank 0 (every CTA of a cluster holds the same state)
+    a.out.value[j] = value;
+    a.out.origin[j] = o;
+    a.out.delta[j] = delta;
+    const int ia = s.phase[b] ? (s.itersA[b] < 255 ? s.itersA[b] : 255) : 255;
+    a.out.flags[j] = flags | (ia << 8);
+    a.out.evals[j] = s.iters[b];
+    for (int c = 0; c < KP; ++c) a.out.y[j * KP + c] = y[c];
+  }
+  (void)ynext;
+  s.active[b] = 2;  // refilled from the root queue by the kernel loop
 }
 
 // Phase A ended at ulp width without isolation: a pole inside [lo, hi] means
@@ -387,16 +402,32 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
 template <int KP>
 constexpr bool kFactorInSmem = (KP <= 16);
 
-template <int KP>
+// CL CTAs (a thread-block cluster on CL SMs) share one batch of 32 slots: CTA
+// r runs the pole pass over pole slice r, the partial sums are combined over
+// distributed shared memory in rank order, and every CTA then advances the
+// (replicated, identical) slot state. Rank 0 alone talks to the root queue
+// and writes records. Splitting the pole sum shortens an iteration by CL, so
+// the tail of the last roots (lockstep slots idle while a few finish) costs
+// CL times less wall time.
+template <int KP, int CL>
 __global__ void __launch_bounds__(kPassThreads, 1) solve_roots_kernel(SolveArgs<KP> a,
                                                                       double* gscratch) {
   using C = PassCfg<KP>;
+  namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double smem[];
   double* y = smem + C::SMEM_DOUBLES;                      // [32][KP]
   double* Fs = y + 32 * KP;                                // [KP*KP][32] (KP <= 16)
-  SolveSmem& s = *reinterpret_cast<SolveSmem*>(Fs + (kFactorInSmem<KP> ? 32 * KP * KP : 0));
+  double* fullred = Fs + (kFactorInSmem<KP> ? 32 * KP * KP : 0);  // [32][OUT] (CL > 1)
+  SolveSmem& s = *reinterpret_cast<SolveSmem*>(fullred + (CL > 1 ? C::RED_DOUBLES : 0));
   __shared__ int any;
   const int t = threadIdx.x;
+  int rank = 0;
+  if constexpr (CL > 1) rank = (int)cg::this_cluster().block_rank();
+  a.writer = (rank == 0);
+  const int64_t N = a.rp.n;
+  const int64_t chunk = (N + CL - 1) / CL;
+  const int64_t plo = (rank * chunk < N) ? rank * chunk : N;
+  const int64_t pcnt = ((plo + chunk < N) ? plo + chunk : N) - plo;
   double* F;
   int es;
   if constexpr (kFactorInSmem<KP>) {
@@ -406,16 +437,32 @@ __global__ void __launch_bounds__(kPassThreads, 1) solve_roots_kernel(SolveArgs<
     F = gscratch + ((size_t)blockIdx.x * 32 + (t & 31)) * KP * KP;
     es = 1;
   }
-  if (t < 32) {
-    const unsigned long long nj = atomicAdd(a.next_root, 1ull);
-    if ((int64_t)nj < a.j_end) slot_init<KP>(s, y, t, (int64_t)nj, a);
-    else s.active[t] = 0;
-  }
+  if (t < 32) s.active[t] = 2;
   __syncthreads();
   PassOpts o;
-  o.alpha = a.alpha;
+  o.alpha = a.alpha ? a.alpha + plo : nullptr;
   o.want_sigma = true;
   for (;;) {
+    // ---- refill finished slots from the root queue
+    if constexpr (CL == 1) {
+      if (t < 32 && s.active[t] == 2) {
+        const unsigned long long nj = atomicAdd(a.next_root, 1ull);
+        if ((int64_t)nj < a.j_end) slot_init<KP>(s, y, t, (int64_t)nj, a);
+        else s.active[t] = 0;
+      }
+    } else {
+      cg::cluster_group cl = cg::this_cluster();
+      if (rank == 0 && t < 32 && s.active[t] == 2) {
+        const unsigned long long nj = atomicAdd(a.next_root, 1ull);
+        for (int r = 0; r < CL; ++r) cl.map_shared_rank(&s, r)->jnext[t] = nj;
+      }
+      cl.sync();
+      if (t < 32 && s.active[t] == 2) {
+        const unsigned long long nj = s.jnext[t];
+        if ((int64_t)nj < a.j_end) slot_init<KP>(s, y, t, (int64_t)nj, a);
+        else s.active[t] = 0;
+      }
+    }
     if (t == 0) {
       int v = 0;
       for (int b = 0; b < 32; ++b) v |= s.active[b];
@@ -423,9 +470,27 @@ __global__ void __launch_bounds__(kPassThreads, 1) solve_roots_kernel(SolveArgs<
     }
     __syncthreads();
     if (!any) break;
+    // ---- pole pass over this CTA's slice
     PassSlots sl{s.dob, s.delta, y, s.active, s.hit};
-    secular_pass<KP>(a.rp.d, a.rp.u, a.rp.n, sl, o, smem);
-    if (t < 32 && s.active[t]) slot_step<KP>(s, y, t, pass_result<KP>(smem), F, es, a);
+    secular_pass<KP>(a.rp.d + plo, a.rp.u + plo * KP, pcnt, sl, o, smem);
+    const double* red = pass_result<KP>(smem);
+    if constexpr (CL > 1) {
+      cg::cluster_group cl = cg::this_cluster();
+      cl.sync();  // all partial sums of this iteration are in place
+      for (int idx = t; idx < C::RED_DOUBLES; idx += kPassThreads) {
+        double v = 0.0;
+        for (int r = 0; r < CL; ++r) v += cl.map_shared_rank(red, r)[idx];
+        fullred[idx] = v;
+      }
+      if (t < 32) {
+        int h = 0;
+        for (int r = 0; r < CL; ++r) h |= cl.map_shared_rank(&s, r)->hit[t];
+        s.hit[t] = h;  // OR is idempotent: safe while others still read it
+      }
+      cl.sync();  // partials no longer read remotely
+      red = fullred;
+    }
+    if (t < 32 && s.active[t] == 1) slot_step<KP>(s, y, t, red, F, es, a);
     __syncthreads();
   }
 }
@@ -493,31 +558,71 @@ __global__ void __launch_bounds__(kPassThreads, 1) group_weights_kernel(WeightAr
   }
 }
 
-template <int KP>
+template <int KP, int CL>
 size_t solve_smem_bytes() {
   using C = PassCfg<KP>;
-  return sizeof(double) * (C::SMEM_DOUBLES + 32 * KP + (kFactorInSmem<KP> ? 32 * KP * KP : 0)) +
+  return sizeof(double) * (C::SMEM_DOUBLES + 32 * KP + (kFactorInSmem<KP> ? 32 * KP * KP : 0) +
+                           (CL > 1 ? C::RED_DOUBLES : 0)) +
          sizeof(SolveSmem);
 }
 
 template <int KP>
-void launch_sweep(const ReducedView& rp, int* counts, cudaStream_t st) {
+void launch_sweep(const ReducedView& rp, int* counts, int64_t qbeg, int64_t qend, cudaStream_t st) {
   using C = PassCfg<KP>;
   const size_t sm = sizeof(double) * (C::SMEM_DOUBLES + 32 * KP * KP);
   EIGB_CUDA(cudaFuncSetAttribute(count_sweep_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sm));
-  count_sweep_kernel<KP><<<(unsigned)cdiv(2 * rp.n, 32), kPassThreads, sm, st>>>(rp, counts);
+  if (qend <= qbeg) return;
+  count_sweep_kernel<KP><<<(unsigned)cdiv(qend - qbeg, 32), kPassThreads, sm, st>>>(rp, counts, qbeg,
+                                                                                  qend);
   EIGB_LAUNCH_CHECK();
 }
 
+// Launches the solver on thread-block clusters of CL CTAs; false when the
+// device cannot co-schedule such clusters (caller falls back to CL = 1).
+template <int KP, int CL>
+bool launch_solve_cluster(const SolveArgs<KP>& a, int64_t nroots, int sms, cudaStream_t st) {
+  if constexpr (!kFactorInSmem<KP>) {
+    return false;
+  } else {
+    const size_t sm = solve_smem_bytes<KP, CL>();
+    auto kern = solve_roots_kernel<KP, CL>;
+    EIGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(kPassThreads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(CL * std::max(1, sms / CL));
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess || nclusters <= 0) {
+      (void)cudaGetLastError();
+      return false;
+    }
+    const int64_t want = cdiv(nroots, 32);
+    cfg.gridDim = dim3((unsigned)(CL * std::min<int64_t>(nclusters, want)));
+    EIGB_CUDA(cudaLaunchKernelEx(&cfg, kern, a, (double*)nullptr));
+    EIGB_LAUNCH_CHECK();
+    return true;
+  }
+}
+
 template <int KP>
-void launch_solve(const ReducedView& rp, const double* alpha, const int* counts, int64_t j0,
-                  int64_t j1, const RootRecords& out, const SolveOptions& opt, DeviceScratch& ws,
-                  int sms, cudaStream_t st) {
+void launch_solve(const ReducedView& rp, const double* alpha, const int* counts, int64_t qbeg,
+                  int64_t qend, int64_t j0, int64_t j1, const RootRecords& out,
+                  const SolveOptions& opt, DeviceScratch& ws, int sms, cudaStream_t st) {
   SolveArgs<KP> a;
   a.rp = rp;
   a.alpha = alpha;
   a.counts = counts;
+  a.qbeg = qbeg;
+  a.qend = qend;
   a.j_end = j1;
   a.out = out;
   a.m_neg = rp.m_neg;
@@ -526,17 +631,24 @@ void launch_solve(const ReducedView& rp, const double* alpha, const int* counts,
   a.hi_clip = rp.hi_clip;
   a.step_tol = opt.step_tol;
   a.max_iters = opt.max_iters;
+  a.writer = 1;
   const int64_t nroots = j1 - j0;
-  const int grid = (int)std::min<int64_t>(sms, cdiv(nroots, 32));
-  double* gscratch = kFactorInSmem<KP> ? nullptr
-                                       : ws.get_f64("solve_scratch", (size_t)grid * 32 * KP * KP);
   a.next_root = reinterpret_cast<unsigned long long*>(ws.get_i64("solve_counter", 1));
   const unsigned long long start = (unsigned long long)j0;
   EIGB_CUDA(cudaMemcpyAsync(a.next_root, &start, sizeof(start), cudaMemcpyHostToDevice, st));
-  const size_t sm = solve_smem_bytes<KP>();
-  EIGB_CUDA(cudaFuncSetAttribute(solve_roots_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sm));
-  solve_roots_kernel<KP><<<grid, kPassThreads, sm, st>>>(a, gscratch);
+  int cl = opt.cluster;
+  if (cl < 0) cl = 4;
+  if (!kFactorInSmem<KP> || cl <= 1 || nroots <= 32) cl = 1;
+  if (cl >= 8 && launch_solve_cluster<KP, 8>(a, nroots, sms, st)) return;
+  if (cl >= 4 && cl < 8 && launch_solve_cluster<KP, 4>(a, nroots, sms, st)) return;
+  if (cl >= 2 && cl < 4 && launch_solve_cluster<KP, 2>(a, nroots, sms, st)) return;
+  const int grid = (int)std::min<int64_t>(sms, cdiv(nroots, 32));
+  double* gscratch = kFactorInSmem<KP> ? nullptr
+                                       : ws.get_f64("solve_scratch", (size_t)grid * 32 * KP * KP);
+  const size_t sm = solve_smem_bytes<KP, 1>();
+  EIGB_CUDA(cudaFuncSetAttribute(solve_roots_kernel<KP, 1>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  solve_roots_kernel<KP, 1><<<grid, kPassThreads, sm, st>>>(a, gscratch);
   EIGB_LAUNCH_CHECK();
 }
 
@@ -562,20 +674,26 @@ void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t
                  cudaStream_t st) {
   if (j1 <= j0) return;
   int* counts = nullptr;
+  // points next to the poles of every Weyl window of roots [j0, j1)
+  // (multi-GPU ranks sweep only their share)
+  const int64_t pb = std::max<int64_t>(0, j0 - rp.m_neg - 1);
+  const int64_t pe = std::min<int64_t>(rp.n, j1 + (rp.k - rp.m_neg) + 1);
+  const int64_t qbeg = 2 * pb, qend = 2 * pe;
   if (opt.sweep) {
     counts = ws.get_i32("sweep_counts", 2 * rp.n);
     switch (rp.kp) {
-      case 1: launch_sweep<1>(rp, counts, st); break;
-      case 2: launch_sweep<2>(rp, counts, st); break;
-      case 4: launch_sweep<4>(rp, counts, st); break;
-      case 8: launch_sweep<8>(rp, counts, st); break;
-      case 16: launch_sweep<16>(rp, counts, st); break;
-      case 32: launch_sweep<32>(rp, counts, st); break;
+      case 1: launch_sweep<1>(rp, counts, qbeg, qend, st); break;
+      case 2: launch_sweep<2>(rp, counts, qbeg, qend, st); break;
+      case 4: launch_sweep<4>(rp, counts, qbeg, qend, st); break;
+      case 8: launch_sweep<8>(rp, counts, qbeg, qend, st); break;
+      case 16: launch_sweep<16>(rp, counts, qbeg, qend, st); break;
+      case 32: launch_sweep<32>(rp, counts, qbeg, qend, st); break;
       default: throw Error(1, "", "solve_roots: unsupported padded rank");
     }
   }
   if (!opt.fnewton) alpha = nullptr;
-#define EIGB_SOLVE(K) launch_solve<K>(rp, alpha, counts, j0, j1, out, opt, ws, sms, st)
+#define EIGB_SOLVE(K) \
+  launch_solve<K>(rp, alpha, counts, qbeg, qend, j0, j1, out, opt, ws, sms, st)
   switch (rp.kp) {
     case 1: EIGB_SOLVE(1); break;
     case 2: EIGB_SOLVE(2); break;

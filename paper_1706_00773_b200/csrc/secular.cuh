@@ -81,6 +81,9 @@ struct SolveOptions {
   int max_iters = 160;
   bool sweep = true;    // count sweep for the initial brackets (else Weyl windows)
   bool fnewton = true;  // Newton on the scalar secular function first
+  // CTAs per thread-block cluster splitting the pole sum: 1, 2, 4, 8, or -1
+  // for the size-based choice (solve_cluster_size)
+  int cluster = -1;
 };
 
 // alpha: residues of the reduced poles for the f-Newton phase (nullptr when
