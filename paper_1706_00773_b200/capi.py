@@ -60,6 +60,8 @@ def _declare(lib):
         "eigmod_b200_last_stage": (C.c_char_p, [_VP]),
         "eigmod_b200_stats": (C.c_int, [_VP, _D]),
         "eigmod_b200_workspace_bytes": (C.c_int64, [_VP]),
+        "eigmod_b200_solver_profile": (C.c_int, [_VP, _D]),
+        "eigmod_b200_solver_trace": (C.c_int, [_VP, _D]),
         "eigmod_b200_stage_times": (C.c_int, [_VP, _D, C.c_int]),
         "eigmod_b200_launch_count": (C.c_int64, []),
         "eigmod_b200_fp64_peaks": (C.c_int, [_VP, _D]),
@@ -190,6 +192,17 @@ class Context:
         out = np.zeros(2)
         self.check(self._l.eigmod_b200_fp64_peaks(self.h, _dp(out)))
         return {"dmma_tflops": float(out[0]), "dfma_tflops": float(out[1])}
+
+    def solver_profile(self) -> dict:
+        o = np.zeros(4)
+        self.check(self._l.eigmod_b200_solver_profile(self.h, o.ctypes.data_as(_D)))
+        return {"passes": o[0], "active_slot_passes": o[1], "batches": o[2],
+                "slot_util": o[1] / max(1.0, 32.0 * o[0])}
+
+    def solver_trace(self) -> np.ndarray:
+        o = np.zeros((200, 12))
+        self.check(self._l.eigmod_b200_solver_trace(self.h, o.ctypes.data_as(_D)))
+        return o[o[:, 0] > 0]
 
     def workspace_bytes(self) -> int:
         return int(self._l.eigmod_b200_workspace_bytes(self.h))

@@ -365,6 +365,14 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
     } else if (std::string(key) == "step_tol") {
       if (!(value > 0.0)) throw Error(1, "", "set_option: step_tol must be positive");
       ctx->sopt.step_tol = value;
+    } else if (std::string(key) == "fexit_rel") {
+      ctx->sopt.fexit_rel = value;
+    } else if (std::string(key) == "floor_rel") {
+      ctx->sopt.floor_rel = value;
+    } else if (std::string(key) == "geo_bisect") {
+      ctx->sopt.geo_bisect = (int)value;
+    } else if (std::string(key) == "trace_root") {
+      ctx->sopt.trace_root = (int64_t)value;
     } else if (std::string(key) == "max_iters") {
       ctx->sopt.max_iters = (int)value;
     } else if (std::string(key) == "sweep") {
@@ -414,6 +422,25 @@ int eigmod_b200_stats(const eigmod_b200_ctx* cctx, double* s) {
       s[3] = tot;
       s[4] = mx;
     }
+  });
+}
+
+int eigmod_b200_solver_profile(eigmod_b200_ctx* ctx, double* out4) {
+  return guarded(ctx, [&] {
+    unsigned long long h[4] = {0, 0, 0, 0};
+    auto* p = reinterpret_cast<unsigned long long*>(ctx->ws.get_i64("solve_prof", 4));
+    EIGB_CUDA(cudaMemcpyAsync(h, p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    EIGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < 4; ++i) out4[i] = (double)h[i];
+  });
+}
+
+int eigmod_b200_solver_trace(eigmod_b200_ctx* ctx, double* out) {
+  return guarded(ctx, [&] {
+    const size_t cnt = (size_t)eigb::kTraceRows * eigb::kTraceCols;
+    const double* p = ctx->ws.get_f64("solve_trace", cnt);
+    EIGB_CUDA(cudaMemcpyAsync(out, p, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    EIGB_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

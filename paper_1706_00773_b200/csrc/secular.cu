@@ -124,6 +124,11 @@ struct SolveArgs {
   int max_iters;
   int writer;  // writes root records (cluster rank 0)
   int64_t qbeg, qend;  // swept point range
+  unsigned long long* prof;  // [0] passes, [1] active slot-passes, [2] slot batches
+  double fexit_rel, floor_rel;
+  int geo_bisect;
+  int64_t trace_j;           // diagnostics (-1: off)
+  double* trace;             // [kTraceRows][kTraceCols]
 };
 
 // Sweep bracket of root j: the last usable sweep point with count <= j and
@@ -319,6 +324,12 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
   if (s.phase[b] == 0) {
     const double x = s.delta[b];
     const int64_t cnt = dev_n_less(d, N, x) + a.m_neg - neg;
+    if (j == a.trace_j && a.writer && s.iters[b] <= kTraceRows) {
+      double* tr = a.trace + (s.iters[b] - 1) * kTraceCols;
+      const double v[kTraceCols] = {(double)s.iters[b], 0.0, (double)cnt, x, s.lo[b], s.hi[b],
+                                    fv, fpv, sigma, gp, 0.0, -1.0};
+      for (int c = 0; c < kTraceCols; ++c) tr[c] = v[c];
+    }
     if (cnt >= j + 1) { s.hi[b] = x; s.hi_ok[b] = (cnt == j + 1); }
     else { s.lo[b] = x; s.lo_ok[b] = (cnt == j); }
     const double lo = s.lo[b], hi = s.hi[b];
@@ -343,7 +354,16 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
   if (s.fmode[b]) {  // Newton on g = -delta f: g' = -f - delta f'
     const double den = fv + dl * fpv;
     step = (den != 0.0) ? -dl * fv / den : NAN;
-    if (!(fabs(step) > kFSwitchRel * fabs(dl))) s.fmode[b] = 0;  // f resolved: polish on S
+    // f resolved, or its root contradicts the certified bracket (residues of
+    // poles next to a root are the least accurate): continue on S
+    const double dt = dl + step;
+    if (!(fabs(step) > kFSwitchRel * fabs(dl)) ||
+        (!(dt > lo && dt < hi) && fabs(step) <= a.fexit_rel * fabs(dl))) {
+      s.fmode[b] = 0;
+      // the first S step corrects the error of the residues, not a
+      // continuation of the f steps: do not judge it against them
+      s.step_prev[b] = hi - lo;
+    }
   }
   if (!s.fmode[b]) {  // Newton on psi = -delta sigma: psi' = -sigma - delta sigma'
     const double den = sigma + dl * gp;
@@ -351,11 +371,17 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
   }
   const double w = hi - lo;
   const double tol = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi));
+  if (j == a.trace_j && a.writer && s.iters[b] <= kTraceRows) {
+    double* tr = a.trace + (s.iters[b] - 1) * kTraceCols;
+    const double v[kTraceCols] = {(double)s.iters[b], 1.0, (double)s.fmode[b], dl, lo, hi,
+                                  fv, fpv, sigma, gp, step, (double)s.o[b]};
+    for (int c = 0; c < kTraceCols; ++c) tr[c] = v[c];
+  }
   // converged: S-Newton correction below step_tol ulps, or stalled at the
   // rounding floor of sigma (no longer shrinking while already tiny)
   const bool sdone = !s.fmode[b] && ((fabs(step) <= a.step_tol * DBL_EPSILON * fabs(dl)) ||
                                      (fabs(step) >= fabs(s.step_prev[b]) &&
-                                      fabs(step) <= 1e3 * DBL_EPSILON * fabs(dl)));
+                                      fabs(step) <= a.floor_rel * fabs(dl)));
   if (sdone || w <= tol || zero || s.iters[b] > a.max_iters) {
     // two more inverse-iteration steps on the same factorization: the
     // eigenvector formula needs y to the accuracy of the root
@@ -375,7 +401,13 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
   // safeguard: bisect when the step leaves the certified bracket or stops
   // shrinking
   if (!(dn > lo && dn < hi) || !(fabs(step) < fabs(s.step_prev[b]))) {
-    dn = 0.5 * (lo + hi);
+    // a bracket spanning orders of magnitude of delta (root next to the
+    // origin pole) is split geometrically
+    const double alo = fabs(lo), ahi = fabs(hi);
+    if (a.geo_bisect && lo * hi > 0.0 && fmax(alo, ahi) > 8.0 * fmin(alo, ahi))
+      dn = copysign(sqrt(alo * ahi), lo);
+    else
+      dn = 0.5 * (lo + hi);
     s.step_prev[b] = w;
   } else {
     s.step_prev[b] = step;
@@ -410,7 +442,7 @@ constexpr bool kFactorInSmem = (KP <= 16);
 // the tail of the last roots (lockstep slots idle while a few finish) costs
 // CL times less wall time.
 template <int KP, int CL>
-__global__ void __launch_bounds__(kPassThreads, 1) solve_roots_kernel(SolveArgs<KP> a,
+__global__ void __launch_bounds__(kPassThreads, KP <= 4 ? 2 : 1) solve_roots_kernel(SolveArgs<KP> a,
                                                                       double* gscratch) {
   using C = PassCfg<KP>;
   namespace cg = cooperative_groups;
@@ -442,6 +474,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) solve_roots_kernel(SolveArgs<
   PassOpts o;
   o.alpha = a.alpha ? a.alpha + plo : nullptr;
   o.want_sigma = true;
+  unsigned long long npass = 0, nact = 0;
   for (;;) {
     // ---- refill finished slots from the root queue
     if constexpr (CL == 1) {
@@ -464,9 +497,14 @@ __global__ void __launch_bounds__(kPassThreads, 1) solve_roots_kernel(SolveArgs<
       }
     }
     if (t == 0) {
-      int v = 0;
-      for (int b = 0; b < 32; ++b) v |= s.active[b];
+      int v = 0, c = 0;
+      for (int b = 0; b < 32; ++b) {
+        v |= s.active[b];
+        c += (s.active[b] == 1);
+      }
       any = v;
+      npass += (v != 0);
+      nact += c;
     }
     __syncthreads();
     if (!any) break;
@@ -492,6 +530,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) solve_roots_kernel(SolveArgs<
     }
     if (t < 32 && s.active[t] == 1) slot_step<KP>(s, y, t, red, F, es, a);
     __syncthreads();
+  }
+  if (t == 0 && rank == 0 && a.prof) {
+    atomicAdd(a.prof, npass);
+    atomicAdd(a.prof + 1, nact);
+    atomicAdd(a.prof + 2, 1ull);
   }
 }
 
@@ -634,10 +677,26 @@ void launch_solve(const ReducedView& rp, const double* alpha, const int* counts,
   a.writer = 1;
   const int64_t nroots = j1 - j0;
   a.next_root = reinterpret_cast<unsigned long long*>(ws.get_i64("solve_counter", 1));
+  a.prof = reinterpret_cast<unsigned long long*>(ws.get_i64("solve_prof", 4));
+  a.trace_j = opt.trace_root;
+  a.fexit_rel = opt.fexit_rel;
+  a.floor_rel = opt.floor_rel;
+  a.geo_bisect = opt.geo_bisect;
+  a.trace = ws.get_f64("solve_trace", (size_t)kTraceRows * kTraceCols);
+  if (opt.trace_root >= 0)
+    EIGB_CUDA(cudaMemsetAsync(a.trace, 0, sizeof(double) * kTraceRows * kTraceCols, st));
+  EIGB_CUDA(cudaMemsetAsync(a.prof, 0, 4 * sizeof(unsigned long long), st));
   const unsigned long long start = (unsigned long long)j0;
   EIGB_CUDA(cudaMemcpyAsync(a.next_root, &start, sizeof(start), cudaMemcpyHostToDevice, st));
+  // Size-based choice (tools/exp_cluster.py, cfg 2/4 at n = 8192/32768):
+  // with many roots per SM the GPC-aligned pairs keep all 148 SMs busy (4-
+  // and 8-CTA clusters leave GPC remainders idle); with few, the shorter
+  // per-iteration pass of larger clusters shrinks the tail of the last roots.
   int cl = opt.cluster;
-  if (cl < 0) cl = 4;
+  if (cl < 0) {
+    const int64_t per_sm = nroots / std::max(1, sms);
+    cl = per_sm >= 160 ? 2 : (per_sm >= 20 ? 4 : 8);
+  }
   if (!kFactorInSmem<KP> || cl <= 1 || nroots <= 32) cl = 1;
   if (cl >= 8 && launch_solve_cluster<KP, 8>(a, nroots, sms, st)) return;
   if (cl >= 4 && cl < 8 && launch_solve_cluster<KP, 4>(a, nroots, sms, st)) return;

@@ -84,7 +84,16 @@ struct SolveOptions {
   // CTAs per thread-block cluster splitting the pole sum: 1, 2, 4, 8, or -1
   // for the size-based choice (solve_cluster_size)
   int cluster = -1;
+  int64_t trace_root = -1;  // diagnostics: record the iterates of this root
+  double fexit_rel = 1e-2;  // f step leaving the bracket below this * |delta|: continue on S
+  double floor_rel = 1e-11; // S-Newton step no longer shrinking below this * |delta|: converged
+  int geo_bisect = 1;       // geometric bisection of brackets spanning decades of delta
 };
+
+// Diagnostics trace of one root: per evaluation kTraceCols doubles
+// (iteration, phase, fmode, delta, lo, hi, f, f', sigma, g, step, origin).
+constexpr int kTraceCols = 12;
+constexpr int kTraceRows = 200;
 
 // alpha: residues of the reduced poles for the f-Newton phase (nullptr when
 // the reduced problem has compressed runs, whose poles are not simple).

@@ -1,4 +1,4 @@
-"""Solve-stage time vs thread-block cluster size and root-range size (dev tool)."""
+"""Solver slot utilisation and per-pass time (dev tool)."""
 import sys
 
 sys.path.insert(0, '.')
@@ -9,7 +9,8 @@ from paper_1706_00773_b200.instances import make_instance_torch
 from paper_1706_00773_b200.sharded import CudaBackend, split
 
 dev = torch.device('cuda', 0)
-for cfg, n in [(4, 32768), (2, 8192), (4, 8192)]:
+cases = [(4, 32768), (2, 8192), (4, 8192)]
+for cfg, n in cases:
     q, lam, kmat, signs = make_instance_torch(cfg, n=n, device=dev)
     k = kmat.shape[1]
     ctx = capi.Context(0)
@@ -18,14 +19,11 @@ for cfg, n in [(4, 32768), (2, 8192), (4, 8192)]:
     u = torch.zeros((n, be.kp), dtype=torch.float64, device=dev)
     be.project(q, kmat, 0, n, u)
     nred = be.plan(lam, u)
-    print(f"cfg{cfg} n={n} nred={nred}", flush=True)
-    for world in (1, 2, 4, 8):
+    for world in (1, 8):
         j0, j1, _ = split(nred, world, world // 2)
         rec = torch.zeros((j1 - j0, be.width), dtype=torch.float64, device=dev)
-        row = []
-        for cl in (1, 2, 4, 8, -1):
-            ctx.set_option('cluster', cl)
-            best = 1e30
+        for sweep in (1, 0):
+            ctx.set_option('sweep', sweep)
             for _ in range(2):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 torch.cuda.synchronize()
@@ -33,17 +31,11 @@ for cfg, n in [(4, 32768), (2, 8192), (4, 8192)]:
                 be.solve(j0, j1, rec)
                 b.record()
                 torch.cuda.synchronize()
-                best = min(best, a.elapsed_time(b))
-            row.append(best)
-        print(f"  roots {j1 - j0:6d}: " + "  ".join(f"CL{c}={t:7.2f}" for c, t in zip((1, 2, 4, 8, "auto"), row)),
-              flush=True)
-    ctx.set_option('sweep', 0)
-    ctx.set_option('cluster', 4)
-    rec = torch.zeros((nred, be.width), dtype=torch.float64, device=dev)
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    be.solve(0, nred, rec)
-    b.record()
-    torch.cuda.synchronize()
-    print(f"  no-sweep full CL4: {a.elapsed_time(b):.2f}", flush=True)
+            t = a.elapsed_time(b)
+            pr = ctx.solver_profile()
+            ev = float(rec[:, 4].sum())
+            per_batch = pr['passes'] / max(1, pr['batches'])
+            print(f"cfg{cfg} n={n} roots={j1 - j0} sweep={sweep}: {t:8.2f} ms evals {ev:.0f} "
+                  f"({ev / (j1 - j0):.2f}/root) batches {pr['batches']:.0f} passes/batch {per_batch:.1f} "
+                  f"slot util {pr['slot_util']:.3f}  ms/pass {t / max(1, per_batch):.3f}", flush=True)
+        ctx.set_option('sweep', 1)
