@@ -103,6 +103,23 @@ int eigmod_b200_deflate_problem(eigmod_b200_ctx* ctx, const double* lambda, cons
                                 double* weights, int64_t* pole_origin, int64_t* unchanged,
                                 int64_t* collided, int64_t* counts);
 
+/* Location vector (replaces the CLI locate path, tools/eigmod.cpp:143-161:
+ * transform_update -> deflate_problem -> locate_rank2 / locate_rank_k,
+ * locate.hpp:13-50): counts_out (capacity n + 1) receives, for the poles
+ * v_0 < ... < v_{N-1} of the deflation record, the number of updated
+ * eigenvalues in each open interval (v_{i-1}, v_i), v_{-1} = -inf,
+ * v_N = +inf; *ncounts_out = N + 1 (1 with counts {0} when every pole
+ * deflates). Counts come from exact inertia limits at the poles; they equal
+ * the reference's wherever its merged secular function is exact (no pole
+ * runs merged for k >= 2). */
+int eigmod_b200_locate(eigmod_b200_ctx* ctx, const double* q, const double* lambda,
+                       const double* kmat, const int* signs, int64_t n, int64_t k,
+                       int64_t* counts_out, int64_t* ncounts_out);
+/* Same from U = Q^T K (n x k). */
+int eigmod_b200_locate_from_u(eigmod_b200_ctx* ctx, const double* lambda, const double* u,
+                              const int* signs, int64_t n, int64_t k, int64_t* counts_out,
+                              int64_t* ncounts_out);
+
 /* Eigenvalue stage (replaces update_eigenvalues_full, rootfind.hpp:51-53 /
  * rootfind.cpp:381-472, for both the rank-2 and the general rank-k entry):
  * values_out (n, ascending), roots_out (n; the first *nroots_out are the

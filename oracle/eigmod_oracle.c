@@ -916,3 +916,113 @@ int eo_update(const double* q, const double* lambda, const double* kmat, const i
   free(rot); free(gs); free(gl); free(rep); free(alpha); free(kind); free(u);
   return 0;
 }
+
+/* ------------------------------------------------------------ location vector */
+/* Location vector of the CLI locate path (tools/eigmod.cpp:143-161): the
+ * poles v_g of the reference deflation record (secular.cpp:278-340, run
+ * threshold 1e-12) and, per open interval between consecutive poles, the
+ * number of updated eigenvalues (the meaning of locate.hpp:13-18). The
+ * reference reaches it by weight-sign parity scans plus Sturm counts
+ * (locate.cpp:70-252); this restatement uses the eigenvalue count instead:
+ * #eig < v_g = #{poles below v_g} + m - nu_g, with nu_g the negative inertia
+ * of T_g = J + sum over the other coupled rows u u^T/(lambda - v_g) on the
+ * orthogonal complement of u_g (the limit of S(x) as x -> v_g from below).
+ * Collided poles (kind 2) stay in T but are neither boundaries nor counted,
+ * as they leave the reference's secular coefficients. Returns 0; 1 invalid
+ * input; 3 a merged multi-row run with k >= 2 (the reference's merged pole
+ * is inexact there, locate.hpp has no exact meaning to restate). */
+int eo_locate(const double* lambda, const double* u, const int* signs, int64_t n, int64_t k,
+              int64_t* counts, int64_t* ncounts) {
+  if (k < 1 || k > EO_MAXK || n < 0) return 1;
+  for (int64_t i = 0; i + 1 < n; ++i)
+    if (!(lambda[i] <= lambda[i + 1])) return 1;
+  int64_t keep[EO_MAXK];
+  const int64_t k2 = eo_drop_zero_columns(u, n, k, keep);
+  if (n == 0 || k2 == 0) {
+    counts[0] = 0;
+    *ncounts = 1;
+    return 0;
+  }
+  double* u2 = (double*)malloc(sizeof(double) * n * k2);
+  int s2[EO_MAXK];
+  int64_t m_neg = 0;
+  for (int64_t c = 0; c < k2; ++c) s2[c] = signs[keep[c]], m_neg += s2[c] < 0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t c = 0; c < k2; ++c) u2[i * k2 + c] = u[i * k + keep[c]];
+  int64_t* gs = (int64_t*)malloc(sizeof(int64_t) * n);
+  int64_t* gl = (int64_t*)malloc(sizeof(int64_t) * n);
+  double* rep = (double*)malloc(sizeof(double) * n);
+  double* alpha = (double*)malloc(sizeof(double) * n);
+  int* kind = (int*)malloc(sizeof(int) * n);
+  const int64_t ng = make_runs(lambda, n, 1e-12, gs, gl, rep);
+  group_weights(rep, gs, gl, ng, u2, s2, k2, alpha);
+  classify(alpha, gs, gl, ng, u2, n, k2, kind);
+  int rc = 0;
+  for (int64_t g = 0; g < ng; ++g)
+    if (kind[g] == 0 && gl[g] > 1 && k2 >= 2) rc = 3;
+  int64_t nb = 0, below = 0, prev = 0;
+  for (int64_t g = 0; g < ng && rc == 0; ++g) {
+    if (kind[g] != 0) continue;
+    const double v = rep[g];
+    double T[EO_MAXK * EO_MAXK];
+    memset(T, 0, sizeof(double) * k2 * k2);
+    for (int64_t h = 0; h < ng; ++h) {
+      if (h == g || kind[h] == 1) continue;
+      for (int64_t s = gs[h]; s < gs[h] + gl[h]; ++s) {
+        const double inv = 1.0 / (lambda[s] - v);
+        const double* ws = u2 + s * k2;
+        for (int64_t r = 0; r < k2; ++r)
+          for (int64_t c = 0; c < k2; ++c) T[r * k2 + c] += ws[r] * inv * ws[c];
+      }
+    }
+    for (int64_t r = 0; r < k2; ++r) T[r * k2 + r] += (double)s2[r];
+    /* complement of u_g: eigenvectors of the projector-deflated T. With the
+     * unit vector e = u_g/|u_g|, B = (I - e e^T) T (I - e e^T) has e as an
+     * exact null direction; its other eigenpairs are those of T restricted
+     * to the complement. */
+    int64_t nu = 0;
+    if (k2 > 1) {
+      const double* ug = u2 + gs[g] * k2;
+      double e[EO_MAXK], nrm = 0.0;
+      for (int64_t c = 0; c < k2; ++c) nrm += ug[c] * ug[c];
+      nrm = sqrt(nrm);
+      for (int64_t c = 0; c < k2; ++c) e[c] = ug[c] / nrm;
+      double Te[EO_MAXK], eTe = 0.0;
+      for (int64_t r = 0; r < k2; ++r) {
+        Te[r] = 0.0;
+        for (int64_t c = 0; c < k2; ++c) Te[r] += T[r * k2 + c] * e[c];
+        eTe += e[r] * Te[r];
+      }
+      double B[EO_MAXK * EO_MAXK], w[EO_MAXK], V[EO_MAXK * EO_MAXK];
+      for (int64_t r = 0; r < k2; ++r)
+        for (int64_t c = 0; c < k2; ++c)
+          B[r * k2 + c] = T[r * k2 + c] - e[r] * Te[c] - Te[r] * e[c] + e[r] * e[c] * eTe;
+      sym_evd(B, (int)k2, w, V);
+      /* drop the eigenpair along e */
+      int64_t skip = 0;
+      double best = -1.0;
+      for (int64_t j = 0; j < k2; ++j) {
+        double d = 0.0;
+        for (int64_t r = 0; r < k2; ++r) d += V[r * k2 + j] * e[r];
+        if (fabs(d) > best) best = fabs(d), skip = j;
+      }
+      for (int64_t j = 0; j < k2; ++j)
+        if (j != skip && w[j] < 0.0) ++nu;
+    }
+    const int64_t cb = below + m_neg - nu;
+    counts[nb++] = cb - prev;
+    prev = cb;
+    below += 1;
+  }
+  if (rc == 0) {
+    if (nb == 0) {
+      counts[0] = 0;
+      *ncounts = 1;
+    } else {
+      counts[nb] = below - prev;
+      *ncounts = nb + 1;
+    }
+  }
+  free(u2), free(gs), free(gl), free(rep), free(alpha), free(kind);
+  return rc;
+}

@@ -57,6 +57,12 @@ int eo_solve_roots(const double* d, const double* ut, const int* signs, int64_t 
 int64_t eo_count_below(const double* d, const double* ut, const int* signs, int64_t n, int64_t k,
                        double x);
 
+/* Location vector over the reference deflation record's poles (CLI locate
+ * path, tools/eigmod.cpp:143-161); counts holds n + 1 entries. Returns 0, 1
+ * (invalid input) or 3 (merged multi-row run with k >= 2: not restated). */
+int eo_locate(const double* lambda, const double* u, const int* signs, int64_t n, int64_t k,
+              int64_t* counts, int64_t* ncounts);
+
 /* C = A B^T (A m x l, B n x l, row-major) — the Q X back-transform with X
  * stored transposed. */
 void eo_gemm_nt(const double* a, const double* b, int64_t m, int64_t nn, int64_t l, double* c);

@@ -132,3 +132,22 @@ def gemm_nt(a, b):
     c = np.empty((m, nn))
     lib().eo_gemm_nt(_D(a), _D(b), C.c_int64(m), C.c_int64(nn), C.c_int64(l), _D(c))
     return c
+
+
+class LocateUnsupported(Exception):
+    """eo_locate does not restate merged multi-row runs (k >= 2)."""
+
+
+def locate_from_u(lam, u, signs):
+    """Location vector over the reference deflation record's poles (oracle)."""
+    lam, u, signs = _f64(lam), _f64(u), _i32(signs)
+    n, k = u.shape
+    out = np.zeros(n + 1, np.int64)
+    cnt = np.zeros(1, np.int64)
+    rc = lib().eo_locate(_D(lam), _D(u), _I(signs), C.c_int64(n), C.c_int64(k), _L(out),
+                         _L(cnt))
+    if rc == 1:
+        raise ValueError("eo_locate: invalid argument")
+    if rc == 3:
+        raise LocateUnsupported("merged multi-row run")
+    return [int(v) for v in out[: int(cnt[0])]]

@@ -250,3 +250,45 @@ def dnc_solve(poles, weights, lo, hi, expected, tol):
                            C.c_double(hi), C.c_int64(expected), C.c_double(tol), _D(out), _L(nr),
                            buf, 1024), buf)
     return out[: int(nr[0])].copy()
+
+
+def locate_from_u(lam, u, signs):
+    """tools/eigmod.cpp:143-161 (cmd_locate) after transform_update: the
+    reference's deflate_problem + locate_rank2 / locate_rank_k counts."""
+    lam, u, signs = _f64(lam), _f64(u), _i32(signs)
+    n, k = u.shape
+    out = np.zeros(n + 1, np.int64)
+    cnt = np.zeros(1, np.int64)
+    buf = C.create_string_buffer(512)
+    _check(lib().ref_locate_from_u(_D(lam), _D(u), _I(signs), C.c_int64(n), C.c_int64(k),
+                                   _L(out), _L(cnt), buf, C.c_size_t(512)), buf)
+    return [int(v) for v in out[: int(cnt[0])]]
+
+
+def reconstruct(q, lam):
+    """core.hpp:11 — Q diag(lambda) Q^T, symmetrized (kernels.cpp:98-109)."""
+    q, lam = _f64(q), _f64(lam)
+    n = lam.shape[0]
+    out = np.empty((n, n))
+    buf = C.create_string_buffer(512)
+    _check(lib().ref_reconstruct(_D(q), _D(lam), C.c_int64(n), _D(out), buf, C.c_size_t(512)), buf)
+    return out
+
+
+def apply_update(a, kmat, signs):
+    """core.hpp:14 — a + sum_r s_r k_r k_r^T, symmetrized (core.cpp:105-115)."""
+    a, kmat, signs = _f64(a), _f64(kmat), _i32(signs)
+    n, k = kmat.shape
+    out = np.empty((n, n))
+    buf = C.create_string_buffer(512)
+    _check(lib().ref_apply_update(_D(a), _D(kmat), _I(signs), C.c_int64(n), C.c_int64(k),
+                                  _D(out), buf, C.c_size_t(512)), buf)
+    return out
+
+
+def ortho_error(a):
+    """kernels.hpp:36 — max |A^T A - I| (kernels.cpp:150-154)."""
+    a = _f64(a)
+    f = lib().ref_ortho_error
+    f.restype = C.c_double
+    return float(f(_D(a), C.c_int64(a.shape[0]), C.c_int64(a.shape[1])))

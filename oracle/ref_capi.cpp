@@ -12,6 +12,9 @@
 //   update_decomposition      proj/include/eigmod/eigvec.hpp:35-36
 //   random_instance           proj/include/eigmod/core.hpp:17-20
 //   jacobi_evd                proj/include/eigmod/baseline.hpp:15
+//   locate (CLI path)         proj/tools/eigmod.cpp:143-161 over locate.hpp:31,50
+//   reconstruct/apply_update  proj/include/eigmod/core.hpp:11-14
+//   ortho_error               proj/include/eigmod/kernels.hpp:36
 // Return codes follow the product C-ABI (include/eigmod_b200.h):
 // 0 ok, 1 std::invalid_argument, 2 NumericalError (stage in the message
 // buffer as "[stage] msg"), 4 any other exception.
@@ -27,6 +30,7 @@
 #include "eigmod/core.hpp"
 #include "eigmod/eigvec.hpp"
 #include "eigmod/kernels.hpp"
+#include "eigmod/locate.hpp"
 #include "eigmod/rootfind.hpp"
 #include "eigmod/secular.hpp"
 #include "eigmod/types.hpp"
@@ -148,6 +152,55 @@ int ref_deflate_problem(const double* lambda, const double* u, const int* signs,
     counts[1] = static_cast<std::int64_t>(dp.unchanged.size());
     counts[2] = static_cast<std::int64_t>(dp.collided.size());
   });
+}
+
+// Location vector of the CLI locate path: transform_update is the caller's
+// (u given), then deflate_problem and locate_rank2 / locate_rank_k exactly as
+// cmd_locate does. counts_out holds n + 1 entries.
+int ref_locate_from_u(const double* lambda, const double* u, const int* signs, std::int64_t n,
+                      std::int64_t k, std::int64_t* counts_out, std::int64_t* ncounts_out,
+                      char* msg, std::size_t len) {
+  return guarded(msg, len, [&] {
+    const Vec lam(lambda, lambda + n);
+    const TransformedUpdate tu = to_tu(u, signs, n, k);
+    const DeflatedProblem dp = deflate_problem(lam, tu);
+    LocationVector loc;
+    if (dp.coeffs.size() == 0) {
+      loc.counts.assign(1, 0);
+    } else if (tu.rank() == 2) {
+      loc = locate_rank2(dp.coeffs, classify_shift(tu.signs));
+    } else {
+      loc = locate_rank_k(dp.coeffs, tu.signs).loc;
+    }
+    for (std::size_t i = 0; i < loc.counts.size(); ++i) counts_out[i] = loc.counts[i];
+    *ncounts_out = static_cast<std::int64_t>(loc.counts.size());
+  });
+}
+
+// core.hpp:11 reconstruct (Q diag(lambda) Q^T, symmetrized) and core.hpp:14
+// apply_update (a + sum_r s_r k_r k_r^T, symmetrized); kernels.hpp:36
+// ortho_error (max |A^T A - I|).
+int ref_reconstruct(const double* q, const double* lambda, std::int64_t n, double* out,
+                    char* msg, std::size_t len) {
+  return guarded(msg, len, [&] {
+    const SymmetricDense a = reconstruct(to_decomp(q, lambda, n));
+    std::memcpy(out, a.entries.data(), sizeof(double) * n * n);
+  });
+}
+
+int ref_apply_update(const double* a, const double* kmat, const int* signs, std::int64_t n,
+                     std::int64_t k, double* out, char* msg, std::size_t len) {
+  return guarded(msg, len, [&] {
+    SymmetricDense s;
+    s.n = static_cast<std::size_t>(n);
+    s.entries = to_matrix(a, n, n);
+    const SymmetricDense r = apply_update(s, to_update(kmat, signs, n, k));
+    std::memcpy(out, r.entries.data(), sizeof(double) * n * n);
+  });
+}
+
+double ref_ortho_error(const double* a, std::int64_t rows, std::int64_t cols) {
+  return kernels::ortho_error(to_matrix(a, rows, cols));
 }
 
 double ref_default_tolerance(const double* lambda, const double* kmat, const int* signs,

@@ -15,6 +15,8 @@ from .capi import (  # noqa: F401
     default_tolerance,
     deflate_problem,
     gemm_nt_device,
+    locate,
+    locate_from_u,
     padded_rank,
     record_width,
     secular_weights,

@@ -69,6 +69,10 @@ def _declare(lib):
         "eigmod_b200_secular_weights": (C.c_int, [_VP, _D, _D, _I32, C.c_int64, C.c_int64, _D]),
         "eigmod_b200_deflate_problem": (C.c_int, [_VP, _D, _D, _I32, C.c_int64, C.c_int64, _D, _D,
                                                   _I64, _I64, _I64, _I64]),
+        "eigmod_b200_locate": (C.c_int, [_VP, _D, _D, _D, _I32, C.c_int64, C.c_int64, _I64,
+                                         _I64]),
+        "eigmod_b200_locate_from_u": (C.c_int, [_VP, _D, _D, _I32, C.c_int64, C.c_int64, _I64,
+                                                _I64]),
         "eigmod_b200_update_eigenvalues": (C.c_int, [_VP, _D, _D, _D, _I32, C.c_int64, C.c_int64,
                                                      C.c_double, _D, _D, _I64, _D, _I64, _I64]),
         "eigmod_b200_update_decomposition": (C.c_int, [_VP, _D, _D, _D, _I32, C.c_int64,
@@ -295,6 +299,38 @@ def deflate_problem(lam, u, signs, ctx: Context | None = None) -> DeflatedProble
     m, nu, nc = (int(x) for x in cnt)
     return DeflatedProblem(poles[:m].copy(), w[:m].copy(), po[:m].copy(), un[:nu].copy(),
                            co[:nc].copy())
+
+
+def locate(q, lam, kmat, signs, ctx: Context | None = None) -> list[int]:
+    """Location vector of the CLI locate path (tools/eigmod.cpp:143-161):
+    transform -> deflate -> per-interval root counts over the deflated poles
+    (locate.hpp:13-50). Returns N + 1 counts ([0] when every pole deflates)."""
+    ctx = ctx or default_context()
+    q, lam, kmat, signs = _f64(q), _f64(lam), _f64(kmat), _i32(signs)
+    _check_update(q, lam, kmat, signs)
+    n, k = kmat.shape
+    out = np.zeros(n + 1, np.int64)
+    cnt = np.zeros(1, np.int64)
+    ctx.check(ctx._l.eigmod_b200_locate(ctx.h, _dp(q), _dp(lam), _dp(kmat),
+                                        signs.ctypes.data_as(_I32), n, k,
+                                        out.ctypes.data_as(_I64), cnt.ctypes.data_as(_I64)))
+    return [int(v) for v in out[: int(cnt[0])]]
+
+
+def locate_from_u(lam, u, signs, ctx: Context | None = None) -> list[int]:
+    """locate() from U = Q^T K."""
+    ctx = ctx or default_context()
+    lam, u, signs = _f64(lam), _f64(u), _i32(signs)
+    if u.ndim != 2 or lam.shape[0] != u.shape[0] or signs.shape[0] != u.shape[1]:
+        raise ValueError("locate: dimension mismatch")
+    n, k = u.shape
+    out = np.zeros(n + 1, np.int64)
+    cnt = np.zeros(1, np.int64)
+    ctx.check(ctx._l.eigmod_b200_locate_from_u(ctx.h, _dp(lam), _dp(u),
+                                               signs.ctypes.data_as(_I32), n, k,
+                                               out.ctypes.data_as(_I64),
+                                               cnt.ctypes.data_as(_I64)))
+    return [int(v) for v in out[: int(cnt[0])]]
 
 
 def _check_update(q, lam, kmat, signs):

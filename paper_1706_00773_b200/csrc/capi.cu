@@ -86,6 +86,13 @@ void check_ascending(const double* lam, int64_t n) {
       throw Error(2, "deflate", "deflate_problem: eigenvalues not ascending");
 }
 
+void check_ascending_invalid(const double* lam, int64_t n) {
+  // proj/src/secular.cpp:281-283 called directly (the CLI locate path)
+  for (int64_t i = 0; i + 1 < n; ++i)
+    if (!(lam[i] <= lam[i + 1]))
+      throw Error(1, "", "deflate_problem: eigenvalues not ascending");
+}
+
 template <class F>
 int guarded(eigmod_b200_ctx* ctx, F&& f) {
   if (!ctx) return EIGMOD_B200_INVALID_ARGUMENT;
@@ -304,6 +311,72 @@ void full_device(eigmod_b200_ctx* c, const double* q, const double* lam, const d
     }
     c->timed_calls += 1;
   }
+}
+
+// Location vector over the parity-deflated poles (tools/eigmod.cpp:143-161,
+// proj/include/eigmod/locate.hpp:13-50): the plan must be built with the
+// reference's run threshold. counts[i] = eigenvalues of the deflated problem
+// in (v_{i-1}, v_i), v the poles of the deflation record (groups of kind 0).
+// Collided poles (kind 2) are no boundaries and their roots are not counted,
+// as in the reference, where they leave the secular coefficients.
+int64_t locate_counts(eigmod_b200_ctx* c, int64_t* counts_out) {
+  const eigb::Plan& p = c->plan;
+  auto st = c->stream;
+  if (p.k == 0 || p.nred == 0 || p.ng == 0) {
+    counts_out[0] = 0;
+    return 1;
+  }
+  const int64_t ng = p.ng;
+  std::vector<int> kd(ng);
+  std::vector<int64_t> gl(ng), rk(ng), offr(ng);
+  std::vector<double> gv(ng);
+  EIGB_CUDA(cudaMemcpyAsync(kd.data(), p.kind, 4 * ng, cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaMemcpyAsync(gl.data(), p.glen, 8 * ng, cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaMemcpyAsync(rk.data(), p.rank, 8 * ng, cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaMemcpyAsync(offr.data(), p.off_red, 8 * ng, cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaMemcpyAsync(gv.data(), p.gval, 8 * ng, cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaStreamSynchronize(st));
+  std::vector<double> bval;
+  std::vector<int64_t> brow, below;
+  std::vector<int> bcnt;
+  int64_t pt = 0;
+  for (int64_t g = 0; g < ng; ++g) {
+    if (kd[g] != 0) continue;
+    const int cnt = (int)(gl[g] == 1 ? 1 : rk[g]);
+    bval.push_back(gv[g]);
+    brow.push_back(offr[g]);
+    bcnt.push_back(cnt);
+    below.push_back(pt);
+    pt += cnt;
+  }
+  const int64_t nb = (int64_t)bval.size();
+  if (nb == 0) {
+    counts_out[0] = 0;
+    return 1;
+  }
+  double* dv = c->ws.get_f64("loc_val", nb);
+  int64_t* dr = c->ws.get_i64("loc_row", nb);
+  int* dc = c->ws.get_i32("loc_cnt", nb);
+  int* dnu = c->ws.get_i32("loc_nu", nb);
+  EIGB_CUDA(cudaMemcpyAsync(dv, bval.data(), 8 * nb, cudaMemcpyHostToDevice, st));
+  EIGB_CUDA(cudaMemcpyAsync(dr, brow.data(), 8 * nb, cudaMemcpyHostToDevice, st));
+  EIGB_CUDA(cudaMemcpyAsync(dc, bcnt.data(), 4 * nb, cudaMemcpyHostToDevice, st));
+  eigb::pole_inertia(p.view(), dv, dr, dc, nb, dnu, c->ws, st);
+  std::vector<int> nu(nb);
+  EIGB_CUDA(cudaMemcpyAsync(nu.data(), dnu, 4 * nb, cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaStreamSynchronize(st));
+  // eigenvalue count below each boundary, collided roots excluded
+  int64_t prev = 0;
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t cb = below[b] + p.m_neg - nu[b];
+    counts_out[b] = cb - prev;
+    prev = cb;
+  }
+  counts_out[nb] = pt - prev;
+  for (int64_t b = 0; b <= nb; ++b)
+    if (counts_out[b] < 0)
+      throw Error(2, "locate", "inertia counts are not monotone (degenerate pole)");
+  return nb + 1;
 }
 
 }  // namespace
@@ -584,6 +657,49 @@ int eigmod_b200_deflate_problem(eigmod_b200_ctx* ctx, const double* lambda, cons
     counts[0] = np;
     counts[1] = nu;
     counts[2] = nc;
+  });
+}
+
+int eigmod_b200_locate_from_u(eigmod_b200_ctx* ctx, const double* lambda, const double* u,
+                              const int* signs, int64_t n, int64_t k, int64_t* counts_out,
+                              int64_t* ncounts_out) {
+  return guarded(ctx, [&] {
+    check_basic(n, k, signs);
+    check_finite(u, n * k, "U");
+    check_ascending_invalid(lambda, n);
+    auto st = ctx->stream;
+    const int kp = eigb::padded_rank(k);
+    std::vector<double> up((size_t)n * kp, 0.0);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t c = 0; c < k; ++c) up[i * kp + c] = u[i * k + c];
+    double* dl = ctx->ws.get_f64("h_l", n);
+    double* du = ctx->ws.get_f64("h_u", (size_t)n * kp);
+    EIGB_CUDA(cudaMemcpyAsync(dl, lambda, 8 * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(du, up.data(), 8 * up.size(), cudaMemcpyHostToDevice, st));
+    plan_from_u(ctx, dl, du, signs, n, k, eigb::kPoleMergeRelGap);
+    *ncounts_out = locate_counts(ctx, counts_out);
+  });
+}
+
+int eigmod_b200_locate(eigmod_b200_ctx* ctx, const double* q, const double* lambda,
+                       const double* kmat, const int* signs, int64_t n, int64_t k,
+                       int64_t* counts_out, int64_t* ncounts_out) {
+  return guarded(ctx, [&] {
+    check_basic(n, k, signs);
+    check_finite(kmat, n * k, "K");
+    check_ascending_invalid(lambda, n);
+    auto st = ctx->stream;
+    const int kp = eigb::padded_rank(k);
+    double* dq = ctx->ws.get_f64("h_q", (size_t)n * n);
+    double* dl = ctx->ws.get_f64("h_l", n);
+    double* dk = ctx->ws.get_f64("h_k", (size_t)n * k);
+    double* du = ctx->ws.get_f64("h_u", (size_t)n * kp);
+    EIGB_CUDA(cudaMemcpyAsync(dq, q, 8 * n * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dl, lambda, 8 * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dk, kmat, 8 * n * k, cudaMemcpyHostToDevice, st));
+    project(ctx, dq, dk, n, k, 0, n, du);
+    plan_from_u(ctx, dl, du, signs, n, k, eigb::kPoleMergeRelGap);
+    *ncounts_out = locate_counts(ctx, counts_out);
   });
 }
 

@@ -726,6 +726,115 @@ void launch_weights(const double* rep, const double* u, int64_t n, const int64_t
   EIGB_LAUNCH_CHECK();
 }
 
+// ------------------------------------------------------- pole inertia (locate)
+// For the location vector (proj/include/eigmod/locate.hpp:13-50; SURVEY.md
+// §8(f)3): at a reduced pole value v with rows R (the pole's own rows of U),
+// S(x) = T + sum_{r in R} u_r u_r^T / (v - x) with T = J + sum over the other
+// rows. As x -> v from below the R-terms add |R| positive eigenvalues, so
+// nu(S(v-)) = nu(T restricted to span(R)^perp), and the eigenvalue count below
+// v is #{d < v} + m - that inertia. One pole pass per batch of 32 poles (the
+// pole's own rows excluded as exact zero differences), then per pole the
+// Householder reflections that map span(R) onto the leading coordinates and a
+// Bunch-Kaufman inertia of the trailing block.
+template <int KP>
+struct InertiaArgs {
+  ReducedView rp;
+  const double* bval;   // pole value per boundary
+  const int64_t* brow;  // first reduced row of the pole
+  const int* bcnt;      // number of rows at the pole
+  int64_t nb;
+  int* nu;              // out: inertia of the projected T
+  double* scratch;      // gridDim.x * 32 * (2 * KP * KP + KP)
+};
+
+template <int KP>
+__global__ void __launch_bounds__(kPassThreads, 1) pole_inertia_kernel(InertiaArgs<KP> a) {
+  using C = PassCfg<KP>;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double dob[32], delta[32];
+  __shared__ int active[32], hit[32];
+  const int t = threadIdx.x;
+  const int64_t g0 = (int64_t)blockIdx.x * 32;
+  if (t < 32) {
+    const int64_t g = g0 + t;
+    active[t] = g < a.nb;
+    dob[t] = 0.0;
+    delta[t] = (g < a.nb) ? a.bval[g] : 0.0;
+    hit[t] = 0;
+  }
+  __syncthreads();
+  PassSlots sl{dob, delta, nullptr, active, hit};
+  PassOpts o;
+  o.exclude_zero = true;
+  secular_pass<KP>(a.rp.d, a.rp.u, a.rp.n, sl, o, smem);
+  if (t >= 32 || !active[t]) return;
+  const int64_t g = g0 + t;
+  const int k = a.rp.k;
+  double* T = a.scratch + ((size_t)blockIdx.x * 32 + t) * (2 * KP * KP + KP);
+  double* W = T + KP * KP;   // reflectors, one per row of R
+  double* x = W + KP * KP;
+  const double* rb = pass_result<KP>(smem) + t * C::OUT;
+  load_S<KP>(rb, a.rp.sgn, k, T, 1);
+  // Householder vectors of span(R): reflector q acts on coordinates q..k-1
+  int q = 0;
+  const int64_t r0 = a.brow[g];
+  for (int r = 0; r < a.bcnt[g] && q < k; ++r) {
+    const double* v = a.rp.u + (r0 + r) * KP;
+    double vn = 0.0;
+    for (int c = 0; c < k; ++c) x[c] = v[c], vn += v[c] * v[c];
+    for (int p = 0; p < q; ++p) {  // apply earlier reflectors
+      const double* w = W + p * KP;
+      double dw = 0.0;
+      for (int c = p; c < k; ++c) dw += w[c] * x[c];
+      for (int c = p; c < k; ++c) x[c] -= 2.0 * dw * w[c];
+    }
+    double tn = 0.0;
+    for (int c = q; c < k; ++c) tn += x[c] * x[c];
+    if (!(tn > 1e-28 * vn)) continue;  // dependent row: span unchanged
+    const double al = (x[q] >= 0.0) ? -sqrt(tn) : sqrt(tn);
+    double* w = W + q * KP;
+    for (int c = 0; c < q; ++c) w[c] = 0.0;
+    for (int c = q; c < k; ++c) w[c] = x[c];
+    w[q] -= al;
+    double wn = 0.0;
+    for (int c = q; c < k; ++c) wn += w[c] * w[c];
+    const double inv = rsqrt(wn);
+    for (int c = q; c < k; ++c) w[c] *= inv;
+    // T <- H T H, H = I - 2 w w^T
+    for (int rr = 0; rr < k; ++rr) {  // T <- T H (rows)
+      double dw = 0.0;
+      for (int c = q; c < k; ++c) dw += T[rr * KP + c] * w[c];
+      for (int c = q; c < k; ++c) T[rr * KP + c] -= 2.0 * dw * w[c];
+    }
+    for (int cc = 0; cc < k; ++cc) {  // T <- H T (columns)
+      double dw = 0.0;
+      for (int c = q; c < k; ++c) dw += w[c] * T[c * KP + cc];
+      for (int c = q; c < k; ++c) T[c * KP + cc] -= 2.0 * dw * w[c];
+    }
+    ++q;
+  }
+  int neg = 0;
+  if (q < k) {
+    int piv[KP], zero;
+    neg = bk_factor(T + q * KP + q, k - q, KP, piv, &zero, 1);
+  }
+  a.nu[g] = neg;
+}
+
+template <int KP>
+void launch_inertia(const ReducedView& rp, const double* bval, const int64_t* brow,
+                    const int* bcnt, int64_t nb, int* nu, DeviceScratch& ws, cudaStream_t st) {
+  using C = PassCfg<KP>;
+  const int grid = (int)cdiv(nb, 32);
+  InertiaArgs<KP> a{rp, bval, brow, bcnt, nb, nu, nullptr};
+  a.scratch = ws.get_f64("inertia_scratch", (size_t)grid * 32 * (2 * KP * KP + KP));
+  const size_t sm = sizeof(double) * C::SMEM_DOUBLES;
+  EIGB_CUDA(cudaFuncSetAttribute(pole_inertia_kernel<KP>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  pole_inertia_kernel<KP><<<grid, kPassThreads, sm, st>>>(a);
+  EIGB_LAUNCH_CHECK();
+}
+
 }  // namespace
 
 void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t j1,
@@ -777,6 +886,20 @@ void group_weights(int kp, const double* rep, const double* u, int64_t n, const 
     case 16: launch_weights<16>(rep, u, n, gstart, glen, gval, ng, sgn, k, alpha, ws, st); break;
     case 32: launch_weights<32>(rep, u, n, gstart, glen, gval, ng, sgn, k, alpha, ws, st); break;
     default: throw Error(1, "", "group_weights: unsupported padded rank");
+  }
+}
+
+void pole_inertia(const ReducedView& rp, const double* bval, const int64_t* brow, const int* bcnt,
+                  int64_t nb, int* nu, DeviceScratch& ws, cudaStream_t st) {
+  if (nb <= 0) return;
+  switch (rp.kp) {
+    case 1: launch_inertia<1>(rp, bval, brow, bcnt, nb, nu, ws, st); break;
+    case 2: launch_inertia<2>(rp, bval, brow, bcnt, nb, nu, ws, st); break;
+    case 4: launch_inertia<4>(rp, bval, brow, bcnt, nb, nu, ws, st); break;
+    case 8: launch_inertia<8>(rp, bval, brow, bcnt, nb, nu, ws, st); break;
+    case 16: launch_inertia<16>(rp, bval, brow, bcnt, nb, nu, ws, st); break;
+    case 32: launch_inertia<32>(rp, bval, brow, bcnt, nb, nu, ws, st); break;
+    default: throw Error(1, "", "pole_inertia: unsupported padded rank");
   }
 }
 

@@ -101,6 +101,13 @@ void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t
                  const RootRecords& out, const SolveOptions& opt, DeviceScratch& ws, int sms,
                  cudaStream_t st);
 
+// Location-vector support: for each of nb reduced pole values bval[b] (rows
+// brow[b] .. brow[b]+bcnt[b]-1 of rp sit at that value), nu[b] = negative
+// inertia of T = J + sum_{other rows} u u^T/(d - v) restricted to the
+// orthogonal complement of the pole's rows. #eig < v = #{d < v} + m - nu.
+void pole_inertia(const ReducedView& rp, const double* bval, const int64_t* brow, const int* bcnt,
+                  int64_t nb, int* nu, DeviceScratch& ws, cudaStream_t st);
+
 void group_weights(int kp, const double* rep, const double* u, int64_t n, const int64_t* gstart,
                    const int64_t* glen, const double* gval, int64_t ng, const int* sgn, int k,
                    double* alpha, DeviceScratch& ws, cudaStream_t st);

@@ -5,7 +5,8 @@ Run in the build container (where /root/reference exists and
 
     python tests/golden/make_golden.py
 
-Writes tests/golden/ref_seeded.npz and tests/golden/ref_cases.npz. Inputs
+Writes tests/golden/ref_seeded.npz, ref_cases.npz and ref_locate.npz
+(`--only-locate` rewrites the last one alone). Inputs
 are stored next to the reference outputs so the fixtures do not depend on
 LAPACK bits of the machine that replays them. The GPU box never reads
 /root/reference: it only reads these files.
@@ -46,7 +47,82 @@ def run_case(q, lam, kmat, signs, tol=None):
     return out
 
 
+def _truth_counts(q, lam, kmat, signs, dp):
+    """Eigenvalues of A' = Q diag(lam) Q^T + K J K^T per open interval of the
+    deflated poles (the check of tests/test_locate.cpp: classify_intervals over
+    oracle_eigenvalues), by LAPACK. Eigenvalues of deflated pairs (unchanged
+    and collided poles, which leave the secular coefficients) are removed,
+    each as the eigenvalue nearest its pole."""
+    poles = dp["poles"]
+    a = (q * lam) @ q.T + (kmat * np.asarray(signs, float)) @ kmat.T
+    ev = list(np.linalg.eigvalsh(0.5 * (a + a.T)))
+    for i in list(dp["unchanged"]) + list(dp["collided"]):
+        ev.pop(int(np.argmin(np.abs(np.asarray(ev) - lam[i]))))
+    ev = np.asarray(ev)
+    edges = np.concatenate([[-np.inf], poles, [np.inf]])
+    return np.array([int(((ev > edges[i]) & (ev < edges[i + 1])).sum())
+                     for i in range(len(poles) + 1)], np.int64)
+
+
+def make_locate():
+    """Location-vector fixtures (CLI locate path, tools/eigmod.cpp:143-161),
+    instance families of tests/test_locate.cpp:80-200 plus a random mixed-sign
+    family: inputs (lam, u, signs), the reference's counts (or its error) and
+    the LAPACK interval counts."""
+    out = {}
+    idx = 0
+
+    def add(q, lam, kmat, signs, family):
+        nonlocal idx
+        signs = np.asarray(signs, np.int32)
+        u = ref.transform_update(q, lam, kmat, signs)
+        dp = ref.deflate_problem(lam, u, signs)
+        try:
+            counts = np.array(ref.locate_from_u(lam, u, signs), np.int64)
+            status = "ok"
+        except Exception as e:  # the reference's own failure, recorded
+            counts = np.zeros(0, np.int64)
+            status = f"{type(e).__name__}: {e}"
+        key = f"L{idx}"
+        out[key + "__lam"] = lam
+        out[key + "__u"] = u
+        out[key + "__signs"] = signs
+        out[key + "__ref"] = counts
+        out[key + "__status"] = np.array(status)
+        out[key + "__truth"] = _truth_counts(q, lam, kmat, signs, dp)
+        out[key + "__family"] = np.array(family)
+        idx += 1
+
+    kinds = {"double_right": [1, 1], "double_left": [-1, -1], "mixed": [1, -1]}
+    for ki, (kind, sg) in enumerate(kinds.items()):  # test_locate.cpp:80-115
+        for seed in range(0, 100, 4):
+            q, lam, kmat = ref.random_instance(4, 2, 0.9, seed * 3 + ki)
+            add(q, lam, kmat, sg, "rank2_" + kind)
+    q, lam, kmat = ref.random_instance(5, 1, 0.8, 31)  # :156-165
+    add(q, lam, kmat, [1], "rank1_classic")
+    for seed in range(40):  # :167-181
+        q, lam, kmat = ref.random_instance(10, 3, 1.2, seed + 70)
+        add(q, lam, kmat, [1, -1 if seed % 2 else 1, 1 if seed % 3 else -1], "rank3")
+    for seed in range(0, 60, 2):  # :183-200 sizes
+        n = 4 + seed % 17
+        sg = list(kinds.values())[seed % 3]
+        q, lam, kmat = ref.random_instance(n, 2, 0.8 + 0.05 * (seed % 5), seed + 1300)
+        add(q, lam, kmat, sg, "rank2_sizes")
+    rng = np.random.default_rng(170600773)
+    for t in range(40):  # random mixed signs, n <= 60, k <= 6
+        n, k = int(rng.integers(6, 61)), int(rng.integers(1, 7))
+        q, lam, kmat = ref.random_instance(n, k, float(rng.uniform(0.2, 3.0)), 7000 + t)
+        add(q, lam, kmat, rng.choice([-1, 1], k), "mixed_random")
+    q, lam, kmat = ref.random_instance(5, 1, 0.8, 31)  # null update
+    add(q, lam, np.zeros_like(kmat), [1], "null_update")
+    np.savez_compressed(os.path.join(HERE, "ref_locate.npz"), **out)
+    print("locate fixtures:", idx)
+
+
 def main():
+    if "--only-locate" in sys.argv:
+        make_locate()
+        return
     ref.set_parallel(False)
     seeded = {}
     for cfg in (0, 1, 2, 3, 4):
@@ -81,6 +157,7 @@ def main():
             if key in c:
                 cases[f"r2_{t}__{key}"] = c[key]
     np.savez_compressed(os.path.join(HERE, "ref_cases.npz"), **cases)
+    make_locate()
     print("wrote", os.listdir(HERE))
 
 
