@@ -120,6 +120,30 @@ int eigmod_b200_locate_from_u(eigmod_b200_ctx* ctx, const double* lambda, const 
                               const int* signs, int64_t n, int64_t k, int64_t* counts_out,
                               int64_t* ncounts_out);
 
+/* Validation products on the K5 DMMA GEMM:
+ * reconstruct   replaces core.hpp:11 (kernels.cpp:98-109): A = Q diag(lambda)
+ *               Q^T, symmetrized; a_out n x n.
+ * apply_update  replaces core.hpp:14 (core.cpp:105-115): a + sum_r s_r k_r
+ *               k_r^T, symmetrized; bit-identical to the reference's rounding
+ *               sequence. a must be symmetric (a SymmetricDense).
+ * ortho_error   replaces kernels.hpp:36 (kernels.cpp:150-154): max |A^T A - I|
+ *               for A rows x cols.
+ * The *_device forms take device pointers and run on the context's stream
+ * (signs stay host int32). */
+int eigmod_b200_reconstruct(eigmod_b200_ctx* ctx, const double* q, const double* lambda, int64_t n,
+                            double* a_out);
+int eigmod_b200_reconstruct_device(eigmod_b200_ctx* ctx, const double* d_q,
+                                   const double* d_lambda, int64_t n, double* d_a_out);
+int eigmod_b200_apply_update(eigmod_b200_ctx* ctx, const double* a, const double* kmat,
+                             const int* signs, int64_t n, int64_t k, double* a_out);
+int eigmod_b200_apply_update_device(eigmod_b200_ctx* ctx, const double* d_a,
+                                    const double* d_kmat, const int* signs, int64_t n, int64_t k,
+                                    double* d_a_out);
+int eigmod_b200_ortho_error(eigmod_b200_ctx* ctx, const double* a, int64_t rows, int64_t cols,
+                            double* err_out);
+int eigmod_b200_ortho_error_device(eigmod_b200_ctx* ctx, const double* d_a, int64_t rows,
+                                   int64_t cols, double* err_out);
+
 /* Eigenvalue stage (replaces update_eigenvalues_full, rootfind.hpp:51-53 /
  * rootfind.cpp:381-472, for both the rank-2 and the general rank-k entry):
  * values_out (n, ascending), roots_out (n; the first *nroots_out are the

@@ -7,7 +7,8 @@
 // libeigmod.a. Value semantics and exception types are the reference's:
 // std::invalid_argument for preconditions, eigmod::NumericalError(stage, msg)
 // for numerical failures; device failures surface as std::runtime_error.
-// Everything O(n^2) and above runs on the GPU; there is no CPU fallback.
+// Everything O(n^2 k) and above runs on the GPU; there is no CPU fallback
+// (the host keeps the reference's O(n^2) SymmetricDense::from symmetrization).
 #pragma once
 
 #include <cstddef>
@@ -91,9 +92,30 @@ class NumericalError : public std::runtime_error {
 
 void validate_update(const SpectralDecomposition& d, const LowRankUpdate& u);
 
-// core.hpp — validation helpers (GPU GEMMs)
+// core.hpp:11-14 — validation helpers (GPU: DMMA GEMM / rank-k kernel)
 SymmetricDense reconstruct(const SpectralDecomposition& d);
 SymmetricDense apply_update(const SymmetricDense& a, const LowRankUpdate& u);
+
+// locate.hpp:13-24 — root counts per interval cut by the deflated poles.
+struct LocationVector {
+  std::vector<long> counts;
+  long total() const {
+    long s = 0;
+    for (long c : counts) s += c;
+    return s;
+  }
+};
+// locate.hpp:27-28
+enum class ShiftKind { double_right, double_left, mixed };
+ShiftKind classify_shift(const std::vector<int>& signs);
+// locate.hpp:33-39
+std::pair<double, double> interlacing_bounds(std::size_t index, const Vec& lambda,
+                                             std::size_t rank, const std::vector<int>& signs);
+// The CLI locate path (tools/eigmod.cpp:143-161: transform_update ->
+// deflate_problem -> locate_rank2 / locate_rank_k) on the GPU. The reference's
+// locate_rank2 / locate_rank_k take only the merged scalar coefficients; the
+// GPU counts from U (exact inertia at the poles), so its entry takes the update.
+LocationVector locate_update(const SpectralDecomposition& d, const LowRankUpdate& u);
 
 // secular.hpp:9-17
 struct SecularCoefficients {
@@ -157,6 +179,8 @@ UpdateResult update_decomposition(const SpectralDecomposition& d, const LowRankU
 
 // kernels.hpp:9-13 — the OpenMP toggle has no meaning on the GPU path.
 namespace kernels {
+// kernels.hpp:36 — max |A^T A - I| (GPU DMMA GEMM)
+double ortho_error(const Matrix& a);
 void set_parallel(bool on);
 bool parallel();
 int worker_count();

@@ -15,8 +15,11 @@ from .capi import (  # noqa: F401
     default_tolerance,
     deflate_problem,
     gemm_nt_device,
+    apply_update,
     locate,
     locate_from_u,
+    ortho_error,
+    reconstruct,
     padded_rank,
     record_width,
     secular_weights,

@@ -73,6 +73,13 @@ def _declare(lib):
                                          _I64]),
         "eigmod_b200_locate_from_u": (C.c_int, [_VP, _D, _D, _I32, C.c_int64, C.c_int64, _I64,
                                                 _I64]),
+        "eigmod_b200_reconstruct": (C.c_int, [_VP, _D, _D, C.c_int64, _D]),
+        "eigmod_b200_reconstruct_device": (C.c_int, [_VP, _VP, _VP, C.c_int64, _VP]),
+        "eigmod_b200_apply_update": (C.c_int, [_VP, _D, _D, _I32, C.c_int64, C.c_int64, _D]),
+        "eigmod_b200_apply_update_device": (C.c_int, [_VP, _VP, _VP, _I32, C.c_int64, C.c_int64,
+                                                      _VP]),
+        "eigmod_b200_ortho_error": (C.c_int, [_VP, _D, C.c_int64, C.c_int64, _D]),
+        "eigmod_b200_ortho_error_device": (C.c_int, [_VP, _VP, C.c_int64, C.c_int64, _D]),
         "eigmod_b200_update_eigenvalues": (C.c_int, [_VP, _D, _D, _D, _I32, C.c_int64, C.c_int64,
                                                      C.c_double, _D, _D, _I64, _D, _I64, _I64]),
         "eigmod_b200_update_decomposition": (C.c_int, [_VP, _D, _D, _D, _I32, C.c_int64,
@@ -331,6 +338,44 @@ def locate_from_u(lam, u, signs, ctx: Context | None = None) -> list[int]:
                                                out.ctypes.data_as(_I64),
                                                cnt.ctypes.data_as(_I64)))
     return [int(v) for v in out[: int(cnt[0])]]
+
+
+def reconstruct(q, lam, ctx: Context | None = None) -> np.ndarray:
+    """core.hpp:11 — Q diag(lambda) Q^T, symmetrized (K5 DMMA GEMM)."""
+    ctx = ctx or default_context()
+    q, lam = _f64(q), _f64(lam)
+    n = lam.shape[0]
+    if q.shape != (n, n):
+        raise ValueError("reconstruct: dimension mismatch")
+    out = np.empty((n, n))
+    ctx.check(ctx._l.eigmod_b200_reconstruct(ctx.h, _dp(q), _dp(lam), n, _dp(out)))
+    return out
+
+
+def apply_update(a, kmat, signs, ctx: Context | None = None) -> np.ndarray:
+    """core.hpp:14 — a + sum_r s_r k_r k_r^T, symmetrized (bit-identical)."""
+    ctx = ctx or default_context()
+    a, kmat, signs = _f64(a), _f64(kmat), _i32(signs)
+    n, k = kmat.shape
+    if a.shape != (n, n):
+        raise ValueError("apply_update: dimension mismatch")
+    if signs.shape[0] != k:
+        raise ValueError("apply_update: signs size")
+    out = np.empty((n, n))
+    ctx.check(ctx._l.eigmod_b200_apply_update(ctx.h, _dp(a), _dp(kmat),
+                                              signs.ctypes.data_as(_I32), n, k, _dp(out)))
+    return out
+
+
+def ortho_error(a, ctx: Context | None = None) -> float:
+    """kernels.hpp:36 — max |A^T A - I| (K5 DMMA GEMM)."""
+    ctx = ctx or default_context()
+    a = _f64(a)
+    if a.ndim != 2:
+        raise ValueError("ortho_error: matrix expected")
+    out = np.zeros(1)
+    ctx.check(ctx._l.eigmod_b200_ortho_error(ctx.h, _dp(a), a.shape[0], a.shape[1], _dp(out)))
+    return float(out[0])
 
 
 def _check_update(q, lam, kmat, signs):

@@ -864,6 +864,78 @@ void update_metrics_dev(const double* q, const double* lam, const double* kmat, 
 
 extern "C" {
 
+int eigmod_b200_reconstruct(eigmod_b200_ctx* ctx, const double* q, const double* lambda, int64_t n,
+                            double* a_out) {
+  return guarded(ctx, [&] {
+    if (n < 1) throw Error(1, "", "reconstruct: dimension mismatch");
+    auto st = ctx->stream;
+    double* dq = ctx->ws.get_f64("h_q", (size_t)n * n);
+    double* dl = ctx->ws.get_f64("h_l", n);
+    double* da = ctx->ws.get_f64("h_qo", (size_t)n * n);
+    EIGB_CUDA(cudaMemcpyAsync(dq, q, 8 * n * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dl, lambda, 8 * n, cudaMemcpyHostToDevice, st));
+    eigb::reconstruct_dev(dq, dl, n, da, ctx->ws, st);
+    EIGB_CUDA(cudaMemcpyAsync(a_out, da, 8 * n * n, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int eigmod_b200_reconstruct_device(eigmod_b200_ctx* ctx, const double* d_q,
+                                   const double* d_lambda, int64_t n, double* d_a_out) {
+  return guarded(ctx, [&] {
+    if (n < 1) throw Error(1, "", "reconstruct: dimension mismatch");
+    eigb::reconstruct_dev(d_q, d_lambda, n, d_a_out, ctx->ws, ctx->stream);
+  });
+}
+
+int eigmod_b200_apply_update(eigmod_b200_ctx* ctx, const double* a, const double* kmat,
+                             const int* signs, int64_t n, int64_t k, double* a_out) {
+  return guarded(ctx, [&] {
+    check_basic(n, k, signs);
+    auto st = ctx->stream;
+    double* da = ctx->ws.get_f64("h_q", (size_t)n * n);
+    double* dk = ctx->ws.get_f64("h_k", (size_t)n * k);
+    int* ds = ctx->ws.get_i32("h_s", k);
+    double* dout = ctx->ws.get_f64("h_qo", (size_t)n * n);
+    EIGB_CUDA(cudaMemcpyAsync(da, a, 8 * n * n, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(dk, kmat, 8 * n * k, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(ds, signs, 4 * k, cudaMemcpyHostToDevice, st));
+    eigb::apply_update_dev(da, dk, ds, n, (int)k, dout, st);
+    EIGB_CUDA(cudaMemcpyAsync(a_out, dout, 8 * n * n, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int eigmod_b200_apply_update_device(eigmod_b200_ctx* ctx, const double* d_a,
+                                    const double* d_kmat, const int* signs, int64_t n, int64_t k,
+                                    double* d_a_out) {
+  return guarded(ctx, [&] {
+    check_basic(n, k, signs);
+    int* ds = ctx->ws.get_i32("h_s", k);
+    EIGB_CUDA(cudaMemcpyAsync(ds, signs, 4 * k, cudaMemcpyHostToDevice, ctx->stream));
+    eigb::apply_update_dev(d_a, d_kmat, ds, n, (int)k, d_a_out, ctx->stream);
+  });
+}
+
+int eigmod_b200_ortho_error(eigmod_b200_ctx* ctx, const double* a, int64_t rows, int64_t cols,
+                            double* err_out) {
+  return guarded(ctx, [&] {
+    if (rows < 1 || cols < 1) throw Error(1, "", "ortho_error: empty matrix");
+    auto st = ctx->stream;
+    double* da = ctx->ws.get_f64("h_q", (size_t)rows * cols);
+    EIGB_CUDA(cudaMemcpyAsync(da, a, 8 * rows * cols, cudaMemcpyHostToDevice, st));
+    *err_out = eigb::ortho_error_dev(da, rows, cols, ctx->ws, st);
+  });
+}
+
+int eigmod_b200_ortho_error_device(eigmod_b200_ctx* ctx, const double* d_a, int64_t rows,
+                                   int64_t cols, double* err_out) {
+  return guarded(ctx, [&] {
+    if (rows < 1 || cols < 1) throw Error(1, "", "ortho_error: empty matrix");
+    *err_out = eigb::ortho_error_dev(d_a, rows, cols, ctx->ws, ctx->stream);
+  });
+}
+
 int eigmod_b200_assemble_from_u(eigmod_b200_ctx* ctx, const double* q, const double* lambda,
                                 const double* u, const int* signs, int64_t n, int64_t k,
                                 double* lambda_out, double* q_out) {

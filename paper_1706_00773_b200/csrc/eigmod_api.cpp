@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <limits>
 #include <memory>
 #include <mutex>
 
@@ -99,27 +100,75 @@ void validate_update(const SpectralDecomposition& d, const LowRankUpdate& u) {
   if (!all_finite(u.kmat)) throw std::invalid_argument("LowRankUpdate: non-finite K");
 }
 
-// core.hpp: Q diag(lambda) Q^T on the DMMA GEMM, symmetrized.
+// core.hpp:11 — Q diag(lambda) Q^T on the DMMA GEMM, symmetrized on the GPU.
 SymmetricDense reconstruct(const SpectralDecomposition& d) {
   if (d.q.cols() != d.lambda.size()) throw std::invalid_argument("reconstruct: dimension mismatch");
   const std::size_t n = d.q.rows(), k = d.q.cols();
-  Matrix w(n, k), a(n, n);
-  for (std::size_t i = 0; i < n; ++i)
-    for (std::size_t j = 0; j < k; ++j) w(i, j) = d.q(i, j) * d.lambda[j];
-  if (n > 0) check(eigmod_b200_gemm_nt(ctx(), w.data(), d.q.data(), n, n, k, a.data()));
-  return SymmetricDense::from(symmetrized(a));
+  SymmetricDense s;
+  s.n = n;
+  s.entries = Matrix(n, n);
+  if (n == 0) return s;
+  if (k == n) {
+    check(eigmod_b200_reconstruct(ctx(), d.q.data(), d.lambda.data(), (int64_t)n,
+                                  s.entries.data()));
+  } else {  // rectangular Q (kernels.cpp:98-109 accepts n x k)
+    Matrix w(n, k);
+    for (std::size_t i = 0; i < n; ++i)
+      for (std::size_t j = 0; j < k; ++j) w(i, j) = d.q(i, j) * d.lambda[j];
+    check(eigmod_b200_gemm_nt(ctx(), w.data(), d.q.data(), n, n, k, s.entries.data()));
+    s.entries = symmetrized(s.entries);
+  }
+  if (!all_finite(s.entries)) throw std::invalid_argument("SymmetricDense: non-finite entries");
+  return s;
 }
 
+// core.hpp:14 — a + sum_r s_r k_r k_r^T, symmetrized; bit-identical to the
+// reference (GPU, reference rounding sequence).
 SymmetricDense apply_update(const SymmetricDense& a, const LowRankUpdate& u) {
   if (u.dim() != a.n) throw std::invalid_argument("apply_update: dimension mismatch");
   if (u.signs.size() != u.rank()) throw std::invalid_argument("apply_update: signs size");
-  Matrix out = a.entries;
-  for (std::size_t r = 0; r < u.rank(); ++r)
-    for (std::size_t i = 0; i < a.n; ++i) {
-      const double cvi = static_cast<double>(u.signs[r]) * u.kmat(i, r);
-      for (std::size_t j = 0; j < a.n; ++j) out(i, j) += cvi * u.kmat(j, r);
-    }
-  return SymmetricDense::from(out);
+  if (u.rank() == 0 || a.n == 0) return SymmetricDense::from(a.entries);
+  SymmetricDense s;
+  s.n = a.n;
+  s.entries = Matrix(a.n, a.n);
+  check(eigmod_b200_apply_update(ctx(), a.entries.data(), u.kmat.data(), u.signs.data(),
+                                 (int64_t)a.n, (int64_t)u.rank(), s.entries.data()));
+  if (!all_finite(s.entries)) throw std::invalid_argument("SymmetricDense: non-finite entries");
+  return s;
+}
+
+// locate.hpp:13-50 host utilities and the GPU location vector of the CLI
+// locate path (tools/eigmod.cpp:143-161).
+ShiftKind classify_shift(const std::vector<int>& signs) {
+  if (signs.size() != 2) throw std::invalid_argument("classify_shift: rank-2 signature required");
+  if (signs[0] > 0 && signs[1] > 0) return ShiftKind::double_right;
+  if (signs[0] < 0 && signs[1] < 0) return ShiftKind::double_left;
+  return ShiftKind::mixed;
+}
+
+std::pair<double, double> interlacing_bounds(std::size_t index, const Vec& lambda,
+                                             std::size_t rank, const std::vector<int>& signs) {
+  const std::size_t n = lambda.size();
+  if (index < 1 || index > n) throw std::invalid_argument("interlacing_bounds: index out of range");
+  if (signs.size() != rank || rank < 1)
+    throw std::invalid_argument("interlacing_bounds: bad signature");
+  std::size_t plus = 0, minus = 0;
+  for (int sg : signs) (sg > 0 ? plus : minus)++;
+  const double inf = std::numeric_limits<double>::infinity();
+  return {index > minus ? lambda[index - minus - 1] : -inf,
+          index + plus <= n ? lambda[index + plus - 1] : inf};
+}
+
+LocationVector locate_update(const SpectralDecomposition& d, const LowRankUpdate& u) {
+  validate_update(d, u);
+  const std::size_t n = d.size();
+  std::vector<int64_t> c(n + 1);
+  int64_t nc = 0;
+  check(eigmod_b200_locate(ctx(), d.q.data(), d.lambda.data(), u.kmat.data(), u.signs.data(),
+                           (int64_t)n, (int64_t)u.rank(), c.data(), &nc));
+  LocationVector loc;
+  loc.counts.assign(c.begin(), c.begin() + nc);
+  return loc;
 }
 
 SecularCoefficients make_secular(Vec poles, Vec weights, double leading) {
@@ -309,6 +358,12 @@ UpdateResult update_decomposition(const SpectralDecomposition& d, const LowRankU
 }
 
 namespace kernels {
+double ortho_error(const Matrix& a) {
+  if (a.rows() == 0 || a.cols() == 0) return 0.0;
+  double e = 0.0;
+  check(eigmod_b200_ortho_error(ctx(), a.data(), (int64_t)a.rows(), (int64_t)a.cols(), &e));
+  return e;
+}
 void set_parallel(bool) {}
 bool parallel() { return false; }
 int worker_count() { return 1; }

@@ -260,8 +260,22 @@ __global__ void any_flip_kernel(const double* flip, int64_t nn, int* any) {
 void gemm_nt_dev(const double* a, const double* b, int64_t m, int64_t nn, int64_t kk, double* c,
                  int64_t ldc, const double* colscale, double* tile_colmax, cudaStream_t st) {
   if (m <= 0 || nn <= 0) return;
-  if ((kk & 1) || (reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
-    throw Error(1, "", "gemm: operands must be 16-byte aligned with an even inner dimension");
+  if ((kk & 1) || (reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15)) {
+    // odd inner dimension (odd n) or unaligned operands: stage zero-padded
+    // copies with an even, 16-byte aligned row pitch (stream-ordered pool)
+    const int64_t kp2 = (kk + 1) & ~int64_t(1);
+    double *ap = nullptr, *bp = nullptr;
+    EIGB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ap), sizeof(double) * m * kp2, st));
+    EIGB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bp), sizeof(double) * nn * kp2, st));
+    EIGB_CUDA(cudaMemsetAsync(ap, 0, sizeof(double) * m * kp2, st));
+    EIGB_CUDA(cudaMemsetAsync(bp, 0, sizeof(double) * nn * kp2, st));
+    EIGB_CUDA(cudaMemcpy2DAsync(ap, 8 * kp2, a, 8 * kk, 8 * kk, m, cudaMemcpyDeviceToDevice, st));
+    EIGB_CUDA(cudaMemcpy2DAsync(bp, 8 * kp2, b, 8 * kk, 8 * kk, nn, cudaMemcpyDeviceToDevice, st));
+    gemm_nt_dev(ap, bp, m, nn, kp2, c, ldc, colscale, tile_colmax, st);
+    EIGB_CUDA(cudaFreeAsync(ap, st));
+    EIGB_CUDA(cudaFreeAsync(bp, st));
+    return;
+  }
   const int64_t tiles = cdiv(m, BM) * cdiv(nn, BN);
   static int use_tma = -1;  // EIGMOD_B200_GEMM=cpasync selects the cp.async kernel
   if (use_tma < 0) {

@@ -74,6 +74,15 @@ double* tile_colmax_buffer(int64_t n, int64_t ncols, DeviceScratch& ws);
 void sign_rule_dev(const double* tile_colmax, int64_t n, int64_t ncols, const int* mode, double* c,
                    int64_t ldc, DeviceScratch& ws, cudaStream_t st);
 
+// metrics.cu: validation products on the K5 GEMM
+void symmetrize_dev(double* a, int64_t n, cudaStream_t st);
+void reconstruct_dev(const double* q, const double* lam, int64_t n, double* out, DeviceScratch& ws,
+                     cudaStream_t st);
+void apply_update_dev(const double* a, const double* kmat, const int* sgn, int64_t n, int k,
+                      double* out, cudaStream_t st);
+double ortho_error_dev(const double* a, int64_t rows, int64_t cols, DeviceScratch& ws,
+                       cudaStream_t st);
+
 // Kernel launches issued by this library (evidence for bench.py's
 // gpu_launches); incremented by EIGB_LAUNCH_CHECK.
 int64_t launch_count();

@@ -10,8 +10,10 @@
 #include <stdexcept>
 #include <string>
 
+#include "eigmod/core.hpp"
 #include "eigmod/eigvec.hpp"
 #include "eigmod/kernels.hpp"
+#include "eigmod/locate.hpp"
 #include "eigmod/rootfind.hpp"
 #include "eigmod/secular.hpp"
 
@@ -238,6 +240,98 @@ int main() {
       const UpdateResult r = update_decomposition(d, u, 1e-13);
       CHECK(r.ortho_err <= 1e-9);
       CHECK(r.residual_fro <= 1e-10);
+    }
+  }
+  // ---- test_core.cpp:24-85 (reconstruct / apply_update examples)
+  {
+    SpectralDecomposition d;
+    d.q = Matrix::identity(2);
+    d.lambda = {3.0, 5.0};
+    const SymmetricDense a = reconstruct(d);
+    CHECK_NEAR(a.entries(0, 0), 3.0, 1e-14);
+    CHECK_NEAR(a.entries(1, 1), 5.0, 1e-14);
+    CHECK_NEAR(a.entries(0, 1), 0.0, 1e-14);
+    const double s2 = 1.0 / std::sqrt(2.0);
+    Matrix q(2, 2);
+    q(0, 0) = s2, q(0, 1) = s2, q(1, 0) = -s2, q(1, 1) = s2;
+    d.q = q;
+    d.lambda = {0.0, 2.0};
+    const SymmetricDense r = reconstruct(d);
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 2; ++j) CHECK_NEAR(r.entries(i, j), 1.0, 1e-14);
+    d.q = Matrix::identity(1);
+    d.lambda = {-4.0};
+    CHECK_NEAR(reconstruct(d).entries(0, 0), -4.0, 1e-15);
+
+    const SymmetricDense z = SymmetricDense::from(Matrix(2, 2));
+    const SymmetricDense o1 = apply_update(z, {Matrix::identity(2), {1, 1}});
+    CHECK(o1.entries(0, 0) == 1.0 && o1.entries(1, 1) == 1.0 && o1.entries(0, 1) == 0.0);
+    Matrix a0(2, 2), k(2, 2);
+    a0(1, 1) = 1.0;
+    k(0, 0) = 1.0, k(1, 0) = 1.0, k(1, 1) = 1.0;
+    const SymmetricDense o2 = apply_update(SymmetricDense::from(a0), {k, {1, 1}});
+    CHECK(o2.entries(0, 0) == 1.0 && o2.entries(0, 1) == 1.0 && o2.entries(1, 1) == 3.0);
+    Matrix a1(2, 2), k1(2, 1);
+    a1(0, 0) = 1.0, a1(1, 1) = 2.0, k1(0, 0) = 1.0;
+    const SymmetricDense o3 = apply_update(SymmetricDense::from(a1), {k1, {-1}});
+    CHECK(o3.entries(0, 0) == 0.0 && o3.entries(1, 1) == 2.0);
+    CHECK(throws<std::invalid_argument>(
+        [&] { (void)apply_update(SymmetricDense::from(Matrix(3, 3)), {Matrix(2, 1), {1}}); }));
+    // test_core.cpp:121-138: reconstruct then apply_update on generated instances
+    for (unsigned seed = 0; seed < 3; ++seed) {
+      auto [dd, uu] = instance(30, 3, 0.8, seed);
+      const SymmetricDense aa = reconstruct(dd);
+      const SymmetricDense direct = apply_update(aa, uu);
+      double diff = 0.0;
+      for (std::size_t i = 0; i < aa.n; ++i)
+        for (std::size_t j = 0; j < aa.n; ++j) {
+          double m = aa.entries(i, j);
+          for (std::size_t r = 0; r < uu.rank(); ++r)
+            m += (uu.signs[r] * uu.kmat(i, r)) * uu.kmat(j, r);
+          diff = std::max(diff, std::fabs(m - direct.entries(i, j)));
+        }
+      CHECK(diff <= 1e-13);
+    }
+  }
+  // ---- test_kernels.cpp:87-92 (ortho_error)
+  {
+    Matrix id = Matrix::identity(8);
+    CHECK(kernels::ortho_error(id) == 0.0);
+    id(0, 0) = 1.5;
+    CHECK(kernels::ortho_error(id) > 1.0);
+  }
+  // ---- test_locate.cpp (classify_shift, interlacing_bounds, rank-1 interlacing)
+  {
+    CHECK(classify_shift({1, 1}) == ShiftKind::double_right);
+    CHECK(classify_shift({-1, -1}) == ShiftKind::double_left);
+    CHECK(classify_shift({1, -1}) == ShiftKind::mixed);
+    CHECK(throws<std::invalid_argument>([] { (void)classify_shift({1}); }));
+    const auto w1 = interlacing_bounds(1, {0.0, 1.0, 5.0, 9.0}, 2, {1, 1});
+    CHECK(w1.first == 0.0 && w1.second == 5.0);
+    const auto w2 = interlacing_bounds(3, {0.0, 1.0, 5.0, 9.0}, 2, {-1, -1});
+    CHECK(w2.first == 0.0 && w2.second == 5.0);
+    CHECK(throws<std::invalid_argument>([] { (void)interlacing_bounds(0, {0.0, 1.0}, 2, {1, 1}); }));
+    auto [d, u] = instance(5, 1, 0.8, 31);
+    const LocationVector loc = locate_update(d, u);
+    CHECK(loc.counts.size() == 6);
+    CHECK(loc.counts[0] == 0);
+    for (std::size_t i = 1; i <= 5; ++i) CHECK(loc.counts[i] == 1);
+    // rank-3 mixed signs: counts agree with eigenvalues of A' located among the poles
+    for (unsigned seed = 0; seed < 10; ++seed) {
+      auto [d3, u3] = instance(10, 3, 1.2, seed + 70);
+      u3.signs = {1, seed % 2 ? -1 : 1, seed % 3 ? 1 : -1};
+      const LocationVector l3 = locate_update(d3, u3);
+      const Vec ev = update_eigenvalues(d3, u3, 1e-12);
+      const DeflatedProblem dp = deflate_problem(d3.lambda, transform_update(d3, u3));
+      std::vector<long> want(dp.coeffs.poles.size() + 1, 0);
+      for (double e : ev) {
+        std::size_t i = 0;
+        while (i < dp.coeffs.poles.size() && dp.coeffs.poles[i] < e) ++i;
+        want[i] += 1;
+      }
+      CHECK(dp.coeffs.size() == 10);
+      CHECK(l3.counts == want);
+      CHECK(l3.total() == 10);
     }
   }
   kernels::set_parallel(true);  // accepted, no effect on the GPU path

@@ -5,8 +5,8 @@ Run in the build container (where /root/reference exists and
 
     python tests/golden/make_golden.py
 
-Writes tests/golden/ref_seeded.npz, ref_cases.npz and ref_locate.npz
-(`--only-locate` rewrites the last one alone). Inputs
+Writes tests/golden/ref_seeded.npz, ref_cases.npz, ref_locate.npz and
+ref_validation.npz (`--only-locate` / `--only-validation` rewrite one alone). Inputs
 are stored next to the reference outputs so the fixtures do not depend on
 LAPACK bits of the machine that replays them. The GPU box never reads
 /root/reference: it only reads these files.
@@ -119,9 +119,32 @@ def make_locate():
     print("locate fixtures:", idx)
 
 
+def make_validation():
+    """reconstruct / apply_update / ortho_error fixtures (core.hpp:11-14,
+    kernels.hpp:36) from the reference, on its own generator's instances."""
+    out = {}
+    for t, (n, k) in enumerate([(7, 2), (40, 3), (96, 5), (130, 8)]):
+        q, lam, kmat = ref.random_instance(n, k, 0.7, 8100 + t)
+        signs = np.array([1 if r % 3 else -1 for r in range(k)], np.int32)
+        a = ref.reconstruct(q, lam)
+        out[f"V{t}__q"], out[f"V{t}__lam"], out[f"V{t}__kmat"] = q, lam, kmat
+        out[f"V{t}__signs"] = signs
+        out[f"V{t}__reconstruct"] = a
+        out[f"V{t}__apply_update"] = ref.apply_update(a, kmat, signs)
+        out[f"V{t}__ortho_q"] = np.array(ref.ortho_error(q))
+        rect = q[:, : max(1, n // 3)] * 1.0000001
+        out[f"V{t}__rect"] = rect
+        out[f"V{t}__ortho_rect"] = np.array(ref.ortho_error(rect))
+    np.savez_compressed(os.path.join(HERE, "ref_validation.npz"), **out)
+    print("validation fixtures:", len(out) // 9)
+
+
 def main():
     if "--only-locate" in sys.argv:
         make_locate()
+        return
+    if "--only-validation" in sys.argv:
+        make_validation()
         return
     ref.set_parallel(False)
     seeded = {}
@@ -158,6 +181,7 @@ def main():
                 cases[f"r2_{t}__{key}"] = c[key]
     np.savez_compressed(os.path.join(HERE, "ref_cases.npz"), **cases)
     make_locate()
+    make_validation()
     print("wrote", os.listdir(HERE))
 
 

@@ -108,6 +108,27 @@ def test_reference_random_instances(api, ctx, name, c):
         assert np.abs(res.q - c["q_out"]).max() <= 1e-5
 
 
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 33, 101, 257, 513])
+def test_odd_and_tiny_sizes(api, ctx, n):
+    """Odd n reaches the K5 GEMM with an odd inner dimension (padded staging)."""
+    from paper_1706_00773_b200.instances import make_instance
+
+    for cfg in (0, 2):
+        q, lam, kmat, signs = make_instance(cfg, n=n, seed=n)
+        k = min(kmat.shape[1], n)
+        kmat, signs = kmat[:, :k], signs[:k]
+        res = api.update_decomposition(q, lam, kmat, signs, 1e-12, ctx=ctx)
+        a = _aprime(q, lam, kmat, signs)
+        ev = np.linalg.eigvalsh(a)
+        nrm = max(1.0, float(np.abs(ev).max()))
+        assert np.abs(res.lam - ev).max() <= 1e-12 * nrm
+        assert np.abs(a @ res.q - res.q * res.lam).max() <= 1e-12 * nrm
+        assert np.abs(res.q.T @ res.q - np.eye(n)).max() <= 1e-11
+        lo, qo, _ = port.update(q, lam, kmat, signs)
+        assert np.abs(res.lam - lo).max() <= 1e-12 * nrm
+        assert np.abs(res.q - qo).max() <= 1e-8
+
+
 def test_update_eigenvalues_full_fields(api, ctx):
     name, c = SEEDED_CASES[0]
     up = api.update_eigenvalues_full(c["q"], c["lam"], c["kmat"], c["signs"], 1e-12, ctx=ctx)
