@@ -13,6 +13,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -90,6 +91,8 @@ class NumericalError : public std::runtime_error {
   std::string stage_;
 };
 
+// types.hpp:91 (core.cpp:76-87); the orthonormality check runs on the GPU.
+void validate_decomposition(const SpectralDecomposition& d, double max_ortho_err = 1e-10);
 void validate_update(const SpectralDecomposition& d, const LowRankUpdate& u);
 
 // core.hpp:11-14 — validation helpers (GPU: DMMA GEMM / rank-k kernel)
@@ -176,6 +179,23 @@ SpectralDecomposition assemble_eigenvectors(const SpectralDecomposition& d,
                                             bool reorthogonalize = false);
 UpdateResult update_decomposition(const SpectralDecomposition& d, const LowRankUpdate& u,
                                   double tol, bool reorthogonalize = false);
+
+// io.hpp:10-35 — Matrix Market / CSV ingest and egest (host, all threads;
+// byte-identical output, same grammar and messages as proj/src/io.cpp).
+class FormatError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+SymmetricDense read_matrix_market(const std::string& path);
+void write_matrix_market(const std::string& path, const SymmetricDense& a);
+struct CsvMatrix {
+  Matrix values;
+  std::optional<std::vector<int>> signs;
+};
+CsvMatrix read_csv_matrix(const std::string& path);
+void write_csv_matrix(const std::string& path, const Matrix& m,
+                      const std::optional<std::vector<int>>& signs = std::nullopt);
+std::vector<int> parse_signs(const std::string& text);
 
 // kernels.hpp:9-13 — the OpenMP toggle has no meaning on the GPU path.
 namespace kernels {

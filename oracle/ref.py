@@ -292,3 +292,60 @@ def ortho_error(a):
     f = lib().ref_ortho_error
     f.restype = C.c_double
     return float(f(_D(a), C.c_int64(a.shape[0]), C.c_int64(a.shape[1])))
+
+
+class RefFormatError(RuntimeError):
+    pass
+
+
+def _io_check(rc, buf):
+    if rc == 0:
+        return
+    msg = buf.value.decode(errors="replace")
+    if rc == 3:
+        raise RefFormatError(msg)
+    raise RuntimeError(msg)
+
+
+def write_csv(path, m, signs=None):
+    """io.cpp:176-194 write_csv_matrix."""
+    m = _f64(m)
+    if m.ndim == 1:
+        m = m[:, None]
+    s = None if signs is None else _i32(signs)
+    buf = C.create_string_buffer(1024)
+    _io_check(lib().ref_write_csv(str(path).encode(), _D(m), C.c_int64(m.shape[0]),
+                                  C.c_int64(m.shape[1]), _I(s) if s is not None else None,
+                                  C.c_int64(0 if s is None else s.shape[0]), buf,
+                                  C.c_size_t(1024)), buf)
+
+
+def read_csv(path):
+    """io.cpp:145-174 read_csv_matrix -> (values, signs or None)."""
+    shape = np.zeros(3, np.int64)
+    buf = C.create_string_buffer(1024)
+    _io_check(lib().ref_read_csv(str(path).encode(), _L(shape), None, None, buf,
+                                 C.c_size_t(1024)), buf)
+    vals = np.empty((int(shape[0]), int(shape[1])))
+    signs = np.empty(max(0, int(shape[2])), np.int32)
+    _io_check(lib().ref_read_csv(str(path).encode(), _L(shape), _D(vals), _I(signs), buf,
+                                 C.c_size_t(1024)), buf)
+    return vals, (signs if shape[2] >= 0 else None)
+
+
+def write_matrix_market(path, a):
+    """io.cpp:119-131."""
+    a = _f64(a)
+    buf = C.create_string_buffer(1024)
+    _io_check(lib().ref_write_mm(str(path).encode(), _D(a), C.c_int64(a.shape[0]), buf,
+                                 C.c_size_t(1024)), buf)
+
+
+def read_matrix_market(path):
+    """io.cpp:59-117."""
+    n = np.zeros(1, np.int64)
+    buf = C.create_string_buffer(1024)
+    _io_check(lib().ref_read_mm(str(path).encode(), _L(n), None, buf, C.c_size_t(1024)), buf)
+    a = np.empty((int(n[0]), int(n[0])))
+    _io_check(lib().ref_read_mm(str(path).encode(), _L(n), _D(a), buf, C.c_size_t(1024)), buf)
+    return a

@@ -15,6 +15,7 @@
 //   locate (CLI path)         proj/tools/eigmod.cpp:143-161 over locate.hpp:31,50
 //   reconstruct/apply_update  proj/include/eigmod/core.hpp:11-14
 //   ortho_error               proj/include/eigmod/kernels.hpp:36
+//   read/write CSV, Matrix Market   proj/include/eigmod/io.hpp:17-33
 // Return codes follow the product C-ABI (include/eigmod_b200.h):
 // 0 ok, 1 std::invalid_argument, 2 NumericalError (stage in the message
 // buffer as "[stage] msg"), 4 any other exception.
@@ -24,11 +25,14 @@
 #include <cstring>
 #include <exception>
 #include <stdexcept>
+#include <optional>
 #include <string>
+#include <vector>
 
 #include "eigmod/baseline.hpp"
 #include "eigmod/core.hpp"
 #include "eigmod/eigvec.hpp"
+#include "eigmod/io.hpp"
 #include "eigmod/kernels.hpp"
 #include "eigmod/locate.hpp"
 #include "eigmod/rootfind.hpp"
@@ -97,6 +101,22 @@ void copy_vec(const Vec& v, double* out) {
 
 void copy_idx(const std::vector<std::size_t>& v, std::int64_t* out) {
   for (std::size_t i = 0; i < v.size(); ++i) out[i] = static_cast<std::int64_t>(v[i]);
+}
+
+// io.hpp: FormatError maps to return code 3.
+template <class F>
+int io_guarded(char* msg, std::size_t len, F&& f) {
+  try {
+    f();
+    put_msg(msg, len, "");
+    return 0;
+  } catch (const FormatError& e) {
+    put_msg(msg, len, e.what());
+    return 3;
+  } catch (const std::exception& e) {
+    put_msg(msg, len, e.what());
+    return 4;
+  }
 }
 
 }  // namespace
@@ -201,6 +221,45 @@ int ref_apply_update(const double* a, const double* kmat, const int* signs, std:
 
 double ref_ortho_error(const double* a, std::int64_t rows, std::int64_t cols) {
   return kernels::ortho_error(to_matrix(a, rows, cols));
+}
+
+int ref_write_csv(const char* path, const double* m, std::int64_t rows, std::int64_t cols,
+                  const int* signs, std::int64_t nsigns, char* msg, std::size_t len) {
+  return io_guarded(msg, len, [&] {
+    std::optional<std::vector<int>> s;
+    if (signs) s = std::vector<int>(signs, signs + nsigns);
+    write_csv_matrix(path, to_matrix(m, rows, cols), s);
+  });
+}
+
+// shape_out = (rows, cols, nsigns); values_out / signs_out sized by the caller
+// (call once with null buffers to get the shape).
+int ref_read_csv(const char* path, std::int64_t* shape_out, double* values_out, int* signs_out,
+                 char* msg, std::size_t len) {
+  return io_guarded(msg, len, [&] {
+    const CsvMatrix c = read_csv_matrix(path);
+    shape_out[0] = static_cast<std::int64_t>(c.values.rows());
+    shape_out[1] = static_cast<std::int64_t>(c.values.cols());
+    shape_out[2] = c.signs ? static_cast<std::int64_t>(c.signs->size()) : -1;
+    if (values_out && c.values.rows() * c.values.cols())
+      std::memcpy(values_out, c.values.data(), sizeof(double) * c.values.rows() * c.values.cols());
+    if (signs_out && c.signs)
+      for (std::size_t i = 0; i < c.signs->size(); ++i) signs_out[i] = (*c.signs)[i];
+  });
+}
+
+int ref_write_mm(const char* path, const double* a, std::int64_t n, char* msg, std::size_t len) {
+  return io_guarded(msg, len, [&] {
+    write_matrix_market(path, SymmetricDense::from(to_matrix(a, n, n)));
+  });
+}
+
+int ref_read_mm(const char* path, std::int64_t* n_out, double* a_out, char* msg, std::size_t len) {
+  return io_guarded(msg, len, [&] {
+    const SymmetricDense s = read_matrix_market(path);
+    *n_out = static_cast<std::int64_t>(s.n);
+    if (a_out) std::memcpy(a_out, s.entries.data(), sizeof(double) * s.n * s.n);
+  });
 }
 
 double ref_default_tolerance(const double* lambda, const double* kmat, const int* signs,

@@ -3,6 +3,7 @@
   lib/libeigmod_b200.so      C ABI (include/eigmod_b200.h) + all CUDA kernels
   lib/libeigmod_b200_cxx.so  the reference's C++ API (namespace eigmod) as a
                              drop-in over the C ABI (include/eigmod/*.hpp)
+  lib/eigmod_b200            the reference CLI's update / locate subcommands
 nvcc cross-compiles without a GPU; sources compile in parallel.
 """
 from __future__ import annotations
@@ -20,11 +21,12 @@ LIB = os.path.join(PKG, "lib")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["secular.cu", "deflate.cu", "eigvec.cu", "gemm.cu", "metrics.cu", "capi.cu"]
-CXX_SOURCES = ["eigmod_api.cpp"]
+CXX_SOURCES = ["eigmod_api.cpp", "io.cpp"]
 NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-O3",
            "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
 CORE = os.path.join(LIB, "libeigmod_b200.so")
 CXX = os.path.join(LIB, "libeigmod_b200_cxx.so")
+CLI = os.path.join(LIB, "eigmod_b200")
 
 
 def _stale(out: str, deps: list[str]) -> bool:
@@ -69,9 +71,14 @@ def build(verbose: bool = False, force: bool = False) -> str:
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", CORE, *objs], verbose)
     cxx_src = [os.path.join(CSRC, f) for f in CXX_SOURCES]
     if all(os.path.exists(s) for s in cxx_src) and (force or _stale(CXX, cxx_src + hdrs + [CORE])):
-        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"),
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-fopenmp", "-I",
+              os.path.join(ROOT, "include"),
               *cxx_src, "-o", CXX, "-L", LIB, "-leigmod_b200", f"-Wl,-rpath,{LIB}",
               "-Wl,-rpath,$ORIGIN"], verbose)
+    cli_src = os.path.join(CSRC, "cli.cpp")
+    if os.path.exists(cli_src) and (force or _stale(CLI, [cli_src, CXX] + hdrs)):
+        _run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), cli_src, "-o", CLI,
+              "-L", LIB, "-leigmod_b200_cxx", "-leigmod_b200", "-Wl,-rpath,$ORIGIN"], verbose)
     return CORE
 
 

@@ -89,6 +89,19 @@ SymmetricDense SymmetricDense::from(const Matrix& m) {
   return s;
 }
 
+void validate_decomposition(const SpectralDecomposition& d, double max_ortho_err) {
+  if (d.q.rows() != d.q.cols() || d.q.rows() != d.lambda.size())
+    throw std::invalid_argument("SpectralDecomposition: inconsistent dimensions");
+  if (!all_finite(d.q)) throw std::invalid_argument("SpectralDecomposition: non-finite Q");
+  for (std::size_t i = 0; i + 1 < d.lambda.size(); ++i)
+    if (!(d.lambda[i] <= d.lambda[i + 1]))
+      throw std::invalid_argument("SpectralDecomposition: eigenvalues not ascending");
+  const double err = kernels::ortho_error(d.q);
+  if (err > max_ortho_err)
+    throw std::invalid_argument("SpectralDecomposition: orthonormality error " +
+                                std::to_string(err));
+}
+
 void validate_update(const SpectralDecomposition& d, const LowRankUpdate& u) {
   // proj/src/core.cpp:89-97
   if (u.dim() != d.size()) throw std::invalid_argument("LowRankUpdate: dimension mismatch");
