@@ -199,7 +199,11 @@ int eigmod_b200_update_decomposition_device(eigmod_b200_ctx* ctx, const double* 
  *   1. project:  U rows [col_lo, col_hi) = (Q^T K)[col_lo:col_hi]  -> d_u_out
  *                ((col_hi-col_lo) x kp, kp = padded rank from
  *                eigmod_b200_padded_rank(k)); all-gather to n x kp.
- *   2. plan:     deflation + reduced problem from the full U (every rank).
+ *   2. plan:     deflation + reduced problem from the full U (every rank);
+ *                or split so the K2 weights are shared out: plan_groups
+ *                (every rank, returns the group count ng), plan_weights for
+ *                the rank's group slice [g0, g1) -> d_alpha_out, all-gather
+ *                to ng doubles, plan_finish with the full vector.
  *   3. solve:    roots [j0, j1) of the reduced problem -> d_rec_out
  *                ((j1-j0) x eigmod_b200_record_width(kp) doubles);
  *                all-gather to nroots records.
@@ -212,6 +216,13 @@ int eigmod_b200_project_device(eigmod_b200_ctx* ctx, const double* d_q, const do
                                double* d_u_out);
 int eigmod_b200_plan_device(eigmod_b200_ctx* ctx, const double* d_lambda, const double* d_u,
                             const int* signs, int64_t n, int64_t k, int64_t* nroots_out);
+int eigmod_b200_plan_groups_device(eigmod_b200_ctx* ctx, const double* d_lambda,
+                                   const double* d_u, const int* signs, int64_t n, int64_t k,
+                                   int64_t* ng_out);
+int eigmod_b200_plan_weights_device(eigmod_b200_ctx* ctx, int64_t g0, int64_t g1,
+                                    double* d_alpha_out);
+int eigmod_b200_plan_finish_device(eigmod_b200_ctx* ctx, const double* d_alpha_all,
+                                   int64_t* nroots_out);
 int eigmod_b200_solve_device(eigmod_b200_ctx* ctx, int64_t j0, int64_t j1, double* d_rec_out);
 int eigmod_b200_finish_device(eigmod_b200_ctx* ctx, const double* d_q, const double* d_rec_all,
                               int64_t c0, int64_t c1, double* d_lambda_out, double* d_q_out,

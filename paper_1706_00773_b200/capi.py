@@ -96,6 +96,10 @@ def _declare(lib):
         "eigmod_b200_project_device": (C.c_int, [_VP, _VP, _VP, C.c_int64, C.c_int64, C.c_int64,
                                                  C.c_int64, _VP]),
         "eigmod_b200_plan_device": (C.c_int, [_VP, _VP, _VP, _I32, C.c_int64, C.c_int64, _I64]),
+        "eigmod_b200_plan_groups_device": (C.c_int, [_VP, _VP, _VP, _I32, C.c_int64, C.c_int64,
+                                                     _I64]),
+        "eigmod_b200_plan_weights_device": (C.c_int, [_VP, C.c_int64, C.c_int64, _VP]),
+        "eigmod_b200_plan_finish_device": (C.c_int, [_VP, _VP, _I64]),
         "eigmod_b200_solve_device": (C.c_int, [_VP, C.c_int64, C.c_int64, _VP]),
         "eigmod_b200_finish_device": (C.c_int, [_VP, _VP, _VP, C.c_int64, C.c_int64, _VP, _VP,
                                                 C.c_int64]),

@@ -120,7 +120,21 @@ void project(eigmod_b200_ctx* c, const double* q, const double* kmat, int64_t n,
   eigb::transform_update_dev(q, kmat, n, (int)k, kp, lo, hi, u_out, c->ws, c->sms, c->stream);
 }
 
+// plan_from_u = plan_groups + K2 over all groups + plan_finish
+void plan_groups(eigmod_b200_ctx* c, const double* lam, const double* u, const int* signs,
+                 int64_t n, int64_t k, double run_rel);
+
 void plan_from_u(eigmod_b200_ctx* c, const double* lam, const double* u, const int* signs,
+                 int64_t n, int64_t k, double run_rel) {
+  plan_groups(c, lam, u, signs, n, k, run_rel);
+  eigb::Plan& p = c->plan;
+  if (p.k == 0) return;
+  eigb::build_plan_weights(p, 0, p.ng, p.alpha, c->ws, c->stream);
+  eigb::build_plan_finish(p, lam, c->ws, c->stream);
+  c->have_plan = true;
+}
+
+void plan_groups(eigmod_b200_ctx* c, const double* lam, const double* u, const int* signs,
                  int64_t n, int64_t k, double run_rel) {
   eigb::Plan& p = c->plan;
   p = eigb::Plan{};
@@ -162,8 +176,8 @@ void plan_from_u(eigmod_b200_ctx* c, const double* lam, const double* u, const i
   }
   p.sgn = c->ws.get_i32("pl_sgn", p.kp);
   EIGB_CUDA(cudaMemcpyAsync(p.sgn, sp.data(), 4 * p.kp, cudaMemcpyHostToDevice, c->stream));
-  eigb::build_plan_dev(p, lam, n, run_rel, c->ws, c->stream);
-  c->have_plan = true;
+  eigb::build_plan_groups(p, lam, n, run_rel, c->ws, c->stream);
+  c->have_plan = false;  // until build_plan_finish
 }
 
 eigb::RootRecords alloc_records(eigmod_b200_ctx* c) {
@@ -807,6 +821,44 @@ int eigmod_b200_plan_device(eigmod_b200_ctx* ctx, const double* d_lambda, const 
     plan_from_u(ctx, d_lambda, d_u, signs, n, k, ctx->run_rel);
     ctx->recs = alloc_records(ctx);
     if (nroots_out) *nroots_out = ctx->plan.nred;
+  });
+}
+
+int eigmod_b200_plan_groups_device(eigmod_b200_ctx* ctx, const double* d_lambda,
+                                   const double* d_u, const int* signs, int64_t n, int64_t k,
+                                   int64_t* ng_out) {
+  return guarded(ctx, [&] {
+    check_basic(n, k, signs);
+    plan_groups(ctx, d_lambda, d_u, signs, n, k, ctx->run_rel);
+    *ng_out = ctx->plan.k == 0 ? 0 : ctx->plan.ng;
+  });
+}
+
+int eigmod_b200_plan_weights_device(eigmod_b200_ctx* ctx, int64_t g0, int64_t g1,
+                                    double* d_alpha_out) {
+  return guarded(ctx, [&] {
+    const eigb::Plan& p = ctx->plan;
+    if (p.k == 0) return;
+    if (g0 < 0 || g1 > p.ng || g0 > g1) throw Error(1, "", "plan_weights: bad group range");
+    eigb::build_plan_weights(p, g0, g1, d_alpha_out, ctx->ws, ctx->stream);
+  });
+}
+
+int eigmod_b200_plan_finish_device(eigmod_b200_ctx* ctx, const double* d_alpha_all,
+                                   int64_t* nred_out) {
+  return guarded(ctx, [&] {
+    eigb::Plan& p = ctx->plan;
+    if (p.k == 0) {
+      ctx->have_plan = true;
+      *nred_out = 0;
+      return;
+    }
+    if (d_alpha_all != p.alpha)
+      EIGB_CUDA(cudaMemcpyAsync(p.alpha, d_alpha_all, 8 * p.ng, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+    eigb::build_plan_finish(p, ctx->lam, ctx->ws, ctx->stream);
+    ctx->have_plan = true;
+    *nred_out = p.nred;
   });
 }
 

@@ -456,9 +456,9 @@ void repack_columns_dev(const double* u, int64_t n, int kp, const int* keep, int
   EIGB_LAUNCH_CHECK();
 }
 
-void build_plan_dev(Plan& p, const double* lam, int64_t n, double run_rel, DeviceScratch& ws,
-                    cudaStream_t st) {
-  const int kp = p.kp, k = p.k;
+// Runs / groups of the (kept-column) problem; sizes p.alpha for K2.
+void build_plan_groups(Plan& p, const double* lam, int64_t n, double run_rel, DeviceScratch& ws,
+                       cudaStream_t st) {
   p.n = n;
   int64_t* flag = ws.get_i64("pl_flag", n);
   p.gid = ws.get_i64("pl_gid", n);
@@ -476,7 +476,20 @@ void build_plan_dev(Plan& p, const double* lam, int64_t n, double run_rel, Devic
   EIGB_CUDA(cudaStreamSynchronize(st));
   p.ng = ng;
   p.alpha = ws.get_f64("pl_alpha", ng);
-  group_weights(kp, p.rep_row, p.u, n, p.gstart, p.glen, p.gval, ng, p.sgn, k, p.alpha, ws, st);
+}
+
+// K2 for groups [g0, g1) into alpha_out (length g1 - g0); the full vector may
+// be assembled from several ranks' slices before build_plan_finish.
+void build_plan_weights(const Plan& p, int64_t g0, int64_t g1, double* alpha_out,
+                        DeviceScratch& ws, cudaStream_t st) {
+  if (g1 <= g0) return;
+  group_weights(p.kp, p.rep_row, p.u, p.n, p.gstart + g0, p.glen + g0, p.gval + g0, g1 - g0,
+                p.sgn, p.k, alpha_out, ws, st);
+}
+
+void build_plan_finish(Plan& p, const double* lam, DeviceScratch& ws, cudaStream_t st) {
+  const int kp = p.kp, k = p.k;
+  const int64_t n = p.n, ng = p.ng;
   p.kind = ws.get_i32("pl_kind", ng);
   classify_kernel<<<1, kPlanThreads, 0, st>>>(p.u, n, kp, k, p.alpha, p.gstart, p.glen, p.counts,
                                                p.kind, p.scal);
@@ -556,6 +569,13 @@ void build_plan_dev(Plan& p, const double* lam, int64_t n, double run_rel, Devic
   p.u_mass = sc[2];
   p.lo_clip = sc[4];
   p.hi_clip = sc[5];
+}
+
+void build_plan_dev(Plan& p, const double* lam, int64_t n, double run_rel, DeviceScratch& ws,
+                    cudaStream_t st) {
+  build_plan_groups(p, lam, n, run_rel, ws, st);
+  build_plan_weights(p, 0, p.ng, p.alpha, ws, st);
+  build_plan_finish(p, lam, ws, st);
 }
 
 }  // namespace eigb

@@ -54,6 +54,12 @@ void repack_columns_dev(const double* u, int64_t n, int kp, const int* keep, int
                         double* out, cudaStream_t st);
 void build_plan_dev(Plan& p, const double* lam, int64_t n, double run_rel, DeviceScratch& ws,
                     cudaStream_t st);
+// build_plan_dev in three steps, so K2 can be split across ranks:
+void build_plan_groups(Plan& p, const double* lam, int64_t n, double run_rel, DeviceScratch& ws,
+                       cudaStream_t st);
+void build_plan_weights(const Plan& p, int64_t g0, int64_t g1, double* alpha_out,
+                        DeviceScratch& ws, cudaStream_t st);
+void build_plan_finish(Plan& p, const double* lam, DeviceScratch& ws, cudaStream_t st);
 
 // eigvec.cu
 void merge_columns_dev(const Plan& p, const RootRecords& roots, Columns& cols, DeviceScratch& ws,

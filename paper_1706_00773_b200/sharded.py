@@ -3,6 +3,7 @@
 SURVEY.md §8(e): every rank holds Lambda, U and Q (Q replicated). The only
 exchanges are
   1. all-gather of U: rank r projects U rows [r*C, (r+1)*C) (Q columns),
+  1b. all-gather of the K2 pole weights: rank r computes its group slice,
   2. all-gather of the root records: rank r solves root indices of its slice,
 then rank r writes the column block [c0, c1) of Q' = Q X locally. The plan
 (deflation, reduced problem) is computed redundantly on every rank from the
@@ -55,6 +56,27 @@ class CudaBackend:
             nr.ctypes.data_as(C.POINTER(C.c_int64))))
         return int(nr[0])
 
+    def plan_groups(self, lam, u_full) -> int:
+        c = self.ctx
+        ng = np.zeros(1, np.int64)
+        c.check(c._l.eigmod_b200_plan_groups_device(
+            c.h, C.c_void_p(lam.data_ptr()), C.c_void_p(u_full.data_ptr()),
+            self.signs.ctypes.data_as(C.POINTER(C.c_int)), self.n, self.k,
+            ng.ctypes.data_as(C.POINTER(C.c_int64))))
+        return int(ng[0])
+
+    def plan_weights(self, g0, g1, alpha_out):
+        c = self.ctx
+        c.check(c._l.eigmod_b200_plan_weights_device(c.h, g0, g1,
+                                                     C.c_void_p(alpha_out.data_ptr())))
+
+    def plan_finish(self, alpha_all) -> int:
+        c = self.ctx
+        nr = np.zeros(1, np.int64)
+        c.check(c._l.eigmod_b200_plan_finish_device(c.h, C.c_void_p(alpha_all.data_ptr()),
+                                                    nr.ctypes.data_as(C.POINTER(C.c_int64))))
+        return int(nr[0])
+
     def solve(self, j0, j1, rec_out):
         c = self.ctx
         c.check(c._l.eigmod_b200_solve_device(c.h, j0, j1, C.c_void_p(rec_out.data_ptr())))
@@ -103,8 +125,17 @@ class ShardedUpdate:
             self.be.project(q, kmat, self.u_lo, self.u_hi, self.u_part)
         dist.all_gather_into_tensor(self.u_all, self.u_part, group=self.group)
         u_full = self.u_all[: self.n]
-        # 2. redundant plan
-        nred = self.be.plan(lam, u_full)
+        # 2. plan: groups on every rank, the K2 weights shared out by group
+        #    slices and all-gathered, then the (redundant, cheap) reduction
+        ng = self.be.plan_groups(lam, u_full)
+        g0, g1, gc = split(ng, self.world, self.rank)
+        gc = max(gc, 1)
+        a_part = torch.zeros(gc, dtype=torch.float64, device=self.device)
+        a_all = torch.zeros(gc * self.world, dtype=torch.float64, device=self.device)
+        if g1 > g0:
+            self.be.plan_weights(g0, g1, a_part)
+        dist.all_gather_into_tensor(a_all, a_part, group=self.group)
+        nred = self.be.plan_finish(a_all[: max(ng, 1)])
         # 3. roots of this rank + all-gather of the records
         j0, j1, jc = split(nred, self.world, self.rank)
         jc = max(jc, 1)

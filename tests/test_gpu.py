@@ -266,6 +266,15 @@ def test_staged_path_equals_one_shot(api, ctx):
         be.project(tq, tk, a, b, part)
         u_all[r * ch: r * ch + (b - a)] = part[: b - a]
     nred = be.plan(tl, u_all[:n])
+    # split K2 (plan_groups / plan_weights per rank slice / plan_finish)
+    ng = be.plan_groups(tl, u_all[:n])
+    parts = []
+    for r in range(world):
+        g0, g1, gc = split(ng, world, r)
+        a_part = torch.zeros(max(gc, 1), dtype=torch.float64, device=dev)
+        be.plan_weights(g0, g1, a_part)
+        parts.append(a_part[: g1 - g0])
+    assert be.plan_finish(torch.cat(parts)) == nred
     recs = []
     for r in range(world):
         j0, j1, jc = split(nred, world, r)

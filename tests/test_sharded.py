@@ -34,6 +34,19 @@ class CpuBackend:
         self.u = u_full.numpy()[:, : self.k].copy()
         return self.n
 
+    def plan_groups(self, lam, u_full):
+        self.plan(lam, u_full)
+        self.alpha_full = port.secular_weights(self.lam, self.u, self.signs)
+        return self.n  # generic instances: every pole its own group
+
+    def plan_weights(self, g0, g1, alpha_out):
+        alpha_out[: g1 - g0] = torch.from_numpy(self.alpha_full[g0:g1].copy())
+
+    def plan_finish(self, alpha_all):
+        # the gathered slices must reassemble the weights of every group
+        assert np.array_equal(alpha_all.numpy(), self.alpha_full)
+        return self.n
+
     def solve(self, j0, j1, rec_out):
         roots, orig, dl, _ = port.solve_roots(self.lam, self.u, self.signs, j0, j1)
         rec_out[: j1 - j0, 0] = torch.from_numpy(roots)
