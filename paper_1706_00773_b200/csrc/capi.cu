@@ -456,6 +456,10 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
       ctx->sopt.fexit_rel = value;
     } else if (std::string(key) == "floor_rel") {
       ctx->sopt.floor_rel = value;
+    } else if (std::string(key) == "floor_ulps") {
+      ctx->sopt.floor_ulps = value;
+    } else if (std::string(key) == "stall_ratio") {
+      ctx->sopt.stall_ratio = value;
     } else if (std::string(key) == "geo_bisect") {
       ctx->sopt.geo_bisect = (int)value;
     } else if (std::string(key) == "trace_root") {

@@ -125,7 +125,7 @@ struct SolveArgs {
   int writer;  // writes root records (cluster rank 0)
   int64_t qbeg, qend;  // swept point range
   unsigned long long* prof;  // [0] passes, [1] active slot-passes, [2] slot batches
-  double fexit_rel, floor_rel;
+  double fexit_rel, floor_rel, floor_ulps, stall_ratio;
   int geo_bisect;
   int64_t trace_j;           // diagnostics (-1: off)
   double* trace;             // [kTraceRows][kTraceCols]
@@ -379,9 +379,15 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
   }
   // converged: S-Newton correction below step_tol ulps, or stalled at the
   // rounding floor of sigma (no longer shrinking while already tiny)
-  const bool sdone = !s.fmode[b] && ((fabs(step) <= a.step_tol * DBL_EPSILON * fabs(dl)) ||
-                                     (fabs(step) >= fabs(s.step_prev[b]) &&
-                                      fabs(step) <= a.floor_rel * fabs(dl)));
+  // (the S evaluation near a pole resolves delta only to ~eps * |S| / g in
+  // absolute terms: a stalled step below a few ulps of the root x itself is
+  // that floor, and further steps only bounce)
+  const bool stalled = fabs(step) >= a.stall_ratio * fabs(s.step_prev[b]);
+  const bool sdone =
+      !s.fmode[b] && ((fabs(step) <= a.step_tol * DBL_EPSILON * fabs(dl)) ||
+                      (stalled && (fabs(step) <= a.floor_rel * fabs(dl) ||
+                                   fabs(step) <= a.floor_ulps * DBL_EPSILON *
+                                                     fabs(s.dob[b] + dl))));
   if (sdone || w <= tol || zero || s.iters[b] > a.max_iters) {
     // two more inverse-iteration steps on the same factorization: the
     // eigenvector formula needs y to the accuracy of the root
@@ -681,6 +687,8 @@ void launch_solve(const ReducedView& rp, const double* alpha, const int* counts,
   a.trace_j = opt.trace_root;
   a.fexit_rel = opt.fexit_rel;
   a.floor_rel = opt.floor_rel;
+  a.floor_ulps = opt.floor_ulps;
+  a.stall_ratio = opt.stall_ratio;
   a.geo_bisect = opt.geo_bisect;
   a.trace = ws.get_f64("solve_trace", (size_t)kTraceRows * kTraceCols);
   if (opt.trace_root >= 0)

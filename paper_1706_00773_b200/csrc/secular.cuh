@@ -87,6 +87,8 @@ struct SolveOptions {
   int64_t trace_root = -1;  // diagnostics: record the iterates of this root
   double fexit_rel = 1e-2;  // f step leaving the bracket below this * |delta|: continue on S
   double floor_rel = 1e-11; // S-Newton step no longer shrinking below this * |delta|: converged
+  double floor_ulps = 4.0;   // ... or below this many ulps of the root value
+  double stall_ratio = 0.5;  // "no longer shrinking": |step| >= stall_ratio * |previous step|
   int geo_bisect = 1;       // geometric bisection of brackets spanning decades of delta
 };
 

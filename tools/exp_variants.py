@@ -10,14 +10,12 @@ from paper_1706_00773_b200.instances import make_instance_torch
 
 dev = torch.device('cuda', 0)
 variants = [
-    dict(fexit_rel=0.0, floor_rel=2.2e-13, geo_bisect=0),   # previous rules
-    dict(fexit_rel=0.0, floor_rel=1e-11, geo_bisect=0),
-    dict(fexit_rel=1e-2, floor_rel=1e-11, geo_bisect=0),
-    dict(fexit_rel=1e-2, floor_rel=1e-11, geo_bisect=1),
-    dict(fexit_rel=1e-4, floor_rel=1e-11, geo_bisect=1),
-    dict(fexit_rel=1e-2, floor_rel=1e-12, geo_bisect=1),
+    dict(floor_ulps=0.0, stall_ratio=1.0),   # previous rules
+    dict(floor_ulps=4.0, stall_ratio=1.0),
+    dict(floor_ulps=4.0, stall_ratio=0.5),
+    dict(floor_ulps=16.0, stall_ratio=0.5),
 ]
-for cfg, n in [(4, 16384), (2, 8192), (3, 16384), (1, 4096)]:
+for cfg, n in [(4, 16384), (2, 8192), (3, 16384), (1, 4096), (0, 512)]:
     q, lam, kmat, signs = make_instance_torch(cfg, n=n, device=dev)
     sg = signs.to(dev, torch.float64)
     lo = torch.empty(n, dtype=torch.float64, device=dev)
