@@ -12,6 +12,9 @@
 // Xt is written row by row with coalesced stores: HBM-bound (8 n^2 bytes).
 #include "pipeline.cuh"
 
+#include <cstdlib>
+#include <string>
+
 #include <thrust/device_ptr.h>
 #include <thrust/execution_policy.h>
 #include <thrust/sequence.h>
@@ -314,11 +317,447 @@ __global__ void xt_norm_kernel(const double* __restrict__ part, int64_t nchunks,
   cmode[c - c0] = (kind != 1);  // sign rule on computed columns (eigvec.cpp:340-347)
 }
 
+// K4 v2: one CTA = 64 original indices x 64 columns. The dot products
+// (U y)_r of the whole tile are a 64 x 64 x KP register-blocked product from
+// shared memory (4 x 4 entries per thread, LDS.128 operands); the epilogue
+// divides by (d_r - d_o) - delta (one MUFU reciprocal + Newton per entry),
+// stages the tile transposed in shared memory for coalesced streaming stores
+// of Xt rows, and leaves per-tile column sums of squares (fixed order). Tiles
+// that touch collided roots, unit / rotation columns or rows of compressed
+// runs take the per-entry path of xt_tile_kernel.
+constexpr int kXt2 = 64;
+
+template <int KP>
+struct Xt2Smem {
+  static constexpr int YS = KP + 2;  // padded row stride: conflict-free LDS.128
+  double ut[kXt2 * YS];
+  double yt[kXt2 * YS];
+  double out[kXt2 * (kXt2 + 1)];
+  double ss[16 * kXt2];
+  double dr[kXt2], cdob[kXt2], cdel[kXt2];
+  int64_t row[kXt2], co[kXt2], ct[kXt2];
+  int ckind[kXt2], cmode[kXt2];
+  int special;
+};
+
+template <int KP>
+__global__ void __launch_bounds__(256, 2) xt_tile64_kernel(
+    ReducedView rp, int64_t n, const int* __restrict__ ckind, const int64_t* __restrict__ cpay,
+    const int64_t* __restrict__ origin, const double* __restrict__ delta,
+    const int* __restrict__ flags, const double* __restrict__ yall,
+    const double* __restrict__ colldir, const int* __restrict__ collok,
+    const int64_t* __restrict__ orig_map, const int64_t* __restrict__ dec_src,
+    const int64_t* __restrict__ gstart, const int64_t* __restrict__ glen,
+    const int64_t* __restrict__ hoff, const double* __restrict__ hbuf,
+    const int64_t* __restrict__ rank, const int64_t* __restrict__ off_red, double gap,
+    int64_t c0, int64_t c1, int64_t tiles_per_split, double* __restrict__ xt,
+    double* __restrict__ part) {
+  using S = Xt2Smem<KP>;
+  constexpr int YS = S::YS;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  S& sm = *reinterpret_cast<S*>(smraw);
+  const int t = threadIdx.x;
+  const int64_t cb = c0 + (int64_t)blockIdx.y * kXt2;
+  const int64_t ntiles = cdiv_dev(n, kXt2);
+  const int64_t tile0 = (int64_t)blockIdx.x * tiles_per_split;
+  const int64_t tile1 = (tile0 + tiles_per_split < ntiles) ? tile0 + tiles_per_split : ntiles;
+  if (t == 0) sm.special = 0;
+  __syncthreads();
+  // ---- this CTA's 64 column parameters, once
+  if (t < kXt2) {
+    const int64_t c = cb + t;
+    int kind = -1, mode = 0;
+    int64_t o = 0, tt = 0;
+    double dob = 0.0, del = 0.0;
+    double* y = sm.yt + t * YS;
+    for (int q = 0; q < YS; ++q) y[q] = 0.0;
+    if (c < c1) {
+      kind = ckind[c];
+      const int64_t pay = cpay[c];
+      if (kind == 0) {
+        const int64_t j = pay;
+        o = origin[j];
+        dob = rp.d[o];
+        del = delta[j];
+        const bool coll = (flags[j] & 1) != 0;
+        mode = coll ? (collok[j] ? 1 : 2) : 0;
+        for (int q = 0; q <= KP; ++q)
+          y[q] = coll ? colldir[j * (KP + 1) + q] : (q < KP ? yall[j * KP + q] : 0.0);
+      } else {
+        const int64_t src = dec_src[pay];
+        if (kind == 1) {
+          o = src;
+        } else {
+          const int64_t code = -(src + 2);
+          o = code / 65536;
+          tt = code % 65536;
+        }
+      }
+      if (kind != 0 || mode != 0) atomicOr(&sm.special, 1);
+    }
+    sm.ckind[t] = kind;
+    sm.cmode[t] = mode;
+    sm.co[t] = o;
+    sm.ct[t] = tt;
+    sm.cdob[t] = dob;
+    sm.cdel[t] = del;
+  }
+  __syncthreads();
+  const int cols_special = sm.special;
+  const int tr = t >> 4, tc = t & 15;
+  double ssum[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t tile = tile0; tile < tile1; ++tile) {
+    const int64_t i0 = tile * kXt2;
+    // ---- row tile: reduced index, pole and U row of 64 original indices
+    if (t < kXt2) {
+      const int64_t i = i0 + t;
+      const int64_t r = (i < n) ? orig_map[i] : -1;
+      sm.row[t] = r;
+      sm.dr[t] = (r >= 0) ? rp.d[r] : 0.0;
+    }
+    if (t == 0) sm.special = cols_special;
+    __syncthreads();
+    for (int e = t; e < kXt2 * YS; e += 256) {
+      const int rr = e / YS, q = e - rr * YS;
+      const int64_t r = sm.row[rr];
+      sm.ut[e] = (r >= 0 && q < KP) ? rp.u[r * KP + q] : 0.0;
+    }
+    if (t < kXt2 && sm.row[t] <= -2) atomicOr(&sm.special, 1);
+    __syncthreads();
+    if (!sm.special) {
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+      if constexpr (KP >= 2) {
+#pragma unroll
+        for (int c = 0; c < KP; c += 2) {
+          double2 ua[4], yb[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+            ua[a] = *reinterpret_cast<const double2*>(sm.ut + (tr + 16 * a) * YS + c);
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            yb[b] = *reinterpret_cast<const double2*>(sm.yt + (tc + 16 * b) * YS + c);
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              acc[a][b] = fma(ua[a].x, yb[b].x, acc[a][b]);
+              acc[a][b] = fma(ua[a].y, yb[b].y, acc[a][b]);
+            }
+        }
+      } else {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            acc[a][b] = sm.ut[(tr + 16 * a) * YS] * sm.yt[(tc + 16 * b) * YS];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int rr = tr + 16 * a;
+        const bool live = sm.row[rr] >= 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int q = tc + 16 * b;
+          double x = 0.0;
+          if (live && sm.ckind[q] == 0)
+            x = acc[a][b] * rcp64((sm.dr[rr] - sm.cdob[q]) - sm.cdel[q]);
+          sm.out[q * (kXt2 + 1) + rr] = x;
+          ssum[b] = fma(x, x, ssum[b]);
+        }
+      }
+    } else {
+      // per-entry path (xt_tile_kernel semantics)
+      for (int a = 0; a < 4; ++a) {
+        const int rr = tr + 16 * a;
+        const int64_t i = i0 + rr;
+        const int64_t r = sm.row[rr];
+        for (int b = 0; b < 4; ++b) {
+          const int q = tc + 16 * b;
+          XtCol<KP> cp;
+          cp.kind = sm.ckind[q];
+          cp.mode = sm.cmode[q];
+          cp.o = sm.co[q];
+          cp.t = sm.ct[q];
+          cp.dob = sm.cdob[q];
+          cp.del = sm.cdel[q];
+          for (int c = 0; c <= KP; ++c) cp.y[c] = sm.yt[q * YS + c];
+          double x = 0.0;
+          if (i < n) {
+            if (cp.kind == 0) {
+              if (r >= 0) {
+                double ur[KP];
+                for (int c = 0; c < KP; ++c) ur[c] = sm.ut[rr * YS + c];
+                x = red_value<KP>(rp, r, ur, cp, gap);
+              } else if (r <= -2) {  // member of a compressed run: rotate back
+                const int64_t g = -2 - r;
+                const int64_t s0 = gstart[g], m = glen[g];
+                const double* H = hbuf + hoff[g];
+                for (int64_t k2 = 0; k2 < rank[g]; ++k2) {
+                  const int64_t r2 = off_red[g] + k2;
+                  double uu[KP];
+                  for (int c = 0; c < KP; ++c) uu[c] = rp.u[r2 * KP + c];
+                  x += H[k2 * m + (i - s0)] * red_value<KP>(rp, r2, uu, cp, gap);
+                }
+              }
+            } else if (cp.kind == 1) {
+              x = (i == cp.o) ? 1.0 : 0.0;
+            } else if (cp.kind == 2) {
+              const int64_t s0 = gstart[cp.o], m = glen[cp.o];
+              x = (i >= s0 && i < s0 + m) ? hbuf[hoff[cp.o] + cp.t * m + (i - s0)] : 0.0;
+            }
+          }
+          sm.out[q * (kXt2 + 1) + rr] = x;
+          ssum[b] = fma(x, x, ssum[b]);
+        }
+      }
+    }
+    __syncthreads();
+    // coalesced streaming stores: a warp writes 32 consecutive rows of a column
+    for (int e = t; e < kXt2 * kXt2; e += 256) {
+      const int q = e >> 6, rr = e & 63;
+      const int64_t c = cb + q, i = i0 + rr;
+      if (c < c1 && i < n) __stcs(xt + (c - c0) * n + i, sm.out[q * (kXt2 + 1) + rr]);
+    }
+  }
+  // column sums of squares: thread (tr, tc) holds rows tr, tr+16, .. of
+  // columns tc + 16 b over this CTA's tiles; combine over tr in order
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < 4; ++b) sm.ss[tr * kXt2 + tc + 16 * b] = ssum[b];
+  __syncthreads();
+  if (t < kXt2) {
+    double s2 = 0.0;
+    for (int w = 0; w < 16; ++w) s2 += sm.ss[w * kXt2 + t];
+    const int64_t c = cb + t;
+    if (c < c1) part[(c - c0) * gridDim.x + blockIdx.x] = s2;
+  }
+}
+
+// K4 v3 (plans without compressed runs or collided roots: every column is a
+// root by the formula or a unit vector): lane = original index, R rows per
+// thread (rows lane + 32 a of the warp's block), 64 columns per CTA with
+// their y in shared memory (LDS.128 broadcasts, each reused for R rows), Xt
+// written straight from registers (warp-coalesced rows), column sums of
+// squares staged per batch of 8 columns and reduced in a fixed order. Other
+// plans use xt_tile64_kernel, whose tiles fall back to the general rules.
+template <int KP>
+struct XtRowsCfg {
+  static constexpr int R = KP >= 32 ? 1 : (KP >= 16 ? 2 : 4);  // rows per thread (registers)
+  static constexpr int ROWS = 8 * 32 * R;           // rows per CTA
+  static constexpr int YS = KP + 2;
+};
+
+template <int KP>
+__global__ void __launch_bounds__(256, KP >= 32 ? 1 : 2) xt_rows_kernel(
+    ReducedView rp, int64_t n, const int* __restrict__ ckind, const int64_t* __restrict__ cpay,
+    const int64_t* __restrict__ origin, const double* __restrict__ delta,
+    const int* __restrict__ flags, const double* __restrict__ yall,
+    const double* __restrict__ colldir, const int* __restrict__ collok,
+    const int64_t* __restrict__ orig_map, const int64_t* __restrict__ dec_src,
+    const int64_t* __restrict__ gstart, const int64_t* __restrict__ glen,
+    const int64_t* __restrict__ hoff, const double* __restrict__ hbuf,
+    const int64_t* __restrict__ rank, const int64_t* __restrict__ off_red, double gap,
+    int64_t c0, int64_t c1, double* __restrict__ xt, double* __restrict__ part) {
+  using RC = XtRowsCfg<KP>;
+  constexpr int R = RC::R, YS = RC::YS;
+  __shared__ __align__(16) double yt[kXt2 * YS];
+  __shared__ double cdob[kXt2], cdel[kXt2];
+  __shared__ int64_t co[kXt2], ct[kXt2];
+  __shared__ int ck[kXt2], cm[kXt2];
+  __shared__ double red[kXt2];
+  __shared__ double sb[8][256];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t cb = c0 + (int64_t)blockIdx.y * kXt2;
+  if (t < kXt2) {
+    const int64_t c = cb + t;
+    int kind = -1, mode = 0;
+    int64_t o = 0, tt = 0;
+    double dob = 0.0, del = 0.0;
+    double* y = yt + t * YS;
+    for (int q = 0; q < YS; ++q) y[q] = 0.0;
+    if (c < c1) {
+      kind = ckind[c];
+      const int64_t pay = cpay[c];
+      if (kind == 0) {
+        const int64_t j = pay;
+        o = origin[j];
+        dob = rp.d[o];
+        del = delta[j];
+        const bool coll = (flags[j] & 1) != 0;
+        mode = coll ? (collok[j] ? 1 : 2) : 0;
+        for (int q = 0; q <= KP; ++q)
+          y[q] = coll ? colldir[j * (KP + 1) + q] : (q < KP ? yall[j * KP + q] : 0.0);
+      } else {
+        const int64_t src = dec_src[pay];
+        if (kind == 1) {
+          o = src;
+        } else {
+          const int64_t code = -(src + 2);
+          o = code / 65536;
+          tt = code % 65536;
+        }
+      }
+    }
+    ck[t] = kind;
+    cm[t] = mode;
+    co[t] = o;
+    ct[t] = tt;
+    cdob[t] = dob;
+    cdel[t] = del;
+  }
+  // this thread's rows
+  const int64_t ib = (int64_t)blockIdx.x * RC::ROWS + warp * 32 * R + lane;
+  int64_t rr[R];
+  double ur[R][KP], drow[R];
+#pragma unroll
+  for (int a = 0; a < R; ++a) {
+    const int64_t i = ib + 32 * a;
+    rr[a] = (i < n) ? orig_map[i] : -1;
+    drow[a] = (rr[a] >= 0) ? rp.d[rr[a]] : 0.0;
+    if constexpr (KP >= 2) {
+#pragma unroll
+      for (int c = 0; c < KP; c += 2) {
+        const double2 v = (rr[a] >= 0) ? __ldg(reinterpret_cast<const double2*>(rp.u + rr[a] * KP + c))
+                                      : make_double2(0.0, 0.0);
+        ur[a][c] = v.x;
+        ur[a][c + 1] = v.y;
+      }
+    } else {
+      ur[a][0] = (rr[a] >= 0) ? rp.u[rr[a]] : 0.0;
+    }
+  }
+  __syncthreads();
+  // columns in batches of 8: per-thread sums of squares staged in shared
+  // memory and reduced once per batch (warp w takes column q0 + w; fixed order).
+  // Entries of special columns or rows take the general rules.
+  for (int q0 = 0; q0 < kXt2; q0 += 8) {
+    double s2[8];
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) s2[qq] = 0.0;
+#pragma unroll
+    for (int qq = 0; qq < 8; qq += 2) {
+      const int q = q0 + qq;
+      // two columns, even/odd partial dot products: 4 R independent chains
+      double e0[R], o0[R], e1[R], o1[R];
+#pragma unroll
+      for (int a = 0; a < R; ++a) e0[a] = o0[a] = e1[a] = o1[a] = 0.0;
+      if constexpr (KP >= 2) {
+#pragma unroll
+        for (int cc = 0; cc < KP; cc += 2) {
+          const double2 y0 = *reinterpret_cast<const double2*>(yt + q * YS + cc);
+          const double2 y1 = *reinterpret_cast<const double2*>(yt + (q + 1) * YS + cc);
+#pragma unroll
+          for (int a = 0; a < R; ++a) {
+            e0[a] = fma(ur[a][cc], y0.x, e0[a]);
+            o0[a] = fma(ur[a][cc + 1], y0.y, o0[a]);
+            e1[a] = fma(ur[a][cc], y1.x, e1[a]);
+            o1[a] = fma(ur[a][cc + 1], y1.y, o1[a]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int a = 0; a < R; ++a) {
+          e0[a] = ur[a][0] * yt[q * YS];
+          e1[a] = ur[a][0] * yt[(q + 1) * YS];
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int qh = q + h;
+        const int64_t c = cb + qh;
+        const int kind = ck[qh];
+        const bool colfast = kind == 0;
+        const double dob = cdob[qh], del = cdel[qh];
+#pragma unroll
+        for (int a = 0; a < R; ++a) {
+          const double dot = h ? (e1[a] + o1[a]) : (e0[a] + o0[a]);
+          const int64_t i = ib + 32 * a;
+          double x;
+          if (colfast) {
+            x = (rr[a] >= 0) ? dot * rcp64((drow[a] - dob) - del) : 0.0;
+          } else {  // unit column of an unchanged pair
+            x = (kind == 1 && i == co[qh]) ? 1.0 : 0.0;
+          }
+          if (c < c1 && i < n) __stcs(xt + (c - c0) * n + i, x);
+          s2[qq + h] = fma(x, x, s2[qq + h]);
+        }
+      }
+    }
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) sb[qq][t] = s2[qq];
+    __syncthreads();
+    {
+      double v = 0.0;
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2) v += sb[warp][lane * 8 + k2];
+      v = warp_sum(v);
+      if (lane == 0) red[q0 + warp] = v;
+    }
+    __syncthreads();
+  }
+  if (t < kXt2) {
+    const int64_t c = cb + t;
+    if (c < c1) part[(c - c0) * gridDim.x + blockIdx.x] = red[t];
+  }
+}
+
 template <int KP>
 void launch_xt(const Plan& p, const RootRecords& roots, const Columns& cols, const double* colldir,
-               const int* collok, int64_t c0, int64_t c1, double* xt, double* colscale, int* cmode,
-               DeviceScratch& ws, cudaStream_t st) {
+               const int* collok, bool general, int64_t c0, int64_t c1, double* xt,
+               double* colscale, int* cmode, DeviceScratch& ws, cudaStream_t st) {
   const double gap = kPoleMergeRelGap * p.scale;
+  static int v1 = -1;  // EIGMOD_B200_XT=v1 selects the one-row-per-thread kernel
+  if (v1 < 0) {
+    const char* e = std::getenv("EIGMOD_B200_XT");
+    v1 = (e && std::string(e) == "v1");
+  }
+  static int v2 = -1;  // EIGMOD_B200_XT=v2 selects the 64 x 64 smem-tile kernel
+  if (v2 < 0) {
+    const char* e = std::getenv("EIGMOD_B200_XT");
+    v2 = (e && std::string(e) == "v2");
+  }
+  if (!v1 && !v2 && !general) {
+    using RC = XtRowsCfg<KP>;
+    const int64_t nchunks = cdiv(p.n, RC::ROWS);
+    double* part = ws.get_f64("xt_part", (size_t)nchunks * (c1 - c0));
+    dim3 grid((unsigned)nchunks, (unsigned)cdiv(c1 - c0, kXt2));
+    xt_rows_kernel<KP><<<grid, 256, 0, st>>>(
+        p.view(), p.n, cols.kind, cols.payload, roots.origin, roots.delta, roots.flags, roots.y,
+        colldir, collok, p.orig_map, p.dec_src, p.gstart, p.glen, p.hoff, p.hbuf, p.rank,
+        p.off_red, gap, c0, c1, xt, part);
+    EIGB_LAUNCH_CHECK();
+    xt_norm_kernel<<<(unsigned)cdiv(c1 - c0, 128), 128, 0, st>>>(part, nchunks, c0, c1,
+                                                                 cols.kind, colscale, cmode);
+    EIGB_LAUNCH_CHECK();
+    return;
+  }
+  if (!v1) {
+    // CTAs keep their 64 columns and sweep a contiguous share of the row
+    // tiles: the column setup is paid once per CTA, not once per tile. The
+    // split depends on n and the column count only (deterministic sums).
+    const int64_t ntiles = cdiv(p.n, kXt2), ctiles = cdiv(c1 - c0, kXt2);
+    const int64_t splits = std::max<int64_t>(1, std::min<int64_t>(ntiles, cdiv(2368, ctiles)));
+    const int64_t per = cdiv(ntiles, splits);
+    const int64_t nchunks = cdiv(ntiles, per);
+    double* part = ws.get_f64("xt_part", (size_t)nchunks * (c1 - c0));
+    dim3 grid((unsigned)nchunks, (unsigned)ctiles);
+    const size_t sm = sizeof(Xt2Smem<KP>);
+    EIGB_CUDA(cudaFuncSetAttribute(xt_tile64_kernel<KP>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    xt_tile64_kernel<KP><<<grid, 256, sm, st>>>(
+        p.view(), p.n, cols.kind, cols.payload, roots.origin, roots.delta, roots.flags, roots.y,
+        colldir, collok, p.orig_map, p.dec_src, p.gstart, p.glen, p.hoff, p.hbuf, p.rank,
+        p.off_red, gap, c0, c1, per, xt, part);
+    EIGB_LAUNCH_CHECK();
+    xt_norm_kernel<<<(unsigned)cdiv(c1 - c0, 128), 128, 0, st>>>(part, nchunks, c0, c1,
+                                                                 cols.kind, colscale, cmode);
+    EIGB_LAUNCH_CHECK();
+    return;
+  }
   const int64_t nchunks = cdiv(p.n, kXtThreads);
   double* part = ws.get_f64("xt_part", (size_t)nchunks * (c1 - c0));
   dim3 grid((unsigned)nchunks, (unsigned)cdiv(c1 - c0, kXtCols));
@@ -386,17 +825,17 @@ void merge_columns_dev(const Plan& p, const RootRecords& roots, Columns& cols, D
   EIGB_LAUNCH_CHECK();
 }
 
-void collision_vectors_dev(const Plan& p, const RootRecords& roots, double* colldir, int* collok,
-                           DeviceScratch& ws, cudaStream_t st) {
+int64_t collision_vectors_dev(const Plan& p, const RootRecords& roots, double* colldir,
+                              int* collok, DeviceScratch& ws, cudaStream_t st) {
   const int64_t nr = p.nred;
-  if (nr == 0) return;
+  if (nr == 0) return 0;
   std::vector<int> fl(nr);
   EIGB_CUDA(cudaMemcpyAsync(fl.data(), roots.flags, 4 * nr, cudaMemcpyDeviceToHost, st));
   EIGB_CUDA(cudaStreamSynchronize(st));
   std::vector<int64_t> list;
   for (int64_t j = 0; j < nr; ++j)
     if (fl[j] & 1) list.push_back(j);
-  if (list.empty()) return;
+  if (list.empty()) return 0;
   int64_t* dl = ws.get_i64("coll_list", list.size());
   EIGB_CUDA(cudaMemcpyAsync(dl, list.data(), 8 * list.size(), cudaMemcpyHostToDevice, st));
   const int64_t cnt = (int64_t)list.size();
@@ -408,19 +847,22 @@ void collision_vectors_dev(const Plan& p, const RootRecords& roots, double* coll
     case 16: launch_collisions<16>(p, roots, dl, cnt, colldir, collok, ws, st); break;
     case 32: launch_collisions<32>(p, roots, dl, cnt, colldir, collok, ws, st); break;
   }
+  return cnt;
 }
 
 void build_xt_dev(const Plan& p, const RootRecords& roots, const Columns& cols,
-                  const double* colldir, const int* collok, int64_t c0, int64_t c1, double* xt,
-                  double* colscale, int* cmode, DeviceScratch& ws, cudaStream_t st) {
+                  const double* colldir, const int* collok, int64_t ncollided, int64_t c0,
+                  int64_t c1, double* xt, double* colscale, int* cmode, DeviceScratch& ws,
+                  cudaStream_t st) {
   if (c1 <= c0) return;
+  const bool general = p.nmulti > 0 || ncollided > 0;
   switch (p.kp) {
-    case 1: launch_xt<1>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, ws, st); break;
-    case 2: launch_xt<2>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, ws, st); break;
-    case 4: launch_xt<4>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, ws, st); break;
-    case 8: launch_xt<8>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, ws, st); break;
-    case 16: launch_xt<16>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, ws, st); break;
-    case 32: launch_xt<32>(p, roots, cols, colldir, collok, c0, c1, xt, colscale, cmode, ws, st); break;
+    case 1: launch_xt<1>(p, roots, cols, colldir, collok, general, c0, c1, xt, colscale, cmode, ws, st); break;
+    case 2: launch_xt<2>(p, roots, cols, colldir, collok, general, c0, c1, xt, colscale, cmode, ws, st); break;
+    case 4: launch_xt<4>(p, roots, cols, colldir, collok, general, c0, c1, xt, colscale, cmode, ws, st); break;
+    case 8: launch_xt<8>(p, roots, cols, colldir, collok, general, c0, c1, xt, colscale, cmode, ws, st); break;
+    case 16: launch_xt<16>(p, roots, cols, colldir, collok, general, c0, c1, xt, colscale, cmode, ws, st); break;
+    case 32: launch_xt<32>(p, roots, cols, colldir, collok, general, c0, c1, xt, colscale, cmode, ws, st); break;
   }
 }
 
