@@ -239,6 +239,18 @@ def fp64_peaks_measured(torch, dev, ctx):
     return pk
 
 
+def _ncu_gemm_traffic(n):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one K5 launch from the
+    committed ncu --set full capture (profiles/ncu_full_cfg4_n32768_r01.json,
+    tools/profile_case.py --n 32768), when this run has that n; else None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                        "ncu_full_cfg4_n32768_r01.json")
+    if n != 32768 or not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f).get("gemm_traffic_bytes_per_launch")
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -348,7 +360,7 @@ def run_ours(args):
                                         "(MEASURED_PEAKS.json has no FP64 entry)",
                          "measured_peaks": peaks,
                          "algorithmic_flops_per_launch": gemm_flops,
-                         "traffic": None},
+                         "traffic": _ncu_gemm_traffic(n)},
         }
         # CPU secular-solver roofline (K3): algorithmic flops per S evaluation
         kp = int(stats["kp"]) or 1

@@ -1,7 +1,7 @@
 """Summarise ncu captures (launch list + full-set reports) into profiles/."""
 import csv, collections, io, json, subprocess, sys
 
-def launches(path):
+def launches(path, only_ours=True):
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if 'Kernel Name' in r][0]
     h = rows[hi]; ki = h.index('Kernel Name'); vi = h.index('Metric Value'); ui = h.index('Metric Unit')
@@ -9,8 +9,11 @@ def launches(path):
     for r in rows[hi + 1:]:
         if len(r) <= vi: continue
         v = float(r[vi].replace(',', ''))
-        v = v / 1e6 if r[ui] == 'nsecond' else v / 1e3 if r[ui] == 'usecond' else v
-        name = r[ki].split('(')[0].replace('void ', '')
+        u = r[ui]
+        v = v / 1e6 if u in ('nsecond', 'ns') else v / 1e3 if u in ('usecond', 'us') else v
+        name = r[ki].split('(')[0].replace('void ', '').replace('eigb::<unnamed>::', '')
+        if only_ours and 'eigb' not in r[ki]:
+            continue
         a = agg.setdefault(name, [0.0, 0]); a[0] += v; a[1] += 1
     return agg
 
