@@ -276,8 +276,36 @@ void finish(eigmod_b200_ctx* c, const double* q, const double* lam_in, int64_t c
     return;
   }
   if (!c->copy) EIGB_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
-  const int64_t nb = std::min<int64_t>(8, eigb::cdiv(nc, 128));
-  const int64_t wb = eigb::cdiv(eigb::cdiv(nc, nb), 128) * 128;
+  // Block width: every block is a separate GEMM launch of 128 x 128 tiles
+  // (one CTA per SM), so a block whose tile count is not a multiple of the SM
+  // count leaves SMs idle in its last wave. Pick, among 6..16 blocks, the
+  // width (in 128-column tiles) that wastes the fewest tile slots.
+  // The last block's copy is not overlapped: it is kept narrow (a few column
+  // tiles, its own launch).
+  const int64_t tiles_m = eigb::cdiv(n, 128), ctiles = eigb::cdiv(nc, 128);
+  auto waste_of = [&](int64_t w_tiles) {
+    const int64_t t = tiles_m * w_tiles;
+    return eigb::cdiv(t, c->sms) * c->sms - t;
+  };
+  int64_t tail = 0;
+  if (ctiles >= 32) {
+    tail = 2;
+    for (int64_t t2 = 3; t2 <= 4; ++t2)
+      if (waste_of(t2) < waste_of(tail)) tail = t2;
+  }
+  const int64_t main_tiles = ctiles - tail;
+  int64_t best_w = eigb::cdiv(main_tiles, std::min<int64_t>(8, main_tiles)), best_waste = -1;
+  for (int64_t want = 6; want <= 16 && want <= main_tiles; ++want) {
+    const int64_t w = eigb::cdiv(main_tiles, want);
+    int64_t waste = 0;
+    for (int64_t a = 0; a < main_tiles; a += w) waste += waste_of(std::min(w, main_tiles - a));
+    if (best_waste < 0 || waste < best_waste) best_waste = waste, best_w = w;
+  }
+  std::vector<int64_t> bstart;  // block boundaries in columns
+  for (int64_t a = 0; a < main_tiles; a += best_w) bstart.push_back(a * 128);
+  if (tail) bstart.push_back(main_tiles * 128);
+  bstart.push_back(nc);
+  const int64_t nb = (int64_t)bstart.size() - 1;
   while ((int64_t)c->blk_ev.size() < nb) {
     cudaEvent_t e;
     EIGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -285,15 +313,15 @@ void finish(eigmod_b200_ctx* c, const double* q, const double* lam_in, int64_t c
   }
   // all blocks are enqueued before the first copy: a pageable destination
   // makes cudaMemcpy2DAsync block the host, and the GPU must not wait on that
-  for (int64_t b = 0; b * wb < nc; ++b) {
-    const int64_t a0 = b * wb, w = std::min(wb, nc - a0);
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t a0 = bstart[b], w = bstart[b + 1] - a0;
     double* cb = q_out + a0;
     eigb::gemm_nt_dev(q, xt + a0 * n, n, w, n, cb, ldq, colscale + a0, tcm, c->stream);
     eigb::sign_rule_dev(tcm, n, w, cmode + a0, cb, ldq, c->ws, c->stream);
     EIGB_CUDA(cudaEventRecord(c->blk_ev[b], c->stream));
   }
-  for (int64_t b = 0; b * wb < nc; ++b) {
-    const int64_t a0 = b * wb, w = std::min(wb, nc - a0);
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t a0 = bstart[b], w = bstart[b + 1] - a0;
     EIGB_CUDA(cudaStreamWaitEvent(c->copy, c->blk_ev[b], 0));
     EIGB_CUDA(cudaMemcpy2DAsync(host_q_out + (c0 + a0), 8 * host_ld, q_out + a0, 8 * ldq, 8 * w,
                                 n, cudaMemcpyDeviceToHost, c->copy));
