@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="override n (smaller smoke runs)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU (ShardedUpdate) path even on one rank")
     return ap.parse_args()
 
 
@@ -263,7 +265,11 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
+        if "MASTER_ADDR" not in os.environ:  # --sharded outside torchrun: a 1-rank group
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0",
+                              WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=dev)
 
     cfg = CONFIGS[args.config]
@@ -288,7 +294,7 @@ def run_ours(args):
     ctx.set_option("timing", 1.0)
     lam_out = torch.empty(n, dtype=torch.float64, device=dev)
 
-    if world == 1:
+    if not sharded:
         q_out = torch.empty((n, n), dtype=torch.float64, device=dev)
 
         def step():
@@ -307,7 +313,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     ctx.stage_times(reset=True)
     launches0 = capi.launch_count()
-    if world > 1:
+    if sharded:
         dist.barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -318,12 +324,12 @@ def run_ours(args):
             step()
         e1.record()
         torch.cuda.synchronize()
-    if world > 1:
+    if sharded:
         dist.barrier()
     launches = capi.launch_count() - launches0
     ms = e0.elapsed_time(e1) / args.steps
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if sharded:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
     stages = ctx.stage_times()
@@ -334,7 +340,7 @@ def run_ours(args):
         value = n / (ms * 1e-3)
         calls = max(1, stages["calls"])
         gemm_ms = stages["k5_gemm"] / calls
-        cols = n if world == 1 else shard.ncols_local
+        cols = shard.ncols_local if sharded else n
         gemm_flops = 2.0 * n * n * cols
         peaks = fp64_peaks_measured(torch, dev, ctx)
         peak = peaks["dmma_tflops"]
@@ -346,7 +352,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded; Q from a GPU QR of a Philox N(0,1) matrix)",
             "config": {"workload": cfg["name"], "n": n, "k": k, "signs": list(cfg["signs"]),
-                       "parallelism": f"roots+columns x{world}",
+                       "parallelism": f"roots+columns x{world}" + (" (sharded path)" if sharded else ""),
                        "l2": "inputs (8.6 GB Q) exceed L2; no flush"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
@@ -369,8 +375,63 @@ def run_ours(args):
             "bound": "fp64", "evals": stats["evals"],
             "achieved": stats["evals"] * fl_eval / (solve_ms * 1e-3) / 1e12 if solve_ms else None,
             "peak": peaks["dfma_tflops"], "unit": "TFLOP/s", "note": f"n*(k(k+1)+1) flops per S(x) evaluation, kp={kp}"}
+    # ---- e2e at N GPUs: host inputs -> every rank copies its 1/N row slice
+    # of Q (pinned) and the small lambda, K; Q is reassembled by an NCCL
+    # all-gather over NVLink; each rank copies its Q' column block and rank 0
+    # lambda' back to pinned host memory. Max over ranks of CUDA-event time.
+    if sharded and not args.no_e2e:
+        del q_out
+        torch.cuda.empty_cache()
+        from paper_1706_00773_b200.sharded import split
+
+        r0, r1, ch = split(n, world, rank)
+        h_qs = torch.zeros((ch, n), dtype=torch.float64, pin_memory=True)
+        h_qs[: r1 - r0].copy_(q[r0:r1])
+        h_lam = lam.cpu().pin_memory()
+        h_k = kmat.cpu().pin_memory()
+        d_slice = torch.empty((ch, n), dtype=torch.float64, device=dev)
+        d_qall = torch.empty((ch * world, n), dtype=torch.float64, device=dev)
+        d_lam = torch.empty_like(lam)
+        d_k = torch.empty_like(kmat)
+        del q
+        torch.cuda.empty_cache()
+        q_blk = shard.alloc_output()
+        h_qo = torch.empty((n, max(shard.ncols_local, 1)), dtype=torch.float64, pin_memory=True)
+        h_lo = torch.empty(n, dtype=torch.float64, pin_memory=True)
+
+        def e2e_step():
+            d_slice.copy_(h_qs, non_blocking=True)
+            d_lam.copy_(h_lam, non_blocking=True)
+            d_k.copy_(h_k, non_blocking=True)
+            dist.all_gather_into_tensor(d_qall, d_slice)
+            shard.run(d_qall[:n], d_lam, d_k, lam_out, q_blk)
+            h_qo.copy_(q_blk, non_blocking=True)
+            if rank == 0:
+                h_lo.copy_(lam_out, non_blocking=True)
+
+        for _ in range(max(1, min(args.warmup, 2))):
+            e2e_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        f1.record()
+        torch.cuda.synchronize()
+        te_t = torch.tensor([f0.elapsed_time(f1) / args.steps], dtype=torch.float64, device=dev)
+        dist.all_reduce(te_t, op=dist.ReduceOp.MAX)
+        te = float(te_t.item()) * 1e-3
+        if rank == 0:
+            out["e2e"] = {"value": n / te, "unit": UNIT,
+                          "h2d_bytes_per_step": 8 * (ch * world * n + world * (n + n * k)),
+                          "d2h_bytes_per_step": 8 * (n * n + n),
+                          "ms_per_step": te * 1e3,
+                          "path": "per-rank 1/N row slice of Q H2D + NCCL all-gather, "
+                                  "ShardedUpdate, column blocks D2H (pinned)"}
     # ---- e2e through the host-pointer C ABI (single GPU)
-    if world == 1 and not args.no_e2e:
+    if not sharded and not args.no_e2e:
         h_q = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
         h_q.copy_(q)
         h_lam = lam.cpu().numpy()
@@ -418,7 +479,7 @@ def run_ours(args):
                                    "kind": "reference", "sample": f"unavailable: {e}"}
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 

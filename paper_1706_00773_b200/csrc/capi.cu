@@ -49,6 +49,15 @@ struct eigmod_b200_ctx {
     if (!ev[i]) EIGB_CUDA(cudaEventCreate(&ev[i]));
     EIGB_CUDA(cudaEventRecord(ev[i], stream));
   }
+  // staged entry points: add stages [i0, i1) once their end mark completed
+  void accumulate(int i0, int i1) {
+    if (!timing || !ev[i1]) return;
+    EIGB_CUDA(cudaEventSynchronize(ev[i1]));
+    for (int i = i0; i < i1; ++i) {
+      float ms = 0.f;
+      if (ev[i] && cudaEventElapsedTime(&ms, ev[i], ev[i + 1]) == cudaSuccess) stage_ms[i] += ms;
+    }
+  }
 };
 
 namespace eigb {
@@ -842,7 +851,10 @@ int eigmod_b200_project_device(eigmod_b200_ctx* ctx, const double* d_q, const do
   return guarded(ctx, [&] {
     check_basic(n, k, nullptr);
     if (col_lo < 0 || col_hi > n || col_hi < col_lo) throw Error(1, "", "project: bad range");
+    ctx->mark(0);
     if (col_hi > col_lo) project(ctx, d_q, d_kmat, n, k, col_lo, col_hi, d_u_out);
+    ctx->mark(1);
+    ctx->accumulate(0, 1);
   });
 }
 
@@ -850,7 +862,10 @@ int eigmod_b200_plan_device(eigmod_b200_ctx* ctx, const double* d_lambda, const 
                             const int* signs, int64_t n, int64_t k, int64_t* nroots_out) {
   return guarded(ctx, [&] {
     check_basic(n, k, signs);
+    ctx->mark(1);
     plan_from_u(ctx, d_lambda, d_u, signs, n, k, ctx->run_rel);
+    ctx->mark(2);
+    ctx->accumulate(1, 2);
     ctx->recs = alloc_records(ctx);
     if (nroots_out) *nroots_out = ctx->plan.nred;
   });
@@ -861,6 +876,7 @@ int eigmod_b200_plan_groups_device(eigmod_b200_ctx* ctx, const double* d_lambda,
                                    int64_t* ng_out) {
   return guarded(ctx, [&] {
     check_basic(n, k, signs);
+    ctx->mark(1);
     plan_groups(ctx, d_lambda, d_u, signs, n, k, ctx->run_rel);
     *ng_out = ctx->plan.k == 0 ? 0 : ctx->plan.ng;
   });
@@ -891,6 +907,8 @@ int eigmod_b200_plan_finish_device(eigmod_b200_ctx* ctx, const double* d_alpha_a
     eigb::build_plan_finish(p, ctx->lam, ctx->ws, ctx->stream);
     ctx->have_plan = true;
     *nred_out = p.nred;
+    ctx->mark(2);
+    ctx->accumulate(1, 2);
   });
 }
 
@@ -898,7 +916,9 @@ int eigmod_b200_solve_device(eigmod_b200_ctx* ctx, int64_t j0, int64_t j1, doubl
   return guarded(ctx, [&] {
     if (!ctx->have_plan) throw Error(1, "", "solve: no plan");
     if (j0 < 0 || j1 > ctx->plan.nred || j1 < j0) throw Error(1, "", "solve: bad root range");
+    ctx->recs = alloc_records(ctx);
     if (ctx->plan.nred == 0) return;
+    ctx->mark(2);
     eigb::solve_roots(ctx->plan.view(), ctx->plan.alpha_red_ok ? ctx->plan.alpha_red : nullptr, j0,
                       j1, ctx->recs, ctx->sopt, ctx->ws, ctx->sms, ctx->stream);
     if (d_rec_out && j1 > j0) {
@@ -906,6 +926,8 @@ int eigmod_b200_solve_device(eigmod_b200_ctx* ctx, int64_t j0, int64_t j1, doubl
           ctx->recs, j0, j1 - j0, ctx->plan.kp, d_rec_out);
       EIGB_LAUNCH_CHECK();
     }
+    ctx->mark(3);
+    ctx->accumulate(2, 3);
   });
 }
 
@@ -916,13 +938,19 @@ int eigmod_b200_finish_device(eigmod_b200_ctx* ctx, const double* d_q, const dou
     if (!ctx->have_plan) throw Error(1, "", "finish: no plan");
     const eigb::Plan& p = ctx->plan;
     if (c0 < 0 || c1 > p.n || c1 < c0) throw Error(1, "", "finish: bad column range");
+    ctx->recs = alloc_records(ctx);
     if (d_rec_all && p.nred > 0) {
       unpack_records_kernel<<<(unsigned)eigb::cdiv(p.nred, 128), 128, 0, ctx->stream>>>(
           d_rec_all, p.nred, p.kp, ctx->recs);
       EIGB_LAUNCH_CHECK();
     }
     // lambda is only needed for the rank-0 copy; the plan keeps no pointer to it
+    ctx->mark(3);
     finish(ctx, d_q, nullptr, c0, c1, d_lambda_out, d_q_out, ldq);
+    if (p.k > 0 && c1 > c0 && d_q_out) {
+      ctx->accumulate(3, 6);
+      if (ctx->timing) ctx->timed_calls += 1;
+    }
   });
 }
 

@@ -294,6 +294,39 @@ def test_staged_path_equals_one_shot(api, ctx):
     assert torch.equal(qo1, qo2)
 
 
+def test_staged_path_on_fresh_context(api):
+    """The staged entry points allocate their own workspaces (no prior
+    one-shot call on the context)."""
+    import torch
+
+    from paper_1706_00773_b200.instances import make_instance
+    from paper_1706_00773_b200.sharded import CudaBackend
+
+    q, lam, kmat, s = make_instance(4, n=640, seed=3)
+    dev = torch.device("cuda", 0)
+    tq, tl, tk = (torch.from_numpy(x).to(dev) for x in (q, lam, kmat))
+    n, k = kmat.shape
+    ctx = api.Context(0)
+    ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+    be = CudaBackend(ctx, n, k, s)
+    u = torch.zeros((n, be.kp), dtype=torch.float64, device=dev)
+    be.project(tq, tk, 0, n, u)
+    ng = be.plan_groups(tl, u)
+    alpha = torch.zeros(ng, dtype=torch.float64, device=dev)
+    be.plan_weights(0, ng, alpha)
+    nred = be.plan_finish(alpha)
+    rec = torch.zeros((nred, be.width), dtype=torch.float64, device=dev)
+    be.solve(0, nred, rec)
+    lo = torch.empty(n, dtype=torch.float64, device=dev)
+    qo = torch.empty((n, n), dtype=torch.float64, device=dev)
+    be.finish(tq, rec, 0, n, lo, qo)
+    torch.cuda.synchronize()
+    ref = api.update_decomposition(q, lam, kmat, s, 1e-12)
+    assert np.array_equal(lo.cpu().numpy(), ref.lam)
+    assert np.array_equal(qo.cpu().numpy(), ref.q)
+    ctx.close()
+
+
 # ------------------------------------------------- full-size configs
 def _device_checks(api, ctx, cfg, n=None, lapack=True, oracle_roots=64):
     import torch
