@@ -225,15 +225,22 @@ int eo_secular_weights(const double* lambda, const double* u, const int* signs, 
 
 /* Runs of near-equal poles (secular.cpp:285-302): a value joins the current run
  * when lambda[i] - lambda[last member] < rel * scale; rep = run mean. */
-static int64_t make_runs(const double* lambda, int64_t n, double rel, int64_t* gstart,
-                         int64_t* glen, double* rep) {
+/* scale_override > 0: the exact mode's scale max(max|lambda|, ||U||_F^2)
+ * (scale invariance); otherwise the reference's max(1, max|lambda|). */
+static int64_t make_runs_s(const double* lambda, int64_t n, double rel, double scale_override,
+                           int64_t* gstart, int64_t* glen, double* rep) {
   double scale = 1.0;
   for (int64_t i = 0; i < n; ++i)
     if (fabs(lambda[i]) > scale) scale = fabs(lambda[i]);
+  if (scale_override > 0.0) scale = scale_override;
   const double gap = rel * scale;
   int64_t ng = 0;
+  /* exact mode: a run never spans more than the gap (merging moves every
+   * member by less than the gap); the reference chains consecutive gaps */
+  const int width_limited = scale_override > 0.0;
   for (int64_t i = 0; i < n; ++i) {
-    if (ng > 0 && lambda[i] - lambda[i - 1] < gap) {
+    const double ref = (width_limited && ng > 0) ? lambda[gstart[ng - 1]] : (i > 0 ? lambda[i - 1] : 0.0);
+    if (ng > 0 && lambda[i] - ref < gap) {
       glen[ng - 1]++;
     } else {
       gstart[ng] = i;
@@ -247,6 +254,11 @@ static int64_t make_runs(const double* lambda, int64_t n, double rel, int64_t* g
     rep[g] = s / (double)glen[g];
   }
   return ng;
+}
+
+static int64_t make_runs(const double* lambda, int64_t n, double rel, int64_t* gstart,
+                         int64_t* glen, double* rep) {
+  return make_runs_s(lambda, n, rel, 0.0, gstart, glen, rep);
 }
 
 static double frob2(const double* u, int64_t cnt) {
@@ -272,6 +284,19 @@ static void classify(const double* alpha, const int64_t* gstart, const int64_t* 
         for (int64_t r = 0; r < k; ++r) row_mass += u[i * k + r] * u[i * k + r];
       kind[g] = (row_mass <= 1e-12 * (1.0 + u_mass)) ? 1 : 2;
     }
+  }
+}
+
+/* Exact mode (the solve): a group decouples unchanged when its rows couple
+ * to the rest by less than 1e-13 of the scale s; no collided class. */
+static void classify_exact(const int64_t* gstart, const int64_t* glen, int64_t ng,
+                           const double* u, int64_t n, int64_t k, double scale, int* kind) {
+  const double fn = sqrt(frob2(u, n * k));
+  for (int64_t g = 0; g < ng; ++g) {
+    double row_mass = 0.0;
+    for (int64_t i = gstart[g]; i < gstart[g] + glen[g]; ++i)
+      for (int64_t r = 0; r < k; ++r) row_mass += u[i * k + r] * u[i * k + r];
+    kind[g] = (sqrt(row_mass) * fn <= 1e-13 * scale) ? 1 : 0;
   }
 }
 
@@ -522,10 +547,10 @@ static void clips(const double* d, const double* ut, const int* signs, int64_t n
       const double v = ut[i * k + r] * ut[i * k + r];
       if (signs[r] > 0) pos += v; else neg += v;
     }
-  double scale = 1.0;
+  double scale = pos + neg;
   for (int64_t i = 0; i < n; ++i)
     if (fabs(d[i]) > scale) scale = fabs(d[i]);
-  const double pad = 1e-9 * scale;
+  const double pad = 1e-9 * (scale > 0.0 ? scale : 1.0);
   *lo_clip = d[0] - neg * (1.0 + 1e-12) - pad;
   *hi_clip = d[n - 1] + pos * (1.0 + 1e-12) + pad;
 }
@@ -571,40 +596,68 @@ static void null_vector_S(const double* d, const double* ut, const int* signs, i
  * bordered system [[M_i, -J w_i],[w_i^T, 0]], smallest singular direction via
  * M^T M + Jacobi, vector from the resolvent at the pole. Returns 0 on
  * rejection (caller falls back to e_idx, eigvec.cpp:298). */
+/* Vector of a root sitting on pole value v = d[idx] (eigvec.cpp:75-119, the
+ * bordered system), generalised to a multiple pole: R = the rows within
+ * merge_gap of v (a compressed run keeps up to k of them). Unknowns beta (k)
+ * and xi (|R|): (I + J T) beta - J U_R^T xi = 0, U_R beta = 0, T the pole sum
+ * over the rows outside R. Its null space holds one direction per root on v;
+ * the which-th root on v takes the eigenvector of B^T B with the which-th
+ * smallest eigenvalue (orthogonal directions for distinct roots). The vector
+ * is x_s = -(u_s . beta) / (d_s - v) outside R and xi on R. */
 static int collision_vector(const double* d, const double* ut, const int* signs, int64_t n,
-                            int64_t k, int64_t idx, double merge_gap, double* w_out) {
-  const int64_t K1 = k + 1;
-  double B[(EO_MAXK + 1) * (EO_MAXK + 1)];
+                            int64_t k, int64_t idx, double merge_gap, int which,
+                            double* w_out) {
+  const double pole = d[idx];
+  int64_t r0 = idx, r1 = idx + 1;
+  while (r0 > 0 && fabs(d[r0 - 1] - pole) < merge_gap) --r0;
+  while (r1 < n && fabs(d[r1] - pole) < merge_gap) ++r1;
+  const int64_t nr = r1 - r0;
+  if (nr > EO_MAXK) return 0;
+  const int64_t K1 = k + nr;
+  enum { MK = 2 * EO_MAXK };
+  static _Thread_local double B[MK * MK], BtB[MK * MK], V[MK * MK];
+  double w[MK];
   memset(B, 0, sizeof(double) * K1 * K1);
   for (int64_t r = 0; r < k; ++r) B[r * K1 + r] = 1.0;
-  const double pole = d[idx];
   for (int64_t s = 0; s < n; ++s) {
+    if (s >= r0 && s < r1) continue;
     const double gap = d[s] - pole;
-    if (fabs(gap) < merge_gap) continue;
     const double* ws = ut + s * k;
     for (int64_t r = 0; r < k; ++r) {
       const double f = (double)signs[r] * ws[r] / gap;
       for (int64_t c = 0; c < k; ++c) B[r * K1 + c] += f * ws[c];
     }
   }
-  const double* wi = ut + idx * k;
-  for (int64_t r = 0; r < k; ++r) {
-    B[r * K1 + k] = -(double)signs[r] * wi[r];
-    B[k * K1 + r] = wi[r];
+  for (int64_t t = 0; t < nr; ++t) {
+    const double* wi = ut + (r0 + t) * k;
+    for (int64_t r = 0; r < k; ++r) {
+      B[r * K1 + k + t] = -(double)signs[r] * wi[r];
+      B[(k + t) * K1 + r] = wi[r];
+    }
   }
-  double BtB[(EO_MAXK + 1) * (EO_MAXK + 1)], w[EO_MAXK + 1], V[(EO_MAXK + 1) * (EO_MAXK + 1)];
   for (int64_t i = 0; i < K1; ++i)
     for (int64_t j = 0; j < K1; ++j) {
-      double s = 0.0;
-      for (int64_t l = 0; l < K1; ++l) s += B[l * K1 + i] * B[l * K1 + j];
-      BtB[i * K1 + j] = s;
+      double s2 = 0.0;
+      for (int64_t l = 0; l < K1; ++l) s2 += B[l * K1 + i] * B[l * K1 + j];
+      BtB[i * K1 + j] = s2;
     }
   sym_evd(BtB, (int)K1, w, V);
-  int imin = 0;
-  for (int r = 1; r < K1; ++r)
-    if (w[r] < w[imin]) imin = r;
-  double dir[EO_MAXK + 1], nrm = 0.0, fro = 0.0, res = 0.0;
-  for (int r = 0; r < K1; ++r) dir[r] = V[r * K1 + imin], nrm += dir[r] * dir[r];
+  /* the which-th smallest eigenvalue (ties broken by index) */
+  int pick = -1;
+  for (int rank = 0; rank <= which; ++rank) {
+    int best = -1;
+    for (int r = 0; r < K1; ++r) {
+      int taken = 0;
+      /* r already used by a smaller rank? */
+      for (int q = 0; q < K1; ++q)
+        if (q != r && (w[q] < w[r] || (w[q] == w[r] && q < r))) ++taken;
+      if (taken == rank) best = r;
+    }
+    pick = best;
+  }
+  if (pick < 0) return 0;
+  double dir[MK], nrm = 0.0, fro = 0.0, res = 0.0;
+  for (int r = 0; r < K1; ++r) dir[r] = V[r * K1 + pick], nrm += dir[r] * dir[r];
   nrm = sqrt(nrm);
   for (int r = 0; r < K1; ++r) dir[r] /= nrm;
   for (int64_t i = 0; i < K1 * K1; ++i) fro += B[i] * B[i];
@@ -617,15 +670,15 @@ static int collision_vector(const double* d, const double* ut, const int* signs,
   double norm2 = 0.0;
   for (int64_t s = 0; s < n; ++s) {
     w_out[s] = 0.0;
-    const double gap = d[s] - pole;
-    if (fabs(gap) < merge_gap) continue;
-    double ub = 0.0;
-    for (int64_t r = 0; r < k; ++r) ub += ut[s * k + r] * dir[r];
-    w_out[s] = -ub / gap;
+    if (s >= r0 && s < r1) {
+      w_out[s] = dir[k + (s - r0)];
+    } else {
+      double ub = 0.0;
+      for (int64_t r = 0; r < k; ++r) ub += ut[s * k + r] * dir[r];
+      w_out[s] = -ub / (d[s] - pole);
+    }
     norm2 += w_out[s] * w_out[s];
   }
-  w_out[idx] = dir[k];
-  norm2 += dir[k] * dir[k];
   if (!(norm2 > 0.0) || !isfinite(norm2)) return 0;
   const double inv = 1.0 / sqrt(norm2);
   for (int64_t s = 0; s < n; ++s) w_out[s] *= inv;
@@ -690,7 +743,22 @@ int eo_update(const double* q, const double* lambda, const double* kmat, const i
   double* u_full = (double*)malloc(sizeof(double) * n * k);
   eo_transform(q, kmat, n, k, u_full);
   int64_t keep[EO_MAXK];
-  const int64_t ke = eo_drop_zero_columns(u_full, n, k, keep);
+  const int exact = run_rel != 1e-12;
+  int64_t ke;
+  if (exact) { /* columns relative to the largest one only */
+    double colnorm[EO_MAXK], maxnorm = 0.0;
+    for (int64_t j = 0; j < k; ++j) {
+      double s2 = 0.0;
+      for (int64_t i = 0; i < n; ++i) s2 += u_full[i * k + j] * u_full[i * k + j];
+      colnorm[j] = sqrt(s2);
+      if (colnorm[j] > maxnorm) maxnorm = colnorm[j];
+    }
+    ke = 0;
+    for (int64_t j = 0; j < k; ++j)
+      if (colnorm[j] > 1e-15 * maxnorm && colnorm[j] > 0.0) keep[ke++] = j;
+  } else {
+    ke = eo_drop_zero_columns(u_full, n, k, keep);
+  }
   if (ke == 0) { /* rootfind.cpp:394-399: nothing couples */
     memcpy(lambda_out, lambda, sizeof(double) * n);
     if (q_out) memcpy(q_out, q, sizeof(double) * n * n);
@@ -711,10 +779,28 @@ int eo_update(const double* q, const double* lambda, const double* kmat, const i
   double* rep = (double*)malloc(sizeof(double) * n);
   double* alpha = (double*)malloc(sizeof(double) * n);
   int* kind = (int*)malloc(sizeof(int) * n);
-  const int64_t ng = make_runs(lambda, n, run_rel, gs, gl, rep);
+  double escale = 0.0;
+  if (exact) { /* max(max|lambda|, max_r ||u_r||^2): the size of A' */
+    for (int64_t r = 0; r < ke; ++r) {
+      double c2 = 0.0;
+      for (int64_t i = 0; i < n; ++i) c2 += u[i * ke + r] * u[i * ke + r];
+      if (c2 > escale) escale = c2;
+    }
+    for (int64_t i = 0; i < n; ++i)
+      if (fabs(lambda[i]) > escale) escale = fabs(lambda[i]);
+    if (!(escale > 0.0)) escale = 1.0;
+  }
+  const int64_t ng = make_runs_s(lambda, n, run_rel, escale, gs, gl, rep);
   group_weights(rep, gs, gl, ng, u, sg, ke, alpha);
-  classify(alpha, gs, gl, ng, u, n, ke, kind);
+  if (exact)
+    classify_exact(gs, gl, ng, u, n, ke, escale, kind);
+  else
+    classify(alpha, gs, gl, ng, u, n, ke, kind);
   const double u_norm = sqrt(frob2(u, n * ke));
+  /* numerical rank of a compressed run; exact mode: directions coupling below
+   * 1e-13 of the scale decouple (the unchanged rule of classify_exact) */
+  double rank_thr = DBL_EPSILON * u_norm;
+  if (exact && u_norm > 0.0 && 1e-13 * escale / u_norm > rank_thr) rank_thr = 1e-13 * escale / u_norm;
 
   /* Reduced problem: singleton groups keep their row; multi-member groups are
    * compressed by a Householder QR of their rows (rows >= rank decouple at
@@ -779,7 +865,7 @@ int eo_update(const double* q, const double* lambda, const double* kmat, const i
     for (int64_t t = 0; t < m; ++t) {
       double rn = 0.0;
       for (int64_t j = 0; j < ke; ++j) rn += B[t * ke + j] * B[t * ke + j];
-      if (t < steps && sqrt(rn) > DBL_EPSILON * u_norm) {
+      if (t < steps && sqrt(rn) > rank_thr) {
         d[N] = rep[g];
         memcpy(ut + N * ke, B + t * ke, sizeof(double) * ke);
         red_group[N] = g;
@@ -844,6 +930,7 @@ int eo_update(const double* q, const double* lambda, const double* kmat, const i
     double scale = 1.0;
     for (int64_t i = 0; i < n; ++i)
       if (fabs(lambda[i]) > scale) scale = fabs(lambda[i]);
+    if (exact) scale = escale;
     const double merge_gap = 1e-12 * scale;
     double* xt = (double*)calloc((size_t)n * n, sizeof(double));
     unsigned char* computed = (unsigned char*)calloc(n, 1);
@@ -864,7 +951,12 @@ int eo_update(const double* q, const double* lambda, const double* kmat, const i
       const int64_t j = e->payload;
       double* xr = (double*)malloc(sizeof(double) * N);
       int ok = 0;
-      if (rcol[j]) ok = collision_vector(d, ut, sg, N, ke, rorig[j], merge_gap, xr);
+      int which = 0; /* earlier roots on the same pole value (adjacent in j) */
+      if (rcol[j])
+        for (int64_t j2 = j - 1; j2 >= 0 && rcol[j2] &&
+                                 fabs(d[rorig[j2]] - d[rorig[j]]) < merge_gap; --j2)
+          ++which;
+      if (rcol[j]) ok = collision_vector(d, ut, sg, N, ke, rorig[j], merge_gap, which, xr);
       if (rcol[j] && !ok) {
         for (int64_t i = 0; i < N; ++i) xr[i] = 0.0;
         xr[rorig[j]] = 1.0;

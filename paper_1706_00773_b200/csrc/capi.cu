@@ -114,10 +114,12 @@ int guarded(eigmod_b200_ctx* ctx, F&& f) {
   } catch (const Error& e) {
     ctx->err = e.what();
     ctx->stage = e.stage;
+    if (e.code == EIGMOD_B200_CUDA) (void)cudaGetLastError();  // clear a non-sticky error
     return e.code;
   } catch (const std::exception& e) {
     ctx->err = e.what();
     ctx->stage = "cuda";
+    (void)cudaGetLastError();  // a non-sticky error must not poison the next call
     return EIGMOD_B200_CUDA;
   }
 }
@@ -155,12 +157,16 @@ void plan_groups(eigmod_b200_ctx* c, const double* lam, const double* u, const i
   std::vector<double> nh(k);
   EIGB_CUDA(cudaMemcpyAsync(nh.data(), norms, 8 * k, cudaMemcpyDeviceToHost, c->stream));
   EIGB_CUDA(cudaStreamSynchronize(c->stream));
-  // proj/src/rootfind.cpp:318-340: drop columns with norm <= 1e-15 max(1, max)
+  // proj/src/rootfind.cpp:318-340: drop columns with norm <= 1e-15 max(1, max);
+  // exact mode: relative to the largest column only (scale invariance)
+  p.exact = run_rel != eigb::kPoleMergeRelGap;
   double maxnorm = 0.0;
   for (auto& v : nh) v = std::sqrt(v), maxnorm = std::max(maxnorm, v);
-  const double drop = eigb::kColumnDropRel * std::max(1.0, maxnorm);
+  const double drop = eigb::kColumnDropRel * (p.exact ? maxnorm : std::max(1.0, maxnorm));
+  p.ufro2 = 0.0;
   for (int64_t j = 0; j < k; ++j)
-    if (nh[j] > drop) p.keep_h.push_back((int)j);
+    if (nh[j] > drop && nh[j] > 0.0)
+      p.keep_h.push_back((int)j), p.ufro2 = std::max(p.ufro2, nh[j] * nh[j]);
   p.n = n;
   p.k = (int)p.keep_h.size();
   if (p.k == 0) {  // rootfind.cpp:394-399: nothing couples

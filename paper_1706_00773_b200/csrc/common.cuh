@@ -50,6 +50,9 @@ constexpr double kPoleMergeRelGap = 1e-12;
 constexpr double kWeightDeflationRel = 1e-14;
 constexpr double kRowMassRel = 1e-12;
 constexpr double kColumnDropRel = 1e-15;
+// exact mode (the solve): rows coupling below this fraction of the problem
+// scale decouple unchanged
+constexpr double kExactCouplingRel = 1e-13;
 // Exact-mode run threshold (near-equal poles are merged and
 // Householder-compressed when closer than this, relative to max(1,|lambda|)).
 constexpr double kExactRunRelGap = 1e-10;

@@ -180,7 +180,8 @@ __device__ void block_exclusive_scan(const int64_t* in, int64_t* out, int64_t n,
 }
 
 __global__ void __launch_bounds__(kPlanThreads) runs_kernel(const double* __restrict__ lam,
-                                                            int64_t n, double rel,
+                                                            int64_t n, double rel, double ufro2,
+                                                            int exact,
                                                             int64_t* __restrict__ flag,
                                                             int64_t* __restrict__ gid,
                                                             int64_t* __restrict__ gstart,
@@ -191,12 +192,40 @@ __global__ void __launch_bounds__(kPlanThreads) runs_kernel(const double* __rest
                                                             double* __restrict__ scal) {
   __shared__ double red[32];
   __shared__ int64_t sh[kPlanThreads];
-  double m = 1.0;
+  // parity: the reference's scale max(1, max|lambda|) (secular.cpp:285-287);
+  // exact: max(max|lambda|, max_r ||u_r||^2), the size of A', so every
+  // threshold is relative to the problem (A -> c A gives c lambda')
+  double m = exact ? 0.0 : 1.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, fabs(lam[i]));
-  const double scale = block_max(m, red);
+  double scale = block_max(m, red);
+  if (exact) {
+    scale = fmax(scale, ufro2);
+    if (!(scale > 0.0)) scale = 1.0;
+  }
   const double gap = rel * scale;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
-    flag[i] = (i == 0 || !(lam[i] - lam[i - 1] < gap)) ? 1 : 0;
+  if (!exact) {
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+      flag[i] = (i == 0 || !(lam[i] - lam[i - 1] < gap)) ? 1 : 0;
+  } else {
+    // exact mode: a run never spans more than the gap (merging moves every
+    // member by less than the gap; the reference chains consecutive gaps).
+    // Run starts are found sequentially over the (rare) chains of close
+    // neighbours: thread 0 walks only positions whose left gap is small.
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+      flag[i] = (i == 0 || !(lam[i] - lam[i - 1] < gap)) ? 1 : 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t start = 0;
+      for (int64_t i = 1; i < n; ++i) {
+        if (flag[i]) {
+          start = i;
+        } else if (!(lam[i] - lam[start] < gap)) {
+          flag[i] = 1;
+          start = i;
+        }
+      }
+    }
+  }
   __syncthreads();
   __shared__ int64_t ng;
   block_exclusive_scan(flag, gid, n, &ng, sh);
@@ -231,7 +260,7 @@ __global__ void __launch_bounds__(kPlanThreads) runs_kernel(const double* __rest
 __global__ void __launch_bounds__(kPlanThreads) classify_kernel(
     const double* __restrict__ u, int64_t n, int kp, int k, const double* __restrict__ alpha,
     const int64_t* __restrict__ gstart, const int64_t* __restrict__ glen, const int64_t* counts,
-    int* __restrict__ kind, double* __restrict__ scal) {
+    int exact, int* __restrict__ kind, double* __restrict__ scal) {
   __shared__ double red[32];
   const int64_t ng = counts[0];
   double am = 0.0;
@@ -245,9 +274,19 @@ __global__ void __launch_bounds__(kPlanThreads) classify_kernel(
   const double fn = sqrt(block_sum(um, red));
   const double u_mass = fn * fn;
   const double drop = kWeightDeflationRel * (1.0 + alpha_mass);
+  // exact mode: a group decouples unchanged when its rows couple to the rest
+  // by less than 1e-13 of the problem scale (|u_g| ||U|| <= 1e-13 s: residual
+  // of the unchanged pair below 1e-13 ||A'||); collided groups stay in the
+  // reduced problem, where the solver finds their roots on the pole
+  const double scale = scal[0];
   for (int64_t g = threadIdx.x; g < ng; g += blockDim.x) {
     int kd = 0;
-    if (fabs(alpha[g]) <= drop) {
+    if (exact) {
+      double row_mass = 0.0;
+      for (int64_t i = gstart[g]; i < gstart[g] + glen[g]; ++i)
+        for (int r = 0; r < k; ++r) row_mass += u[i * kp + r] * u[i * kp + r];
+      kd = (sqrt(row_mass) * fn <= kExactCouplingRel * scale) ? 1 : 0;
+    } else if (fabs(alpha[g]) <= drop) {
       double row_mass = 0.0;
       for (int64_t i = gstart[g]; i < gstart[g] + glen[g]; ++i)
         for (int r = 0; r < k; ++r) row_mass += u[i * kp + r] * u[i * kp + r];
@@ -271,7 +310,7 @@ __global__ void compress_kernel(const double* __restrict__ u, int kp, int k,
                                 const int64_t* counts, const int64_t* __restrict__ hoff,
                                 const int64_t* __restrict__ roff, double* __restrict__ hbuf,
                                 double* __restrict__ rbuf, int64_t* __restrict__ rank,
-                                const double* __restrict__ scal) {
+                                const double* __restrict__ scal, int exact) {
   const int64_t ng = counts[0];
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= ng) return;
@@ -325,8 +364,11 @@ __global__ void compress_kernel(const double* __restrict__ u, int kp, int k,
       }
     }
   }
-  // numerical rank: leading rows with norm above eps * ||U||_F
-  const double thr = DBL_EPSILON * scal[3];
+  // numerical rank: leading rows with norm above eps * ||U||_F; in exact mode
+  // also above the decoupling level of classify_kernel (a direction whose
+  // coupling |r| ||U|| is below 1e-13 of the scale decouples at the run value)
+  double thr = DBL_EPSILON * scal[3];
+  if (exact && scal[3] > 0.0) thr = fmax(thr, kExactCouplingRel * scal[0] / scal[3]);
   int64_t r = 0;
   for (int64_t t = 0; t < steps; ++t) {
     double rn = 0.0;
@@ -410,7 +452,7 @@ __global__ void clips_kernel(const double* __restrict__ d, const double* __restr
                              int64_t nr, int kp, int k, const int* __restrict__ sgn,
                              double* __restrict__ scal) {
   __shared__ double red[32];
-  double pos = 0.0, neg = 0.0, m = 1.0;
+  double pos = 0.0, neg = 0.0, m = 0.0;
   for (int64_t t = threadIdx.x; t < nr * kp; t += blockDim.x) {
     const int c = (int)(t % kp);
     if (c >= k) continue;
@@ -422,7 +464,8 @@ __global__ void clips_kernel(const double* __restrict__ d, const double* __restr
   neg = block_sum(neg, red);
   m = block_max(m, red);
   if (threadIdx.x == 0) {
-    const double pad = 1e-9 * m;
+    m = fmax(m, pos + neg);
+    const double pad = 1e-9 * (m > 0.0 ? m : 1.0);
     scal[4] = (nr > 0) ? d[0] - neg * (1.0 + 1e-12) - pad : 0.0;
     scal[5] = (nr > 0) ? d[nr - 1] + pos * (1.0 + 1e-12) + pad : 0.0;
   }
@@ -460,6 +503,7 @@ void repack_columns_dev(const double* u, int64_t n, int kp, const int* keep, int
 void build_plan_groups(Plan& p, const double* lam, int64_t n, double run_rel, DeviceScratch& ws,
                        cudaStream_t st) {
   p.n = n;
+  p.exact = run_rel != kPoleMergeRelGap;
   int64_t* flag = ws.get_i64("pl_flag", n);
   p.gid = ws.get_i64("pl_gid", n);
   p.gstart = ws.get_i64("pl_gstart", n);
@@ -468,7 +512,8 @@ void build_plan_groups(Plan& p, const double* lam, int64_t n, double run_rel, De
   p.rep_row = ws.get_f64("pl_rep_row", n);
   p.counts = ws.get_i64("pl_counts", 8);
   p.scal = ws.get_f64("pl_scal", 8);
-  runs_kernel<<<1, kPlanThreads, 0, st>>>(lam, n, run_rel, flag, p.gid, p.gstart, p.glen, p.gval,
+  runs_kernel<<<1, kPlanThreads, 0, st>>>(lam, n, run_rel, p.ufro2, p.exact ? 1 : 0, flag, p.gid,
+                                           p.gstart, p.glen, p.gval,
                                            p.rep_row, p.counts, p.scal);
   EIGB_LAUNCH_CHECK();
   int64_t ng = 0;
@@ -492,7 +537,7 @@ void build_plan_finish(Plan& p, const double* lam, DeviceScratch& ws, cudaStream
   const int64_t n = p.n, ng = p.ng;
   p.kind = ws.get_i32("pl_kind", ng);
   classify_kernel<<<1, kPlanThreads, 0, st>>>(p.u, n, kp, k, p.alpha, p.gstart, p.glen, p.counts,
-                                               p.kind, p.scal);
+                                               p.exact ? 1 : 0, p.kind, p.scal);
   EIGB_LAUNCH_CHECK();
 
   // multi-member runs: host-side offsets (lengths are needed for H/R storage)
@@ -521,7 +566,7 @@ void build_plan_finish(Plan& p, const double* lam, DeviceScratch& ws, cudaStream
   if (nmulti > 0) {
     compress_kernel<<<(unsigned)cdiv(ng, 64), 64, 0, st>>>(p.u, kp, k, p.gstart, p.glen, p.kind,
                                                          p.counts, p.hoff, p.roff, p.hbuf, p.rbuf,
-                                                         p.rank, p.scal);
+                                                         p.rank, p.scal, p.exact ? 1 : 0);
     EIGB_LAUNCH_CHECK();
   } else {
     EIGB_CUDA(cudaMemsetAsync(p.rank, 0, 8 * ng, st));

@@ -32,6 +32,8 @@ struct Plan {
           *off_dec = nullptr;
   double scale = 1.0, alpha_mass = 0.0, u_mass = 0.0, lo_clip = 0.0, hi_clip = 0.0;
   double run_rel = kExactRunRelGap;
+  bool exact = true;     // scale-relative thresholds (run_rel != the reference's 1e-12)
+  double ufro2 = 0.0;    // max_r ||u_r||^2 over the kept columns (exact-mode scale)
 
   ReducedView view() const {
     return ReducedView{d, ur, sgn, nred, k, kp, m_neg, lo_clip, hi_clip};

@@ -71,10 +71,16 @@ __device__ __forceinline__ void load_S(const double* rb, const int* sgn, int k, 
 template <int KP>
 __global__ void __launch_bounds__(kPassThreads, 1) count_sweep_kernel(ReducedView rp,
                                                                       int* __restrict__ counts,
-                                                                      int64_t qbeg, int64_t qend) {
+                                                                      int64_t qbeg, int64_t qend,
+                                                                      double* __restrict__ gscratch) {
   using C = PassCfg<KP>;
   extern __shared__ __align__(16) double smem[];
-  double* F = smem + C::SMEM_DOUBLES;  // interleaved [KP*KP][32]
+  // factor storage: interleaved [KP*KP][32] in shared memory for KP <= 16,
+  // per-slot rows in global scratch above (32 x 32 x 32 doubles do not fit)
+  constexpr bool kSmemF = KP <= 16;
+  double* F = kSmemF ? smem + C::SMEM_DOUBLES
+                     : gscratch + (size_t)blockIdx.x * 32 * KP * KP;
+  constexpr int es = kSmemF ? 32 : 1;
   __shared__ double dob[32], delta[32];
   __shared__ int active[32], hit[32];
   const int t = threadIdx.x;
@@ -93,9 +99,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) count_sweep_kernel(ReducedVie
   secular_pass<KP>(rp.d, rp.u, rp.n, sl, o, smem);
   if (t < 32 && active[t]) {
     const double* rb = pass_result<KP>(smem) + t * C::OUT;
-    load_S<KP>(rb, rp.sgn, rp.k, F + t, 32);
+    double* Ft = kSmemF ? F + t : F + (size_t)t * KP * KP;
+    load_S<KP>(rb, rp.sgn, rp.k, Ft, es);
     int piv[KP], zero;
-    const int neg = bk_factor(F + t, KP, KP, piv, &zero, 32);
+    const int neg = bk_factor(Ft, KP, KP, piv, &zero, es);
     const double x = delta[t];
     // a hit (x on a pole, duplicates) gives an unusable point: -1
     counts[q0 + t] = hit[t] ? -1 : (int)(dev_n_less(rp.d, rp.n, x) + rp.m_neg - neg);
@@ -616,14 +623,17 @@ size_t solve_smem_bytes() {
 }
 
 template <int KP>
-void launch_sweep(const ReducedView& rp, int* counts, int64_t qbeg, int64_t qend, cudaStream_t st) {
+void launch_sweep(const ReducedView& rp, int* counts, int64_t qbeg, int64_t qend,
+                  DeviceScratch& ws, cudaStream_t st) {
   using C = PassCfg<KP>;
-  const size_t sm = sizeof(double) * (C::SMEM_DOUBLES + 32 * KP * KP);
+  constexpr bool kSmemF = KP <= 16;
+  const size_t sm = sizeof(double) * (C::SMEM_DOUBLES + (kSmemF ? 32 * KP * KP : 0));
   EIGB_CUDA(cudaFuncSetAttribute(count_sweep_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sm));
   if (qend <= qbeg) return;
-  count_sweep_kernel<KP><<<(unsigned)cdiv(qend - qbeg, 32), kPassThreads, sm, st>>>(rp, counts, qbeg,
-                                                                                  qend);
+  const int64_t grid = cdiv(qend - qbeg, 32);
+  double* gs = kSmemF ? nullptr : ws.get_f64("sweep_scratch", (size_t)grid * 32 * KP * KP);
+  count_sweep_kernel<KP><<<(unsigned)grid, kPassThreads, sm, st>>>(rp, counts, qbeg, qend, gs);
   EIGB_LAUNCH_CHECK();
 }
 
@@ -858,12 +868,12 @@ void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t
   if (opt.sweep) {
     counts = ws.get_i32("sweep_counts", 2 * rp.n);
     switch (rp.kp) {
-      case 1: launch_sweep<1>(rp, counts, qbeg, qend, st); break;
-      case 2: launch_sweep<2>(rp, counts, qbeg, qend, st); break;
-      case 4: launch_sweep<4>(rp, counts, qbeg, qend, st); break;
-      case 8: launch_sweep<8>(rp, counts, qbeg, qend, st); break;
-      case 16: launch_sweep<16>(rp, counts, qbeg, qend, st); break;
-      case 32: launch_sweep<32>(rp, counts, qbeg, qend, st); break;
+      case 1: launch_sweep<1>(rp, counts, qbeg, qend, ws, st); break;
+      case 2: launch_sweep<2>(rp, counts, qbeg, qend, ws, st); break;
+      case 4: launch_sweep<4>(rp, counts, qbeg, qend, ws, st); break;
+      case 8: launch_sweep<8>(rp, counts, qbeg, qend, ws, st); break;
+      case 16: launch_sweep<16>(rp, counts, qbeg, qend, ws, st); break;
+      case 32: launch_sweep<32>(rp, counts, qbeg, qend, ws, st); break;
       default: throw Error(1, "", "solve_roots: unsupported padded rank");
     }
   }
