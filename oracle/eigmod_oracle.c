@@ -21,6 +21,7 @@
 
 #include <float.h>
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -432,6 +433,89 @@ int64_t eo_count_below(const double* d, const double* ut, const int* signs, int6
   return hit ? -1 : c;
 }
 
+/* Eigenvalue count at a pole value v itself (the limit from either side):
+ * T = J + sum over the rows off v of u u^T/(d - v), restricted to the
+ * orthogonal complement of the rows R at v (their span gets |R| huge
+ * eigenvalues of either sign), nu = its negative inertia; then
+ * #eig < v = #eig <= v = #{d < v} + m - nu when the restriction is
+ * nonsingular. Returns -1 if v has no rows. */
+static int64_t n_less(const double* d, int64_t n, double x);
+static int64_t n_leq(const double* d, int64_t n, double x);
+static int64_t count_at_pole(const double* d, const double* ut, const int* signs, int64_t n,
+                             int64_t k, double v, int64_t m_neg, int64_t* zeros) {
+  const int64_t p0 = n_less(d, n, v), p1 = n_leq(d, n, v);
+  if (p1 <= p0) return -1;
+  double T[EO_MAXK * EO_MAXK];
+  memset(T, 0, sizeof(double) * k * k);
+  for (int64_t s = 0; s < n; ++s) {
+    if (s >= p0 && s < p1) continue;
+    const double inv = 1.0 / (d[s] - v);
+    const double* ws = ut + s * k;
+    for (int64_t r = 0; r < k; ++r)
+      for (int64_t c = 0; c < k; ++c) T[r * k + c] += ws[r] * inv * ws[c];
+  }
+  for (int64_t r = 0; r < k; ++r) T[r * k + r] += (double)signs[r];
+  /* orthonormal basis of span(R) by modified Gram-Schmidt, then its
+   * complement: basis Z of k - q vectors from the identity columns */
+  double Bs[EO_MAXK * EO_MAXK];
+  int q = 0;
+  for (int64_t t = p0; t < p1 && q < k; ++t) {
+    double v2[EO_MAXK], nn = 0.0, n0 = 0.0;
+    for (int64_t c = 0; c < k; ++c) v2[c] = ut[t * k + c], n0 += v2[c] * v2[c];
+    for (int rep = 0; rep < 2; ++rep)
+      for (int b = 0; b < q; ++b) {
+        double dp = 0.0;
+        for (int64_t c = 0; c < k; ++c) dp += Bs[b * EO_MAXK + c] * v2[c];
+        for (int64_t c = 0; c < k; ++c) v2[c] -= dp * Bs[b * EO_MAXK + c];
+      }
+    for (int64_t c = 0; c < k; ++c) nn += v2[c] * v2[c];
+    if (!(nn > 1e-28 * n0)) continue;
+    nn = 1.0 / sqrt(nn);
+    for (int64_t c = 0; c < k; ++c) Bs[q * EO_MAXK + c] = v2[c] * nn;
+    ++q;
+  }
+  int nz = q;
+  for (int64_t e = 0; e < k && nz < k; ++e) {
+    double v2[EO_MAXK], nn = 0.0;
+    for (int64_t c = 0; c < k; ++c) v2[c] = (c == e) ? 1.0 : 0.0;
+    for (int rep = 0; rep < 2; ++rep)
+      for (int b = 0; b < nz; ++b) {
+        double dp = 0.0;
+        for (int64_t c = 0; c < k; ++c) dp += Bs[b * EO_MAXK + c] * v2[c];
+        for (int64_t c = 0; c < k; ++c) v2[c] -= dp * Bs[b * EO_MAXK + c];
+      }
+    for (int64_t c = 0; c < k; ++c) nn += v2[c] * v2[c];
+    if (!(nn > 1e-6)) continue;
+    nn = 1.0 / sqrt(nn);
+    for (int64_t c = 0; c < k; ++c) Bs[nz * EO_MAXK + c] = v2[c] * nn;
+    ++nz;
+  }
+  const int kc = nz - q;
+  int64_t nu = 0;
+  *zeros = 0;
+  if (kc > 0) {
+    double M[EO_MAXK * EO_MAXK], w[EO_MAXK], V[EO_MAXK * EO_MAXK];
+    for (int a = 0; a < kc; ++a)
+      for (int b = 0; b < kc; ++b) {
+        double acc = 0.0;
+        for (int64_t r = 0; r < k; ++r) {
+          double tr = 0.0;
+          for (int64_t c = 0; c < k; ++c) tr += T[r * k + c] * Bs[(q + b) * EO_MAXK + c];
+          acc += Bs[(q + a) * EO_MAXK + r] * tr;
+        }
+        M[a * kc + b] = acc;
+      }
+    sym_evd(M, kc, w, V);
+    double wmax = 0.0;
+    for (int a = 0; a < kc; ++a) wmax = fmax(wmax, fabs(w[a]));
+    for (int a = 0; a < kc; ++a) {
+      if (fabs(w[a]) <= 1e-14 * wmax) ++*zeros; /* eigenvalue of A' exactly at v */
+      else if (w[a] < 0.0) ++nu;
+    }
+  }
+  return p0 + m_neg - nu; /* #eig <= v; #eig < v is this minus *zeros */
+}
+
 /* #{d_i < x} and #{d_i <= x} by binary search. */
 static int64_t n_less(const double* d, int64_t n, double x) {
   int64_t lo = 0, hi = n;
@@ -462,9 +546,40 @@ static void solve_one(const double* d, const double* ut, const int* signs, int64
   double hi = (j + p_pos <= n - 1) ? d[j + p_pos] : hi_clip;
   int lo_ok = 0, hi_ok = 0;  /* endpoint evaluated with count == j / == j+1 */
   int64_t ne = 0;
+  double last_pole = NAN;    /* pole value whose limit count was taken */
   *collided = 0;
   for (int it = 0; it < 4000; ++it) {
     if (lo_ok && hi_ok && n_less(d, n, hi) == n_leq(d, n, lo)) break; /* isolated */
+    /* exactly one pole value v in [lo, hi] that is inside or an uncertified
+     * endpoint: split the bracket at the pole itself (its limit count says on
+     * which side root j lies; both sides empty means the root is v) */
+    {
+      const int64_t a = n_less(d, n, lo), b = n_leq(d, n, hi); /* poles in [lo, hi] */
+      if (b > a && d[a] == d[b - 1]) {
+        const double v = d[a];
+        const int inside = v > lo && v < hi;
+        const int open_end = (v == hi && !hi_ok) || (v == lo && !lo_ok);
+        if ((inside || open_end) && v != last_pole) {
+          last_pole = v;
+          int64_t zeros = 0;
+          const int64_t cplus = count_at_pole(d, ut, signs, n, k, v, m_neg, &zeros);
+          const int64_t cminus = cplus - zeros;
+          ++ne;
+          if (cminus >= j + 1) {
+            hi = v;
+            hi_ok = (cminus == j + 1);
+          } else if (cplus <= j) {
+            lo = v;
+            lo_ok = (cplus == j);
+          } else { /* the root sits on v (a collision) */
+            lo = hi = v;
+            break;
+          }
+          if (lo == hi) break;
+          continue;
+        }
+      }
+    }
     double mid = 0.5 * (lo + hi);
     if (!(mid > lo && mid < hi)) break;
     int hit;
@@ -596,16 +711,19 @@ static void null_vector_S(const double* d, const double* ut, const int* signs, i
  * bordered system [[M_i, -J w_i],[w_i^T, 0]], smallest singular direction via
  * M^T M + Jacobi, vector from the resolvent at the pole. Returns 0 on
  * rejection (caller falls back to e_idx, eigvec.cpp:298). */
-/* Vector of a root sitting on pole value v = d[idx] (eigvec.cpp:75-119, the
- * bordered system), generalised to a multiple pole: R = the rows within
- * merge_gap of v (a compressed run keeps up to k of them). Unknowns beta (k)
- * and xi (|R|): (I + J T) beta - J U_R^T xi = 0, U_R beta = 0, T the pole sum
- * over the rows outside R. Its null space holds one direction per root on v;
- * the which-th root on v takes the eigenvector of B^T B with the which-th
- * smallest eigenvalue (orthogonal directions for distinct roots). The vector
- * is x_s = -(u_s . beta) / (d_s - v) outside R and xi on R. */
+/* Vector of a root lambda = v + delta at or next to the pole value v = d[idx]
+ * (eigvec.cpp:75-119, the bordered system), generalised to a multiple pole
+ * and to delta != 0: R = the rows at v (within merge_gap of it; a compressed
+ * run keeps up to k of them). With z = J U^T x and xi = x_R,
+ *   (I + J T(lambda)) z - J U_R^T xi = 0,   U_R z - delta xi = 0,
+ * T(lambda) the pole sum over the rows outside R; x_s = -(u_s . z) /
+ * ((d_s - v) - delta) outside R and xi on R. Unlike the formula
+ * x_s = (u_s . y) / (d_s - lambda) this keeps x_R accurate when delta is far
+ * below the pole's coupling (0/0 in the formula). With delta = 0 the null
+ * space holds one direction per root on v; the which-th root takes the
+ * eigenvector of B^T B with the which-th smallest eigenvalue. */
 static int collision_vector(const double* d, const double* ut, const int* signs, int64_t n,
-                            int64_t k, int64_t idx, double merge_gap, int which,
+                            int64_t k, int64_t idx, double delta, double merge_gap, int which,
                             double* w_out) {
   const double pole = d[idx];
   int64_t r0 = idx, r1 = idx + 1;
@@ -621,7 +739,7 @@ static int collision_vector(const double* d, const double* ut, const int* signs,
   for (int64_t r = 0; r < k; ++r) B[r * K1 + r] = 1.0;
   for (int64_t s = 0; s < n; ++s) {
     if (s >= r0 && s < r1) continue;
-    const double gap = d[s] - pole;
+    const double gap = (d[s] - pole) - delta;
     const double* ws = ut + s * k;
     for (int64_t r = 0; r < k; ++r) {
       const double f = (double)signs[r] * ws[r] / gap;
@@ -634,6 +752,7 @@ static int collision_vector(const double* d, const double* ut, const int* signs,
       B[r * K1 + k + t] = -(double)signs[r] * wi[r];
       B[(k + t) * K1 + r] = wi[r];
     }
+    B[(k + t) * K1 + k + t] = -delta;
   }
   for (int64_t i = 0; i < K1; ++i)
     for (int64_t j = 0; j < K1; ++j) {
@@ -661,6 +780,52 @@ static int collision_vector(const double* d, const double* ut, const int* signs,
   nrm = sqrt(nrm);
   for (int r = 0; r < K1; ++r) dir[r] /= nrm;
   for (int64_t i = 0; i < K1 * K1; ++i) fro += B[i] * B[i];
+  if (which == 0) {
+    /* B^T B squares the conditioning: two inverse-iteration steps on B itself
+     * (LU with partial pivoting; exact zero pivots replaced by eps ||B||) */
+    static _Thread_local double L[MK * MK];
+    int piv[MK];
+    memcpy(L, B, sizeof(double) * K1 * K1);
+    const double tiny = DBL_EPSILON * sqrt(fro);
+    for (int c = 0; c < K1; ++c) {
+      int pr = c;
+      for (int r = c + 1; r < K1; ++r)
+        if (fabs(L[r * K1 + c]) > fabs(L[pr * K1 + c])) pr = r;
+      piv[c] = pr;
+      if (pr != c)
+        for (int t = 0; t < K1; ++t) {
+          const double x = L[c * K1 + t];
+          L[c * K1 + t] = L[pr * K1 + t];
+          L[pr * K1 + t] = x;
+        }
+      if (fabs(L[c * K1 + c]) < tiny) L[c * K1 + c] = (L[c * K1 + c] < 0.0 ? -tiny : tiny);
+      for (int r = c + 1; r < K1; ++r) {
+        const double f = L[r * K1 + c] / L[c * K1 + c];
+        L[r * K1 + c] = f;
+        for (int t = c + 1; t < K1; ++t) L[r * K1 + t] -= f * L[c * K1 + t];
+      }
+    }
+    for (int it = 0; it < 2; ++it) {
+      double x[MK];
+      memcpy(x, dir, sizeof(double) * K1);
+      for (int c = 0; c < K1; ++c) {
+        const double t2 = x[c];
+        x[c] = x[piv[c]];
+        x[piv[c]] = t2;
+      }
+      for (int r = 1; r < K1; ++r)
+        for (int c = 0; c < r; ++c) x[r] -= L[r * K1 + c] * x[c];
+      for (int r = K1 - 1; r >= 0; --r) {
+        for (int c = r + 1; c < K1; ++c) x[r] -= L[r * K1 + c] * x[c];
+        x[r] /= L[r * K1 + r];
+      }
+      double xn = 0.0;
+      for (int r = 0; r < K1; ++r) xn += x[r] * x[r];
+      if (!(xn > 0.0) || !isfinite(xn)) break;
+      xn = 1.0 / sqrt(xn);
+      for (int r = 0; r < K1; ++r) dir[r] = x[r] * xn;
+    }
+  }
   for (int64_t i = 0; i < K1; ++i) {
     double mi = 0.0;
     for (int64_t j = 0; j < K1; ++j) mi += B[i * K1 + j] * dir[j];
@@ -675,7 +840,7 @@ static int collision_vector(const double* d, const double* ut, const int* signs,
     } else {
       double ub = 0.0;
       for (int64_t r = 0; r < k; ++r) ub += ut[s * k + r] * dir[r];
-      w_out[s] = -ub / (d[s] - pole);
+      w_out[s] = -ub / ((d[s] - pole) - delta);
     }
     norm2 += w_out[s] * w_out[s];
   }
@@ -835,15 +1000,25 @@ int eo_update(const double* q, const double* lambda, const double* kmat, const i
     for (int64_t i = 0; i < m * m; ++i) H[i] = 0.0;
     for (int64_t i = 0; i < m; ++i) H[i * m + i] = 1.0;
     const int64_t steps = m < ke ? m : ke;
+    /* column pivoting (largest remaining column): rank-revealing, so a
+     * numerically dependent run row ends up with a tiny residual row */
+    int64_t used = 0; /* bit mask of pivot columns (ke <= 64) */
     for (int64_t c = 0; c < steps; ++c) {
-      double nrm = 0.0;
-      for (int64_t i = c; i < m; ++i) nrm += B[i * ke + c] * B[i * ke + c];
-      nrm = sqrt(nrm);
-      if (nrm == 0.0) continue;
-      const double al = B[c * ke + c] >= 0.0 ? -nrm : nrm;
+      int64_t pc = -1;
+      double best = 0.0;
+      for (int64_t jj = 0; jj < ke; ++jj) {
+        if ((used >> jj) & 1) continue;
+        double s2 = 0.0;
+        for (int64_t i = c; i < m; ++i) s2 += B[i * ke + jj] * B[i * ke + jj];
+        if (s2 > best) best = s2, pc = jj;
+      }
+      if (pc < 0) break;
+      used |= (int64_t)1 << pc;
+      const double nrm = sqrt(best);
+      const double al = B[c * ke + pc] >= 0.0 ? -nrm : nrm;
       double vn = 0.0;
       for (int64_t i = c; i < m; ++i) {
-        v[i] = B[i * ke + c] - (i == c ? al : 0.0);
+        v[i] = B[i * ke + pc] - (i == c ? al : 0.0);
         vn += v[i] * v[i];
       }
       if (vn == 0.0) continue;
@@ -956,7 +1131,11 @@ int eo_update(const double* q, const double* lambda, const double* kmat, const i
         for (int64_t j2 = j - 1; j2 >= 0 && rcol[j2] &&
                                  fabs(d[rorig[j2]] - d[rorig[j]]) < merge_gap; --j2)
           ++which;
-      if (rcol[j]) ok = collision_vector(d, ut, sg, N, ke, rorig[j], merge_gap, which, xr);
+      /* origin on a multiple pole: the shifted bordered system */
+      const int64_t oj = rorig[j];
+      const int multi = (oj > 0 && d[oj - 1] == d[oj]) || (oj + 1 < N && d[oj + 1] == d[oj]);
+      if (rcol[j]) ok = collision_vector(d, ut, sg, N, ke, oj, 0.0, merge_gap, which, xr);
+      else if (multi) ok = collision_vector(d, ut, sg, N, ke, oj, rdel[j], 0.0, 0, xr);
       if (rcol[j] && !ok) {
         for (int64_t i = 0; i < N; ++i) xr[i] = 0.0;
         xr[rorig[j]] = 1.0;

@@ -25,7 +25,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libeigmod_b200.so")
+LIB_PATH = os.environ.get("EIGMOD_B200_LIB") or os.path.join(_PKG, "lib", "libeigmod_b200.so")
 
 _lib = None
 _lock = threading.Lock()

@@ -495,6 +495,8 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
     } else if (std::string(key) == "step_tol") {
       if (!(value > 0.0)) throw Error(1, "", "set_option: step_tol must be positive");
       ctx->sopt.step_tol = value;
+    } else if (std::string(key) == "pole_split") {
+      ctx->sopt.pole_split = value != 0.0;
     } else if (std::string(key) == "fexit_rel") {
       ctx->sopt.fexit_rel = value;
     } else if (std::string(key) == "floor_rel") {

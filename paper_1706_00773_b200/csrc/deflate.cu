@@ -327,42 +327,46 @@ __global__ void compress_kernel(const double* __restrict__ u, int kp, int k,
   for (int64_t i = 0; i < m * m; ++i) H[i] = 0.0;
   for (int64_t i = 0; i < m; ++i) H[i * m + i] = 1.0;
   const int64_t steps = m < k ? m : k;
+  // Householder QR with column pivoting (largest remaining column): rank-
+  // revealing, so a numerically dependent run row leaves a tiny residual row.
+  unsigned long long used = 0ull;  // pivot columns (k <= 32)
   for (int64_t c = 0; c < steps; ++c) {
-    double nrm = 0.0;
-    for (int64_t i = c; i < m; ++i) nrm += B[i * kp + c] * B[i * kp + c];
-    nrm = sqrt(nrm);
-    if (nrm == 0.0) continue;
-    const double al = B[c * kp + c] >= 0.0 ? -nrm : nrm;
-    double vn = 0.0;
-    // v stored temporarily in column c of B below the diagonal is not safe;
-    // recompute per use from (B[i][c] - (i==c ? al : 0)).
-    for (int64_t i = c; i < m; ++i) {
-      const double vi = B[i * kp + c] - (i == c ? al : 0.0);
-      vn += vi * vi;
+    int pc = -1;
+    double best = 0.0;
+    for (int jj = 0; jj < k; ++jj) {
+      if ((used >> jj) & 1ull) continue;
+      double s2 = 0.0;
+      for (int64_t i = c; i < m; ++i) s2 += B[i * kp + jj] * B[i * kp + jj];
+      if (s2 > best) best = s2, pc = jj;
     }
+    if (pc < 0) break;
+    used |= 1ull << pc;
+    const double nrm = sqrt(best);
+    const double al = B[c * kp + pc] >= 0.0 ? -nrm : nrm;
+    const double v_c = B[c * kp + pc] - al;
+    double vn = v_c * v_c;
+    for (int64_t i = c + 1; i < m; ++i) vn += B[i * kp + pc] * B[i * kp + pc];
     if (vn == 0.0) continue;
     const double beta = 2.0 / vn;
-    const double v_c = B[c * kp + c] - al;
-    // H <- (I - beta v v^T) H, B <- (I - beta v v^T) B; column c of B last.
+    // H <- (I - beta v v^T) H, B <- (I - beta v v^T) B, v = (v_c, B[c+1.., pc]);
+    // the pivot column is updated last (it holds v)
     for (int64_t j = 0; j < m; ++j) {
       double s = v_c * H[c * m + j];
-      for (int64_t i = c + 1; i < m; ++i) s += B[i * kp + c] * H[i * m + j];
+      for (int64_t i = c + 1; i < m; ++i) s += B[i * kp + pc] * H[i * m + j];
       s *= beta;
       H[c * m + j] -= s * v_c;
-      for (int64_t i = c + 1; i < m; ++i) H[i * m + j] -= s * B[i * kp + c];
+      for (int64_t i = c + 1; i < m; ++i) H[i * m + j] -= s * B[i * kp + pc];
     }
-    for (int j = kp - 1; j >= (int)c; --j) {
+    for (int j = 0; j < kp; ++j) {
+      if (j == pc) continue;
       double s = v_c * B[c * kp + j];
-      for (int64_t i = c + 1; i < m; ++i) s += B[i * kp + c] * B[i * kp + j];
+      for (int64_t i = c + 1; i < m; ++i) s += B[i * kp + pc] * B[i * kp + j];
       s *= beta;
-      if (j == c) {
-        B[c * kp + c] -= s * v_c;  // = al
-        for (int64_t i = c + 1; i < m; ++i) B[i * kp + c] = 0.0;
-      } else {
-        B[c * kp + j] -= s * v_c;
-        for (int64_t i = c + 1; i < m; ++i) B[i * kp + j] -= s * B[i * kp + c];
-      }
+      B[c * kp + j] -= s * v_c;
+      for (int64_t i = c + 1; i < m; ++i) B[i * kp + j] -= s * B[i * kp + pc];
     }
+    B[c * kp + pc] = al;
+    for (int64_t i = c + 1; i < m; ++i) B[i * kp + pc] = 0.0;
   }
   // numerical rank: leading rows with norm above eps * ||U||_F; in exact mode
   // also above the decoupling level of classify_kernel (a direction whose

@@ -121,7 +121,10 @@ template <int KP>
 struct SolveArgs {
   ReducedView rp;
   const double* alpha;     // residues of the reduced poles (nullptr: no f-Newton)
-  const int* counts;       // sweep counts [2N] (-1 = unusable point)
+  const double* br_lo;     // initial brackets of roots [j0, j1) (bracket_kernel); nullptr:
+  const double* br_hi;     //   Weyl windows
+  const int* br_ok;        // bit 0: lo certified (count == j), bit 1: hi (count == j + 1)
+  int64_t j0;
   int64_t j_end;
   unsigned long long* next_root;
   RootRecords out;
@@ -130,7 +133,6 @@ struct SolveArgs {
   double step_tol;
   int max_iters;
   int writer;  // writes root records (cluster rank 0)
-  int64_t qbeg, qend;  // swept point range
   unsigned long long* prof;  // [0] passes, [1] active slot-passes, [2] slot batches
   double fexit_rel, floor_rel, floor_ulps, stall_ratio;
   int geo_bisect;
@@ -138,47 +140,74 @@ struct SolveArgs {
   double* trace;             // [kTraceRows][kTraceCols]
 };
 
-// Sweep bracket of root j: the last usable sweep point with count <= j and
-// the first with count > j (outer clips count 0 and N).
-template <int KP>
-__device__ void sweep_bracket(const SolveArgs<KP>& a, int64_t j, double* lo, double* hi,
-                              int* lo_ok, int* hi_ok) {
-  // the swept points are [qbeg, qend); outside them fall back to the Weyl
-  // window bound (proj/src/locate.cpp:159-171), uncertified
-  const int64_t N = a.rp.n;
-  const int64_t QB = a.qbeg, QE = a.qend;
-  int64_t L = QB, R = QE;  // first usable q with counts[q] > j
+// Sweep bracket of root j: the last usable point with count <= j and the
+// first with count > j, over the sequence d_a - theta g, d_a (the limit count
+// at the pole itself, taken for poles with roots next to them), d_a + theta g
+// (outer clips count 0 and N).
+__device__ __forceinline__ int comb_count(const int* counts, const int* pcounts, int64_t q3) {
+  const int64_t a = q3 / 3;
+  const int r = (int)(q3 - 3 * a);
+  if (r == 1) return pcounts ? pcounts[a] : -1;
+  return counts[2 * a + (r == 2)];
+}
+
+__device__ __forceinline__ double comb_point(const double* d, int64_t N, int64_t q3) {
+  const int64_t a = q3 / 3;
+  const int r = (int)(q3 - 3 * a);
+  if (r == 1) return d[a];
+  return sweep_point(d, N, 2 * a + (r == 2));
+}
+
+// Initial brackets of roots [j0, j1): the last usable point with count <= j
+// and the first with count > j over the sequence d_a - theta g, d_a (the
+// limit count at the pole itself, where taken), d_a + theta g for the swept
+// poles [pbeg, pend); outside them the Weyl window bound (proj/src/locate.cpp:
+// 159-171), uncertified; outer clips count 0 and N.
+__global__ void bracket_kernel(const double* __restrict__ d, int64_t N, const int* __restrict__ counts,
+                               const int* __restrict__ pcounts, int64_t pbeg, int64_t pend,
+                               int64_t j0, int64_t j1, int m_neg, int p_pos, double lo_clip,
+                               double hi_clip, double* __restrict__ br_lo,
+                               double* __restrict__ br_hi, int* __restrict__ br_ok) {
+  const int64_t j = j0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= j1) return;
+  const int64_t QB = 3 * pbeg, QE = 3 * pend;
+  int64_t L = QB, R = QE;  // first usable q3 with count > j
   while (L < R) {
     const int64_t mid = (L + R) >> 1;
     int64_t q = mid;
-    while (q < R && a.counts[q] < 0) ++q;
+    while (q < R && comb_count(counts, pcounts, q) < 0) ++q;
     if (q == R) { R = mid; continue; }
-    if (a.counts[q] > j) R = mid; else L = q + 1;
+    if (comb_count(counts, pcounts, q) > j) R = mid; else L = q + 1;
   }
   int64_t qh = L;
-  while (qh < QE && a.counts[qh] < 0) ++qh;
+  while (qh < QE && comb_count(counts, pcounts, qh) < 0) ++qh;
   int64_t ql = L - 1;
-  while (ql >= QB && a.counts[ql] < 0) --ql;
+  while (ql >= QB && comb_count(counts, pcounts, ql) < 0) --ql;
+  double lo, hi;
+  int lok, hok;
   if (ql >= QB) {
-    *lo = sweep_point(a.rp.d, N, ql);
-    *lo_ok = (a.counts[ql] == j);
+    lo = comb_point(d, N, ql);
+    lok = (comb_count(counts, pcounts, ql) == j);
   } else if (QB == 0) {
-    *lo = a.lo_clip;
-    *lo_ok = (j == 0);
+    lo = lo_clip;
+    lok = (j == 0);
   } else {
-    *lo = (j - a.m_neg >= 0) ? a.rp.d[j - a.m_neg] : a.lo_clip;
-    *lo_ok = 0;
+    lo = (j - m_neg >= 0) ? d[j - m_neg] : lo_clip;
+    lok = 0;
   }
   if (qh < QE) {
-    *hi = sweep_point(a.rp.d, N, qh);
-    *hi_ok = (a.counts[qh] == j + 1);
-  } else if (QE == 2 * N) {
-    *hi = a.hi_clip;
-    *hi_ok = (j + 1 == N);
+    hi = comb_point(d, N, qh);
+    hok = (comb_count(counts, pcounts, qh) == j + 1);
+  } else if (QE == 3 * N) {
+    hi = hi_clip;
+    hok = (j + 1 == N);
   } else {
-    *hi = (j + a.p_pos <= N - 1) ? a.rp.d[j + a.p_pos] : a.hi_clip;
-    *hi_ok = 0;
+    hi = (j + p_pos <= N - 1) ? d[j + p_pos] : hi_clip;
+    hok = 0;
   }
+  br_lo[j - j0] = lo;
+  br_hi[j - j0] = hi;
+  br_ok[j - j0] = lok | (hok << 1);
 }
 
 template <int KP>
@@ -219,8 +248,11 @@ __device__ void slot_init(SolveSmem& s, double* y, int b, int64_t j, const Solve
   for (int c = 0; c < KP; ++c) y[b * KP + c] = (c < a.rp.k) ? y0 : 0.0;
   double lo, hi;
   int lok, hok;
-  if (a.counts) {
-    sweep_bracket<KP>(a, j, &lo, &hi, &lok, &hok);
+  if (a.br_lo) {
+    lo = a.br_lo[j - a.j0];
+    hi = a.br_hi[j - a.j0];
+    lok = a.br_ok[j - a.j0] & 1;
+    hok = (a.br_ok[j - a.j0] >> 1) & 1;
   } else {  // Weyl window (proj/src/locate.cpp:159-171)
     lo = (j - a.m_neg >= 0) ? d[j - a.m_neg] : a.lo_clip;
     hi = (j + a.p_pos <= N - 1) ? d[j + a.p_pos] : a.hi_clip;
@@ -673,15 +705,17 @@ bool launch_solve_cluster(const SolveArgs<KP>& a, int64_t nroots, int sms, cudaS
 }
 
 template <int KP>
-void launch_solve(const ReducedView& rp, const double* alpha, const int* counts, int64_t qbeg,
-                  int64_t qend, int64_t j0, int64_t j1, const RootRecords& out,
-                  const SolveOptions& opt, DeviceScratch& ws, int sms, cudaStream_t st) {
+void launch_solve(const ReducedView& rp, const double* alpha, const double* br_lo,
+                  const double* br_hi, const int* br_ok, int64_t j0, int64_t j1,
+                  const RootRecords& out, const SolveOptions& opt, DeviceScratch& ws, int sms,
+                  cudaStream_t st) {
   SolveArgs<KP> a;
   a.rp = rp;
   a.alpha = alpha;
-  a.counts = counts;
-  a.qbeg = qbeg;
-  a.qend = qend;
+  a.br_lo = br_lo;
+  a.br_hi = br_hi;
+  a.br_ok = br_ok;
+  a.j0 = j0;
   a.j_end = j1;
   a.out = out;
   a.m_neg = rp.m_neg;
@@ -853,6 +887,44 @@ void launch_inertia(const ReducedView& rp, const double* bval, const int64_t* br
   EIGB_LAUNCH_CHECK();
 }
 
+// Poles with roots next to them (the sweep points d_a -/+ theta g count
+// differently, or one of them is unusable) that are multiple (rows of a
+// compressed run) or lost a point: their limit counts split those brackets
+// at the pole itself. Rows at the pole value: [brow, brow + bcnt).
+__global__ void pole_select_kernel(const double* __restrict__ d, int64_t N, int64_t pbeg,
+                                   int64_t pend, const int* __restrict__ counts,
+                                   int* __restrict__ pcounts, int64_t* __restrict__ list,
+                                   double* __restrict__ bval, int64_t* __restrict__ brow,
+                                   int* __restrict__ bcnt, unsigned long long* nsel) {
+  const int64_t a = pbeg + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= pend) return;
+  pcounts[a] = -1;
+  const int c0 = counts[2 * a], c1 = counts[2 * a + 1];
+  if (c0 >= 0 && c1 >= 0 && c0 == c1) return;
+  const double v = d[a];
+  if (a > 0 && d[a - 1] == v) return;  // one evaluation per pole value
+  // simple poles with usable points are resolved by phase A bisection; the
+  // limit count is needed where rows coincide (a compressed run) or a point
+  // was unusable
+  const bool multi = a + 1 < N && d[a + 1] == v;
+  if (c0 >= 0 && c1 >= 0 && !multi) return;
+  const int64_t r1 = dev_n_leq(d, N, v);
+  const unsigned long long i = atomicAdd(nsel, 1ull);
+  list[i] = a;
+  bval[i] = v;
+  brow[i] = a;
+  bcnt[i] = (int)(r1 - a);
+}
+
+__global__ void pole_scatter_kernel(const int64_t* __restrict__ list, const int64_t* __restrict__ brow,
+                                    const int* __restrict__ bcnt, const int* __restrict__ nu,
+                                    int64_t nsel, int m_neg, int* __restrict__ pcounts) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nsel) return;
+  const int c = (int)(brow[i] + m_neg - nu[i]);
+  for (int t = 0; t < bcnt[i]; ++t) pcounts[list[i] + t] = c;
+}
+
 }  // namespace
 
 void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t j1,
@@ -877,9 +949,46 @@ void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t
       default: throw Error(1, "", "solve_roots: unsupported padded rank");
     }
   }
+  int* pcounts = nullptr;
+  if (opt.sweep && opt.pole_split && pe > pb) {
+    pcounts = ws.get_i32("sweep_pole_counts", rp.n);
+    const int64_t np = pe - pb;
+    int64_t* list = ws.get_i64("psel_list", np);
+    double* bval = ws.get_f64("psel_val", np);
+    int64_t* brow = ws.get_i64("psel_row", np);
+    int* bcnt = ws.get_i32("psel_cnt", np);
+    int* nu = ws.get_i32("psel_nu", np);
+    auto* nsel = reinterpret_cast<unsigned long long*>(ws.get_i64("psel_n", 1));
+    EIGB_CUDA(cudaMemsetAsync(nsel, 0, 8, st));
+    pole_select_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(rp.d, rp.n, pb, pe, counts, pcounts,
+                                                                 list, bval, brow, bcnt, nsel);
+    EIGB_LAUNCH_CHECK();
+    unsigned long long nh = 0;
+    EIGB_CUDA(cudaMemcpyAsync(&nh, nsel, 8, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaStreamSynchronize(st));
+    if (nh > 0) {
+      pole_inertia(rp, bval, brow, bcnt, (int64_t)nh, nu, ws, st);
+      pole_scatter_kernel<<<(unsigned)cdiv((int64_t)nh, 256), 256, 0, st>>>(list, brow, bcnt, nu,
+                                                                           (int64_t)nh, rp.m_neg,
+                                                                           pcounts);
+      EIGB_LAUNCH_CHECK();
+    }
+  }
+  double *br_lo = nullptr, *br_hi = nullptr;
+  int* br_ok = nullptr;
+  if (opt.sweep) {
+    const int64_t nr = j1 - j0;
+    br_lo = ws.get_f64("br_lo", nr);
+    br_hi = ws.get_f64("br_hi", nr);
+    br_ok = ws.get_i32("br_ok", nr);
+    bracket_kernel<<<(unsigned)cdiv(nr, 256), 256, 0, st>>>(
+        rp.d, rp.n, counts, pcounts, pb, pe, j0, j1, rp.m_neg, rp.k - rp.m_neg, rp.lo_clip,
+        rp.hi_clip, br_lo, br_hi, br_ok);
+    EIGB_LAUNCH_CHECK();
+  }
   if (!opt.fnewton) alpha = nullptr;
 #define EIGB_SOLVE(K) \
-  launch_solve<K>(rp, alpha, counts, qbeg, qend, j0, j1, out, opt, ws, sms, st)
+  launch_solve<K>(rp, alpha, br_lo, br_hi, br_ok, j0, j1, out, opt, ws, sms, st)
   switch (rp.kp) {
     case 1: EIGB_SOLVE(1); break;
     case 2: EIGB_SOLVE(2); break;

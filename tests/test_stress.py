@@ -55,11 +55,7 @@ def _case(seed):
     return q, lam, kmat, signs, kind
 
 
-NEAR_COLLISION_MULTIPOLE = {43}  # a root 15 ulps from a doubly-coupled pole
-
-
-@pytest.mark.parametrize("seed", [pytest.param(s, marks=pytest.mark.xfail(strict=True))
-                                  if s in NEAR_COLLISION_MULTIPOLE else s for s in range(60)])
+@pytest.mark.parametrize("seed", list(range(60)))
 def test_random_update(seed):
     from paper_1706_00773_b200 import capi
 

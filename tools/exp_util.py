@@ -1,4 +1,5 @@
 """Solver slot utilisation and per-pass time (dev tool)."""
+import os
 import sys
 
 sys.path.insert(0, '.')
@@ -9,12 +10,17 @@ from paper_1706_00773_b200.instances import make_instance_torch
 from paper_1706_00773_b200.sharded import CudaBackend, split
 
 dev = torch.device('cuda', 0)
-cases = [(4, 32768), (2, 8192), (4, 8192)]
+cases = [(4, 32768), (2, 8192), (4, 8192)][: int(os.environ.get('EXP_NCASES', '3'))]
 for cfg, n in cases:
     q, lam, kmat, signs = make_instance_torch(cfg, n=n, device=dev)
     k = kmat.shape[1]
     ctx = capi.Context(0)
     ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+    import os
+    for kv in os.environ.get("EIGMOD_OPTS", "").split(","):
+        if kv:
+            kk, vv = kv.split("=")
+            ctx.set_option(kk, float(vv))
     be = CudaBackend(ctx, n, k, signs.numpy())
     u = torch.zeros((n, be.kp), dtype=torch.float64, device=dev)
     be.project(q, kmat, 0, n, u)
