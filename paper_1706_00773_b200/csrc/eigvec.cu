@@ -12,6 +12,7 @@
 // Xt is written row by row with coalesced stores: HBM-bound (8 n^2 bytes).
 #include "pipeline.cuh"
 
+#include <cfloat>
 #include <cstdlib>
 #include <string>
 
@@ -90,40 +91,75 @@ __device__ void sym_evd_dev(double* a, int k, double* v) {
   }
 }
 
-// Bordered systems for collided roots, 32 per CTA: the pole pass with
-// |d_s - pole| < gap excluded gives T; B = [[I + J T, -J w],[w^T, 0]];
-// null direction from B^T B (eigvec.cpp:157-185); residual check 1e-6.
+// Bordered systems, 32 roots per CTA (proj/src/eigvec.cpp:75-119 generalised):
+// a root lambda = v + delta at or next to the pole value v = d[o], R = the rows
+// within gap of v (a compressed run keeps up to k of them). With z = J U^T x and
+// xi = x_R: (I + J T(lambda)) z - J U_R^T xi = 0, U_R z - delta xi = 0, T the
+// pole pass at lambda over the rows outside R. Used for collided roots (delta
+// = 0; the which-th root on v takes the which-th smallest direction of B^T B)
+// and for roots whose origin is a multiple pole, where the formula
+// x_s = (u_s . y)/(d_s - lambda) is 0/0 on R. The direction of B^T B is refined
+// by two inverse-iteration steps on B (LU, partial pivoting). Output per root
+// (stride kCollStride(KP)): z (KP), xi (KP), r0, |R|, delta, v.
+template <int KP>
+constexpr int kCollStride = 2 * KP + 4;
+
 template <int KP>
 __global__ void __launch_bounds__(kPassThreads, 1) collision_kernel(
     ReducedView rp, const int64_t* __restrict__ list, int64_t cnt, const int64_t* __restrict__ origin,
+    const double* __restrict__ rdelta, const int* __restrict__ mark, const int* __restrict__ which,
     double gap, double* __restrict__ colldir, int* __restrict__ collok, double* __restrict__ scratch) {
   using C = PassCfg<KP>;
+  constexpr int MK = 2 * KP;
   extern __shared__ __align__(16) double smem[];
   __shared__ double dob[32], delta[32];
   __shared__ int active[32], hit[32];
+  __shared__ int64_t xrow[32];
   const int t = threadIdx.x;
   const int64_t b0 = (int64_t)blockIdx.x * 32;
   if (t < 32) {
     const int64_t q = b0 + t;
     active[t] = q < cnt;
-    dob[t] = 0.0;
-    delta[t] = (q < cnt) ? rp.d[origin[list[q]]] : 0.0;
+    double v = 0.0, dl = 0.0;
+    int64_t xr = -1;
+    if (q < cnt) {
+      const int64_t j = list[q];
+      v = rp.d[origin[j]];
+      const bool coll = (mark[j] & 1) != 0;
+      dl = coll ? 0.0 : rdelta[j];
+      // a root next to (not on) a multiple pole: R = its origin row alone; the
+      // other rows at v stay in T at the finite difference -delta
+      if (!coll) xr = origin[j];
+    }
+    dob[t] = v;
+    delta[t] = dl;
+    xrow[t] = xr;
     hit[t] = 0;
   }
   __syncthreads();
-  PassSlots sl{dob, delta, nullptr, active, hit};
+  PassSlots sl{dob, delta, nullptr, active, hit, xrow};
   PassOpts o;
   o.exclude_zero = true;
-  o.excl_gap = gap;
+  o.excl_gap = gap;  // rows within gap of v: the bordered block
   secular_pass<KP>(rp.d, rp.u, rp.n, sl, o, smem);
   const double* red = pass_result<KP>(smem);
   if (t < 32 && active[t]) {
     const int64_t j = list[b0 + t];
-    const int64_t idx = origin[j];
-    const int k = rp.k, K1 = k + 1;
-    double* B = scratch + ((size_t)blockIdx.x * 32 + t) * 3 * (KP + 1) * (KP + 1);
-    double* BtB = B + K1 * K1;
-    double* V = BtB + K1 * K1;
+    const int64_t N = rp.n;
+    const double v = dob[t], dl = delta[t];
+    int64_t r0 = dev_n_leq(rp.d, N, v - gap), r1 = dev_n_less(rp.d, N, v + gap);
+    if (xrow[t] >= 0) r0 = xrow[t], r1 = r0 + 1;
+    const int nr = (int)(r1 - r0);
+    double* out = colldir + j * kCollStride<KP>;
+    if (nr < 1 || nr > KP) {
+      collok[j] = 2;
+      return;
+    }
+    const int k = rp.k, K1 = k + nr;
+    double* B = scratch + ((size_t)blockIdx.x * 32 + t) * 4 * MK * MK;
+    double* BtB = B + MK * MK;
+    double* V = BtB + MK * MK;
+    double* L = V + MK * MK;
     const double* rb = red + t * C::OUT;
     for (int r = 0; r < K1 * K1; ++r) B[r] = 0.0;
     for (int r = 0; r < k; ++r)
@@ -131,10 +167,13 @@ __global__ void __launch_bounds__(kPassThreads, 1) collision_kernel(
         const double tv = (r <= c) ? rb[C::pidx(r, c)] : rb[C::pidx(c, r)];
         B[r * K1 + c] = (r == c ? 1.0 : 0.0) + (double)rp.sgn[r] * tv;
       }
-    const double* wi = rp.u + idx * KP;
-    for (int r = 0; r < k; ++r) {
-      B[r * K1 + k] = -(double)rp.sgn[r] * wi[r];
-      B[k * K1 + r] = wi[r];
+    for (int tt = 0; tt < nr; ++tt) {
+      const double* wi = rp.u + (r0 + tt) * KP;
+      for (int r = 0; r < k; ++r) {
+        B[r * K1 + k + tt] = -(double)rp.sgn[r] * wi[r];
+        B[(k + tt) * K1 + r] = wi[r];
+      }
+      B[(k + tt) * K1 + k + tt] = -dl;
     }
     double fro = 0.0;
     for (int i = 0; i < K1; ++i)
@@ -145,24 +184,112 @@ __global__ void __launch_bounds__(kPassThreads, 1) collision_kernel(
         fro += B[i * K1 + jj] * B[i * K1 + jj];
       }
     sym_evd_dev(BtB, K1, V);
-    int imin = 0;
-    for (int r = 1; r < K1; ++r)
-      if (BtB[r * K1 + r] < BtB[imin * K1 + imin]) imin = r;
+    // the which-th smallest eigenvalue of B^T B (ties by index)
+    const int w = (mark[j] & 1) ? which[j] : 0;
+    int pick = -1;
+    for (int r = 0; r < K1; ++r) {
+      int below = 0;
+      for (int q = 0; q < K1; ++q)
+        if (q != r && (BtB[q * K1 + q] < BtB[r * K1 + r] ||
+                       (BtB[q * K1 + q] == BtB[r * K1 + r] && q < r)))
+          ++below;
+      if (below == w) pick = r;
+    }
+    if (pick < 0) {
+      collok[j] = 2;
+      return;
+    }
+    double dir[MK];
     double nrm = 0.0;
-    for (int r = 0; r < K1; ++r) nrm += V[r * K1 + imin] * V[r * K1 + imin];
-    nrm = sqrt(nrm);
+    for (int r = 0; r < K1; ++r) dir[r] = V[r * K1 + pick], nrm += dir[r] * dir[r];
+    nrm = rsqrt(nrm);
+    for (int r = 0; r < K1; ++r) dir[r] *= nrm;
+    if (w == 0) {  // B^T B squares the conditioning: refine on B itself
+      int piv[MK];
+      for (int r = 0; r < K1 * K1; ++r) L[r] = B[r];
+      const double tiny = DBL_EPSILON * sqrt(fro);
+      for (int c = 0; c < K1; ++c) {
+        int pr = c;
+        for (int r = c + 1; r < K1; ++r)
+          if (fabs(L[r * K1 + c]) > fabs(L[pr * K1 + c])) pr = r;
+        piv[c] = pr;
+        if (pr != c)
+          for (int q = 0; q < K1; ++q) {
+            const double x = L[c * K1 + q];
+            L[c * K1 + q] = L[pr * K1 + q];
+            L[pr * K1 + q] = x;
+          }
+        if (fabs(L[c * K1 + c]) < tiny) L[c * K1 + c] = (L[c * K1 + c] < 0.0 ? -tiny : tiny);
+        for (int r = c + 1; r < K1; ++r) {
+          const double f = L[r * K1 + c] / L[c * K1 + c];
+          L[r * K1 + c] = f;
+          for (int q = c + 1; q < K1; ++q) L[r * K1 + q] -= f * L[c * K1 + q];
+        }
+      }
+      for (int it = 0; it < 2; ++it) {
+        double x[MK];
+        for (int r = 0; r < K1; ++r) x[r] = dir[r];
+        for (int c = 0; c < K1; ++c) {
+          const double x2 = x[c];
+          x[c] = x[piv[c]];
+          x[piv[c]] = x2;
+        }
+        for (int r = 1; r < K1; ++r)
+          for (int c = 0; c < r; ++c) x[r] -= L[r * K1 + c] * x[c];
+        for (int r = K1 - 1; r >= 0; --r) {
+          for (int c = r + 1; c < K1; ++c) x[r] -= L[r * K1 + c] * x[c];
+          x[r] /= L[r * K1 + r];
+        }
+        double xn = 0.0;
+        for (int r = 0; r < K1; ++r) xn += x[r] * x[r];
+        if (!(xn > 0.0) || !isfinite(xn)) break;
+        xn = rsqrt(xn);
+        for (int r = 0; r < K1; ++r) dir[r] = x[r] * xn;
+      }
+    }
     double res = 0.0;
     for (int i = 0; i < K1; ++i) {
       double mi = 0.0;
-      for (int l = 0; l < K1; ++l) mi += B[i * K1 + l] * V[l * K1 + imin] / nrm;
+      for (int l = 0; l < K1; ++l) mi += B[i * K1 + l] * dir[l];
       res += mi * mi;
     }
     const int ok = sqrt(res) <= 1e-6 * fmax(1.0, sqrt(fro));
-    // beta (k entries, zero pads) then xi = direction[k] at index KP
-    for (int r = 0; r < KP; ++r) colldir[j * (KP + 1) + r] = (r < k) ? V[r * K1 + imin] / nrm : 0.0;
-    colldir[j * (KP + 1) + KP] = V[k * K1 + imin] / nrm;
-    collok[j] = ok;
+    for (int r = 0; r < KP; ++r) out[r] = (r < k) ? dir[r] : 0.0;
+    for (int r = 0; r < KP; ++r) out[KP + r] = (r < nr) ? dir[k + r] : 0.0;
+    out[2 * KP] = (double)r0;
+    out[2 * KP + 1] = (double)nr;
+    out[2 * KP + 2] = dl;
+    out[2 * KP + 3] = v;
+    collok[j] = ok ? 1 : 2;
   }
+}
+
+// mark[j]: bit 0 collided (flag), bit 1 origin on a multiple pole, bit 2 the
+// root is so close to its pole that the formula's y loses the small
+// components (|delta| < 1e-6 |u_o|^2: S(lambda) has a term |u_o|^2/|delta|
+// above 1e6 times its O(1) part); which[j]: earlier collided roots on the
+// same pole value (adjacent in j).
+__global__ void bordered_mark_kernel(const double* __restrict__ d, const double* __restrict__ u,
+                                     int kp, int64_t N, const int64_t* __restrict__ origin,
+                                     const double* __restrict__ rdelta,
+                                     const int* __restrict__ flags, int64_t nr,
+                                     int* __restrict__ mark, int* __restrict__ which,
+                                     int* __restrict__ collok, int allow_multi) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nr) return;
+  const int64_t o = origin[j];
+  const double v = d[o];
+  const bool coll = (flags[j] & 1) != 0;
+  const bool multi = allow_multi && ((o > 0 && d[o - 1] == v) || (o + 1 < N && d[o + 1] == v));
+  double uo2 = 0.0;
+  for (int c = 0; c < kp; ++c) uo2 += u[o * kp + c] * u[o * kp + c];
+  const bool near = allow_multi && !coll && fabs(rdelta[j]) < 1e-6 * uo2;
+  mark[j] = (coll ? 1 : 0) | (multi ? 2 : 0) | (near ? 4 : 0);
+  collok[j] = 0;
+  int w = 0;
+  if (coll)
+    for (int64_t j2 = j - 1; j2 >= 0 && (flags[j2] & 1) && d[origin[j2]] == v; --j2) ++w;
+  which[j] = w;
 }
 
 // Per-column parameters of a tile (shared memory).
@@ -174,6 +301,7 @@ struct XtCol {
   int64_t t;     // rotation row
   double dob, del;
   double y[KP + 1];
+  const double* cd;  // mode 1: the root's bordered-system record (collision_kernel)
 };
 
 // Value of reduced coordinate r for column parameters cp (eigvec.cpp:133-153
@@ -188,9 +316,15 @@ __device__ __forceinline__ double red_value(const ReducedView& rp, int64_t r, co
   const double dr = rp.d[r];
   if (cp.mode == 0) return t * rcp64((dr - cp.dob) - cp.del);
   if (cp.mode == 2) return (r == cp.o) ? 1.0 : 0.0;
-  const double g = dr - cp.dob;
-  if (fabs(g) < gap) return (r == cp.o) ? cp.y[KP] : 0.0;
-  return -t / g;
+  // bordered system: xi on the rows of the pole, -(u_r . z)/((d_r - v) - delta)
+  const double* cd = cp.cd;
+  const int64_t r0 = (int64_t)cd[2 * KP], nr = (int64_t)cd[2 * KP + 1];
+  if (r >= r0 && r < r0 + nr) return cd[KP + (r - r0)];
+  double tz = 0.0;
+#pragma unroll
+  for (int c = 0; c < KP; ++c) tz = fma(ur[c], cd[c], tz);
+  (void)gap;
+  return -tz / ((dr - cd[2 * KP + 3]) - cd[2 * KP + 2]);
 }
 
 constexpr int kXtThreads = 256;
@@ -228,9 +362,9 @@ __global__ void __launch_bounds__(kXtThreads) xt_tile_kernel(
         cp.dob = rp.d[cp.o];
         cp.del = delta[j];
         const bool coll = (flags[j] & 1) != 0;
-        cp.mode = coll ? (collok[j] ? 1 : 2) : 0;
-        for (int q = 0; q <= KP; ++q)
-          cp.y[q] = coll ? colldir[j * (KP + 1) + q] : (q < KP ? yall[j * KP + q] : 0.0);
+        cp.mode = (collok[j] == 1) ? 1 : ((collok[j] == 2 && coll) ? 2 : 0);
+        cp.cd = colldir + j * kCollStride<KP>;
+        for (int q = 0; q <= KP; ++q) cp.y[q] = (q < KP) ? yall[j * KP + q] : 0.0;
       } else {
         const int64_t src = dec_src[pay];
         if (cp.kind == 1) {
@@ -335,7 +469,7 @@ struct Xt2Smem {
   double out[kXt2 * (kXt2 + 1)];
   double ss[16 * kXt2];
   double dr[kXt2], cdob[kXt2], cdel[kXt2];
-  int64_t row[kXt2], co[kXt2], ct[kXt2];
+  int64_t row[kXt2], co[kXt2], ct[kXt2], cj[kXt2];
   int ckind[kXt2], cmode[kXt2];
   int special;
 };
@@ -367,7 +501,7 @@ __global__ void __launch_bounds__(256, 2) xt_tile64_kernel(
   if (t < kXt2) {
     const int64_t c = cb + t;
     int kind = -1, mode = 0;
-    int64_t o = 0, tt = 0;
+    int64_t o = 0, tt = 0, cjj = -1;
     double dob = 0.0, del = 0.0;
     double* y = sm.yt + t * YS;
     for (int q = 0; q < YS; ++q) y[q] = 0.0;
@@ -380,9 +514,9 @@ __global__ void __launch_bounds__(256, 2) xt_tile64_kernel(
         dob = rp.d[o];
         del = delta[j];
         const bool coll = (flags[j] & 1) != 0;
-        mode = coll ? (collok[j] ? 1 : 2) : 0;
-        for (int q = 0; q <= KP; ++q)
-          y[q] = coll ? colldir[j * (KP + 1) + q] : (q < KP ? yall[j * KP + q] : 0.0);
+        mode = (collok[j] == 1) ? 1 : ((collok[j] == 2 && coll) ? 2 : 0);
+        cjj = j;
+        for (int q = 0; q <= KP; ++q) y[q] = (q < KP) ? yall[j * KP + q] : 0.0;
       } else {
         const int64_t src = dec_src[pay];
         if (kind == 1) {
@@ -397,6 +531,7 @@ __global__ void __launch_bounds__(256, 2) xt_tile64_kernel(
     }
     sm.ckind[t] = kind;
     sm.cmode[t] = mode;
+    sm.cj[t] = cjj;
     sm.co[t] = o;
     sm.ct[t] = tt;
     sm.cdob[t] = dob;
@@ -484,6 +619,7 @@ __global__ void __launch_bounds__(256, 2) xt_tile64_kernel(
           cp.t = sm.ct[q];
           cp.dob = sm.cdob[q];
           cp.del = sm.cdel[q];
+          cp.cd = colldir + (sm.cj[q] >= 0 ? sm.cj[q] : 0) * kCollStride<KP>;
           for (int c = 0; c <= KP; ++c) cp.y[c] = sm.yt[q * YS + c];
           double x = 0.0;
           if (i < n) {
@@ -588,9 +724,8 @@ __global__ void __launch_bounds__(256, KP >= 32 ? 1 : 2) xt_rows_kernel(
         dob = rp.d[o];
         del = delta[j];
         const bool coll = (flags[j] & 1) != 0;
-        mode = coll ? (collok[j] ? 1 : 2) : 0;
-        for (int q = 0; q <= KP; ++q)
-          y[q] = coll ? colldir[j * (KP + 1) + q] : (q < KP ? yall[j * KP + q] : 0.0);
+        mode = (collok[j] == 1) ? 1 : ((collok[j] == 2 && coll) ? 2 : 0);
+        for (int q = 0; q <= KP; ++q) y[q] = (q < KP) ? yall[j * KP + q] : 0.0;
       } else {
         const int64_t src = dec_src[pay];
         if (kind == 1) {
@@ -773,16 +908,18 @@ void launch_xt(const Plan& p, const RootRecords& roots, const Columns& cols, con
 
 template <int KP>
 void launch_collisions(const Plan& p, const RootRecords& roots, const int64_t* list, int64_t cnt,
-                       double* colldir, int* collok, DeviceScratch& ws, cudaStream_t st) {
+                       const int* mark, const int* which, double* colldir, int* collok,
+                       DeviceScratch& ws, cudaStream_t st) {
   using C = PassCfg<KP>;
   const int grid = (int)cdiv(cnt, 32);
-  double* scratch = ws.get_f64("coll_scratch", (size_t)grid * 32 * 3 * (KP + 1) * (KP + 1));
+  double* scratch = ws.get_f64("coll_scratch", (size_t)grid * 32 * 4 * (2 * KP) * (2 * KP));
   const size_t sm = sizeof(double) * C::SMEM_DOUBLES;
   EIGB_CUDA(cudaFuncSetAttribute(collision_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sm));
   collision_kernel<KP><<<grid, kPassThreads, sm, st>>>(p.view(), list, cnt, roots.origin,
-                                                       kPoleMergeRelGap * p.scale, colldir,
-                                                       collok, scratch);
+                                                       roots.delta, mark, which,
+                                                       kPoleMergeRelGap * p.scale, colldir, collok,
+                                                       scratch);
   EIGB_LAUNCH_CHECK();
 }
 
@@ -829,23 +966,34 @@ int64_t collision_vectors_dev(const Plan& p, const RootRecords& roots, double* c
                               int* collok, DeviceScratch& ws, cudaStream_t st) {
   const int64_t nr = p.nred;
   if (nr == 0) return 0;
-  std::vector<int> fl(nr);
-  EIGB_CUDA(cudaMemcpyAsync(fl.data(), roots.flags, 4 * nr, cudaMemcpyDeviceToHost, st));
+  int* mark = ws.get_i32("coll_mark", nr);
+  int* which = ws.get_i32("coll_which", nr);
+  static int allow_multi = -1;  // EIGMOD_B200_BORDERED_MULTI=0: collided roots only (diagnostics)
+  if (allow_multi < 0) {
+    const char* e = std::getenv("EIGMOD_B200_BORDERED_MULTI");
+    allow_multi = !(e && std::string(e) == "0");
+  }
+  bordered_mark_kernel<<<(unsigned)cdiv(nr, 256), 256, 0, st>>>(p.d, p.ur, p.kp, nr, roots.origin,
+                                                                roots.delta, roots.flags, nr, mark,
+                                                                which, collok, allow_multi);
+  EIGB_LAUNCH_CHECK();
+  std::vector<int> mh(nr);
+  EIGB_CUDA(cudaMemcpyAsync(mh.data(), mark, 4 * nr, cudaMemcpyDeviceToHost, st));
   EIGB_CUDA(cudaStreamSynchronize(st));
   std::vector<int64_t> list;
   for (int64_t j = 0; j < nr; ++j)
-    if (fl[j] & 1) list.push_back(j);
+    if (mh[j]) list.push_back(j);
   if (list.empty()) return 0;
   int64_t* dl = ws.get_i64("coll_list", list.size());
   EIGB_CUDA(cudaMemcpyAsync(dl, list.data(), 8 * list.size(), cudaMemcpyHostToDevice, st));
   const int64_t cnt = (int64_t)list.size();
   switch (p.kp) {
-    case 1: launch_collisions<1>(p, roots, dl, cnt, colldir, collok, ws, st); break;
-    case 2: launch_collisions<2>(p, roots, dl, cnt, colldir, collok, ws, st); break;
-    case 4: launch_collisions<4>(p, roots, dl, cnt, colldir, collok, ws, st); break;
-    case 8: launch_collisions<8>(p, roots, dl, cnt, colldir, collok, ws, st); break;
-    case 16: launch_collisions<16>(p, roots, dl, cnt, colldir, collok, ws, st); break;
-    case 32: launch_collisions<32>(p, roots, dl, cnt, colldir, collok, ws, st); break;
+    case 1: launch_collisions<1>(p, roots, dl, cnt, mark, which, colldir, collok, ws, st); break;
+    case 2: launch_collisions<2>(p, roots, dl, cnt, mark, which, colldir, collok, ws, st); break;
+    case 4: launch_collisions<4>(p, roots, dl, cnt, mark, which, colldir, collok, ws, st); break;
+    case 8: launch_collisions<8>(p, roots, dl, cnt, mark, which, colldir, collok, ws, st); break;
+    case 16: launch_collisions<16>(p, roots, dl, cnt, mark, which, colldir, collok, ws, st); break;
+    case 32: launch_collisions<32>(p, roots, dl, cnt, mark, which, colldir, collok, ws, st); break;
   }
   return cnt;
 }

@@ -421,12 +421,23 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
   // (the S evaluation near a pole resolves delta only to ~eps * |S| / g in
   // absolute terms: a stalled step below a few ulps of the root x itself is
   // that floor, and further steps only bounce)
+  // -- but only while the other poles are far: the vector's entries on a
+  // pole s are 1/((d_s - d_o) - delta), so a neighbour within 1e10 steps
+  // (clustered poles) needs delta to its own ulps
   const bool stalled = fabs(step) >= a.stall_ratio * fabs(s.step_prev[b]);
+  bool far = false;
+  if (stalled) {
+    const int64_t o = s.o[b];
+    double gn = INFINITY;
+    if (o > 0) gn = fmin(gn, fabs((d[o - 1] - s.dob[b]) - dl));
+    if (o + 1 < N) gn = fmin(gn, fabs((d[o + 1] - s.dob[b]) - dl));
+    far = fabs(step) <= 1e-10 * gn;
+  }
   const bool sdone =
       !s.fmode[b] && ((fabs(step) <= a.step_tol * DBL_EPSILON * fabs(dl)) ||
                       (stalled && (fabs(step) <= a.floor_rel * fabs(dl) ||
-                                   fabs(step) <= a.floor_ulps * DBL_EPSILON *
-                                                     fabs(s.dob[b] + dl))));
+                                   (far && fabs(step) <= a.floor_ulps * DBL_EPSILON *
+                                                             fabs(s.dob[b] + dl)))));
   if (sdone || w <= tol || zero || s.iters[b] > a.max_iters) {
     // two more inverse-iteration steps on the same factorization: the
     // eigenvector formula needs y to the accuracy of the root

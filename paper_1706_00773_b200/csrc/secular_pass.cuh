@@ -76,13 +76,14 @@ struct PassSlots {
   double* y;       // [32][KP]  direction for g_b
   int* active;     // [32]
   int* hit;        // [32]  set when some d_i - x_b == 0 (solver: pole hit)
+  const int64_t* excl_row = nullptr;  // [32] with excl_gap: exclude this row only (>= 0)
 };
 
 struct PassOpts {
   const double* alpha = nullptr;  // residues for f (nullptr: f not needed)
   bool want_sigma = false;        // accumulate g_b along y_b
   bool exclude_zero = false;      // diff == 0 drops the term (no hit flag)
-  double excl_gap = 0.0;          // > 0: drop poles with |diff| < excl_gap
+  double excl_gap = 0.0;          // > 0: drop poles with |d_i - dob| < excl_gap
 };
 
 template <int KP>
@@ -192,8 +193,10 @@ __device__ __forceinline__ void pass_body(const double* __restrict__ d, const do
     for (int i = warp; i < kPoleTile; i += kPassWarps) {
       const double diff = (td[i] - dob) - del;
       double D;
-      if (o.excl_gap > 0.0) {
-        D = (act && fabs(diff) >= o.excl_gap) ? rcp64(diff) : 0.0;
+      if (o.excl_gap > 0.0) {  // the bordered block: rows within excl_gap of dob, or one row
+        const int64_t xr = slots.excl_row ? slots.excl_row[lane] : -1;
+        const bool ex = (xr >= 0) ? (t * kPoleTile + i == xr) : (fabs(td[i] - dob) < o.excl_gap);
+        D = (act && !ex && diff == diff) ? rcp64(diff) : 0.0;
       } else if (diff == 0.0) {
         hit |= !o.exclude_zero;
         D = 0.0;

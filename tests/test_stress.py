@@ -10,7 +10,7 @@ import pytest
 
 from oracle import port
 
-pytestmark = pytest.mark.gpu
+
 
 
 def _orthogonal(rng, n):
@@ -55,7 +55,8 @@ def _case(seed):
     return q, lam, kmat, signs, kind
 
 
-@pytest.mark.parametrize("seed", list(range(60)))
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", list(range(200)))
 def test_random_update(seed):
     from paper_1706_00773_b200 import capi
 
@@ -77,6 +78,24 @@ def test_random_update(seed):
         assert np.abs(res.lam - lo).max() <= 1e-12 * nrm
 
 
+@pytest.mark.parametrize("seed", list(range(40)))
+def test_oracle_random_update(seed):
+    """The CPU oracle on the same degenerate families (pins the checker)."""
+    q, lam, kmat, signs, kind = _case(1000 + seed)
+    n = len(lam)
+    if n > 300:
+        pytest.skip("CPU suite budget")
+    lo, qo, _ = port.update(q, lam, kmat, signs)
+    a = (q * lam) @ q.T + (kmat * signs) @ kmat.T
+    a = 0.5 * (a + a.T)
+    ev = np.linalg.eigvalsh(a)
+    nrm = max(float(np.abs(ev).max()), np.finfo(float).tiny)
+    assert np.abs(lo - ev).max() <= 1e-10 * nrm, kind
+    assert np.abs(a @ qo - qo * lo).max() / nrm <= 1e-10, kind
+    assert np.abs(qo.T @ qo - np.eye(n)).max() <= 1e-9, kind
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("seed", list(range(12)))
 def test_random_locate_matches_lapack(seed):
     from paper_1706_00773_b200 import capi

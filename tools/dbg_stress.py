@@ -9,7 +9,13 @@ for seed in seeds:
     q, lam, kmat, signs, kind = _case(1000 + seed)
     n = len(lam)
     try:
-        res = capi.update_decomposition(q, lam, kmat, signs, 1e-12)
+        ctx = capi.default_context()
+        import os
+        for kv in os.environ.get("EIGMOD_OPTS", "").split(","):
+            if kv:
+                kk, vv = kv.split("=")
+                ctx.set_option(kk, float(vv))
+        res = capi.update_decomposition(q, lam, kmat, signs, 1e-12, ctx=ctx)
     except Exception as e:
         print(seed, kind, n, kmat.shape[1], 'EXC', type(e).__name__, getattr(e, 'stage', ''), str(e)[:200])
         continue
