@@ -70,11 +70,16 @@ int64_t eigmod_b200_launch_count(void);
 /* Live FP64 ceilings of the context's device in TFLOP/s: out2[0] DMMA.8x8x4
  * tensor-pipe loop, out2[1] DFMA loop (roofline denominators). */
 int eigmod_b200_fp64_peaks(eigmod_b200_ctx* ctx, double* out2);
-/* Solver occupancy of the last solve: out4[0] pole passes (iterations of all
+/* Solver occupancy of the last solve: out8[0] pole passes (iterations of all
  * slot batches), [1] active slot-passes (sum over passes of slots holding an
- * unfinished root), [2] slot batches (CTAs or clusters), [3] 0.
+ * unfinished root), [2] slot batches (CTAs or clusters); SM cycles summed
+ * over the batches spent in [3] slot refills, [4] pole passes, [5] cluster
+ * reductions, [6] per-slot steps (factorization, Newton logic); [7] 0.
  * [1] / (32 * [0]) is the fraction of slot work that was not idle. */
-int eigmod_b200_solver_profile(eigmod_b200_ctx* ctx, double* out4);
+int eigmod_b200_solver_profile(eigmod_b200_ctx* ctx, double* out8);
+/* Scalar f presolve of the last solve: out4[0] roots converged, [1] roots
+ * handed to the S solver unconverged, [2] f evaluations, [3] max per root. */
+int eigmod_b200_presolve_profile(eigmod_b200_ctx* ctx, double* out4);
 /* Diagnostics: iterates of the root selected by set_option("trace_root", j)
  * in the last solve, 200 rows x 12 doubles (iteration, phase, fmode or count,
  * delta, lo, hi, f, f', sigma, g, step, origin); unused rows are zero. */

@@ -62,6 +62,7 @@ def _declare(lib):
         "eigmod_b200_workspace_bytes": (C.c_int64, [_VP]),
         "eigmod_b200_solver_profile": (C.c_int, [_VP, _D]),
         "eigmod_b200_solver_trace": (C.c_int, [_VP, _D]),
+        "eigmod_b200_presolve_profile": (C.c_int, [_VP, _D]),
         "eigmod_b200_stage_times": (C.c_int, [_VP, _D, C.c_int]),
         "eigmod_b200_launch_count": (C.c_int64, []),
         "eigmod_b200_fp64_peaks": (C.c_int, [_VP, _D]),
@@ -209,10 +210,19 @@ class Context:
         return {"dmma_tflops": float(out[0]), "dfma_tflops": float(out[1])}
 
     def solver_profile(self) -> dict:
-        o = np.zeros(4)
+        o = np.zeros(8)
         self.check(self._l.eigmod_b200_solver_profile(self.h, o.ctypes.data_as(_D)))
+        cyc = max(1.0, o[3] + o[4] + o[5] + o[6])
         return {"passes": o[0], "active_slot_passes": o[1], "batches": o[2],
-                "slot_util": o[1] / max(1.0, 32.0 * o[0])}
+                "slot_util": o[1] / max(1.0, 32.0 * o[0]),
+                "cycles": {"refill": o[3], "pass": o[4], "reduce": o[5], "step": o[6]},
+                "share": {"refill": o[3] / cyc, "pass": o[4] / cyc, "reduce": o[5] / cyc,
+                          "step": o[6] / cyc}}
+
+    def presolve_profile(self) -> dict:
+        o = np.zeros(4)
+        self.check(self._l.eigmod_b200_presolve_profile(self.h, o.ctypes.data_as(_D)))
+        return {"converged": o[0], "unconverged": o[1], "evals": o[2], "max_evals": o[3]}
 
     def solver_trace(self) -> np.ndarray:
         o = np.zeros((200, 12))

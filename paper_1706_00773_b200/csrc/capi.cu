@@ -515,6 +515,10 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
       ctx->sopt.sweep = value != 0.0;
     } else if (std::string(key) == "fnewton") {
       ctx->sopt.fnewton = value != 0.0;
+    } else if (std::string(key) == "fpre") {
+      ctx->sopt.fpre = value != 0.0;
+    } else if (std::string(key) == "fpre_iters") {
+      ctx->sopt.fpre_iters = (int)value;
     } else if (std::string(key) == "cluster") {
       ctx->sopt.cluster = (int)value;
     } else if (std::string(key) == "timing") {
@@ -561,10 +565,20 @@ int eigmod_b200_stats(const eigmod_b200_ctx* cctx, double* s) {
   });
 }
 
-int eigmod_b200_solver_profile(eigmod_b200_ctx* ctx, double* out4) {
+int eigmod_b200_solver_profile(eigmod_b200_ctx* ctx, double* out8) {
+  return guarded(ctx, [&] {
+    unsigned long long h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    auto* p = reinterpret_cast<unsigned long long*>(ctx->ws.get_i64("solve_prof", 8));
+    EIGB_CUDA(cudaMemcpyAsync(h, p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    EIGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < 8; ++i) out8[i] = (double)h[i];
+  });
+}
+
+int eigmod_b200_presolve_profile(eigmod_b200_ctx* ctx, double* out4) {
   return guarded(ctx, [&] {
     unsigned long long h[4] = {0, 0, 0, 0};
-    auto* p = reinterpret_cast<unsigned long long*>(ctx->ws.get_i64("solve_prof", 4));
+    auto* p = reinterpret_cast<unsigned long long*>(ctx->ws.get_i64("fpre_prof", 4));
     EIGB_CUDA(cudaMemcpyAsync(h, p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
     EIGB_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int i = 0; i < 4; ++i) out4[i] = (double)h[i];

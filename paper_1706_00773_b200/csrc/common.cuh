@@ -106,5 +106,22 @@ __device__ __forceinline__ int64_t dev_n_leq(const double* d, int64_t n, double 
   return lo;
 }
 
+// The same within a known window: the count lies in [a, b] (every d[i < a]
+// is below x, every d[i >= b] above it), so only log2(b - a) probes.
+__device__ __forceinline__ int64_t dev_n_less_in(const double* d, int64_t a, int64_t b, double x) {
+  while (a < b) {
+    const int64_t m = (a + b) >> 1;
+    if (d[m] < x) a = m + 1; else b = m;
+  }
+  return a;
+}
+__device__ __forceinline__ int64_t dev_n_leq_in(const double* d, int64_t a, int64_t b, double x) {
+  while (a < b) {
+    const int64_t m = (a + b) >> 1;
+    if (d[m] <= x) a = m + 1; else b = m;
+  }
+  return a;
+}
+
 }  // namespace eigb
 #endif

@@ -55,16 +55,35 @@ __device__ __forceinline__ double sweep_point(const double* d, int64_t N, int64_
   return da - kSweepTheta * g;
 }
 
+// The compile-time factorization (bkl_*) for KP <= 16; KP = 32 (global
+// scratch) keeps the generic one.
 template <int KP>
-__device__ __forceinline__ void load_S(const double* rb, const int* sgn, int k, double* F, int es) {
+constexpr bool kBkl = (KP <= 16);
+
+template <int KP>
+__device__ __forceinline__ void load_S(const double* rb, const int* sgn, int k, double* F, int es,
+                                       bool full = false) {
   using C = PassCfg<KP>;
   for (int r = 0; r < KP; ++r)
     for (int c = r; c < KP; ++c) {
       double v = rb[C::pidx(r, c)];
       if (r == c) v += (r < k) ? (double)sgn[r] : 1.0;
-      F[(r * KP + c) * es] = v;
       F[(c * KP + r) * es] = v;
+      if (full || !kBkl<KP>) F[(r * KP + c) * es] = v;  // bkl_* reads the lower triangle only
     }
+}
+
+template <int KP>
+__device__ __forceinline__ int slot_factor(double* F, int es, int* piv, int* zero) {
+  if constexpr (kBkl<KP>) return bkl_factor<KP>(F, es, piv, zero);
+  else return bk_factor(F, KP, KP, piv, zero, es);
+}
+
+template <int KP>
+__device__ __forceinline__ void slot_solve(const double* F, int es, const int* piv, double* z,
+                                           double tiny) {
+  if constexpr (kBkl<KP>) bkl_solve<KP>(F, es, piv, z, tiny);
+  else bk_solve(F, KP, KP, piv, z, tiny, es);
 }
 
 // ------------------------------------------------------------ sweep kernel
@@ -102,7 +121,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) count_sweep_kernel(ReducedVie
     double* Ft = kSmemF ? F + t : F + (size_t)t * KP * KP;
     load_S<KP>(rb, rp.sgn, rp.k, Ft, es);
     int piv[KP], zero;
-    const int neg = bk_factor(Ft, KP, KP, piv, &zero, es);
+    const int neg = slot_factor<KP>(Ft, es, piv, &zero);
     const double x = delta[t];
     // a hit (x on a pole, duplicates) gives an unusable point: -1
     counts[q0 + t] = hit[t] ? -1 : (int)(dev_n_less(rp.d, rp.n, x) + rp.m_neg - neg);
@@ -113,7 +132,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) count_sweep_kernel(ReducedVie
 struct SolveSmem {
   double dob[32], delta[32], lo[32], hi[32], step_prev[32];
   int64_t j[32], o[32], below[32];
+  int64_t pl[32], ph[32];  // pole window of the bracket: #{d <= lo}, #{d < hi}
   int active[32], hit[32], phase[32], lo_ok[32], hi_ok[32], iters[32], itersA[32], fmode[32];
+  int warm[32];  // next evaluation only refreshes y (start at the f presolve's root)
   unsigned long long jnext[32];  // root handed out by cluster rank 0
 };
 
@@ -124,6 +145,8 @@ struct SolveArgs {
   const double* br_lo;     // initial brackets of roots [j0, j1) (bracket_kernel); nullptr:
   const double* br_hi;     //   Weyl windows
   const int* br_ok;        // bit 0: lo certified (count == j), bit 1: hi (count == j + 1)
+  const int64_t* br_pl;    // #{d <= lo} and #{d < hi} of those brackets
+  const int64_t* br_ph;
   int64_t j0;
   int64_t j_end;
   unsigned long long* next_root;
@@ -138,6 +161,9 @@ struct SolveArgs {
   int geo_bisect;
   int64_t trace_j;           // diagnostics (-1: off)
   double* trace;             // [kTraceRows][kTraceCols]
+  const int64_t* f_o;        // f presolve per root [j0, j1) (nullptr: none): origin,
+  const double* f_delta;     //   delta of the f-root, state 0 none / 1 converged /
+  const int* f_state;        //   2 stopped early (continue f-Newton on S)
 };
 
 // Sweep bracket of root j: the last usable point with count <= j and the
@@ -167,7 +193,8 @@ __global__ void bracket_kernel(const double* __restrict__ d, int64_t N, const in
                                const int* __restrict__ pcounts, int64_t pbeg, int64_t pend,
                                int64_t j0, int64_t j1, int m_neg, int p_pos, double lo_clip,
                                double hi_clip, double* __restrict__ br_lo,
-                               double* __restrict__ br_hi, int* __restrict__ br_ok) {
+                               double* __restrict__ br_hi, int* __restrict__ br_ok,
+                               int64_t* __restrict__ br_pl, int64_t* __restrict__ br_ph) {
   const int64_t j = j0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= j1) return;
   const int64_t QB = 3 * pbeg, QE = 3 * pend;
@@ -208,6 +235,239 @@ __global__ void bracket_kernel(const double* __restrict__ d, int64_t N, const in
   br_lo[j - j0] = lo;
   br_hi[j - j0] = hi;
   br_ok[j - j0] = lok | (hok << 1);
+  br_pl[j - j0] = dev_n_leq(d, N, lo);
+  br_ph[j - j0] = dev_n_less(d, N, hi);
+}
+
+// ------------------------------------------------------------ f presolve
+// Scalar Newton on g(delta) = -delta f(d_o + delta), f(x) = 1 + sum_i alpha_i
+// / (d_i - x) with the K2 residues, for every isolated root, before the S
+// solver. One f evaluation costs ~8 flops per pole against ~KP^2/2 for an S
+// evaluation, so the f phase of K3 (about half its evaluations) moves here
+// and K3 starts psi-Newton next to the root. f(x) = det(I + J U^T (D - x)^-1
+// U) = prod(lambda'_i - x) / prod(d_i - x), so inside an isolated bracket f
+// changes sign only at the root and is (-1)^(j + #{d < x}) to its left: sign
+// bisection safeguards the Newton steps. The residues carry rounding, so the
+// result is only a starting point: K3 keeps the count-certified bracket.
+struct FPreArgs {
+  const double* d;
+  const double* alpha;
+  int64_t N;
+  const double* br_lo;
+  const double* br_hi;
+  const int* br_ok;
+  const int64_t* br_pl;
+  const int64_t* br_ph;
+  int64_t j0, j1;
+  int64_t* f_o;
+  double* f_delta;
+  int* f_state;
+  unsigned long long* next_root;
+  int max_iters;
+  unsigned long long* prof;  // [0] converged, [1] unconverged, [2] evaluations, [3] max
+};
+
+constexpr int kFPreWarps = 8;
+constexpr int kFPreTile = 1024;  // poles per shared-memory tile (d, alpha pairs)
+
+struct FPreSmem {
+  double dob[32], del[32], lo[32], hi[32], stepp[32];
+  int64_t j[32], o[32], below[32];
+  int act[32], it[32], hit[32];
+  double pf[kFPreWarps][32], pfp[kFPreWarps][32];
+};
+
+__device__ __forceinline__ void fpre_finish(FPreSmem& s, int b, const FPreArgs& a, int state,
+                                            double delta) {
+  const int64_t r = s.j[b] - a.j0;
+  a.f_o[r] = s.o[b];
+  a.f_delta[r] = delta;
+  a.f_state[r] = state;
+  s.act[b] = 2;
+  if (state) atomicAdd(a.prof + (state == 1 ? 0 : 1), 1ull);
+  atomicAdd(a.prof + 2, (unsigned long long)s.it[b]);
+  atomicMax(a.prof + 3, (unsigned long long)s.it[b]);
+}
+
+__device__ void fpre_step(FPreSmem& s, int b, const FPreArgs& a) {
+  const double* d = a.d;
+  const int64_t N = a.N;
+  const int it = ++s.it[b];
+  double f = 1.0, fp = 0.0;
+  for (int w = 0; w < kFPreWarps; ++w) f += s.pf[w][b], fp += s.pfp[w][b];
+  const double dl = s.del[b];
+  double lo = s.lo[b], hi = s.hi[b];
+  if (s.hit[b]) {  // on a pole (cannot happen inside an isolated bracket but at its ends)
+    s.hit[b] = 0;
+    double alt = nextafter(dl, hi);
+    if (!(alt < hi)) alt = nextafter(dl, lo);
+    if (!(alt > lo && alt < hi) || it > a.max_iters) fpre_finish(s, b, a, 0, dl);
+    else s.del[b] = alt;
+    return;
+  }
+  if (!isfinite(f) || !isfinite(fp)) { fpre_finish(s, b, a, 0, dl); return; }
+  if (f == 0.0) { fpre_finish(s, b, a, 1, dl); return; }
+  const bool pos_left = ((s.j[b] + s.below[b]) & 1) == 0;
+  if ((f > 0.0) == pos_left) lo = dl; else hi = dl;
+  const double den = f + dl * fp;
+  const double step = (den != 0.0) ? -dl * f / den : NAN;
+  const double dn0 = dl + step;
+  const bool inside = dn0 > lo && dn0 < hi;
+  // converged: a few ulps, or no longer shrinking at the rounding floor of f
+  if (inside && (fabs(step) <= 4.0 * DBL_EPSILON * fabs(dl) ||
+                 (fabs(step) >= 0.5 * fabs(s.stepp[b]) && fabs(step) <= 1e-11 * fabs(dl)))) {
+    fpre_finish(s, b, a, 1, dn0);
+    return;
+  }
+  if (hi - lo <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi))) {
+    fpre_finish(s, b, a, 1, 0.5 * (lo + hi));
+    return;
+  }
+  if (it >= a.max_iters) { fpre_finish(s, b, a, 2, dl); return; }
+  double dn = dn0;
+  if (!inside || !(fabs(step) < fabs(s.stepp[b]))) {
+    const double alo = fabs(lo), ahi = fabs(hi);
+    if (lo * hi > 0.0 && fmax(alo, ahi) > 8.0 * fmin(alo, ahi)) dn = copysign(sqrt(alo * ahi), lo);
+    else dn = 0.5 * (lo + hi);
+    s.stepp[b] = hi - lo;
+  } else {
+    s.stepp[b] = step;
+  }
+  // re-origin at the pole nearest the new iterate (as K3)
+  const int64_t pa = s.below[b] - 1, pb = s.below[b];
+  if (pa >= 0 && pb < N) {
+    const double xn = s.dob[b] + dn;
+    const int64_t want = (xn - d[pa] <= d[pb] - xn) ? pa : pb;
+    if (want != s.o[b]) {
+      const double sh = s.dob[b] - d[want];
+      s.o[b] = want;
+      s.dob[b] = d[want];
+      lo += sh;
+      hi += sh;
+      dn += sh;
+      if (!(dn > lo && dn < hi)) dn = 0.5 * (lo + hi);
+    }
+  }
+  s.lo[b] = lo;
+  s.hi[b] = hi;
+  s.del[b] = dn;
+}
+
+__global__ void __launch_bounds__(kFPreWarps * 32) fpresolve_kernel(FPreArgs a) {
+  constexpr int NT = kFPreWarps * 32;
+  constexpr int PER = kFPreTile / NT;  // tile entries loaded per thread
+  __shared__ FPreSmem s;
+  __shared__ double2 tile[kFPreTile];
+  __shared__ int any;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const double* __restrict__ d = a.d;
+  const double* __restrict__ al = a.alpha;
+  const int64_t N = a.N;
+  const int64_t ntiles = (N + kFPreTile - 1) / kFPreTile;
+  if (t < 32) s.act[t] = 2;
+  __syncthreads();
+  for (;;) {
+    if (t < 32 && s.act[t] == 2) {
+      s.act[t] = 0;
+      for (;;) {
+        const unsigned long long nj = atomicAdd(a.next_root, 1ull);
+        if ((int64_t)nj >= a.j1) break;
+        const int64_t j = (int64_t)nj, r = j - a.j0;
+        a.f_state[r] = 0;
+        if (a.br_ok[r] != 3) continue;
+        const double lo = a.br_lo[r], hi = a.br_hi[r];
+        const int64_t below = a.br_pl[r];
+        if (a.br_ph[r] != below) continue;  // not isolated: phase A in K3
+        const double mid = 0.5 * (lo + hi);
+        const int64_t pa = below - 1, pb = below;
+        const int64_t o = (pa < 0) ? pb : (pb >= N ? pa : ((mid - d[pa] <= d[pb] - mid) ? pa : pb));
+        const double dob = d[o];
+        s.j[t] = j;
+        s.o[t] = o;
+        s.below[t] = below;
+        s.dob[t] = dob;
+        s.lo[t] = lo - dob;
+        s.hi[t] = hi - dob;
+        s.del[t] = mid - dob;
+        s.stepp[t] = s.hi[t] - s.lo[t];
+        s.it[t] = 0;
+        s.hit[t] = 0;
+        s.act[t] = 1;
+        break;
+      }
+    }
+    __syncthreads();
+    if (t == 0) {
+      int v = 0;
+      for (int b = 0; b < 32; ++b) v |= s.act[b];
+      any = v;
+    }
+    __syncthreads();
+    if (!any) break;
+    // one f evaluation of the 32 slots: tiles of (d, alpha) in shared memory,
+    // poles of a tile split over the warps, slots over the lanes
+    const bool act = s.act[lane] == 1;
+    const double dob = s.dob[lane], del = s.del[lane];
+    double f = 0.0, fp = 0.0;
+    int hit = 0;
+    double2 nxt[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+      const int64_t i = e * NT + t;
+      nxt[e] = (i < N) ? make_double2(__ldg(d + i), __ldg(al + i)) : make_double2(NAN, 0.0);
+    }
+    for (int64_t tt = 0; tt < ntiles; ++tt) {
+#pragma unroll
+      for (int e = 0; e < PER; ++e) tile[e * NT + t] = nxt[e];
+      __syncthreads();
+      if (tt + 1 < ntiles) {
+        const int64_t base = (tt + 1) * kFPreTile;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+          const int64_t i = base + e * NT + t;
+          nxt[e] = (i < N) ? make_double2(__ldg(d + i), __ldg(al + i)) : make_double2(NAN, 0.0);
+        }
+      }
+      if (act) {
+#pragma unroll 4
+        for (int i = warp; i < kFPreTile; i += kFPreWarps) {
+          const double2 p = tile[i];
+          const double diff = (p.x - dob) - del;
+          hit |= (diff == 0.0);
+          const double D = (diff == 0.0 || diff != diff) ? 0.0 : rcp64(diff);
+          const double aD = p.y * D;
+          f += aD;
+          fp = fma(aD, D, fp);
+        }
+      }
+      __syncthreads();
+    }
+    if (hit) s.hit[lane] = 1;
+    s.pf[warp][lane] = f;
+    s.pfp[warp][lane] = fp;
+    __syncthreads();
+    if (t < 32 && s.act[t] == 1) fpre_step(s, t, a);
+    __syncthreads();
+  }
+}
+
+template <int KP>
+__device__ void enter_phase_b_at(SolveSmem& s, int b, const SolveArgs<KP>& a, int64_t o,
+                                 double delta, int fmode) {
+  const double* d = a.rp.d;
+  const double lo = s.lo[b], hi = s.hi[b];
+  const double dob = d[o];
+  s.o[b] = o;
+  s.below[b] = s.pl[b];
+  s.dob[b] = dob;
+  s.lo[b] = lo - dob;
+  s.hi[b] = hi - dob;
+  s.phase[b] = 1;
+  s.itersA[b] = s.iters[b];
+  s.fmode[b] = fmode && (a.alpha != nullptr);
+  s.warm[b] = !s.fmode[b];
+  s.step_prev[b] = s.hi[b] - s.lo[b];
+  s.delta[b] = (delta > s.lo[b] && delta < s.hi[b]) ? delta : 0.5 * (s.lo[b] + s.hi[b]);
 }
 
 template <int KP>
@@ -215,7 +475,7 @@ __device__ void enter_phase_b(SolveSmem& s, int b, const SolveArgs<KP>& a, doubl
   const double* d = a.rp.d;
   const int64_t N = a.rp.n;
   const double lo = s.lo[b], hi = s.hi[b];
-  const int64_t pa = dev_n_leq(d, N, lo) - 1, pb = pa + 1;
+  const int64_t pa = s.pl[b] - 1, pb = pa + 1;
   int64_t o;
   if (pa < 0) o = pb;
   else if (pb >= N) o = pa;
@@ -229,6 +489,7 @@ __device__ void enter_phase_b(SolveSmem& s, int b, const SolveArgs<KP>& a, doubl
   s.phase[b] = 1;
   s.itersA[b] = s.iters[b];
   s.fmode[b] = (a.alpha != nullptr);
+  s.warm[b] = 0;
   s.step_prev[b] = s.hi[b] - s.lo[b];
   s.delta[b] = xstart - dob;
 }
@@ -242,6 +503,7 @@ __device__ void slot_init(SolveSmem& s, double* y, int b, int64_t j, const Solve
   s.itersA[b] = 0;
   s.hit[b] = 0;
   s.phase[b] = 0;
+  s.warm[b] = 0;
   s.active[b] = 1;
   s.dob[b] = 0.0;
   const double y0 = rsqrt((double)a.rp.k);
@@ -253,17 +515,23 @@ __device__ void slot_init(SolveSmem& s, double* y, int b, int64_t j, const Solve
     hi = a.br_hi[j - a.j0];
     lok = a.br_ok[j - a.j0] & 1;
     hok = (a.br_ok[j - a.j0] >> 1) & 1;
+    s.pl[b] = a.br_pl[j - a.j0];
+    s.ph[b] = a.br_ph[j - a.j0];
   } else {  // Weyl window (proj/src/locate.cpp:159-171)
     lo = (j - a.m_neg >= 0) ? d[j - a.m_neg] : a.lo_clip;
     hi = (j + a.p_pos <= N - 1) ? d[j + a.p_pos] : a.hi_clip;
     lok = hok = 0;
+    s.pl[b] = dev_n_leq(d, N, lo);
+    s.ph[b] = dev_n_less(d, N, hi);
   }
   s.lo[b] = lo;
   s.hi[b] = hi;
   s.lo_ok[b] = lok;
   s.hi_ok[b] = hok;
-  if (lok && hok && dev_n_less(d, N, hi) == dev_n_leq(d, N, lo)) {
-    enter_phase_b<KP>(s, b, a, 0.5 * (lo + hi));
+  if (lok && hok && s.ph[b] == s.pl[b]) {
+    const int fs = a.f_state ? a.f_state[j - a.j0] : 0;
+    if (fs != 0) enter_phase_b_at<KP>(s, b, a, a.f_o[j - a.j0], a.f_delta[j - a.j0], fs == 2);
+    else enter_phase_b<KP>(s, b, a, 0.5 * (lo + hi));
   } else {
     s.delta[b] = 0.5 * (lo + hi);
   }
@@ -309,7 +577,7 @@ __device__ void slot_finish_unisolated(SolveSmem& s, double* y, int b, const Sol
 }
 
 template <int KP>
-__device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, double* F, int es,
+__device__ __noinline__ void slot_step(SolveSmem& s, double* y, int b, const double* red, double* F, int es,
                           const SolveArgs<KP>& a) {
   using C = PassCfg<KP>;
   const double* d = a.rp.d;
@@ -338,7 +606,7 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
   const double gp = rb[C::IG];
   const double fv = 1.0 + rb[C::IF], fpv = rb[C::IFP];
   int piv[KP], zero = 0;
-  const int neg = bk_factor(F, KP, KP, piv, &zero, es);
+  const int neg = slot_factor<KP>(F, es, piv, &zero);
   double pscale = 0.0;
   for (int c = 0; c < KP; ++c) pscale = fmax(pscale, fabs(F[(c * KP + c) * es]));
   // an exactly zero pivot (x is a root to working precision) is replaced by a
@@ -347,12 +615,18 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
   const double tiny = 1e-4 * DBL_EPSILON * fmax(pscale, 1e-300);
   double yv[KP], z[KP];
   for (int c = 0; c < KP; ++c) yv[c] = y[b * KP + c];
-  for (int c = 0; c < KP; ++c) z[c] = yv[c];
-  bk_solve(F, KP, KP, piv, z, tiny, es);
-  double zz = 0.0, zy = 0.0;
-  for (int c = 0; c < KP; ++c) zz += z[c] * z[c], zy += z[c] * yv[c];
+  // a slot started at the f presolve's root has no y from earlier
+  // evaluations: its first evaluation takes three inverse-iteration steps on
+  // this factorization and makes no Newton step (the pass computed sigma'
+  // with the unconverged y), the second repeats the point with the new y
+  const int ninv = s.warm[b] ? 3 : 1;
   double sigma = 0.0;
-  if (zz > 0.0 && isfinite(zz)) {
+  for (int it = 0; it < ninv; ++it) {
+    for (int c = 0; c < KP; ++c) z[c] = yv[c];
+    slot_solve<KP>(F, es, piv, z, tiny);
+    double zz = 0.0, zy = 0.0;
+    for (int c = 0; c < KP; ++c) zz += z[c] * z[c], zy += z[c] * yv[c];
+    if (!(zz > 0.0 && isfinite(zz))) break;
     sigma = zy / zz;  // Rayleigh quotient of S at z
     const double inv = rsqrt(zz);
     for (int c = 0; c < KP; ++c) yv[c] = z[c] * inv;
@@ -362,17 +636,27 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
 
   if (s.phase[b] == 0) {
     const double x = s.delta[b];
-    const int64_t cnt = dev_n_less(d, N, x) + a.m_neg - neg;
+    // x strictly inside (lo, hi): the count lies in the bracket's pole window
+    const bool inside = x > s.lo[b] && x < s.hi[b] && s.pl[b] <= s.ph[b];
+    const int64_t nl = inside ? dev_n_less_in(d, s.pl[b], s.ph[b], x) : dev_n_less(d, N, x);
+    const int64_t cnt = nl + a.m_neg - neg;
     if (j == a.trace_j && a.writer && s.iters[b] <= kTraceRows) {
       double* tr = a.trace + (s.iters[b] - 1) * kTraceCols;
       const double v[kTraceCols] = {(double)s.iters[b], 0.0, (double)cnt, x, s.lo[b], s.hi[b],
                                     fv, fpv, sigma, gp, 0.0, -1.0};
       for (int c = 0; c < kTraceCols; ++c) tr[c] = v[c];
     }
-    if (cnt >= j + 1) { s.hi[b] = x; s.hi_ok[b] = (cnt == j + 1); }
-    else { s.lo[b] = x; s.lo_ok[b] = (cnt == j); }
+    if (cnt >= j + 1) {
+      s.hi[b] = x;
+      s.hi_ok[b] = (cnt == j + 1);
+      s.ph[b] = nl;  // #{d < x}
+    } else {
+      s.lo[b] = x;
+      s.lo_ok[b] = (cnt == j);
+      s.pl[b] = inside ? dev_n_leq_in(d, nl, s.ph[b], x) : dev_n_leq(d, N, x);
+    }
     const double lo = s.lo[b], hi = s.hi[b];
-    if (s.lo_ok[b] && s.hi_ok[b] && dev_n_less(d, N, hi) == dev_n_leq(d, N, lo)) {
+    if (s.lo_ok[b] && s.hi_ok[b] && s.ph[b] == s.pl[b]) {
       enter_phase_b<KP>(s, b, a, 0.5 * (lo + hi));
       return;
     }
@@ -389,6 +673,11 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
   const int64_t cnt = s.below[b] + a.m_neg - neg;
   if (cnt >= j + 1) s.hi[b] = dl; else s.lo[b] = dl;
   const double lo = s.lo[b], hi = s.hi[b];
+  if (s.warm[b]) {
+    s.warm[b] = 0;
+    s.step_prev[b] = hi - lo;
+    return;  // same point again (it is now a bracket end)
+  }
   double step = NAN;
   if (s.fmode[b]) {  // Newton on g = -delta f: g' = -f - delta f'
     const double den = fv + dl * fpv;
@@ -443,7 +732,7 @@ __device__ void slot_step(SolveSmem& s, double* y, int b, const double* red, dou
     // eigenvector formula needs y to the accuracy of the root
     for (int it = 0; it < 2; ++it) {
       for (int c = 0; c < KP; ++c) z[c] = yv[c];
-      bk_solve(F, KP, KP, piv, z, tiny, es);
+      slot_solve<KP>(F, es, piv, z, tiny);
       double z2 = 0.0;
       for (int c = 0; c < KP; ++c) z2 += z[c] * z[c];
       if (!(z2 > 0.0 && isfinite(z2))) break;
@@ -531,7 +820,9 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 4 ? 2 : 1) solve_roots_ker
   o.alpha = a.alpha ? a.alpha + plo : nullptr;
   o.want_sigma = true;
   unsigned long long npass = 0, nact = 0;
+  long long c_refill = 0, c_pass = 0, c_red = 0, c_step = 0;  // SM cycles (thread 0)
   for (;;) {
+    const long long t0 = clock64();
     // ---- refill finished slots from the root queue
     if constexpr (CL == 1) {
       if (t < 32 && s.active[t] == 2) {
@@ -564,10 +855,12 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 4 ? 2 : 1) solve_roots_ker
     }
     __syncthreads();
     if (!any) break;
+    const long long t1 = clock64();
     // ---- pole pass over this CTA's slice
     PassSlots sl{s.dob, s.delta, y, s.active, s.hit};
     secular_pass<KP>(a.rp.d + plo, a.rp.u + plo * KP, pcnt, sl, o, smem);
     const double* red = pass_result<KP>(smem);
+    const long long t2 = clock64();
     if constexpr (CL > 1) {
       cg::cluster_group cl = cg::this_cluster();
       cl.sync();  // all partial sums of this iteration are in place
@@ -584,13 +877,23 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 4 ? 2 : 1) solve_roots_ker
       cl.sync();  // partials no longer read remotely
       red = fullred;
     }
+    const long long t3 = clock64();
     if (t < 32 && s.active[t] == 1) slot_step<KP>(s, y, t, red, F, es, a);
     __syncthreads();
+    const long long t4 = clock64();
+    c_refill += t1 - t0;
+    c_pass += t2 - t1;
+    c_red += t3 - t2;
+    c_step += t4 - t3;
   }
   if (t == 0 && rank == 0 && a.prof) {
     atomicAdd(a.prof, npass);
     atomicAdd(a.prof + 1, nact);
     atomicAdd(a.prof + 2, 1ull);
+    atomicAdd(a.prof + 3, (unsigned long long)c_refill);
+    atomicAdd(a.prof + 4, (unsigned long long)c_pass);
+    atomicAdd(a.prof + 5, (unsigned long long)c_red);
+    atomicAdd(a.prof + 6, (unsigned long long)c_step);
   }
 }
 
@@ -717,15 +1020,22 @@ bool launch_solve_cluster(const SolveArgs<KP>& a, int64_t nroots, int sms, cudaS
 
 template <int KP>
 void launch_solve(const ReducedView& rp, const double* alpha, const double* br_lo,
-                  const double* br_hi, const int* br_ok, int64_t j0, int64_t j1,
+                  const double* br_hi, const int* br_ok, const int64_t* br_pl,
+                  const int64_t* br_ph, const int64_t* f_o,
+                  const double* f_delta, const int* f_state, int64_t j0, int64_t j1,
                   const RootRecords& out, const SolveOptions& opt, DeviceScratch& ws, int sms,
                   cudaStream_t st) {
   SolveArgs<KP> a;
+  a.f_o = f_o;
+  a.f_delta = f_delta;
+  a.f_state = f_state;
   a.rp = rp;
   a.alpha = alpha;
   a.br_lo = br_lo;
   a.br_hi = br_hi;
   a.br_ok = br_ok;
+  a.br_pl = br_pl;
+  a.br_ph = br_ph;
   a.j0 = j0;
   a.j_end = j1;
   a.out = out;
@@ -738,7 +1048,7 @@ void launch_solve(const ReducedView& rp, const double* alpha, const double* br_l
   a.writer = 1;
   const int64_t nroots = j1 - j0;
   a.next_root = reinterpret_cast<unsigned long long*>(ws.get_i64("solve_counter", 1));
-  a.prof = reinterpret_cast<unsigned long long*>(ws.get_i64("solve_prof", 4));
+  a.prof = reinterpret_cast<unsigned long long*>(ws.get_i64("solve_prof", 8));
   a.trace_j = opt.trace_root;
   a.fexit_rel = opt.fexit_rel;
   a.floor_rel = opt.floor_rel;
@@ -748,7 +1058,7 @@ void launch_solve(const ReducedView& rp, const double* alpha, const double* br_l
   a.trace = ws.get_f64("solve_trace", (size_t)kTraceRows * kTraceCols);
   if (opt.trace_root >= 0)
     EIGB_CUDA(cudaMemsetAsync(a.trace, 0, sizeof(double) * kTraceRows * kTraceCols, st));
-  EIGB_CUDA(cudaMemsetAsync(a.prof, 0, 4 * sizeof(unsigned long long), st));
+  EIGB_CUDA(cudaMemsetAsync(a.prof, 0, 8 * sizeof(unsigned long long), st));
   const unsigned long long start = (unsigned long long)j0;
   EIGB_CUDA(cudaMemcpyAsync(a.next_root, &start, sizeof(start), cudaMemcpyHostToDevice, st));
   // Size-based choice (tools/exp_cluster.py, cfg 2/4 at n = 8192/32768):
@@ -837,7 +1147,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pole_inertia_kernel(InertiaAr
   double* W = T + KP * KP;   // reflectors, one per row of R
   double* x = W + KP * KP;
   const double* rb = pass_result<KP>(smem) + t * C::OUT;
-  load_S<KP>(rb, a.rp.sgn, k, T, 1);
+  load_S<KP>(rb, a.rp.sgn, k, T, 1, true);
   // Householder vectors of span(R): reflector q acts on coordinates q..k-1
   int q = 0;
   const int64_t r0 = a.brow[g];
@@ -987,19 +1297,45 @@ void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t
   }
   double *br_lo = nullptr, *br_hi = nullptr;
   int* br_ok = nullptr;
+  int64_t *br_pl = nullptr, *br_ph = nullptr;
   if (opt.sweep) {
     const int64_t nr = j1 - j0;
     br_lo = ws.get_f64("br_lo", nr);
     br_hi = ws.get_f64("br_hi", nr);
     br_ok = ws.get_i32("br_ok", nr);
+    br_pl = ws.get_i64("br_pl", nr);
+    br_ph = ws.get_i64("br_ph", nr);
     bracket_kernel<<<(unsigned)cdiv(nr, 256), 256, 0, st>>>(
         rp.d, rp.n, counts, pcounts, pb, pe, j0, j1, rp.m_neg, rp.k - rp.m_neg, rp.lo_clip,
-        rp.hi_clip, br_lo, br_hi, br_ok);
+        rp.hi_clip, br_lo, br_hi, br_ok, br_pl, br_ph);
     EIGB_LAUNCH_CHECK();
   }
   if (!opt.fnewton) alpha = nullptr;
-#define EIGB_SOLVE(K) \
-  launch_solve<K>(rp, alpha, br_lo, br_hi, br_ok, j0, j1, out, opt, ws, sms, st)
+  int64_t* f_o = nullptr;
+  double* f_delta = nullptr;
+  int* f_state = nullptr;
+  if (alpha && br_lo && opt.fpre) {
+    const int64_t nr = j1 - j0;
+    f_o = ws.get_i64("fpre_o", nr);
+    f_delta = ws.get_f64("fpre_delta", nr);
+    f_state = ws.get_i32("fpre_state", nr);
+    FPreArgs fa{rp.d, alpha, rp.n, br_lo, br_hi, br_ok, br_pl, br_ph, j0, j1, f_o, f_delta, f_state,
+                reinterpret_cast<unsigned long long*>(ws.get_i64("fpre_counter", 1)),
+                opt.fpre_iters,
+                reinterpret_cast<unsigned long long*>(ws.get_i64("fpre_prof", 4))};
+    EIGB_CUDA(cudaMemsetAsync(fa.prof, 0, 4 * sizeof(unsigned long long), st));
+    const unsigned long long start = (unsigned long long)j0;
+    EIGB_CUDA(cudaMemcpyAsync(fa.next_root, &start, sizeof(start), cudaMemcpyHostToDevice, st));
+    int per_sm = 0;
+    EIGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fpresolve_kernel,
+                                                            kFPreWarps * 32, 0));
+    const int64_t grid = std::min<int64_t>((int64_t)std::max(1, per_sm) * sms, cdiv(nr, 32));
+    fpresolve_kernel<<<(unsigned)grid, kFPreWarps * 32, 0, st>>>(fa);
+    EIGB_LAUNCH_CHECK();
+  }
+#define EIGB_SOLVE(K)                                                                          \
+  launch_solve<K>(rp, alpha, br_lo, br_hi, br_ok, br_pl, br_ph, f_o, f_delta, f_state, j0, j1, \
+                  out, opt, ws, sms, st)
   switch (rp.kp) {
     case 1: EIGB_SOLVE(1); break;
     case 2: EIGB_SOLVE(2); break;

@@ -91,6 +91,10 @@ struct SolveOptions {
   double floor_ulps = 4.0;   // ... or below this many ulps of the root value
   double stall_ratio = 0.5;  // "no longer shrinking": |step| >= stall_ratio * |previous step|
   int geo_bisect = 1;       // geometric bisection of brackets spanning decades of delta
+  // scalar presolve: Newton on f alone (K2 residues) for every isolated root
+  // before the S solver, which then starts psi-Newton at the f-root
+  bool fpre = false;
+  int fpre_iters = 60;
 };
 
 // Diagnostics trace of one root: per evaluation kTraceCols doubles

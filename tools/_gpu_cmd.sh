@@ -1,0 +1,2 @@
+python tools/exp_solver_share.py > gpurun_out/share.log 2>&1
+python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; tail -3 gpurun_out/gpu_tests.log
