@@ -70,13 +70,14 @@ int64_t eigmod_b200_launch_count(void);
 /* Live FP64 ceilings of the context's device in TFLOP/s: out2[0] DMMA.8x8x4
  * tensor-pipe loop, out2[1] DFMA loop (roofline denominators). */
 int eigmod_b200_fp64_peaks(eigmod_b200_ctx* ctx, double* out2);
-/* Solver occupancy of the last solve: out8[0] pole passes (iterations of all
+/* Solver occupancy of the last solve: out10[0] pole passes (iterations of all
  * slot batches), [1] active slot-passes (sum over passes of slots holding an
  * unfinished root), [2] slot batches (CTAs or clusters); SM cycles summed
  * over the batches spent in [3] slot refills, [4] pole passes, [5] cluster
- * reductions, [6] per-slot steps (factorization, Newton logic); [7] 0.
+ * reductions, [6] per-slot steps, of which [7] loading S, [8] its
+ * Bunch-Kaufman factorization, [9] the inverse-iteration solves.
  * [1] / (32 * [0]) is the fraction of slot work that was not idle. */
-int eigmod_b200_solver_profile(eigmod_b200_ctx* ctx, double* out8);
+int eigmod_b200_solver_profile(eigmod_b200_ctx* ctx, double* out10);
 /* Scalar f presolve of the last solve: out4[0] roots converged, [1] roots
  * handed to the S solver unconverged, [2] f evaluations, [3] max per root. */
 int eigmod_b200_presolve_profile(eigmod_b200_ctx* ctx, double* out4);

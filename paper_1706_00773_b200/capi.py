@@ -154,6 +154,11 @@ class Context:
                               "no usable sm_100 GPU")
         self.h = h
         self.device = device
+        # diagnostics: solver options for every new context, "key=value,..."
+        for kv in os.environ.get("EIGMOD_B200_OPTS", "").split(","):
+            if kv.strip():
+                key, val = kv.split("=")
+                self.set_option(key.strip(), float(val))
 
     def close(self):
         if getattr(self, "h", None):
@@ -210,14 +215,15 @@ class Context:
         return {"dmma_tflops": float(out[0]), "dfma_tflops": float(out[1])}
 
     def solver_profile(self) -> dict:
-        o = np.zeros(8)
+        o = np.zeros(10)
         self.check(self._l.eigmod_b200_solver_profile(self.h, o.ctypes.data_as(_D)))
         cyc = max(1.0, o[3] + o[4] + o[5] + o[6])
         return {"passes": o[0], "active_slot_passes": o[1], "batches": o[2],
                 "slot_util": o[1] / max(1.0, 32.0 * o[0]),
                 "cycles": {"refill": o[3], "pass": o[4], "reduce": o[5], "step": o[6]},
                 "share": {"refill": o[3] / cyc, "pass": o[4] / cyc, "reduce": o[5] / cyc,
-                          "step": o[6] / cyc}}
+                          "step": o[6] / cyc, "step_load": o[7] / cyc, "step_factor": o[8] / cyc,
+                          "step_solve": o[9] / cyc}}
 
     def presolve_profile(self) -> dict:
         o = np.zeros(4)

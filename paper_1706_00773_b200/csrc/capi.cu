@@ -517,6 +517,8 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
       ctx->sopt.fnewton = value != 0.0;
     } else if (std::string(key) == "fpre") {
       ctx->sopt.fpre = value != 0.0;
+    } else if (std::string(key) == "fpre_min_kp") {
+      ctx->sopt.fpre_min_kp = (int)value;
     } else if (std::string(key) == "fpre_iters") {
       ctx->sopt.fpre_iters = (int)value;
     } else if (std::string(key) == "cluster") {
@@ -565,13 +567,13 @@ int eigmod_b200_stats(const eigmod_b200_ctx* cctx, double* s) {
   });
 }
 
-int eigmod_b200_solver_profile(eigmod_b200_ctx* ctx, double* out8) {
+int eigmod_b200_solver_profile(eigmod_b200_ctx* ctx, double* out10) {
   return guarded(ctx, [&] {
-    unsigned long long h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    auto* p = reinterpret_cast<unsigned long long*>(ctx->ws.get_i64("solve_prof", 8));
+    unsigned long long h[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    auto* p = reinterpret_cast<unsigned long long*>(ctx->ws.get_i64("solve_prof", 12));
     EIGB_CUDA(cudaMemcpyAsync(h, p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
     EIGB_CUDA(cudaStreamSynchronize(ctx->stream));
-    for (int i = 0; i < 8; ++i) out8[i] = (double)h[i];
+    for (int i = 0; i < 10; ++i) out10[i] = (double)h[i];
   });
 }
 

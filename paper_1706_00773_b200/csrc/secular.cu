@@ -55,77 +55,17 @@ __device__ __forceinline__ double sweep_point(const double* d, int64_t N, int64_
   return da - kSweepTheta * g;
 }
 
-// The compile-time factorization (bkl_*) for KP <= 16; KP = 32 (global
-// scratch) keeps the generic one.
+// S = J + (pass result) into a full KP x KP matrix (padded diagonal 1).
 template <int KP>
-constexpr bool kBkl = (KP <= 16);
-
-template <int KP>
-__device__ __forceinline__ void load_S(const double* rb, const int* sgn, int k, double* F, int es,
-                                       bool full = false) {
+__device__ __forceinline__ void load_S(const double* rb, const int* sgn, int k, double* F, int es) {
   using C = PassCfg<KP>;
   for (int r = 0; r < KP; ++r)
     for (int c = r; c < KP; ++c) {
       double v = rb[C::pidx(r, c)];
       if (r == c) v += (r < k) ? (double)sgn[r] : 1.0;
       F[(c * KP + r) * es] = v;
-      if (full || !kBkl<KP>) F[(r * KP + c) * es] = v;  // bkl_* reads the lower triangle only
+      F[(r * KP + c) * es] = v;
     }
-}
-
-template <int KP>
-__device__ __forceinline__ int slot_factor(double* F, int es, int* piv, int* zero) {
-  if constexpr (kBkl<KP>) return bkl_factor<KP>(F, es, piv, zero);
-  else return bk_factor(F, KP, KP, piv, zero, es);
-}
-
-template <int KP>
-__device__ __forceinline__ void slot_solve(const double* F, int es, const int* piv, double* z,
-                                           double tiny) {
-  if constexpr (kBkl<KP>) bkl_solve<KP>(F, es, piv, z, tiny);
-  else bk_solve(F, KP, KP, piv, z, tiny, es);
-}
-
-// ------------------------------------------------------------ sweep kernel
-template <int KP>
-__global__ void __launch_bounds__(kPassThreads, 1) count_sweep_kernel(ReducedView rp,
-                                                                      int* __restrict__ counts,
-                                                                      int64_t qbeg, int64_t qend,
-                                                                      double* __restrict__ gscratch) {
-  using C = PassCfg<KP>;
-  extern __shared__ __align__(16) double smem[];
-  // factor storage: interleaved [KP*KP][32] in shared memory for KP <= 16,
-  // per-slot rows in global scratch above (32 x 32 x 32 doubles do not fit)
-  constexpr bool kSmemF = KP <= 16;
-  double* F = kSmemF ? smem + C::SMEM_DOUBLES
-                     : gscratch + (size_t)blockIdx.x * 32 * KP * KP;
-  constexpr int es = kSmemF ? 32 : 1;
-  __shared__ double dob[32], delta[32];
-  __shared__ int active[32], hit[32];
-  const int t = threadIdx.x;
-  const int64_t Q = qend;
-  const int64_t q0 = qbeg + (int64_t)blockIdx.x * 32;
-  if (t < 32) {
-    const int64_t q = q0 + t;
-    active[t] = q < Q;
-    dob[t] = 0.0;
-    delta[t] = (q < Q) ? sweep_point(rp.d, rp.n, q) : 0.0;
-    hit[t] = 0;
-  }
-  __syncthreads();
-  PassSlots sl{dob, delta, nullptr, active, hit};
-  PassOpts o;
-  secular_pass<KP>(rp.d, rp.u, rp.n, sl, o, smem);
-  if (t < 32 && active[t]) {
-    const double* rb = pass_result<KP>(smem) + t * C::OUT;
-    double* Ft = kSmemF ? F + t : F + (size_t)t * KP * KP;
-    load_S<KP>(rb, rp.sgn, rp.k, Ft, es);
-    int piv[KP], zero;
-    const int neg = slot_factor<KP>(Ft, es, piv, &zero);
-    const double x = delta[t];
-    // a hit (x on a pole, duplicates) gives an unusable point: -1
-    counts[q0 + t] = hit[t] ? -1 : (int)(dev_n_less(rp.d, rp.n, x) + rp.m_neg - neg);
-  }
 }
 
 // ------------------------------------------------------------ solver
@@ -135,6 +75,9 @@ struct SolveSmem {
   int64_t pl[32], ph[32];  // pole window of the bracket: #{d <= lo}, #{d < hi}
   int active[32], hit[32], phase[32], lo_ok[32], hi_ok[32], iters[32], itersA[32], fmode[32];
   int warm[32];  // next evaluation only refreshes y (start at the f presolve's root)
+  // a converged slot: record fields, written after the final inverse iterations
+  int64_t fin_o[32];
+  double fin_delta[32], fin_value[32];
   unsigned long long jnext[32];  // root handed out by cluster rank 0
 };
 
@@ -274,7 +217,8 @@ struct FPreSmem {
   double dob[32], del[32], lo[32], hi[32], stepp[32];
   int64_t j[32], o[32], below[32];
   int act[32], it[32], hit[32];
-  double pf[kFPreWarps][32], pfp[kFPreWarps][32];
+  // f split at the bracket: psi over the poles left of it, phi right of it
+  double ps[kFPreWarps][32], psp[kFPreWarps][32], ph[kFPreWarps][32], php[kFPreWarps][32];
 };
 
 __device__ __forceinline__ void fpre_finish(FPreSmem& s, int b, const FPreArgs& a, int state,
@@ -293,8 +237,12 @@ __device__ void fpre_step(FPreSmem& s, int b, const FPreArgs& a) {
   const double* d = a.d;
   const int64_t N = a.N;
   const int it = ++s.it[b];
-  double f = 1.0, fp = 0.0;
-  for (int w = 0; w < kFPreWarps; ++w) f += s.pf[w][b], fp += s.pfp[w][b];
+  double psi = 0.0, psip = 0.0, phi = 0.0, phip = 0.0;
+  for (int w = 0; w < kFPreWarps; ++w) {
+    psi += s.ps[w][b], psip += s.psp[w][b];
+    phi += s.ph[w][b], phip += s.php[w][b];
+  }
+  const double f = 1.0 + psi + phi, fp = psip + phip;
   const double dl = s.del[b];
   double lo = s.lo[b], hi = s.hi[b];
   if (s.hit[b]) {  // on a pole (cannot happen inside an isolated bracket but at its ends)
@@ -310,7 +258,27 @@ __device__ void fpre_step(FPreSmem& s, int b, const FPreArgs& a) {
   const bool pos_left = ((s.j[b] + s.below[b]) & 1) == 0;
   if ((f > 0.0) == pos_left) lo = dl; else hi = dl;
   const double den = f + dl * fp;
-  const double step = (den != 0.0) ? -dl * f / den : NAN;
+  double step = (den != 0.0) ? -dl * f / den : NAN;
+  // the two-pole model of the bracket (psi ~ a1 + b1 / (d_A - x), phi ~ a2 +
+  // b2 / (d_B - x), value and slope matched at the iterate; the classical
+  // "middle way" of rank-one secular solvers): its root in the bracket
+  const int64_t pa = s.below[b] - 1, pb = s.below[b];
+  if (pa >= 0 && pb < N) {
+    const double dA = d[pa] - s.dob[b], dB = d[pb] - s.dob[b];
+    const double eA = dA - dl, eB = dB - dl;
+    const double b1 = psip * eA * eA, b2 = phip * eB * eB;
+    const double cc = 1.0 + (psi - b1 / eA) + (phi - b2 / eB);
+    // cc (dA - t)(dB - t) + b1 (dB - t) + b2 (dA - t) = 0
+    const double qa = cc, qb = -(cc * (dA + dB) + b1 + b2), qc = cc * dA * dB + b1 * dB + b2 * dA;
+    const double disc = qb * qb - 4.0 * qa * qc;
+    if (disc >= 0.0 && qa != 0.0) {
+      const double q = -0.5 * (qb + copysign(sqrt(disc), qb));
+      const double r1 = q / qa, r2 = (q != 0.0) ? qc / q : r1;
+      const bool in1 = r1 > lo && r1 < hi, in2 = r2 > lo && r2 < hi;
+      if (in1 != in2) step = (in1 ? r1 : r2) - dl;
+      else if (in1) step = ((fabs(r1 - dl) <= fabs(r2 - dl)) ? r1 : r2) - dl;
+    }
+  }
   const double dn0 = dl + step;
   const bool inside = dn0 > lo && dn0 < hi;
   // converged: a few ulps, or no longer shrinking at the rounding floor of f
@@ -334,7 +302,6 @@ __device__ void fpre_step(FPreSmem& s, int b, const FPreArgs& a) {
     s.stepp[b] = step;
   }
   // re-origin at the pole nearest the new iterate (as K3)
-  const int64_t pa = s.below[b] - 1, pb = s.below[b];
   if (pa >= 0 && pb < N) {
     const double xn = s.dob[b] + dn;
     const int64_t want = (xn - d[pa] <= d[pb] - xn) ? pa : pb;
@@ -408,7 +375,8 @@ __global__ void __launch_bounds__(kFPreWarps * 32) fpresolve_kernel(FPreArgs a) 
     // poles of a tile split over the warps, slots over the lanes
     const bool act = s.act[lane] == 1;
     const double dob = s.dob[lane], del = s.del[lane];
-    double f = 0.0, fp = 0.0;
+    const int64_t below = s.below[lane];
+    double ps = 0.0, psp = 0.0, ph = 0.0, php = 0.0;
     int hit = 0;
     double2 nxt[PER];
 #pragma unroll
@@ -436,15 +404,20 @@ __global__ void __launch_bounds__(kFPreWarps * 32) fpresolve_kernel(FPreArgs a) 
           hit |= (diff == 0.0);
           const double D = (diff == 0.0 || diff != diff) ? 0.0 : rcp64(diff);
           const double aD = p.y * D;
-          f += aD;
-          fp = fma(aD, D, fp);
+          const double aL = (tt * kFPreTile + i < below) ? aD : 0.0, aR = aD - aL;
+          ps += aL;
+          psp = fma(aL, D, psp);
+          ph += aR;
+          php = fma(aR, D, php);
         }
       }
       __syncthreads();
     }
     if (hit) s.hit[lane] = 1;
-    s.pf[warp][lane] = f;
-    s.pfp[warp][lane] = fp;
+    s.ps[warp][lane] = ps;
+    s.psp[warp][lane] = psp;
+    s.ph[warp][lane] = ph;
+    s.php[warp][lane] = php;
     __syncthreads();
     if (t < 32 && s.act[t] == 1) fpre_step(s, t, a);
     __syncthreads();
@@ -576,14 +549,374 @@ __device__ void slot_finish_unisolated(SolveSmem& s, double* y, int b, const Sol
   slot_finish<KP>(s, yc, b, a, o, mid - d[o], mid, FLAG_UNISOLATED, y);
 }
 
+// ---- the per-slot step, spread over the CTA's 8 warps
+// After each pass the 32 slots' k x k matrices S are factored and solved by
+// all 256 threads: thread (warp w, lane b) works on slot b's rows r with
+// r % 8 == w (the Bunch-Kaufman pivot decisions and the permutations by warp
+// 0). The same pivots and operations as bk_factor / bk_solve, with the
+// column-oriented form of the L^T solve. A serial per-lane factorization
+// left seven warps idle at a barrier and ran its dependent shared-memory
+// chain without latency hiding (up to ~30% of the kernel at 4096 poles per
+// CTA).
 template <int KP>
-__device__ __noinline__ void slot_step(SolveSmem& s, double* y, int b, const double* red, double* F, int es,
-                          const SolveArgs<KP>& a) {
+struct ParSmem {
+  double z[KP][32];             // right-hand side / solution per slot
+  int piv[KP][32];
+  int bs[KP][32];               // 0: 1x1 pivot, 1: first row of a 2x2, 2: its second row
+  double redv[kPassWarps][32];  // pivot search partials
+  int redi[kPassWarps][32];
+  int dkp[32], dstep[32], dskip[32], neg[32], zero[32], ev[32], fin[32], ninv[32];
+  double tiny[32], sigma[32];
+};
+
+constexpr size_t kSolveSmemPad = (sizeof(SolveSmem) + 15) / 16 * 16;
+
+// element (i, j), i >= j, of slot b's matrix
+#define FA(i, j) F[(size_t)b * esl + ((i) * KP + (j)) * es]
+// Warps sharing the rows of a slot: one row per warp up to 8 (KP = 1, 2, 4
+// use KP warps, synchronised by a named barrier over those warps).
+template <int KP>
+constexpr int kParWarps = (KP >= kPassWarps) ? kPassWarps : KP;
+constexpr int kRowsPer(int kp) { return (kp + kPassWarps - 1) / kPassWarps; }
+template <int KP>
+__device__ __forceinline__ void par_sync() {
+  if constexpr (kParWarps<KP> == kPassWarps) __syncthreads();
+  else if constexpr (kParWarps<KP> == 1) __syncwarp();
+  else asm volatile("bar.sync 1, %0;" ::"r"(kParWarps<KP> * 32) : "memory");
+}
+
+template <int KP>
+__device__ __forceinline__ void par_load_S(const double* red, const int* sgn, int k, double* F,
+                                           size_t esl, int es, const ParSmem<KP>& P) {
   using C = PassCfg<KP>;
-  const double* d = a.rp.d;
-  const int64_t N = a.rp.n;
+  const int b = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (w >= kParWarps<KP> || !P.ev[b]) return;
+  const double* rb = red + b * C::OUT;
+#pragma unroll
+  for (int m = 0; m < kRowsPer(KP); ++m) {
+    const int i = w + kParWarps<KP> * m;
+    if (i >= KP) break;
+    for (int c = 0; c <= i; ++c) {
+      double v = rb[C::pidx(c, i)];
+      if (c == i) v += (i < k) ? (double)sgn[i] : 1.0;
+      FA(i, c) = v;
+    }
+  }
+}
+
+template <int KP>
+__device__ void par_factor(double* F, size_t esl, int es, ParSmem<KP>& P) {
+  const double alpha = 0.6403882032022076;
+  const int b = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int RP = kRowsPer(KP);
+  if (w >= kParWarps<KP>) return;
+  for (int k = 0; k < KP; ++k) {
+    const bool on = P.ev[b] && !P.dskip[b];
+    // 1. column maximum below the diagonal over this thread's rows
+    double cm = 0.0;
+    int ci = k;
+#pragma unroll
+    for (int m = 0; m < RP; ++m) {
+      const int i = w + kParWarps<KP> * m;
+      if (on && i > k && i < KP) {
+        const double v = fabs(FA(i, k));
+        if (v > cm) cm = v, ci = i;
+      }
+    }
+    P.redv[w][b] = cm;
+    P.redi[w][b] = ci;
+    par_sync<KP>();
+    // 2. pivot decision (warp 0)
+    if (w == 0) {
+      int step = 0;
+      if (P.ev[b] && P.dskip[b]) {
+        P.dskip[b] = 0;  // second row of a 2x2 pivot
+      } else if (P.ev[b]) {
+        double colmax = 0.0;
+        int imax = k;
+        for (int ww = 0; ww < kParWarps<KP>; ++ww) {  // first maximum in row order
+          const double v = P.redv[ww][b];
+          const int i = P.redi[ww][b];
+          if (v > colmax || (v == colmax && v > 0.0 && i < imax)) colmax = v, imax = i;
+        }
+        const double absakk = fabs(FA(k, k));
+        if (fmax(absakk, colmax) == 0.0) {
+          P.piv[k][b] = k;
+          P.bs[k][b] = 0;
+          P.zero[b] = 1;
+        } else {
+          int kp = k;
+          step = 1;
+          if (!(absakk >= alpha * colmax)) {
+            double rowmax = 0.0;
+            for (int j = k; j < KP; ++j) {
+              if (j == imax) continue;
+              rowmax = fmax(rowmax, fabs(j < imax ? FA(imax, j) : FA(j, imax)));
+            }
+            if (absakk >= alpha * colmax * (colmax / rowmax)) {
+              kp = k;
+            } else if (fabs(FA(imax, imax)) >= alpha * rowmax) {
+              kp = imax;
+            } else {
+              kp = imax;
+              step = 2;
+            }
+          }
+          if (k + 1 >= KP) step = 1;
+          P.dkp[b] = kp;
+          if (step == 1) {
+            P.piv[k][b] = kp;
+            P.bs[k][b] = 0;
+          } else {
+            P.piv[k][b] = P.piv[k + 1][b] = -kp - 1;
+            P.bs[k][b] = 1;
+            P.bs[k + 1][b] = 2;
+            P.dskip[b] = 1;
+          }
+        }
+      }
+      P.dstep[b] = step;
+    }
+    par_sync<KP>();
+    const int step = P.dstep[b];
+    // 3. symmetric interchange of kk < kp on the lower triangle (entry sets
+    //    indexed by c, thread = owner of c)
+    if (step) {
+      const int kk = k + step - 1, kp = P.dkp[b];
+      if (kp != kk) {
+#pragma unroll
+        for (int m = 0; m < RP; ++m) {
+          const int c = w + kParWarps<KP> * m;
+          if (c >= KP) break;
+          if (c < kk) {
+            const double t = FA(kk, c); FA(kk, c) = FA(kp, c); FA(kp, c) = t;
+          } else if (c == kk) {
+            const double t = FA(kk, kk); FA(kk, kk) = FA(kp, kp); FA(kp, kp) = t;
+          } else if (c < kp) {
+            const double t = FA(c, kk); FA(c, kk) = FA(kp, c); FA(kp, c) = t;
+          } else if (c > kp) {
+            const double t = FA(c, kk); FA(c, kk) = FA(c, kp); FA(c, kp) = t;
+          }
+        }
+      }
+    }
+    par_sync<KP>();
+    // 4. rank-1 / rank-2 update of this thread's trailing rows (reads the
+    //    pivot columns, writes columns beyond them); multipliers kept
+    double m1[RP], m2[RP];
+    double dk = 0.0, det = 0.0;
+    if (step == 1) {
+      dk = FA(k, k);
+      if (dk != 0.0) {
+        const double r1 = 1.0 / dk;
+#pragma unroll
+        for (int m = 0; m < RP; ++m) {
+          const int i = w + kParWarps<KP> * m;
+          if (i > k && i < KP) {
+            const double li = FA(i, k) * r1;
+            for (int j = k + 1; j <= i; ++j) FA(i, j) -= li * FA(j, k);
+            m1[m] = li;
+          }
+        }
+      }
+    } else if (step == 2) {
+      const double a = FA(k, k), bb = FA(k + 1, k), c = FA(k + 1, k + 1);
+      det = a * c - bb * bb;
+      if (det != 0.0) {
+        const double id = 1.0 / det;
+#pragma unroll
+        for (int m = 0; m < RP; ++m) {
+          const int i = w + kParWarps<KP> * m;
+          if (i >= k + 2 && i < KP) {
+            const double x1 = FA(i, k), x2 = FA(i, k + 1);
+            const double w1 = (c * x1 - bb * x2) * id;
+            const double w2 = (a * x2 - bb * x1) * id;
+            for (int j = k + 2; j <= i; ++j) FA(i, j) -= w1 * FA(j, k) + w2 * FA(j, k + 1);
+            m1[m] = w1;
+            m2[m] = w2;
+          }
+        }
+      }
+      if (w == 0) {
+        if (det < 0.0) P.neg[b] += 1;
+        else if (a + c < 0.0) P.neg[b] += 2;
+        if (det == 0.0) P.zero[b] = 1;
+      }
+    }
+    if (step == 1 && w == 0) {
+      if (dk < 0.0) P.neg[b] += 1;
+      if (dk == 0.0) P.zero[b] = 1;
+    }
+    par_sync<KP>();
+    // 5. multipliers into the pivot columns (read by nobody until after the
+    //    next barrier)
+    if (step == 1 && dk != 0.0) {
+#pragma unroll
+      for (int m = 0; m < RP; ++m) {
+        const int i = w + kParWarps<KP> * m;
+        if (i > k && i < KP) FA(i, k) = m1[m];
+      }
+    } else if (step == 2 && det != 0.0) {
+#pragma unroll
+      for (int m = 0; m < RP; ++m) {
+        const int i = w + kParWarps<KP> * m;
+        if (i >= k + 2 && i < KP) FA(i, k) = m1[m], FA(i, k + 1) = m2[m];
+      }
+    }
+  }
+  par_sync<KP>();
+}
+
+// z[.][b] <- S^-1 z for the slots with sel (zero pivots replaced by tiny[b]).
+template <int KP>
+__device__ void par_solve(const double* F, size_t esl, int es, ParSmem<KP>& P, bool sel) {
+  const int b = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int RP = kRowsPer(KP);
+  if (w >= kParWarps<KP>) return;
+  if (w == 0 && sel) {  // z <- P z
+    for (int k = 0; k < KP; ++k) {
+      const int t = P.bs[k][b];
+      int r = -1, kp = 0;
+      if (t == 0) r = k, kp = P.piv[k][b];
+      else if (t == 1) r = k + 1, kp = -P.piv[k][b] - 1;
+      if (r >= 0 && kp != r) { const double v = P.z[r][b]; P.z[r][b] = P.z[kp][b]; P.z[kp][b] = v; }
+    }
+  }
+  par_sync<KP>();
+  for (int k = 0; k < KP; ++k) {  // L y = z
+    if (sel) {
+      const int t = P.bs[k][b];
+      if (t == 0) {
+        const double zk = P.z[k][b];
+#pragma unroll
+        for (int m = 0; m < RP; ++m) {
+          const int i = w + kParWarps<KP> * m;
+          if (i > k && i < KP) P.z[i][b] -= FA(i, k) * zk;
+        }
+      } else if (t == 1) {
+        const double zk = P.z[k][b], zk1 = P.z[k + 1][b];
+#pragma unroll
+        for (int m = 0; m < RP; ++m) {
+          const int i = w + kParWarps<KP> * m;
+          if (i >= k + 2 && i < KP) P.z[i][b] -= FA(i, k) * zk + FA(i, k + 1) * zk1;
+        }
+      }
+    }
+    par_sync<KP>();
+  }
+  if (sel) {  // D w = y
+#pragma unroll
+    for (int m = 0; m < RP; ++m) {
+      const int i = w + kParWarps<KP> * m;
+      if (i >= KP) break;
+      const int t = P.bs[i][b];
+      if (t == 0) {
+        double dk = FA(i, i);
+        if (dk == 0.0) dk = P.tiny[b];
+        P.z[i][b] /= dk;
+      } else if (t == 1) {
+        const double a = FA(i, i), bb = FA(i + 1, i), c = FA(i + 1, i + 1);
+        double det = a * c - bb * bb;
+        if (det == 0.0) det = P.tiny[b];
+        const double z1 = P.z[i][b], z2 = P.z[i + 1][b];
+        P.z[i][b] = (c * z1 - bb * z2) / det;
+        P.z[i + 1][b] = (a * z2 - bb * z1) / det;
+      }
+    }
+  }
+  par_sync<KP>();
+  for (int i = KP - 1; i >= 0; --i) {  // L^T z = w, column-oriented
+    if (sel) {
+      const int t = P.bs[i][b];
+      if (t == 0) {
+        const double zi = P.z[i][b];
+#pragma unroll
+        for (int m = 0; m < RP; ++m) {
+          const int k = w + kParWarps<KP> * m;
+          if (k < i) P.z[k][b] -= FA(i, k) * zi;
+        }
+      } else if (t == 2) {
+        const double zi = P.z[i][b], zi1 = P.z[i - 1][b];
+#pragma unroll
+        for (int m = 0; m < RP; ++m) {
+          const int k = w + kParWarps<KP> * m;
+          if (k < i - 1) P.z[k][b] -= FA(i, k) * zi + FA(i - 1, k) * zi1;
+        }
+      }
+    }
+    par_sync<KP>();
+  }
+  if (w == 0 && sel) {  // z <- P^T z
+    for (int k = KP - 1; k >= 0; --k) {
+      const int t = P.bs[k][b];
+      int kp = -1;
+      if (t == 0) kp = P.piv[k][b];
+      else if (t == 2) kp = -P.piv[k][b] - 1;
+      if (kp >= 0 && kp != k) { const double v = P.z[k][b]; P.z[k][b] = P.z[kp][b]; P.z[kp][b] = v; }
+    }
+  }
+  par_sync<KP>();
+}
+
+// ------------------------------------------------------------ sweep kernel
+template <int KP>
+__global__ void __launch_bounds__(kPassThreads, 1) count_sweep_kernel(ReducedView rp,
+                                                                      int* __restrict__ counts,
+                                                                      int64_t qbeg, int64_t qend,
+                                                                      double* __restrict__ gscratch) {
+  using C = PassCfg<KP>;
+  extern __shared__ __align__(16) double smem[];
+  // factor storage: interleaved [KP*KP][32] in shared memory for KP <= 16,
+  // per-slot matrices in global scratch above (32 x 32 x 32 doubles do not fit)
+  constexpr bool kSmemF = KP <= 16;
+  double* F = kSmemF ? smem + C::SMEM_DOUBLES : gscratch + (size_t)blockIdx.x * 32 * KP * KP;
+  const size_t esl = kSmemF ? 1 : (size_t)KP * KP;
+  constexpr int es = kSmemF ? 32 : 1;
+  ParSmem<KP>& P = *reinterpret_cast<ParSmem<KP>*>(smem + C::SMEM_DOUBLES + (kSmemF ? 32 * KP * KP : 0));
+  __shared__ double dob[32], delta[32];
+  __shared__ int active[32], hit[32];
+  const int t = threadIdx.x;
+  const int64_t Q = qend;
+  const int64_t q0 = qbeg + (int64_t)blockIdx.x * 32;
+  if (t < 32) {
+    const int64_t q = q0 + t;
+    active[t] = q < Q;
+    dob[t] = 0.0;
+    delta[t] = (q < Q) ? sweep_point(rp.d, rp.n, q) : 0.0;
+    hit[t] = 0;
+  }
+  __syncthreads();
+  PassSlots sl{dob, delta, nullptr, active, hit};
+  PassOpts o;
+  secular_pass<KP>(rp.d, rp.u, rp.n, sl, o, smem);
+  // inertia of the 32 S(x) by the CTA's warps (par_factor)
+  if (t < 32) {
+    P.ev[t] = active[t] && !hit[t];
+    P.neg[t] = 0;
+    P.zero[t] = 0;
+    P.dskip[t] = 0;
+  }
+  __syncthreads();
+  par_load_S<KP>(pass_result<KP>(smem), rp.sgn, rp.k, F, esl, es, P);
+  __syncthreads();
+  par_factor<KP>(F, esl, es, P);
+  if (t < 32 && active[t]) {
+    const double x = delta[t];
+    // a hit (x on a pole, duplicates) gives an unusable point: -1
+    counts[q0 + t] = hit[t] ? -1 : (int)(dev_n_less(rp.d, rp.n, x) + rp.m_neg - P.neg[t]);
+  }
+}
+
+// Warp 0, before the factorization: the evaluation count, and a pass that
+// landed exactly on a pole (nudge and retry without factoring).
+template <int KP>
+__device__ void slot_pre(SolveSmem& s, ParSmem<KP>& P, double* y, int b, const SolveArgs<KP>& a) {
+  P.ev[b] = 0;
+  P.fin[b] = 0;
+  P.ninv[b] = 0;
+  if (s.active[b] != 1) return;
   s.iters[b] += 1;
-  if (s.hit[b]) {  // evaluation landed exactly on a pole: nudge and retry
+  if (s.hit[b]) {
     s.hit[b] = 0;
     const double cur = s.delta[b], lo = s.lo[b], hi = s.hi[b];
     double alt = nextafter(cur, hi);
@@ -601,39 +934,33 @@ __device__ __noinline__ void slot_step(SolveSmem& s, double* y, int b, const dou
     s.delta[b] = alt;
     return;
   }
-  const double* rb = red + b * C::OUT;
-  load_S<KP>(rb, a.rp.sgn, a.rp.k, F, es);
-  const double gp = rb[C::IG];
-  const double fv = 1.0 + rb[C::IF], fpv = rb[C::IFP];
-  int piv[KP], zero = 0;
-  const int neg = slot_factor<KP>(F, es, piv, &zero);
-  double pscale = 0.0;
-  for (int c = 0; c < KP; ++c) pscale = fmax(pscale, fabs(F[(c * KP + c) * es]));
-  // an exactly zero pivot (x is a root to working precision) is replaced by a
-  // tiny multiple of the pivot scale: inverse iteration then still returns
-  // the null vector instead of overflowing
-  const double tiny = 1e-4 * DBL_EPSILON * fmax(pscale, 1e-300);
-  double yv[KP], z[KP];
-  for (int c = 0; c < KP; ++c) yv[c] = y[b * KP + c];
+  P.ev[b] = 1;
+  P.neg[b] = 0;
+  P.zero[b] = 0;
+  P.dskip[b] = 0;
   // a slot started at the f presolve's root has no y from earlier
   // evaluations: its first evaluation takes three inverse-iteration steps on
   // this factorization and makes no Newton step (the pass computed sigma'
   // with the unconverged y), the second repeats the point with the new y
-  const int ninv = s.warm[b] ? 3 : 1;
-  double sigma = 0.0;
-  for (int it = 0; it < ninv; ++it) {
-    for (int c = 0; c < KP; ++c) z[c] = yv[c];
-    slot_solve<KP>(F, es, piv, z, tiny);
-    double zz = 0.0, zy = 0.0;
-    for (int c = 0; c < KP; ++c) zz += z[c] * z[c], zy += z[c] * yv[c];
-    if (!(zz > 0.0 && isfinite(zz))) break;
-    sigma = zy / zz;  // Rayleigh quotient of S at z
-    const double inv = rsqrt(zz);
-    for (int c = 0; c < KP; ++c) yv[c] = z[c] * inv;
-  }
-  for (int c = 0; c < KP; ++c) y[b * KP + c] = yv[c];
-  const int64_t j = s.j[b];
+  P.ninv[b] = s.warm[b] ? 3 : 1;
+}
 
+// Warp 0, after the factorization and inverse iteration: the count, bracket
+// update and Newton step of the slot (y already holds the new vector).
+// A converged slot gets fin = 1 (two more inverse-iteration steps, then its
+// record).
+template <int KP>
+__device__ void slot_post(SolveSmem& s, ParSmem<KP>& P, double* y, int b, const double* red,
+                          const SolveArgs<KP>& a) {
+  using C = PassCfg<KP>;
+  const double* d = a.rp.d;
+  const int64_t N = a.rp.n;
+  const double* rb = red + b * C::OUT;
+  const double gp = rb[C::IG];
+  const double fv = 1.0 + rb[C::IF], fpv = rb[C::IFP];
+  const int neg = P.neg[b], zero = P.zero[b];
+  const double sigma = P.sigma[b];
+  const int64_t j = s.j[b];
   if (s.phase[b] == 0) {
     const double x = s.delta[b];
     // x strictly inside (lo, hi): the count lies in the bracket's pole window
@@ -728,18 +1055,12 @@ __device__ __noinline__ void slot_step(SolveSmem& s, double* y, int b, const dou
                                    (far && fabs(step) <= a.floor_ulps * DBL_EPSILON *
                                                              fabs(s.dob[b] + dl)))));
   if (sdone || w <= tol || zero || s.iters[b] > a.max_iters) {
-    // two more inverse-iteration steps on the same factorization: the
-    // eigenvector formula needs y to the accuracy of the root
-    for (int it = 0; it < 2; ++it) {
-      for (int c = 0; c < KP; ++c) z[c] = yv[c];
-      slot_solve<KP>(F, es, piv, z, tiny);
-      double z2 = 0.0;
-      for (int c = 0; c < KP; ++c) z2 += z[c] * z[c];
-      if (!(z2 > 0.0 && isfinite(z2))) break;
-      const double inv = rsqrt(z2);
-      for (int c = 0; c < KP; ++c) yv[c] = z[c] * inv;
-    }
-    slot_finish<KP>(s, yv, b, a, s.o[b], dl, s.dob[b] + dl, 0, y);
+    // two more inverse-iteration steps on the same factorization follow (the
+    // eigenvector formula needs y to the accuracy of the root)
+    P.fin[b] = 1;
+    s.fin_o[b] = s.o[b];
+    s.fin_delta[b] = dl;
+    s.fin_value[b] = s.dob[b] + dl;
     return;
   }
   double dn = dl + step;
@@ -776,6 +1097,7 @@ __device__ __noinline__ void slot_step(SolveSmem& s, double* y, int b, const dou
   s.delta[b] = dn;
 }
 
+
 template <int KP>
 constexpr bool kFactorInSmem = (KP <= 16);
 
@@ -796,6 +1118,7 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 4 ? 2 : 1) solve_roots_ker
   double* Fs = y + 32 * KP;                                // [KP*KP][32] (KP <= 16)
   double* fullred = Fs + (kFactorInSmem<KP> ? 32 * KP * KP : 0);  // [32][OUT] (CL > 1)
   SolveSmem& s = *reinterpret_cast<SolveSmem*>(fullred + (CL > 1 ? C::RED_DOUBLES : 0));
+  ParSmem<KP>& P = *reinterpret_cast<ParSmem<KP>*>(reinterpret_cast<char*>(&s) + kSolveSmemPad);
   __shared__ int any;
   const int t = threadIdx.x;
   int rank = 0;
@@ -805,15 +1128,20 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 4 ? 2 : 1) solve_roots_ker
   const int64_t chunk = (N + CL - 1) / CL;
   const int64_t plo = (rank * chunk < N) ? rank * chunk : N;
   const int64_t pcnt = ((plo + chunk < N) ? plo + chunk : N) - plo;
+  // slot b's matrix: element (i, j) at F[b * esl + (i * KP + j) * es]
   double* F;
+  size_t esl;
   int es;
   if constexpr (kFactorInSmem<KP>) {
-    F = Fs + (t & 31);
+    F = Fs;
+    esl = 1;
     es = 32;
   } else {
-    F = gscratch + ((size_t)blockIdx.x * 32 + (t & 31)) * KP * KP;
+    F = gscratch + (size_t)blockIdx.x * 32 * KP * KP;
+    esl = (size_t)KP * KP;
     es = 1;
   }
+  const int lane = t & 31;
   if (t < 32) s.active[t] = 2;
   __syncthreads();
   PassOpts o;
@@ -821,6 +1149,7 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 4 ? 2 : 1) solve_roots_ker
   o.want_sigma = true;
   unsigned long long npass = 0, nact = 0;
   long long c_refill = 0, c_pass = 0, c_red = 0, c_step = 0;  // SM cycles (thread 0)
+  long long c_load = 0, c_fact = 0, c_solve = 0;
   for (;;) {
     const long long t0 = clock64();
     // ---- refill finished slots from the root queue
@@ -878,9 +1207,77 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 4 ? 2 : 1) solve_roots_ker
       red = fullred;
     }
     const long long t3 = clock64();
-    if (t < 32 && s.active[t] == 1) slot_step<KP>(s, y, t, red, F, es, a);
+    // ---- per-slot step (all warps): factor S, inverse iteration, Newton
+    if (t < 32) slot_pre<KP>(s, P, y, t, a);
+    __syncthreads();
+    par_load_S<KP>(red, a.rp.sgn, a.rp.k, F, esl, es, P);
+    __syncthreads();
+    const long long t3a = clock64();
+    par_factor<KP>(F, esl, es, P);
+    const long long t3b = clock64();
+    if (t < 32 && P.ev[t]) {
+      const int b = t;
+      double pscale = 0.0;
+      for (int c = 0; c < KP; ++c) pscale = fmax(pscale, fabs(FA(c, c)));
+      // an exactly zero pivot (x is a root to working precision) is replaced
+      // by a tiny multiple of the pivot scale: inverse iteration then still
+      // returns the null vector instead of overflowing
+      P.tiny[b] = 1e-4 * DBL_EPSILON * fmax(pscale, 1e-300);
+      P.sigma[b] = 0.0;
+      for (int c = 0; c < KP; ++c) P.z[c][b] = y[b * KP + c];
+    }
+    for (int it = 0; it < 3; ++it) {  // inverse iteration: y <- S^-1 y / |.|, sigma
+      const bool sel = P.ev[lane] && P.ninv[lane] > it;
+      if (!__syncthreads_or(sel)) break;
+      par_solve<KP>(F, esl, es, P, sel);
+      if (t < 32 && sel) {
+        double zz = 0.0, zy = 0.0;
+        for (int c = 0; c < KP; ++c) zz += P.z[c][t] * P.z[c][t], zy += P.z[c][t] * y[t * KP + c];
+        if (!(zz > 0.0 && isfinite(zz))) {
+          P.ninv[t] = 0;
+        } else {
+          P.sigma[t] = zy / zz;  // Rayleigh quotient of S at z
+          const double inv = rsqrt(zz);
+          for (int c = 0; c < KP; ++c) {
+            const double v = P.z[c][t] * inv;
+            y[t * KP + c] = v;
+            P.z[c][t] = v;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    const long long t3c = clock64();
+    if (t < 32 && P.ev[t]) slot_post<KP>(s, P, y, t, red, a);
+    for (int it = 0; it < 2; ++it) {  // converged slots: two more steps
+      const bool sel = P.fin[lane] == 1;
+      if (!__syncthreads_or(sel)) break;
+      if (t < 32 && sel)
+        for (int c = 0; c < KP; ++c) P.z[c][t] = y[t * KP + c];
+      __syncthreads();
+      par_solve<KP>(F, esl, es, P, sel);
+      if (t < 32 && sel) {
+        double z2 = 0.0;
+        for (int c = 0; c < KP; ++c) z2 += P.z[c][t] * P.z[c][t];
+        if (!(z2 > 0.0 && isfinite(z2))) {
+          P.fin[t] = 2;
+        } else {
+          const double inv = rsqrt(z2);
+          for (int c = 0; c < KP; ++c) y[t * KP + c] = P.z[c][t] * inv;
+        }
+      }
+    }
+    __syncthreads();
+    if (t < 32 && P.fin[t]) {
+      double yc[KP];
+      for (int c = 0; c < KP; ++c) yc[c] = y[t * KP + c];
+      slot_finish<KP>(s, yc, t, a, s.fin_o[t], s.fin_delta[t], s.fin_value[t], 0, y);
+    }
     __syncthreads();
     const long long t4 = clock64();
+    c_load += t3a - t3;
+    c_fact += t3b - t3a;
+    c_solve += t3c - t3b;
     c_refill += t1 - t0;
     c_pass += t2 - t1;
     c_red += t3 - t2;
@@ -894,6 +1291,9 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 4 ? 2 : 1) solve_roots_ker
     atomicAdd(a.prof + 4, (unsigned long long)c_pass);
     atomicAdd(a.prof + 5, (unsigned long long)c_red);
     atomicAdd(a.prof + 6, (unsigned long long)c_step);
+    atomicAdd(a.prof + 7, (unsigned long long)c_load);
+    atomicAdd(a.prof + 8, (unsigned long long)c_fact);
+    atomicAdd(a.prof + 9, (unsigned long long)c_solve);
   }
 }
 
@@ -965,7 +1365,7 @@ size_t solve_smem_bytes() {
   using C = PassCfg<KP>;
   return sizeof(double) * (C::SMEM_DOUBLES + 32 * KP + (kFactorInSmem<KP> ? 32 * KP * KP : 0) +
                            (CL > 1 ? C::RED_DOUBLES : 0)) +
-         sizeof(SolveSmem);
+         kSolveSmemPad + sizeof(ParSmem<KP>);
 }
 
 template <int KP>
@@ -973,7 +1373,7 @@ void launch_sweep(const ReducedView& rp, int* counts, int64_t qbeg, int64_t qend
                   DeviceScratch& ws, cudaStream_t st) {
   using C = PassCfg<KP>;
   constexpr bool kSmemF = KP <= 16;
-  const size_t sm = sizeof(double) * (C::SMEM_DOUBLES + (kSmemF ? 32 * KP * KP : 0));
+  const size_t sm = sizeof(double) * (C::SMEM_DOUBLES + (kSmemF ? 32 * KP * KP : 0)) + sizeof(ParSmem<KP>);
   EIGB_CUDA(cudaFuncSetAttribute(count_sweep_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sm));
   if (qend <= qbeg) return;
@@ -1048,7 +1448,7 @@ void launch_solve(const ReducedView& rp, const double* alpha, const double* br_l
   a.writer = 1;
   const int64_t nroots = j1 - j0;
   a.next_root = reinterpret_cast<unsigned long long*>(ws.get_i64("solve_counter", 1));
-  a.prof = reinterpret_cast<unsigned long long*>(ws.get_i64("solve_prof", 8));
+  a.prof = reinterpret_cast<unsigned long long*>(ws.get_i64("solve_prof", 12));
   a.trace_j = opt.trace_root;
   a.fexit_rel = opt.fexit_rel;
   a.floor_rel = opt.floor_rel;
@@ -1058,7 +1458,7 @@ void launch_solve(const ReducedView& rp, const double* alpha, const double* br_l
   a.trace = ws.get_f64("solve_trace", (size_t)kTraceRows * kTraceCols);
   if (opt.trace_root >= 0)
     EIGB_CUDA(cudaMemsetAsync(a.trace, 0, sizeof(double) * kTraceRows * kTraceCols, st));
-  EIGB_CUDA(cudaMemsetAsync(a.prof, 0, 8 * sizeof(unsigned long long), st));
+  EIGB_CUDA(cudaMemsetAsync(a.prof, 0, 12 * sizeof(unsigned long long), st));
   const unsigned long long start = (unsigned long long)j0;
   EIGB_CUDA(cudaMemcpyAsync(a.next_root, &start, sizeof(start), cudaMemcpyHostToDevice, st));
   // Size-based choice (tools/exp_cluster.py, cfg 2/4 at n = 8192/32768):
@@ -1147,7 +1547,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) pole_inertia_kernel(InertiaAr
   double* W = T + KP * KP;   // reflectors, one per row of R
   double* x = W + KP * KP;
   const double* rb = pass_result<KP>(smem) + t * C::OUT;
-  load_S<KP>(rb, a.rp.sgn, k, T, 1, true);
+  load_S<KP>(rb, a.rp.sgn, k, T, 1);
   // Householder vectors of span(R): reflector q acts on coordinates q..k-1
   int q = 0;
   const int64_t r0 = a.brow[g];
@@ -1314,7 +1714,7 @@ void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t
   int64_t* f_o = nullptr;
   double* f_delta = nullptr;
   int* f_state = nullptr;
-  if (alpha && br_lo && opt.fpre) {
+  if (alpha && br_lo && opt.fpre && rp.kp >= opt.fpre_min_kp) {
     const int64_t nr = j1 - j0;
     f_o = ws.get_i64("fpre_o", nr);
     f_delta = ws.get_f64("fpre_delta", nr);
@@ -1329,7 +1729,10 @@ void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t
     int per_sm = 0;
     EIGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fpresolve_kernel,
                                                             kFPreWarps * 32, 0));
-    const int64_t grid = std::min<int64_t>((int64_t)std::max(1, per_sm) * sms, cdiv(nr, 32));
+    // few CTAs per SM so that each refills its slots from the root queue many
+    // times (iteration counts vary; a one-batch CTA runs as long as its
+    // slowest root)
+    const int64_t grid = std::min<int64_t>((int64_t)std::min(2, std::max(1, per_sm)) * sms, cdiv(nr, 32));
     fpresolve_kernel<<<(unsigned)grid, kFPreWarps * 32, 0, st>>>(fa);
     EIGB_LAUNCH_CHECK();
   }

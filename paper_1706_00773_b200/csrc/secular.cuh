@@ -91,10 +91,13 @@ struct SolveOptions {
   double floor_ulps = 4.0;   // ... or below this many ulps of the root value
   double stall_ratio = 0.5;  // "no longer shrinking": |step| >= stall_ratio * |previous step|
   int geo_bisect = 1;       // geometric bisection of brackets spanning decades of delta
-  // scalar presolve: Newton on f alone (K2 residues) for every isolated root
-  // before the S solver, which then starts psi-Newton at the f-root
-  bool fpre = false;
-  int fpre_iters = 60;
+  // scalar presolve: the f-root (K2 residues) of every isolated root before
+  // the S solver, which then starts psi-Newton there. Used from kp = 16 up,
+  // where an S evaluation costs ~10x an f evaluation (cfg4 n = 32768: solve
+  // 180 -> 157 ms); below that it does not pay (tools/exp_fpre.py).
+  bool fpre = true;
+  int fpre_min_kp = 16;
+  int fpre_iters = 12;
 };
 
 // Diagnostics trace of one root: per evaluation kTraceCols doubles

@@ -475,235 +475,6 @@ __host__ __device__ inline void bk_solve(const double* A, int n, int ld, const i
   }
 }
 
-// ------------------------------------------- Bunch-Kaufman, compile-time KP
-// The same factorization as bk_factor / bk_solve for the solver's per-slot
-// step (one lane, KP x KP, element (i, j) at A[(i * KP + j) * es]), written
-// for latency: only the lower triangle is read or written (no mirrored
-// stores), every loop has compile-time bounds (k, i, j unrolled; a 2x2 pivot
-// skips the next k), columns are staged in registers before the rank-1/2
-// update so the shared-memory read-modify-writes are independent, and the
-// solve keeps b in registers (runtime interchanges become unrolled selects).
-// Pivots and interchanges match bk_factor, so the inertia is the same.
-template <int KP>
-__device__ __forceinline__ int bkl_factor(double* A, int es, int* piv, int* zero) {
-#define AL(i, j) A[((i) * KP + (j)) * es]
-  const double alpha = 0.6403882032022076;
-  int neg = 0;
-  *zero = 0;
-  bool skip = false;
-#pragma unroll
-  for (int k = 0; k < KP; ++k) {
-    if (skip) {
-      skip = false;
-      continue;
-    }
-    const double absakk = fabs(AL(k, k));
-    int imax = k;
-    double colmax = 0.0;
-#pragma unroll
-    for (int i = k + 1; i < KP; ++i) {
-      const double v = fabs(AL(i, k));
-      if (v > colmax) colmax = v, imax = i;
-    }
-    if (fmax(absakk, colmax) == 0.0) {
-      piv[k] = k;
-      *zero = 1;
-      continue;
-    }
-    int kstep = 1, kp = k;
-    if (!(absakk >= alpha * colmax)) {
-      double rowmax = 0.0;  // max |A(imax, j)|, j in [k, KP), j != imax
-#pragma unroll
-      for (int j = k; j < KP; ++j) {
-        if (j == imax) continue;
-        const int r = j < imax ? imax : j, c = j < imax ? j : imax;
-        rowmax = fmax(rowmax, fabs(AL(r, c)));
-      }
-      if (absakk >= alpha * colmax * (colmax / rowmax)) {
-        kp = k;
-      } else if (fabs(AL(imax, imax)) >= alpha * rowmax) {
-        kp = imax;
-      } else {
-        kp = imax;
-        kstep = 2;
-      }
-    }
-    if (k + 1 >= KP) kstep = 1;  // (cannot pair past the end: imax > k excludes it)
-    const int kk = k + kstep - 1;
-    if (kp != kk) {  // symmetric interchange of kk < kp on the lower triangle
-#pragma unroll
-      for (int c = 0; c < KP; ++c) {
-        if (c < kk) {
-          const double t = AL(kk, c);
-          AL(kk, c) = AL(kp, c);
-          AL(kp, c) = t;
-        }
-      }
-      {
-        const double t = AL(kk, kk);
-        AL(kk, kk) = AL(kp, kp);
-        AL(kp, kp) = t;
-      }
-#pragma unroll
-      for (int r = 1; r < KP; ++r) {
-        if (r > kk && r < kp) {
-          const double t = AL(r, kk);
-          AL(r, kk) = AL(kp, r);
-          AL(kp, r) = t;
-        } else if (r > kp) {
-          const double t = AL(r, kk);
-          AL(r, kk) = AL(r, kp);
-          AL(r, kp) = t;
-        }
-      }
-    }
-    if (kstep == 1) {
-      const double dk = AL(k, k);
-      piv[k] = kp;
-      if (dk < 0.0) ++neg;
-      if (dk == 0.0) {
-        *zero = 1;
-      } else {
-        const double r1 = 1.0 / dk;
-        double col[KP];
-#pragma unroll
-        for (int i = k + 1; i < KP; ++i) col[i] = AL(i, k);
-        // rows one at a time (bounded register pressure), the row's columns
-        // unrolled with predicates
-#pragma unroll 1
-        for (int i = k + 1; i < KP; ++i) {
-          const double li = AL(i, k) * r1;
-#pragma unroll
-          for (int j = k + 1; j < KP; ++j)
-            if (j <= i) AL(i, j) -= li * col[j];
-        }
-#pragma unroll
-        for (int i = k + 1; i < KP; ++i) AL(i, k) = col[i] * r1;
-      }
-    } else {
-      const double a = AL(k, k), b = AL(k + 1, k), c = AL(k + 1, k + 1);
-      const double det = a * c - b * b;
-      piv[k] = -kp - 1;
-      piv[k + 1] = -kp - 1;
-      if (det < 0.0) neg += 1;
-      else if (a + c < 0.0) neg += 2;
-      skip = true;
-      if (det == 0.0) {
-        *zero = 1;
-      } else {
-        const double id = 1.0 / det;
-        double c1[KP], c2[KP];
-#pragma unroll
-        for (int i = k + 2; i < KP; ++i) c1[i] = AL(i, k), c2[i] = AL(i, k + 1);
-#pragma unroll 1
-        for (int i = k + 2; i < KP; ++i) {
-          const double x1 = AL(i, k), x2 = AL(i, k + 1);
-          const double w1 = (c * x1 - b * x2) * id;
-          const double w2 = (a * x2 - b * x1) * id;
-#pragma unroll
-          for (int j = k + 2; j < KP; ++j)
-            if (j <= i) AL(i, j) -= w1 * c1[j] + w2 * c2[j];
-          AL(i, k) = w1;
-          AL(i, k + 1) = w2;
-        }
-      }
-    }
-  }
-  return neg;
-}
-
-// b[k] <-> b[kp] for compile-time k and runtime kp >= k, b in registers.
-template <int KP>
-__device__ __forceinline__ void bkl_swap(double* b, int k, int kp) {
-  const double bk = b[k];
-  double bp = bk;
-#pragma unroll
-  for (int c = 0; c < KP; ++c)
-    if (c > k && c == kp) bp = b[c];
-#pragma unroll
-  for (int c = 0; c < KP; ++c)
-    if (c > k && c == kp) b[c] = bk;
-  b[k] = bp;
-}
-
-template <int KP>
-__device__ __forceinline__ void bkl_solve(const double* A, int es, const int* piv, double* b,
-                                          double tiny) {
-  bool skip = false;
-#pragma unroll
-  for (int k = 0; k < KP; ++k) {  // b <- P b
-    if (skip) { skip = false; continue; }
-    if (piv[k] >= 0) {
-      bkl_swap<KP>(b, k, piv[k]);
-    } else if (k + 1 < KP) {
-      bkl_swap<KP>(b, k + 1, -piv[k] - 1);
-      skip = true;
-    }
-  }
-  skip = false;
-#pragma unroll
-  for (int k = 0; k < KP; ++k) {  // L y = b
-    if (skip) { skip = false; continue; }
-    if (piv[k] >= 0) {
-#pragma unroll
-      for (int i = k + 1; i < KP; ++i) b[i] -= AL(i, k) * b[k];
-    } else {
-#pragma unroll
-      for (int i = k + 2; i < KP; ++i) b[i] -= AL(i, k) * b[k] + AL(i, k + 1) * b[k + 1];
-      skip = true;
-    }
-    asm volatile("" ::: "memory");  // one column's loads in flight at a time (registers)
-  }
-  skip = false;
-#pragma unroll
-  for (int k = 0; k < KP; ++k) {  // D w = y
-    if (skip) { skip = false; continue; }
-    if (piv[k] >= 0) {
-      double dk = AL(k, k);
-      if (dk == 0.0) dk = tiny;
-      b[k] /= dk;
-    } else if (k + 1 < KP) {
-      const double a = AL(k, k), bb = AL(k + 1, k), c = AL(k + 1, k + 1);
-      double det = a * c - bb * bb;
-      if (det == 0.0) det = tiny;
-      const double x1 = (c * b[k] - bb * b[k + 1]) / det;
-      const double x2 = (a * b[k + 1] - bb * b[k]) / det;
-      b[k] = x1;
-      b[k + 1] = x2;
-      skip = true;
-    }
-  }
-  skip = false;
-#pragma unroll
-  for (int k = KP - 1; k >= 0; --k) {  // L^T z = w
-    if (skip) { skip = false; continue; }
-    if (piv[k] >= 0) {
-#pragma unroll
-      for (int i = k + 1; i < KP; ++i) b[k] -= AL(i, k) * b[i];
-    } else if (k >= 1) {  // block (k-1, k)
-#pragma unroll
-      for (int i = k + 1; i < KP; ++i) {
-        b[k] -= AL(i, k) * b[i];
-        b[k - 1] -= AL(i, k - 1) * b[i];
-      }
-      skip = true;
-    }
-    asm volatile("" ::: "memory");
-  }
-  skip = false;
-#pragma unroll
-  for (int k = KP - 1; k >= 0; --k) {  // z <- P^T z
-    if (skip) { skip = false; continue; }
-    if (piv[k] >= 0) {
-      bkl_swap<KP>(b, k, piv[k]);
-    } else {
-      bkl_swap<KP>(b, k, -piv[k] - 1);
-      skip = true;
-    }
-  }
-#undef AL
-}
-
 // proj/src/secular.cpp:14-38 (LU with partial pivoting, det on the fly).
 __device__ inline int lu_factor_dev(double* m, int k, int ld, int* piv, double* det) {
   for (int i = 0; i < k; ++i) piv[i] = i;

@@ -1,6 +1,7 @@
 """Solver stage with and without the scalar f presolve (dev tool): time,
 S evaluations per root, max evaluations, and the eigenvalue / orthogonality
 agreement of the two variants."""
+import os
 import sys
 sys.path.insert(0, '.')
 import torch
@@ -17,6 +18,8 @@ for cfg, n in cases:
         ctx = capi.Context(0)
         ctx.set_option('timing', 1)
         ctx.set_option('fpre', fp)
+        if 'EIGMOD_FPRE_ITERS' in os.environ:
+            ctx.set_option('fpre_iters', float(os.environ['EIGMOD_FPRE_ITERS']))
         for rep in range(2):
             ctx.stage_times(reset=True)
             capi.update_decomposition_device(q, lam, kmat, signs.numpy(), lo, qo, ctx=ctx)

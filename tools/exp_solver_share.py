@@ -30,6 +30,7 @@ for cfg, n in [(4, 32768), (4, 16384), (2, 16384), (1, 16384)]:
         sh = pr['share']
         print(f"cfg{cfg} n={n} roots={j1 - j0}: {a.elapsed_time(b):7.2f} ms evals/root "
               f"{float(rec[:, 4].sum()) / (j1 - j0):.2f} util {pr['slot_util']:.3f} share refill "
-              f"{sh['refill']:.3f} pass {sh['pass']:.3f} reduce {sh['reduce']:.3f} step {sh['step']:.3f}", flush=True)
+              f"{sh['refill']:.3f} pass {sh['pass']:.3f} reduce {sh['reduce']:.3f} step {sh['step']:.3f} "
+              f"(load {sh['step_load']:.3f} factor {sh['step_factor']:.3f} solve {sh['step_solve']:.3f})", flush=True)
     ctx.close()
     del q; torch.cuda.empty_cache()
