@@ -274,7 +274,8 @@ void finish(eigmod_b200_ctx* c, const double* q, const double* lam_in, int64_t c
   if (!q_out || c1 <= c0) return;
   double* colldir = c->ws.get_f64("colldir", (size_t)std::max<int64_t>(p.nred, 1) * (2 * p.kp + 4));
   int* collok = c->ws.get_i32("collok", std::max<int64_t>(p.nred, 1));
-  const int64_t ncoll = eigb::collision_vectors_dev(p, c->recs, colldir, collok, c->ws, c->stream);
+  const int64_t ncoll =
+      eigb::collision_vectors_dev(p, c->recs, cols, c0, c1, colldir, collok, c->ws, c->stream);
   const int64_t nc = c1 - c0;
   double* xt = c->ws.get_f64("xt", (size_t)nc * n);
   double* colscale = c->ws.get_f64("colscale", nc);

@@ -673,8 +673,9 @@ __global__ void __launch_bounds__(256, 2) xt_tile64_kernel(
   }
 }
 
-// K4 v3 (plans without compressed runs or collided roots: every column is a
-// root by the formula or a unit vector): lane = original index, R rows per
+// K4 v3 (plans without compressed runs: every column is a root -- by the
+// formula, the bordered-system vector of a collided / near-pole root, or its
+// e_o fallback -- or a unit vector): lane = original index, R rows per
 // thread (rows lane + 32 a of the warp's block), 64 columns per CTA with
 // their y in shared memory (LDS.128 broadcasts, each reused for R rows), Xt
 // written straight from registers (warp-coalesced rows), column sums of
@@ -702,7 +703,7 @@ __global__ void __launch_bounds__(256, KP >= 32 ? 1 : 2) xt_rows_kernel(
   constexpr int R = RC::R, YS = RC::YS;
   __shared__ __align__(16) double yt[kXt2 * YS];
   __shared__ double cdob[kXt2], cdel[kXt2];
-  __shared__ int64_t co[kXt2], ct[kXt2];
+  __shared__ int64_t co[kXt2], ct[kXt2], cj[kXt2];
   __shared__ int ck[kXt2], cm[kXt2];
   __shared__ double red[kXt2];
   __shared__ double sb[8][256];
@@ -711,7 +712,7 @@ __global__ void __launch_bounds__(256, KP >= 32 ? 1 : 2) xt_rows_kernel(
   if (t < kXt2) {
     const int64_t c = cb + t;
     int kind = -1, mode = 0;
-    int64_t o = 0, tt = 0;
+    int64_t o = 0, tt = 0, jr = 0;
     double dob = 0.0, del = 0.0;
     double* y = yt + t * YS;
     for (int q = 0; q < YS; ++q) y[q] = 0.0;
@@ -720,12 +721,16 @@ __global__ void __launch_bounds__(256, KP >= 32 ? 1 : 2) xt_rows_kernel(
       const int64_t pay = cpay[c];
       if (kind == 0) {
         const int64_t j = pay;
+        jr = j;
         o = origin[j];
         dob = rp.d[o];
         del = delta[j];
         const bool coll = (flags[j] & 1) != 0;
         mode = (collok[j] == 1) ? 1 : ((collok[j] == 2 && coll) ? 2 : 0);
-        for (int q = 0; q <= KP; ++q) y[q] = (q < KP) ? yall[j * KP + q] : 0.0;
+        if (mode == 1)  // the bordered-system vector z (as y)
+          for (int q = 0; q <= KP; ++q) y[q] = (q < KP) ? colldir[j * kCollStride<KP> + q] : 0.0;
+        else
+          for (int q = 0; q <= KP; ++q) y[q] = (q < KP) ? yall[j * KP + q] : 0.0;
       } else {
         const int64_t src = dec_src[pay];
         if (kind == 1) {
@@ -741,6 +746,7 @@ __global__ void __launch_bounds__(256, KP >= 32 ? 1 : 2) xt_rows_kernel(
     cm[t] = mode;
     co[t] = o;
     ct[t] = tt;
+    cj[t] = jr;
     cdob[t] = dob;
     cdel[t] = del;
   }
@@ -812,8 +818,16 @@ __global__ void __launch_bounds__(256, KP >= 32 ? 1 : 2) xt_rows_kernel(
           const double dot = h ? (e1[a] + o1[a]) : (e0[a] + o0[a]);
           const int64_t i = ib + 32 * a;
           double x;
-          if (colfast) {
+          if (colfast && cm[qh] == 0) {
             x = (rr[a] >= 0) ? dot * rcp64((drow[a] - dob) - del) : 0.0;
+          } else if (colfast && cm[qh] == 2) {  // collided fallback e_o
+            x = (rr[a] >= 0 && rr[a] == co[qh]) ? 1.0 : 0.0;
+          } else if (colfast) {  // bordered system (red_value mode 1); dot = u_r . z
+            const double* cd = colldir + cj[qh] * kCollStride<KP>;
+            const int64_t r0 = (int64_t)cd[2 * KP], nr0 = (int64_t)cd[2 * KP + 1];
+            if (rr[a] < 0) x = 0.0;
+            else if (rr[a] >= r0 && rr[a] < r0 + nr0) x = cd[KP + (rr[a] - r0)];
+            else x = -dot / ((drow[a] - cd[2 * KP + 3]) - cd[2 * KP + 2]);
           } else {  // unit column of an unchanged pair
             x = (kind == 1 && i == co[qh]) ? 1.0 : 0.0;
           }
@@ -855,7 +869,7 @@ void launch_xt(const Plan& p, const RootRecords& roots, const Columns& cols, con
     const char* e = std::getenv("EIGMOD_B200_XT");
     v2 = (e && std::string(e) == "v2");
   }
-  if (!v1 && !v2 && !general) {
+  if (!v1 && !v2 && p.nmulti == 0) {
     using RC = XtRowsCfg<KP>;
     const int64_t nchunks = cdiv(p.n, RC::ROWS);
     double* part = ws.get_f64("xt_part", (size_t)nchunks * (c1 - c0));
@@ -962,10 +976,25 @@ void merge_columns_dev(const Plan& p, const RootRecords& roots, Columns& cols, D
   EIGB_LAUNCH_CHECK();
 }
 
-int64_t collision_vectors_dev(const Plan& p, const RootRecords& roots, double* colldir,
-                              int* collok, DeviceScratch& ws, cudaStream_t st) {
+__global__ void column_roots_kernel(const int* __restrict__ ckind, const int64_t* __restrict__ cpay,
+                                    int64_t c0, int64_t c1, int* __restrict__ need) {
+  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < c1 && ckind[c] == 0) need[cpay[c]] = 1;
+}
+
+int64_t collision_vectors_dev(const Plan& p, const RootRecords& roots, const Columns& cols,
+                              int64_t c0, int64_t c1, double* colldir, int* collok,
+                              DeviceScratch& ws, cudaStream_t st) {
   const int64_t nr = p.nred;
   if (nr == 0) return 0;
+  // only the roots whose columns [c0, c1) this call builds (a rank's block)
+  int* need = ws.get_i32("coll_need", nr);
+  EIGB_CUDA(cudaMemsetAsync(need, 0, 4 * nr, st));
+  if (c1 > c0) {
+    column_roots_kernel<<<(unsigned)cdiv(c1 - c0, 256), 256, 0, st>>>(cols.kind, cols.payload, c0,
+                                                                      c1, need);
+    EIGB_LAUNCH_CHECK();
+  }
   int* mark = ws.get_i32("coll_mark", nr);
   int* which = ws.get_i32("coll_which", nr);
   static int allow_multi = -1;  // EIGMOD_B200_BORDERED_MULTI=0: collided roots only (diagnostics)
@@ -977,12 +1006,13 @@ int64_t collision_vectors_dev(const Plan& p, const RootRecords& roots, double* c
                                                                 roots.delta, roots.flags, nr, mark,
                                                                 which, collok, allow_multi);
   EIGB_LAUNCH_CHECK();
-  std::vector<int> mh(nr);
+  std::vector<int> mh(nr), nh(nr);
   EIGB_CUDA(cudaMemcpyAsync(mh.data(), mark, 4 * nr, cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaMemcpyAsync(nh.data(), need, 4 * nr, cudaMemcpyDeviceToHost, st));
   EIGB_CUDA(cudaStreamSynchronize(st));
   std::vector<int64_t> list;
   for (int64_t j = 0; j < nr; ++j)
-    if (mh[j]) list.push_back(j);
+    if (mh[j] && nh[j]) list.push_back(j);
   if (list.empty()) return 0;
   int64_t* dl = ws.get_i64("coll_list", list.size());
   EIGB_CUDA(cudaMemcpyAsync(dl, list.data(), 8 * list.size(), cudaMemcpyHostToDevice, st));

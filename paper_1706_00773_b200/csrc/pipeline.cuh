@@ -67,8 +67,9 @@ void build_plan_finish(Plan& p, const double* lam, DeviceScratch& ws, cudaStream
 void merge_columns_dev(const Plan& p, const RootRecords& roots, Columns& cols, DeviceScratch& ws,
                        cudaStream_t st);
 // returns the number of collided roots
-int64_t collision_vectors_dev(const Plan& p, const RootRecords& roots, double* colldir,
-                              int* collok, DeviceScratch& ws, cudaStream_t st);
+int64_t collision_vectors_dev(const Plan& p, const RootRecords& roots, const Columns& cols,
+                              int64_t c0, int64_t c1, double* colldir, int* collok,
+                              DeviceScratch& ws, cudaStream_t st);
 void build_xt_dev(const Plan& p, const RootRecords& roots, const Columns& cols,
                   const double* colldir, const int* collok, int64_t ncollided, int64_t c0,
                   int64_t c1, double* xt, double* colscale, int* colsign_mode, DeviceScratch& ws,

@@ -1313,13 +1313,20 @@ struct WeightArgs {
   double* scratch;       // gridDim.x * 32 * 4 * KP * KP
 };
 
+// alpha_g = sum_s w_s^T adj(M_g) J w_s with M_g = I + J T_g = J S_g (S_g = J +
+// T_g symmetric, J^2 = I), so adj(M_g) J = det(M_g) S_g^-1 and alpha_g =
+// det(J) det(S_g) sum_s w_s^T S_g^-1 w_s: one Bunch-Kaufman factorization of
+// S_g (par_factor, all warps) and one solve per row of the group. Groups
+// whose pivots span more than 1e8 (the reference's switch to cofactor
+// expansion, secular.cpp:49-124) take the reference's adjugate route.
 template <int KP>
 __global__ void __launch_bounds__(kPassThreads, 1) group_weights_kernel(WeightArgs<KP> a) {
   using C = PassCfg<KP>;
   extern __shared__ __align__(16) double smem[];
-  __shared__ double dob[32], delta[32];
-  __shared__ int active[32], hit[32];
-  const int t = threadIdx.x;
+  __shared__ double dob[32], delta[32], acc[32];
+  __shared__ int active[32], hit[32], route[32];
+  __shared__ int64_t maxlen;
+  const int t = threadIdx.x, lane = t & 31;
   const int64_t g0 = (int64_t)blockIdx.x * 32;
   if (t < 32) {
     const int64_t g = g0 + t;
@@ -1333,30 +1340,102 @@ __global__ void __launch_bounds__(kPassThreads, 1) group_weights_kernel(WeightAr
   PassOpts o;
   o.exclude_zero = true;
   secular_pass<KP>(a.rep, a.u, a.n, sl, o, smem);
+  const double* red = pass_result<KP>(smem);
+  constexpr bool kSmemF = KP <= 16;
+  double* F = kSmemF ? smem + C::SMEM_DOUBLES : a.scratch + (size_t)blockIdx.x * 32 * 4 * KP * KP;
+  const size_t esl = kSmemF ? 1 : (size_t)4 * KP * KP;
+  constexpr int es = kSmemF ? 32 : 1;
+  ParSmem<KP>& P = *reinterpret_cast<ParSmem<KP>*>(smem + C::SMEM_DOUBLES + (kSmemF ? 32 * KP * KP : 0));
+  if (t < 32) {
+    P.ev[t] = active[t];
+    P.neg[t] = 0;
+    P.zero[t] = 0;
+    P.dskip[t] = 0;
+  }
+  if (t == 0) {
+    int64_t m = 0;
+    for (int b = 0; b < 32; ++b)
+      if (g0 + b < a.ng) m = (a.glen[g0 + b] > m) ? a.glen[g0 + b] : m;
+    maxlen = m;
+  }
+  __syncthreads();
+  par_load_S<KP>(red, a.sgn, a.k, F, esl, es, P);
+  __syncthreads();
+  par_factor<KP>(F, esl, es, P);
+  __syncthreads();
+  if (t < 32 && active[t]) {
+    const int b = t;
+    double det = 1.0, pmax = 0.0, pmin = INFINITY;
+    for (int k = 0; k < KP; ++k) {
+      const int bt = P.bs[k][b];
+      double pv;
+      if (bt == 0) {
+        pv = FA(k, k);
+        det *= pv;
+        pv = fabs(pv);
+      } else if (bt == 1) {
+        const double d2 = FA(k, k) * FA(k + 1, k + 1) - FA(k + 1, k) * FA(k + 1, k);
+        det *= d2;
+        pv = sqrt(fabs(d2));
+      } else {
+        continue;
+      }
+      pmax = fmax(pmax, pv);
+      pmin = fmin(pmin, pv);
+    }
+    double sj = 1.0;
+    for (int r = 0; r < a.k; ++r) sj *= (double)a.sgn[r];
+    route[b] = (!P.zero[b] && pmin > 1e-8 * pmax && isfinite(det)) ? 1 : 0;
+    P.sigma[b] = sj * det;
+    acc[b] = 0.0;
+  }
+  __syncthreads();
+  for (int64_t si = 0; si < maxlen; ++si) {
+    const int64_t g = g0 + lane;
+    const bool sel = active[lane] && route[lane] && si < a.glen[g];
+    if (t < 32 && sel) {
+      const double* w = a.u + (a.gstart[g] + si) * KP;
+      for (int c = 0; c < KP; ++c) P.z[c][t] = w[c];
+    }
+    __syncthreads();
+    par_solve<KP>(F, esl, es, P, sel);
+    __syncthreads();
+    if (t < 32 && sel) {
+      const double* w = a.u + (a.gstart[g] + si) * KP;
+      double v = 0.0;
+      for (int c = 0; c < KP; ++c) v += w[c] * P.z[c][t];
+      acc[t] += v;
+    }
+  }
+  __syncthreads();
   if (t < 32 && active[t]) {
     const int64_t g = g0 + t;
-    const int k = a.k;
-    double* M = a.scratch + ((size_t)blockIdx.x * 32 + t) * 4 * KP * KP;
-    double* adj = M + KP * KP;
-    double* work = adj + KP * KP;
-    const double* rb = pass_result<KP>(smem) + t * C::OUT;
-    // M = I + J T (proj/src/secular.cpp:176-188): row r scaled by sign r.
-    for (int r = 0; r < k; ++r)
-      for (int c = 0; c < k; ++c) {
-        const double tv = (r <= c) ? rb[C::pidx(r, c)] : rb[C::pidx(c, r)];
-        M[r * KP + c] = (r == c ? 1.0 : 0.0) + (double)a.sgn[r] * tv;
+    if (route[t]) {
+      a.alpha[g] = P.sigma[t] * acc[t];
+    } else {  // the reference's adjugate route (ill-conditioned M_g)
+      const int k = a.k;
+      double* M = a.scratch + ((size_t)blockIdx.x * 32 + t) * 4 * KP * KP;
+      double* adj = M + KP * KP;
+      double* work = adj + KP * KP;
+      const double* rb = red + t * C::OUT;
+      // M = I + J T (proj/src/secular.cpp:176-188): row r scaled by sign r.
+      for (int r = 0; r < k; ++r)
+        for (int c = 0; c < k; ++c) {
+          const double tv = (r <= c) ? rb[C::pidx(r, c)] : rb[C::pidx(c, r)];
+          M[r * KP + c] = (r == c ? 1.0 : 0.0) + (double)a.sgn[r] * tv;
+        }
+      adjugate_dev(M, k, KP, adj, work);
+      double al = 0.0;
+      for (int64_t s = a.gstart[g]; s < a.gstart[g] + a.glen[g]; ++s) {
+        const double* ws = a.u + s * KP;
+        for (int r = 0; r < k; ++r) {
+          double tt = 0.0;
+          for (int c = 0; c < k; ++c) tt += adj[r * KP + c] * (double)a.sgn[c] * ws[c];
+          al += ws[r] * tt;
+        }
       }
-    adjugate_dev(M, k, KP, adj, work);
-    double al = 0.0;
-    for (int64_t s = a.gstart[g]; s < a.gstart[g] + a.glen[g]; ++s) {
-      const double* ws = a.u + s * KP;
-      for (int r = 0; r < k; ++r) {
-        double tt = 0.0;
-        for (int c = 0; c < k; ++c) tt += adj[r * KP + c] * (double)a.sgn[c] * ws[c];
-        al += ws[r] * tt;
-      }
+      a.alpha[g] = al;
     }
-    a.alpha[g] = al;
   }
 }
 
@@ -1492,7 +1571,8 @@ void launch_weights(const double* rep, const double* u, int64_t n, const int64_t
   WeightArgs<KP> a{rep, u, n, gstart, glen, gval, ng, sgn, k, alpha, nullptr};
   const int grid = (int)cdiv(ng, 32);
   a.scratch = ws.get_f64("weights_scratch", (size_t)grid * 32 * 4 * KP * KP);
-  const size_t sm = sizeof(double) * C::SMEM_DOUBLES;
+  const size_t sm = sizeof(double) * (C::SMEM_DOUBLES + (KP <= 16 ? 32 * KP * KP : 0)) +
+                    sizeof(ParSmem<KP>);
   EIGB_CUDA(cudaFuncSetAttribute(group_weights_kernel<KP>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   group_weights_kernel<KP><<<grid, kPassThreads, sm, st>>>(a);
