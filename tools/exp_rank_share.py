@@ -62,7 +62,7 @@ for world in (1, 2, 4, 8):
         ts = t(lambda: be.solve(j0, j1, rp)) if j1 > j0 else 0.0
         c0, c1, _ = split(n, world, r)
         blk = torch.empty((n, max(c1 - c0, 1)), dtype=torch.float64, device=dev)
-        tq = t(lambda: be.finish(q, rec_all, c0, c1, lo, blk), reps=1)
+        tq = t(lambda: be.finish(q, rec_all, c0, c1, lo, blk), reps=2)
         del blk
         row = dict(project=tp, groups=tg, weights=tw, finish_plan=tf, solve=ts, finish=tq)
         row['total'] = sum(row.values())

@@ -8,7 +8,7 @@ from paper_1706_00773_b200 import capi
 from paper_1706_00773_b200.instances import make_instance_torch
 from paper_1706_00773_b200.sharded import CudaBackend, split
 dev = torch.device('cuda', 0)
-for cfg, n in [(4, 32768), (4, 16384), (2, 16384), (1, 16384)]:
+for cfg, n in [(4, 32768)] + ([(4, 16384), (2, 16384), (1, 16384)] if os.environ.get('EXP_ALL') else []):
     q, lam, kmat, signs = make_instance_torch(cfg, n=n, device=dev)
     ctx = capi.Context(0)
     ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
@@ -20,8 +20,8 @@ for cfg, n in [(4, 32768), (4, 16384), (2, 16384), (1, 16384)]:
     u = torch.zeros((n, be.kp), dtype=torch.float64, device=dev)
     be.project(q, kmat, 0, n, u)
     nred = be.plan(lam, u)
-    for world in (1, 8):
-        j0, j1, _ = split(nred, world, world // 2)
+    for world, r in ((1, 0), (8, 0), (8, 3), (8, 4), (8, 7)):
+        j0, j1, _ = split(nred, world, r)
         rec = torch.zeros((j1 - j0, be.width), dtype=torch.float64, device=dev)
         for _ in range(2):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -32,5 +32,9 @@ for cfg, n in [(4, 32768), (4, 16384), (2, 16384), (1, 16384)]:
               f"{float(rec[:, 4].sum()) / (j1 - j0):.2f} util {pr['slot_util']:.3f} share refill "
               f"{sh['refill']:.3f} pass {sh['pass']:.3f} reduce {sh['reduce']:.3f} step {sh['step']:.3f} "
               f"(load {sh['step_load']:.3f} factor {sh['step_factor']:.3f} solve {sh['step_solve']:.3f})", flush=True)
+        cyc = pr['cycles']
+        tot = sum(cyc.values())
+        print(f"    batches {pr['batches']:.0f} passes/batch {pr['passes'] / max(1, pr['batches']):.1f} "
+              f"us/pass {tot / max(1, pr['passes']) / 1965.0:.1f}", flush=True)
     ctx.close()
     del q; torch.cuda.empty_cache()

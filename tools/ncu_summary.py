@@ -12,7 +12,7 @@ def launches(path, only_ours=True):
         u = r[ui]
         v = v / 1e6 if u in ('nsecond', 'ns') else v / 1e3 if u in ('usecond', 'us') else v
         name = r[ki].split('(')[0].replace('void ', '').replace('eigb::<unnamed>::', '')
-        if only_ours and 'eigb' not in r[ki]:
+        if only_ours and 'eigb' not in r[ki] and 'unnamed>::' not in r[ki]:
             continue
         a = agg.setdefault(name, [0.0, 0]); a[0] += v; a[1] += 1
     return agg
@@ -29,14 +29,18 @@ KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'smsp__issue_active.avg.pct_of_peak_sustained_active']
 
 def full(rep):
+    """One entry per captured kernel launch of the report."""
     out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h, units, v = rows[0], rows[1], rows[-1]
-    d = {'kernel': v[h.index('Kernel Name')][:80]}
-    for k in KEYS:
-        if k in h:
-            d[k] = v[h.index(k)] + (' ' + units[h.index(k)] if units[h.index(k)] else '')
-    return d
+    h, units = rows[0], rows[1]
+    res = []
+    for v in rows[2:]:
+        d = {'kernel': v[h.index('Kernel Name')][:80]}
+        for k in KEYS:
+            if k in h:
+                d[k] = v[h.index(k)] + (' ' + units[h.index(k)] if units[h.index(k)] else '')
+        res.append(d)
+    return res
 
 if __name__ == '__main__':
     res = {}
