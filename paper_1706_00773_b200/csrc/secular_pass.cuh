@@ -189,7 +189,7 @@ __device__ __forceinline__ void pass_body(const double* __restrict__ d, const do
     const double* ta = cur + kPoleTile;
     const double* tu = cur + 2 * kPoleTile;
     // ---- D phase
-#pragma unroll 2
+#pragma unroll 8
     for (int i = warp; i < kPoleTile; i += kPassWarps) {
       const double diff = (td[i] - dob) - del;
       double D;
@@ -207,12 +207,15 @@ __device__ __forceinline__ void pass_body(const double* __restrict__ d, const do
       if (sig) {
         double tt = 0.0;
         if constexpr (KP >= 2) {
+          // two partial dot products: half the dependent DFMA chain
+          double t0 = 0.0, t1 = 0.0;
 #pragma unroll
           for (int c = 0; c < KP; c += 2) {
             const double2 v = *reinterpret_cast<const double2*>(tu + i * KP + c);
-            tt = fma(v.x, yv[c], tt);
-            tt = fma(v.y, yv[c + 1], tt);
+            t0 = fma(v.x, yv[c], t0);
+            t1 = fma(v.y, yv[c + 1], t1);
           }
+          tt = t0 + t1;
         } else {
           tt = tu[i] * yv[0];
         }

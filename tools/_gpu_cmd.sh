@@ -1,1 +1,1 @@
-for cl in 2 8; do echo "cluster=$cl"; EIGMOD_OPTS=cluster=$cl python tools/exp_solver_share.py; done > gpurun_out/share.log 2>&1
+python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; tail -3 gpurun_out/gpu_tests.log
