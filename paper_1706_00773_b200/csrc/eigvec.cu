@@ -108,7 +108,8 @@ template <int KP>
 __global__ void __launch_bounds__(kPassThreads, 1) collision_kernel(
     ReducedView rp, const int64_t* __restrict__ list, int64_t cnt, const int64_t* __restrict__ origin,
     const double* __restrict__ rdelta, const int* __restrict__ mark, const int* __restrict__ which,
-    double gap, double* __restrict__ colldir, int* __restrict__ collok, double* __restrict__ scratch) {
+    double gap, double* __restrict__ colldir, int* __restrict__ collok, double* __restrict__ scratch,
+    const double* __restrict__ yall) {
   using C = PassCfg<KP>;
   constexpr int MK = 2 * KP;
   extern __shared__ __align__(16) double smem[];
@@ -176,34 +177,49 @@ __global__ void __launch_bounds__(kPassThreads, 1) collision_kernel(
       B[(k + tt) * K1 + k + tt] = -dl;
     }
     double fro = 0.0;
-    for (int i = 0; i < K1; ++i)
-      for (int jj = 0; jj < K1; ++jj) {
-        double s = 0.0;
-        for (int l = 0; l < K1; ++l) s += B[l * K1 + i] * B[l * K1 + jj];
-        BtB[i * K1 + jj] = s;
-        fro += B[i * K1 + jj] * B[i * K1 + jj];
-      }
-    sym_evd_dev(BtB, K1, V);
-    // the which-th smallest eigenvalue of B^T B (ties by index)
+    for (int i = 0; i < K1 * K1; ++i) fro += B[i] * B[i];
     const int w = (mark[j] & 1) ? which[j] : 0;
-    int pick = -1;
-    for (int r = 0; r < K1; ++r) {
-      int below = 0;
-      for (int q = 0; q < K1; ++q)
-        if (q != r && (BtB[q * K1 + q] < BtB[r * K1 + r] ||
-                       (BtB[q * K1 + q] == BtB[r * K1 + r] && q < r)))
-          ++below;
-      if (below == w) pick = r;
-    }
-    if (pick < 0) {
-      collok[j] = 2;
-      return;
-    }
     double dir[MK];
-    double nrm = 0.0;
-    for (int r = 0; r < K1; ++r) dir[r] = V[r * K1 + pick], nrm += dir[r] * dir[r];
-    nrm = rsqrt(nrm);
-    for (int r = 0; r < K1; ++r) dir[r] *= nrm;
+    const double* yj = yall + j * KP;
+    double uy = 0.0;
+    for (int r = 0; r < k; ++r) uy += rp.u[r0 * KP + r] * yj[r];
+    if (!(mark[j] & 1) && nr == 1 && dl != 0.0 && isfinite(uy / dl)) {
+      // a root next to its pole (R = its origin row, delta != 0): the solver's
+      // null vector y of S(lambda) already solves the bordered system
+      // (z = y, xi = u_o.y / delta); the inverse iterations on B below refine it
+      double nrm = 0.0;
+      for (int r = 0; r < k; ++r) dir[r] = yj[r], nrm += dir[r] * dir[r];
+      dir[k] = uy / dl;
+      nrm += dir[k] * dir[k];
+      nrm = rsqrt(nrm);
+      for (int r = 0; r < K1; ++r) dir[r] *= nrm;
+    } else {
+      for (int i = 0; i < K1; ++i)
+        for (int jj = 0; jj < K1; ++jj) {
+          double s = 0.0;
+          for (int l = 0; l < K1; ++l) s += B[l * K1 + i] * B[l * K1 + jj];
+          BtB[i * K1 + jj] = s;
+        }
+      sym_evd_dev(BtB, K1, V);
+      // the which-th smallest eigenvalue of B^T B (ties by index)
+      int pick = -1;
+      for (int r = 0; r < K1; ++r) {
+        int below = 0;
+        for (int q = 0; q < K1; ++q)
+          if (q != r && (BtB[q * K1 + q] < BtB[r * K1 + r] ||
+                         (BtB[q * K1 + q] == BtB[r * K1 + r] && q < r)))
+            ++below;
+        if (below == w) pick = r;
+      }
+      if (pick < 0) {
+        collok[j] = 2;
+        return;
+      }
+      double nrm = 0.0;
+      for (int r = 0; r < K1; ++r) dir[r] = V[r * K1 + pick], nrm += dir[r] * dir[r];
+      nrm = rsqrt(nrm);
+      for (int r = 0; r < K1; ++r) dir[r] *= nrm;
+    }
     if (w == 0) {  // B^T B squares the conditioning: refine on B itself
       int piv[MK];
       for (int r = 0; r < K1 * K1; ++r) L[r] = B[r];
@@ -933,7 +949,7 @@ void launch_collisions(const Plan& p, const RootRecords& roots, const int64_t* l
   collision_kernel<KP><<<grid, kPassThreads, sm, st>>>(p.view(), list, cnt, roots.origin,
                                                        roots.delta, mark, which,
                                                        kPoleMergeRelGap * p.scale, colldir, collok,
-                                                       scratch);
+                                                       scratch, roots.y);
   EIGB_LAUNCH_CHECK();
 }
 
