@@ -144,11 +144,15 @@ __device__ __forceinline__ void fma_tile(const double* __restrict__ tu, const do
     } else {
       ur[0] = tu[i];
     }
+    // all row scales first: the DFMAs then never wait on the DMUL latency
+    double v[RHI - RLO];
+#pragma unroll
+    for (int r = RLO; r < RHI; ++r) v[r - RLO] = D * ur[r];
 #pragma unroll
     for (int r = RLO; r < RHI; ++r) {
-      const double v = D * ur[r];
 #pragma unroll
-      for (int c = r; c < KP; ++c) acc[C::pidx(r, c) - E0] = fma(v, ur[c], acc[C::pidx(r, c) - E0]);
+      for (int c = r; c < KP; ++c)
+        acc[C::pidx(r, c) - E0] = fma(v[r - RLO], ur[c], acc[C::pidx(r, c) - E0]);
     }
   }
 }

@@ -1,2 +1,2 @@
-python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; tail -3 gpurun_out/gpu_tests.log
-python tools/exp_xt.py > gpurun_out/xt.log 2>&1
+python tools/exp_solver_share.py 2>&1 | head -4 > gpurun_out/share.log
+python tools/exp_fpre.py 2>&1 | grep -v "Warn\|_warn" | head -8 >> gpurun_out/share.log
