@@ -51,7 +51,12 @@ int eigmod_b200_ctx_use_own_stream(eigmod_b200_ctx* ctx);
 /* Options: "timing" = 1 enables per-stage CUDA-event timing;
  * "run_rel" = near-equal-pole run threshold relative to
  * max(1,max|lambda|) used by the solve (1e-10 exact mode, the default;
- * 1e-12 = the reference's kPoleMergeRelGap, secular.hpp:66). */
+ * 1e-12 = the reference's kPoleMergeRelGap, secular.hpp:66).
+ * Solver tuning and diagnostics (defaults in secular.cuh SolveOptions):
+ * "step_tol", "max_iters", "sweep", "pole_split", "fnewton", "fpre",
+ * "fpre_min_kp", "fpre_iters", "cluster", "fexit_rel", "floor_rel",
+ * "floor_ulps", "stall_ratio", "geo_bisect", "trace_root". Unknown keys
+ * fail with a message. */
 int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value);
 const char* eigmod_b200_last_error(const eigmod_b200_ctx* ctx);
 const char* eigmod_b200_last_stage(const eigmod_b200_ctx* ctx);

@@ -1,9 +1,11 @@
 // K2 deflation weights, the count sweep and K3 batched per-root solver (sm_100a).
 //
 // K2 (proj/src/secular.cpp:168-202 group_weights): one pole pass per batch of
-//   32 pole groups evaluated at their representatives, then per group the
-//   reference's adjugate route (cofactors k <= 3, LU det*inverse, cofactor
-//   expansion fallback) on M_g = J S_g, alpha_g = sum_s w_s^T adj(M_g) J w_s.
+//   32 pole groups evaluated at their representatives; M_g = J S_g, so
+//   alpha_g = sum_s w_s^T adj(M_g) J w_s = det(J) det(S_g) sum_s w_s^T S_g^-1
+//   w_s from one Bunch-Kaufman factorization of S_g (all warps); groups whose
+//   pivots span more than 1e8 take the reference's adjugate route (cofactors
+//   k <= 3, LU det*inverse, cofactor expansion fallback).
 //
 // Count sweep (replaces the location stage, proj/src/locate.cpp:65-252 and
 //   sturm.cpp): the exact eigenvalue count #eig < x = #{d_i < x} + m -
@@ -11,6 +13,10 @@
 //   points d_a -/+ theta * gap next to every pole. Between consecutive points
 //   the counts bracket every root; a bracket that holds one root and no pole
 //   is "isolated". Two S evaluations per root locate all n roots at once.
+//
+// f presolve (k >= 16): the f-root of every isolated root from the scalar
+//   secular function alone (two-pole "middle way" model, sign-safeguarded),
+//   a start for K3 that costs ~14 flops per pole per evaluation.
 //
 // K3 (replaces rootfind.cpp:89-229, 342-377): a persistent kernel whose CTAs
 //   own 32 root slots. Each slot starts from its sweep bracket; phase A
@@ -20,9 +26,11 @@
 //   residues; a pole of f at d_o becomes a line) until |step| < 1e-6 |delta|,
 //   then Newton on psi = -delta sigma (sigma the eigenvalue of S nearest zero,
 //   from inverse iteration; sigma' = y^T S' y from the same pass) to a few ulps
-//   of delta. Every step is confined to the count-certified bracket. A
-//   converged slot writes its root record (value, origin, delta, y) and takes
-//   the next root index from a global counter.
+//   of delta. Every step is confined to the count-certified bracket. After
+//   each pass the 32 matrices S are factored and solved by all warps of the
+//   CTA (par_factor / par_solve). A converged slot writes its root record
+//   (value, origin, delta, y) and takes the next root index from a global
+//   counter.
 #include "secular.cuh"
 
 #include <cfloat>
