@@ -218,7 +218,7 @@ struct FPreArgs {
   unsigned long long* prof;  // [0] converged, [1] unconverged, [2] evaluations, [3] max
 };
 
-constexpr int kFPreWarps = 8;
+constexpr int kFPreWarps = 32;
 constexpr int kFPreTile = 1024;  // poles per shared-memory tile (d, alpha pairs)
 
 struct FPreSmem {
@@ -331,8 +331,9 @@ __device__ void fpre_step(FPreSmem& s, int b, const FPreArgs& a) {
 __global__ void __launch_bounds__(kFPreWarps * 32) fpresolve_kernel(FPreArgs a) {
   constexpr int NT = kFPreWarps * 32;
   constexpr int PER = kFPreTile / NT;  // tile entries loaded per thread
-  __shared__ FPreSmem s;
-  __shared__ double2 tile[kFPreTile];
+  extern __shared__ __align__(16) double fpre_smem[];
+  FPreSmem& s = *reinterpret_cast<FPreSmem*>(fpre_smem);
+  double2* tile = reinterpret_cast<double2*>(fpre_smem + (sizeof(FPreSmem) + 15) / 16 * 2);
   __shared__ int any;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const double* __restrict__ d = a.d;
@@ -1814,14 +1815,17 @@ void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t
     EIGB_CUDA(cudaMemsetAsync(fa.prof, 0, 4 * sizeof(unsigned long long), st));
     const unsigned long long start = (unsigned long long)j0;
     EIGB_CUDA(cudaMemcpyAsync(fa.next_root, &start, sizeof(start), cudaMemcpyHostToDevice, st));
+    const size_t fsm = (sizeof(FPreSmem) + 15) / 16 * 16 + sizeof(double2) * kFPreTile;
+    EIGB_CUDA(cudaFuncSetAttribute(fpresolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)fsm));
     int per_sm = 0;
     EIGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fpresolve_kernel,
-                                                            kFPreWarps * 32, 0));
+                                                            kFPreWarps * 32, fsm));
     // few CTAs per SM so that each refills its slots from the root queue many
     // times (iteration counts vary; a one-batch CTA runs as long as its
     // slowest root)
     const int64_t grid = std::min<int64_t>((int64_t)std::min(2, std::max(1, per_sm)) * sms, cdiv(nr, 32));
-    fpresolve_kernel<<<(unsigned)grid, kFPreWarps * 32, 0, st>>>(fa);
+    fpresolve_kernel<<<(unsigned)grid, kFPreWarps * 32, fsm, st>>>(fa);
     EIGB_LAUNCH_CHECK();
   }
 #define EIGB_SOLVE(K)                                                                          \
