@@ -115,6 +115,7 @@ struct SolveArgs {
   const int64_t* f_o;        // f presolve per root [j0, j1) (nullptr: none): origin,
   const double* f_delta;     //   delta of the f-root, state 0 none / 1 converged /
   const int* f_state;        //   2 stopped early (continue f-Newton on S)
+  const int64_t* order;      // queue position -> root (hard roots first), nullptr: identity
 };
 
 // Sweep bracket of root j: the last usable point with count <= j and the
@@ -431,6 +432,35 @@ __global__ void __launch_bounds__(kFPreWarps * 32) fpresolve_kernel(FPreArgs a) 
     if (t < 32 && s.act[t] == 1) fpre_step(s, t, a);
     __syncthreads();
   }
+}
+
+// Root queue order: the roots expected to need the most evaluations first
+// (brackets without isolation, then presolve not converged, then the rest),
+// so the last batches of a solve drain short roots (longest-first).
+__device__ __forceinline__ int root_class(const int* br_ok, const int64_t* br_pl,
+                                          const int64_t* br_ph, const int* f_state, int64_t r) {
+  if (br_ok[r] != 3 || br_pl[r] != br_ph[r]) return 0;
+  if (!f_state || f_state[r] != 1) return 1;
+  return 2;
+}
+
+__global__ void order_count_kernel(const int* __restrict__ br_ok, const int64_t* __restrict__ br_pl,
+                                   const int64_t* __restrict__ br_ph, const int* __restrict__ f_state,
+                                   int64_t nr, unsigned long long* __restrict__ cnt) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < nr) atomicAdd(cnt + root_class(br_ok, br_pl, br_ph, f_state, r), 1ull);
+}
+
+__global__ void order_scatter_kernel(const int* __restrict__ br_ok, const int64_t* __restrict__ br_pl,
+                                     const int64_t* __restrict__ br_ph, const int* __restrict__ f_state,
+                                     int64_t nr, int64_t j0, unsigned long long* __restrict__ cnt,
+                                     int64_t* __restrict__ order) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nr) return;
+  const int c = root_class(br_ok, br_pl, br_ph, f_state, r);
+  const unsigned long long base = (c == 0) ? 0ull : (c == 1 ? cnt[0] : cnt[0] + cnt[1]);
+  const unsigned long long pos = base + atomicAdd(cnt + 3 + c, 1ull);
+  order[pos] = j0 + r;
 }
 
 template <int KP>
@@ -1165,7 +1195,7 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 4 ? 2 : 1) solve_roots_ker
     if constexpr (CL == 1) {
       if (t < 32 && s.active[t] == 2) {
         const unsigned long long nj = atomicAdd(a.next_root, 1ull);
-        if ((int64_t)nj < a.j_end) slot_init<KP>(s, y, t, (int64_t)nj, a);
+        if ((int64_t)nj < a.j_end) slot_init<KP>(s, y, t, a.order ? a.order[nj - a.j0] : (int64_t)nj, a);
         else s.active[t] = 0;
       }
     } else {
@@ -1177,7 +1207,7 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 4 ? 2 : 1) solve_roots_ker
       cl.sync();
       if (t < 32 && s.active[t] == 2) {
         const unsigned long long nj = s.jnext[t];
-        if ((int64_t)nj < a.j_end) slot_init<KP>(s, y, t, (int64_t)nj, a);
+        if ((int64_t)nj < a.j_end) slot_init<KP>(s, y, t, a.order ? a.order[nj - a.j0] : (int64_t)nj, a);
         else s.active[t] = 0;
       }
     }
@@ -1510,13 +1540,15 @@ template <int KP>
 void launch_solve(const ReducedView& rp, const double* alpha, const double* br_lo,
                   const double* br_hi, const int* br_ok, const int64_t* br_pl,
                   const int64_t* br_ph, const int64_t* f_o,
-                  const double* f_delta, const int* f_state, int64_t j0, int64_t j1,
+                  const double* f_delta, const int* f_state, const int64_t* order, int64_t j0,
+                  int64_t j1,
                   const RootRecords& out, const SolveOptions& opt, DeviceScratch& ws, int sms,
                   cudaStream_t st) {
   SolveArgs<KP> a;
   a.f_o = f_o;
   a.f_delta = f_delta;
   a.f_state = f_state;
+  a.order = order;
   a.rp = rp;
   a.alpha = alpha;
   a.br_lo = br_lo;
@@ -1828,9 +1860,21 @@ void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t
     fpresolve_kernel<<<(unsigned)grid, kFPreWarps * 32, fsm, st>>>(fa);
     EIGB_LAUNCH_CHECK();
   }
-#define EIGB_SOLVE(K)                                                                          \
-  launch_solve<K>(rp, alpha, br_lo, br_hi, br_ok, br_pl, br_ph, f_o, f_delta, f_state, j0, j1, \
-                  out, opt, ws, sms, st)
+  int64_t* order = nullptr;
+  if (br_lo) {
+    const int64_t nr = j1 - j0;
+    order = ws.get_i64("root_order", nr);
+    auto* cnt = reinterpret_cast<unsigned long long*>(ws.get_i64("root_order_cnt", 6));
+    EIGB_CUDA(cudaMemsetAsync(cnt, 0, 6 * sizeof(unsigned long long), st));
+    order_count_kernel<<<(unsigned)cdiv(nr, 256), 256, 0, st>>>(br_ok, br_pl, br_ph, f_state, nr, cnt);
+    EIGB_LAUNCH_CHECK();
+    order_scatter_kernel<<<(unsigned)cdiv(nr, 256), 256, 0, st>>>(br_ok, br_pl, br_ph, f_state, nr,
+                                                                  j0, cnt, order);
+    EIGB_LAUNCH_CHECK();
+  }
+#define EIGB_SOLVE(K)                                                                      \
+  launch_solve<K>(rp, alpha, br_lo, br_hi, br_ok, br_pl, br_ph, f_o, f_delta, f_state, order, \
+                  j0, j1, out, opt, ws, sms, st)
   switch (rp.kp) {
     case 1: EIGB_SOLVE(1); break;
     case 2: EIGB_SOLVE(2); break;
