@@ -83,6 +83,7 @@ struct SolveSmem {
   int64_t pl[32], ph[32];  // pole window of the bracket: #{d <= lo}, #{d < hi}
   int active[32], hit[32], phase[32], lo_ok[32], hi_ok[32], iters[32], itersA[32], fmode[32];
   int warm[32];  // next evaluation only refreshes y (start at the f presolve's root)
+  int psi_new[32];  // the next psi step is the first after the f -> psi switch
   // a converged slot: record fields, written after the final inverse iterations
   int64_t fin_o[32];
   double fin_delta[32], fin_value[32];
@@ -477,7 +478,12 @@ __device__ void enter_phase_b_at(SolveSmem& s, int b, const SolveArgs<KP>& a, in
   s.phase[b] = 1;
   s.itersA[b] = s.iters[b];
   s.fmode[b] = fmode && (a.alpha != nullptr);
-  s.warm[b] = !s.fmode[b];
+  // the first evaluation only refreshes y (also for an unconverged presolve:
+  // an immediate switch to psi-Newton would take its first step with the
+  // sigma' of the initial y, and the must-shrink safeguard would then reject
+  // the correct second step and bisect)
+  s.warm[b] = 1;
+  s.psi_new[b] = 0;
   s.step_prev[b] = s.hi[b] - s.lo[b];
   s.delta[b] = (delta > s.lo[b] && delta < s.hi[b]) ? delta : 0.5 * (s.lo[b] + s.hi[b]);
 }
@@ -502,6 +508,7 @@ __device__ void enter_phase_b(SolveSmem& s, int b, const SolveArgs<KP>& a, doubl
   s.itersA[b] = s.iters[b];
   s.fmode[b] = (a.alpha != nullptr);
   s.warm[b] = 0;
+  s.psi_new[b] = 0;
   s.step_prev[b] = s.hi[b] - s.lo[b];
   s.delta[b] = xstart - dob;
 }
@@ -516,6 +523,7 @@ __device__ void slot_init(SolveSmem& s, double* y, int b, int64_t j, const Solve
   s.hit[b] = 0;
   s.phase[b] = 0;
   s.warm[b] = 0;
+  s.psi_new[b] = 0;
   s.active[b] = 1;
   s.dob[b] = 0.0;
   const double y0 = rsqrt((double)a.rp.k);
@@ -1057,6 +1065,7 @@ __device__ void slot_post(SolveSmem& s, ParSmem<KP>& P, double* y, int b, const 
       // the first S step corrects the error of the residues, not a
       // continuation of the f steps: do not judge it against them
       s.step_prev[b] = hi - lo;
+      s.psi_new[b] = 1;
     }
   }
   if (!s.fmode[b]) {  // Newton on psi = -delta sigma: psi' = -sigma - delta sigma'
@@ -1114,9 +1123,14 @@ __device__ void slot_post(SolveSmem& s, ParSmem<KP>& P, double* y, int b, const 
     else
       dn = 0.5 * (lo + hi);
     s.step_prev[b] = w;
+  } else if (s.psi_new[b]) {
+    // the first psi step after the switch used sigma' along the y of the
+    // previous (f-Newton) iterate: too inaccurate to judge the next one by
+    s.step_prev[b] = w;
   } else {
     s.step_prev[b] = step;
   }
+  s.psi_new[b] = 0;
   // re-origin at the pole nearest the new iterate (keeps relative accuracy
   // of delta when the root sits next to the far end of the interval)
   const int64_t pa = s.below[b] - 1, pb = s.below[b];
