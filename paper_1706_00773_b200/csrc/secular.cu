@@ -1168,8 +1168,12 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 4 ? 2 : 1) solve_roots_ker
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double smem[];
   double* y = smem + C::SMEM_DOUBLES;                      // [32][KP]
-  double* Fs = y + 32 * KP;                                // [KP*KP][32] (KP <= 16)
-  double* fullred = Fs + (kFactorInSmem<KP> ? 32 * KP * KP : 0);  // [32][OUT] (CL > 1)
+  // [KP*KP][32] (KP <= 16): overlays the pass's tiles and D buffer, which are
+  // dead while the step runs (the pass result it reads lies beyond them)
+  double* Fs = smem;
+  static_assert(!kFactorInSmem<KP> || 32 * KP * KP <= 2 * C::TILE_DOUBLES + C::DBUF_DOUBLES,
+                "factor storage must fit in the pass tiles");
+  double* fullred = y + 32 * KP;                           // [32][OUT] (CL > 1)
   SolveSmem& s = *reinterpret_cast<SolveSmem*>(fullred + (CL > 1 ? C::RED_DOUBLES : 0));
   ParSmem<KP>& P = *reinterpret_cast<ParSmem<KP>*>(reinterpret_cast<char*>(&s) + kSolveSmemPad);
   __shared__ int any;
@@ -1495,8 +1499,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) group_weights_kernel(WeightAr
 template <int KP, int CL>
 size_t solve_smem_bytes() {
   using C = PassCfg<KP>;
-  return sizeof(double) * (C::SMEM_DOUBLES + 32 * KP + (kFactorInSmem<KP> ? 32 * KP * KP : 0) +
-                           (CL > 1 ? C::RED_DOUBLES : 0)) +
+  return sizeof(double) * (C::SMEM_DOUBLES + 32 * KP + (CL > 1 ? C::RED_DOUBLES : 0)) +
          kSolveSmemPad + sizeof(ParSmem<KP>);
 }
 

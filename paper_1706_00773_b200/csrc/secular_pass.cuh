@@ -61,8 +61,10 @@ struct PassCfg {
   static constexpr int OUT = P + 3;
   static constexpr int IG = P, IF = P + 1, IFP = P + 2;
   // shared memory (doubles): tile = d, alpha, u rows
-  static constexpr int TILE_DOUBLES = kPoleTile * (KP + 2);
-  static constexpr int DBUF_DOUBLES = kPoleTile * 32;
+  // poles per tile: 128 (64 for KP = 32, whose reduction buffer is 136 KB)
+  static constexpr int T = (KP >= 32) ? kPoleTile : 2 * kPoleTile;
+  static constexpr int TILE_DOUBLES = T * (KP + 2);
+  static constexpr int DBUF_DOUBLES = T * 32;
   static constexpr int RED_DOUBLES = 32 * OUT;
   static constexpr int SMEM_DOUBLES = 2 * TILE_DOUBLES + DBUF_DOUBLES + RED_DOUBLES;
 };
@@ -93,12 +95,13 @@ __device__ __forceinline__ void load_pole_tile(double* tile, const double* __res
                                                int64_t n) {
   // tile layout: [T] d, [T] alpha, then [T][KP] rows. Rows beyond n are zero
   // with d = NaN (NaN difference => term skipped).
+  constexpr int T = PassCfg<KP>::T;
   double* td = tile;
-  double* ta = tile + kPoleTile;
-  double* tu = tile + 2 * kPoleTile;
+  double* ta = tile + T;
+  double* tu = tile + 2 * T;
   const int tid = threadIdx.x;
-  const int64_t cnt = (n - i0) < kPoleTile ? (n - i0) : kPoleTile;
-  for (int t = tid; t < kPoleTile; t += kPassThreads) {
+  const int64_t cnt = (n - i0) < T ? (n - i0) : T;
+  for (int t = tid; t < T; t += kPassThreads) {
     td[t] = (t < cnt) ? d[i0 + t] : __longlong_as_double(0x7ff8000000000000ll);
     ta[t] = (t < cnt && alpha) ? alpha[i0 + t] : 0.0;
   }
@@ -106,7 +109,7 @@ __device__ __forceinline__ void load_pole_tile(double* tile, const double* __res
     constexpr int CH = KP / 2;  // 16-byte chunks per row
     const double2* src = reinterpret_cast<const double2*>(u + i0 * KP);
     double2* dst = reinterpret_cast<double2*>(tu);
-    for (int t = tid; t < kPoleTile * CH; t += kPassThreads) {
+    for (int t = tid; t < T * CH; t += kPassThreads) {
       if (t < cnt * CH) {
         const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst + t));
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(src + t));
@@ -115,7 +118,7 @@ __device__ __forceinline__ void load_pole_tile(double* tile, const double* __res
       }
     }
   } else {
-    for (int t = tid; t < kPoleTile; t += kPassThreads) tu[t] = (t < cnt) ? u[i0 + t] : 0.0;
+    for (int t = tid; t < T; t += kPassThreads) tu[t] = (t < cnt) ? u[i0 + t] : 0.0;
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -128,7 +131,7 @@ __device__ __forceinline__ void fma_tile(const double* __restrict__ tu, const do
   using C = PassCfg<KP>;
   constexpr int RLO = C::row_lo(G), RHI = C::row_lo(G + 1);
   constexpr int E0 = C::pidx(RLO, RLO);
-  constexpr int per = kPoleTile / C::PS;
+  constexpr int per = C::T / C::PS;
 #pragma unroll 2
   for (int ii = 0; ii < per; ++ii) {
     const int i = p * per + ii;
@@ -180,7 +183,7 @@ __device__ __forceinline__ void pass_body(const double* __restrict__ d, const do
   double gs = 0.0, fs = 0.0, fps = 0.0;
   int hit = 0;
 
-  const int64_t ntiles = (n + kPoleTile - 1) / kPoleTile;
+  const int64_t ntiles = (n + C::T - 1) / C::T;
   if (ntiles > 0) load_pole_tile<KP>(tiles, d, o.alpha, u, 0, n);
   for (int64_t t = 0; t < ntiles; ++t) {
     const double* cur = tiles + (t & 1) * C::TILE_DOUBLES;
@@ -188,18 +191,18 @@ __device__ __forceinline__ void pass_body(const double* __restrict__ d, const do
     __syncthreads();  // tile t landed; previous FMA phase done with dbuf
     if (t + 1 < ntiles)
       load_pole_tile<KP>(tiles + ((t + 1) & 1) * C::TILE_DOUBLES, d, o.alpha, u,
-                         (t + 1) * kPoleTile, n);
+                         (t + 1) * C::T, n);
     const double* td = cur;
-    const double* ta = cur + kPoleTile;
-    const double* tu = cur + 2 * kPoleTile;
+    const double* ta = cur + C::T;
+    const double* tu = cur + 2 * C::T;
     // ---- D phase
 #pragma unroll 8
-    for (int i = warp; i < kPoleTile; i += kPassWarps) {
+    for (int i = warp; i < C::T; i += kPassWarps) {
       const double diff = (td[i] - dob) - del;
       double D;
       if (o.excl_gap > 0.0) {  // the bordered block: rows within excl_gap of dob, or one row
         const int64_t xr = slots.excl_row ? slots.excl_row[lane] : -1;
-        const bool ex = (xr >= 0) ? (t * kPoleTile + i == xr) : (fabs(td[i] - dob) < o.excl_gap);
+        const bool ex = (xr >= 0) ? (t * C::T + i == xr) : (fabs(td[i] - dob) < o.excl_gap);
         D = (act && !ex && diff == diff) ? rcp64(diff) : 0.0;
       } else if (diff == 0.0) {
         hit |= !o.exclude_zero;
