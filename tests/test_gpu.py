@@ -238,6 +238,45 @@ def test_deterministic(api, ctx):
     assert np.array_equal(r1.lam, r2.lam) and np.array_equal(r1.q, r2.q)
 
 
+@pytest.mark.parametrize("opts", [{"fpre": 0}, {"fpre": 1, "fpre_min_kp": 1},
+                                  {"fpre": 1, "fpre_iters": 2}, {"cluster": 1}, {"cluster": 8},
+                                  {"fnewton": 0}])
+def test_solver_variants_meet_tolerances(api, opts):
+    """The solver's optional phases (scalar f presolve, f-Newton, cluster
+    sizes) change only the path to each root: every variant meets the
+    north-star tolerances against LAPACK and agrees with the default."""
+    from paper_1706_00773_b200.instances import make_instance
+
+    q, lam, kmat, s = make_instance(4, n=640, seed=33)
+    base = api.update_decomposition(q, lam, kmat, s, 1e-12, ctx=api.Context(0))
+    c = api.Context(0)
+    for key, val in opts.items():
+        c.set_option(key, float(val))
+    r = api.update_decomposition(q, lam, kmat, s, 1e-12, ctx=c)
+    a = _aprime(q, lam, kmat, s)
+    ev = np.linalg.eigvalsh(a)
+    nrm = np.abs(ev).max()
+    assert np.abs(r.lam - ev).max() <= 1e-10 * nrm
+    assert np.abs(r.lam - base.lam).max() <= 1e-12 * nrm
+    assert np.abs(a @ r.q - r.q * r.lam).max() / nrm <= 1e-10
+    assert np.abs(r.q.T @ r.q - np.eye(len(lam))).max() <= 1e-9
+    prof = c.solver_profile()
+    assert prof["passes"] > 0 and 0.0 < prof["slot_util"] <= 1.0
+    assert abs(sum(prof["share"][k] for k in ("refill", "pass", "reduce", "step")) - 1.0) < 1e-9
+    pre = c.presolve_profile()
+    if opts.get("fpre", 1) and opts.get("fpre_min_kp", 16) <= 16 and opts.get("fnewton", 1):
+        assert pre["converged"] + pre["unconverged"] > 0
+        assert pre["max_evals"] <= opts.get("fpre_iters", 12)
+    c.close()
+
+
+def test_unknown_option_is_rejected(api):
+    c = api.Context(0)
+    with pytest.raises(ValueError):
+        c.set_option("no_such_option", 1.0)
+    c.close()
+
+
 # ----------------------------------------------- staged (multi-GPU) path
 def test_staged_path_equals_one_shot(api, ctx):
     """The root/column-partitioned data path, run as two virtual ranks on one
