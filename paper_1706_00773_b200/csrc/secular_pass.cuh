@@ -25,6 +25,8 @@
 
 #include "common.cuh"
 
+#include <utility>
+
 namespace eigb {
 
 constexpr int kPassWarps = 8;
@@ -36,22 +38,18 @@ struct PassCfg {
   static constexpr int P = KP * (KP + 1) / 2;
   static constexpr int EG = (KP <= 8) ? 1 : (KP == 16 ? 2 : 8);
   static constexpr int PS = kPassWarps / EG;
-  // Row range [row_lo(g), row_lo(g+1)) of entry group g: greedy split of the
-  // packed triangle into EG groups of about P/EG entries.
-  __host__ __device__ static constexpr int row_lo(int g) {
-    if (g <= 0) return 0;
-    if (g >= EG) return KP;
-    int acc = 0, r = 0;
-    while (r < KP && acc < (P * g + EG - 1) / EG) {
-      acc += KP - r;
-      ++r;
-    }
+  // Entry group g = packed entries [e_lo(g), e_lo(g+1)): an even split of the
+  // packed triangle (a row may straddle two groups), so no warp waits for the
+  // other group at the tile barriers.
+  __host__ __device__ static constexpr int e_lo(int g) { return (P * g) / EG; }
+  // row and column of packed entry e
+  __host__ __device__ static constexpr int row_of(int e) {
+    int r = 0;
+    while (r + 1 < KP && (r + 1) * KP - (r + 1) * r / 2 <= e) ++r;
     return r;
   }
-  __host__ __device__ static constexpr int entries(int g) {
-    int e = 0;
-    for (int r = row_lo(g); r < row_lo(g + 1); ++r) e += KP - r;
-    return e;
+  __host__ __device__ static constexpr int col_of(int e) {
+    return row_of(e) + (e - (row_of(e) * KP - row_of(e) * (row_of(e) - 1) / 2));
   }
   // packed index of (r, c), r <= c
   __host__ __device__ static constexpr int pidx(int r, int c) {
@@ -123,14 +121,28 @@ __device__ __forceinline__ void load_pole_tile(double* tile, const double* __res
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// FMA phase of entry group G on one tile (compile-time rows, so only this
+// One packed entry E of group offset E0: compile-time row and column.
+template <int KP, int E, int E0, int RLO>
+__device__ __forceinline__ void fma_entry(double* acc, const double* v, const double* ur) {
+  constexpr int r = PassCfg<KP>::row_of(E), c = PassCfg<KP>::col_of(E);
+  acc[E - E0] = fma(v[r - RLO], ur[c], acc[E - E0]);
+}
+
+template <int KP, int E0, int RLO, int... Es>
+__device__ __forceinline__ void fma_entries(double* acc, const double* v, const double* ur,
+                                            std::integer_sequence<int, Es...>) {
+  (fma_entry<KP, E0 + Es, E0, RLO>(acc, v, ur), ...);
+}
+
+// FMA phase of entry group G on one tile (compile-time entries, so only this
 // group's accumulators are live).
 template <int KP, int G>
 __device__ __forceinline__ void fma_tile(const double* __restrict__ tu, const double* __restrict__ db,
                                          int p, int lane, double* acc) {
   using C = PassCfg<KP>;
-  constexpr int RLO = C::row_lo(G), RHI = C::row_lo(G + 1);
-  constexpr int E0 = C::pidx(RLO, RLO);
+  constexpr int E0 = C::e_lo(G), E1 = C::e_lo(G + 1);
+  constexpr int RLO = C::row_of(E0), RHI = C::row_of(E1 - 1) + 1;
+  constexpr int CLO = RLO;  // v needs ur[r] of every row touched
   constexpr int per = C::T / C::PS;
 #pragma unroll 2
   for (int ii = 0; ii < per; ++ii) {
@@ -139,7 +151,7 @@ __device__ __forceinline__ void fma_tile(const double* __restrict__ tu, const do
     double ur[KP];
     if constexpr (KP >= 2) {
 #pragma unroll
-      for (int c = RLO & ~1; c < KP; c += 2) {
+      for (int c = CLO & ~1; c < KP; c += 2) {
         const double2 v = *reinterpret_cast<const double2*>(tu + i * KP + c);
         ur[c] = v.x;
         ur[c + 1] = v.y;
@@ -151,12 +163,7 @@ __device__ __forceinline__ void fma_tile(const double* __restrict__ tu, const do
     double v[RHI - RLO];
 #pragma unroll
     for (int r = RLO; r < RHI; ++r) v[r - RLO] = D * ur[r];
-#pragma unroll
-    for (int r = RLO; r < RHI; ++r) {
-#pragma unroll
-      for (int c = r; c < KP; ++c)
-        acc[C::pidx(r, c) - E0] = fma(v[r - RLO], ur[c], acc[C::pidx(r, c) - E0]);
-    }
+    fma_entries<KP, E0, RLO>(acc, v, ur, std::make_integer_sequence<int, E1 - E0>{});
   }
 }
 
@@ -165,8 +172,8 @@ __device__ __forceinline__ void pass_body(const double* __restrict__ d, const do
                                           int64_t n, const PassSlots& slots, const PassOpts& o,
                                           double* tiles, double* dbuf, double* red, int p) {
   using C = PassCfg<KP>;
-  constexpr int E = C::entries(G);
-  constexpr int E0 = C::pidx(C::row_lo(G), C::row_lo(G));
+  constexpr int E = C::e_lo(G + 1) - C::e_lo(G);
+  constexpr int E0 = C::e_lo(G);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const double dob = slots.dob[lane];

@@ -1,4 +1,2 @@
-python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
-python bench.py > gpurun_out/bench_v12.json 2> gpurun_out/bench_v12.err
-tail -c 300 gpurun_out/bench_v12.err
-python bench.py --impl reference > gpurun_out/bench_ref_v12.json 2> gpurun_out/bench_ref_v12.err; tail -c 300 gpurun_out/bench_ref_v12.err
+python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; tail -2 gpurun_out/gpu_tests.log
+EIGMOD_B200_OPTS=fpre_min_kp=1 python -m pytest tests/test_stress.py -m gpu -x -q > gpurun_out/gpu_stress_all.log 2>&1; tail -1 gpurun_out/gpu_stress_all.log
