@@ -94,11 +94,14 @@ template <int KP>
 struct SolveArgs {
   ReducedView rp;
   const double* alpha;     // residues of the reduced poles (nullptr: no f-Newton)
-  const double* br_lo;     // initial brackets of roots [j0, j1) (bracket_kernel); nullptr:
-  const double* br_hi;     //   Weyl windows
-  const int* br_ok;        // bit 0: lo certified (count == j), bit 1: hi (count == j + 1)
-  const int64_t* br_pl;    // #{d <= lo} and #{d < hi} of those brackets
-  const int64_t* br_ph;
+  double* br_lo;           // initial brackets of roots [j0, j1) (bracket_kernel); nullptr:
+  double* br_hi;           //   Weyl windows
+  int* br_ok;              // bit 0: lo certified (count == j), bit 1: hi (count == j + 1),
+                           //   bit 2: root finished (record written) by the phase-A stage
+  int64_t* br_pl;          // #{d <= lo} and #{d < hi} of those brackets
+  int64_t* br_ph;
+  int phase_a_only;        // stage 1 of a split solve: stop each root once isolated and
+  int* pa_evals;           //   store its bracket and evaluations (seed of stage 2)
   int64_t j0;
   int64_t j_end;
   unsigned long long* next_root;
@@ -440,6 +443,7 @@ __global__ void __launch_bounds__(kFPreWarps * 32) fpresolve_kernel(FPreArgs a) 
 // so the last batches of a solve drain short roots (longest-first).
 __device__ __forceinline__ int root_class(const int* br_ok, const int64_t* br_pl,
                                           const int64_t* br_ph, const int* f_state, int64_t r) {
+  if (br_ok[r] & 4) return 3;  // finished by the phase-A stage: last (skipped)
   if (br_ok[r] != 3 || br_pl[r] != br_ph[r]) return 0;
   if (!f_state || f_state[r] != 1) return 1;
   return 2;
@@ -459,8 +463,9 @@ __global__ void order_scatter_kernel(const int* __restrict__ br_ok, const int64_
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nr) return;
   const int c = root_class(br_ok, br_pl, br_ph, f_state, r);
-  const unsigned long long base = (c == 0) ? 0ull : (c == 1 ? cnt[0] : cnt[0] + cnt[1]);
-  const unsigned long long pos = base + atomicAdd(cnt + 3 + c, 1ull);
+  unsigned long long base = 0;
+  for (int q = 0; q < c; ++q) base += cnt[q];
+  const unsigned long long pos = base + atomicAdd(cnt + 4 + c, 1ull);
   order[pos] = j0 + r;
 }
 
@@ -518,8 +523,12 @@ __device__ void slot_init(SolveSmem& s, double* y, int b, int64_t j, const Solve
   const double* d = a.rp.d;
   const int64_t N = a.rp.n;
   s.j[b] = j;
-  s.iters[b] = 0;
+  s.iters[b] = a.pa_evals ? a.pa_evals[j - a.j0] : 0;  // phase-A evaluations of a split solve
   s.itersA[b] = 0;
+  if (a.br_ok && (a.br_ok[j - a.j0] & 4)) {  // finished by the phase-A stage
+    s.active[b] = 2;
+    return;
+  }
   s.hit[b] = 0;
   s.phase[b] = 0;
   s.warm[b] = 0;
@@ -562,6 +571,7 @@ __device__ void slot_finish(SolveSmem& s, const double* y, int b, const SolveArg
                             int64_t o, double delta, double value, int flags, double* ynext) {
   const int64_t j = s.j[b];
   if (a.writer) {  // cluster rank 0 (every CTA of a cluster holds the same state)
+    if (a.phase_a_only) a.br_ok[j - a.j0] |= 4;
     a.out.value[j] = value;
     a.out.origin[j] = o;
     a.out.delta[j] = delta;
@@ -1031,6 +1041,19 @@ __device__ void slot_post(SolveSmem& s, ParSmem<KP>& P, double* y, int b, const 
     }
     const double lo = s.lo[b], hi = s.hi[b];
     if (s.lo_ok[b] && s.hi_ok[b] && s.ph[b] == s.pl[b]) {
+      if (a.phase_a_only) {  // isolated: hand the bracket to the presolve and stage 2
+        if (a.writer) {
+          const int64_t r = j - a.j0;
+          a.br_lo[r] = lo;
+          a.br_hi[r] = hi;
+          a.br_ok[r] = 3;
+          a.br_pl[r] = s.pl[b];
+          a.br_ph[r] = s.ph[b];
+          a.pa_evals[r] = s.iters[b];
+        }
+        s.active[b] = 2;
+        return;
+      }
       enter_phase_b<KP>(s, b, a, 0.5 * (lo + hi));
       return;
     }
@@ -1554,14 +1577,15 @@ bool launch_solve_cluster(const SolveArgs<KP>& a, int64_t nroots, int sms, cudaS
 }
 
 template <int KP>
-void launch_solve(const ReducedView& rp, const double* alpha, const double* br_lo,
-                  const double* br_hi, const int* br_ok, const int64_t* br_pl,
-                  const int64_t* br_ph, const int64_t* f_o,
+void launch_solve(const ReducedView& rp, const double* alpha, double* br_lo, double* br_hi,
+                  int* br_ok, int64_t* br_pl, int64_t* br_ph, const int64_t* f_o,
                   const double* f_delta, const int* f_state, const int64_t* order, int64_t j0,
-                  int64_t j1,
+                  int64_t j1, int64_t q_end, int phase_a_only, int* pa_evals, bool first_stage,
                   const RootRecords& out, const SolveOptions& opt, DeviceScratch& ws, int sms,
                   cudaStream_t st) {
   SolveArgs<KP> a;
+  a.phase_a_only = phase_a_only;
+  a.pa_evals = pa_evals;
   a.f_o = f_o;
   a.f_delta = f_delta;
   a.f_state = f_state;
@@ -1574,7 +1598,7 @@ void launch_solve(const ReducedView& rp, const double* alpha, const double* br_l
   a.br_pl = br_pl;
   a.br_ph = br_ph;
   a.j0 = j0;
-  a.j_end = j1;
+  a.j_end = q_end;  // queue positions [j0, q_end) (order maps them to roots)
   a.out = out;
   a.m_neg = rp.m_neg;
   a.p_pos = rp.k - rp.m_neg;
@@ -1583,7 +1607,8 @@ void launch_solve(const ReducedView& rp, const double* alpha, const double* br_l
   a.step_tol = opt.step_tol;
   a.max_iters = opt.max_iters;
   a.writer = 1;
-  const int64_t nroots = j1 - j0;
+  const int64_t nroots = q_end - j0;
+  (void)j1;
   a.next_root = reinterpret_cast<unsigned long long*>(ws.get_i64("solve_counter", 1));
   a.prof = reinterpret_cast<unsigned long long*>(ws.get_i64("solve_prof", 12));
   a.trace_j = opt.trace_root;
@@ -1593,9 +1618,11 @@ void launch_solve(const ReducedView& rp, const double* alpha, const double* br_l
   a.stall_ratio = opt.stall_ratio;
   a.geo_bisect = opt.geo_bisect;
   a.trace = ws.get_f64("solve_trace", (size_t)kTraceRows * kTraceCols);
-  if (opt.trace_root >= 0)
-    EIGB_CUDA(cudaMemsetAsync(a.trace, 0, sizeof(double) * kTraceRows * kTraceCols, st));
-  EIGB_CUDA(cudaMemsetAsync(a.prof, 0, 12 * sizeof(unsigned long long), st));
+  if (first_stage) {  // a split solve's second stage keeps the first stage's trace and profile
+    if (opt.trace_root >= 0)
+      EIGB_CUDA(cudaMemsetAsync(a.trace, 0, sizeof(double) * kTraceRows * kTraceCols, st));
+    EIGB_CUDA(cudaMemsetAsync(a.prof, 0, 12 * sizeof(unsigned long long), st));
+  }
   const unsigned long long start = (unsigned long long)j0;
   EIGB_CUDA(cudaMemcpyAsync(a.next_root, &start, sizeof(start), cudaMemcpyHostToDevice, st));
   // Size-based choice (tools/exp_cluster.py, cfg 2/4 at n = 8192/32768):
@@ -1849,11 +1876,12 @@ void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t
     EIGB_LAUNCH_CHECK();
   }
   if (!opt.fnewton) alpha = nullptr;
+  const int64_t nr = j1 - j0;
   int64_t* f_o = nullptr;
   double* f_delta = nullptr;
   int* f_state = nullptr;
-  if (alpha && br_lo && opt.fpre && rp.kp >= opt.fpre_min_kp) {
-    const int64_t nr = j1 - j0;
+  const bool pre = alpha && br_lo && opt.fpre && rp.kp >= opt.fpre_min_kp;
+  auto run_presolve = [&]() {
     f_o = ws.get_i64("fpre_o", nr);
     f_delta = ws.get_f64("fpre_delta", nr);
     f_state = ws.get_i32("fpre_state", nr);
@@ -1876,32 +1904,53 @@ void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t
     const int64_t grid = std::min<int64_t>((int64_t)std::min(2, std::max(1, per_sm)) * sms, cdiv(nr, 32));
     fpresolve_kernel<<<(unsigned)grid, kFPreWarps * 32, fsm, st>>>(fa);
     EIGB_LAUNCH_CHECK();
-  }
+  };
   int64_t* order = nullptr;
-  if (br_lo) {
-    const int64_t nr = j1 - j0;
+  unsigned long long* cnt = nullptr;
+  auto build_order = [&]() {
     order = ws.get_i64("root_order", nr);
-    auto* cnt = reinterpret_cast<unsigned long long*>(ws.get_i64("root_order_cnt", 6));
-    EIGB_CUDA(cudaMemsetAsync(cnt, 0, 6 * sizeof(unsigned long long), st));
+    cnt = reinterpret_cast<unsigned long long*>(ws.get_i64("root_order_cnt", 8));
+    EIGB_CUDA(cudaMemsetAsync(cnt, 0, 8 * sizeof(unsigned long long), st));
     order_count_kernel<<<(unsigned)cdiv(nr, 256), 256, 0, st>>>(br_ok, br_pl, br_ph, f_state, nr, cnt);
     EIGB_LAUNCH_CHECK();
     order_scatter_kernel<<<(unsigned)cdiv(nr, 256), 256, 0, st>>>(br_ok, br_pl, br_ph, f_state, nr,
                                                                   j0, cnt, order);
     EIGB_LAUNCH_CHECK();
-  }
-#define EIGB_SOLVE(K)                                                                      \
-  launch_solve<K>(rp, alpha, br_lo, br_hi, br_ok, br_pl, br_ph, f_o, f_delta, f_state, order, \
-                  j0, j1, out, opt, ws, sms, st)
-  switch (rp.kp) {
-    case 1: EIGB_SOLVE(1); break;
-    case 2: EIGB_SOLVE(2); break;
-    case 4: EIGB_SOLVE(4); break;
-    case 8: EIGB_SOLVE(8); break;
-    case 16: EIGB_SOLVE(16); break;
-    case 32: EIGB_SOLVE(32); break;
-    default: throw Error(1, "", "solve_roots: unsupported padded rank");
-  }
+  };
+#define EIGB_SOLVE(K)                                                                          \
+  launch_solve<K>(rp, alpha, br_lo, br_hi, br_ok, br_pl, br_ph, f_o, f_delta, f_state, order,   \
+                  j0, j1, q_end, phase_a_only, pa_evals, first_stage, out, opt, ws, sms, st)
+  auto solve = [&](int64_t q_end, int phase_a_only, int* pa_evals, bool first_stage) {
+    switch (rp.kp) {
+      case 1: EIGB_SOLVE(1); break;
+      case 2: EIGB_SOLVE(2); break;
+      case 4: EIGB_SOLVE(4); break;
+      case 8: EIGB_SOLVE(8); break;
+      case 16: EIGB_SOLVE(16); break;
+      case 32: EIGB_SOLVE(32); break;
+      default: throw Error(1, "", "solve_roots: unsupported padded rank");
+    }
+  };
 #undef EIGB_SOLVE
+  if (pre && opt.split_phase_a) {
+    // stage 1: the roots whose sweep bracket holds other roots or poles are
+    // bisected on the count until isolated (their bracket is stored); then
+    // every isolated root gets the scalar presolve, and stage 2 finishes all
+    build_order();  // unisolated roots first
+    unsigned long long c0 = 0;
+    EIGB_CUDA(cudaMemcpyAsync(&c0, cnt, sizeof(c0), cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaStreamSynchronize(st));
+    int* pa_evals = ws.get_i32("pa_evals", nr);
+    EIGB_CUDA(cudaMemsetAsync(pa_evals, 0, 4 * nr, st));
+    if (c0 > 0) solve(j0 + (int64_t)c0, 1, pa_evals, true);
+    run_presolve();
+    build_order();
+    solve(j1, 0, pa_evals, c0 == 0);
+    return;
+  }
+  if (pre) run_presolve();
+  if (br_lo) build_order();
+  solve(j1, 0, nullptr, true);
 }
 
 void group_weights(int kp, const double* rep, const double* u, int64_t n, const int64_t* gstart,

@@ -97,6 +97,9 @@ struct SolveOptions {
   // 180 -> 157 ms); below that it does not pay (tools/exp_fpre.py).
   bool fpre = true;
   int fpre_min_kp = 16;
+  // with the presolve: bisect unisolated roots to isolation first (stage 1),
+  // so they get the presolve too, then finish every root (stage 2)
+  bool split_phase_a = true;
   int fpre_iters = 12;
 };
 
