@@ -624,6 +624,8 @@ struct ParSmem {
   int redi[kPassWarps][32];
   int dkp[32], dstep[32], dskip[32], neg[32], zero[32], ev[32], fin[32], ninv[32];
   double tiny[32], sigma[32];
+  double ldet[32];  // log2 |det S| of the factored matrix (warm evaluations)
+  int dsgn[32];     // its sign
 };
 
 constexpr size_t kSolveSmemPad = (sizeof(SolveSmem) + 15) / 16 * 16;
@@ -1073,7 +1075,29 @@ __device__ void slot_post(SolveSmem& s, ParSmem<KP>& P, double* y, int b, const 
   if (s.warm[b]) {
     s.warm[b] = 0;
     s.step_prev[b] = hi - lo;
-    return;  // same point again (it is now a bracket end)
+    // sigma' from the scalar secular function instead of the stale y: f =
+    // det(J) det S and sigma = det S / P with P the product of S's other
+    // eigenvalues, so sigma' = det(J) f' / P - sigma P'/P ~ det(J) f' sigma
+    // / det S (sigma is tiny at the presolved root). One psi-Newton step
+    // with it replaces a second evaluation at the same point.
+    double sj = 1.0;
+    for (int r = 0; r < a.rp.k; ++r) sj *= (double)a.rp.sgn[r];
+    if (sigma != 0.0 && isfinite(fpv) && P.ldet[b] == P.ldet[b]) {
+      const double ratio = (double)P.dsgn[b] * copysign(exp2(log2(fabs(sigma)) - P.ldet[b]), sigma);
+      const double gest = sj * fpv * ratio;
+      if (gest > 0.0 && isfinite(gest)) {
+        const double den = sigma + dl * gest;
+        const double st = (den != 0.0) ? -dl * sigma / den : NAN;
+        // (never a convergence verdict: sigma' is an estimate; the next
+        // evaluation, with the refreshed y, judges the step)
+        const double dn = dl + st;
+        if (dn > lo && dn < hi) {
+          s.delta[b] = dn;
+          s.psi_new[b] = 1;  // do not judge the next step by this estimate
+        }
+      }
+    }
+    return;  // (else the same point again, now a bracket end)
   }
   double step = NAN;
   if (s.fmode[b]) {  // Newton on g = -delta f: g' = -f - delta f'
@@ -1305,6 +1329,21 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 4 ? 2 : 1) solve_roots_ker
       P.tiny[b] = 1e-4 * DBL_EPSILON * fmax(pscale, 1e-300);
       P.sigma[b] = 0.0;
       for (int c = 0; c < KP; ++c) P.z[c][b] = y[b * KP + c];
+      if (s.warm[b]) {  // det S from the pivots (log scale: k pivots may over/underflow)
+        double l2 = 0.0;
+        int sg = 1;
+        for (int k = 0; k < KP; ++k) {
+          const int bt = P.bs[k][b];
+          double v;
+          if (bt == 0) v = FA(k, k);
+          else if (bt == 1) v = FA(k, k) * FA(k + 1, k + 1) - FA(k + 1, k) * FA(k + 1, k);
+          else continue;
+          if (v < 0.0) sg = -sg;
+          l2 += log2(fabs(v));
+        }
+        P.ldet[b] = l2;
+        P.dsgn[b] = sg;
+      }
     }
     for (int it = 0; it < 3; ++it) {  // inverse iteration: y <- S^-1 y / |.|, sigma
       const bool sel = P.ev[lane] && P.ninv[lane] > it;
