@@ -518,6 +518,8 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
       ctx->sopt.fnewton = value != 0.0;
     } else if (std::string(key) == "fpre") {
       ctx->sopt.fpre = value != 0.0;
+    } else if (std::string(key) == "sweep_poles") {
+      ctx->sopt.sweep_poles = value != 0.0;
     } else if (std::string(key) == "split_phase_a") {
       ctx->sopt.split_phase_a = value != 0.0;
     } else if (std::string(key) == "fpre_min_kp") {

@@ -130,7 +130,7 @@ __device__ __forceinline__ int comb_count(const int* counts, const int* pcounts,
   const int64_t a = q3 / 3;
   const int r = (int)(q3 - 3 * a);
   if (r == 1) return pcounts ? pcounts[a] : -1;
-  return counts[2 * a + (r == 2)];
+  return counts ? counts[2 * a + (r == 2)] : -1;
 }
 
 __device__ __forceinline__ double comb_point(const double* d, int64_t N, int64_t q3) {
@@ -1841,6 +1841,29 @@ __global__ void pole_select_kernel(const double* __restrict__ d, int64_t N, int6
   bcnt[i] = (int)(r1 - a);
 }
 
+// Every distinct pole value of [pbeg, pend) (first row of its run): the
+// pole-limit counts alone bracket the roots (sweep_poles mode).
+__global__ void pole_all_kernel(const double* __restrict__ d, int64_t N, int64_t pbeg, int64_t pend,
+                                int* __restrict__ pcounts, int64_t* __restrict__ list,
+                                double* __restrict__ bval, int64_t* __restrict__ brow,
+                                int* __restrict__ bcnt, unsigned long long* nsel) {
+  const int64_t a = pbeg + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= pend) return;
+  const double v = d[a];
+  if (a > 0 && d[a - 1] == v) return;  // one evaluation per pole value
+  const int64_t r1 = dev_n_leq(d, N, v);
+  const unsigned long long i = atomicAdd(nsel, 1ull);
+  list[i] = a;
+  bval[i] = v;
+  brow[i] = a;
+  bcnt[i] = (int)(r1 - a);
+}
+
+__global__ void fill_i32_kernel(int* __restrict__ p, int64_t n, int v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
 __global__ void pole_scatter_kernel(const int64_t* __restrict__ list, const int64_t* __restrict__ brow,
                                     const int* __restrict__ bcnt, const int* __restrict__ nu,
                                     int64_t nsel, int m_neg, int* __restrict__ pcounts) {
@@ -1850,55 +1873,12 @@ __global__ void pole_scatter_kernel(const int64_t* __restrict__ list, const int6
   for (int t = 0; t < bcnt[i]; ++t) pcounts[list[i] + t] = c;
 }
 
-}  // namespace
-
-void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t j1,
-                 const RootRecords& out, const SolveOptions& opt, DeviceScratch& ws, int sms,
-                 cudaStream_t st) {
-  if (j1 <= j0) return;
-  int* counts = nullptr;
-  // points next to the poles of every Weyl window of roots [j0, j1)
-  // (multi-GPU ranks sweep only their share)
-  const int64_t pb = std::max<int64_t>(0, j0 - rp.m_neg - 1);
-  const int64_t pe = std::min<int64_t>(rp.n, j1 + (rp.k - rp.m_neg) + 1);
-  const int64_t qbeg = 2 * pb, qend = 2 * pe;
-  if (opt.sweep) {
-    counts = ws.get_i32("sweep_counts", 2 * rp.n);
-    switch (rp.kp) {
-      case 1: launch_sweep<1>(rp, counts, qbeg, qend, ws, st); break;
-      case 2: launch_sweep<2>(rp, counts, qbeg, qend, ws, st); break;
-      case 4: launch_sweep<4>(rp, counts, qbeg, qend, ws, st); break;
-      case 8: launch_sweep<8>(rp, counts, qbeg, qend, ws, st); break;
-      case 16: launch_sweep<16>(rp, counts, qbeg, qend, ws, st); break;
-      case 32: launch_sweep<32>(rp, counts, qbeg, qend, ws, st); break;
-      default: throw Error(1, "", "solve_roots: unsupported padded rank");
-    }
-  }
-  int* pcounts = nullptr;
-  if (opt.sweep && opt.pole_split && pe > pb) {
-    pcounts = ws.get_i32("sweep_pole_counts", rp.n);
-    const int64_t np = pe - pb;
-    int64_t* list = ws.get_i64("psel_list", np);
-    double* bval = ws.get_f64("psel_val", np);
-    int64_t* brow = ws.get_i64("psel_row", np);
-    int* bcnt = ws.get_i32("psel_cnt", np);
-    int* nu = ws.get_i32("psel_nu", np);
-    auto* nsel = reinterpret_cast<unsigned long long*>(ws.get_i64("psel_n", 1));
-    EIGB_CUDA(cudaMemsetAsync(nsel, 0, 8, st));
-    pole_select_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(rp.d, rp.n, pb, pe, counts, pcounts,
-                                                                 list, bval, brow, bcnt, nsel);
-    EIGB_LAUNCH_CHECK();
-    unsigned long long nh = 0;
-    EIGB_CUDA(cudaMemcpyAsync(&nh, nsel, 8, cudaMemcpyDeviceToHost, st));
-    EIGB_CUDA(cudaStreamSynchronize(st));
-    if (nh > 0) {
-      pole_inertia(rp, bval, brow, bcnt, (int64_t)nh, nu, ws, st);
-      pole_scatter_kernel<<<(unsigned)cdiv((int64_t)nh, 256), 256, 0, st>>>(list, brow, bcnt, nu,
-                                                                           (int64_t)nh, rp.m_neg,
-                                                                           pcounts);
-      EIGB_LAUNCH_CHECK();
-    }
-  }
+// Brackets from the counts (sweep points and / or pole-limit counts), then the
+// presolve and the solver stages.
+void solve_after_counts(const ReducedView& rp, const double* alpha, int64_t j0, int64_t j1,
+                        const RootRecords& out, const SolveOptions& opt, DeviceScratch& ws,
+                        int sms, cudaStream_t st, int* counts, int* pcounts, int64_t pb,
+                        int64_t pe) {
   double *br_lo = nullptr, *br_hi = nullptr;
   int* br_ok = nullptr;
   int64_t *br_pl = nullptr, *br_ph = nullptr;
@@ -1990,6 +1970,88 @@ void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t
   if (pre) run_presolve();
   if (br_lo) build_order();
   solve(j1, 0, nullptr, true);
+}
+
+}  // namespace
+
+void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t j1,
+                 const RootRecords& out, const SolveOptions& opt, DeviceScratch& ws, int sms,
+                 cudaStream_t st) {
+  if (j1 <= j0) return;
+  int* counts = nullptr;
+  // points next to the poles of every Weyl window of roots [j0, j1)
+  // (multi-GPU ranks sweep only their share)
+  const int64_t pb = std::max<int64_t>(0, j0 - rp.m_neg - 1);
+  const int64_t pe = std::min<int64_t>(rp.n, j1 + (rp.k - rp.m_neg) + 1);
+  const int64_t qbeg = 2 * pb, qend = 2 * pe;
+  if (opt.sweep && opt.sweep_poles && pe > pb) {
+    // brackets from the pole-limit counts alone: one evaluation per distinct
+    // pole value (the projected inertia at the pole) instead of two points
+    int* pcounts = ws.get_i32("sweep_pole_counts", rp.n);
+    const int64_t np = pe - pb;
+    int64_t* list = ws.get_i64("psel_list", np);
+    double* bval = ws.get_f64("psel_val", np);
+    int64_t* brow = ws.get_i64("psel_row", np);
+    int* bcnt = ws.get_i32("psel_cnt", np);
+    int* nu = ws.get_i32("psel_nu", np);
+    auto* nsel = reinterpret_cast<unsigned long long*>(ws.get_i64("psel_n", 1));
+    EIGB_CUDA(cudaMemsetAsync(nsel, 0, 8, st));
+    fill_i32_kernel<<<(unsigned)cdiv(rp.n, 256), 256, 0, st>>>(pcounts, rp.n, -1);
+    EIGB_LAUNCH_CHECK();
+    pole_all_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(rp.d, rp.n, pb, pe, pcounts, list, bval,
+                                                              brow, bcnt, nsel);
+    EIGB_LAUNCH_CHECK();
+    unsigned long long nh = 0;
+    EIGB_CUDA(cudaMemcpyAsync(&nh, nsel, 8, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaStreamSynchronize(st));
+    if (nh > 0) {
+      pole_inertia(rp, bval, brow, bcnt, (int64_t)nh, nu, ws, st);
+      pole_scatter_kernel<<<(unsigned)cdiv((int64_t)nh, 256), 256, 0, st>>>(list, brow, bcnt, nu,
+                                                                           (int64_t)nh, rp.m_neg,
+                                                                           pcounts);
+      EIGB_LAUNCH_CHECK();
+    }
+    solve_after_counts(rp, alpha, j0, j1, out, opt, ws, sms, st, nullptr, pcounts, pb, pe);
+    return;
+  }
+  if (opt.sweep) {
+    counts = ws.get_i32("sweep_counts", 2 * rp.n);
+    switch (rp.kp) {
+      case 1: launch_sweep<1>(rp, counts, qbeg, qend, ws, st); break;
+      case 2: launch_sweep<2>(rp, counts, qbeg, qend, ws, st); break;
+      case 4: launch_sweep<4>(rp, counts, qbeg, qend, ws, st); break;
+      case 8: launch_sweep<8>(rp, counts, qbeg, qend, ws, st); break;
+      case 16: launch_sweep<16>(rp, counts, qbeg, qend, ws, st); break;
+      case 32: launch_sweep<32>(rp, counts, qbeg, qend, ws, st); break;
+      default: throw Error(1, "", "solve_roots: unsupported padded rank");
+    }
+  }
+  int* pcounts = nullptr;
+  if (opt.sweep && opt.pole_split && pe > pb) {
+    pcounts = ws.get_i32("sweep_pole_counts", rp.n);
+    const int64_t np = pe - pb;
+    int64_t* list = ws.get_i64("psel_list", np);
+    double* bval = ws.get_f64("psel_val", np);
+    int64_t* brow = ws.get_i64("psel_row", np);
+    int* bcnt = ws.get_i32("psel_cnt", np);
+    int* nu = ws.get_i32("psel_nu", np);
+    auto* nsel = reinterpret_cast<unsigned long long*>(ws.get_i64("psel_n", 1));
+    EIGB_CUDA(cudaMemsetAsync(nsel, 0, 8, st));
+    pole_select_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(rp.d, rp.n, pb, pe, counts, pcounts,
+                                                                 list, bval, brow, bcnt, nsel);
+    EIGB_LAUNCH_CHECK();
+    unsigned long long nh = 0;
+    EIGB_CUDA(cudaMemcpyAsync(&nh, nsel, 8, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaStreamSynchronize(st));
+    if (nh > 0) {
+      pole_inertia(rp, bval, brow, bcnt, (int64_t)nh, nu, ws, st);
+      pole_scatter_kernel<<<(unsigned)cdiv((int64_t)nh, 256), 256, 0, st>>>(list, brow, bcnt, nu,
+                                                                           (int64_t)nh, rp.m_neg,
+                                                                           pcounts);
+      EIGB_LAUNCH_CHECK();
+    }
+  }
+  solve_after_counts(rp, alpha, j0, j1, out, opt, ws, sms, st, counts, pcounts, pb, pe);
 }
 
 void group_weights(int kp, const double* rep, const double* u, int64_t n, const int64_t* gstart,

@@ -81,6 +81,7 @@ struct SolveOptions {
   int max_iters = 160;
   bool sweep = true;    // count sweep for the initial brackets (else Weyl windows)
   bool pole_split = true;  // limit counts at poles with roots next to them (sweep)
+  bool sweep_poles = true;  // brackets from pole-limit counts only (one evaluation per pole)
   bool fnewton = true;  // Newton on the scalar secular function first
   // CTAs per thread-block cluster splitting the pole sum: 1, 2, 4, 8, or -1
   // for the size-based choice (solve_cluster_size)
