@@ -371,16 +371,16 @@ def run_ours(args):
         # CPU secular-solver roofline (K3): algorithmic flops per S evaluation
         kp = int(stats["kp"]) or 1
         fl_eval = n * (k * (k + 1) + 1)
-        # S evaluations of the stage: the solver's (records) and the count
-        # sweep's two points per reduced pole; the scalar f presolve and the
-        # pole-limit inertias are not counted
-        ev_total = stats["evals"] + 2 * stats["roots"]
+        # S evaluations of the stage: the solver's (records) and the bracket
+        # counts, one pole-limit inertia evaluation per reduced pole value
+        # (one pole pass each); the scalar f presolve is not counted
+        ev_total = stats["evals"] + stats["roots"]
         out["roofline_k3"] = {
             "bound": "fp64", "evals": ev_total, "evals_solver": stats["evals"],
-            "evals_sweep": 2 * stats["roots"],
+            "evals_counts": stats["roots"],
             "achieved": ev_total * fl_eval / (solve_ms * 1e-3) / 1e12 if solve_ms else None,
             "peak": peaks["dfma_tflops"], "unit": "TFLOP/s",
-            "note": f"n*(k(k+1)+1) flops per S(x) evaluation (solver + count sweep), kp={kp}"}
+            "note": f"n*(k(k+1)+1) flops per S(x) evaluation (solver + one pole-limit count per pole), kp={kp}"}
         if out["roofline_k3"]["achieved"]:
             out["roofline_k3"]["frac"] = out["roofline_k3"]["achieved"] / peaks["dfma_tflops"]
     # ---- e2e at N GPUs: host inputs -> every rank copies its 1/N row slice

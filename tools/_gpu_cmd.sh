@@ -1,4 +1,6 @@
-EIGMOD_B200_OPTS=fpre_min_kp=1 python -m pytest tests/test_stress.py -m gpu -x -q > gpurun_out/gpu_stress_all.log 2>&1; tail -1 gpurun_out/gpu_stress_all.log
-EIGMOD_B200_OPTS=sweep_poles=0 python -m pytest tests/test_stress.py tests/test_locate.py -m gpu -x -q > gpurun_out/gpu_stress_old.log 2>&1; tail -1 gpurun_out/gpu_stress_old.log
-python tools/exp_rank_kernels.py 8 3 > gpurun_out/rk.log 2>&1
-python tools/exp_fpre.py 2>&1 | grep -v "Warn\|_warn" | head -8 >> gpurun_out/rk.log
+python bench.py > gpurun_out/bench_v14.json 2> gpurun_out/bench_v14.err
+tail -c 300 gpurun_out/bench_v14.err
+ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k regex:eigb --csv --log-file gpurun_out/launches_v14.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_bench_v14.log 2>&1
+echo "ncu rc=$?"
+python tools/exp_rank_share.py 4 32768 > gpurun_out/rank_share.log 2>&1
+python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; tail -1 gpurun_out/gpu_tests.log
