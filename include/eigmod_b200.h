@@ -53,7 +53,10 @@ int eigmod_b200_ctx_use_own_stream(eigmod_b200_ctx* ctx);
  * max(1,max|lambda|) used by the solve (1e-10 exact mode, the default;
  * 1e-12 = the reference's kPoleMergeRelGap, secular.hpp:66).
  * Solver tuning and diagnostics (defaults in secular.cuh SolveOptions):
- * "step_tol", "max_iters", "sweep", "pole_split", "fnewton", "fpre",
+ * "step_tol", "max_iters", "sweep" (1), "sweep_poles" (1: brackets from
+ * one pole-limit count per pole value; 0: the two-point count sweep),
+ * "pole_split" (1), "split_phase_a" (1: unisolated roots are bisected in a
+ * first solver stage before the scalar presolve), "fnewton" (1), "fpre" (1),
  * "fpre_min_kp", "fpre_iters", "cluster", "fexit_rel", "floor_rel",
  * "floor_ulps", "stall_ratio", "geo_bisect", "trace_root". Unknown keys
  * fail with a message. */

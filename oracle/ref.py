@@ -69,6 +69,11 @@ def set_parallel(on: bool) -> None:
     lib().ref_set_parallel(1 if on else 0)
 
 
+def set_threads(n: int) -> None:
+    """omp_set_num_threads for the reference's OpenMP paths."""
+    lib().ref_set_threads(int(n))
+
+
 def worker_count() -> int:
     return lib().ref_worker_count()
 
@@ -148,6 +153,27 @@ def update_pairs(q, lam, kmat, signs, tol, reorthogonalize=False):
     return lo, qo, (float(sec[0]), float(sec[1]))
 
 
+def timed_pairs(q, lam, kmat, signs, tol, vectors=True):
+    """Both stages timed separately, failures recorded:
+    dict(t_eig, t_vec, failed_stage ("" / "eigenvalues" / "eigenvectors"),
+    error, values, q_out). A failing stage's time is its time to failure."""
+    q, lam, kmat, signs = _f64(q), _f64(lam), _f64(kmat), _i32(signs)
+    n, k = kmat.shape
+    lo = np.empty(n)
+    qo = np.empty((n, n)) if vectors else None
+    out3 = np.zeros(3)
+    buf = C.create_string_buffer(1024)
+    L = lib()
+    rc = L.ref_timed_pairs(_D(q), _D(lam), _D(kmat), _I(signs), C.c_int64(n), C.c_int64(k),
+                           C.c_double(tol), _D(lo), _D(qo) if vectors else None, _D(out3), buf,
+                           1024)
+    failed = {0: "", 1: "eigenvalues", 2: "eigenvectors"}[int(out3[2])]
+    return dict(t_eig=float(out3[0]), t_vec=float(out3[1]) if vectors else None,
+                failed_stage=failed, error=buf.value.decode(errors="replace") if rc else "",
+                values=lo if rc == 0 or failed == "eigenvectors" else None,
+                q_out=qo if rc == 0 else None)
+
+
 def update_decomposition(q, lam, kmat, signs, tol, reorthogonalize=False):
     """eigvec.hpp:35-36 → (lambda', Q', residual_fro, ortho_err, wall_time)."""
     q, lam, kmat, signs = _f64(q), _f64(lam), _f64(kmat), _i32(signs)
@@ -201,6 +227,15 @@ def matrix(a):
     return _Handle(p, L.ref_matrix_free)
 
 
+def matrix_const(rows, cols, value):
+    """Persistent rows x cols eigmod::Matrix filled with value."""
+    L = lib()
+    L.ref_matrix_const.restype = C.c_void_p
+    L.ref_matrix_const.argtypes = [C.c_int64, C.c_int64, C.c_double]
+    L.ref_matrix_free.argtypes = [C.c_void_p]
+    return _Handle(L.ref_matrix_const(rows, cols, value), L.ref_matrix_free)
+
+
 def gemm_nn(h, b):
     """kernels::gemm_nn (the reference's Q X, kernels.cpp:32-48) on a handle."""
     b = _f64(b)
@@ -211,6 +246,17 @@ def gemm_nn(h, b):
     out = np.empty((b.shape[0] if rows is None else rows, b.shape[1]))
     buf = C.create_string_buffer(512)
     _check(L.ref_gemm_nn(h.ptr, _D(b), C.c_int64(b.shape[1]), _D(out), buf, 512), buf)
+    return out
+
+
+def gemm_nn_hh(ha, hb, rows, cols):
+    """kernels::gemm_nn on two persistent handles (rows x cols result)."""
+    L = lib()
+    L.ref_gemm_nn_hh.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_double), C.c_char_p,
+                                 C.c_size_t]
+    out = np.empty((rows, cols))
+    buf = C.create_string_buffer(512)
+    _check(L.ref_gemm_nn_hh(ha.ptr, hb.ptr, _D(out), buf, 512), buf)
     return out
 
 

@@ -19,6 +19,8 @@
 // Return codes follow the product C-ABI (include/eigmod_b200.h):
 // 0 ok, 1 std::invalid_argument, 2 NumericalError (stage in the message
 // buffer as "[stage] msg"), 4 any other exception.
+#include <omp.h>
+
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -125,6 +127,9 @@ extern "C" {
 
 void ref_set_parallel(int on) { kernels::set_parallel(on != 0); }
 int ref_worker_count() { return kernels::worker_count(); }
+// OpenMP team size of the reference's parallel paths (torchrun exports
+// OMP_NUM_THREADS=1 to every rank; the reference arm wants all host cores)
+void ref_set_threads(int n) { omp_set_num_threads(n > 0 ? n : 1); }
 
 int ref_random_instance(std::int64_t n, std::int64_t k, double norm, std::uint64_t seed, double* q,
                         double* lambda, double* kmat, char* msg, std::size_t len) {
@@ -312,6 +317,47 @@ int ref_update_pairs(const double* q, const double* lambda, const double* kmat, 
   });
 }
 
+// BASELINE.md §3 timing of the two stages with the failure record: out3[0]
+// seconds of update_eigenvalues_full, out3[1] of assemble_eigenvectors,
+// out3[2] the stage that threw (0 none, 1 eigenvalues, 2 eigenvectors); the
+// time of a failing stage is its time to failure. q_out may be null (the
+// eigenvalue stage only).
+int ref_timed_pairs(const double* q, const double* lambda, const double* kmat, const int* signs,
+                    std::int64_t n, std::int64_t k, double tol, double* lambda_out, double* q_out,
+                    double* out3, char* msg, std::size_t len) {
+  out3[0] = out3[1] = out3[2] = 0.0;
+  return guarded(msg, len, [&] {
+    const auto d = to_decomp(q, lambda, n);
+    const auto u = to_update(kmat, signs, n, k);
+    auto t0 = std::chrono::steady_clock::now();
+    auto since = [&] {
+      return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    };
+    std::optional<EigenvalueUpdate> plan;
+    try {
+      plan.emplace(update_eigenvalues_full(d, u, tol));
+    } catch (...) {
+      out3[0] = since();
+      out3[2] = 1.0;
+      throw;
+    }
+    out3[0] = since();
+    copy_vec(plan->values, lambda_out);
+    if (!q_out) return;
+    t0 = std::chrono::steady_clock::now();
+    try {
+      const SpectralDecomposition out = assemble_eigenvectors(d, *plan, false);
+      out3[1] = since();
+      copy_vec(out.lambda, lambda_out);
+      std::memcpy(q_out, out.q.data(), sizeof(double) * n * n);
+    } catch (...) {
+      out3[1] = since();
+      out3[2] = 2.0;
+      throw;
+    }
+  });
+}
+
 // Full update with the reference's own metrics (residual_fro, ortho_err,
 // wall_time) in metrics[0..2].
 int ref_update_decomposition(const double* q, const double* lambda, const double* kmat,
@@ -361,6 +407,11 @@ void* ref_matrix_new(const double* data, std::int64_t rows, std::int64_t cols) {
   return new Matrix(to_matrix(data, rows, cols));
 }
 void ref_matrix_free(void* h) { delete static_cast<Matrix*>(h); }
+// rows x cols filled with v (a timing operand: the i-l-j kernel's cost does
+// not depend on the values)
+void* ref_matrix_const(std::int64_t rows, std::int64_t cols, double v) {
+  return new Matrix(static_cast<std::size_t>(rows), static_cast<std::size_t>(cols), v);
+}
 
 // C = A * B with the reference's back-transform kernel (kernels.cpp:32-48,
 // called at eigvec.cpp:339). b: A.cols() x bcols, c_out: A.rows() x bcols.
@@ -370,6 +421,15 @@ int ref_gemm_nn(void* a, const double* b, std::int64_t bcols, double* c_out, cha
     const Matrix& A = *static_cast<Matrix*>(a);
     const Matrix B = to_matrix(b, static_cast<std::int64_t>(A.cols()), bcols);
     const Matrix Cm = kernels::gemm_nn(A, B);
+    std::memcpy(c_out, Cm.data(), sizeof(double) * Cm.rows() * Cm.cols());
+  });
+}
+
+// Same kernel with both operands persistent (no per-call copy of B): the
+// sampled rows of Q' = Q X against the full n x n X (bench.py).
+int ref_gemm_nn_hh(void* a, void* b, double* c_out, char* msg, std::size_t len) {
+  return guarded(msg, len, [&] {
+    const Matrix Cm = kernels::gemm_nn(*static_cast<Matrix*>(a), *static_cast<Matrix*>(b));
     std::memcpy(c_out, Cm.data(), sizeof(double) * Cm.rows() * Cm.cols());
   });
 }

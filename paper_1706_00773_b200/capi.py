@@ -484,15 +484,39 @@ def record_width(kp: int) -> int:
     return int(lib().eigmod_b200_record_width(int(kp)))
 
 
+def check_device_operands(ctx, ops):
+    """The C ABI takes raw device pointers to dense row-major float64 with
+    leading dimension = the column count: reject anything else before the
+    call (a float32, strided or wrongly sized tensor would otherwise be read
+    out of bounds or silently misinterpreted)."""
+    import torch
+
+    for name, (t, shape) in ops.items():
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{name}: expected a torch CUDA tensor")
+        if t.dtype != torch.float64:
+            raise TypeError(f"{name}: expected float64, got {t.dtype}")
+        if t.device.type != "cuda" or (t.device.index or 0) != ctx.device:
+            raise ValueError(f"{name}: expected a tensor on cuda:{ctx.device}, got {t.device}")
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name}: expected a contiguous (row-major) tensor")
+
+
 def update_decomposition_device(q, lam, kmat, signs, lam_out, q_out, ctx: Context | None = None):
     """All-device update on torch CUDA float64 tensors (runs on torch's
     current stream)."""
     import torch
 
     ctx = ctx or default_context(q.device.index or 0)
+    n, k = kmat.shape
+    check_device_operands(ctx, {"q": (q, (n, n)), "lam": (lam, (n,)), "kmat": (kmat, (n, k)),
+                                "lam_out": (lam_out, (n,)), "q_out": (q_out, (n, n))})
     ctx.set_stream(torch.cuda.current_stream(q.device).cuda_stream)
     sg = _i32(np.asarray(signs))
-    n, k = kmat.shape
+    if sg.shape != (k,):
+        raise ValueError(f"signs: expected {k} entries, got {sg.shape}")
     ctx.check(ctx._l.eigmod_b200_update_decomposition_device(
         ctx.h, _ptr(q), _ptr(lam), _ptr(kmat), sg.ctypes.data_as(_I32), n, k, _ptr(lam_out),
         _ptr(q_out)))
@@ -502,8 +526,11 @@ def gemm_nt_device(a, b, c, ctx: Context | None = None):
     import torch
 
     ctx = ctx or default_context(a.device.index or 0)
-    ctx.set_stream(torch.cuda.current_stream(a.device).cuda_stream)
     m, kk = a.shape
     nn = b.shape[0]
+    check_device_operands(ctx, {"a": (a, (m, kk)), "b": (b, (nn, kk))})
+    if c.dtype != torch.float64 or tuple(c.shape) != (m, nn) or c.stride(1) != 1:
+        raise ValueError("c: expected a float64 (m, nn) tensor with unit column stride")
+    ctx.set_stream(torch.cuda.current_stream(a.device).cuda_stream)
     ctx.check(ctx._l.eigmod_b200_gemm_nt_device(ctx.h, _ptr(a), _ptr(b), m, nn, kk, _ptr(c),
                                                  c.stride(0)))

@@ -34,7 +34,7 @@ struct eigmod_b200_ctx {
   eigb::RootRecords recs{};
   double run_rel = eigb::kExactRunRelGap;
   eigb::SolveOptions sopt;
-  const double* lam = nullptr;  // lambda of the current plan (rank-0 copy)
+  const double* lam = nullptr;  // the plan's own copy of lambda (workspace "plan_lam")
   cudaStream_t copy = nullptr;   // D2H stream of the blocked host path
   std::vector<cudaEvent_t> blk_ev;
   std::string err, stage;
@@ -150,7 +150,12 @@ void plan_groups(eigmod_b200_ctx* c, const double* lam, const double* u, const i
   eigb::Plan& p = c->plan;
   p = eigb::Plan{};
   p.run_rel = run_rel;
-  c->lam = lam;
+  // the plan keeps its own copy of lambda: the staged entry points
+  // (plan_finish, finish) must not depend on the caller's buffer staying alive
+  double* lam_copy = c->ws.get_f64("plan_lam", n);
+  EIGB_CUDA(cudaMemcpyAsync(lam_copy, lam, 8 * n, cudaMemcpyDeviceToDevice, c->stream));
+  lam = lam_copy;
+  c->lam = lam_copy;
   const int kp = eigb::padded_rank(k);
   double* norms = c->ws.get_f64("cap_norms", k);
   eigb::column_norms2_dev(u, n, kp, (int)k, norms, c->stream);
@@ -973,7 +978,7 @@ int eigmod_b200_finish_device(eigmod_b200_ctx* ctx, const double* d_q, const dou
           d_rec_all, p.nred, p.kp, ctx->recs);
       EIGB_LAUNCH_CHECK();
     }
-    // lambda is only needed for the rank-0 copy; the plan keeps no pointer to it
+    // lambda (for the rank-0 copy) comes from the plan's own copy
     ctx->mark(3);
     finish(ctx, d_q, nullptr, c0, c1, d_lambda_out, d_q_out, ldq);
     if (p.k > 0 && c1 > c0 && d_q_out) {

@@ -1827,18 +1827,20 @@ __global__ void pole_select_kernel(const double* __restrict__ d, int64_t N, int6
   const int c0 = counts[2 * a], c1 = counts[2 * a + 1];
   if (c0 >= 0 && c1 >= 0 && c0 == c1) return;
   const double v = d[a];
-  if (a > 0 && d[a - 1] == v) return;  // one evaluation per pole value
+  // one evaluation per pole value: at the first row of its run, or at pbeg
+  // when the run starts before this slice (a sharded rank)
+  if (a > pbeg && d[a - 1] == v) return;
   // simple poles with usable points are resolved by phase A bisection; the
   // limit count is needed where rows coincide (a compressed run) or a point
   // was unusable
-  const bool multi = a + 1 < N && d[a + 1] == v;
+  const bool multi = (a + 1 < N && d[a + 1] == v) || (a > 0 && d[a - 1] == v);
   if (c0 >= 0 && c1 >= 0 && !multi) return;
-  const int64_t r1 = dev_n_leq(d, N, v);
+  const int64_t r0 = dev_n_less(d, N, v), r1 = dev_n_leq(d, N, v);
   const unsigned long long i = atomicAdd(nsel, 1ull);
-  list[i] = a;
+  list[i] = a;   // first row of the slice whose count is written
   bval[i] = v;
-  brow[i] = a;
-  bcnt[i] = (int)(r1 - a);
+  brow[i] = r0;  // the whole run [r0, r1): excluded rows and #{d < v}
+  bcnt[i] = (int)(r1 - r0);
 }
 
 // Every distinct pole value of [pbeg, pend) (first row of its run): the
@@ -1850,13 +1852,15 @@ __global__ void pole_all_kernel(const double* __restrict__ d, int64_t N, int64_t
   const int64_t a = pbeg + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= pend) return;
   const double v = d[a];
-  if (a > 0 && d[a - 1] == v) return;  // one evaluation per pole value
-  const int64_t r1 = dev_n_leq(d, N, v);
+  // one evaluation per pole value: at the first row of its run, or at pbeg
+  // when the run starts before this slice (a sharded rank)
+  if (a > pbeg && d[a - 1] == v) return;
+  const int64_t r0 = dev_n_less(d, N, v), r1 = dev_n_leq(d, N, v);
   const unsigned long long i = atomicAdd(nsel, 1ull);
-  list[i] = a;
+  list[i] = a;   // first row of the slice whose count is written
   bval[i] = v;
-  brow[i] = a;
-  bcnt[i] = (int)(r1 - a);
+  brow[i] = r0;  // the whole run [r0, r1): excluded rows and #{d < v}
+  bcnt[i] = (int)(r1 - r0);
 }
 
 __global__ void fill_i32_kernel(int* __restrict__ p, int64_t n, int v) {
@@ -1870,7 +1874,7 @@ __global__ void pole_scatter_kernel(const int64_t* __restrict__ list, const int6
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nsel) return;
   const int c = (int)(brow[i] + m_neg - nu[i]);
-  for (int t = 0; t < bcnt[i]; ++t) pcounts[list[i] + t] = c;
+  for (int64_t a = list[i]; a < brow[i] + bcnt[i]; ++a) pcounts[a] = c;
 }
 
 // Brackets from the counts (sweep points and / or pole-limit counts), then the

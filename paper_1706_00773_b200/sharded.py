@@ -41,8 +41,16 @@ class CudaBackend:
         self.kp = capi.padded_rank(k)
         self.width = capi.record_width(self.kp)
 
+    @staticmethod
+    def capi_f64():
+        import torch
+
+        return torch.float64
+
     def project(self, q, kmat, lo, hi, u_out):
         c = self.ctx
+        self.capi.check_device_operands(c, {"q": (q, (self.n, self.n)),
+                                            "kmat": (kmat, (self.n, self.k))})
         c.check(c._l.eigmod_b200_project_device(c.h, C.c_void_p(q.data_ptr()),
                                                 C.c_void_p(kmat.data_ptr()), self.n, self.k, lo,
                                                 hi, C.c_void_p(u_out.data_ptr())))
@@ -83,6 +91,11 @@ class CudaBackend:
 
     def finish(self, q, rec_all, c0, c1, lam_out, q_out):
         c = self.ctx
+        self.capi.check_device_operands(c, {"q": (q, (self.n, self.n)),
+                                            "lam_out": (lam_out, (self.n,))})
+        if q_out.dtype != self.capi_f64() or q_out.shape[0] != self.n or q_out.stride(1) != 1 \
+                or q_out.shape[1] < c1 - c0:
+            raise ValueError("q_out: expected float64 (n, >= c1 - c0) with unit column stride")
         c.check(c._l.eigmod_b200_finish_device(
             c.h, C.c_void_p(q.data_ptr()), C.c_void_p(rec_all.data_ptr()), c0, c1,
             C.c_void_p(lam_out.data_ptr()), C.c_void_p(q_out.data_ptr()), q_out.stride(0)))
