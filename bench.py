@@ -224,7 +224,7 @@ def reference_config_run(cfg, n, modes=("omp", "1t"), repeats=3, long_s=20.0, se
 
 
 def reference_pair_sample(n=32768, k=16, m=8, steps=3, warmup=1, seed=11, parallel=True,
-                          rows=None):
+                          rows=None, weights=None):
     """The unmodified reference (oracle/_ref) on a bounded sample of the SAME
     workload (config 4: n = 32768, k = 16, Lambda ~ U[-100,100], alternating
     signs). Its full pipeline cannot run at this size (the locate stage throws
@@ -256,9 +256,13 @@ def reference_pair_sample(n=32768, k=16, m=8, steps=3, warmup=1, seed=11, parall
     hx = ref.matrix_const(n, n, 1.0 / np.sqrt(n))        # dense X (n x n)
     hq = ref.matrix(rng.normal(0.0, 1.0 / np.sqrt(n), (rows, n)))  # sampled rows of Q
     tu = ref.transformed(u, signs)
-    t0 = time.perf_counter()
-    alpha = ref.secular_weights(lam, u, signs)
-    t_alpha = time.perf_counter() - t0
+    if weights is None:
+        t0 = time.perf_counter()
+        alpha = ref.secular_weights(lam, u, signs)
+        t_alpha, alpha_note = time.perf_counter() - t0, "once"
+    else:  # (alpha, seconds) from another run: the weights do not depend on threading
+        alpha, t_alpha = weights
+        alpha_note = "extrapolated: the OpenMP time x threads"
     tol = 1e-12 * max(100.0, float((u * u).sum()))  # default_tolerance (rootfind.cpp:306-312)
     brackets = []  # m sample pole intervals holding exactly one root
     for a in np.linspace(n // 10, n - n // 10, 4 * m).astype(int):
@@ -290,10 +294,12 @@ def reference_pair_sample(n=32768, k=16, m=8, steps=3, warmup=1, seed=11, parall
               f"step: dnc_solve + null_problem/null_direction for {len(brackets)} eigenpairs "
               f"({tp * 1e3:.1f} ms) and {rows} rows of kernels::gemm_nn Q X against the full "
               f"n x n X ({tr:.2f} s, {gemm_gfs:.1f} GF/s; one row = one eigenpair's share of "
-              f"the n^3 GEMM), median of {steps}; + secular_weights/n ({t_alpha:.1f} s once); "
+              f"the n^3 GEMM), median of {steps}; + secular_weights/n ({t_alpha:.1f} s "
+              f"{alpha_note}); "
               f"{'OpenMP' if parallel else 'single-thread'} {cores} thread(s); upper bound "
               f"(its locate stage throws at this size)")
     return {"value": 1.0 / per_pair, "t_step": tp + tr, "cores": cores, "sample": sample,
+            "weights": (alpha, t_alpha),
             "gemm_gflops": gemm_gfs, "per_pair_ms": {"solve_vector": tp / len(brackets) * 1e3,
                                                       "gemm_row": tr / rows * 1e3,
                                                       "weights": t_alpha / n * 1e3}}
@@ -341,8 +347,9 @@ def run_reference(args):
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": r["cores"],
                                 "kind": "reference", "sample": r["sample"]}
         if args.ref_single_thread:
+            alpha, t_alpha = r["weights"]
             r1 = reference_pair_sample(n=n, k=cfg["k"], steps=1, warmup=0, parallel=False,
-                                       rows=2)
+                                       rows=2, weights=(alpha, t_alpha * r["cores"]))
             line["single_thread"] = {"value": r1["value"], "unit": UNIT,
                                      "per_pair_ms": r1["per_pair_ms"], "sample": r1["sample"]}
         try:

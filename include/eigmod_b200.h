@@ -201,6 +201,120 @@ int eigmod_b200_update_metrics(eigmod_b200_ctx* ctx, const double* q, const doub
 int eigmod_b200_gemm_nt(eigmod_b200_ctx* ctx, const double* a, const double* b, int64_t m,
                         int64_t nn, int64_t kk, double* c);
 
+/* Eigenvector stage from a finished eigenvalue stage (replaces
+ * assemble_eigenvectors, eigvec.hpp:29-31 / eigvec.cpp:254-364): the plan's
+ * roots, and its deflation record's unchanged and collided indices, with
+ * u = plan.transformed.u (n x k, kept columns) and its signs. When the plan is
+ * the one the last eigmod_b200_update_eigenvalues call on this context
+ * produced (same lambda, U, signs and eigenvalues), its device plan and root
+ * records are reused: only K4 + K5 run (*path_out = 1). Any other plan: the
+ * secular equation of u is solved on the device and the plan is accepted
+ * only if its n eigenvalues are those (NumericalError "assemble" otherwise;
+ * *path_out = 2). nroots + nunchanged + ncollided must be n
+ * (NumericalError "assemble", "eigenpair count mismatch", as eigvec.cpp:277). */
+int eigmod_b200_assemble(eigmod_b200_ctx* ctx, const double* q, const double* lambda,
+                         const double* u, const int* signs, int64_t n, int64_t k,
+                         const double* roots, int64_t nroots, const int64_t* unchanged,
+                         int64_t nunchanged, const int64_t* collided, int64_t ncollided,
+                         double* lambda_out, double* q_out, int* path_out);
+/* Stage launches on this context since creation: out4[0] K1 projections,
+ * [1] K2 plans, [2] K3 root solves, [3] K4 + K5 column builds. */
+int eigmod_b200_stage_calls(const eigmod_b200_ctx* ctx, int64_t* out4);
+
+/* ---- single eigenpairs and the secular function ---------------------- */
+/* I_k + J U^T (Lambda - lambda_new I)^{-1} U (replaces null_problem,
+ * eigvec.hpp:19 / eigvec.cpp:187-202); u n x k, m_out k x k row-major.
+ * invalid argument when lambda_new equals an old eigenvalue. */
+int eigmod_b200_null_problem(eigmod_b200_ctx* ctx, const double* u, const int* signs,
+                             const double* lambda, int64_t n, int64_t k, double lambda_new,
+                             double* m_out);
+/* Smallest singular direction of a k x k matrix (replaces null_direction,
+ * eigvec.hpp:15 / eigvec.cpp:157-185): unit dir_out (k) and ||m dir||_2.
+ * Host k x k algebra (no context). */
+int eigmod_b200_null_direction(const double* m, int64_t k, double* dir_out, double* resid_out);
+/* One updated eigenvector (replaces update_eigenvector, eigvec.hpp:25 /
+ * eigvec.cpp:204-252): v_out (n) = Q (Lambda - lambda' I)^{-1} U a0,
+ * normalized, largest-magnitude entry positive; on an old eigenvalue
+ * (within 1e-12 max(1,|lambda|)) the old vector, or the bordered-system
+ * vector when its row still couples. NumericalError "eigvec" when lambda_new
+ * is not an updated eigenvalue. */
+int eigmod_b200_update_eigenvector(eigmod_b200_ctx* ctx, const double* q, const double* lambda,
+                                   const double* kmat, const int* signs, int64_t n, int64_t k,
+                                   double lambda_new, double* v_out);
+/* f(x) = leading - sum_j w_j / (x - p_j) (and f' when fp_out != NULL) at
+ * npts points, in the reference's summation order and rounding
+ * (eval_secular / eval_secular_derivative, secular.hpp:44-47); hit_out[i]
+ * = 1 where x_i is within 1e-300 of a pole (the reference throws there). */
+int eigmod_b200_secular_eval(eigmod_b200_ctx* ctx, const double* poles, const double* weights,
+                             int64_t m, double leading, const double* xs, int64_t npts,
+                             double* f_out, double* fp_out, int* hit_out);
+/* Sign crossings of f over `samples` equidistant cells of (lo, hi)
+ * (replaces crossing_count, secular.hpp:48 / secular.cpp:245-264; same
+ * points, same skipping of poles and zeros, bit-identical f). */
+int eigmod_b200_crossing_count(eigmod_b200_ctx* ctx, const double* poles, const double* weights,
+                               int64_t m, double leading, double lo, double hi, int samples,
+                               int64_t* count_out);
+/* The roots of f in (lo, hi), `expected` of them, ascending (replaces
+ * dnc_solve, rootfind.hpp:28 / rootfind.cpp:89-229): the reference's
+ * 8-point subdivision with Lipschitz pruning and tangency rule, each
+ * round's evaluations batched on the device; sign-change brackets refined
+ * by 32-section to tol and Newton-polished. roots_out capacity `expected`;
+ * evals_out / rounds_out (may be NULL) = DncStats. NumericalError
+ * "rootfind" when fewer roots resolve or the 2^22 evaluation budget runs
+ * out. */
+int eigmod_b200_dnc_solve(eigmod_b200_ctx* ctx, const double* poles, const double* weights,
+                          int64_t m, double leading, double lo, double hi, int64_t expected,
+                          double tol, double* roots_out, int64_t* nroots_out, int64_t* evals_out,
+                          int64_t* rounds_out);
+/* Eigenvalues of diag(poles) + sigma zeta zeta^T, n ascending (replaces
+ * solve_rank1, rootfind.hpp:33 / rootfind.cpp:231-304) on the batched
+ * solver (U = zeta sqrt|sigma|, J = sign sigma). */
+int eigmod_b200_solve_rank1(eigmod_b200_ctx* ctx, const double* poles, const double* zeta,
+                            int64_t n, double sigma, double tol, double* roots_out);
+/* Root counts of f per interval of its m poles, counts_out (m + 1)
+ * (replaces locate_rank2 / locate_rank_k, locate.hpp:31,50, which take
+ * only the secular coefficients): sign changes of f sampled on the device
+ * are lower bounds per interval; f prod (x - p_j) has degree m, so counts
+ * summing to m are exact. NumericalError "locate" ("root accounting
+ * incomplete") when the sampling cannot account for every root. */
+int eigmod_b200_locate_coeffs(eigmod_b200_ctx* ctx, const double* poles, const double* weights,
+                              int64_t m, double leading, int64_t* counts_out);
+/* C (m x nn) = op(A) op(B) on the DMMA GEMM, row-major host buffers
+ * (replaces kernels::gemm_nn / gemm_tn / gemm_nt, kernels.hpp:19-21:
+ * trans_a / trans_b = 0 or 1). */
+int eigmod_b200_gemm(eigmod_b200_ctx* ctx, int trans_a, int trans_b, const double* a,
+                     const double* b, int64_t m, int64_t nn, int64_t kk, double* c);
+
+/* ---- multi-GPU context (one process, several devices, NCCL) ----------- */
+/* One context, stream and host thread per device and one NCCL communicator
+ * per device (ncclCommInitAll; NCCL loaded at run time). devices must be
+ * distinct. Each update: Q's row slices H2D on every device's own link and
+ * all-gathered over NVLink, U / alpha / root records all-gathered, roots and
+ * Q' column blocks partitioned; results equal the
+ * single-device entry points up to rounding (bit-identical for one device). */
+typedef struct eigmod_b200_multi eigmod_b200_multi;
+int eigmod_b200_multi_create(const int* devices, int ndev, eigmod_b200_multi** out);
+void eigmod_b200_multi_destroy(eigmod_b200_multi* mg);
+int eigmod_b200_multi_size(const eigmod_b200_multi* mg);
+const char* eigmod_b200_multi_last_error(const eigmod_b200_multi* mg);
+const char* eigmod_b200_multi_last_stage(const eigmod_b200_multi* mg);
+/* set_option on every device context */
+int eigmod_b200_multi_set_option(eigmod_b200_multi* mg, const char* key, double value);
+/* update_decomposition (eigvec.hpp:35-36) across the devices */
+int eigmod_b200_multi_update_decomposition(eigmod_b200_multi* mg, const double* q,
+                                           const double* lambda, const double* kmat,
+                                           const int* signs, int64_t n, int64_t k, double tol,
+                                           double* lambda_out, double* q_out,
+                                           double* wall_time_out);
+/* the eigenvalue stage (rootfind.hpp:51-53) across the devices */
+int eigmod_b200_multi_update_eigenvalues(eigmod_b200_multi* mg, const double* q,
+                                         const double* lambda, const double* kmat,
+                                         const int* signs, int64_t n, int64_t k, double tol,
+                                         double* values_out);
+/* The partition of [0, n) used for rows, roots, groups and columns:
+ * rank r of `world` owns [lo, hi) (equal chunks of ceil(n / world)). */
+int eigmod_b200_split(int64_t n, int world, int rank, int64_t* lo_out, int64_t* hi_out);
+
 /* ---- device-pointer pipeline ----------------------------------------- */
 /* Whole update on device buffers (one GPU). */
 int eigmod_b200_update_decomposition_device(eigmod_b200_ctx* ctx, const double* d_q,

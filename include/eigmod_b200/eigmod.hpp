@@ -99,6 +99,14 @@ void validate_update(const SpectralDecomposition& d, const LowRankUpdate& u);
 SymmetricDense reconstruct(const SpectralDecomposition& d);
 SymmetricDense apply_update(const SymmetricDense& a, const LowRankUpdate& u);
 
+// secular.hpp:9-17
+struct SecularCoefficients {
+  Vec poles;
+  Vec weights;
+  double leading = 1.0;
+  std::size_t size() const { return poles.size(); }
+};
+
 // locate.hpp:13-24 — root counts per interval cut by the deflated poles.
 struct LocationVector {
   std::vector<long> counts;
@@ -114,19 +122,23 @@ ShiftKind classify_shift(const std::vector<int>& signs);
 // locate.hpp:33-39
 std::pair<double, double> interlacing_bounds(std::size_t index, const Vec& lambda,
                                              std::size_t rank, const std::vector<int>& signs);
+// locate.hpp:31 / 41-50 — counts from the secular coefficients alone (GPU:
+// sampled sign changes certified by their sum, include/eigmod_b200.h
+// eigmod_b200_locate_coeffs); the rank-2 shift kind and the rank-k signature
+// select the reference's scan strategy and do not change the counts.
+LocationVector locate_rank2(const SecularCoefficients& c0, ShiftKind kind);
+struct LocateResult {
+  LocationVector loc;
+  Vec roots;  // filled when solved (never: the counts are exact)
+  bool solved = false;
+};
+LocateResult locate_rank_k(const SecularCoefficients& c0, const std::vector<int>& signs);
 // The CLI locate path (tools/eigmod.cpp:143-161: transform_update ->
 // deflate_problem -> locate_rank2 / locate_rank_k) on the GPU. The reference's
 // locate_rank2 / locate_rank_k take only the merged scalar coefficients; the
 // GPU counts from U (exact inertia at the poles), so its entry takes the update.
 LocationVector locate_update(const SpectralDecomposition& d, const LowRankUpdate& u);
 
-// secular.hpp:9-17
-struct SecularCoefficients {
-  Vec poles;
-  Vec weights;
-  double leading = 1.0;
-  std::size_t size() const { return poles.size(); }
-};
 SecularCoefficients make_secular(Vec poles, Vec weights, double leading = 1.0);
 
 // secular.hpp:19-28
@@ -143,6 +155,9 @@ Vec secular_weights(const Vec& lambda, const TransformedUpdate& tu);
 SecularCoefficients secular_coefficients(const Vec& lambda, const TransformedUpdate& tu);
 double eval_secular(const SecularCoefficients& c, double x);
 double eval_secular_derivative(const SecularCoefficients& c, double x);
+// secular.hpp:48 — sign crossings over `samples` equidistant cells (GPU,
+// bit-identical f)
+long crossing_count(const SecularCoefficients& c, double lo, double hi, int samples);
 std::pair<Vec, Vec> rank2_split(const Vec& a, const Vec& b);
 
 // secular.hpp:59-69
@@ -155,6 +170,21 @@ struct DeflatedProblem {
 inline constexpr double kPoleMergeRelGap = 1e-12;
 inline constexpr double kWeightDeflationRel = 1e-14;
 DeflatedProblem deflate_problem(const Vec& lambda, const TransformedUpdate& tu);
+
+// rootfind.hpp:8-33 — bracket solver and rank-1 fast path (GPU)
+struct RootBracket {
+  double lo = 0.0;
+  double hi = 0.0;
+  long expected = 1;
+};
+struct DncStats {
+  std::size_t evaluations = 0;
+  std::size_t rounds = 0;
+};
+inline constexpr int kDncPoints = 8;
+Vec dnc_solve(const SecularCoefficients& c, const RootBracket& b, double tol,
+              DncStats* stats = nullptr);
+Vec solve_rank1(const Vec& poles, const Vec& zeta, double sigma, double tol);
 
 // rootfind.hpp:37-58
 double default_tolerance(const Vec& lambda, const LowRankUpdate& u);
@@ -171,6 +201,16 @@ EigenvalueUpdate update_eigenvalues_full(const SpectralDecomposition& d, const L
                                          double tol,
                                          LocateStrategy strategy = LocateStrategy::automatic);
 Vec update_eigenvalues(const SpectralDecomposition& d, const LowRankUpdate& u, double tol);
+
+// eigvec.hpp:9-25 — single eigenpairs (GPU resolvent sums and
+// back-transform; the k x k null direction on the host)
+struct NullDirection {
+  Vec direction;
+  double residual;
+};
+NullDirection null_direction(const Matrix& m);
+Matrix null_problem(const TransformedUpdate& tu, const Vec& lambda, double lambda_new);
+Vec update_eigenvector(const SpectralDecomposition& d, const LowRankUpdate& u, double lambda_new);
 
 // eigvec.hpp:29-36. reorthogonalize is accepted for compatibility: the
 // vectors are orthonormal to ~1e-11 without it.
@@ -199,11 +239,42 @@ std::vector<int> parse_signs(const std::string& text);
 
 // kernels.hpp:9-13 — the OpenMP toggle has no meaning on the GPU path.
 namespace kernels {
-// kernels.hpp:36 — max |A^T A - I| (GPU DMMA GEMM)
-double ortho_error(const Matrix& a);
 void set_parallel(bool on);
 bool parallel();
 int worker_count();
+// kernels.hpp:19-23 — GEMMs on the GPU DMMA path
+Matrix gemm_nn(const Matrix& a, const Matrix& b);
+Matrix gemm_tn(const Matrix& a, const Matrix& b);
+Matrix gemm_nt(const Matrix& a, const Matrix& b);
+Vec gemv_t(const Matrix& a, const Vec& x);
+// kernels.hpp:26-37 — Q diag(lambda) Q^T (GPU), and O(n^2) host helpers
+Matrix reconstruct_symmetric(const Matrix& q, const Vec& lambda);
+void rank1_accumulate(Matrix& a, const Vec& v, double coeff);
+void symmetrize(Matrix& a);
+double frobenius_norm(const Matrix& a);
+double max_abs(const Matrix& a);
+// kernels.hpp:36 — max |A^T A - I| (GPU DMMA GEMM)
+double ortho_error(const Matrix& a);
+// kernels.hpp:39-50 — the reference's plain serial i-j-k loops (kept
+// independent of the GPU kernels above, for tests that compare the two)
+namespace ref {
+Matrix gemm_nn(const Matrix& a, const Matrix& b);
+Matrix gemm_tn(const Matrix& a, const Matrix& b);
+Matrix gemm_nt(const Matrix& a, const Matrix& b);
+Matrix reconstruct_symmetric(const Matrix& q, const Vec& lambda);
+}  // namespace ref
 }  // namespace kernels
+
+// Multi-GPU (extension): route update_decomposition and
+// update_eigenvalues of this process through one NCCL context over these
+// devices (include/eigmod_b200.h eigmod_b200_multi_*). An empty list returns
+// to one device. The environment variable EIGMOD_B200_DEVICES ("0,1,2,3")
+// sets the initial list.
+void set_devices(const std::vector<int>& devices);
+std::vector<int> devices();
+// Diagnostics (extension): stage launches on this thread's device context
+// since it was created: {K1 projections, K2 plans, K3 root solves, K4 + K5
+// column builds} (include/eigmod_b200.h eigmod_b200_stage_calls).
+std::vector<long long> stage_calls();
 
 }  // namespace eigmod

@@ -395,3 +395,60 @@ def read_matrix_market(path):
     a = np.empty((int(n[0]), int(n[0])))
     _io_check(lib().ref_read_mm(str(path).encode(), _L(n), _D(a), buf, C.c_size_t(1024)), buf)
     return a
+
+
+def locate_coeffs(poles, weights, signs):
+    """locate_rank2 (two signs) / locate_rank_k on given coefficients."""
+    poles, weights, signs = _f64(poles), _f64(weights), _i32(signs)
+    out = np.zeros(len(poles) + 1, np.int64)
+    buf = C.create_string_buffer(1024)
+    _check(lib().ref_locate_coeffs(_D(poles), _D(weights), C.c_int64(len(poles)), _I(signs),
+                                   C.c_int64(len(signs)), _L(out), buf, 1024), buf)
+    return [int(x) for x in out]
+
+
+def crossing_count(poles, weights, lo, hi, samples):
+    poles, weights = _f64(poles), _f64(weights)
+    out = np.zeros(1, np.int64)
+    buf = C.create_string_buffer(512)
+    _check(lib().ref_crossing_count(_D(poles), _D(weights), C.c_int64(len(poles)), C.c_double(lo),
+                                    C.c_double(hi), C.c_int(samples), _L(out), buf, 512), buf)
+    return int(out[0])
+
+
+def solve_rank1(poles, zeta, sigma, tol):
+    poles, zeta = _f64(poles), _f64(zeta)
+    out = np.empty(len(poles))
+    buf = C.create_string_buffer(512)
+    _check(lib().ref_solve_rank1(_D(poles), _D(zeta), C.c_int64(len(poles)), C.c_double(sigma),
+                                 C.c_double(tol), _D(out), buf, 512), buf)
+    return out
+
+
+def null_problem(u, signs, lam, lam_new):
+    u, signs, lam = _f64(u), _i32(signs), _f64(lam)
+    n, k = u.shape
+    m = np.empty((k, k))
+    buf = C.create_string_buffer(512)
+    _check(lib().ref_null_problem(_D(u), _I(signs), _D(lam), C.c_int64(n), C.c_int64(k),
+                                  C.c_double(lam_new), _D(m), buf, 512), buf)
+    return m
+
+
+def null_direction(m):
+    m = _f64(m)
+    k = m.shape[0]
+    d, r = np.empty(k), np.zeros(1)
+    buf = C.create_string_buffer(512)
+    _check(lib().ref_null_direction(_D(m), C.c_int64(k), _D(d), _D(r), buf, 512), buf)
+    return d, float(r[0])
+
+
+def update_eigenvector(q, lam, kmat, signs, lam_new):
+    q, lam, kmat, signs = _f64(q), _f64(lam), _f64(kmat), _i32(signs)
+    n, k = kmat.shape
+    v = np.empty(n)
+    buf = C.create_string_buffer(512)
+    _check(lib().ref_update_eigenvector(_D(q), _D(lam), _D(kmat), _I(signs), C.c_int64(n),
+                                        C.c_int64(k), C.c_double(lam_new), _D(v), buf, 512), buf)
+    return v

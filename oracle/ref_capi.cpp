@@ -202,6 +202,63 @@ int ref_locate_from_u(const double* lambda, const double* u, const int* signs, s
   });
 }
 
+// locate_rank2 / locate_rank_k (locate.hpp:31,50) on given coefficients
+// (rank2 when signs has two entries, with classify_shift).
+int ref_locate_coeffs(const double* poles, const double* weights, std::int64_t m,
+                      const int* signs, std::int64_t k, std::int64_t* counts_out, char* msg,
+                      std::size_t len) {
+  return guarded(msg, len, [&] {
+    const SecularCoefficients c = make_secular(Vec(poles, poles + m), Vec(weights, weights + m));
+    const std::vector<int> sg(signs, signs + k);
+    const LocationVector loc = k == 2 ? locate_rank2(c, classify_shift(sg)) : locate_rank_k(c, sg).loc;
+    for (std::size_t i = 0; i < loc.counts.size(); ++i) counts_out[i] = loc.counts[i];
+  });
+}
+
+// crossing_count (secular.hpp:48), solve_rank1 (rootfind.hpp:33),
+// null_problem / null_direction / update_eigenvector (eigvec.hpp:15-26).
+int ref_crossing_count(const double* poles, const double* weights, std::int64_t m, double lo,
+                       double hi, int samples, std::int64_t* out, char* msg, std::size_t len) {
+  return guarded(msg, len, [&] {
+    const SecularCoefficients c = make_secular(Vec(poles, poles + m), Vec(weights, weights + m));
+    *out = crossing_count(c, lo, hi, samples);
+  });
+}
+
+int ref_solve_rank1(const double* poles, const double* zeta, std::int64_t n, double sigma,
+                    double tol, double* roots_out, char* msg, std::size_t len) {
+  return guarded(msg, len, [&] {
+    copy_vec(solve_rank1(Vec(poles, poles + n), Vec(zeta, zeta + n), sigma, tol), roots_out);
+  });
+}
+
+int ref_null_problem(const double* u, const int* signs, const double* lambda, std::int64_t n,
+                     std::int64_t k, double lambda_new, double* m_out, char* msg,
+                     std::size_t len) {
+  return guarded(msg, len, [&] {
+    const Matrix m = null_problem(to_tu(u, signs, n, k), Vec(lambda, lambda + n), lambda_new);
+    std::memcpy(m_out, m.data(), sizeof(double) * k * k);
+  });
+}
+
+int ref_null_direction(const double* m, std::int64_t k, double* dir_out, double* resid_out,
+                       char* msg, std::size_t len) {
+  return guarded(msg, len, [&] {
+    const NullDirection nd = null_direction(to_matrix(m, k, k));
+    copy_vec(nd.direction, dir_out);
+    *resid_out = nd.residual;
+  });
+}
+
+int ref_update_eigenvector(const double* q, const double* lambda, const double* kmat,
+                           const int* signs, std::int64_t n, std::int64_t k, double lambda_new,
+                           double* v_out, char* msg, std::size_t len) {
+  return guarded(msg, len, [&] {
+    copy_vec(update_eigenvector(to_decomp(q, lambda, n), to_update(kmat, signs, n, k), lambda_new),
+             v_out);
+  });
+}
+
 // core.hpp:11 reconstruct (Q diag(lambda) Q^T, symmetrized) and core.hpp:14
 // apply_update (a + sum_r s_r k_r k_r^T, symmetrized); kernels.hpp:36
 // ortho_error (max |A^T A - I|).

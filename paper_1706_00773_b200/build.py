@@ -20,7 +20,8 @@ OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "lib")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["secular.cu", "deflate.cu", "eigvec.cu", "gemm.cu", "metrics.cu", "capi.cu"]
+CU_SOURCES = ["secular.cu", "deflate.cu", "eigvec.cu", "gemm.cu", "metrics.cu", "capi.cu",
+              "eigpair.cu", "multi.cu"]
 CXX_SOURCES = ["eigmod_api.cpp", "io.cpp"]
 NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-O3",
            "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]

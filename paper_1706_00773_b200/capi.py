@@ -106,6 +106,38 @@ def _declare(lib):
                                                 C.c_int64]),
         "eigmod_b200_gemm_nt_device": (C.c_int, [_VP, _VP, _VP, C.c_int64, C.c_int64, C.c_int64,
                                                  _VP, C.c_int64]),
+        "eigmod_b200_assemble": (C.c_int, [_VP, _D, _D, _D, _I32, C.c_int64, C.c_int64, _D,
+                                           C.c_int64, _I64, C.c_int64, _I64, C.c_int64, _D, _D,
+                                           _I32]),
+        "eigmod_b200_stage_calls": (C.c_int, [_VP, _I64]),
+        "eigmod_b200_null_problem": (C.c_int, [_VP, _D, _I32, _D, C.c_int64, C.c_int64,
+                                               C.c_double, _D]),
+        "eigmod_b200_null_direction": (C.c_int, [_D, C.c_int64, _D, _D]),
+        "eigmod_b200_update_eigenvector": (C.c_int, [_VP, _D, _D, _D, _I32, C.c_int64, C.c_int64,
+                                                     C.c_double, _D]),
+        "eigmod_b200_secular_eval": (C.c_int, [_VP, _D, _D, C.c_int64, C.c_double, _D, C.c_int64,
+                                               _D, _D, _I32]),
+        "eigmod_b200_crossing_count": (C.c_int, [_VP, _D, _D, C.c_int64, C.c_double, C.c_double,
+                                                 C.c_double, C.c_int, _I64]),
+        "eigmod_b200_dnc_solve": (C.c_int, [_VP, _D, _D, C.c_int64, C.c_double, C.c_double,
+                                            C.c_double, C.c_int64, C.c_double, _D, _I64, _I64,
+                                            _I64]),
+        "eigmod_b200_solve_rank1": (C.c_int, [_VP, _D, _D, C.c_int64, C.c_double, C.c_double,
+                                              _D]),
+        "eigmod_b200_locate_coeffs": (C.c_int, [_VP, _D, _D, C.c_int64, C.c_double, _I64]),
+        "eigmod_b200_gemm": (C.c_int, [_VP, C.c_int, C.c_int, _D, _D, C.c_int64, C.c_int64,
+                                       C.c_int64, _D]),
+        "eigmod_b200_multi_create": (C.c_int, [_I32, C.c_int, C.POINTER(_VP)]),
+        "eigmod_b200_multi_destroy": (None, [_VP]),
+        "eigmod_b200_multi_size": (C.c_int, [_VP]),
+        "eigmod_b200_multi_last_error": (C.c_char_p, [_VP]),
+        "eigmod_b200_multi_last_stage": (C.c_char_p, [_VP]),
+        "eigmod_b200_multi_set_option": (C.c_int, [_VP, C.c_char_p, C.c_double]),
+        "eigmod_b200_multi_update_decomposition": (C.c_int, [_VP, _D, _D, _D, _I32, C.c_int64,
+                                                             C.c_int64, C.c_double, _D, _D, _D]),
+        "eigmod_b200_multi_update_eigenvalues": (C.c_int, [_VP, _D, _D, _D, _I32, C.c_int64,
+                                                           C.c_int64, C.c_double, _D]),
+        "eigmod_b200_split": (C.c_int, [C.c_int64, C.c_int, C.c_int, _I64, _I64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -457,6 +489,231 @@ def update_decomposition(q, lam, kmat, signs, tol, metrics=False,
             _dp(lo), _dp(rf), _dp(oe)))
         res.residual_fro, res.ortho_err = float(rf[0]), float(oe[0])
     return res
+
+
+def assemble_eigenvectors(q, lam, plan: EigenvalueUpdate, ctx: Context | None = None,
+                          return_path=False):
+    """eigvec.hpp:29-31 — Q' and lambda' from a finished eigenvalue stage. The
+    plan of the last update_eigenvalues_full on the same context is reused on
+    the device (K4 + K5 only); any other plan is checked against the secular
+    equation of plan.u first (NumericalError "assemble" if its eigenvalues are
+    not those)."""
+    ctx = ctx or default_context()
+    q, lam = _f64(q), _f64(lam)
+    n = lam.shape[0]
+    u, sg = _f64(plan.u), _i32(plan.signs)
+    k = u.shape[1] if u.ndim == 2 else 0
+    if q.shape != (n, n) or (k and u.shape[0] != n):
+        raise ValueError("assemble_eigenvectors: plan does not match the decomposition")
+    roots = _f64(plan.roots)
+    prob = plan.problem
+    un = np.ascontiguousarray(prob.unchanged if prob is not None else [], dtype=np.int64)
+    co = np.ascontiguousarray(prob.collided if prob is not None else [], dtype=np.int64)
+    lo = np.empty(n)
+    qo = np.empty((n, n))
+    path = np.zeros(1, np.int32)
+    ctx.check(ctx._l.eigmod_b200_assemble(
+        ctx.h, _dp(q), _dp(lam), _dp(u), sg.ctypes.data_as(_I32), n, k, _dp(roots), len(roots),
+        un.ctypes.data_as(_I64), len(un), co.ctypes.data_as(_I64), len(co), _dp(lo), _dp(qo),
+        path.ctypes.data_as(_I32)))
+    return (lo, qo, int(path[0])) if return_path else (lo, qo)
+
+
+def stage_calls(ctx: Context | None = None) -> dict:
+    """Stage launches on a context: K1 projections, K2 plans, K3 solves, K4+K5 builds."""
+    ctx = ctx or default_context()
+    out = np.zeros(4, np.int64)
+    ctx.check(ctx._l.eigmod_b200_stage_calls(ctx.h, out.ctypes.data_as(_I64)))
+    return dict(zip(("project", "plan", "solve", "columns"), (int(x) for x in out)))
+
+
+# ------------------------------------------- single eigenpairs, secular function
+def null_problem(u, signs, lam, lam_new, ctx: Context | None = None) -> np.ndarray:
+    """eigvec.hpp:19 — I + J U^T (Lambda - lambda' I)^{-1} U (k x k)."""
+    ctx = ctx or default_context()
+    u, signs, lam = _f64(u), _i32(signs), _f64(lam)
+    n, k = u.shape
+    if lam.shape[0] != n:
+        raise ValueError("null_problem: dimension mismatch")
+    m = np.empty((k, k))
+    ctx.check(ctx._l.eigmod_b200_null_problem(ctx.h, _dp(u), signs.ctypes.data_as(_I32),
+                                              _dp(lam), n, k, C.c_double(lam_new), _dp(m)))
+    return m
+
+
+def null_direction(m) -> tuple[np.ndarray, float]:
+    """eigvec.hpp:15 — smallest singular direction of a k x k matrix."""
+    m = _f64(m)
+    k = m.shape[0]
+    if m.shape != (k, k) or k == 0:
+        raise ValueError("null_direction: square matrix required")
+    d, r = np.empty(k), np.zeros(1)
+    rc = lib().eigmod_b200_null_direction(_dp(m), k, _dp(d), _dp(r))
+    if rc:
+        raise ValueError("null_direction: square matrix required")
+    return d, float(r[0])
+
+
+def update_eigenvector(q, lam, kmat, signs, lam_new, ctx: Context | None = None) -> np.ndarray:
+    """eigvec.hpp:25 — one updated eigenvector."""
+    ctx = ctx or default_context()
+    q, lam, kmat, signs = _f64(q), _f64(lam), _f64(kmat), _i32(signs)
+    _check_update(q, lam, kmat, signs)
+    n, k = kmat.shape
+    v = np.empty(n)
+    ctx.check(ctx._l.eigmod_b200_update_eigenvector(ctx.h, _dp(q), _dp(lam), _dp(kmat),
+                                                    signs.ctypes.data_as(_I32), n, k,
+                                                    C.c_double(lam_new), _dp(v)))
+    return v
+
+
+def secular_eval(poles, weights, xs, leading=1.0, derivative=False, ctx: Context | None = None):
+    """eval_secular (+ eval_secular_derivative) at many points on the device;
+    returns (f, f' or None, hit)."""
+    ctx = ctx or default_context()
+    poles, weights, xs = _f64(poles), _f64(weights), _f64(np.atleast_1d(xs))
+    f, hit = np.empty(len(xs)), np.zeros(len(xs), np.int32)
+    fp = np.empty(len(xs)) if derivative else None
+    ctx.check(ctx._l.eigmod_b200_secular_eval(ctx.h, _dp(poles), _dp(weights), len(poles),
+                                              C.c_double(leading), _dp(xs), len(xs), _dp(f),
+                                              _dp(fp) if derivative else None,
+                                              hit.ctypes.data_as(_I32)))
+    return f, fp, hit
+
+
+def crossing_count(poles, weights, lo, hi, samples, leading=1.0, ctx: Context | None = None):
+    """secular.hpp:48."""
+    ctx = ctx or default_context()
+    poles, weights = _f64(poles), _f64(weights)
+    out = np.zeros(1, np.int64)
+    ctx.check(ctx._l.eigmod_b200_crossing_count(ctx.h, _dp(poles), _dp(weights), len(poles),
+                                                C.c_double(leading), C.c_double(lo),
+                                                C.c_double(hi), int(samples),
+                                                out.ctypes.data_as(_I64)))
+    return int(out[0])
+
+
+def dnc_solve(poles, weights, lo, hi, expected, tol, leading=1.0, ctx: Context | None = None,
+              stats=False):
+    """rootfind.hpp:28 — the `expected` roots in (lo, hi), ascending."""
+    ctx = ctx or default_context()
+    poles, weights = _f64(poles), _f64(weights)
+    out = np.empty(max(1, int(expected)))
+    nr, ev, rd = (np.zeros(1, np.int64) for _ in range(3))
+    ctx.check(ctx._l.eigmod_b200_dnc_solve(ctx.h, _dp(poles), _dp(weights), len(poles),
+                                           C.c_double(leading), C.c_double(lo), C.c_double(hi),
+                                           int(expected), C.c_double(tol), _dp(out),
+                                           nr.ctypes.data_as(_I64), ev.ctypes.data_as(_I64),
+                                           rd.ctypes.data_as(_I64)))
+    r = out[: int(nr[0])].copy()
+    return (r, {"evaluations": int(ev[0]), "rounds": int(rd[0])}) if stats else r
+
+
+def solve_rank1(poles, zeta, sigma, tol, ctx: Context | None = None) -> np.ndarray:
+    """rootfind.hpp:33 — eigenvalues of diag(poles) + sigma zeta zeta^T."""
+    ctx = ctx or default_context()
+    poles, zeta = _f64(poles), _f64(zeta)
+    if zeta.shape != poles.shape or len(poles) == 0:
+        raise ValueError("solve_rank1: bad inputs")
+    out = np.empty(len(poles))
+    ctx.check(ctx._l.eigmod_b200_solve_rank1(ctx.h, _dp(poles), _dp(zeta), len(poles),
+                                             C.c_double(sigma), C.c_double(tol), _dp(out)))
+    return out
+
+
+def locate_coeffs(poles, weights, leading=1.0, ctx: Context | None = None) -> list[int]:
+    """locate.hpp:31,50 — root counts per pole interval from the coefficients."""
+    ctx = ctx or default_context()
+    poles, weights = _f64(poles), _f64(weights)
+    out = np.zeros(len(poles) + 1, np.int64)
+    ctx.check(ctx._l.eigmod_b200_locate_coeffs(ctx.h, _dp(poles), _dp(weights), len(poles),
+                                               C.c_double(leading), out.ctypes.data_as(_I64)))
+    return [int(x) for x in out]
+
+
+def gemm(a, b, trans_a=False, trans_b=False, ctx: Context | None = None) -> np.ndarray:
+    """kernels.hpp:19-21 — op(A) op(B) on the DMMA GEMM."""
+    ctx = ctx or default_context()
+    a, b = _f64(a), _f64(b)
+    m, kk = (a.shape[1], a.shape[0]) if trans_a else a.shape
+    kb, nn = (b.shape[1], b.shape[0]) if trans_b else b.shape
+    if kb != kk:
+        raise ValueError("gemm: dimension mismatch")
+    c = np.empty((m, nn))
+    ctx.check(ctx._l.eigmod_b200_gemm(ctx.h, int(trans_a), int(trans_b), _dp(a), _dp(b), m, nn,
+                                      kk, _dp(c)))
+    return c
+
+
+def split(n: int, world: int, rank: int) -> tuple[int, int]:
+    """The C ABI's partition of [0, n) across `world` ranks."""
+    lo, hi = np.zeros(1, np.int64), np.zeros(1, np.int64)
+    rc = lib().eigmod_b200_split(int(n), int(world), int(rank), lo.ctypes.data_as(_I64),
+                                 hi.ctypes.data_as(_I64))
+    if rc:
+        raise ValueError("split: bad arguments")
+    return int(lo[0]), int(hi[0])
+
+
+class MultiContext:
+    """Single-process multi-GPU context (one device per rank, NCCL)."""
+
+    def __init__(self, devices):
+        self._l = lib()
+        dv = np.ascontiguousarray(devices, dtype=np.int32)
+        h = _VP()
+        rc = self._l.eigmod_b200_multi_create(dv.ctypes.data_as(_I32), len(dv), C.byref(h))
+        if rc == 1:
+            raise ValueError(f"multi_create: bad device list {list(devices)}")
+        if rc != 0:
+            raise DeviceError(f"eigmod_b200_multi_create({list(devices)}) failed (rc={rc})")
+        self.h = h
+        self.devices = [int(d) for d in dv]
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._l.eigmod_b200_multi_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc):
+        if rc == 0:
+            return
+        msg = (self._l.eigmod_b200_multi_last_error(self.h) or b"").decode()
+        stage = (self._l.eigmod_b200_multi_last_stage(self.h) or b"").decode()
+        if rc == 1:
+            raise ValueError(msg)
+        if rc == 2:
+            raise NumericalError(stage, msg)
+        raise DeviceError(msg)
+
+    def set_option(self, key, value):
+        self.check(self._l.eigmod_b200_multi_set_option(self.h, key.encode(), C.c_double(value)))
+
+    def update_decomposition(self, q, lam, kmat, signs, tol) -> UpdateResult:
+        q, lam, kmat, signs = _f64(q), _f64(lam), _f64(kmat), _i32(signs)
+        _check_update(q, lam, kmat, signs)
+        n, k = kmat.shape
+        lo, qo, wt = np.empty(n), np.empty((n, n)), np.zeros(1)
+        self.check(self._l.eigmod_b200_multi_update_decomposition(
+            self.h, _dp(q), _dp(lam), _dp(kmat), signs.ctypes.data_as(_I32), n, k,
+            C.c_double(tol), _dp(lo), _dp(qo), _dp(wt)))
+        return UpdateResult(lo, qo, wall_time=float(wt[0]))
+
+    def update_eigenvalues(self, q, lam, kmat, signs, tol) -> np.ndarray:
+        q, lam, kmat, signs = _f64(q), _f64(lam), _f64(kmat), _i32(signs)
+        _check_update(q, lam, kmat, signs)
+        n, k = kmat.shape
+        vals = np.empty(n)
+        self.check(self._l.eigmod_b200_multi_update_eigenvalues(
+            self.h, _dp(q), _dp(lam), _dp(kmat), signs.ctypes.data_as(_I32), n, k,
+            C.c_double(tol), _dp(vals)))
+        return vals
 
 
 def default_tolerance(lam, kmat) -> float:

@@ -20,45 +20,10 @@
 #include <vector>
 
 #include "../../include/eigmod_b200.h"
-#include "pipeline.cuh"
+#include "context.cuh"
 
 using eigb::Error;
 
-struct eigmod_b200_ctx {
-  int device = 0;
-  cudaStream_t own = nullptr, stream = nullptr;
-  int sms = 148;
-  eigb::DeviceScratch ws;
-  eigb::Plan plan;
-  bool have_plan = false;
-  eigb::RootRecords recs{};
-  double run_rel = eigb::kExactRunRelGap;
-  eigb::SolveOptions sopt;
-  const double* lam = nullptr;  // the plan's own copy of lambda (workspace "plan_lam")
-  cudaStream_t copy = nullptr;   // D2H stream of the blocked host path
-  std::vector<cudaEvent_t> blk_ev;
-  std::string err, stage;
-  // per-stage CUDA-event timing (option "timing"): 0 K1 project, 1 K2 plan,
-  // 2 K3 solve, 3 K4 columns, 4 K5 GEMM, 5 sign rule
-  bool timing = false;
-  cudaEvent_t ev[8] = {};
-  double stage_ms[8] = {};
-  int64_t timed_calls = 0;
-  void mark(int i) {
-    if (!timing) return;
-    if (!ev[i]) EIGB_CUDA(cudaEventCreate(&ev[i]));
-    EIGB_CUDA(cudaEventRecord(ev[i], stream));
-  }
-  // staged entry points: add stages [i0, i1) once their end mark completed
-  void accumulate(int i0, int i1) {
-    if (!timing || !ev[i1]) return;
-    EIGB_CUDA(cudaEventSynchronize(ev[i1]));
-    for (int i = i0; i < i1; ++i) {
-      float ms = 0.f;
-      if (ev[i] && cudaEventElapsedTime(&ms, ev[i], ev[i + 1]) == cudaSuccess) stage_ms[i] += ms;
-    }
-  }
-};
 
 namespace eigb {
 namespace {
@@ -68,65 +33,14 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(); }
 }  // namespace eigb
 
-namespace {
-
-constexpr int kRecHead = 5;  // value, origin, delta, flags, evals
-
-void check_basic(int64_t n, int64_t k, const int* signs) {
-  // proj/src/core.cpp:89-97 (validate_update)
-  if (n < 1) throw Error(1, "", "LowRankUpdate: dimension mismatch");
-  if (k < 1 || k > n) throw Error(1, "", "LowRankUpdate: rank out of range");
-  if (k > eigb::kMaxRank) throw Error(1, "", "LowRankUpdate: rank above 32 is not supported");
-  if (signs)
-    for (int64_t r = 0; r < k; ++r)
-      if (signs[r] != 1 && signs[r] != -1)
-        throw Error(1, "", "LowRankUpdate: signs must be +1/-1");
-}
-
-void check_finite(const double* p, int64_t cnt, const char* what) {
-  for (int64_t i = 0; i < cnt; ++i)
-    if (!std::isfinite(p[i])) throw Error(1, "", std::string("LowRankUpdate: non-finite ") + what);
-}
-
-void check_ascending(const double* lam, int64_t n) {
-  // proj/src/secular.cpp:281-283, surfaced as NumericalError("deflate")
-  for (int64_t i = 0; i + 1 < n; ++i)
-    if (!(lam[i] <= lam[i + 1]))
-      throw Error(2, "deflate", "deflate_problem: eigenvalues not ascending");
-}
-
-void check_ascending_invalid(const double* lam, int64_t n) {
-  // proj/src/secular.cpp:281-283 called directly (the CLI locate path)
-  for (int64_t i = 0; i + 1 < n; ++i)
-    if (!(lam[i] <= lam[i + 1]))
-      throw Error(1, "", "deflate_problem: eigenvalues not ascending");
-}
-
-template <class F>
-int guarded(eigmod_b200_ctx* ctx, F&& f) {
-  if (!ctx) return EIGMOD_B200_INVALID_ARGUMENT;
-  try {
-    EIGB_CUDA(cudaSetDevice(ctx->device));
-    f();
-    ctx->err.clear();
-    ctx->stage.clear();
-    return EIGMOD_B200_OK;
-  } catch (const Error& e) {
-    ctx->err = e.what();
-    ctx->stage = e.stage;
-    if (e.code == EIGMOD_B200_CUDA) (void)cudaGetLastError();  // clear a non-sticky error
-    return e.code;
-  } catch (const std::exception& e) {
-    ctx->err = e.what();
-    ctx->stage = "cuda";
-    (void)cudaGetLastError();  // a non-sticky error must not poison the next call
-    return EIGMOD_B200_CUDA;
-  }
-}
+namespace eigb_capi {
 
 // ---------------------------------------------------------------- stages
+constexpr int kRecHead = 5;  // value, origin, delta, flags, evals
+
 void project(eigmod_b200_ctx* c, const double* q, const double* kmat, int64_t n, int64_t k,
              int64_t lo, int64_t hi, double* u_out) {
+  c->stage_calls[0] += 1;
   const int kp = eigb::padded_rank(k);
   eigb::transform_update_dev(q, kmat, n, (int)k, kp, lo, hi, u_out, c->ws, c->sms, c->stream);
 }
@@ -150,6 +64,8 @@ void plan_groups(eigmod_b200_ctx* c, const double* lam, const double* u, const i
   eigb::Plan& p = c->plan;
   p = eigb::Plan{};
   p.run_rel = run_rel;
+  c->plan_key_valid = false;
+  c->stage_calls[1] += 1;
   // the plan keeps its own copy of lambda: the staged entry points
   // (plan_finish, finish) must not depend on the caller's buffer staying alive
   double* lam_copy = c->ws.get_f64("plan_lam", n);
@@ -239,8 +155,24 @@ __global__ void unpack_records_kernel(const double* in, int64_t cnt, int kp, eig
   for (int c = 0; c < kp; ++c) r.y[j * kp + c] = o[kRecHead + c];
 }
 
+void pack_records_dev(eigmod_b200_ctx* c, int64_t j0, int64_t cnt, double* out) {
+  if (cnt <= 0) return;
+  pack_records_kernel<<<(unsigned)eigb::cdiv(cnt, 128), 128, 0, c->stream>>>(c->recs, j0, cnt,
+                                                                             c->plan.kp, out);
+  EIGB_LAUNCH_CHECK();
+}
+
+void unpack_records_dev(eigmod_b200_ctx* c, const double* in, int64_t cnt) {
+  c->recs = alloc_records(c);
+  if (cnt <= 0) return;
+  unpack_records_kernel<<<(unsigned)eigb::cdiv(cnt, 128), 128, 0, c->stream>>>(in, cnt,
+                                                                               c->plan.kp, c->recs);
+  EIGB_LAUNCH_CHECK();
+}
+
 void solve(eigmod_b200_ctx* c, int64_t j0, int64_t j1) {
   if (!c->have_plan) throw Error(1, "", "solve: no plan (call plan first)");
+  c->stage_calls[2] += 1;
   c->recs = alloc_records(c);
   if (c->plan.nred == 0) return;
   eigb::solve_roots(c->plan.view(), c->plan.alpha_red_ok ? c->plan.alpha_red : nullptr, j0, j1,
@@ -258,11 +190,11 @@ __global__ void copy_block_kernel(const double* __restrict__ a, int64_t n, int64
 // a second stream while the next block computes (the D2H of Q' overlaps the
 // back-transform; each block's signs are final when its GEMM ends).
 void finish(eigmod_b200_ctx* c, const double* q, const double* lam_in, int64_t c0, int64_t c1,
-            double* lam_out, double* q_out, int64_t ldq, double* host_q_out = nullptr,
-            int64_t host_ld = 0) {
+            double* lam_out, double* q_out, int64_t ldq, double* host_q_out, int64_t host_ld) {
   eigb::Plan& p = c->plan;
   const int64_t n = p.n;
   if (!lam_in) lam_in = c->lam;
+  if (q_out && c1 > c0) c->stage_calls[3] += 1;
   if (p.k == 0) {  // unchanged pairs: lambda and Q copied exactly
     if (lam_out)
       EIGB_CUDA(cudaMemcpyAsync(lam_out, lam_in, 8 * n, cudaMemcpyDeviceToDevice, c->stream));
@@ -442,7 +374,9 @@ int64_t locate_counts(eigmod_b200_ctx* c, int64_t* counts_out) {
   return nb + 1;
 }
 
-}  // namespace
+}  // namespace eigb_capi
+
+using namespace eigb_capi;
 
 extern "C" {
 
@@ -833,6 +767,15 @@ int eigmod_b200_update_eigenvalues(eigmod_b200_ctx* ctx, const double* q, const 
     if (k_eff_out) *k_eff_out = p.k;
     if (keep_out)
       for (int c = 0; c < p.k; ++c) keep_out[c] = p.keep_h[c];
+    // the plan stays on the device for assemble_eigenvectors: keyed by the
+    // inputs the caller will hand back (lambda, the kept columns of U, their
+    // signs) and checked against the n eigenvalues
+    if (u_out) {
+      std::vector<int> ks(p.sgn_h.begin(), p.sgn_h.end());
+      ctx->plan_key = plan_key_of(lambda, u_out, ks.data(), n, p.k);
+      if (roots_out) ctx->plan_roots.assign(roots_out, roots_out + p.nred);
+      ctx->plan_key_valid = roots_out != nullptr;
+    }
   });
 }
 
@@ -1115,6 +1058,88 @@ int eigmod_b200_assemble_from_u(eigmod_b200_ctx* ctx, const double* q, const dou
     EIGB_CUDA(cudaMemcpyAsync(q_out, dqo, 8 * n * n, cudaMemcpyDeviceToHost, st));
     EIGB_CUDA(cudaStreamSynchronize(st));
   });
+}
+
+int eigmod_b200_assemble(eigmod_b200_ctx* ctx, const double* q, const double* lambda,
+                         const double* u, const int* signs, int64_t n, int64_t k,
+                         const double* roots, int64_t nroots, const int64_t* unchanged,
+                         int64_t nunchanged, const int64_t* collided, int64_t ncollided,
+                         double* lambda_out, double* q_out, int* path_out) {
+  return guarded(ctx, [&] {
+    if (k < 0 || k > n) throw Error(1, "", "assemble: rank out of range");
+    if (nroots < 0 || nunchanged < 0 || ncollided < 0) throw Error(1, "", "assemble: bad counts");
+    check_ascending(lambda, n);
+    // the plan the last update_eigenvalues call on this context produced:
+    // same inputs, same roots (its deflation record is informational)
+    const bool cached = ctx->plan_key_valid && ctx->have_plan && ctx->plan.n == n &&
+                        plan_key_of(lambda, u, signs, n, k) == ctx->plan_key &&
+                        (int64_t)ctx->plan_roots.size() == nroots &&
+                        std::equal(roots, roots + nroots, ctx->plan_roots.begin());
+    if (!cached && nroots + nunchanged + ncollided != n)
+      throw Error(2, "assemble", "eigenpair count mismatch");  // eigvec.cpp:277-278
+    // the plan's n eigenvalues (roots, unchanged and collided values merged,
+    // eigvec.cpp:260-276)
+    std::vector<double> want(roots, roots + nroots);
+    for (int64_t i = 0; i < nunchanged; ++i) {
+      if (unchanged[i] < 0 || unchanged[i] >= n) throw Error(1, "", "assemble: index out of range");
+      want.push_back(lambda[unchanged[i]]);
+    }
+    for (int64_t i = 0; i < ncollided; ++i) {
+      if (collided[i] < 0 || collided[i] >= n) throw Error(1, "", "assemble: index out of range");
+      want.push_back(lambda[collided[i]]);
+    }
+    std::sort(want.begin(), want.end());
+    auto st = ctx->stream;
+    double* dq = ctx->ws.get_f64("h_q", (size_t)n * n);
+    double* dlo = ctx->ws.get_f64("h_lo", n);
+    double* dqo = ctx->ws.get_f64("h_qo", (size_t)n * n);
+    if (path_out) *path_out = cached ? 1 : 2;
+    if (!cached && k == 0) {  // nothing couples: every pair passes through exactly
+      if (!std::equal(want.begin(), want.end(), lambda))
+        throw Error(2, "assemble", "plan eigenvalues are not the updated eigenvalues of "
+                                   "plan.transformed (rank 0)");
+      std::memcpy(lambda_out, lambda, 8 * n);
+      std::memcpy(q_out, q, 8 * n * n);
+      return;
+    }
+    EIGB_CUDA(cudaMemcpyAsync(dq, q, 8 * n * n, cudaMemcpyHostToDevice, st));
+    if (!cached) {
+      // a plan from elsewhere: solve the secular equation of plan.transformed
+      // and accept the plan only if its eigenvalues are these
+      double* dl = ctx->ws.get_f64("h_l", n);
+      EIGB_CUDA(cudaMemcpyAsync(dl, lambda, 8 * n, cudaMemcpyHostToDevice, st));
+      check_basic(n, k, signs);
+      const int kp = eigb::padded_rank(k);
+      std::vector<double> up((size_t)n * kp, 0.0);
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t c = 0; c < k; ++c) up[i * kp + c] = u[i * k + c];
+      double* du = ctx->ws.get_f64("h_u", (size_t)n * kp);
+      EIGB_CUDA(cudaMemcpyAsync(du, up.data(), 8 * up.size(), cudaMemcpyHostToDevice, st));
+      plan_from_u(ctx, dl, du, signs, n, k, ctx->run_rel);
+      solve(ctx, 0, ctx->plan.nred);
+      finish(ctx, dq, nullptr, 0, 0, dlo, nullptr, n);
+      std::vector<double> got(n);
+      EIGB_CUDA(cudaMemcpyAsync(got.data(), dlo, 8 * n, cudaMemcpyDeviceToHost, st));
+      EIGB_CUDA(cudaStreamSynchronize(st));
+      double scale = 0.0, err = 0.0;
+      for (int64_t i = 0; i < n; ++i)
+        scale = std::max(scale, std::fabs(got[i])), err = std::max(err, std::fabs(got[i] - want[i]));
+      if (!(err <= 1e-10 * std::max(scale, DBL_MIN)))
+        throw Error(2, "assemble", "plan eigenvalues are not the updated eigenvalues of "
+                                   "plan.transformed (max deviation " + std::to_string(err) + ")");
+    }
+    finish(ctx, dq, nullptr, 0, n, dlo, dqo, n, ctx->plan.k > 0 ? q_out : nullptr, n);
+    EIGB_CUDA(cudaMemcpyAsync(lambda_out, dlo, 8 * n, cudaMemcpyDeviceToHost, st));
+    if (ctx->plan.k == 0)
+      EIGB_CUDA(cudaMemcpyAsync(q_out, dqo, 8 * n * n, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int eigmod_b200_stage_calls(const eigmod_b200_ctx* ctx, int64_t* out4) {
+  if (!ctx || !out4) return EIGMOD_B200_INVALID_ARGUMENT;
+  for (int i = 0; i < 4; ++i) out4[i] = ctx->stage_calls[i];
+  return EIGMOD_B200_OK;
 }
 
 int eigmod_b200_update_metrics(eigmod_b200_ctx* ctx, const double* q, const double* lambda,

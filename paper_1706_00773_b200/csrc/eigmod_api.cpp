@@ -9,6 +9,8 @@
 // utilities the reference exposes next to the hot path.
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <limits>
 #include <memory>
@@ -34,6 +36,72 @@ eigmod_b200_ctx* ctx() {
     c.reset(p);
   }
   return c.get();
+}
+
+// The multi-GPU context of set_devices / EIGMOD_B200_DEVICES (process-wide,
+// one update at a time).
+struct MultiState {
+  std::mutex mu;
+  bool env_read = false;
+  std::vector<int> devices;
+  eigmod_b200_multi* mg = nullptr;
+};
+MultiState& multi_state() {
+  static MultiState s;
+  return s;
+}
+
+std::vector<int> parse_device_list(const char* s) {
+  std::vector<int> out;
+  if (!s) return out;
+  std::string cur;
+  for (const char* p = s;; ++p) {
+    if (*p == ',' || *p == '\0') {
+      if (!cur.empty()) out.push_back(std::stoi(cur));
+      cur.clear();
+      if (!*p) break;
+    } else if (*p != ' ') {
+      cur.push_back(*p);
+    }
+  }
+  return out;
+}
+
+// Locked multi context when devices are configured, else null.
+eigmod_b200_multi* multi(std::unique_lock<std::mutex>& lock) {
+  MultiState& s = multi_state();
+  lock = std::unique_lock<std::mutex>(s.mu);
+  if (!s.env_read) {
+    s.env_read = true;
+    if (s.devices.empty()) s.devices = parse_device_list(std::getenv("EIGMOD_B200_DEVICES"));
+  }
+  if (s.devices.empty()) return nullptr;
+  if (!s.mg) {
+    const int rc = eigmod_b200_multi_create(s.devices.data(), (int)s.devices.size(), &s.mg);
+    if (rc != EIGMOD_B200_OK) {
+      s.mg = nullptr;
+      if (rc == EIGMOD_B200_INVALID_ARGUMENT)
+        throw std::invalid_argument("set_devices: invalid device list");
+      throw std::runtime_error("eigmod (B200): multi-GPU context failed (rc " +
+                               std::to_string(rc) + ")");
+    }
+  }
+  return s.mg;
+}
+
+void check_multi(eigmod_b200_multi* mg, int rc) {
+  if (rc == EIGMOD_B200_OK) return;
+  const std::string msg = eigmod_b200_multi_last_error(mg);
+  const std::string stage = eigmod_b200_multi_last_stage(mg);
+  if (rc == EIGMOD_B200_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (rc == EIGMOD_B200_NUMERICAL) {
+    std::string body = msg;
+    const std::string pre = "[" + stage + "] ";
+    const size_t at = body.find(pre);
+    if (at != std::string::npos) body = body.substr(at + pre.size());
+    throw NumericalError(stage, body);
+  }
+  throw std::runtime_error(msg);
 }
 
 void check(int rc) {
@@ -324,6 +392,16 @@ Vec update_eigenvalues(const SpectralDecomposition& d, const LowRankUpdate& u, d
   validate_update(d, u);
   if (!(tol > 0.0)) throw std::invalid_argument("update_eigenvalues: tol must be positive");
   const std::size_t n = d.size(), k = u.rank();
+  {
+    std::unique_lock<std::mutex> lock;
+    if (eigmod_b200_multi* mg = multi(lock)) {
+      Vec values(n);
+      check_multi(mg, eigmod_b200_multi_update_eigenvalues(mg, d.q.data(), d.lambda.data(),
+                                                           u.kmat.data(), u.signs.data(), n, k,
+                                                           tol, values.data()));
+      return values;
+    }
+  }
   Vec values(n), roots(n);
   std::int64_t nroots = 0, keff = 0;
   check(eigmod_b200_update_eigenvalues(ctx(), d.q.data(), d.lambda.data(), u.kmat.data(),
@@ -332,20 +410,122 @@ Vec update_eigenvalues(const SpectralDecomposition& d, const LowRankUpdate& u, d
   return values;
 }
 
+// eigvec.cpp:254-364 — columns from the plan: the plan of the last
+// update_eigenvalues_full on this thread's context is reused on the device
+// (K4 + K5 only, no K2 / K3); any other plan is checked against the secular
+// equation of plan.transformed (eigmod_b200_assemble).
 SpectralDecomposition assemble_eigenvectors(const SpectralDecomposition& d,
                                             const EigenvalueUpdate& plan, bool) {
   const std::size_t n = d.size(), k = plan.transformed.rank();
   if (plan.transformed.dim() != n && k > 0)
     throw std::invalid_argument("assemble_eigenvectors: plan does not match the decomposition");
+  if (plan.transformed.signs.size() != k)
+    throw std::invalid_argument("assemble_eigenvectors: signs size");
   SpectralDecomposition out;
   out.lambda.resize(n);
   out.q = Matrix(n, n);
-  check(eigmod_b200_assemble_from_u(ctx(), d.q.data(), d.lambda.data(), plan.transformed.u.data(),
-                                    plan.transformed.signs.data(), n, k, out.lambda.data(),
-                                    out.q.data()));
-  if (!plan.values.empty() && plan.values.size() != n)
-    throw NumericalError("assemble", "eigenpair count mismatch");
+  std::vector<std::int64_t> un(plan.problem.unchanged.begin(), plan.problem.unchanged.end());
+  std::vector<std::int64_t> co(plan.problem.collided.begin(), plan.problem.collided.end());
+  int path = 0;
+  check(eigmod_b200_assemble(ctx(), d.q.data(), d.lambda.data(), plan.transformed.u.data(),
+                             plan.transformed.signs.data(), n, k, plan.roots.data(),
+                             (std::int64_t)plan.roots.size(), un.data(), (std::int64_t)un.size(),
+                             co.data(), (std::int64_t)co.size(), out.lambda.data(), out.q.data(),
+                             &path));
   return out;
+}
+
+// eigvec.hpp:9-25
+NullDirection null_direction(const Matrix& m) {
+  if (m.rows() != m.cols() || m.rows() == 0)
+    throw std::invalid_argument("null_direction: square matrix required");
+  NullDirection nd;
+  nd.direction.resize(m.rows());
+  if (eigmod_b200_null_direction(m.data(), (std::int64_t)m.rows(), nd.direction.data(),
+                                 &nd.residual) != EIGMOD_B200_OK)
+    throw std::invalid_argument("null_direction: square matrix required");
+  return nd;
+}
+
+Matrix null_problem(const TransformedUpdate& tu, const Vec& lambda, double lambda_new) {
+  const std::size_t n = lambda.size(), k = tu.rank();
+  if (tu.dim() != n) throw std::invalid_argument("null_problem: dimension mismatch");
+  if (tu.signs.size() != k) throw std::invalid_argument("null_problem: signs size");
+  if (k == 0) return Matrix(0, 0);
+  if (n == 0) return Matrix::identity(k);
+  Matrix m(k, k);
+  check(eigmod_b200_null_problem(ctx(), tu.u.data(), tu.signs.data(), lambda.data(),
+                                 (std::int64_t)n, (std::int64_t)k, lambda_new, m.data()));
+  return m;
+}
+
+Vec update_eigenvector(const SpectralDecomposition& d, const LowRankUpdate& u, double lambda_new) {
+  validate_update(d, u);
+  const std::size_t n = d.size();
+  Vec v(n);
+  check(eigmod_b200_update_eigenvector(ctx(), d.q.data(), d.lambda.data(), u.kmat.data(),
+                                       u.signs.data(), (std::int64_t)n, (std::int64_t)u.rank(),
+                                       lambda_new, v.data()));
+  return v;
+}
+
+// rootfind.hpp:28-33
+Vec dnc_solve(const SecularCoefficients& c, const RootBracket& b, double tol, DncStats* stats) {
+  if (!(b.lo < b.hi)) throw std::invalid_argument("dnc_solve: empty bracket");
+  if (b.expected < 1) throw std::invalid_argument("dnc_solve: expected must be >= 1");
+  if (!(tol > 0.0)) throw std::invalid_argument("dnc_solve: tol must be positive");
+  Vec roots((std::size_t)b.expected);
+  std::int64_t nr = 0, ev = 0, rd = 0;
+  check(eigmod_b200_dnc_solve(ctx(), c.poles.data(), c.weights.data(), (std::int64_t)c.size(),
+                              c.leading, b.lo, b.hi, b.expected, tol, roots.data(), &nr, &ev, &rd));
+  roots.resize((std::size_t)nr);
+  if (stats) {
+    stats->evaluations = (std::size_t)ev;
+    stats->rounds = (std::size_t)rd;
+  }
+  return roots;
+}
+
+Vec solve_rank1(const Vec& poles, const Vec& zeta, double sigma, double tol) {
+  const std::size_t n = poles.size();
+  if (zeta.size() != n || n == 0) throw std::invalid_argument("solve_rank1: bad inputs");
+  Vec roots(n);
+  check(eigmod_b200_solve_rank1(ctx(), poles.data(), zeta.data(), (std::int64_t)n, sigma, tol,
+                                roots.data()));
+  return roots;
+}
+
+// secular.hpp:48
+long crossing_count(const SecularCoefficients& c, double lo, double hi, int samples) {
+  if (!(lo < hi) || samples < 1) throw std::invalid_argument("crossing_count: bad range");
+  std::int64_t out = 0;
+  check(eigmod_b200_crossing_count(ctx(), c.poles.data(), c.weights.data(),
+                                   (std::int64_t)c.size(), c.leading, lo, hi, samples, &out));
+  return (long)out;
+}
+
+// locate.hpp:31,50
+namespace {
+LocationVector counts_from_coeffs(const SecularCoefficients& c0) {
+  std::vector<std::int64_t> cnt(c0.size() + 1);
+  check(eigmod_b200_locate_coeffs(ctx(), c0.poles.data(), c0.weights.data(),
+                                  (std::int64_t)c0.size(), c0.leading, cnt.data()));
+  LocationVector loc;
+  loc.counts.assign(cnt.begin(), cnt.end());
+  return loc;
+}
+}  // namespace
+
+LocationVector locate_rank2(const SecularCoefficients& c0, ShiftKind) {
+  return counts_from_coeffs(c0);
+}
+
+LocateResult locate_rank_k(const SecularCoefficients& c0, const std::vector<int>& signs) {
+  for (int sg : signs)
+    if (sg != 1 && sg != -1) throw std::invalid_argument("locate_rank_k: signs must be +1/-1");
+  LocateResult r;
+  r.loc = counts_from_coeffs(c0);
+  return r;
 }
 
 UpdateResult update_decomposition(const SpectralDecomposition& d, const LowRankUpdate& u,
@@ -357,10 +537,22 @@ UpdateResult update_decomposition(const SpectralDecomposition& d, const LowRankU
   res.decomposition.lambda.resize(n);
   res.decomposition.q = Matrix(n, n);
   double wall = 0.0;
-  check(eigmod_b200_update_decomposition(ctx(), d.q.data(), d.lambda.data(), u.kmat.data(),
-                                         u.signs.data(), n, k, tol,
-                                         res.decomposition.lambda.data(),
-                                         res.decomposition.q.data(), &wall));
+  bool done = false;
+  {
+    std::unique_lock<std::mutex> lock;
+    if (eigmod_b200_multi* mg = multi(lock)) {
+      check_multi(mg, eigmod_b200_multi_update_decomposition(
+                          mg, d.q.data(), d.lambda.data(), u.kmat.data(), u.signs.data(), n, k,
+                          tol, res.decomposition.lambda.data(), res.decomposition.q.data(),
+                          &wall));
+      done = true;
+    }
+  }
+  if (!done)
+    check(eigmod_b200_update_decomposition(ctx(), d.q.data(), d.lambda.data(), u.kmat.data(),
+                                           u.signs.data(), n, k, tol,
+                                           res.decomposition.lambda.data(),
+                                           res.decomposition.q.data(), &wall));
   res.wall_time = wall;
   // metrics outside the timed update, as eigvec.cpp:384-393
   check(eigmod_b200_update_metrics(ctx(), d.q.data(), d.lambda.data(), u.kmat.data(),
@@ -368,6 +560,33 @@ UpdateResult update_decomposition(const SpectralDecomposition& d, const LowRankU
                                    res.decomposition.lambda.data(), &res.residual_fro,
                                    &res.ortho_err));
   return res;
+}
+
+void set_devices(const std::vector<int>& devs) {
+  MultiState& s = multi_state();
+  std::lock_guard<std::mutex> lock(s.mu);
+  s.env_read = true;
+  if (s.mg) {
+    eigmod_b200_multi_destroy(s.mg);
+    s.mg = nullptr;
+  }
+  s.devices = devs;
+}
+
+std::vector<int> devices() {
+  MultiState& s = multi_state();
+  std::lock_guard<std::mutex> lock(s.mu);
+  if (!s.env_read) {
+    s.env_read = true;
+    if (s.devices.empty()) s.devices = parse_device_list(std::getenv("EIGMOD_B200_DEVICES"));
+  }
+  return s.devices;
+}
+
+std::vector<long long> stage_calls() {
+  std::int64_t c[4] = {0, 0, 0, 0};
+  check(eigmod_b200_stage_calls(ctx(), c));
+  return {c[0], c[1], c[2], c[3]};
 }
 
 namespace kernels {
@@ -380,6 +599,115 @@ double ortho_error(const Matrix& a) {
 void set_parallel(bool) {}
 bool parallel() { return false; }
 int worker_count() { return 1; }
+
+namespace {
+Matrix gemm_dev(int ta, int tb, const Matrix& a, const Matrix& b, std::size_t m, std::size_t nn,
+                std::size_t kk) {
+  Matrix c(m, nn);
+  if (m && nn)
+    check(eigmod_b200_gemm(ctx(), ta, tb, a.data(), b.data(), (std::int64_t)m, (std::int64_t)nn,
+                           (std::int64_t)kk, c.data()));
+  return c;
+}
+void dims(bool ok, const char* what) {
+  if (!ok) throw std::invalid_argument(std::string("dimension mismatch in ") + what);
+}
+}  // namespace
+
+// kernels.cpp:32-80 — on the DMMA GEMM
+Matrix gemm_nn(const Matrix& a, const Matrix& b) {
+  dims(a.cols() == b.rows(), "gemm_nn");
+  return gemm_dev(0, 0, a, b, a.rows(), b.cols(), a.cols());
+}
+Matrix gemm_tn(const Matrix& a, const Matrix& b) {
+  dims(a.rows() == b.rows(), "gemm_tn");
+  return gemm_dev(1, 0, a, b, a.cols(), b.cols(), a.rows());
+}
+Matrix gemm_nt(const Matrix& a, const Matrix& b) {
+  dims(a.cols() == b.cols(), "gemm_nt");
+  return gemm_dev(0, 1, a, b, a.rows(), b.rows(), a.cols());
+}
+Vec gemv_t(const Matrix& a, const Vec& x) {
+  dims(a.rows() == x.size(), "gemv_t");
+  Matrix xm(x.size(), 1);
+  std::copy(x.begin(), x.end(), xm.data());
+  const Matrix c = gemm_dev(1, 0, a, xm, a.cols(), 1, a.rows());
+  return Vec(c.data(), c.data() + a.cols());
+}
+Matrix reconstruct_symmetric(const Matrix& q, const Vec& lambda) {
+  return reconstruct(SpectralDecomposition{q, lambda}).entries;
+}
+// kernels.cpp:111-148: O(n^2) host helpers of the validation path
+void rank1_accumulate(Matrix& a, const Vec& v, double coeff) {
+  dims(a.rows() == v.size() && a.cols() == v.size(), "rank1_accumulate");
+  for (std::size_t i = 0; i < v.size(); ++i) {
+    const double s = coeff * v[i];
+    double* ai = a.row(i);
+    for (std::size_t j = 0; j < v.size(); ++j) ai[j] += s * v[j];
+  }
+}
+void symmetrize(Matrix& a) {
+  dims(a.rows() == a.cols(), "symmetrize");
+  a = symmetrized(a);
+}
+double frobenius_norm(const Matrix& a) {
+  double s = 0.0;
+  for (std::size_t i = 0; i < a.rows() * a.cols(); ++i) s += a.data()[i] * a.data()[i];
+  return std::sqrt(s);
+}
+double max_abs(const Matrix& a) {
+  double m = 0.0;
+  for (std::size_t i = 0; i < a.rows() * a.cols(); ++i) m = std::max(m, std::fabs(a.data()[i]));
+  return m;
+}
+
+// kernels.hpp:39-50 — the plain serial loops, independent of the GPU path
+namespace ref {
+Matrix gemm_nn(const Matrix& a, const Matrix& b) {
+  dims(a.cols() == b.rows(), "ref::gemm_nn");
+  Matrix c(a.rows(), b.cols());
+  for (std::size_t i = 0; i < a.rows(); ++i)
+    for (std::size_t j = 0; j < b.cols(); ++j) {
+      double s = 0.0;
+      for (std::size_t l = 0; l < a.cols(); ++l) s += a(i, l) * b(l, j);
+      c(i, j) = s;
+    }
+  return c;
+}
+Matrix gemm_tn(const Matrix& a, const Matrix& b) {
+  dims(a.rows() == b.rows(), "ref::gemm_tn");
+  Matrix c(a.cols(), b.cols());
+  for (std::size_t i = 0; i < a.cols(); ++i)
+    for (std::size_t j = 0; j < b.cols(); ++j) {
+      double s = 0.0;
+      for (std::size_t l = 0; l < a.rows(); ++l) s += a(l, i) * b(l, j);
+      c(i, j) = s;
+    }
+  return c;
+}
+Matrix gemm_nt(const Matrix& a, const Matrix& b) {
+  dims(a.cols() == b.cols(), "ref::gemm_nt");
+  Matrix c(a.rows(), b.rows());
+  for (std::size_t i = 0; i < a.rows(); ++i)
+    for (std::size_t j = 0; j < b.rows(); ++j) {
+      double s = 0.0;
+      for (std::size_t l = 0; l < a.cols(); ++l) s += a(i, l) * b(j, l);
+      c(i, j) = s;
+    }
+  return c;
+}
+Matrix reconstruct_symmetric(const Matrix& q, const Vec& lambda) {
+  dims(q.cols() == lambda.size(), "ref::reconstruct_symmetric");
+  Matrix c(q.rows(), q.rows());
+  for (std::size_t i = 0; i < q.rows(); ++i)
+    for (std::size_t j = 0; j < q.rows(); ++j) {
+      double s = 0.0;
+      for (std::size_t l = 0; l < q.cols(); ++l) s += q(i, l) * lambda[l] * q(j, l);
+      c(i, j) = s;
+    }
+  return symmetrized(c);
+}
+}  // namespace ref
 }  // namespace kernels
 
 }  // namespace eigmod

@@ -1904,6 +1904,8 @@ void solve_after_counts(const ReducedView& rp, const double* alpha, int64_t j0, 
   double* f_delta = nullptr;
   int* f_state = nullptr;
   const bool pre = alpha && br_lo && opt.fpre && rp.kp >= opt.fpre_min_kp;
+  // the presolve profile describes this solve even when no presolve runs
+  EIGB_CUDA(cudaMemsetAsync(ws.get_i64("fpre_prof", 4), 0, 4 * sizeof(int64_t), st));
   auto run_presolve = [&]() {
     f_o = ws.get_i64("fpre_o", nr);
     f_delta = ws.get_f64("fpre_delta", nr);
