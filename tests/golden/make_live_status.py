@@ -33,7 +33,7 @@ from paper_1706_00773_b200.instances import default_seed, make_instance  # noqa:
 LIVE_CASES = [
     (0, 512, range(5), "pairs"),
     (1, 4096, range(2), "pairs"),
-    (4, 2048, range(3), "pairs"),
+    (4, 2048, range(5), "pairs"),
 ]
 
 

@@ -407,12 +407,22 @@ def _device_checks(api, ctx, cfg, n=None, lapack=True, oracle_roots=64):
     assert ortho <= 1e-9, ortho
     del qtq
     if lapack:
-        # independent eigensolver: cuSOLVER syevd (torch.linalg.eigvalsh) on A'
+        # independent eigensolver on A': cuSOLVER syevd (torch.linalg.eigvalsh);
+        # cuSOLVER rejects n = 32768 (cusolverDnXsyevd_bufferSize and the legacy
+        # cusolverDnDsyevd_bufferSize both return INVALID_VALUE,
+        # tools/probe_eigvalsh.py), so above 16384 MAGMA's dsyevd (torch's
+        # other backend: 88 s at n = 32768) takes its place
         a = q @ (lam[:, None] * q.T)
         a += kmat @ (sg[:, None] * kmat.T)
         a += a.T.clone()
         a *= 0.5
-        ev = torch.linalg.eigvalsh(a)
+        prev = torch.backends.cuda.preferred_linalg_library()
+        if n > 16384:
+            torch.backends.cuda.preferred_linalg_library("magma")
+        try:
+            ev = torch.linalg.eigvalsh(a)
+        finally:
+            torch.backends.cuda.preferred_linalg_library(prev)
         del a
         torch.cuda.empty_cache()
         assert float((lo - ev).abs().max()) <= 1e-10 * nrm
@@ -442,5 +452,6 @@ def test_config3_full_size_deflation(api, ctx):
 
 @pytest.mark.slow
 def test_config4_full_size(api, ctx):
-    # includes the cuSOLVER syevd eigenvalue check at n = 32768
+    # includes the LAPACK-style eigenvalue check at n = 32768 (
+    # MAGMA dsyevd, since cuSOLVER's syevd rejects this size)
     _device_checks(api, ctx, 4, lapack=True, oracle_roots=24)
