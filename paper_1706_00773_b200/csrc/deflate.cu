@@ -16,6 +16,8 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
+#include <string>
 
 namespace eigb {
 
@@ -75,10 +77,276 @@ __global__ void transform_reduce_kernel(const double* __restrict__ part, int64_t
   u[t] = s;
 }
 
+// ---------------------------------------------------------------- K1 on DMMA
+// U^T = K^T Q as a tall-skinny GEMM on the FP64 tensor pipe (m = KP rows of
+// U^T in DMMA m-tiles of 8, n = Q columns, the reduction over Q rows). At
+// k = 16 the projection needs 4 flops per byte of Q, ~0.7 of the FP64 peak
+// at full HBM bandwidth, so the FMA issue must be cheap: one
+// mma.sync.m8n8k4.f64 per 512 flops (DMMA.8x8x4), fragments from shared
+// memory. Q arrives by 1D bulk copies (cp.async.bulk, one 2 KB row segment
+// of a 256-column block each, rows padded by 64 B so the four rows of a B
+// fragment fall into different bank halves) and K by one bulk copy per stage
+// of 8 rows, into a 4-stage mbarrier ring. The grid is persistent: CTA b
+// walks the flattened (column block, row stage) range [f0, f1) in order, so
+// the ring never drains at a column-block boundary; when its column block
+// changes it stores its partial U rows as one of at most two records, and a
+// second kernel sums the records of each column block in CTA order
+// (deterministic for a given grid).
+constexpr int kK1Cols = 256;                  // Q columns per block
+constexpr int kK1Rows = 8;                    // Q rows per stage (2 k-steps)
+constexpr int kK1Ld = kK1Cols + 8;            // padded smem row (doubles)
+constexpr int kK1Threads = 256;               // 8 warps x 32 columns
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         uint64_t* bar) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(d), "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void k1_mbar_init(uint64_t* bar, unsigned count) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void k1_mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void k1_mbar_arrive(uint64_t* bar) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void k1_mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "K1WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra K1WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+struct K1Geom {
+  int64_t n, ncols, col_lo;
+  int k;
+  int64_t ncb, spc;  // column blocks, row stages per column block
+  int64_t total;     // ncb * spc
+};
+
+template <int KP, int kK1Stages>
+__global__ void __launch_bounds__(kK1Threads, (KP >= 32 ? 2 : 4)) transform_dmma_kernel(
+    const double* __restrict__ q, const double* __restrict__ kmat, K1Geom g,
+    double* __restrict__ part, int64_t* __restrict__ rec_cb) {
+  constexpr int MT = (KP + 7) / 8;  // m-tiles of 8 U columns
+  constexpr int KSTAGE = kK1Rows * (KP < 2 ? 2 : KP);  // K doubles per stage (padded)
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* sq = reinterpret_cast<double*>(smraw);                          // [S][R][Ld]
+  double* sk = sq + kK1Stages * kK1Rows * kK1Ld;                          // [S][R*k]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sk + kK1Stages * KSTAGE);
+  uint64_t* empty = full + kK1Stages;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  const int64_t f0 = g.total * b / G, f1 = g.total * (b + 1) / G;
+  if (tid == 0) {
+    for (int s = 0; s < kK1Stages; ++s) {
+      k1_mbar_init(&full[s], 1);
+      k1_mbar_init(&empty[s], kK1Threads / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // producer position (thread 0): the next flattened stage to issue, as a
+  // running (column block, row stage) pair (no 64-bit divisions in the loop)
+  int64_t p_cb = f0 / g.spc, p_st = f0 % g.spc;
+  int p_slot = 0;
+  auto issue = [&]() {
+    const int s = p_slot;
+    const int64_t cb = p_cb, st = p_st;
+    p_slot = (p_slot + 1 == kK1Stages) ? 0 : p_slot + 1;
+    if (++p_st == g.spc) p_st = 0, ++p_cb;
+    const int64_t r0 = st * kK1Rows;
+    const int rows = (int)min((int64_t)kK1Rows, g.n - r0);
+    const int64_t c0 = g.col_lo + cb * kK1Cols;
+    const int cols = (int)min((int64_t)kK1Cols, g.col_lo + g.ncols - c0);
+    const unsigned qb = (unsigned)cols * 8u, kb = (unsigned)(rows * g.k) * 8u;
+    k1_mbar_expect_tx(&full[s], qb * (unsigned)rows + kb);
+    double* dq = sq + (size_t)s * kK1Rows * kK1Ld;
+    for (int r = 0; r < rows; ++r) bulk_g2s(dq + r * kK1Ld, q + (r0 + r) * g.n + c0, qb, &full[s]);
+    bulk_g2s(sk + (size_t)s * KSTAGE, kmat + r0 * g.k, kb, &full[s]);
+  };
+  if (tid == 0)
+    for (int64_t f = f0; f < f1 && f < f0 + kK1Stages; ++f) issue();
+
+  double acc[MT][4][2];
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[m][j][0] = acc[m][j][1] = 0.0;
+  const int t4 = lane & 3, g8 = lane >> 2;
+  int slot = 0;
+  int64_t cur_cb = f0 / g.spc;
+  auto flush = [&](int64_t cb) {
+    const int64_t c0 = cb * kK1Cols;  // relative to col_lo
+    double* out = part + (size_t)(b * 2 + slot) * kK1Cols * KP;
+    if (tid == 0) rec_cb[b * 2 + slot] = cb;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int col = warp * 32 + nt * 8 + 2 * t4 + j;
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          const int kc = m * 8 + g8;
+          if (kc < KP && c0 + col < g.ncols) out[col * KP + kc] = acc[m][nt][j];
+          acc[m][nt][j] = 0.0;
+        }
+      }
+    ++slot;
+  };
+  int64_t c_st = f0 % g.spc;  // consumer row stage within cur_cb
+  int s = 0;                  // ring slot of iteration it
+  unsigned phase = 0;         // its mbarrier parity
+  int ps = kK1Stages - 1;     // slot of the previous iteration
+  unsigned pphase = 1;
+  const int64_t iters = f1 - f0;
+  for (int64_t it = 0; it < iters; ++it) {
+    if (c_st == g.spc) {
+      flush(cur_cb);
+      ++cur_cb;
+      c_st = 0;
+    }
+    // refill the slot released in the previous iteration
+    if (tid == 0 && it > 0 && it - 1 + kK1Stages < iters) {
+      k1_mbar_wait(&empty[ps], pphase);
+      issue();
+    }
+    k1_mbar_wait(&full[s], phase);
+    const int64_t r0 = c_st * kK1Rows;
+    const int rows = (int)min((int64_t)kK1Rows, g.n - r0);
+    const double* dq = sq + (size_t)s * kK1Rows * kK1Ld + warp * 32;
+    const double* dk = sk + (size_t)s * KSTAGE;
+#pragma unroll
+    for (int ks = 0; ks < kK1Rows / 4; ++ks) {
+      const int r = ks * 4 + t4;
+      const bool ok = r < rows;
+      double a[MT];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const int kc = m * 8 + g8;
+        a[m] = (ok && kc < g.k) ? dk[r * g.k + kc] : 0.0;
+      }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const double bq = ok ? dq[r * kK1Ld + nt * 8 + g8] : 0.0;
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+          asm volatile(
+              "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+              : "+d"(acc[m][nt][0]), "+d"(acc[m][nt][1])
+              : "d"(a[m]), "d"(bq));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) k1_mbar_arrive(&empty[s]);
+    ps = s;
+    pphase = phase;
+    if (++s == kK1Stages) s = 0, phase ^= 1u;
+    ++c_st;
+  }
+  if (f1 > f0) flush(cur_cb);
+}
+
+// U[c, :] = sum of the records of column block c / 256, in CTA order.
+template <int KP>
+__global__ void transform_dmma_reduce_kernel(const double* __restrict__ part,
+                                             const int64_t* __restrict__ rec_cb, K1Geom g,
+                                             int64_t grid, double* __restrict__ u) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= g.ncols * KP) return;
+  const int64_t c = t / KP;
+  const int kc = (int)(t % KP);
+  const int64_t cb = c / kK1Cols;
+  const int col = (int)(c % kK1Cols);
+  // CTAs whose range touches column block cb: [cb*spc, (cb+1)*spc) of the
+  // flattened range, b = floor(f * G / total) .. (monotone)
+  const int64_t blo = (cb * g.spc) * grid / g.total;
+  const int64_t bhi = min(grid - 1, (((cb + 1) * g.spc) * grid + g.total - 1) / g.total);
+  double s = 0.0;
+  for (int64_t b = max((int64_t)0, blo - 1); b <= bhi; ++b)
+    for (int sl = 0; sl < 2; ++sl)
+      if (rec_cb[b * 2 + sl] == cb) s += part[(size_t)(b * 2 + sl) * kK1Cols * KP + col * KP + kc];
+  u[t] = s;
+}
+
+template <int KP, int kK1Stages>
+void launch_transform_dmma_s(const double* q, const double* kmat, int64_t n, int k, int64_t col_lo,
+                             int64_t col_hi, double* u, DeviceScratch& ws, int sms, cudaStream_t st) {
+  constexpr int KSTAGE = kK1Rows * (KP < 2 ? 2 : KP);
+  const size_t smem = (size_t)kK1Stages * kK1Rows * kK1Ld * 8 + (size_t)kK1Stages * KSTAGE * 8 +
+                      2 * kK1Stages * 8;
+  static bool attr = false;
+  if (!attr) {
+    EIGB_CUDA(cudaFuncSetAttribute(transform_dmma_kernel<KP, kK1Stages>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  int per_sm = 0;
+  EIGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, transform_dmma_kernel<KP, kK1Stages>,
+                                                          kK1Threads, smem));
+  K1Geom g;
+  g.n = n;
+  g.ncols = col_hi - col_lo;
+  g.col_lo = col_lo;
+  g.k = k;
+  g.ncb = cdiv(g.ncols, kK1Cols);
+  g.spc = cdiv(n, kK1Rows);
+  g.total = g.ncb * g.spc;
+  // persistent grid: every resident slot busy, at least one CTA per column
+  // block (so a CTA's range spans at most two column blocks)
+  const int64_t grid = std::min<int64_t>(g.total, std::max<int64_t>((int64_t)std::max(1, per_sm) * sms, g.ncb));
+  double* part = ws.get_f64("tf_dpart", (size_t)grid * 2 * kK1Cols * KP);
+  int64_t* rec = ws.get_i64("tf_drec", (size_t)grid * 2);
+  EIGB_CUDA(cudaMemsetAsync(rec, 0xff, 8 * (size_t)grid * 2, st));  // -1: no record
+  transform_dmma_kernel<KP, kK1Stages><<<(unsigned)grid, kK1Threads, smem, st>>>(q, kmat, g, part, rec);
+  EIGB_LAUNCH_CHECK();
+  const int64_t cnt = g.ncols * KP;
+  transform_dmma_reduce_kernel<KP><<<(unsigned)cdiv(cnt, 256), 256, 0, st>>>(part, rec, g, grid, u);
+  EIGB_LAUNCH_CHECK();
+}
+
+// Ring depth: 3 stages (17 KB each at k = 16) let 4 CTAs share an SM: 32
+// warps hide the DMMA latency better than 2 CTAs of 4 stages
+// (EIGMOD_B200_K1_STAGES = 2..4 for experiments).
+template <int KP>
+void launch_transform_dmma(const double* q, const double* kmat, int64_t n, int k, int64_t col_lo,
+                           int64_t col_hi, double* u, DeviceScratch& ws, int sms, cudaStream_t st) {
+  static const char* env = std::getenv("EIGMOD_B200_K1_STAGES");
+  const int stages = env ? std::atoi(env) : 3;
+  if (stages == 2) launch_transform_dmma_s<KP, 2>(q, kmat, n, k, col_lo, col_hi, u, ws, sms, st);
+  else if (stages == 4) launch_transform_dmma_s<KP, 4>(q, kmat, n, k, col_lo, col_hi, u, ws, sms, st);
+  else launch_transform_dmma_s<KP, 3>(q, kmat, n, k, col_lo, col_hi, u, ws, sms, st);
+}
+
 template <int KP>
 void launch_transform(const double* q, const double* kmat, int64_t n, int k, int64_t col_lo,
                       int64_t col_hi, double* u, DeviceScratch& ws, int sms, cudaStream_t st) {
   const int64_t ncols = col_hi - col_lo;
+  // DMMA path: 16-byte aligned bulk copies need even n, column range and
+  // 16-byte aligned Q and K (EIGMOD_B200_K1=fma selects the DFMA kernel)
+  static const char* env = std::getenv("EIGMOD_B200_K1");
+  const bool aligned = (n % 2 == 0) && (col_lo % 2 == 0) && (ncols % 2 == 0) &&
+                       (reinterpret_cast<uintptr_t>(q) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(kmat) % 16 == 0);
+  if (aligned && !(env && std::string(env) == "fma")) {
+    launch_transform_dmma<KP>(q, kmat, n, k, col_lo, col_hi, u, ws, sms, st);
+    return;
+  }
   const int64_t gx = cdiv(ncols, kTfCols);
   int64_t splits = std::max<int64_t>(1, cdiv(4 * (int64_t)sms, gx));
   splits = std::min<int64_t>(splits, cdiv(n, kTfRows));

@@ -36,8 +36,22 @@ constexpr int kPoleTile = 64;
 template <int KP>
 struct PassCfg {
   static constexpr int P = KP * (KP + 1) / 2;
+  // KP = 8, 16: the FMA phase on the FP64 tensor pipe (DMMA.8x8x4, see
+  // pass_body_mma); other ranks: DFMA with compile-time entries
+  static constexpr bool MMA = (KP == 8 || KP == 16);
   static constexpr int EG = (KP <= 8) ? 1 : (KP == 16 ? 2 : 8);
   static constexpr int PS = kPassWarps / EG;
+  // MMA layout: S (32 slots x P entries) = D (32 x poles) W (poles x P),
+  // W[i][e] = u_i[r_e] u_i[c_e]: 4 m-tiles of 8 slots, NT n-tiles of 8
+  // entries split into NG contiguous groups, MPS pole splits (NG x MPS = 8
+  // warps).
+  static constexpr int NT = (P + 7) / 8;
+  static constexpr int NG = (KP == 16) ? 2 : 1;
+  static constexpr int MPS = kPassWarps / NG;
+  __host__ __device__ static constexpr int nt_lo(int g) { return (NT * g) / NG; }
+  // u rows in the tile: padded to 64 B mod 128 B in MMA mode, so the four
+  // pole rows of a B fragment fall into different bank halves
+  static constexpr int LDU = MMA ? KP + 8 : KP;
   // Entry group g = packed entries [e_lo(g), e_lo(g+1)): an even split of the
   // packed triangle (a row may straddle two groups), so no warp waits for the
   // other group at the tile barriers.
@@ -59,10 +73,18 @@ struct PassCfg {
   static constexpr int OUT = P + 3;
   static constexpr int IG = P, IF = P + 1, IFP = P + 2;
   // shared memory (doubles): tile = d, alpha, u rows
-  // poles per tile: 128 (64 for KP = 32, whose reduction buffer is 136 KB)
-  static constexpr int T = (KP >= 32) ? kPoleTile : 2 * kPoleTile;
-  static constexpr int TILE_DOUBLES = T * (KP + 2);
-  static constexpr int DBUF_DOUBLES = T * 32;
+  // poles per tile: 128 (64 for KP = 32, whose reduction buffer is 136 KB;
+  // 64 in MMA mode, 16 k-steps of 4 poles)
+  static constexpr int T = MMA ? kPoleTile : ((KP >= 32) ? kPoleTile : 2 * kPoleTile);
+  static constexpr int TILE_DOUBLES = T * (LDU + 2);
+  // D buffer: lane = slot order (DFMA), or A fragments per k-step and m-tile
+  // in blocks of 33 (conflict-free writes by slot and reads by fragment lane)
+  static constexpr int DBUF_MIN = MMA ? (T / 4) * 4 * 33 : T * 32;
+  // the solver and K2 overlay their k x k factors (32 KP^2 doubles for
+  // KP <= 16) on the tiles and the D buffer
+  static constexpr int FACT = (KP <= 16) ? 32 * KP * KP : 0;
+  static constexpr int DBUF_DOUBLES =
+      (2 * TILE_DOUBLES + DBUF_MIN >= FACT) ? DBUF_MIN : FACT - 2 * TILE_DOUBLES;
   static constexpr int RED_DOUBLES = 32 * OUT;
   static constexpr int SMEM_DOUBLES = 2 * TILE_DOUBLES + DBUF_DOUBLES + RED_DOUBLES;
 };
@@ -93,7 +115,7 @@ __device__ __forceinline__ void load_pole_tile(double* tile, const double* __res
                                                int64_t n) {
   // tile layout: [T] d, [T] alpha, then [T][KP] rows. Rows beyond n are zero
   // with d = NaN (NaN difference => term skipped).
-  constexpr int T = PassCfg<KP>::T;
+  constexpr int T = PassCfg<KP>::T, LDU = PassCfg<KP>::LDU;
   double* td = tile;
   double* ta = tile + T;
   double* tu = tile + 2 * T;
@@ -106,13 +128,13 @@ __device__ __forceinline__ void load_pole_tile(double* tile, const double* __res
   if constexpr (KP >= 2) {
     constexpr int CH = KP / 2;  // 16-byte chunks per row
     const double2* src = reinterpret_cast<const double2*>(u + i0 * KP);
-    double2* dst = reinterpret_cast<double2*>(tu);
     for (int t = tid; t < T * CH; t += kPassThreads) {
+      double2* dst = reinterpret_cast<double2*>(tu + (t / CH) * LDU) + (t % CH);
       if (t < cnt * CH) {
-        const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst + t));
+        const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst));
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(src + t));
       } else {
-        dst[t] = make_double2(0.0, 0.0);
+        *dst = make_double2(0.0, 0.0);
       }
     }
   } else {
@@ -278,6 +300,162 @@ __device__ __forceinline__ void pass_body(const double* __restrict__ d, const do
   if (hit) atomicOr(&slots.hit[lane], 1);
 }
 
+// The pass with its FMA phase on the FP64 tensor pipe (KP = 8, 16):
+//   S[b][e] = sum_i D[i][b] W[i][e],  W[i][e] = u_i[r_e] u_i[c_e]
+// as mma.sync.m8n8k4.f64 tiles (M = 32 slots in 4 m-tiles, N = P packed
+// entries in n-tiles of 8, K = the poles of the tile in k-steps of 4). The D
+// phase is the DFMA pass's (lane = slot: the reciprocal, g, f, f'), writing
+// D in A-fragment order. A B fragment element (pole 4 ks + lane % 4, entry
+// 8 nt + lane / 4) is the product of two u entries of the pole's row, formed
+// where it is consumed: each (pole, entry) product once per CTA, reused by
+// the 4 m-tiles. One DMMA replaces 16 warp-wide DFMAs (512 flops per issue),
+// so the FP64 budget, which DFMA and DMMA share on B200
+// (profiles/coissue_dmma_dfma_r02.json), goes to the contraction instead of
+// instruction issue. Warp = (n-group G, pole split p).
+template <int KP, int G>
+__device__ __forceinline__ void pass_body_mma(const double* __restrict__ d,
+                                              const double* __restrict__ u, int64_t n,
+                                              const PassSlots& slots, const PassOpts& o,
+                                              double* tiles, double* dbuf, double* red, int p) {
+  using C = PassCfg<KP>;
+  constexpr int NT0 = C::nt_lo(G), NTL = C::nt_lo(G + 1) - C::nt_lo(G);
+  constexpr int KSW = (C::T / 4) / C::MPS;  // k-steps per warp per tile
+  constexpr int LDU = C::LDU;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int t4 = lane & 3, g8 = lane >> 2;
+  const double dob = slots.dob[lane];
+  const double del = slots.delta[lane];
+  const bool act = slots.active[lane] != 0;
+  const bool sig = o.want_sigma;
+  const bool wf = o.alpha != nullptr;
+  double yv[KP];
+#pragma unroll
+  for (int c = 0; c < KP; ++c) yv[c] = sig ? slots.y[lane * KP + c] : 0.0;
+  // this lane's B entries: (row, column) of packed entry 8 nt + lane / 4
+  int er[NTL], ec[NTL];
+#pragma unroll
+  for (int j = 0; j < NTL; ++j) {
+    const int e = 8 * (NT0 + j) + g8;
+    er[j] = (e < C::P) ? C::row_of(e) : 0;
+    ec[j] = (e < C::P) ? C::col_of(e) : 0;
+  }
+  double acc[4][NTL][2];
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int j = 0; j < NTL; ++j) acc[m][j][0] = acc[m][j][1] = 0.0;
+  double gs = 0.0, fs = 0.0, fps = 0.0;
+  int hit = 0;
+  // D write position of this slot within a k-step block
+  const int dslot = (lane >> 3) * 33 + (lane & 7) * 4;
+
+  const int64_t ntiles = (n + C::T - 1) / C::T;
+  if (ntiles > 0) load_pole_tile<KP>(tiles, d, o.alpha, u, 0, n);
+  for (int64_t t = 0; t < ntiles; ++t) {
+    const double* cur = tiles + (t & 1) * C::TILE_DOUBLES;
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // tile t landed; previous MMA phase done with dbuf
+    if (t + 1 < ntiles)
+      load_pole_tile<KP>(tiles + ((t + 1) & 1) * C::TILE_DOUBLES, d, o.alpha, u,
+                         (t + 1) * C::T, n);
+    const double* td = cur;
+    const double* ta = cur + C::T;
+    const double* tu = cur + 2 * C::T;
+    // ---- D phase (lane = slot)
+#pragma unroll 4
+    for (int i = warp; i < C::T; i += kPassWarps) {
+      const double diff = (td[i] - dob) - del;
+      double D;
+      if (o.excl_gap > 0.0) {
+        const int64_t xr = slots.excl_row ? slots.excl_row[lane] : -1;
+        const bool ex = (xr >= 0) ? (t * C::T + i == xr) : (fabs(td[i] - dob) < o.excl_gap);
+        D = (act && !ex && diff == diff) ? rcp64(diff) : 0.0;
+      } else if (diff == 0.0) {
+        hit |= !o.exclude_zero;
+        D = 0.0;
+      } else {
+        D = (act && diff == diff) ? rcp64(diff) : 0.0;
+      }
+      dbuf[(i >> 2) * 132 + dslot + (i & 3)] = D;
+      if (sig) {
+        double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+        for (int c = 0; c < KP; c += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(tu + i * LDU + c);
+          t0 = fma(v.x, yv[c], t0);
+          t1 = fma(v.y, yv[c + 1], t1);
+        }
+        const double td2 = (t0 + t1) * D;
+        gs = fma(td2, td2, gs);
+      }
+      if (wf) {
+        const double aD = ta[i] * D;
+        fs += aD;
+        fps = fma(aD, D, fps);
+      }
+    }
+    __syncthreads();  // D of this tile visible
+    // ---- MMA phase: k-steps p * KSW .. of this tile
+#pragma unroll
+    for (int kk = 0; kk < KSW; ++kk) {
+      const int ks = p * KSW + kk;
+      double a[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) a[m] = dbuf[ks * 132 + m * 33 + lane];
+      const double* ur = tu + (4 * ks + t4) * LDU;
+#pragma unroll
+      for (int j = 0; j < NTL; ++j) {
+        const double b = ur[er[j]] * ur[ec[j]];
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          asm volatile(
+              "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+              : "+d"(acc[m][j][0]), "+d"(acc[m][j][1])
+              : "d"(a[m]), "d"(b));
+      }
+    }
+  }
+  __syncthreads();
+
+  // Deterministic reduction: the C fragments (slot 8 m + lane / 4, entries
+  // 8 nt + 2 (lane % 4) + h) over pole splits p = 0.. in order, D-phase
+  // partials (g, f, f') over warps 0..7 in order.
+  constexpr int OUT = C::OUT;
+  for (int q = 0; q < C::MPS; ++q) {
+    if (p == q) {
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int j = 0; j < NTL; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int e = 8 * (NT0 + j) + 2 * t4 + h;
+            if (e < C::P) {
+              double* r = red + (8 * m + g8) * OUT + e;
+              *r = (q == 0) ? acc[m][j][h] : *r + acc[m][j][h];
+            }
+          }
+    }
+    __syncthreads();
+  }
+  for (int q = 0; q < kPassWarps; ++q) {
+    if (warp == q) {
+      if (q == 0) {
+        red[lane * OUT + C::IG] = gs;
+        red[lane * OUT + C::IF] = fs;
+        red[lane * OUT + C::IFP] = fps;
+      } else {
+        red[lane * OUT + C::IG] += gs;
+        red[lane * OUT + C::IF] += fs;
+        red[lane * OUT + C::IFP] += fps;
+      }
+    }
+    __syncthreads();
+  }
+  if (hit) atomicOr(&slots.hit[lane], 1);
+}
+
 // Runs the pass. On return (after __syncthreads) red[b * OUT + e] holds the
 // packed S_b (without J) and red[b*OUT + P..P+2] = g_b, f_b - 1, f'_b.
 // smem: SMEM_DOUBLES doubles (tiles, D buffer, reduction).
@@ -289,6 +467,16 @@ __device__ void secular_pass(const double* __restrict__ d, const double* __restr
   double* dbuf = tiles + 2 * C::TILE_DOUBLES;
   double* red = dbuf + C::DBUF_DOUBLES;
   const int warp = threadIdx.x >> 5;
+  if constexpr (C::MMA) {
+    const int g = warp % C::NG;
+    const int p = warp / C::NG;
+    if (g == 0) pass_body_mma<KP, 0>(d, u, n, slots, o, tiles, dbuf, red, p);
+    if constexpr (C::NG > 1) {
+      if (g == 1) pass_body_mma<KP, 1>(d, u, n, slots, o, tiles, dbuf, red, p);
+    }
+    __syncthreads();
+    return;
+  }
   const int g = warp % C::EG;
   const int p = warp / C::EG;
 #define EIGB_PASS_CASE(GG)                                                     \

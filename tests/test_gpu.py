@@ -46,6 +46,39 @@ def test_transform_update(api, ctx, name, c):
     assert np.abs(u - c["u"]).max() <= 1e-13 * scale
 
 
+@pytest.mark.parametrize("n,k", [(2, 1), (8, 3), (64, 16), (130, 2), (256, 5), (512, 32),
+                                 (1000, 16), (1026, 8), (333, 4), (4096, 16)])
+def test_projection_dmma_vs_numpy(api, ctx, n, k):
+    """K1 on the DMMA path (even n) and the DFMA path (odd n, misaligned
+    slices): U = Q^T K to FP64 rounding of the products, every padded rank,
+    partial column blocks, partial row stages, multi-GPU column slices."""
+    import torch
+
+    rng = np.random.default_rng(n * 100 + k)
+    q = rng.standard_normal((n, n))
+    kmat = rng.standard_normal((n, k))
+    want = q.T @ kmat
+    scale = np.abs(q).T @ np.abs(kmat)
+    u = api.transform_update(q, kmat, ctx=ctx)
+    assert np.all(np.abs(u - want) <= 1e-14 * n * scale + 1e-300)
+    from paper_1706_00773_b200.sharded import CudaBackend, split
+
+    dev = torch.device("cuda", 0)
+    tq, tk = torch.from_numpy(q).to(dev), torch.from_numpy(kmat).to(dev)
+    ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+    be = CudaBackend(ctx, n, k, np.ones(k, np.int32))
+    for world in (2, 3):
+        for r in range(world):
+            lo, hi, ch = split(n, world, r)
+            part = torch.zeros((max(ch, 1), be.kp), dtype=torch.float64, device=dev)
+            if hi > lo:
+                be.project(tq, tk, lo, hi, part)
+            torch.cuda.synchronize()
+            got = part[: hi - lo, :k].cpu().numpy()
+            assert np.all(np.abs(got - want[lo:hi]) <= 1e-14 * n * scale[lo:hi] + 1e-300)
+    ctx.set_stream(None)
+
+
 @pytest.mark.parametrize("name,c", SEEDED_CASES, ids=IDS)
 def test_deflation_record_matches_reference(api, ctx, name, c):
     d = api.deflate_problem(c["lam"], c["u"], c["signs"], ctx=ctx)

@@ -56,8 +56,6 @@ __global__ void loop(double* out, int iters, double a, double b) {
       for (int i = 0; i < MCH; ++i) dmma(c[i][0], c[i][1], A, B);
     }
   } else if (f_warp) {
-    // DFMA-only warps do 4x the iterations' worth of chains per step so the
-    // two roles take comparable time
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
       for (int i = 0; i < FCH; ++i) f[i] = fma(f[i], a, b);
