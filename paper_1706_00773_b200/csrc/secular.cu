@@ -927,11 +927,15 @@ __global__ void __launch_bounds__(kPassThreads, 1) count_sweep_kernel(ReducedVie
   extern __shared__ __align__(16) double smem[];
   // factor storage: interleaved [KP*KP][32] in shared memory for KP <= 16,
   // per-slot matrices in global scratch above (32 x 32 x 32 doubles do not fit)
+  // (KP <= 16: overlays the pass's tiles and D buffer, dead after the pass;
+  // the pass result lies beyond them)
   constexpr bool kSmemF = KP <= 16;
-  double* F = kSmemF ? smem + C::SMEM_DOUBLES : gscratch + (size_t)blockIdx.x * 32 * KP * KP;
+  static_assert(!kSmemF || 32 * KP * KP <= 2 * C::TILE_DOUBLES + C::DBUF_DOUBLES,
+                "factor storage must fit in the pass tiles");
+  double* F = kSmemF ? smem : gscratch + (size_t)blockIdx.x * 32 * KP * KP;
   const size_t esl = kSmemF ? 1 : (size_t)KP * KP;
   constexpr int es = kSmemF ? 32 : 1;
-  ParSmem<KP>& P = *reinterpret_cast<ParSmem<KP>*>(smem + C::SMEM_DOUBLES + (kSmemF ? 32 * KP * KP : 0));
+  ParSmem<KP>& P = *reinterpret_cast<ParSmem<KP>*>(smem + C::SMEM_DOUBLES);
   __shared__ double dob[32], delta[32];
   __shared__ int active[32], hit[32];
   const int t = threadIdx.x;
@@ -1460,11 +1464,14 @@ __global__ void __launch_bounds__(kPassThreads, 1) group_weights_kernel(WeightAr
   o.exclude_zero = true;
   secular_pass<KP>(a.rep, a.u, a.n, sl, o, smem);
   const double* red = pass_result<KP>(smem);
+  // (KP <= 16: overlays the pass's tiles and D buffer, dead after the pass)
   constexpr bool kSmemF = KP <= 16;
-  double* F = kSmemF ? smem + C::SMEM_DOUBLES : a.scratch + (size_t)blockIdx.x * 32 * 4 * KP * KP;
+  static_assert(!kSmemF || 32 * KP * KP <= 2 * C::TILE_DOUBLES + C::DBUF_DOUBLES,
+                "factor storage must fit in the pass tiles");
+  double* F = kSmemF ? smem : a.scratch + (size_t)blockIdx.x * 32 * 4 * KP * KP;
   const size_t esl = kSmemF ? 1 : (size_t)4 * KP * KP;
   constexpr int es = kSmemF ? 32 : 1;
-  ParSmem<KP>& P = *reinterpret_cast<ParSmem<KP>*>(smem + C::SMEM_DOUBLES + (kSmemF ? 32 * KP * KP : 0));
+  ParSmem<KP>& P = *reinterpret_cast<ParSmem<KP>*>(smem + C::SMEM_DOUBLES);
   if (t < 32) {
     P.ev[t] = active[t];
     P.neg[t] = 0;
@@ -1569,13 +1576,12 @@ template <int KP>
 void launch_sweep(const ReducedView& rp, int* counts, int64_t qbeg, int64_t qend,
                   DeviceScratch& ws, cudaStream_t st) {
   using C = PassCfg<KP>;
-  constexpr bool kSmemF = KP <= 16;
-  const size_t sm = sizeof(double) * (C::SMEM_DOUBLES + (kSmemF ? 32 * KP * KP : 0)) + sizeof(ParSmem<KP>);
+  const size_t sm = sizeof(double) * C::SMEM_DOUBLES + sizeof(ParSmem<KP>);
   EIGB_CUDA(cudaFuncSetAttribute(count_sweep_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sm));
   if (qend <= qbeg) return;
   const int64_t grid = cdiv(qend - qbeg, 32);
-  double* gs = kSmemF ? nullptr : ws.get_f64("sweep_scratch", (size_t)grid * 32 * KP * KP);
+  double* gs = KP <= 16 ? nullptr : ws.get_f64("sweep_scratch", (size_t)grid * 32 * KP * KP);
   count_sweep_kernel<KP><<<(unsigned)grid, kPassThreads, sm, st>>>(rp, counts, qbeg, qend, gs);
   EIGB_LAUNCH_CHECK();
 }
@@ -1695,8 +1701,7 @@ void launch_weights(const double* rep, const double* u, int64_t n, const int64_t
   WeightArgs<KP> a{rep, u, n, gstart, glen, gval, ng, sgn, k, alpha, nullptr};
   const int grid = (int)cdiv(ng, 32);
   a.scratch = ws.get_f64("weights_scratch", (size_t)grid * 32 * 4 * KP * KP);
-  const size_t sm = sizeof(double) * (C::SMEM_DOUBLES + (KP <= 16 ? 32 * KP * KP : 0)) +
-                    sizeof(ParSmem<KP>);
+  const size_t sm = sizeof(double) * C::SMEM_DOUBLES + sizeof(ParSmem<KP>);
   EIGB_CUDA(cudaFuncSetAttribute(group_weights_kernel<KP>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   group_weights_kernel<KP><<<grid, kPassThreads, sm, st>>>(a);

@@ -20,7 +20,11 @@ ctx = capi.Context(0)
 ctx.set_option("timing", 1)
 lo = torch.empty(a.n, dtype=torch.float64, device=dev)
 qo = torch.empty((a.n, a.n), dtype=torch.float64, device=dev)
-for _ in range(a.reps):
+for r in range(a.reps):
+    if r == 1:  # the first call pays the one-time setup (workspaces, attributes)
+        torch.cuda.synchronize()
+        ctx.stage_times(reset=True)
     capi.update_decomposition_device(q, lam, kmat, signs.numpy(), lo, qo, ctx=ctx)
 torch.cuda.synchronize()
-print(ctx.stage_times(), ctx.stats())
+st = ctx.stage_times()
+print({k: (v / max(1, st["calls"]) if k != "calls" else v) for k, v in st.items()}, ctx.stats())
