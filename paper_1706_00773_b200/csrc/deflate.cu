@@ -135,14 +135,32 @@ __device__ __forceinline__ void k1_mbar_wait(uint64_t* bar, unsigned parity) {
 struct K1Geom {
   int64_t n, ncols, col_lo;
   int k;
-  int64_t ncb, spc;  // column blocks, row stages per column block
-  int64_t total;     // ncb * spc
+  int64_t ncb;   // 256-column blocks
+  int64_t spc;   // row stages (8 rows) per column block
+  int64_t cs;    // row stages per chunk (a function of n only)
+  int64_t nch;   // chunks per column block
+  int64_t items; // ncb * nch work items (column block, row chunk)
+};
+
+// Work item i = (column block i / nch, row chunk i % nch): its stages
+// (32-bit: at most 2^31 / 8 rows, far beyond 180 GB of Q).
+__device__ __forceinline__ void k1_item(const K1Geom& g, int i, int* cb, int* st0, int* st1) {
+  *cb = i / (int)g.nch;
+  const int m = i - *cb * (int)g.nch;
+  *st0 = m * (int)g.cs;
+  *st1 = min((int)g.spc, *st0 + (int)g.cs);
+}
+
+// The producer's position (thread 0 only): kept in shared memory, off the
+// consumers' register budget.
+struct K1Prod {
+  int item, cb, st, end, slot;
 };
 
 template <int KP, int kK1Stages>
 __global__ void __launch_bounds__(kK1Threads, (KP >= 32 ? 2 : 4)) transform_dmma_kernel(
     const double* __restrict__ q, const double* __restrict__ kmat, K1Geom g,
-    double* __restrict__ part, int64_t* __restrict__ rec_cb) {
+    double* __restrict__ part) {
   constexpr int MT = (KP + 7) / 8;  // m-tiles of 8 U columns
   constexpr int KSTAGE = kK1Rows * (KP < 2 ? 2 : KP);  // K doubles per stage (padded)
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -152,7 +170,9 @@ __global__ void __launch_bounds__(kK1Threads, (KP >= 32 ? 2 : 4)) transform_dmma
   uint64_t* empty = full + kK1Stages;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t G = gridDim.x, b = blockIdx.x;
-  const int64_t f0 = g.total * b / G, f1 = g.total * (b + 1) / G;
+  const int i0 = (int)(g.items * b / G), i1 = (int)(g.items * (b + 1) / G);
+  if (i1 <= i0) return;
+  __shared__ K1Prod pp;
   if (tid == 0) {
     for (int s = 0; s < kK1Stages; ++s) {
       k1_mbar_init(&full[s], 1);
@@ -161,15 +181,25 @@ __global__ void __launch_bounds__(kK1Threads, (KP >= 32 ? 2 : 4)) transform_dmma
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // producer position (thread 0): the next flattened stage to issue, as a
-  // running (column block, row stage) pair (no 64-bit divisions in the loop)
-  int64_t p_cb = f0 / g.spc, p_st = f0 % g.spc;
-  int p_slot = 0;
+  // stages of this CTA's items in order; iters = their total
+  int iters = 0;
+  for (int i = i0; i < i1; ++i) {
+    int cb, a, e;
+    k1_item(g, i, &cb, &a, &e);
+    iters += e - a;
+  }
+  // producer position: the next stage to issue as a running (item, stage)
+  // pair (no divisions per stage)
+  if (tid == 0) {
+    pp.item = i0;
+    k1_item(g, i0, &pp.cb, &pp.st, &pp.end);
+    pp.slot = 0;
+  }
   auto issue = [&]() {
-    const int s = p_slot;
-    const int64_t cb = p_cb, st = p_st;
-    p_slot = (p_slot + 1 == kK1Stages) ? 0 : p_slot + 1;
-    if (++p_st == g.spc) p_st = 0, ++p_cb;
+    const int s = pp.slot;
+    const int64_t cb = pp.cb, st = pp.st;
+    pp.slot = (pp.slot + 1 == kK1Stages) ? 0 : pp.slot + 1;
+    if (++pp.st == pp.end && ++pp.item < i1) k1_item(g, pp.item, &pp.cb, &pp.st, &pp.end);
     const int64_t r0 = st * kK1Rows;
     const int rows = (int)min((int64_t)kK1Rows, g.n - r0);
     const int64_t c0 = g.col_lo + cb * kK1Cols;
@@ -181,7 +211,7 @@ __global__ void __launch_bounds__(kK1Threads, (KP >= 32 ? 2 : 4)) transform_dmma
     bulk_g2s(sk + (size_t)s * KSTAGE, kmat + r0 * g.k, kb, &full[s]);
   };
   if (tid == 0)
-    for (int64_t f = f0; f < f1 && f < f0 + kK1Stages; ++f) issue();
+    for (int f = 0; f < iters && f < kK1Stages; ++f) issue();
 
   double acc[MT][4][2];
 #pragma unroll
@@ -189,12 +219,10 @@ __global__ void __launch_bounds__(kK1Threads, (KP >= 32 ? 2 : 4)) transform_dmma
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[m][j][0] = acc[m][j][1] = 0.0;
   const int t4 = lane & 3, g8 = lane >> 2;
-  int slot = 0;
-  int64_t cur_cb = f0 / g.spc;
-  auto flush = [&](int64_t cb) {
+  // the item's partial U rows: record `item` (summed over chunks in order)
+  auto flush = [&](int item, int cb) {
     const int64_t c0 = cb * kK1Cols;  // relative to col_lo
-    double* out = part + (size_t)(b * 2 + slot) * kK1Cols * KP;
-    if (tid == 0) rec_cb[b * 2 + slot] = cb;
+    double* out = part + (size_t)item * kK1Cols * KP;
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
@@ -207,27 +235,21 @@ __global__ void __launch_bounds__(kK1Threads, (KP >= 32 ? 2 : 4)) transform_dmma
           acc[m][nt][j] = 0.0;
         }
       }
-    ++slot;
   };
-  int64_t c_st = f0 % g.spc;  // consumer row stage within cur_cb
+  int c_item = i0, c_cb, c_st, c_end;
+  k1_item(g, c_item, &c_cb, &c_st, &c_end);
   int s = 0;                  // ring slot of iteration it
   unsigned phase = 0;         // its mbarrier parity
   int ps = kK1Stages - 1;     // slot of the previous iteration
   unsigned pphase = 1;
-  const int64_t iters = f1 - f0;
-  for (int64_t it = 0; it < iters; ++it) {
-    if (c_st == g.spc) {
-      flush(cur_cb);
-      ++cur_cb;
-      c_st = 0;
-    }
+  for (int it = 0; it < iters; ++it) {
     // refill the slot released in the previous iteration
     if (tid == 0 && it > 0 && it - 1 + kK1Stages < iters) {
       k1_mbar_wait(&empty[ps], pphase);
       issue();
     }
     k1_mbar_wait(&full[s], phase);
-    const int64_t r0 = c_st * kK1Rows;
+    const int64_t r0 = (int64_t)c_st * kK1Rows;
     const int rows = (int)min((int64_t)kK1Rows, g.n - r0);
     const double* dq = sq + (size_t)s * kK1Rows * kK1Ld + warp * 32;
     const double* dk = sk + (size_t)s * KSTAGE;
@@ -257,30 +279,28 @@ __global__ void __launch_bounds__(kK1Threads, (KP >= 32 ? 2 : 4)) transform_dmma
     ps = s;
     pphase = phase;
     if (++s == kK1Stages) s = 0, phase ^= 1u;
-    ++c_st;
+    if (++c_st == c_end) {
+      flush(c_item, c_cb);
+      if (++c_item < i1) k1_item(g, c_item, &c_cb, &c_st, &c_end);
+    }
   }
-  if (f1 > f0) flush(cur_cb);
 }
 
-// U[c, :] = sum of the records of column block c / 256, in CTA order.
+// U[c, :] = the sum of the chunk records of c's column block, in row order:
+// every column's sum runs over the same row chunks whatever the column range
+// (a multi-GPU slice gives the one-shot bits).
 template <int KP>
-__global__ void transform_dmma_reduce_kernel(const double* __restrict__ part,
-                                             const int64_t* __restrict__ rec_cb, K1Geom g,
-                                             int64_t grid, double* __restrict__ u) {
+__global__ void transform_dmma_reduce_kernel(const double* __restrict__ part, K1Geom g,
+                                             double* __restrict__ u) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= g.ncols * KP) return;
   const int64_t c = t / KP;
   const int kc = (int)(t % KP);
   const int64_t cb = c / kK1Cols;
   const int col = (int)(c % kK1Cols);
-  // CTAs whose range touches column block cb: [cb*spc, (cb+1)*spc) of the
-  // flattened range, b = floor(f * G / total) .. (monotone)
-  const int64_t blo = (cb * g.spc) * grid / g.total;
-  const int64_t bhi = min(grid - 1, (((cb + 1) * g.spc) * grid + g.total - 1) / g.total);
+  const double* p = part + (size_t)cb * g.nch * kK1Cols * KP + col * KP + kc;
   double s = 0.0;
-  for (int64_t b = max((int64_t)0, blo - 1); b <= bhi; ++b)
-    for (int sl = 0; sl < 2; ++sl)
-      if (rec_cb[b * 2 + sl] == cb) s += part[(size_t)(b * 2 + sl) * kK1Cols * KP + col * KP + kc];
+  for (int64_t m = 0; m < g.nch; ++m) s += p[(size_t)m * kK1Cols * KP];
   u[t] = s;
 }
 
@@ -306,17 +326,19 @@ void launch_transform_dmma_s(const double* q, const double* kmat, int64_t n, int
   g.k = k;
   g.ncb = cdiv(g.ncols, kK1Cols);
   g.spc = cdiv(n, kK1Rows);
-  g.total = g.ncb * g.spc;
-  // persistent grid: every resident slot busy, at least one CTA per column
-  // block (so a CTA's range spans at most two column blocks)
-  const int64_t grid = std::min<int64_t>(g.total, std::max<int64_t>((int64_t)std::max(1, per_sm) * sms, g.ncb));
-  double* part = ws.get_f64("tf_dpart", (size_t)grid * 2 * kK1Cols * KP);
-  int64_t* rec = ws.get_i64("tf_drec", (size_t)grid * 2);
-  EIGB_CUDA(cudaMemsetAsync(rec, 0xff, 8 * (size_t)grid * 2, st));  // -1: no record
-  transform_dmma_kernel<KP, kK1Stages><<<(unsigned)grid, kK1Threads, smem, st>>>(q, kmat, g, part, rec);
+  // row chunks of 32 .. 1024 rows (n / 32, a function of n alone: the same
+  // summation order for any column range), at most 32 records per column
+  const int64_t cr = std::min<int64_t>(1024, std::max<int64_t>(32, cdiv(cdiv(n, 32), kK1Rows) * kK1Rows));
+  g.cs = cr / kK1Rows;
+  g.nch = cdiv(g.spc, g.cs);
+  g.items = g.ncb * g.nch;
+  // persistent grid: every resident slot busy (items split evenly)
+  const int64_t grid = std::min<int64_t>(g.items, (int64_t)std::max(1, per_sm) * sms);
+  double* part = ws.get_f64("tf_dpart", (size_t)g.items * kK1Cols * KP);
+  transform_dmma_kernel<KP, kK1Stages><<<(unsigned)grid, kK1Threads, smem, st>>>(q, kmat, g, part);
   EIGB_LAUNCH_CHECK();
   const int64_t cnt = g.ncols * KP;
-  transform_dmma_reduce_kernel<KP><<<(unsigned)cdiv(cnt, 256), 256, 0, st>>>(part, rec, g, grid, u);
+  transform_dmma_reduce_kernel<KP><<<(unsigned)cdiv(cnt, 256), 256, 0, st>>>(part, g, u);
   EIGB_LAUNCH_CHECK();
 }
 
@@ -516,8 +538,12 @@ __global__ void __launch_bounds__(kPlanThreads) runs_kernel(const double* __rest
   }
   __syncthreads();
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) rep_row[i] = gval[gid[i]];
+  int64_t nm = 0;  // multi-member runs (read back with ng: no separate round trip)
+  for (int64_t g = threadIdx.x; g < ng; g += blockDim.x) nm += glen[g] > 1;
+  nm = (int64_t)block_sum((double)nm, red);
   if (threadIdx.x == 0) {
     counts[0] = ng;
+    counts[4] = nm;
     scal[0] = scale;
   }
 }
@@ -721,9 +747,10 @@ __global__ void __launch_bounds__(kPlanThreads) assemble_reduced_kernel(
 }
 
 __global__ void clips_kernel(const double* __restrict__ d, const double* __restrict__ ur,
-                             int64_t nr, int kp, int k, const int* __restrict__ sgn,
-                             double* __restrict__ scal) {
+                             const int64_t* __restrict__ counts, int kp, int k,
+                             const int* __restrict__ sgn, double* __restrict__ scal) {
   __shared__ double red[32];
+  const int64_t nr = counts[1];  // from assemble_reduced_kernel, no host round trip
   double pos = 0.0, neg = 0.0, m = 0.0;
   for (int64_t t = threadIdx.x; t < nr * kp; t += blockDim.x) {
     const int c = (int)(t % kp);
@@ -788,11 +815,12 @@ void build_plan_groups(Plan& p, const double* lam, int64_t n, double run_rel, De
                                            p.gstart, p.glen, p.gval,
                                            p.rep_row, p.counts, p.scal);
   EIGB_LAUNCH_CHECK();
-  int64_t ng = 0;
-  EIGB_CUDA(cudaMemcpyAsync(&ng, p.counts, 8, cudaMemcpyDeviceToHost, st));
+  int64_t cnt[5] = {0, 0, 0, 0, 0};
+  EIGB_CUDA(cudaMemcpyAsync(cnt, p.counts, sizeof(cnt), cudaMemcpyDeviceToHost, st));
   EIGB_CUDA(cudaStreamSynchronize(st));
-  p.ng = ng;
-  p.alpha = ws.get_f64("pl_alpha", ng);
+  p.ng = cnt[0];
+  p.nmulti = cnt[4];
+  p.alpha = ws.get_f64("pl_alpha", p.ng);
 }
 
 // K2 for groups [g0, g1) into alpha_out (length g1 - g0); the full vector may
@@ -812,29 +840,37 @@ void build_plan_finish(Plan& p, const double* lam, DeviceScratch& ws, cudaStream
                                                p.exact ? 1 : 0, p.kind, p.scal);
   EIGB_LAUNCH_CHECK();
 
-  // multi-member runs: host-side offsets (lengths are needed for H/R storage)
-  std::vector<int64_t> glen_h(ng);
-  EIGB_CUDA(cudaMemcpyAsync(glen_h.data(), p.glen, 8 * ng, cudaMemcpyDeviceToHost, st));
-  EIGB_CUDA(cudaStreamSynchronize(st));
-  std::vector<int64_t> hoff(ng), roff(ng);
-  int64_t hs = 0, rs = 0, nmulti = 0;
-  for (int64_t g = 0; g < ng; ++g) {
-    hoff[g] = hs;
-    roff[g] = rs;
-    if (glen_h[g] > 1) {
-      hs += glen_h[g] * glen_h[g];
-      rs += glen_h[g] * kp;
-      ++nmulti;
-    }
-  }
-  p.nmulti = nmulti;
+  // multi-member runs (their count came back with ng): host-side offsets,
+  // since the lengths size the H/R storage; none (the common case): no trip
+  const int64_t nmulti = p.nmulti;
+  std::vector<int64_t> glen_h;
   p.hoff = ws.get_i64("pl_hoff", ng);
   p.roff = ws.get_i64("pl_roff", ng);
+  p.rank = ws.get_i64("pl_rank", ng);
+  int64_t hs = 0, rs = 0;
+  if (nmulti > 0) {
+    glen_h.resize(ng);
+    EIGB_CUDA(cudaMemcpyAsync(glen_h.data(), p.glen, 8 * ng, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaStreamSynchronize(st));
+    std::vector<int64_t> hoff(ng), roff(ng);
+    for (int64_t g = 0; g < ng; ++g) {
+      hoff[g] = hs;
+      roff[g] = rs;
+      if (glen_h[g] > 1) {
+        hs += glen_h[g] * glen_h[g];
+        rs += glen_h[g] * kp;
+      }
+    }
+    EIGB_CUDA(cudaMemcpyAsync(p.hoff, hoff.data(), 8 * ng, cudaMemcpyHostToDevice, st));
+    EIGB_CUDA(cudaMemcpyAsync(p.roff, roff.data(), 8 * ng, cudaMemcpyHostToDevice, st));
+    // the host vectors must outlive the copies
+    EIGB_CUDA(cudaStreamSynchronize(st));
+  } else {
+    EIGB_CUDA(cudaMemsetAsync(p.hoff, 0, 8 * ng, st));
+    EIGB_CUDA(cudaMemsetAsync(p.roff, 0, 8 * ng, st));
+  }
   p.hbuf = ws.get_f64("pl_hbuf", hs);
   p.rbuf = ws.get_f64("pl_rbuf", rs);
-  p.rank = ws.get_i64("pl_rank", ng);
-  EIGB_CUDA(cudaMemcpyAsync(p.hoff, hoff.data(), 8 * ng, cudaMemcpyHostToDevice, st));
-  EIGB_CUDA(cudaMemcpyAsync(p.roff, roff.data(), 8 * ng, cudaMemcpyHostToDevice, st));
   if (nmulti > 0) {
     compress_kernel<<<(unsigned)cdiv(ng, 64), 64, 0, st>>>(p.u, kp, k, p.gstart, p.glen, p.kind,
                                                          p.counts, p.hoff, p.roff, p.hbuf, p.rbuf,
@@ -859,28 +895,28 @@ void build_plan_finish(Plan& p, const double* lam, DeviceScratch& ws, cudaStream
       p.off_red, p.off_dec, p.alpha, p.alpha_red, p.d, p.ur, p.red_src, p.dec_val, p.dec_src,
       p.orig_map);
   EIGB_LAUNCH_CHECK();
+  clips_kernel<<<1, kPlanThreads, 0, st>>>(p.d, p.ur, p.counts, kp, k, p.sgn, p.scal);
+  EIGB_LAUNCH_CHECK();
+  // one round trip for the sizes, the scales and (with multi-member runs) the
+  // run ranks and kinds
   int64_t cnt[3];
+  double sc[8];
+  std::vector<int64_t> rk(nmulti > 0 ? ng : 0);
+  std::vector<int> kd(nmulti > 0 ? ng : 0);
   EIGB_CUDA(cudaMemcpyAsync(cnt, p.counts, 24, cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaMemcpyAsync(sc, p.scal, 64, cudaMemcpyDeviceToHost, st));
+  if (nmulti > 0) {
+    EIGB_CUDA(cudaMemcpyAsync(rk.data(), p.rank, 8 * ng, cudaMemcpyDeviceToHost, st));
+    EIGB_CUDA(cudaMemcpyAsync(kd.data(), p.kind, 4 * ng, cudaMemcpyDeviceToHost, st));
+  }
   EIGB_CUDA(cudaStreamSynchronize(st));
   p.nred = cnt[1];
   p.ndec = cnt[2];
-  {  // rows of compressed runs are not simple poles of f
-    std::vector<int64_t> rk(ng), gl2(ng);
-    std::vector<int> kd(ng);
-    EIGB_CUDA(cudaMemcpyAsync(rk.data(), p.rank, 8 * ng, cudaMemcpyDeviceToHost, st));
-    EIGB_CUDA(cudaMemcpyAsync(kd.data(), p.kind, 4 * ng, cudaMemcpyDeviceToHost, st));
-    EIGB_CUDA(cudaStreamSynchronize(st));
-    bool ok = true;
-    for (int64_t g = 0; g < ng && ok; ++g)
-      if (glen_h[g] > 1 && kd[g] != 1 && rk[g] > 0) ok = false;
-    p.alpha_red_ok = ok;
-  }
+  bool ok = true;  // rows of compressed runs are not simple poles of f
+  for (int64_t g = 0; g < (nmulti > 0 ? ng : 0) && ok; ++g)
+    if (glen_h[g] > 1 && kd[g] != 1 && rk[g] > 0) ok = false;
+  p.alpha_red_ok = ok;
   if (p.nred + p.ndec != n) throw Error(2, "merge", "reduced problem does not account for n pairs");
-  clips_kernel<<<1, kPlanThreads, 0, st>>>(p.d, p.ur, p.nred, kp, k, p.sgn, p.scal);
-  EIGB_LAUNCH_CHECK();
-  double sc[8];
-  EIGB_CUDA(cudaMemcpyAsync(sc, p.scal, 64, cudaMemcpyDeviceToHost, st));
-  EIGB_CUDA(cudaStreamSynchronize(st));
   p.scale = sc[0];
   p.alpha_mass = sc[1];
   p.u_mass = sc[2];

@@ -955,6 +955,23 @@ void launch_collisions(const Plan& p, const RootRecords& roots, const int64_t* l
 
 }  // namespace
 
+namespace {
+// EIGMOD_B200_BORDERED_MULTI=0: collided roots only (diagnostics)
+int bordered_multi() {
+  static int allow_multi = -1;
+  if (allow_multi < 0) {
+    const char* e = std::getenv("EIGMOD_B200_BORDERED_MULTI");
+    allow_multi = !(e && std::string(e) == "0");
+  }
+  return allow_multi;
+}
+
+__global__ void any_mark_kernel(const int* __restrict__ mark, int64_t nr, int* __restrict__ any) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < nr && mark[j]) atomicOr(any, 1);
+}
+}  // namespace
+
 void merge_columns_dev(const Plan& p, const RootRecords& roots, Columns& cols, DeviceScratch& ws,
                        cudaStream_t st) {
   const int64_t nr = p.nred, nd = p.ndec, n = p.n;
@@ -963,16 +980,32 @@ void merge_columns_dev(const Plan& p, const RootRecords& roots, Columns& cols, D
   cols.value = ws.get_f64("col_value", n);
   const double* rv = roots.value;
   const int64_t* perm = nullptr;
-  if (nr > 1) {
+  cols.nmarked = -1;
+  if (nr > 0) {
     // Roots come out ascending from the count-certified brackets; ties within
-    // an ulp can swap, so verify and fall back to a stable device sort.
-    int* bad = ws.get_i32("merge_bad", 1);
-    EIGB_CUDA(cudaMemsetAsync(bad, 0, 4, st));
-    root_order_check_kernel<<<(unsigned)cdiv(nr, 256), 256, 0, st>>>(rv, nr, bad);
+    // an ulp can swap, so verify and fall back to a stable device sort. The
+    // same round trip brings back how many roots need a bordered-system
+    // vector (collision_vectors_dev skips its own when none do).
+    int* bad = ws.get_i32("merge_bad", 2);
+    EIGB_CUDA(cudaMemsetAsync(bad, 0, 8, st));
+    if (nr > 1) {
+      root_order_check_kernel<<<(unsigned)cdiv(nr, 256), 256, 0, st>>>(rv, nr, bad);
+      EIGB_LAUNCH_CHECK();
+    }
+    int* mark = ws.get_i32("coll_mark", nr);
+    int* which = ws.get_i32("coll_which", nr);
+    int* collok = ws.get_i32("collok", nr);
+    bordered_mark_kernel<<<(unsigned)cdiv(nr, 256), 256, 0, st>>>(
+        p.d, p.ur, p.kp, nr, roots.origin, roots.delta, roots.flags, nr, mark, which, collok,
+        bordered_multi());
     EIGB_LAUNCH_CHECK();
-    int bad_h = 0;
-    EIGB_CUDA(cudaMemcpyAsync(&bad_h, bad, 4, cudaMemcpyDeviceToHost, st));
+    any_mark_kernel<<<(unsigned)cdiv(nr, 256), 256, 0, st>>>(mark, nr, bad + 1);
+    EIGB_LAUNCH_CHECK();
+    int h[2] = {0, 0};
+    EIGB_CUDA(cudaMemcpyAsync(h, bad, 8, cudaMemcpyDeviceToHost, st));
     EIGB_CUDA(cudaStreamSynchronize(st));
+    const int bad_h = h[0];
+    cols.nmarked = h[1];
     if (bad_h) {
       double* sv = ws.get_f64("merge_sorted", nr);
       int64_t* pm = ws.get_i64("merge_perm", nr);
@@ -1013,14 +1046,10 @@ int64_t collision_vectors_dev(const Plan& p, const RootRecords& roots, const Col
   }
   int* mark = ws.get_i32("coll_mark", nr);
   int* which = ws.get_i32("coll_which", nr);
-  static int allow_multi = -1;  // EIGMOD_B200_BORDERED_MULTI=0: collided roots only (diagnostics)
-  if (allow_multi < 0) {
-    const char* e = std::getenv("EIGMOD_B200_BORDERED_MULTI");
-    allow_multi = !(e && std::string(e) == "0");
-  }
+  if (cols.nmarked == 0) return 0;  // merge_columns_dev found no root to border (collok zeroed)
   bordered_mark_kernel<<<(unsigned)cdiv(nr, 256), 256, 0, st>>>(p.d, p.ur, p.kp, nr, roots.origin,
                                                                 roots.delta, roots.flags, nr, mark,
-                                                                which, collok, allow_multi);
+                                                                which, collok, bordered_multi());
   EIGB_LAUNCH_CHECK();
   std::vector<int> mh(nr), nh(nr);
   EIGB_CUDA(cudaMemcpyAsync(mh.data(), mark, 4 * nr, cudaMemcpyDeviceToHost, st));

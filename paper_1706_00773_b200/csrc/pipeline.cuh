@@ -45,6 +45,7 @@ struct Columns {
   int* kind = nullptr;        // 0 root, 1 unit vector, 2 run rotation vector
   int64_t* payload = nullptr; // root j or decoupled entry e
   double* value = nullptr;    // lambda' (ascending)
+  int64_t nmarked = -1;       // roots needing a bordered-system vector (0: none; -1: unknown)
 };
 
 // deflate.cu
