@@ -631,7 +631,8 @@ struct ParSmem {
 constexpr size_t kSolveSmemPad = (sizeof(SolveSmem) + 15) / 16 * 16;
 
 // element (i, j), i >= j, of slot b's matrix
-#define FA(i, j) F[(size_t)b * esl + ((i) * KP + (j)) * es]
+// (lower triangle, packed by rows: every access has i >= j)
+#define FA(i, j) F[(size_t)b * esl + ((i) * ((i) + 1) / 2 + (j)) * es]
 // Warps sharing the rows of a slot: one row per warp up to 8 (KP = 1, 2, 4
 // use KP warps, synchronised by a named barrier over those warps).
 template <int KP>
@@ -919,18 +920,18 @@ __device__ void par_solve(const double* F, size_t esl, int es, ParSmem<KP>& P, b
 
 // ------------------------------------------------------------ sweep kernel
 template <int KP>
-__global__ void __launch_bounds__(kPassThreads, 1) count_sweep_kernel(ReducedView rp,
+__global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) count_sweep_kernel(ReducedView rp,
                                                                       int* __restrict__ counts,
                                                                       int64_t qbeg, int64_t qend,
                                                                       double* __restrict__ gscratch) {
   using C = PassCfg<KP>;
   extern __shared__ __align__(16) double smem[];
-  // factor storage: interleaved [KP*KP][32] in shared memory for KP <= 16,
+  // factor storage: interleaved [KP(KP+1)/2][32] in shared memory for KP <= 16,
   // per-slot matrices in global scratch above (32 x 32 x 32 doubles do not fit)
   // (KP <= 16: overlays the pass's tiles and D buffer, dead after the pass;
   // the pass result lies beyond them)
   constexpr bool kSmemF = KP <= 16;
-  static_assert(!kSmemF || 32 * KP * KP <= 2 * C::TILE_DOUBLES + C::DBUF_DOUBLES,
+  static_assert(!kSmemF || C::FACT <= 2 * C::TILE_DOUBLES + C::DBUF_DOUBLES,
                 "factor storage must fit in the pass tiles");
   double* F = kSmemF ? smem : gscratch + (size_t)blockIdx.x * 32 * KP * KP;
   const size_t esl = kSmemF ? 1 : (size_t)KP * KP;
@@ -1213,19 +1214,18 @@ constexpr bool kFactorInSmem = (KP <= 16);
 // the tail of the last roots (lockstep slots idle while a few finish) costs
 // CL times less wall time.
 template <int KP, int CL>
-__global__ void __launch_bounds__(kPassThreads, KP <= 4 ? 2 : 1) solve_roots_kernel(SolveArgs<KP> a,
+__global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) solve_roots_kernel(SolveArgs<KP> a,
                                                                       double* gscratch) {
   using C = PassCfg<KP>;
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double smem[];
   double* y = smem + C::SMEM_DOUBLES;                      // [32][KP]
-  // [KP*KP][32] (KP <= 16): overlays the pass's tiles and D buffer, which are
+  // [KP(KP+1)/2][32] (KP <= 16): overlays the pass's tiles and D buffer, which are
   // dead while the step runs (the pass result it reads lies beyond them)
   double* Fs = smem;
-  static_assert(!kFactorInSmem<KP> || 32 * KP * KP <= 2 * C::TILE_DOUBLES + C::DBUF_DOUBLES,
+  static_assert(!kFactorInSmem<KP> || C::FACT <= 2 * C::TILE_DOUBLES + C::DBUF_DOUBLES,
                 "factor storage must fit in the pass tiles");
-  double* fullred = y + 32 * KP;                           // [32][OUT] (CL > 1)
-  SolveSmem& s = *reinterpret_cast<SolveSmem*>(fullred + (CL > 1 ? C::RED_DOUBLES : 0));
+  SolveSmem& s = *reinterpret_cast<SolveSmem*>(y + 32 * KP);
   ParSmem<KP>& P = *reinterpret_cast<ParSmem<KP>*>(reinterpret_cast<char*>(&s) + kSolveSmemPad);
   __shared__ int any;
   const int t = threadIdx.x;
@@ -1236,7 +1236,7 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 4 ? 2 : 1) solve_roots_ker
   const int64_t chunk = (N + CL - 1) / CL;
   const int64_t plo = (rank * chunk < N) ? rank * chunk : N;
   const int64_t pcnt = ((plo + chunk < N) ? plo + chunk : N) - plo;
-  // slot b's matrix: element (i, j) at F[b * esl + (i * KP + j) * es]
+  // slot b's matrix: element (i, j), i >= j, at F[b * esl + (i (i + 1) / 2 + j) * es]
   double* F;
   size_t esl;
   int es;
@@ -1299,20 +1299,33 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 4 ? 2 : 1) solve_roots_ker
     const double* red = pass_result<KP>(smem);
     const long long t2 = clock64();
     if constexpr (CL > 1) {
+      // in place, in two phases: rank r sums its slice of the partials over
+      // the ranks in rank order, then stores the sums into every rank's copy
       cg::cluster_group cl = cg::this_cluster();
+      constexpr int SL = (C::RED_DOUBLES + CL - 1) / CL;
+      constexpr int PER = (SL + kPassThreads - 1) / kPassThreads;
+      double* redw = const_cast<double*>(red);
       cl.sync();  // all partial sums of this iteration are in place
-      for (int idx = t; idx < C::RED_DOUBLES; idx += kPassThreads) {
-        double v = 0.0;
-        for (int r = 0; r < CL; ++r) v += cl.map_shared_rank(red, r)[idx];
-        fullred[idx] = v;
+      double v[PER];
+#pragma unroll
+      for (int m = 0; m < PER; ++m) {
+        const int idx = rank * SL + m * kPassThreads + t;
+        v[m] = 0.0;
+        if (m * kPassThreads + t < SL && idx < C::RED_DOUBLES)
+          for (int r = 0; r < CL; ++r) v[m] += cl.map_shared_rank(redw, r)[idx];
       }
-      if (t < 32) {
-        int h = 0;
+      int h = 0;
+      if (t < 32)
         for (int r = 0; r < CL; ++r) h |= cl.map_shared_rank(&s, r)->hit[t];
-        s.hit[t] = h;  // OR is idempotent: safe while others still read it
-      }
       cl.sync();  // partials no longer read remotely
-      red = fullred;
+#pragma unroll
+      for (int m = 0; m < PER; ++m) {
+        const int idx = rank * SL + m * kPassThreads + t;
+        if (m * kPassThreads + t < SL && idx < C::RED_DOUBLES)
+          for (int r = 0; r < CL; ++r) cl.map_shared_rank(redw, r)[idx] = v[m];
+      }
+      if (t < 32) s.hit[t] = h;
+      cl.sync();  // sums in place everywhere
     }
     const long long t3 = clock64();
     // ---- per-slot step (all warps): factor S, inverse iteration, Newton
@@ -1443,7 +1456,7 @@ struct WeightArgs {
 // whose pivots span more than 1e8 (the reference's switch to cofactor
 // expansion, secular.cpp:49-124) take the reference's adjugate route.
 template <int KP>
-__global__ void __launch_bounds__(kPassThreads, 1) group_weights_kernel(WeightArgs<KP> a) {
+__global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) group_weights_kernel(WeightArgs<KP> a) {
   using C = PassCfg<KP>;
   extern __shared__ __align__(16) double smem[];
   __shared__ double dob[32], delta[32], acc[32];
@@ -1466,7 +1479,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) group_weights_kernel(WeightAr
   const double* red = pass_result<KP>(smem);
   // (KP <= 16: overlays the pass's tiles and D buffer, dead after the pass)
   constexpr bool kSmemF = KP <= 16;
-  static_assert(!kSmemF || 32 * KP * KP <= 2 * C::TILE_DOUBLES + C::DBUF_DOUBLES,
+  static_assert(!kSmemF || C::FACT <= 2 * C::TILE_DOUBLES + C::DBUF_DOUBLES,
                 "factor storage must fit in the pass tiles");
   double* F = kSmemF ? smem : a.scratch + (size_t)blockIdx.x * 32 * 4 * KP * KP;
   const size_t esl = kSmemF ? 1 : (size_t)4 * KP * KP;
@@ -1568,7 +1581,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) group_weights_kernel(WeightAr
 template <int KP, int CL>
 size_t solve_smem_bytes() {
   using C = PassCfg<KP>;
-  return sizeof(double) * (C::SMEM_DOUBLES + 32 * KP + (CL > 1 ? C::RED_DOUBLES : 0)) +
+  return sizeof(double) * (C::SMEM_DOUBLES + 32 * KP) +
          kSolveSmemPad + sizeof(ParSmem<KP>);
 }
 
@@ -1730,7 +1743,7 @@ struct InertiaArgs {
 };
 
 template <int KP>
-__global__ void __launch_bounds__(kPassThreads, 1) pole_inertia_kernel(InertiaArgs<KP> a) {
+__global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) pole_inertia_kernel(InertiaArgs<KP> a) {
   using C = PassCfg<KP>;
   extern __shared__ __align__(16) double smem[];
   __shared__ double dob[32], delta[32];

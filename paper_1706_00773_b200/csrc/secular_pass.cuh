@@ -42,16 +42,17 @@ struct PassCfg {
   static constexpr int EG = (KP <= 8) ? 1 : (KP == 16 ? 2 : 8);
   static constexpr int PS = kPassWarps / EG;
   // MMA layout: S (32 slots x P entries) = D (32 x poles) W (poles x P),
-  // W[i][e] = u_i[r_e] u_i[c_e]: 4 m-tiles of 8 slots, NT n-tiles of 8
-  // entries split into NG contiguous groups, MPS pole splits (NG x MPS = 8
-  // warps).
-  static constexpr int NT = (P + 7) / 8;
+  // W[i][e] = u_i[r_e] u_i[c_e]: 4 m-tiles of 8 slots, n-tiles of 8 entries in
+  // NG groups (MmaMap), warps = 2 m-halves x NG groups x MPS pole splits.
   static constexpr int NG = (KP == 16) ? 2 : 1;
-  static constexpr int MPS = kPassWarps / NG;
-  __host__ __device__ static constexpr int nt_lo(int g) { return (NT * g) / NG; }
-  // u rows in the tile: padded to 64 B mod 128 B in MMA mode, so the four
-  // pole rows of a B fragment fall into different bank halves
-  static constexpr int LDU = MMA ? KP + 8 : KP;
+  static constexpr int MPS = kPassWarps / (2 * NG);
+  // u rows in the tile: KP + 4 doubles (20 / 12), so the fragment loads of
+  // both MMA phases (rows by lane / 4 or by lane % 4) fall into distinct bank
+  // pairs (two wavefronts per warp load)
+  static constexpr int LDU = MMA ? KP + 4 : KP;
+  // D buffer stride per k-step: 4 m-tiles x 32 A-fragment elements + 1, so
+  // the D phase's stores (two k-steps per warp store) hit distinct bank pairs
+  static constexpr int DKS = 4 * 32 + 1;
   // Entry group g = packed entries [e_lo(g), e_lo(g+1)): an even split of the
   // packed triangle (a row may straddle two groups), so no warp waits for the
   // other group at the tile barriers.
@@ -77,12 +78,11 @@ struct PassCfg {
   // 64 in MMA mode, 16 k-steps of 4 poles)
   static constexpr int T = MMA ? kPoleTile : ((KP >= 32) ? kPoleTile : 2 * kPoleTile);
   static constexpr int TILE_DOUBLES = T * (LDU + 2);
-  // D buffer: lane = slot order (DFMA), or A fragments per k-step and m-tile
-  // in blocks of 33 (conflict-free writes by slot and reads by fragment lane)
-  static constexpr int DBUF_MIN = MMA ? (T / 4) * 4 * 33 : T * 32;
-  // the solver and K2 overlay their k x k factors (32 KP^2 doubles for
-  // KP <= 16) on the tiles and the D buffer
-  static constexpr int FACT = (KP <= 16) ? 32 * KP * KP : 0;
+  // D buffer: lane = slot order (DFMA), or A fragments per k-step (MMA)
+  static constexpr int DBUF_MIN = MMA ? (T / 4) * DKS : T * 32;
+  // the solver and K2 overlay their k x k factors (lower triangles, packed:
+  // 32 KP (KP + 1) / 2 doubles for KP <= 16) on the tiles and the D buffer
+  static constexpr int FACT = (KP <= 16) ? 32 * P : 0;
   static constexpr int DBUF_DOUBLES =
       (2 * TILE_DOUBLES + DBUF_MIN >= FACT) ? DBUF_MIN : FACT - 2 * TILE_DOUBLES;
   static constexpr int RED_DOUBLES = 32 * OUT;
@@ -303,52 +303,124 @@ __device__ __forceinline__ void pass_body(const double* __restrict__ d, const do
 // The pass with its FMA phase on the FP64 tensor pipe (KP = 8, 16):
 //   S[b][e] = sum_i D[i][b] W[i][e],  W[i][e] = u_i[r_e] u_i[c_e]
 // as mma.sync.m8n8k4.f64 tiles (M = 32 slots in 4 m-tiles, N = P packed
-// entries in n-tiles of 8, K = the poles of the tile in k-steps of 4). The D
-// phase is the DFMA pass's (lane = slot: the reciprocal, g, f, f'), writing
-// D in A-fragment order. A B fragment element (pole 4 ks + lane % 4, entry
-// 8 nt + lane / 4) is the product of two u entries of the pole's row, formed
-// where it is consumed: each (pole, entry) product once per CTA, reused by
-// the 4 m-tiles. One DMMA replaces 16 warp-wide DFMAs (512 flops per issue),
-// so the FP64 budget, which DFMA and DMMA share on B200
-// (profiles/coissue_dmma_dfma_r02.json), goes to the contraction instead of
-// instruction issue. Warp = (n-group G, pole split p).
+// entries in n-tiles of 8, K = the poles of the tile in k-steps of 4). One DMMA
+// replaces 16 warp-wide DFMAs (512 flops per issue), so the FP64 budget, which
+// DFMA and DMMA share on B200 (profiles/coissue_dmma_dfma_r02.json), goes to
+// the contraction instead of instruction issue.
+//
+// Round 2 layout (two CTAs per SM: <= 128 registers, <= ~100 KB of shared
+// memory per CTA, so one CTA's D phase overlaps the other's MMA phase):
+//  * D phase in C-fragment layout: warp w owns m-tile w & 3 (lane -> slot
+//    8 (w & 3) + lane / 4) and the pole n-tiles (w >> 2) + 2 j. With sigma,
+//    P = Y U^T (the projections u_i . y_b) is itself a DMMA (A = Y fragments
+//    held in registers, B = the u rows of the tile), then per element the
+//    reciprocal D, g += (P D)^2, f, f'. D is stored in A-fragment order.
+//  * MMA phase: warp = (m-half, n-group, pole split): 2 m-tiles x 8-9 n-tiles
+//    of accumulators (36 doubles). The packed entries are ordered by lane
+//    pattern (mma_entry): within an n-tile the entry of B column n is
+//    (n, 8 + nt) (the off-diagonal 8 x 8 block), (n, (n + s) & 7) or
+//    (8 + n, 8 + ((n + s) & 7)) (the diagonal blocks by cyclic distance s),
+//    so a lane forms its B elements from 2-8 loads of its pole row instead of
+//    two per element.
+// The k x k matrix entries come out in any order: the reduction writes them
+// at their packed index.
+template <int KP>
+struct MmaMap {
+  // global n-tiles: KP = 16: group 0 = tiles 0..8, group 1 = 9..16; KP = 8: 0..4
+  static constexpr int NTILES = (KP == 16) ? 17 : 5;
+  __host__ __device__ static constexpr int nt_lo(int g) { return (KP == 16) ? (g == 0 ? 0 : 9) : 0; }
+  __host__ __device__ static constexpr int nt_cnt(int g) { return (KP == 16) ? (g == 0 ? 9 : 8) : 5; }
+  // (row, column) of B column n of n-tile nt, or -1 (unused)
+  __host__ __device__ static inline void entry(int nt, int n, int& r, int& c) {
+    if constexpr (KP == 16) {
+      if (nt < 8) { r = n; c = 8 + nt; return; }
+      if (nt == 8) { r = (n < 4) ? n : n + 4; c = r + 4; return; }
+      if (nt < 13) { r = n; c = (n + (nt - 9)) & 7; return; }
+      r = 8 + n; c = 8 + ((n + (nt - 13)) & 7);
+      return;
+    } else {
+      if (nt < 4) { r = n; c = (n + nt) & 7; return; }
+      if (n < 4) { r = n; c = n + 4; return; }
+      r = c = -1;
+    }
+  }
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// B elements of one k-step for n-group G: ur = this lane's pole row
+template <int KP, int G>
+__device__ __forceinline__ void mma_bvals(const double* __restrict__ ur, int g8, double* b) {
+  if constexpr (KP == 16 && G == 0) {
+    const double r0 = ur[g8];
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(ur + 8 + j);
+      b[j] = r0 * v.x;
+      b[j + 1] = r0 * v.y;
+    }
+    const int rm = (g8 < 4) ? g8 : g8 + 4;
+    b[8] = ur[rm] * ur[rm + 4];
+  } else {
+    constexpr int OFF = (KP == 16) ? 8 : 0;  // G == 1 of KP = 16: the lower block too
+    const double x0 = ur[g8], x1 = ur[(g8 + 1) & 7], x2 = ur[(g8 + 2) & 7], x3 = ur[(g8 + 3) & 7];
+    b[0] = x0 * x0;
+    b[1] = x0 * x1;
+    b[2] = x0 * x2;
+    b[3] = x0 * x3;
+    if constexpr (KP == 16) {
+      const double y0 = ur[OFF + g8], y1 = ur[OFF + ((g8 + 1) & 7)], y2 = ur[OFF + ((g8 + 2) & 7)],
+                   y3 = ur[OFF + ((g8 + 3) & 7)];
+      b[4] = y0 * y0;
+      b[5] = y0 * y1;
+      b[6] = y0 * y2;
+      b[7] = y0 * y3;
+    } else {
+      b[4] = (g8 < 4) ? x0 * ur[g8 + 4] : 0.0;
+    }
+  }
+}
+
 template <int KP, int G>
 __device__ __forceinline__ void pass_body_mma(const double* __restrict__ d,
                                               const double* __restrict__ u, int64_t n,
                                               const PassSlots& slots, const PassOpts& o,
-                                              double* tiles, double* dbuf, double* red, int p) {
+                                              double* tiles, double* dbuf, double* red, int mh,
+                                              int p) {
   using C = PassCfg<KP>;
-  constexpr int NT0 = C::nt_lo(G), NTL = C::nt_lo(G + 1) - C::nt_lo(G);
+  using MM = MmaMap<KP>;
+  constexpr int NTL = MM::nt_cnt(G);
   constexpr int KSW = (C::T / 4) / C::MPS;  // k-steps per warp per tile
   constexpr int LDU = C::LDU;
+  constexpr int KC = KP / 4;                // k-steps of P = Y U^T
+  constexpr int DKS = C::DKS;               // D buffer stride per k-step
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int t4 = lane & 3, g8 = lane >> 2;
-  const double dob = slots.dob[lane];
-  const double del = slots.delta[lane];
-  const bool act = slots.active[lane] != 0;
+  // ---- D-phase role: m-tile md, lane -> slot
+  const int md = warp & 3;
+  const int slot = 8 * md + g8;
+  const double dob = slots.dob[slot];
+  const double del = slots.delta[slot];
+  const bool act = slots.active[slot] != 0;
   const bool sig = o.want_sigma;
   const bool wf = o.alpha != nullptr;
-  double yv[KP];
+  const bool exg = o.excl_gap > 0.0;
+  const int64_t xr = (exg && slots.excl_row) ? slots.excl_row[slot] : -1;
+  double yf[KC];
 #pragma unroll
-  for (int c = 0; c < KP; ++c) yv[c] = sig ? slots.y[lane * KP + c] : 0.0;
-  // this lane's B entries: (row, column) of packed entry 8 nt + lane / 4
-  int er[NTL], ec[NTL];
+  for (int kc = 0; kc < KC; ++kc) yf[kc] = sig ? slots.y[slot * KP + 4 * kc + t4] : 0.0;
+  double acc[2][NTL][2];
 #pragma unroll
-  for (int j = 0; j < NTL; ++j) {
-    const int e = 8 * (NT0 + j) + g8;
-    er[j] = (e < C::P) ? C::row_of(e) : 0;
-    ec[j] = (e < C::P) ? C::col_of(e) : 0;
-  }
-  double acc[4][NTL][2];
-#pragma unroll
-  for (int m = 0; m < 4; ++m)
+  for (int m = 0; m < 2; ++m)
 #pragma unroll
     for (int j = 0; j < NTL; ++j) acc[m][j][0] = acc[m][j][1] = 0.0;
   double gs = 0.0, fs = 0.0, fps = 0.0;
   int hit = 0;
-  // D write position of this slot within a k-step block
-  const int dslot = (lane >> 3) * 33 + (lane & 7) * 4;
 
   const int64_t ntiles = (n + C::T - 1) / C::T;
   if (ntiles > 0) load_pole_tile<KP>(tiles, d, o.alpha, u, 0, n);
@@ -362,98 +434,106 @@ __device__ __forceinline__ void pass_body_mma(const double* __restrict__ d,
     const double* td = cur;
     const double* ta = cur + C::T;
     const double* tu = cur + 2 * C::T;
-    // ---- D phase (lane = slot)
-#pragma unroll 4
-    for (int i = warp; i < C::T; i += kPassWarps) {
-      const double diff = (td[i] - dob) - del;
-      double D;
-      if (o.excl_gap > 0.0) {
-        const int64_t xr = slots.excl_row ? slots.excl_row[lane] : -1;
-        const bool ex = (xr >= 0) ? (t * C::T + i == xr) : (fabs(td[i] - dob) < o.excl_gap);
-        D = (act && !ex && diff == diff) ? rcp64(diff) : 0.0;
-      } else if (diff == 0.0) {
-        hit |= !o.exclude_zero;
-        D = 0.0;
-      } else {
-        D = (act && diff == diff) ? rcp64(diff) : 0.0;
-      }
-      dbuf[(i >> 2) * 132 + dslot + (i & 3)] = D;
-      if (sig) {
-        double t0 = 0.0, t1 = 0.0;
+    // ---- D phase (C-fragment layout: slot row g8, poles 8 nd + 2 t4 + h)
 #pragma unroll
-        for (int c = 0; c < KP; c += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(tu + i * LDU + c);
-          t0 = fma(v.x, yv[c], t0);
-          t1 = fma(v.y, yv[c + 1], t1);
-        }
-        const double td2 = (t0 + t1) * D;
-        gs = fma(td2, td2, gs);
+    for (int jn = 0; jn < C::T / 16; ++jn) {
+      const int nd = (warp >> 2) + 2 * jn;
+      double pv0 = 0.0, pv1 = 0.0;
+      if (sig) {
+        const double* ub = tu + (8 * nd + g8) * LDU + t4;
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) dmma(pv0, pv1, yf[kc], ub[4 * kc]);
       }
-      if (wf) {
-        const double aD = ta[i] * D;
-        fs += aD;
-        fps = fma(aD, D, fps);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = 8 * nd + 2 * t4 + h;
+        const double diff = (td[i] - dob) - del;
+        double D;
+        if (exg) {  // the bordered block: rows within excl_gap of dob, or one row
+          const bool ex = (xr >= 0) ? (t * C::T + i == xr) : (fabs(td[i] - dob) < o.excl_gap);
+          D = (act && !ex && diff == diff) ? rcp64(diff) : 0.0;
+        } else if (diff == 0.0) {
+          hit |= !o.exclude_zero;
+          D = 0.0;
+        } else {
+          D = (act && diff == diff) ? rcp64(diff) : 0.0;
+        }
+        dbuf[(i >> 2) * DKS + md * 32 + g8 * 4 + (i & 3)] = D;
+        if (sig) {
+          const double td2 = (h ? pv1 : pv0) * D;
+          gs = fma(td2, td2, gs);
+        }
+        if (wf) {
+          const double aD = ta[i] * D;
+          fs += aD;
+          fps = fma(aD, D, fps);
+        }
       }
     }
     __syncthreads();  // D of this tile visible
-    // ---- MMA phase: k-steps p * KSW .. of this tile
-#pragma unroll
+    // ---- MMA phase: k-steps p * KSW .. of this tile, m-tiles 2 mh, 2 mh + 1
+#pragma unroll 2
     for (int kk = 0; kk < KSW; ++kk) {
       const int ks = p * KSW + kk;
-      double a[4];
-#pragma unroll
-      for (int m = 0; m < 4; ++m) a[m] = dbuf[ks * 132 + m * 33 + lane];
-      const double* ur = tu + (4 * ks + t4) * LDU;
+      const double a0 = dbuf[ks * DKS + (2 * mh) * 32 + lane];
+      const double a1 = dbuf[ks * DKS + (2 * mh + 1) * 32 + lane];
+      double b[NTL];
+      mma_bvals<KP, G>(tu + (4 * ks + t4) * LDU, g8, b);
 #pragma unroll
       for (int j = 0; j < NTL; ++j) {
-        const double b = ur[er[j]] * ur[ec[j]];
-#pragma unroll
-        for (int m = 0; m < 4; ++m)
-          asm volatile(
-              "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-              : "+d"(acc[m][j][0]), "+d"(acc[m][j][1])
-              : "d"(a[m]), "d"(b));
+        dmma(acc[0][j][0], acc[0][j][1], a0, b[j]);
+        dmma(acc[1][j][0], acc[1][j][1], a1, b[j]);
       }
     }
   }
   __syncthreads();
 
-  // Deterministic reduction: the C fragments (slot 8 m + lane / 4, entries
-  // 8 nt + 2 (lane % 4) + h) over pole splits p = 0.. in order, D-phase
-  // partials (g, f, f') over warps 0..7 in order.
+  // Deterministic reduction: the C fragments (slot 8 m + lane / 4, B columns
+  // 2 (lane % 4) + h) over pole splits p = 0.. in order; the D-phase partials
+  // (g, f, f') over the 4 lanes of a slot (butterfly: every lane the same
+  // sum), then over the two warps of an m-tile in order.
   constexpr int OUT = C::OUT;
   for (int q = 0; q < C::MPS; ++q) {
     if (p == q) {
 #pragma unroll
-      for (int m = 0; m < 4; ++m)
+      for (int m = 0; m < 2; ++m)
 #pragma unroll
         for (int j = 0; j < NTL; ++j)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int e = 8 * (NT0 + j) + 2 * t4 + h;
-            if (e < C::P) {
-              double* r = red + (8 * m + g8) * OUT + e;
-              *r = (q == 0) ? acc[m][j][h] : *r + acc[m][j][h];
+            int r, c;
+            MM::entry(MM::nt_lo(G) + j, 2 * t4 + h, r, c);
+            if (r >= 0) {
+              const int e = (r <= c) ? C::pidx(r, c) : C::pidx(c, r);
+              double* rr = red + (8 * (2 * mh + m) + g8) * OUT + e;
+              *rr = (q == 0) ? acc[m][j][h] : *rr + acc[m][j][h];
             }
           }
     }
     __syncthreads();
   }
-  for (int q = 0; q < kPassWarps; ++q) {
-    if (warp == q) {
+#pragma unroll
+  for (int o2 = 1; o2 <= 2; o2 <<= 1) {
+    gs += __shfl_xor_sync(0xffffffffu, gs, o2);
+    fs += __shfl_xor_sync(0xffffffffu, fs, o2);
+    fps += __shfl_xor_sync(0xffffffffu, fps, o2);
+  }
+  for (int q = 0; q < 2; ++q) {
+    if ((warp >> 2) == q && t4 == 0) {
+      double* rb = red + slot * OUT;
       if (q == 0) {
-        red[lane * OUT + C::IG] = gs;
-        red[lane * OUT + C::IF] = fs;
-        red[lane * OUT + C::IFP] = fps;
+        rb[C::IG] = gs;
+        rb[C::IF] = fs;
+        rb[C::IFP] = fps;
       } else {
-        red[lane * OUT + C::IG] += gs;
-        red[lane * OUT + C::IF] += fs;
-        red[lane * OUT + C::IFP] += fps;
+        rb[C::IG] += gs;
+        rb[C::IF] += fs;
+        rb[C::IFP] += fps;
       }
     }
     __syncthreads();
   }
-  if (hit) atomicOr(&slots.hit[lane], 1);
+  if (hit) atomicOr(&slots.hit[slot], 1);
 }
 
 // Runs the pass. On return (after __syncthreads) red[b * OUT + e] holds the
@@ -468,11 +548,12 @@ __device__ void secular_pass(const double* __restrict__ d, const double* __restr
   double* red = dbuf + C::DBUF_DOUBLES;
   const int warp = threadIdx.x >> 5;
   if constexpr (C::MMA) {
-    const int g = warp % C::NG;
-    const int p = warp / C::NG;
-    if (g == 0) pass_body_mma<KP, 0>(d, u, n, slots, o, tiles, dbuf, red, p);
+    const int mh = warp & 1;
+    const int g = (warp >> 1) % C::NG;
+    const int p = warp / (2 * C::NG);
+    if (g == 0) pass_body_mma<KP, 0>(d, u, n, slots, o, tiles, dbuf, red, mh, p);
     if constexpr (C::NG > 1) {
-      if (g == 1) pass_body_mma<KP, 1>(d, u, n, slots, o, tiles, dbuf, red, p);
+      if (g == 1) pass_body_mma<KP, 1>(d, u, n, slots, o, tiles, dbuf, red, mh, p);
     }
     __syncthreads();
     return;
