@@ -58,7 +58,9 @@ int eigmod_b200_ctx_use_own_stream(eigmod_b200_ctx* ctx);
  * "pole_split" (1), "split_phase_a" (1: unisolated roots are bisected in a
  * first solver stage before the scalar presolve), "fnewton" (1), "fpre" (1),
  * "fpre_min_kp", "fpre_iters", "cluster", "fexit_rel", "floor_rel",
- * "floor_ulps", "stall_ratio", "geo_bisect", "trace_root". Unknown keys
+ * "floor_ulps", "stall_ratio", "geo_bisect", "trace_root", "fuse_alpha" (1:
+ * one-shot updates in exact mode take the residues of the scalar presolve
+ * from the pole-limit count pass instead of a separate K2 pass). Unknown keys
  * fail with a message. */
 int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value);
 const char* eigmod_b200_last_error(const eigmod_b200_ctx* ctx);

@@ -45,16 +45,25 @@ void project(eigmod_b200_ctx* c, const double* q, const double* kmat, int64_t n,
   eigb::transform_update_dev(q, kmat, n, (int)k, kp, lo, hi, u_out, c->ws, c->sms, c->stream);
 }
 
-// plan_from_u = plan_groups + K2 over all groups + plan_finish
+// plan_from_u = plan_groups + K2 over all groups + plan_finish.
+// fuse (one-shot callers whose solve covers all roots on this device): in
+// exact mode the plan needs no residues (classification is by coupling
+// mass), so K2 is skipped and the solve's pole-limit count pass, which
+// evaluates the same pole sum at every pole value, computes alpha_red.
 void plan_groups(eigmod_b200_ctx* c, const double* lam, const double* u, const int* signs,
                  int64_t n, int64_t k, double run_rel);
 
 void plan_from_u(eigmod_b200_ctx* c, const double* lam, const double* u, const int* signs,
-                 int64_t n, int64_t k, double run_rel) {
+                 int64_t n, int64_t k, double run_rel, bool fuse) {
   plan_groups(c, lam, u, signs, n, k, run_rel);
   eigb::Plan& p = c->plan;
   if (p.k == 0) return;
-  eigb::build_plan_weights(p, 0, p.ng, p.alpha, c->ws, c->stream);
+  const eigb::SolveOptions& o = c->sopt;
+  p.alpha_fused = fuse && p.exact && o.fuse_alpha && o.sweep && o.sweep_poles && o.fnewton;
+  if (p.alpha_fused)
+    EIGB_CUDA(cudaMemsetAsync(p.alpha, 0, 8 * std::max<int64_t>(p.ng, 1), c->stream));
+  else
+    eigb::build_plan_weights(p, 0, p.ng, p.alpha, c->ws, c->stream);
   eigb::build_plan_finish(p, lam, c->ws, c->stream);
   c->have_plan = true;
 }
@@ -175,8 +184,12 @@ void solve(eigmod_b200_ctx* c, int64_t j0, int64_t j1) {
   c->stage_calls[2] += 1;
   c->recs = alloc_records(c);
   if (c->plan.nred == 0) return;
-  eigb::solve_roots(c->plan.view(), c->plan.alpha_red_ok ? c->plan.alpha_red : nullptr, j0, j1,
-                    c->recs, c->sopt, c->ws, c->sms, c->stream);
+  const eigb::Plan& p = c->plan;
+  if (p.alpha_fused && !(j0 == 0 && j1 == p.nred))
+    throw Error(1, "", "solve: a fused-residue plan solves all roots at once");
+  eigb::solve_roots(p.view(), p.alpha_red_ok ? p.alpha_red : nullptr, j0, j1, c->recs, c->sopt,
+                    c->ws, c->sms, c->stream,
+                    (p.alpha_fused && p.alpha_red_ok) ? p.alpha_red : nullptr);
 }
 
 __global__ void copy_block_kernel(const double* __restrict__ a, int64_t n, int64_t c0, int64_t nc,
@@ -292,7 +305,7 @@ void full_device(eigmod_b200_ctx* c, const double* q, const double* lam, const d
   c->mark(0);
   project(c, q, kmat, n, k, 0, n, u);
   c->mark(1);
-  plan_from_u(c, lam, u, signs, n, k, c->run_rel);
+  plan_from_u(c, lam, u, signs, n, k, c->run_rel, true);
   c->mark(2);
   solve(c, 0, c->plan.nred);
   c->mark(3);
@@ -457,6 +470,8 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
       ctx->sopt.fnewton = value != 0.0;
     } else if (std::string(key) == "fpre") {
       ctx->sopt.fpre = value != 0.0;
+    } else if (std::string(key) == "fuse_alpha") {
+      ctx->sopt.fuse_alpha = value != 0.0;
     } else if (std::string(key) == "sweep_poles") {
       ctx->sopt.sweep_poles = value != 0.0;
     } else if (std::string(key) == "split_phase_a") {
@@ -747,7 +762,7 @@ int eigmod_b200_update_eigenvalues(eigmod_b200_ctx* ctx, const double* q, const 
     EIGB_CUDA(cudaMemcpyAsync(dl, lambda, 8 * n, cudaMemcpyHostToDevice, st));
     EIGB_CUDA(cudaMemcpyAsync(dk, kmat, 8 * n * k, cudaMemcpyHostToDevice, st));
     project(ctx, dq, dk, n, k, 0, n, du);
-    plan_from_u(ctx, dl, du, signs, n, k, ctx->run_rel);
+    plan_from_u(ctx, dl, du, signs, n, k, ctx->run_rel, true);
     solve(ctx, 0, ctx->plan.nred);
     finish(ctx, dq, dl, 0, 0, dlo, nullptr, n);
     const eigb::Plan& p = ctx->plan;
@@ -1051,7 +1066,7 @@ int eigmod_b200_assemble_from_u(eigmod_b200_ctx* ctx, const double* q, const dou
       for (int64_t c = 0; c < k; ++c) up[i * kp + c] = u[i * k + c];
     double* du = ctx->ws.get_f64("h_u", (size_t)n * kp);
     EIGB_CUDA(cudaMemcpyAsync(du, up.data(), 8 * up.size(), cudaMemcpyHostToDevice, st));
-    plan_from_u(ctx, dl, du, signs, n, k, ctx->run_rel);
+    plan_from_u(ctx, dl, du, signs, n, k, ctx->run_rel, true);
     solve(ctx, 0, ctx->plan.nred);
     finish(ctx, dq, dl, 0, n, dlo, dqo, n);
     EIGB_CUDA(cudaMemcpyAsync(lambda_out, dlo, 8 * n, cudaMemcpyDeviceToHost, st));
@@ -1115,7 +1130,7 @@ int eigmod_b200_assemble(eigmod_b200_ctx* ctx, const double* q, const double* la
         for (int64_t c = 0; c < k; ++c) up[i * kp + c] = u[i * k + c];
       double* du = ctx->ws.get_f64("h_u", (size_t)n * kp);
       EIGB_CUDA(cudaMemcpyAsync(du, up.data(), 8 * up.size(), cudaMemcpyHostToDevice, st));
-      plan_from_u(ctx, dl, du, signs, n, k, ctx->run_rel);
+      plan_from_u(ctx, dl, du, signs, n, k, ctx->run_rel, true);
       solve(ctx, 0, ctx->plan.nred);
       finish(ctx, dq, nullptr, 0, 0, dlo, nullptr, n);
       std::vector<double> got(n);

@@ -141,7 +141,7 @@ void project(eigmod_b200_ctx* c, const double* q, const double* kmat, int64_t n,
 void plan_groups(eigmod_b200_ctx* c, const double* lam, const double* u, const int* signs,
                  int64_t n, int64_t k, double run_rel);
 void plan_from_u(eigmod_b200_ctx* c, const double* lam, const double* u, const int* signs,
-                 int64_t n, int64_t k, double run_rel);
+                 int64_t n, int64_t k, double run_rel, bool fuse = false);
 void solve(eigmod_b200_ctx* c, int64_t j0, int64_t j1);
 // root records of [j0, j0 + cnt) packed as eigmod_b200_record_width(kp)
 // doubles each (the all-gather payload), and all records back from it

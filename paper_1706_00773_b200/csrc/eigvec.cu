@@ -104,20 +104,14 @@ __device__ void sym_evd_dev(double* a, int k, double* v) {
 template <int KP>
 constexpr int kCollStride = 2 * KP + 4;
 
-template <int KP>
-__global__ void __launch_bounds__(kPassThreads, 1) collision_kernel(
-    ReducedView rp, const int64_t* __restrict__ list, int64_t cnt, const int64_t* __restrict__ origin,
-    const double* __restrict__ rdelta, const int* __restrict__ mark, const int* __restrict__ which,
-    double gap, double* __restrict__ colldir, int* __restrict__ collok, double* __restrict__ scratch,
-    const double* __restrict__ yall) {
-  using C = PassCfg<KP>;
-  constexpr int MK = 2 * KP;
-  extern __shared__ __align__(16) double smem[];
-  __shared__ double dob[32], delta[32];
-  __shared__ int active[32], hit[32];
-  __shared__ int64_t xrow[32];
+// Slots of a batch of 32 bordered roots: pole value, delta, and the row of R
+// when R is the origin row alone (-1: the rows within gap of v).
+__device__ __forceinline__ void collision_slots(const ReducedView& rp, const int64_t* list,
+                                                int64_t cnt, const int64_t* origin,
+                                                const double* rdelta, const int* mark, int64_t b0,
+                                                double* dob, double* delta, int* active, int* hit,
+                                                int64_t* xrow) {
   const int t = threadIdx.x;
-  const int64_t b0 = (int64_t)blockIdx.x * 32;
   if (t < 32) {
     const int64_t q = b0 + t;
     active[t] = q < cnt;
@@ -137,13 +131,75 @@ __global__ void __launch_bounds__(kPassThreads, 1) collision_kernel(
     xrow[t] = xr;
     hit[t] = 0;
   }
+}
+
+// The pole pass of collision_kernel split over gridDim.y pole slices (one
+// bordered root would otherwise run the whole pass on one CTA): slice s
+// writes its partial sums to partial[(blockIdx.x * S + s)][32][OUT].
+template <int KP>
+__global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) collision_pass_kernel(
+    ReducedView rp, const int64_t* __restrict__ list, int64_t cnt, const int64_t* __restrict__ origin,
+    const double* __restrict__ rdelta, const int* __restrict__ mark, double gap,
+    double* __restrict__ partial) {
+  using C = PassCfg<KP>;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double dob[32], delta[32];
+  __shared__ int active[32], hit[32];
+  __shared__ int64_t xrow[32];
+  const int64_t b0 = (int64_t)blockIdx.x * 32;
+  collision_slots(rp, list, cnt, origin, rdelta, mark, b0, dob, delta, active, hit, xrow);
+  const int S = gridDim.y, s = blockIdx.y;
+  const int64_t chunk = cdiv_dev(rp.n, (int64_t)S);
+  const int64_t plo = (s * chunk < rp.n) ? s * chunk : rp.n;
+  const int64_t pcnt = ((plo + chunk < rp.n) ? plo + chunk : rp.n) - plo;
+  __syncthreads();
+  if (threadIdx.x < 32 && xrow[threadIdx.x] >= 0) {  // slice-local row index (none: never matches)
+    const int64_t xl = xrow[threadIdx.x] - plo;
+    xrow[threadIdx.x] = (xl >= 0 && xl < pcnt) ? xl : INT64_MAX;
+  }
   __syncthreads();
   PassSlots sl{dob, delta, nullptr, active, hit, xrow};
   PassOpts o;
   o.exclude_zero = true;
-  o.excl_gap = gap;  // rows within gap of v: the bordered block
-  secular_pass<KP>(rp.d, rp.u, rp.n, sl, o, smem);
+  o.excl_gap = gap;
+  secular_pass<KP>(rp.d + plo, rp.u + plo * KP, pcnt, sl, o, smem);
   const double* red = pass_result<KP>(smem);
+  double* out = partial + ((size_t)blockIdx.x * S + s) * C::RED_DOUBLES;
+  for (int e = threadIdx.x; e < C::RED_DOUBLES; e += kPassThreads) out[e] = red[e];
+}
+
+template <int KP>
+__global__ void __launch_bounds__(kPassThreads, 1) collision_kernel(
+    ReducedView rp, const int64_t* __restrict__ list, int64_t cnt, const int64_t* __restrict__ origin,
+    const double* __restrict__ rdelta, const int* __restrict__ mark, const int* __restrict__ which,
+    double gap, double* __restrict__ colldir, int* __restrict__ collok, double* __restrict__ scratch,
+    const double* __restrict__ yall, const double* __restrict__ partial, int splits) {
+  using C = PassCfg<KP>;
+  constexpr int MK = 2 * KP;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double dob[32], delta[32];
+  __shared__ int active[32], hit[32];
+  __shared__ int64_t xrow[32];
+  const int t = threadIdx.x;
+  const int64_t b0 = (int64_t)blockIdx.x * 32;
+  collision_slots(rp, list, cnt, origin, rdelta, mark, b0, dob, delta, active, hit, xrow);
+  __syncthreads();
+  double* red = const_cast<double*>(pass_result<KP>(smem));
+  if (splits > 1) {  // the slices' partial sums, in slice order
+    const double* pb = partial + (size_t)blockIdx.x * splits * C::RED_DOUBLES;
+    for (int e = t; e < C::RED_DOUBLES; e += kPassThreads) {
+      double v = 0.0;
+      for (int s = 0; s < splits; ++s) v += pb[(size_t)s * C::RED_DOUBLES + e];
+      red[e] = v;
+    }
+    __syncthreads();
+  } else {
+    PassSlots sl{dob, delta, nullptr, active, hit, xrow};
+    PassOpts o;
+    o.exclude_zero = true;
+    o.excl_gap = gap;  // rows within gap of v: the bordered block
+    secular_pass<KP>(rp.d, rp.u, rp.n, sl, o, smem);
+  }
   if (t < 32 && active[t]) {
     const int64_t j = list[b0 + t];
     const int64_t N = rp.n;
@@ -870,6 +926,178 @@ __global__ void __launch_bounds__(256, KP >= 32 ? 1 : 2) xt_rows_kernel(
   }
 }
 
+// K4 v4 (plans without compressed runs, KP >= 4): the dot products
+// P[c][i] = y_c . u_r(i) on the FP64 tensor pipe. One CTA = 128 columns
+// (16 m-tiles of 8 columns, two per warp) x 256 original rows (32 n-tiles);
+// A fragments (y of the warp's columns) stay in registers, B fragments come
+// from the CTA's U rows staged in shared memory (rows padded to KP + 4
+// doubles: conflict-free fragment loads). A lane holds P for column
+// 8 m + lane / 4 and rows 8 nt + 2 (lane % 4) + {0, 1}: the epilogue divides
+// by (d_r - d_o) - delta (or applies the bordered / unit rules of special
+// columns, as xt_rows_kernel) and stores the row pair as one 16-byte store
+// (a warp store fills 8 columns x 64 contiguous bytes). Column sums of
+// squares: per lane, then over the 4 lanes of a column (butterfly), one
+// partial per (column, CTA row block) reduced in order by xt_norm_kernel.
+constexpr int kXtmCols = 128, kXtmRows = 256;
+
+template <int KP>
+struct XtmSmem {
+  static constexpr int LDU = KP + 4;
+  double ut[kXtmRows * LDU];
+  double yt[kXtmCols * LDU];
+  double drow[kXtmRows];
+  int64_t rr[kXtmRows];
+  double cdob[kXtmCols], cdel[kXtmCols];
+  int64_t co[kXtmCols], cj[kXtmCols];
+  int ck[kXtmCols], cm[kXtmCols];
+};
+
+template <int KP>
+__global__ void __launch_bounds__(256, 2) xt_mma_kernel(
+    ReducedView rp, int64_t n, const int* __restrict__ ckind, const int64_t* __restrict__ cpay,
+    const int64_t* __restrict__ origin, const double* __restrict__ delta,
+    const int* __restrict__ flags, const double* __restrict__ yall,
+    const double* __restrict__ colldir, const int* __restrict__ collok,
+    const int64_t* __restrict__ orig_map, const int64_t* __restrict__ dec_src, int64_t c0,
+    int64_t c1, double* __restrict__ xt, double* __restrict__ part) {
+  using SM = XtmSmem<KP>;
+  constexpr int LDU = SM::LDU, KC = KP / 4;
+  extern __shared__ __align__(16) double xsm[];
+  SM& sm = *reinterpret_cast<SM*>(xsm);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int t4 = lane & 3, g8 = lane >> 2;
+  const int64_t cb = c0 + (int64_t)blockIdx.y * kXtmCols;
+  const int64_t ib = (int64_t)blockIdx.x * kXtmRows;
+  // column parameters (as xt_rows_kernel)
+  if (t < kXtmCols) {
+    const int64_t c = cb + t;
+    int kind = -1, mode = 0;
+    int64_t o = 0, jr = 0;
+    double dob = 0.0, del = 0.0;
+    double* y = sm.yt + t * LDU;
+    for (int q = 0; q < KP; ++q) y[q] = 0.0;
+    if (c < c1) {
+      kind = ckind[c];
+      const int64_t pay = cpay[c];
+      if (kind == 0) {
+        const int64_t j = pay;
+        jr = j;
+        o = origin[j];
+        dob = rp.d[o];
+        del = delta[j];
+        const bool coll = (flags[j] & 1) != 0;
+        mode = (collok[j] == 1) ? 1 : ((collok[j] == 2 && coll) ? 2 : 0);
+        const double* src = (mode == 1) ? colldir + j * kCollStride<KP> : yall + j * KP;
+        for (int q = 0; q < KP; ++q) y[q] = src[q];
+      } else if (kind == 1) {
+        o = dec_src[pay];
+      }
+    }
+    sm.ck[t] = kind;
+    sm.cm[t] = mode;
+    sm.co[t] = o;
+    sm.cj[t] = jr;
+    sm.cdob[t] = dob;
+    sm.cdel[t] = del;
+  }
+  // rows: reduced index, pole value, u row (zero outside the reduced problem)
+  for (int q = t; q < kXtmRows; q += 256) {
+    const int64_t i = ib + q;
+    const int64_t r = (i < n) ? orig_map[i] : -1;
+    sm.rr[q] = r;
+    sm.drow[q] = (r >= 0) ? rp.d[r] : 0.0;
+  }
+  __syncthreads();
+  for (int q = t; q < kXtmRows * (KP / 2); q += 256) {
+    const int row = q / (KP / 2), c2 = q % (KP / 2);
+    const int64_t r = sm.rr[row];
+    const double2 v = (r >= 0) ? __ldg(reinterpret_cast<const double2*>(rp.u + r * KP) + c2)
+                               : make_double2(0.0, 0.0);
+    *reinterpret_cast<double2*>(sm.ut + row * LDU + 2 * c2) = v;
+  }
+  __syncthreads();
+  // this lane's two columns (m-tiles 2 warp, 2 warp + 1)
+  double af[2][KC];
+  int qc[2];
+  bool fast[2];
+  double s2[2] = {0.0, 0.0};
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    qc[m] = 8 * (2 * warp + m) + g8;
+#pragma unroll
+    for (int kc = 0; kc < KC; ++kc) af[m][kc] = sm.yt[qc[m] * LDU + 4 * kc + t4];
+    fast[m] = sm.ck[qc[m]] == 0 && sm.cm[qc[m]] == 0;
+  }
+  const bool vec = (n % 2) == 0;
+#pragma unroll 2
+  for (int nt = 0; nt < kXtmRows / 8; ++nt) {
+    double bf[KC];
+#pragma unroll
+    for (int kc = 0; kc < KC; ++kc) bf[kc] = sm.ut[(8 * nt + g8) * LDU + 4 * kc + t4];
+    const int q0 = 8 * nt + 2 * t4;  // this lane's rows q0, q0 + 1
+    const double d0 = sm.drow[q0], d1 = sm.drow[q0 + 1];
+    const int64_t r0 = sm.rr[q0], r1 = sm.rr[q0 + 1];
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) dmma(p0, p1, af[m][kc], bf[kc]);
+      const int qm = qc[m];
+      const int64_t c = cb + qm;
+      double x0, x1;
+      if (fast[m]) {
+        const double dob = sm.cdob[qm], del = sm.cdel[qm];
+        x0 = (r0 >= 0) ? p0 * rcp64((d0 - dob) - del) : 0.0;
+        x1 = (r1 >= 0) ? p1 * rcp64((d1 - dob) - del) : 0.0;
+      } else {
+        const int kind = sm.ck[qm], mode = sm.cm[qm];
+        const int64_t co = sm.co[qm];
+        double xv[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t r = h ? r1 : r0;
+          const int64_t i = ib + q0 + h;
+          const double dot = h ? p1 : p0, dr = h ? d1 : d0;
+          double x = 0.0;
+          if (kind == 0 && mode == 2) {  // collided fallback e_o
+            x = (r >= 0 && r == co) ? 1.0 : 0.0;
+          } else if (kind == 0) {  // bordered system; dot = u_r . z
+            const double* cd = colldir + sm.cj[qm] * kCollStride<KP>;
+            const int64_t rb0 = (int64_t)cd[2 * KP], nr0 = (int64_t)cd[2 * KP + 1];
+            if (r < 0) x = 0.0;
+            else if (r >= rb0 && r < rb0 + nr0) x = cd[KP + (r - rb0)];
+            else x = -dot / ((dr - cd[2 * KP + 3]) - cd[2 * KP + 2]);
+          } else if (kind == 1) {  // unit column of an unchanged pair
+            x = (i == co) ? 1.0 : 0.0;
+          }
+          xv[h] = x;
+        }
+        x0 = xv[0];
+        x1 = xv[1];
+      }
+      const int64_t i = ib + q0;
+      if (c < c1) {
+        double* dst = xt + (c - c0) * n + i;
+        if (vec && i + 1 < n) {
+          __stcs(reinterpret_cast<double2*>(dst), make_double2(x0, x1));
+        } else {
+          if (i < n) __stcs(dst, x0);
+          if (i + 1 < n) __stcs(dst + 1, x1);
+        }
+      }
+      s2[m] = fma(x0, x0, s2[m]);
+      s2[m] = fma(x1, x1, s2[m]);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    s2[m] += __shfl_xor_sync(0xffffffffu, s2[m], 1);
+    s2[m] += __shfl_xor_sync(0xffffffffu, s2[m], 2);
+    const int64_t c = cb + qc[m];
+    if (t4 == 0 && c < c1) part[(c - c0) * gridDim.x + blockIdx.x] = s2[m];
+  }
+}
+
 template <int KP>
 void launch_xt(const Plan& p, const RootRecords& roots, const Columns& cols, const double* colldir,
                const int* collok, bool general, int64_t c0, int64_t c1, double* xt,
@@ -884,6 +1112,30 @@ void launch_xt(const Plan& p, const RootRecords& roots, const Columns& cols, con
   if (v2 < 0) {
     const char* e = std::getenv("EIGMOD_B200_XT");
     v2 = (e && std::string(e) == "v2");
+  }
+  static int v3 = -1;  // EIGMOD_B200_XT=v3 selects the DFMA row kernel
+  if (v3 < 0) {
+    const char* e = std::getenv("EIGMOD_B200_XT");
+    v3 = (e && std::string(e) == "v3");
+  }
+  if constexpr (KP >= 4) {
+    if (!v1 && !v2 && !v3 && p.nmulti == 0) {
+      const int64_t nchunks = cdiv(p.n, kXtmRows);
+      double* part = ws.get_f64("xt_part", (size_t)nchunks * (c1 - c0));
+      dim3 grid((unsigned)nchunks, (unsigned)cdiv(c1 - c0, kXtmCols));
+      const size_t sm = sizeof(XtmSmem<KP>);
+      EIGB_CUDA(cudaFuncSetAttribute(xt_mma_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sm));
+      xt_mma_kernel<KP><<<grid, 256, sm, st>>>(p.view(), p.n, cols.kind, cols.payload,
+                                               roots.origin, roots.delta, roots.flags, roots.y,
+                                               colldir, collok, p.orig_map, p.dec_src, c0, c1, xt,
+                                               part);
+      EIGB_LAUNCH_CHECK();
+      xt_norm_kernel<<<(unsigned)cdiv(c1 - c0, 128), 128, 0, st>>>(part, nchunks, c0, c1,
+                                                                   cols.kind, colscale, cmode);
+      EIGB_LAUNCH_CHECK();
+      return;
+    }
   }
   if (!v1 && !v2 && p.nmulti == 0) {
     using RC = XtRowsCfg<KP>;
@@ -944,12 +1196,28 @@ void launch_collisions(const Plan& p, const RootRecords& roots, const int64_t* l
   const int grid = (int)cdiv(cnt, 32);
   double* scratch = ws.get_f64("coll_scratch", (size_t)grid * 32 * 4 * (2 * KP) * (2 * KP));
   const size_t sm = sizeof(double) * C::SMEM_DOUBLES;
+  const double gap = kPoleMergeRelGap * p.scale;
+  // few batches: split each batch's pole pass over slices of >= 256 poles so
+  // that about two CTAs per SM run it
+  int dev = 0, sms = 148;
+  EIGB_CUDA(cudaGetDevice(&dev));
+  EIGB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int splits = (int)std::max<int64_t>(
+      1, std::min<int64_t>(cdiv(p.nred, 256), (2 * sms) / grid));
+  double* partial = nullptr;
+  if (splits > 1) {
+    partial = ws.get_f64("coll_partial", (size_t)grid * splits * C::RED_DOUBLES);
+    EIGB_CUDA(cudaFuncSetAttribute(collision_pass_kernel<KP>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    collision_pass_kernel<KP><<<dim3(grid, splits), kPassThreads, sm, st>>>(
+        p.view(), list, cnt, roots.origin, roots.delta, mark, gap, partial);
+    EIGB_LAUNCH_CHECK();
+  }
   EIGB_CUDA(cudaFuncSetAttribute(collision_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sm));
   collision_kernel<KP><<<grid, kPassThreads, sm, st>>>(p.view(), list, cnt, roots.origin,
-                                                       roots.delta, mark, which,
-                                                       kPoleMergeRelGap * p.scale, colldir, collok,
-                                                       scratch, roots.y);
+                                                       roots.delta, mark, which, gap, colldir,
+                                                       collok, scratch, roots.y, partial, splits);
   EIGB_LAUNCH_CHECK();
 }
 

@@ -133,25 +133,33 @@ void rank_update(eigmod_b200_multi* mg, int g, const double* q, const double* la
   EIGB_CUDA(cudaMemsetAsync(u_part, 0, 8 * (size_t)std::max<int64_t>(rc, 1) * kp, st));
   if (r1 > r0) project(c, dq, dk, n, k, r0, r1, u_part);
   EIGB_NCCL(nc, nc->AllGather(u_part, u_all, (size_t)rc * kp, ncclDouble, comm, st));
-  // 3. plan: groups everywhere, K2 weights by group slice, all-gathered
-  plan_groups(c, dl, u_all, signs, n, k, c->run_rel);
+  // 3. plan: groups everywhere, K2 weights by group slice, all-gathered (one
+  // device: the one-shot plan, whose solve takes the residues from its count
+  // pass, so G = 1 is the single-device path bit for bit)
   eigb::Plan& p = c->plan;
-  if (k_eff_out && g == 0) *k_eff_out = p.k;
-  if (p.k == 0) {  // nothing couples: rank 0 copies lambda and Q on the host
+  if (G == 1) {
+    plan_from_u(c, dl, u_all, signs, n, k, c->run_rel, true);
+    if (k_eff_out) *k_eff_out = p.k;
+    if (p.k == 0) return;  // nothing couples: rank 0 copies lambda and Q on the host
+  } else {
+    plan_groups(c, dl, u_all, signs, n, k, c->run_rel);
+    if (k_eff_out && g == 0) *k_eff_out = p.k;
+    if (p.k == 0) {  // nothing couples: rank 0 copies lambda and Q on the host
+      c->have_plan = true;
+      return;
+    }
+    int64_t g0, g1, gc;
+    split_range(p.ng, G, g, &g0, &g1, &gc);
+    gc = std::max<int64_t>(gc, 1);
+    double* a_part = c->ws.get_f64("mg_apart", gc);
+    double* a_all = c->ws.get_f64("mg_aall", (size_t)gc * G);
+    EIGB_CUDA(cudaMemsetAsync(a_part, 0, 8 * gc, st));
+    if (g1 > g0) eigb::build_plan_weights(p, g0, g1, a_part, c->ws, st);
+    EIGB_NCCL(nc, nc->AllGather(a_part, a_all, (size_t)gc, ncclDouble, comm, st));
+    EIGB_CUDA(cudaMemcpyAsync(p.alpha, a_all, 8 * p.ng, cudaMemcpyDeviceToDevice, st));
+    eigb::build_plan_finish(p, c->lam, c->ws, st);
     c->have_plan = true;
-    return;
   }
-  int64_t g0, g1, gc;
-  split_range(p.ng, G, g, &g0, &g1, &gc);
-  gc = std::max<int64_t>(gc, 1);
-  double* a_part = c->ws.get_f64("mg_apart", gc);
-  double* a_all = c->ws.get_f64("mg_aall", (size_t)gc * G);
-  EIGB_CUDA(cudaMemsetAsync(a_part, 0, 8 * gc, st));
-  if (g1 > g0) eigb::build_plan_weights(p, g0, g1, a_part, c->ws, st);
-  EIGB_NCCL(nc, nc->AllGather(a_part, a_all, (size_t)gc, ncclDouble, comm, st));
-  EIGB_CUDA(cudaMemcpyAsync(p.alpha, a_all, 8 * p.ng, cudaMemcpyDeviceToDevice, st));
-  eigb::build_plan_finish(p, c->lam, c->ws, st);
-  c->have_plan = true;
   // 4. roots of index slice g, records all-gathered
   const int64_t nred = p.nred;
   int64_t j0, j1, jc;

@@ -28,6 +28,7 @@ struct Plan {
   int64_t nred = 0, ndec = 0;
   double *d = nullptr, *ur = nullptr, *dec_val = nullptr, *alpha_red = nullptr;
   bool alpha_red_ok = false;  // every reduced pole is simple (no compressed run rows)
+  bool alpha_fused = false;  // alpha_red comes from the solve's count pass (no K2 pass)
   int64_t *red_src = nullptr, *dec_src = nullptr, *orig_map = nullptr, *off_red = nullptr,
           *off_dec = nullptr;
   double scale = 1.0, alpha_mass = 0.0, u_mass = 0.0, lo_clip = 0.0, hi_clip = 0.0;

@@ -1739,8 +1739,72 @@ struct InertiaArgs {
   const int* bcnt;      // number of rows at the pole
   int64_t nb;
   int* nu;              // out: inertia of the projected T
-  double* scratch;      // gridDim.x * 32 * (2 * KP * KP + KP)
+  double* scratch;      // gridDim.x * 32 * kInertiaScratch<KP>
+  double* alpha_out;    // != nullptr: residue of every simple pole (at its row)
 };
+
+template <int KP>
+constexpr int kInertiaScratch = 6 * KP * KP + KP;
+
+// Residue of the simple pole v with row w (proj/src/secular.cpp:168-202, as
+// group_weights_kernel): S = J + T(v) over the other rows, M = J S, alpha =
+// w^T adj(M) J w = det(J) det(S) w^T S^-1 w from a Bunch-Kaufman
+// factorization of S; pivots spanning more than 1e8 take the reference's
+// adjugate route. S: full k x k (ld KP); rb: the pass result (packed T).
+template <int KP>
+__device__ double pole_residue(const double* S, const double* rb, const int* sgn, int k,
+                               const double* w, double* work) {
+  using C = PassCfg<KP>;
+  double* A = work;  // KP * KP
+  for (int r = 0; r < k; ++r)
+    for (int c = 0; c < k; ++c) A[r * KP + c] = S[r * KP + c];
+  int piv[KP], zero = 0;
+  bk_factor(A, k, KP, piv, &zero, 1);
+  double det = 1.0, pmax = 0.0, pmin = INFINITY;
+  for (int q = 0; q < k;) {
+    double pv;
+    if (piv[q] >= 0) {
+      pv = A[q * KP + q];
+      det *= pv;
+      pv = fabs(pv);
+      q += 1;
+    } else {
+      const double d2 = A[q * KP + q] * A[(q + 1) * KP + q + 1] - A[(q + 1) * KP + q] * A[(q + 1) * KP + q];
+      det *= d2;
+      pv = sqrt(fabs(d2));
+      q += 2;
+    }
+    pmax = fmax(pmax, pv);
+    pmin = fmin(pmin, pv);
+  }
+  double sj = 1.0;
+  for (int r = 0; r < k; ++r) sj *= (double)sgn[r];
+  if (!zero && pmin > 1e-8 * pmax && isfinite(det)) {
+    double z[KP];
+    for (int r = 0; r < k; ++r) z[r] = w[r];
+    bk_solve(A, k, KP, piv, z, 0.0, 1);
+    double v = 0.0;
+    for (int r = 0; r < k; ++r) v += w[r] * z[r];
+    return sj * det * v;
+  }
+  // the reference's adjugate route (ill-conditioned M)
+  double* M = work;  // KP * KP (A is dead)
+  double* adj = M + KP * KP;
+  double* aw = adj + KP * KP;  // 2 KP * KP
+  for (int r = 0; r < k; ++r)
+    for (int c = 0; c < k; ++c) {
+      const double tv = (r <= c) ? rb[C::pidx(r, c)] : rb[C::pidx(c, r)];
+      M[r * KP + c] = (r == c ? 1.0 : 0.0) + (double)sgn[r] * tv;
+    }
+  adjugate_dev(M, k, KP, adj, aw);
+  double al = 0.0;
+  for (int r = 0; r < k; ++r) {
+    double tt = 0.0;
+    for (int c = 0; c < k; ++c) tt += adj[r * KP + c] * (double)sgn[c] * w[c];
+    al += w[r] * tt;
+  }
+  return al;
+}
 
 template <int KP>
 __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) pole_inertia_kernel(InertiaArgs<KP> a) {
@@ -1765,11 +1829,18 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) pole_inertia_k
   if (t >= 32 || !active[t]) return;
   const int64_t g = g0 + t;
   const int k = a.rp.k;
-  double* T = a.scratch + ((size_t)blockIdx.x * 32 + t) * (2 * KP * KP + KP);
+  double* T = a.scratch + ((size_t)blockIdx.x * 32 + t) * kInertiaScratch<KP>;
   double* W = T + KP * KP;   // reflectors, one per row of R
   double* x = W + KP * KP;
   const double* rb = pass_result<KP>(smem) + t * C::OUT;
   load_S<KP>(rb, a.rp.sgn, k, T, 1);
+  if (a.alpha_out) {
+    const int64_t r0 = a.brow[g];
+    if (a.bcnt[g] == 1)
+      a.alpha_out[r0] = pole_residue<KP>(T, rb, a.rp.sgn, k, a.rp.u + r0 * KP, x + KP);
+    else
+      for (int r = 0; r < a.bcnt[g]; ++r) a.alpha_out[r0 + r] = 0.0;  // not a simple pole
+  }
   // Householder vectors of span(R): reflector q acts on coordinates q..k-1
   int q = 0;
   const int64_t r0 = a.brow[g];
@@ -1818,11 +1889,12 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) pole_inertia_k
 
 template <int KP>
 void launch_inertia(const ReducedView& rp, const double* bval, const int64_t* brow,
-                    const int* bcnt, int64_t nb, int* nu, DeviceScratch& ws, cudaStream_t st) {
+                    const int* bcnt, int64_t nb, int* nu, double* alpha_out, DeviceScratch& ws,
+                    cudaStream_t st) {
   using C = PassCfg<KP>;
   const int grid = (int)cdiv(nb, 32);
-  InertiaArgs<KP> a{rp, bval, brow, bcnt, nb, nu, nullptr};
-  a.scratch = ws.get_f64("inertia_scratch", (size_t)grid * 32 * (2 * KP * KP + KP));
+  InertiaArgs<KP> a{rp, bval, brow, bcnt, nb, nu, nullptr, alpha_out};
+  a.scratch = ws.get_f64("inertia_scratch", (size_t)grid * 32 * kInertiaScratch<KP>);
   const size_t sm = sizeof(double) * C::SMEM_DOUBLES;
   EIGB_CUDA(cudaFuncSetAttribute(pole_inertia_kernel<KP>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -2000,7 +2072,7 @@ void solve_after_counts(const ReducedView& rp, const double* alpha, int64_t j0, 
 
 void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t j1,
                  const RootRecords& out, const SolveOptions& opt, DeviceScratch& ws, int sms,
-                 cudaStream_t st) {
+                 cudaStream_t st, double* alpha_fill) {
   if (j1 <= j0) return;
   int* counts = nullptr;
   // points next to the poles of every Weyl window of roots [j0, j1)
@@ -2028,16 +2100,21 @@ void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t
     unsigned long long nh = 0;
     EIGB_CUDA(cudaMemcpyAsync(&nh, nsel, 8, cudaMemcpyDeviceToHost, st));
     EIGB_CUDA(cudaStreamSynchronize(st));
+    // the residues need every pole value of the problem in the window
+    if (alpha_fill && !(pb == 0 && pe == rp.n))
+      throw Error(1, "", "solve_roots: fused residues need all poles");
     if (nh > 0) {
-      pole_inertia(rp, bval, brow, bcnt, (int64_t)nh, nu, ws, st);
+      pole_inertia(rp, bval, brow, bcnt, (int64_t)nh, nu, ws, st, alpha_fill);
       pole_scatter_kernel<<<(unsigned)cdiv((int64_t)nh, 256), 256, 0, st>>>(list, brow, bcnt, nu,
                                                                            (int64_t)nh, rp.m_neg,
                                                                            pcounts);
       EIGB_LAUNCH_CHECK();
     }
+    if (alpha_fill) alpha = alpha_fill;
     solve_after_counts(rp, alpha, j0, j1, out, opt, ws, sms, st, nullptr, pcounts, pb, pe);
     return;
   }
+  if (alpha_fill) throw Error(1, "", "solve_roots: fused residues need the pole-limit counts");
   if (opt.sweep) {
     counts = ws.get_i32("sweep_counts", 2 * rp.n);
     switch (rp.kp) {
@@ -2068,7 +2145,7 @@ void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t
     EIGB_CUDA(cudaMemcpyAsync(&nh, nsel, 8, cudaMemcpyDeviceToHost, st));
     EIGB_CUDA(cudaStreamSynchronize(st));
     if (nh > 0) {
-      pole_inertia(rp, bval, brow, bcnt, (int64_t)nh, nu, ws, st);
+      pole_inertia(rp, bval, brow, bcnt, (int64_t)nh, nu, ws, st, nullptr);
       pole_scatter_kernel<<<(unsigned)cdiv((int64_t)nh, 256), 256, 0, st>>>(list, brow, bcnt, nu,
                                                                            (int64_t)nh, rp.m_neg,
                                                                            pcounts);
@@ -2094,15 +2171,15 @@ void group_weights(int kp, const double* rep, const double* u, int64_t n, const 
 }
 
 void pole_inertia(const ReducedView& rp, const double* bval, const int64_t* brow, const int* bcnt,
-                  int64_t nb, int* nu, DeviceScratch& ws, cudaStream_t st) {
+                  int64_t nb, int* nu, DeviceScratch& ws, cudaStream_t st, double* alpha_out) {
   if (nb <= 0) return;
   switch (rp.kp) {
-    case 1: launch_inertia<1>(rp, bval, brow, bcnt, nb, nu, ws, st); break;
-    case 2: launch_inertia<2>(rp, bval, brow, bcnt, nb, nu, ws, st); break;
-    case 4: launch_inertia<4>(rp, bval, brow, bcnt, nb, nu, ws, st); break;
-    case 8: launch_inertia<8>(rp, bval, brow, bcnt, nb, nu, ws, st); break;
-    case 16: launch_inertia<16>(rp, bval, brow, bcnt, nb, nu, ws, st); break;
-    case 32: launch_inertia<32>(rp, bval, brow, bcnt, nb, nu, ws, st); break;
+    case 1: launch_inertia<1>(rp, bval, brow, bcnt, nb, nu, alpha_out, ws, st); break;
+    case 2: launch_inertia<2>(rp, bval, brow, bcnt, nb, nu, alpha_out, ws, st); break;
+    case 4: launch_inertia<4>(rp, bval, brow, bcnt, nb, nu, alpha_out, ws, st); break;
+    case 8: launch_inertia<8>(rp, bval, brow, bcnt, nb, nu, alpha_out, ws, st); break;
+    case 16: launch_inertia<16>(rp, bval, brow, bcnt, nb, nu, alpha_out, ws, st); break;
+    case 32: launch_inertia<32>(rp, bval, brow, bcnt, nb, nu, alpha_out, ws, st); break;
     default: throw Error(1, "", "pole_inertia: unsupported padded rank");
   }
 }

@@ -102,6 +102,9 @@ struct SolveOptions {
   // so they get the presolve too, then finish every root (stage 2)
   bool split_phase_a = true;
   int fpre_iters = 12;
+  // exact mode, one device: the residues alpha come from the pole-limit count
+  // pass (the same pole sum at every pole value) instead of a K2 pass
+  bool fuse_alpha = true;
 };
 
 // Diagnostics trace of one root: per evaluation kTraceCols doubles
@@ -111,16 +114,21 @@ constexpr int kTraceRows = 200;
 
 // alpha: residues of the reduced poles for the f-Newton phase (nullptr when
 // the reduced problem has compressed runs, whose poles are not simple).
+// alpha_fill != nullptr (pole-limit counts on, every pole in the window): the
+// count pass also computes the residue of every simple reduced pole into
+// alpha_fill (proj/src/secular.cpp:168-202 at the pole value, the pole's own
+// row excluded) and the solve uses them as alpha.
 void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t j1,
                  const RootRecords& out, const SolveOptions& opt, DeviceScratch& ws, int sms,
-                 cudaStream_t st);
+                 cudaStream_t st, double* alpha_fill = nullptr);
 
 // Location-vector support: for each of nb reduced pole values bval[b] (rows
 // brow[b] .. brow[b]+bcnt[b]-1 of rp sit at that value), nu[b] = negative
 // inertia of T = J + sum_{other rows} u u^T/(d - v) restricted to the
 // orthogonal complement of the pole's rows. #eig < v = #{d < v} + m - nu.
 void pole_inertia(const ReducedView& rp, const double* bval, const int64_t* brow, const int* bcnt,
-                  int64_t nb, int* nu, DeviceScratch& ws, cudaStream_t st);
+                  int64_t nb, int* nu, DeviceScratch& ws, cudaStream_t st,
+                  double* alpha_out = nullptr);
 
 void group_weights(int kp, const double* rep, const double* u, int64_t n, const int64_t* gstart,
                    const int64_t* glen, const double* gval, int64_t ng, const int* sgn, int k,

@@ -276,7 +276,7 @@ def test_deterministic(api, ctx):
                                   {"fpre": 1, "fpre_iters": 2}, {"cluster": 1}, {"cluster": 8},
                                   {"fnewton": 0}, {"sweep_poles": 0},
                                   {"sweep_poles": 0, "pole_split": 0}, {"split_phase_a": 0},
-                                  {"sweep": 0}])
+                                  {"sweep": 0}, {"fuse_alpha": 0}])
 def test_solver_variants_meet_tolerances(api, opts):
     """The solver's optional phases (scalar f presolve, f-Newton, cluster
     sizes) change only the path to each root: every variant meets the
@@ -310,6 +310,24 @@ def test_solver_variants_meet_tolerances(api, opts):
     c.close()
 
 
+def test_fused_residues_match_k2(api):
+    """The residues the pole-limit count pass computes (one-shot exact mode)
+    are the K2 residues of the same simple poles: the f presolve then
+    converges to the same starts, evaluation counts agree closely."""
+    from paper_1706_00773_b200.instances import make_instance
+
+    for cfg, n in [(4, 2048), (2, 1024), (1, 1024)]:
+        q, lam, kmat, s = make_instance(cfg, n=n, seed=5)
+        c0, c1 = api.Context(0), api.Context(0)
+        c0.set_option("fuse_alpha", 0)
+        r0 = api.update_decomposition(q, lam, kmat, s, 1e-12, ctx=c0)
+        r1 = api.update_decomposition(q, lam, kmat, s, 1e-12, ctx=c1)
+        nrm = np.abs(r0.lam).max()
+        assert np.abs(r0.lam - r1.lam).max() <= 1e-13 * nrm
+        e0, e1 = c0.stats()["evals"], c1.stats()["evals"]
+        assert abs(e0 - e1) <= 0.02 * e0 + 4
+
+
 def test_unknown_option_is_rejected(api):
     c = api.Context(0)
     with pytest.raises(ValueError):
@@ -320,7 +338,10 @@ def test_unknown_option_is_rejected(api):
 # ----------------------------------------------- staged (multi-GPU) path
 def test_staged_path_equals_one_shot(api, ctx):
     """The root/column-partitioned data path, run as two virtual ranks on one
-    GPU one after the other (no cross-rank waits): same bits as one shot."""
+    GPU one after the other (no cross-rank waits): same bits as one shot with
+    the K2 residues (option fuse_alpha 0; the staged path runs K2 split over
+    the ranks), and the default one shot (residues from the count pass)
+    within 1e-13 ||A'||."""
     import ctypes as C
 
     import torch
@@ -334,7 +355,14 @@ def test_staged_path_equals_one_shot(api, ctx):
     n, k = kmat.shape
     lo1 = torch.empty(n, dtype=torch.float64, device=dev)
     qo1 = torch.empty((n, n), dtype=torch.float64, device=dev)
-    api.update_decomposition_device(tq, tl, tk, s, lo1, qo1, ctx=ctx)
+    lo0 = torch.empty(n, dtype=torch.float64, device=dev)
+    qo0 = torch.empty((n, n), dtype=torch.float64, device=dev)
+    api.update_decomposition_device(tq, tl, tk, s, lo0, qo0, ctx=ctx)
+    ctx.set_option("fuse_alpha", 0)
+    try:
+        api.update_decomposition_device(tq, tl, tk, s, lo1, qo1, ctx=ctx)
+    finally:
+        ctx.set_option("fuse_alpha", 1)
     ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
     be = CudaBackend(ctx, n, k, s)
     world = 2
@@ -371,6 +399,8 @@ def test_staged_path_equals_one_shot(api, ctx):
     torch.cuda.synchronize()
     assert torch.equal(lo1, lo2)
     assert torch.equal(qo1, qo2)
+    nrm = float(lo0.abs().max())
+    assert float((lo0 - lo1).abs().max()) <= 1e-13 * nrm
 
 
 def test_staged_path_on_fresh_context(api):
@@ -400,7 +430,10 @@ def test_staged_path_on_fresh_context(api):
     qo = torch.empty((n, n), dtype=torch.float64, device=dev)
     be.finish(tq, rec, 0, n, lo, qo)
     torch.cuda.synchronize()
-    ref = api.update_decomposition(q, lam, kmat, s, 1e-12)
+    c0 = api.Context(0)
+    c0.set_option("fuse_alpha", 0)  # the staged path's K2 residues
+    ref = api.update_decomposition(q, lam, kmat, s, 1e-12, ctx=c0)
+    c0.close()
     assert np.array_equal(lo.cpu().numpy(), ref.lam)
     assert np.array_equal(qo.cpu().numpy(), ref.q)
     ctx.close()

@@ -28,3 +28,5 @@ for r in range(a.reps):
 torch.cuda.synchronize()
 st = ctx.stage_times()
 print({k: (v / max(1, st["calls"]) if k != "calls" else v) for k, v in st.items()}, ctx.stats())
+print("solver_profile", ctx.solver_profile())
+print("presolve_profile", ctx.presolve_profile())
