@@ -470,6 +470,8 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
       ctx->sopt.fnewton = value != 0.0;
     } else if (std::string(key) == "fpre") {
       ctx->sopt.fpre = value != 0.0;
+    } else if (std::string(key) == "compact") {
+      ctx->sopt.compact = value != 0.0 ? 1 : 0;
     } else if (std::string(key) == "fuse_alpha") {
       ctx->sopt.fuse_alpha = value != 0.0;
     } else if (std::string(key) == "sweep_poles") {

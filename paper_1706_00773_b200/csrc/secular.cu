@@ -114,6 +114,7 @@ struct SolveArgs {
   unsigned long long* prof;  // [0] passes, [1] active slot-passes, [2] slot batches
   double fexit_rel, floor_rel, floor_ulps, stall_ratio;
   int geo_bisect;
+  int compact;               // pack the slots of drained batches (tail passes on fewer m-tiles)
   int64_t trace_j;           // diagnostics (-1: off)
   double* trace;             // [kTraceRows][kTraceCols]
   const int64_t* f_o;        // f presolve per root [j0, j1) (nullptr: none): origin,
@@ -1203,6 +1204,46 @@ __device__ void slot_post(SolveSmem& s, ParSmem<KP>& P, double* y, int b, const 
 }
 
 
+// Tail compaction (warp 0): once the root queue is drained, the active slots
+// move to the lowest positions so the pass runs only the m-tiles that hold
+// them (secular_pass mt < 4). A slot's arithmetic does not depend on its
+// position, so this changes only the cost of the tail passes. Returns the
+// number of active slots.
+template <int KP>
+__device__ int compact_slots(SolveSmem& s, double* y) {
+  const int b = threadIdx.x & 31;
+  const bool on = s.active[b] == 1;
+  const unsigned mask = __ballot_sync(0xffffffffu, on);
+  const int dst = __popc(mask & ((1u << b) - 1u));
+  const int na = __popc(mask);
+  if (mask == ((na == 32) ? 0xffffffffu : ((1u << na) - 1u))) return na;  // already packed
+  double dv[5];
+  int64_t iv[5];
+  int nv[10];
+  double yv[KP];
+  if (on) {
+    dv[0] = s.dob[b], dv[1] = s.delta[b], dv[2] = s.lo[b], dv[3] = s.hi[b], dv[4] = s.step_prev[b];
+    iv[0] = s.j[b], iv[1] = s.o[b], iv[2] = s.below[b], iv[3] = s.pl[b], iv[4] = s.ph[b];
+    nv[0] = s.hit[b], nv[1] = s.phase[b], nv[2] = s.lo_ok[b], nv[3] = s.hi_ok[b];
+    nv[4] = s.iters[b], nv[5] = s.itersA[b], nv[6] = s.fmode[b], nv[7] = s.warm[b];
+    nv[8] = s.psi_new[b];
+    for (int c = 0; c < KP; ++c) yv[c] = y[b * KP + c];
+  }
+  __syncwarp();
+  s.active[b] = (b < na) ? 1 : 0;
+  if (on) {
+    const int d = dst;
+    s.dob[d] = dv[0], s.delta[d] = dv[1], s.lo[d] = dv[2], s.hi[d] = dv[3], s.step_prev[d] = dv[4];
+    s.j[d] = iv[0], s.o[d] = iv[1], s.below[d] = iv[2], s.pl[d] = iv[3], s.ph[d] = iv[4];
+    s.hit[d] = nv[0], s.phase[d] = nv[1], s.lo_ok[d] = nv[2], s.hi_ok[d] = nv[3];
+    s.iters[d] = nv[4], s.itersA[d] = nv[5], s.fmode[d] = nv[6], s.warm[d] = nv[7];
+    s.psi_new[d] = nv[8];
+    for (int c = 0; c < KP; ++c) y[d * KP + c] = yv[c];
+  }
+  __syncwarp();
+  return na;
+}
+
 template <int KP>
 constexpr bool kFactorInSmem = (KP <= 16);
 
@@ -1227,7 +1268,8 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) solve_roots_ke
                 "factor storage must fit in the pass tiles");
   SolveSmem& s = *reinterpret_cast<SolveSmem*>(y + 32 * KP);
   ParSmem<KP>& P = *reinterpret_cast<ParSmem<KP>*>(reinterpret_cast<char*>(&s) + kSolveSmemPad);
-  __shared__ int any;
+  __shared__ int any, mt_sh;
+  __shared__ int drained;
   const int t = threadIdx.x;
   int rank = 0;
   if constexpr (CL > 1) rank = (int)cg::this_cluster().block_rank();
@@ -1251,6 +1293,7 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) solve_roots_ke
   }
   const int lane = t & 31;
   if (t < 32) s.active[t] = 2;
+  if (t == 0) drained = 0;
   __syncthreads();
   PassOpts o;
   o.alpha = a.alpha ? a.alpha + plo : nullptr;
@@ -1265,7 +1308,7 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) solve_roots_ke
       if (t < 32 && s.active[t] == 2) {
         const unsigned long long nj = atomicAdd(a.next_root, 1ull);
         if ((int64_t)nj < a.j_end) slot_init<KP>(s, y, t, a.order ? a.order[nj - a.j0] : (int64_t)nj, a);
-        else s.active[t] = 0;
+        else s.active[t] = 0, drained = 1;
       }
     } else {
       cg::cluster_group cl = cg::this_cluster();
@@ -1277,8 +1320,19 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) solve_roots_ke
       if (t < 32 && s.active[t] == 2) {
         const unsigned long long nj = s.jnext[t];
         if ((int64_t)nj < a.j_end) slot_init<KP>(s, y, t, a.order ? a.order[nj - a.j0] : (int64_t)nj, a);
-        else s.active[t] = 0;
+        else s.active[t] = 0, drained = 1;
       }
+    }
+    // the queue is drained: pack the remaining slots (every CTA of a cluster
+    // holds the same state and packs it the same way)
+    if (t < 32) {
+      __syncwarp();
+      int mt = 4;
+      if (C::MMA && a.compact && drained) {
+        const int na = compact_slots<KP>(s, y);
+        mt = (na <= 8) ? 1 : (na <= 16 ? 2 : 4);
+      }
+      if (t == 0) mt_sh = mt;
     }
     if (t == 0) {
       int v = 0, c = 0;
@@ -1295,7 +1349,7 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) solve_roots_ke
     const long long t1 = clock64();
     // ---- pole pass over this CTA's slice
     PassSlots sl{s.dob, s.delta, y, s.active, s.hit};
-    secular_pass<KP>(a.rp.d + plo, a.rp.u + plo * KP, pcnt, sl, o, smem);
+    secular_pass<KP>(a.rp.d + plo, a.rp.u + plo * KP, pcnt, sl, o, smem, mt_sh);
     const double* red = pass_result<KP>(smem);
     const long long t2 = clock64();
     if constexpr (CL > 1) {
@@ -1675,6 +1729,7 @@ void launch_solve(const ReducedView& rp, const double* alpha, double* br_lo, dou
   a.floor_ulps = opt.floor_ulps;
   a.stall_ratio = opt.stall_ratio;
   a.geo_bisect = opt.geo_bisect;
+  a.compact = opt.compact;
   a.trace = ws.get_f64("solve_trace", (size_t)kTraceRows * kTraceCols);
   if (first_stage) {  // a split solve's second stage keeps the first stage's trace and profile
     if (opt.trace_root >= 0)

@@ -92,6 +92,7 @@ struct SolveOptions {
   double floor_ulps = 4.0;   // ... or below this many ulps of the root value
   double stall_ratio = 0.5;  // "no longer shrinking": |step| >= stall_ratio * |previous step|
   int geo_bisect = 1;       // geometric bisection of brackets spanning decades of delta
+  int compact = 1;          // pack the slots of drained solver batches (tail passes)
   // scalar presolve: the f-root (K2 residues) of every isolated root before
   // the S solver, which then starts psi-Newton there. Used from kp = 16 up,
   // where an S evaluation costs ~10x an f evaluation (cfg4 n = 32768: solve

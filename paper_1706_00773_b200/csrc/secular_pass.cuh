@@ -385,15 +385,29 @@ __device__ __forceinline__ void mma_bvals(const double* __restrict__ ur, int g8,
   }
 }
 
-template <int KP, int G>
+// MT = active m-tiles (4, 2 or 1: the solver's compacted tail batches hold
+// slots 0 .. 8 MT - 1 only). The warps' shares change with MT, the
+// arithmetic of a slot does not: every (slot, entry) sum runs the same DMMA
+// chain over the same pole split (p), and the D-phase partials of a slot
+// stay with the same (m-tile, pole n-tile set) -- results are independent of
+// MT, so compaction keeps the solver deterministic.
+//   MT = 4: warp (sel = m-half, g, p): m-tiles 2 sel, 2 sel + 1, all n-tiles
+//   MT = 2: warp (sel = m-tile, g, p): one m-tile, all n-tiles
+//   MT = 1: warp (sel = n-half, g, p): m-tile 0, half the n-tiles
+template <int KP, int G, int MT>
 __device__ __forceinline__ void pass_body_mma(const double* __restrict__ d,
                                               const double* __restrict__ u, int64_t n,
                                               const PassSlots& slots, const PassOpts& o,
-                                              double* tiles, double* dbuf, double* red, int mh,
+                                              double* tiles, double* dbuf, double* red, int sel,
                                               int p) {
   using C = PassCfg<KP>;
   using MM = MmaMap<KP>;
   constexpr int NTL = MM::nt_cnt(G);
+  constexpr int MW = (MT == 4) ? 2 : 1;  // m-tiles per warp
+  const int m0 = (MT == 4) ? 2 * sel : (MT == 2 ? sel : 0);
+  // n-tiles [j_lo, j_hi) of the group (MT = 1 splits them)
+  const int j_lo = (MT == 1) ? sel * ((NTL + 1) / 2) : 0;
+  const int j_hi = (MT == 1) ? (sel ? NTL : (NTL + 1) / 2) : NTL;
   constexpr int KSW = (C::T / 4) / C::MPS;  // k-steps per warp per tile
   constexpr int LDU = C::LDU;
   constexpr int KC = KP / 4;                // k-steps of P = Y U^T
@@ -437,6 +451,7 @@ __device__ __forceinline__ void pass_body_mma(const double* __restrict__ d,
     // ---- D phase (C-fragment layout: slot row g8, poles 8 nd + 2 t4 + h)
 #pragma unroll
     for (int jn = 0; jn < C::T / 16; ++jn) {
+      if (md >= MT) break;  // slots of this m-tile are empty (compacted batch)
       const int nd = (warp >> 2) + 2 * jn;
       double pv0 = 0.0, pv1 = 0.0;
       if (sig) {
@@ -475,14 +490,15 @@ __device__ __forceinline__ void pass_body_mma(const double* __restrict__ d,
 #pragma unroll 2
     for (int kk = 0; kk < KSW; ++kk) {
       const int ks = p * KSW + kk;
-      const double a0 = dbuf[ks * DKS + (2 * mh) * 32 + lane];
-      const double a1 = dbuf[ks * DKS + (2 * mh + 1) * 32 + lane];
+      const double a0 = dbuf[ks * DKS + m0 * 32 + lane];
+      const double a1 = (MW > 1) ? dbuf[ks * DKS + (m0 + 1) * 32 + lane] : 0.0;
       double b[NTL];
       mma_bvals<KP, G>(tu + (4 * ks + t4) * LDU, g8, b);
 #pragma unroll
       for (int j = 0; j < NTL; ++j) {
+        if (MT == 1 && (j < j_lo || j >= j_hi)) continue;
         dmma(acc[0][j][0], acc[0][j][1], a0, b[j]);
-        dmma(acc[1][j][0], acc[1][j][1], a1, b[j]);
+        if constexpr (MW > 1) dmma(acc[1][j][0], acc[1][j][1], a1, b[j]);
       }
     }
   }
@@ -496,16 +512,17 @@ __device__ __forceinline__ void pass_body_mma(const double* __restrict__ d,
   for (int q = 0; q < C::MPS; ++q) {
     if (p == q) {
 #pragma unroll
-      for (int m = 0; m < 2; ++m)
+      for (int m = 0; m < MW; ++m)
 #pragma unroll
         for (int j = 0; j < NTL; ++j)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
+            if (MT == 1 && (j < j_lo || j >= j_hi)) continue;
             int r, c;
             MM::entry(MM::nt_lo(G) + j, 2 * t4 + h, r, c);
             if (r >= 0) {
               const int e = (r <= c) ? C::pidx(r, c) : C::pidx(c, r);
-              double* rr = red + (8 * (2 * mh + m) + g8) * OUT + e;
+              double* rr = red + (8 * (m0 + m) + g8) * OUT + e;
               *rr = (q == 0) ? acc[m][j][h] : *rr + acc[m][j][h];
             }
           }
@@ -539,22 +556,37 @@ __device__ __forceinline__ void pass_body_mma(const double* __restrict__ d,
 // Runs the pass. On return (after __syncthreads) red[b * OUT + e] holds the
 // packed S_b (without J) and red[b*OUT + P..P+2] = g_b, f_b - 1, f'_b.
 // smem: SMEM_DOUBLES doubles (tiles, D buffer, reduction).
+template <int KP, int MT>
+__device__ __forceinline__ void pass_mma_dispatch(const double* __restrict__ d,
+                                                  const double* __restrict__ u, int64_t n,
+                                                  const PassSlots& slots, const PassOpts& o,
+                                                  double* tiles, double* dbuf, double* red) {
+  using C = PassCfg<KP>;
+  const int warp = threadIdx.x >> 5;
+  const int sel = warp & 1;
+  const int g = (warp >> 1) % C::NG;
+  const int p = warp / (2 * C::NG);
+  if (g == 0) pass_body_mma<KP, 0, MT>(d, u, n, slots, o, tiles, dbuf, red, sel, p);
+  if constexpr (C::NG > 1) {
+    if (g == 1) pass_body_mma<KP, 1, MT>(d, u, n, slots, o, tiles, dbuf, red, sel, p);
+  }
+}
+
+// mt: active m-tiles (4: all 32 slots; 2 or 1: only slots < 8 mt are active,
+// the solver's compacted tail batches; MMA ranks only, others ignore it)
 template <int KP>
 __device__ void secular_pass(const double* __restrict__ d, const double* __restrict__ u, int64_t n,
-                             const PassSlots& slots, const PassOpts& o, double* smem_pass) {
+                             const PassSlots& slots, const PassOpts& o, double* smem_pass,
+                             int mt = 4) {
   using C = PassCfg<KP>;
   double* tiles = smem_pass;
   double* dbuf = tiles + 2 * C::TILE_DOUBLES;
   double* red = dbuf + C::DBUF_DOUBLES;
   const int warp = threadIdx.x >> 5;
   if constexpr (C::MMA) {
-    const int mh = warp & 1;
-    const int g = (warp >> 1) % C::NG;
-    const int p = warp / (2 * C::NG);
-    if (g == 0) pass_body_mma<KP, 0>(d, u, n, slots, o, tiles, dbuf, red, mh, p);
-    if constexpr (C::NG > 1) {
-      if (g == 1) pass_body_mma<KP, 1>(d, u, n, slots, o, tiles, dbuf, red, mh, p);
-    }
+    if (mt >= 4) pass_mma_dispatch<KP, 4>(d, u, n, slots, o, tiles, dbuf, red);
+    else if (mt == 2) pass_mma_dispatch<KP, 2>(d, u, n, slots, o, tiles, dbuf, red);
+    else pass_mma_dispatch<KP, 1>(d, u, n, slots, o, tiles, dbuf, red);
     __syncthreads();
     return;
   }
