@@ -34,6 +34,7 @@
 #include "secular.cuh"
 
 #include <cfloat>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -412,18 +413,37 @@ __global__ void __launch_bounds__(kFPreWarps * 32) fpresolve_kernel(FPreArgs a) 
         }
       }
       if (act) {
+        const int64_t t0 = tt * kFPreTile;
+        if (t0 + kFPreTile <= below || t0 >= below) {
+          // the whole tile on one side of the slot's bracket: one accumulator
+          // pair, added to psi or phi after the tile (same terms, same order)
+          double fa = 0.0, fpa = 0.0;
 #pragma unroll 4
-        for (int i = warp; i < kFPreTile; i += kFPreWarps) {
-          const double2 p = tile[i];
-          const double diff = (p.x - dob) - del;
-          hit |= (diff == 0.0);
-          const double D = (diff == 0.0 || diff != diff) ? 0.0 : rcp64(diff);
-          const double aD = p.y * D;
-          const double aL = (tt * kFPreTile + i < below) ? aD : 0.0, aR = aD - aL;
-          ps += aL;
-          psp = fma(aL, D, psp);
-          ph += aR;
-          php = fma(aR, D, php);
+          for (int i = warp; i < kFPreTile; i += kFPreWarps) {
+            const double2 p = tile[i];
+            const double diff = (p.x - dob) - del;
+            hit |= (diff == 0.0);
+            const double D = (diff == 0.0 || diff != diff) ? 0.0 : rcp64(diff);
+            const double aD = p.y * D;
+            fa += aD;
+            fpa = fma(aD, D, fpa);
+          }
+          if (t0 >= below) ph += fa, php += fpa;
+          else ps += fa, psp += fpa;
+        } else {
+#pragma unroll 4
+          for (int i = warp; i < kFPreTile; i += kFPreWarps) {
+            const double2 p = tile[i];
+            const double diff = (p.x - dob) - del;
+            hit |= (diff == 0.0);
+            const double D = (diff == 0.0 || diff != diff) ? 0.0 : rcp64(diff);
+            const double aD = p.y * D;
+            const double aL = (t0 + i < below) ? aD : 0.0, aR = aD - aL;
+            ps += aL;
+            psp = fma(aL, D, psp);
+            ph += aR;
+            php = fma(aR, D, php);
+          }
         }
       }
       __syncthreads();
@@ -1861,14 +1881,22 @@ __device__ double pole_residue(const double* S, const double* rb, const int* sgn
   return al;
 }
 
-template <int KP>
+// CL > 1: a thread-block cluster of CL CTAs per batch of 32 pole values,
+// CTA r passing over pole slice r (so the 1024 batches of n = 32768 fill the
+// GPU's CTA slots in 7-14 waves instead of 3.5 -- less idle last wave); rank
+// 0 sums the partials in rank order over distributed shared memory and does
+// the per-pole work.
+template <int KP, int CL>
 __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) pole_inertia_kernel(InertiaArgs<KP> a) {
   using C = PassCfg<KP>;
+  namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double smem[];
   __shared__ double dob[32], delta[32];
   __shared__ int active[32], hit[32];
   const int t = threadIdx.x;
-  const int64_t g0 = (int64_t)blockIdx.x * 32;
+  int rank = 0;
+  if constexpr (CL > 1) rank = (int)cg::this_cluster().block_rank();
+  const int64_t g0 = (int64_t)(blockIdx.x / CL) * 32;
   if (t < 32) {
     const int64_t g = g0 + t;
     active[t] = g < a.nb;
@@ -1880,11 +1908,29 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) pole_inertia_k
   PassSlots sl{dob, delta, nullptr, active, hit};
   PassOpts o;
   o.exclude_zero = true;
-  secular_pass<KP>(a.rp.d, a.rp.u, a.rp.n, sl, o, smem);
+  const int64_t N = a.rp.n, chunk = (N + CL - 1) / CL;
+  const int64_t plo = (rank * chunk < N) ? rank * chunk : N;
+  const int64_t pcnt = ((plo + chunk < N) ? plo + chunk : N) - plo;
+  secular_pass<KP>(a.rp.d + plo, a.rp.u + plo * KP, pcnt, sl, o, smem);
+  if constexpr (CL > 1) {
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();  // every slice's partial sums in place
+    if (rank == 0) {
+      double* red = const_cast<double*>(pass_result<KP>(smem));
+      for (int idx = t; idx < C::RED_DOUBLES; idx += kPassThreads) {
+        double v = red[idx];
+        for (int r = 1; r < CL; ++r) v += cl.map_shared_rank(red, r)[idx];
+        red[idx] = v;
+      }
+    }
+    cl.sync();  // remote partials read: the other ranks may exit
+    if (rank != 0) return;
+    __syncthreads();
+  }
   if (t >= 32 || !active[t]) return;
   const int64_t g = g0 + t;
   const int k = a.rp.k;
-  double* T = a.scratch + ((size_t)blockIdx.x * 32 + t) * kInertiaScratch<KP>;
+  double* T = a.scratch + ((size_t)(blockIdx.x / CL) * 32 + t) * kInertiaScratch<KP>;
   double* W = T + KP * KP;   // reflectors, one per row of R
   double* x = W + KP * KP;
   const double* rb = pass_result<KP>(smem) + t * C::OUT;
@@ -1951,9 +1997,37 @@ void launch_inertia(const ReducedView& rp, const double* bval, const int64_t* br
   InertiaArgs<KP> a{rp, bval, brow, bcnt, nb, nu, nullptr, alpha_out};
   a.scratch = ws.get_f64("inertia_scratch", (size_t)grid * 32 * kInertiaScratch<KP>);
   const size_t sm = sizeof(double) * C::SMEM_DOUBLES;
-  EIGB_CUDA(cudaFuncSetAttribute(pole_inertia_kernel<KP>,
+  // pole slices of >= 4096 per CTA; pairs for the MMA ranks (two CTAs per SM)
+  static int count_cl = -1;  // EIGMOD_B200_COUNT_CL=2: pole slices on CTA pairs (experiment)
+  if (count_cl < 0) {
+    const char* e = std::getenv("EIGMOD_B200_COUNT_CL");
+    count_cl = e ? std::atoi(e) : 1;
+  }
+  if constexpr (PassCfg<KP>::MMA) {
+    if (count_cl == 2 && rp.n >= 8192) {
+      constexpr int CL = 2;
+      auto kern = pole_inertia_kernel<KP, CL>;
+      EIGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = CL;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3((unsigned)(grid * CL));
+      cfg.blockDim = dim3(kPassThreads);
+      cfg.dynamicSmemBytes = sm;
+      cfg.stream = st;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      EIGB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+      EIGB_LAUNCH_CHECK();
+      return;
+    }
+  }
+  EIGB_CUDA(cudaFuncSetAttribute(pole_inertia_kernel<KP, 1>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  pole_inertia_kernel<KP><<<grid, kPassThreads, sm, st>>>(a);
+  pole_inertia_kernel<KP, 1><<<grid, kPassThreads, sm, st>>>(a);
   EIGB_LAUNCH_CHECK();
 }
 
