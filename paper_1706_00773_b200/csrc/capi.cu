@@ -50,26 +50,31 @@ void project(eigmod_b200_ctx* c, const double* q, const double* kmat, int64_t n,
 // exact mode the plan needs no residues (classification is by coupling
 // mass), so K2 is skipped and the solve's pole-limit count pass, which
 // evaluates the same pole sum at every pole value, computes alpha_red.
-void plan_groups(eigmod_b200_ctx* c, const double* lam, const double* u, const int* signs,
-                 int64_t n, int64_t k, double run_rel);
-
 void plan_from_u(eigmod_b200_ctx* c, const double* lam, const double* u, const int* signs,
                  int64_t n, int64_t k, double run_rel, bool fuse) {
-  plan_groups(c, lam, u, signs, n, k, run_rel);
-  eigb::Plan& p = c->plan;
-  if (p.k == 0) return;
   const eigb::SolveOptions& o = c->sopt;
-  p.alpha_fused = fuse && p.exact && o.fuse_alpha && o.sweep && o.sweep_poles && o.fnewton;
-  if (p.alpha_fused)
-    EIGB_CUDA(cudaMemsetAsync(p.alpha, 0, 8 * std::max<int64_t>(p.ng, 1), c->stream));
-  else
-    eigb::build_plan_weights(p, 0, p.ng, p.alpha, c->ws, c->stream);
-  eigb::build_plan_finish(p, lam, c->ws, c->stream);
-  c->have_plan = true;
+  const bool fused = fuse && run_rel != eigb::kPoleMergeRelGap && o.fuse_alpha && o.sweep &&
+                     o.sweep_poles && o.fnewton;
+  // fused plans are speculative (one host round trip); a failed assumption
+  // (a dropped column or a multi-member run) rebuilds it the staged way
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    plan_groups(c, lam, u, signs, n, k, run_rel, fused && attempt == 0 && o.spec_plan);
+    eigb::Plan& p = c->plan;
+    if (p.k == 0) return;
+    p.alpha_fused = fused;
+    if (p.alpha_fused)
+      EIGB_CUDA(cudaMemsetAsync(p.alpha, 0, 8 * std::max<int64_t>(p.ng, 1), c->stream));
+    else
+      eigb::build_plan_weights(p, 0, p.ng, p.alpha, c->ws, c->stream);
+    eigb::build_plan_finish(p, c->lam, c->ws, c->stream);
+    if (p.spec_failed) continue;
+    c->have_plan = true;
+    return;
+  }
 }
 
 void plan_groups(eigmod_b200_ctx* c, const double* lam, const double* u, const int* signs,
-                 int64_t n, int64_t k, double run_rel) {
+                 int64_t n, int64_t k, double run_rel, bool spec) {
   eigb::Plan& p = c->plan;
   p = eigb::Plan{};
   p.run_rel = run_rel;
@@ -84,6 +89,30 @@ void plan_groups(eigmod_b200_ctx* c, const double* lam, const double* u, const i
   const int kp = eigb::padded_rank(k);
   double* norms = c->ws.get_f64("cap_norms", k);
   eigb::column_norms2_dev(u, n, kp, (int)k, norms, c->stream);
+  if (spec) {  // every column kept (checked on the device, eigb::Plan::spec)
+    p.exact = run_rel != eigb::kPoleMergeRelGap;
+    p.spec = true;
+    p.norms_dev = norms;
+    p.n = n;
+    p.k = (int)k;
+    for (int j = 0; j < (int)k; ++j) p.keep_h.push_back(j);
+    p.kp = kp;
+    p.u = c->ws.get_f64("pl_u", (size_t)n * p.kp);
+    EIGB_CUDA(cudaMemcpyAsync(p.u, u, 8 * (size_t)n * kp, cudaMemcpyDeviceToDevice, c->stream));
+    p.sgn_h.clear();
+    p.m_neg = 0;
+    std::vector<int> sp(p.kp, 1);
+    for (int r = 0; r < p.k; ++r) {
+      sp[r] = signs[r];
+      p.sgn_h.push_back(sp[r]);
+      p.m_neg += sp[r] < 0;
+    }
+    p.sgn = c->ws.get_i32("pl_sgn", p.kp);
+    EIGB_CUDA(cudaMemcpyAsync(p.sgn, sp.data(), 4 * p.kp, cudaMemcpyHostToDevice, c->stream));
+    eigb::build_plan_groups(p, lam, n, run_rel, c->ws, c->stream);
+    c->have_plan = false;
+    return;
+  }
   std::vector<double> nh(k);
   EIGB_CUDA(cudaMemcpyAsync(nh.data(), norms, 8 * k, cudaMemcpyDeviceToHost, c->stream));
   EIGB_CUDA(cudaStreamSynchronize(c->stream));
@@ -470,6 +499,8 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
       ctx->sopt.fnewton = value != 0.0;
     } else if (std::string(key) == "fpre") {
       ctx->sopt.fpre = value != 0.0;
+    } else if (std::string(key) == "spec_plan") {
+      ctx->sopt.spec_plan = value != 0.0;
     } else if (std::string(key) == "compact") {
       ctx->sopt.compact = value != 0.0 ? 1 : 0;
     } else if (std::string(key) == "fuse_alpha") {

@@ -139,7 +139,7 @@ int guarded(eigmod_b200_ctx* ctx, F&& f) {
 void project(eigmod_b200_ctx* c, const double* q, const double* kmat, int64_t n, int64_t k,
              int64_t lo, int64_t hi, double* u_out);
 void plan_groups(eigmod_b200_ctx* c, const double* lam, const double* u, const int* signs,
-                 int64_t n, int64_t k, double run_rel);
+                 int64_t n, int64_t k, double run_rel, bool spec = false);
 void plan_from_u(eigmod_b200_ctx* c, const double* lam, const double* u, const int* signs,
                  int64_t n, int64_t k, double run_rel, bool fuse = false);
 void solve(eigmod_b200_ctx* c, int64_t j0, int64_t j1);

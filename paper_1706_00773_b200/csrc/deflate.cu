@@ -471,7 +471,8 @@ __device__ void block_exclusive_scan(const int64_t* in, int64_t* out, int64_t n,
 
 __global__ void __launch_bounds__(kPlanThreads) runs_kernel(const double* __restrict__ lam,
                                                             int64_t n, double rel, double ufro2,
-                                                            int exact,
+                                                            const double* __restrict__ norms2,
+                                                            int k, int exact,
                                                             int64_t* __restrict__ flag,
                                                             int64_t* __restrict__ gid,
                                                             int64_t* __restrict__ gstart,
@@ -485,6 +486,23 @@ __global__ void __launch_bounds__(kPlanThreads) runs_kernel(const double* __rest
   // parity: the reference's scale max(1, max|lambda|) (secular.cpp:285-287);
   // exact: max(max|lambda|, max_r ||u_r||^2), the size of A', so every
   // threshold is relative to the problem (A -> c A gives c lambda')
+  if (norms2) {
+    // speculative plan: the column-drop rule of plan_groups (capi.cu,
+    // proj/src/rootfind.cpp:318-340) on the device; any dropped column is
+    // flagged in scal[7] (the host rebuilds the plan) and ufro2 is the max
+    // over all columns
+    double mx = 0.0;
+    for (int c = 0; c < k; ++c) mx = fmax(mx, sqrt(norms2[c]));
+    const double drop = kColumnDropRel * (exact ? mx : fmax(1.0, mx));
+    int bad = 0;
+    ufro2 = 0.0;
+    for (int c = 0; c < k; ++c) {
+      const double v = sqrt(norms2[c]);
+      if (v > drop && v > 0.0) ufro2 = fmax(ufro2, v * v);
+      else bad = 1;
+    }
+    if (threadIdx.x == 0) scal[7] = bad;
+  }
   double m = exact ? 0.0 : 1.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, fabs(lam[i]));
   double scale = block_max(m, red);
@@ -503,13 +521,18 @@ __global__ void __launch_bounds__(kPlanThreads) runs_kernel(const double* __rest
     // neighbours: thread 0 walks only positions whose left gap is small.
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
       flag[i] = (i == 0 || !(lam[i] - lam[i - 1] < gap)) ? 1 : 0;
+    // Chains are independent: one thread per chain start (a start followed
+    // by a close neighbour) walks its chain; candidates are marked first (in
+    // gid, free until the scan) so no walk reads another chain's new starts.
     __syncthreads();
-    if (threadIdx.x == 0) {
-      int64_t start = 0;
-      for (int64_t i = 1; i < n; ++i) {
-        if (flag[i]) {
-          start = i;
-        } else if (!(lam[i] - lam[start] < gap)) {
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+      gid[i] = (flag[i] && i + 1 < n && !flag[i + 1]) ? 1 : 0;
+    __syncthreads();
+    for (int64_t i0 = threadIdx.x; i0 < n; i0 += blockDim.x) {
+      if (!gid[i0]) continue;
+      int64_t start = i0;
+      for (int64_t i = i0 + 1; i < n && !flag[i]; ++i) {
+        if (!(lam[i] - lam[start] < gap)) {
           flag[i] = 1;
           start = i;
         }
@@ -811,10 +834,16 @@ void build_plan_groups(Plan& p, const double* lam, int64_t n, double run_rel, De
   p.rep_row = ws.get_f64("pl_rep_row", n);
   p.counts = ws.get_i64("pl_counts", 8);
   p.scal = ws.get_f64("pl_scal", 8);
-  runs_kernel<<<1, kPlanThreads, 0, st>>>(lam, n, run_rel, p.ufro2, p.exact ? 1 : 0, flag, p.gid,
-                                           p.gstart, p.glen, p.gval,
-                                           p.rep_row, p.counts, p.scal);
+  runs_kernel<<<1, kPlanThreads, 0, st>>>(lam, n, run_rel, p.ufro2, p.spec ? p.norms_dev : nullptr,
+                                           p.k, p.exact ? 1 : 0, flag, p.gid, p.gstart, p.glen,
+                                           p.gval, p.rep_row, p.counts, p.scal);
   EIGB_LAUNCH_CHECK();
+  if (p.spec) {  // sizes read back by build_plan_finish; n bounds the group count
+    p.ng = n;
+    p.nmulti = 0;
+    p.alpha = ws.get_f64("pl_alpha", n);
+    return;
+  }
   int64_t cnt[5] = {0, 0, 0, 0, 0};
   EIGB_CUDA(cudaMemcpyAsync(cnt, p.counts, sizeof(cnt), cudaMemcpyDeviceToHost, st));
   EIGB_CUDA(cudaStreamSynchronize(st));
@@ -898,18 +927,25 @@ void build_plan_finish(Plan& p, const double* lam, DeviceScratch& ws, cudaStream
   clips_kernel<<<1, kPlanThreads, 0, st>>>(p.d, p.ur, p.counts, kp, k, p.sgn, p.scal);
   EIGB_LAUNCH_CHECK();
   // one round trip for the sizes, the scales and (with multi-member runs) the
-  // run ranks and kinds
-  int64_t cnt[3];
+  // run ranks and kinds; a speculative plan also learns its group count and
+  // whether its assumptions held
+  int64_t cnt[5];
   double sc[8];
   std::vector<int64_t> rk(nmulti > 0 ? ng : 0);
   std::vector<int> kd(nmulti > 0 ? ng : 0);
-  EIGB_CUDA(cudaMemcpyAsync(cnt, p.counts, 24, cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaMemcpyAsync(cnt, p.counts, 40, cudaMemcpyDeviceToHost, st));
   EIGB_CUDA(cudaMemcpyAsync(sc, p.scal, 64, cudaMemcpyDeviceToHost, st));
   if (nmulti > 0) {
     EIGB_CUDA(cudaMemcpyAsync(rk.data(), p.rank, 8 * ng, cudaMemcpyDeviceToHost, st));
     EIGB_CUDA(cudaMemcpyAsync(kd.data(), p.kind, 4 * ng, cudaMemcpyDeviceToHost, st));
   }
   EIGB_CUDA(cudaStreamSynchronize(st));
+  if (p.spec) {
+    p.ng = cnt[0];
+    p.nmulti = cnt[4];
+    p.spec_failed = (p.nmulti > 0) || (sc[7] != 0.0);
+    if (p.spec_failed) return;
+  }
   p.nred = cnt[1];
   p.ndec = cnt[2];
   bool ok = true;  // rows of compressed runs are not simple poles of f

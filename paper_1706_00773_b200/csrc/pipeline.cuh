@@ -35,6 +35,12 @@ struct Plan {
   double run_rel = kExactRunRelGap;
   bool exact = true;     // scale-relative thresholds (run_rel != the reference's 1e-12)
   double ufro2 = 0.0;    // max_r ||u_r||^2 over the kept columns (exact-mode scale)
+  // speculative plan (one-shot paths): every column kept and no multi-member
+  // run assumed; the device checks both and build_plan_finish reads the
+  // verdict back with the plan's sizes (one host round trip for the plan).
+  // spec_failed: an assumption failed, the caller rebuilds the plan.
+  bool spec = false, spec_failed = false;
+  const double* norms_dev = nullptr;  // squared column norms of U (spec)
 
   ReducedView view() const {
     return ReducedView{d, ur, sgn, nred, k, kp, m_neg, lo_clip, hi_clip};

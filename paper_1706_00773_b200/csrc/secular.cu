@@ -459,6 +459,10 @@ __global__ void __launch_bounds__(kFPreWarps * 32) fpresolve_kernel(FPreArgs a) 
   }
 }
 
+// A root-queue counter set on the stream (a pageable host-to-device copy of
+// the start would synchronise the host with the stream).
+__global__ void set_u64_kernel(unsigned long long* p, unsigned long long v) { *p = v; }
+
 // Root queue order: the roots expected to need the most evaluations first
 // (brackets without isolation, then presolve not converged, then the rest),
 // so the last batches of a solve drain short roots (longest-first).
@@ -1756,8 +1760,8 @@ void launch_solve(const ReducedView& rp, const double* alpha, double* br_lo, dou
       EIGB_CUDA(cudaMemsetAsync(a.trace, 0, sizeof(double) * kTraceRows * kTraceCols, st));
     EIGB_CUDA(cudaMemsetAsync(a.prof, 0, 12 * sizeof(unsigned long long), st));
   }
-  const unsigned long long start = (unsigned long long)j0;
-  EIGB_CUDA(cudaMemcpyAsync(a.next_root, &start, sizeof(start), cudaMemcpyHostToDevice, st));
+  set_u64_kernel<<<1, 1, 0, st>>>(a.next_root, (unsigned long long)j0);
+  EIGB_LAUNCH_CHECK();
   // Size-based choice (tools/exp_cluster.py, cfg 2/4 at n = 8192/32768):
   // with many roots per SM the GPC-aligned pairs keep all 148 SMs busy (4-
   // and 8-CTA clusters leave GPC remainders idle); with few, the shorter
@@ -1816,6 +1820,7 @@ struct InertiaArgs {
   int* nu;              // out: inertia of the projected T
   double* scratch;      // gridDim.x * 32 * kInertiaScratch<KP>
   double* alpha_out;    // != nullptr: residue of every simple pole (at its row)
+  const unsigned long long* nb_dev;  // != nullptr: the count on the device (nb: upper bound)
 };
 
 template <int KP>
@@ -1897,6 +1902,10 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) pole_inertia_k
   int rank = 0;
   if constexpr (CL > 1) rank = (int)cg::this_cluster().block_rank();
   const int64_t g0 = (int64_t)(blockIdx.x / CL) * 32;
+  if (a.nb_dev) {  // launched for an upper bound of the pole values
+    a.nb = (int64_t)*a.nb_dev;
+    if (g0 >= a.nb) return;  // (whole clusters exit together: g0 is per cluster)
+  }
   if (t < 32) {
     const int64_t g = g0 + t;
     active[t] = g < a.nb;
@@ -1990,11 +1999,11 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) pole_inertia_k
 
 template <int KP>
 void launch_inertia(const ReducedView& rp, const double* bval, const int64_t* brow,
-                    const int* bcnt, int64_t nb, int* nu, double* alpha_out, DeviceScratch& ws,
-                    cudaStream_t st) {
+                    const int* bcnt, int64_t nb, int* nu, double* alpha_out,
+                    const unsigned long long* nb_dev, DeviceScratch& ws, cudaStream_t st) {
   using C = PassCfg<KP>;
   const int grid = (int)cdiv(nb, 32);
-  InertiaArgs<KP> a{rp, bval, brow, bcnt, nb, nu, nullptr, alpha_out};
+  InertiaArgs<KP> a{rp, bval, brow, bcnt, nb, nu, nullptr, alpha_out, nb_dev};
   a.scratch = ws.get_f64("inertia_scratch", (size_t)grid * 32 * kInertiaScratch<KP>);
   const size_t sm = sizeof(double) * C::SMEM_DOUBLES;
   // pole slices of >= 4096 per CTA; pairs for the MMA ranks (two CTAs per SM)
@@ -2089,8 +2098,10 @@ __global__ void fill_i32_kernel(int* __restrict__ p, int64_t n, int v) {
 
 __global__ void pole_scatter_kernel(const int64_t* __restrict__ list, const int64_t* __restrict__ brow,
                                     const int* __restrict__ bcnt, const int* __restrict__ nu,
-                                    int64_t nsel, int m_neg, int* __restrict__ pcounts) {
+                                    int64_t nsel, int m_neg, int* __restrict__ pcounts,
+                                    const unsigned long long* nsel_dev = nullptr) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (nsel_dev) nsel = (int64_t)*nsel_dev;
   if (i >= nsel) return;
   const int c = (int)(brow[i] + m_neg - nu[i]);
   for (int64_t a = list[i]; a < brow[i] + bcnt[i]; ++a) pcounts[a] = c;
@@ -2134,8 +2145,8 @@ void solve_after_counts(const ReducedView& rp, const double* alpha, int64_t j0, 
                 opt.fpre_iters,
                 reinterpret_cast<unsigned long long*>(ws.get_i64("fpre_prof", 4))};
     EIGB_CUDA(cudaMemsetAsync(fa.prof, 0, 4 * sizeof(unsigned long long), st));
-    const unsigned long long start = (unsigned long long)j0;
-    EIGB_CUDA(cudaMemcpyAsync(fa.next_root, &start, sizeof(start), cudaMemcpyHostToDevice, st));
+    set_u64_kernel<<<1, 1, 0, st>>>(fa.next_root, (unsigned long long)j0);
+    EIGB_LAUNCH_CHECK();
     const size_t fsm = (sizeof(FPreSmem) + 15) / 16 * 16 + sizeof(double2) * kFPreTile;
     EIGB_CUDA(cudaFuncSetAttribute(fpresolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)fsm));
@@ -2226,19 +2237,15 @@ void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t
     pole_all_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(rp.d, rp.n, pb, pe, pcounts, list, bval,
                                                               brow, bcnt, nsel);
     EIGB_LAUNCH_CHECK();
-    unsigned long long nh = 0;
-    EIGB_CUDA(cudaMemcpyAsync(&nh, nsel, 8, cudaMemcpyDeviceToHost, st));
-    EIGB_CUDA(cudaStreamSynchronize(st));
     // the residues need every pole value of the problem in the window
     if (alpha_fill && !(pb == 0 && pe == rp.n))
       throw Error(1, "", "solve_roots: fused residues need all poles");
-    if (nh > 0) {
-      pole_inertia(rp, bval, brow, bcnt, (int64_t)nh, nu, ws, st, alpha_fill);
-      pole_scatter_kernel<<<(unsigned)cdiv((int64_t)nh, 256), 256, 0, st>>>(list, brow, bcnt, nu,
-                                                                           (int64_t)nh, rp.m_neg,
-                                                                           pcounts);
-      EIGB_LAUNCH_CHECK();
-    }
+    // launched for all np pole positions; the kernels read the number of
+    // distinct pole values from the device (no host round trip)
+    pole_inertia(rp, bval, brow, bcnt, np, nu, ws, st, alpha_fill, nsel);
+    pole_scatter_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(list, brow, bcnt, nu, np, rp.m_neg,
+                                                                 pcounts, nsel);
+    EIGB_LAUNCH_CHECK();
     if (alpha_fill) alpha = alpha_fill;
     solve_after_counts(rp, alpha, j0, j1, out, opt, ws, sms, st, nullptr, pcounts, pb, pe);
     return;
@@ -2300,15 +2307,16 @@ void group_weights(int kp, const double* rep, const double* u, int64_t n, const 
 }
 
 void pole_inertia(const ReducedView& rp, const double* bval, const int64_t* brow, const int* bcnt,
-                  int64_t nb, int* nu, DeviceScratch& ws, cudaStream_t st, double* alpha_out) {
+                  int64_t nb, int* nu, DeviceScratch& ws, cudaStream_t st, double* alpha_out,
+                  const unsigned long long* nb_dev) {
   if (nb <= 0) return;
   switch (rp.kp) {
-    case 1: launch_inertia<1>(rp, bval, brow, bcnt, nb, nu, alpha_out, ws, st); break;
-    case 2: launch_inertia<2>(rp, bval, brow, bcnt, nb, nu, alpha_out, ws, st); break;
-    case 4: launch_inertia<4>(rp, bval, brow, bcnt, nb, nu, alpha_out, ws, st); break;
-    case 8: launch_inertia<8>(rp, bval, brow, bcnt, nb, nu, alpha_out, ws, st); break;
-    case 16: launch_inertia<16>(rp, bval, brow, bcnt, nb, nu, alpha_out, ws, st); break;
-    case 32: launch_inertia<32>(rp, bval, brow, bcnt, nb, nu, alpha_out, ws, st); break;
+    case 1: launch_inertia<1>(rp, bval, brow, bcnt, nb, nu, alpha_out, nb_dev, ws, st); break;
+    case 2: launch_inertia<2>(rp, bval, brow, bcnt, nb, nu, alpha_out, nb_dev, ws, st); break;
+    case 4: launch_inertia<4>(rp, bval, brow, bcnt, nb, nu, alpha_out, nb_dev, ws, st); break;
+    case 8: launch_inertia<8>(rp, bval, brow, bcnt, nb, nu, alpha_out, nb_dev, ws, st); break;
+    case 16: launch_inertia<16>(rp, bval, brow, bcnt, nb, nu, alpha_out, nb_dev, ws, st); break;
+    case 32: launch_inertia<32>(rp, bval, brow, bcnt, nb, nu, alpha_out, nb_dev, ws, st); break;
     default: throw Error(1, "", "pole_inertia: unsupported padded rank");
   }
 }

@@ -106,6 +106,8 @@ struct SolveOptions {
   // exact mode, one device: the residues alpha come from the pole-limit count
   // pass (the same pole sum at every pole value) instead of a K2 pass
   bool fuse_alpha = true;
+  // fused one-shot plans: sizes and the column-drop decision read back once
+  bool spec_plan = true;
 };
 
 // Diagnostics trace of one root: per evaluation kTraceCols doubles
@@ -129,7 +131,7 @@ void solve_roots(const ReducedView& rp, const double* alpha, int64_t j0, int64_t
 // orthogonal complement of the pole's rows. #eig < v = #{d < v} + m - nu.
 void pole_inertia(const ReducedView& rp, const double* bval, const int64_t* brow, const int* bcnt,
                   int64_t nb, int* nu, DeviceScratch& ws, cudaStream_t st,
-                  double* alpha_out = nullptr);
+                  double* alpha_out = nullptr, const unsigned long long* nb_dev = nullptr);
 
 void group_weights(int kp, const double* rep, const double* u, int64_t n, const int64_t* gstart,
                    const int64_t* glen, const double* gval, int64_t ng, const int* sgn, int k,
