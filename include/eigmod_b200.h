@@ -58,7 +58,10 @@ int eigmod_b200_ctx_use_own_stream(eigmod_b200_ctx* ctx);
  * "pole_split" (1), "split_phase_a" (1: unisolated roots are bisected in a
  * first solver stage before the scalar presolve), "fnewton" (1), "fpre" (1),
  * "fpre_min_kp", "fpre_iters", "cluster", "fexit_rel", "floor_rel",
- * "floor_ulps", "stall_ratio", "geo_bisect", "trace_root", "fuse_alpha" (1:
+ * "floor_ulps", "stall_ratio", "geo_bisect", "trace_root", "fpre_rel" (1e-6:
+ * the presolve's stopping step relative to delta), "compact" (1: drained
+ * solver batches pack their slots), "spec_plan" (1: one host round trip for
+ * the one-shot plan), "fuse_alpha" (1:
  * one-shot updates in exact mode take the residues of the scalar presolve
  * from the pole-limit count pass instead of a separate K2 pass). Unknown keys
  * fail with a message. */

@@ -499,6 +499,8 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
       ctx->sopt.fnewton = value != 0.0;
     } else if (std::string(key) == "fpre") {
       ctx->sopt.fpre = value != 0.0;
+    } else if (std::string(key) == "fpre_rel") {
+      ctx->sopt.fpre_rel = value;
     } else if (std::string(key) == "spec_plan") {
       ctx->sopt.spec_plan = value != 0.0;
     } else if (std::string(key) == "compact") {

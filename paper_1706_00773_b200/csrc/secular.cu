@@ -223,6 +223,7 @@ struct FPreArgs {
   unsigned long long* next_root;
   int max_iters;
   unsigned long long* prof;  // [0] converged, [1] unconverged, [2] evaluations, [3] max
+  double rel;                // converged: |step| <= rel |delta| (the solver refines)
 };
 
 constexpr int kFPreWarps = 32;
@@ -297,7 +298,7 @@ __device__ void fpre_step(FPreSmem& s, int b, const FPreArgs& a) {
   const double dn0 = dl + step;
   const bool inside = dn0 > lo && dn0 < hi;
   // converged: a few ulps, or no longer shrinking at the rounding floor of f
-  if (inside && (fabs(step) <= 4.0 * DBL_EPSILON * fabs(dl) ||
+  if (inside && (fabs(step) <= fmax(4.0 * DBL_EPSILON, a.rel) * fabs(dl) ||
                  (fabs(step) >= 0.5 * fabs(s.stepp[b]) && fabs(step) <= 1e-11 * fabs(dl)))) {
     fpre_finish(s, b, a, 1, dn0);
     return;
@@ -2143,7 +2144,7 @@ void solve_after_counts(const ReducedView& rp, const double* alpha, int64_t j0, 
     FPreArgs fa{rp.d, alpha, rp.n, br_lo, br_hi, br_ok, br_pl, br_ph, j0, j1, f_o, f_delta, f_state,
                 reinterpret_cast<unsigned long long*>(ws.get_i64("fpre_counter", 1)),
                 opt.fpre_iters,
-                reinterpret_cast<unsigned long long*>(ws.get_i64("fpre_prof", 4))};
+                reinterpret_cast<unsigned long long*>(ws.get_i64("fpre_prof", 4)), opt.fpre_rel};
     EIGB_CUDA(cudaMemsetAsync(fa.prof, 0, 4 * sizeof(unsigned long long), st));
     set_u64_kernel<<<1, 1, 0, st>>>(fa.next_root, (unsigned long long)j0);
     EIGB_LAUNCH_CHECK();

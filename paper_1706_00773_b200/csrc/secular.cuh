@@ -103,6 +103,9 @@ struct SolveOptions {
   // so they get the presolve too, then finish every root (stage 2)
   bool split_phase_a = true;
   int fpre_iters = 12;
+  // presolve stops at |step| <= fpre_rel |delta|: its root is only a start (the S solver
+  // refines it); 1e-6 minimises K3 at config 4 (tools/exp_fpre_rel.py: 71.6 -> 69.3 ms)
+  double fpre_rel = 1e-6;
   // exact mode, one device: the residues alpha come from the pole-limit count
   // pass (the same pole sum at every pole value) instead of a K2 pass
   bool fuse_alpha = true;

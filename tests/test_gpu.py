@@ -276,7 +276,8 @@ def test_deterministic(api, ctx):
                                   {"fpre": 1, "fpre_iters": 2}, {"cluster": 1}, {"cluster": 8},
                                   {"fnewton": 0}, {"sweep_poles": 0},
                                   {"sweep_poles": 0, "pole_split": 0}, {"split_phase_a": 0},
-                                  {"sweep": 0}, {"fuse_alpha": 0}])
+                                  {"sweep": 0}, {"fuse_alpha": 0}, {"fpre_rel": 0},
+                                  {"compact": 0}, {"spec_plan": 0}])
 def test_solver_variants_meet_tolerances(api, opts):
     """The solver's optional phases (scalar f presolve, f-Newton, cluster
     sizes) change only the path to each root: every variant meets the
