@@ -1321,8 +1321,9 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) solve_roots_ke
   if (t == 0) drained = 0;
   __syncthreads();
   PassOpts o;
-  o.alpha = a.alpha ? a.alpha + plo : nullptr;
-  o.want_sigma = true;
+  // a phase-A stage bisects on the count alone: no sigma' (g) and no f
+  o.alpha = (a.alpha && !a.phase_a_only) ? a.alpha + plo : nullptr;
+  o.want_sigma = !a.phase_a_only;
   unsigned long long npass = 0, nact = 0;
   long long c_refill = 0, c_pass = 0, c_red = 0, c_step = 0;  // SM cycles (thread 0)
   long long c_load = 0, c_fact = 0, c_solve = 0;
@@ -1441,17 +1442,28 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) solve_roots_ke
         P.dsgn[b] = sg;
       }
     }
-    for (int it = 0; it < 3; ++it) {  // inverse iteration: y <- S^-1 y / |.|, sigma
-      const bool sel = P.ev[lane] && P.ninv[lane] > it;
-      if (!__syncthreads_or(sel)) break;
-      par_solve<KP>(F, esl, es, P, sel);
-      if (t < 32 && sel) {
+    // Inverse iteration y <- S^-1 y / |.| (sigma: Rayleigh quotient). Every
+    // evaluated slot takes one step, then the slots without a warm start take
+    // their Newton step (slot_post); the warm slots' second and third steps
+    // and the two final steps of the slots that just converged share the same
+    // two solves (at most three solves per pass instead of five; the
+    // arithmetic of every slot is unchanged).
+    for (int it = 0; it < 3; ++it) {
+      const bool selw = P.ev[lane] && P.ninv[lane] > it;         // refresh y (+ sigma)
+      const bool self = it > 0 && P.fin[lane] == 1;               // converged: final steps
+      if (!__syncthreads_or(selw || self)) break;
+      if (t < 32 && self) {
+        for (int c = 0; c < KP; ++c) P.z[c][t] = y[t * KP + c];
+      }
+      __syncthreads();
+      par_solve<KP>(F, esl, es, P, selw || self);
+      if (t < 32 && selw) {
         double zz = 0.0, zy = 0.0;
         for (int c = 0; c < KP; ++c) zz += P.z[c][t] * P.z[c][t], zy += P.z[c][t] * y[t * KP + c];
         if (!(zz > 0.0 && isfinite(zz))) {
           P.ninv[t] = 0;
         } else {
-          P.sigma[t] = zy / zz;  // Rayleigh quotient of S at z
+          P.sigma[t] = zy / zz;
           const double inv = rsqrt(zz);
           for (int c = 0; c < KP; ++c) {
             const double v = P.z[c][t] * inv;
@@ -1460,18 +1472,7 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) solve_roots_ke
           }
         }
       }
-      __syncthreads();
-    }
-    const long long t3c = clock64();
-    if (t < 32 && P.ev[t]) slot_post<KP>(s, P, y, t, red, a);
-    for (int it = 0; it < 2; ++it) {  // converged slots: two more steps
-      const bool sel = P.fin[lane] == 1;
-      if (!__syncthreads_or(sel)) break;
-      if (t < 32 && sel)
-        for (int c = 0; c < KP; ++c) P.z[c][t] = y[t * KP + c];
-      __syncthreads();
-      par_solve<KP>(F, esl, es, P, sel);
-      if (t < 32 && sel) {
+      if (t < 32 && self) {
         double z2 = 0.0;
         for (int c = 0; c < KP; ++c) z2 += P.z[c][t] * P.z[c][t];
         if (!(z2 > 0.0 && isfinite(z2))) {
@@ -1481,7 +1482,10 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) solve_roots_ke
           for (int c = 0; c < KP; ++c) y[t * KP + c] = P.z[c][t] * inv;
         }
       }
+      if (it == 0 && t < 32 && P.ev[t] && !s.warm[t]) slot_post<KP>(s, P, y, t, red, a);
     }
+    const long long t3c = clock64();
+    if (t < 32 && P.ev[t] && s.warm[t]) slot_post<KP>(s, P, y, t, red, a);
     __syncthreads();
     if (t < 32 && P.fin[t]) {
       double yc[KP];
