@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(kFPreWarps * 32) fpresolve_kernel(FPreArgs a) 
             const double2 p = tile[i];
             const double diff = (p.x - dob) - del;
             hit |= (diff == 0.0);
-            const double D = (diff == 0.0 || diff != diff) ? 0.0 : rcp64(diff);
+            const double D = (diff == 0.0 || diff != diff) ? 0.0 : rcp64_fast(diff);
             const double aD = p.y * D;
             fa += aD;
             fpa = fma(aD, D, fpa);
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(kFPreWarps * 32) fpresolve_kernel(FPreArgs a) 
             const double2 p = tile[i];
             const double diff = (p.x - dob) - del;
             hit |= (diff == 0.0);
-            const double D = (diff == 0.0 || diff != diff) ? 0.0 : rcp64(diff);
+            const double D = (diff == 0.0 || diff != diff) ? 0.0 : rcp64_fast(diff);
             const double aD = p.y * D;
             const double aL = (t0 + i < below) ? aD : 0.0, aR = aD - aL;
             ps += aL;
