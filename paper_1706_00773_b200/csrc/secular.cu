@@ -1941,7 +1941,78 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) pole_inertia_k
     if (rank != 0) return;
     __syncthreads();
   }
-  if (t >= 32 || !active[t]) return;
+  // Simple poles (one row w at v), all warps (par_factor / par_solve on the
+  // shared-memory factor storage, as K2): one Bunch-Kaufman factorization of
+  // T = S(v) without w's term gives nu(T) and z = T^-1 w; the bordered matrix
+  // [[T, w], [w^T, 0]] has inertia In(T) + In(-w^T z) = In(T restricted to
+  // w-perp) + (1, 1), so nu(T|w-perp) = nu(T) - [w^T z < 0], and the residue
+  // is alpha = det(J) det(T) w^T z. Ill-conditioned T (pivots spanning more
+  // than 1e8, a zero pivot, w^T z = 0) and multiple poles take the per-slot
+  // path below (Householder projection, the reference's adjugate route).
+  __shared__ int slow[32];
+  if constexpr (kFactorInSmem<KP>) {
+    ParSmem<KP>& P = *reinterpret_cast<ParSmem<KP>*>(smem + C::SMEM_DOUBLES);
+    double* F = smem;
+    constexpr size_t esl = 1;
+    constexpr int es = 32;
+    const double* red = pass_result<KP>(smem);
+    if (t < 32) {
+      P.ev[t] = active[t] && a.bcnt[g0 + t] == 1;
+      P.neg[t] = 0;
+      P.zero[t] = 0;
+      P.dskip[t] = 0;
+      slow[t] = active[t];
+    }
+    __syncthreads();
+    par_load_S<KP>(red, a.rp.sgn, a.rp.k, F, esl, es, P);
+    __syncthreads();
+    par_factor<KP>(F, esl, es, P);
+    if (t < 32 && P.ev[t]) {
+      const double* w = a.rp.u + a.brow[g0 + t] * KP;
+      for (int c = 0; c < KP; ++c) P.z[c][t] = (c < a.rp.k) ? w[c] : 0.0;
+      P.tiny[t] = 0.0;
+    }
+    __syncthreads();
+    par_solve<KP>(F, esl, es, P, P.ev[t & 31] != 0);
+    if (t < 32 && P.ev[t]) {
+      const int b = t;
+      const double* w = a.rp.u + a.brow[g0 + b] * KP;
+      double wz = 0.0;
+      for (int c = 0; c < a.rp.k; ++c) wz += w[c] * P.z[c][b];
+      double det = 1.0, pmax = 0.0, pmin = INFINITY;
+      for (int q = 0; q < KP; ++q) {
+        const int bt = P.bs[q][b];
+        double pv;
+        if (bt == 0) {
+          pv = FA(q, q);
+          det *= pv;
+          pv = fabs(pv);
+        } else if (bt == 1) {
+          const double d2 = FA(q, q) * FA(q + 1, q + 1) - FA(q + 1, q) * FA(q + 1, q);
+          det *= d2;
+          pv = sqrt(fabs(d2));
+        } else {
+          continue;
+        }
+        pmax = fmax(pmax, pv);
+        pmin = fmin(pmin, pv);
+      }
+      if (!P.zero[b] && pmin > 1e-8 * pmax && isfinite(det) && wz != 0.0 && isfinite(wz)) {
+        a.nu[g0 + b] = P.neg[b] - (wz < 0.0 ? 1 : 0);
+        if (a.alpha_out) {
+          double sj = 1.0;
+          for (int r = 0; r < a.rp.k; ++r) sj *= (double)a.rp.sgn[r];
+          a.alpha_out[a.brow[g0 + b]] = sj * det * wz;
+        }
+        slow[b] = 0;
+      }
+    }
+    __syncthreads();
+  } else {
+    if (t < 32) slow[t] = active[t];
+    __syncthreads();
+  }
+  if (t >= 32 || !slow[t]) return;
   const int64_t g = g0 + t;
   const int k = a.rp.k;
   double* T = a.scratch + ((size_t)(blockIdx.x / CL) * 32 + t) * kInertiaScratch<KP>;
@@ -2010,7 +2081,7 @@ void launch_inertia(const ReducedView& rp, const double* bval, const int64_t* br
   const int grid = (int)cdiv(nb, 32);
   InertiaArgs<KP> a{rp, bval, brow, bcnt, nb, nu, nullptr, alpha_out, nb_dev};
   a.scratch = ws.get_f64("inertia_scratch", (size_t)grid * 32 * kInertiaScratch<KP>);
-  const size_t sm = sizeof(double) * C::SMEM_DOUBLES;
+  const size_t sm = sizeof(double) * C::SMEM_DOUBLES + (kFactorInSmem<KP> ? sizeof(ParSmem<KP>) : 0);
   // pole slices of >= 4096 per CTA; pairs for the MMA ranks (two CTAs per SM)
   static int count_cl = -1;  // EIGMOD_B200_COUNT_CL=2: pole slices on CTA pairs (experiment)
   if (count_cl < 0) {
