@@ -1293,7 +1293,7 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) solve_roots_ke
                 "factor storage must fit in the pass tiles");
   SolveSmem& s = *reinterpret_cast<SolveSmem*>(y + 32 * KP);
   ParSmem<KP>& P = *reinterpret_cast<ParSmem<KP>*>(reinterpret_cast<char*>(&s) + kSolveSmemPad);
-  __shared__ int any, mt_sh;
+  __shared__ int any, mt_sh, need_f;
   __shared__ int drained;
   const int t = threadIdx.x;
   int rank = 0;
@@ -1322,7 +1322,8 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) solve_roots_ke
   __syncthreads();
   PassOpts o;
   // a phase-A stage bisects on the count alone: no sigma' (g) and no f
-  o.alpha = (a.alpha && !a.phase_a_only) ? a.alpha + plo : nullptr;
+  const double* alpha_pass = (a.alpha && !a.phase_a_only) ? a.alpha + plo : nullptr;
+  o.alpha = alpha_pass;
   o.want_sigma = !a.phase_a_only;
   unsigned long long npass = 0, nact = 0;
   long long c_refill = 0, c_pass = 0, c_red = 0, c_step = 0;  // SM cycles (thread 0)
@@ -1361,12 +1362,16 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) solve_roots_ke
       if (t == 0) mt_sh = mt;
     }
     if (t == 0) {
-      int v = 0, c = 0;
+      int v = 0, c = 0, nf = 0;
       for (int b = 0; b < 32; ++b) {
         v |= s.active[b];
         c += (s.active[b] == 1);
+        // f, f' are read by the f-Newton phase and by the first (warm)
+        // evaluation of a presolved root (its sigma' estimate)
+        nf |= (s.active[b] == 1 && s.phase[b] == 1 && (s.fmode[b] || s.warm[b]));
       }
       any = v;
+      need_f = nf;
       npass += (v != 0);
       nact += c;
     }
@@ -1375,6 +1380,7 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) solve_roots_ke
     const long long t1 = clock64();
     // ---- pole pass over this CTA's slice
     PassSlots sl{s.dob, s.delta, y, s.active, s.hit};
+    o.alpha = need_f ? alpha_pass : nullptr;
     secular_pass<KP>(a.rp.d + plo, a.rp.u + plo * KP, pcnt, sl, o, smem, mt_sh);
     const double* red = pass_result<KP>(smem);
     const long long t2 = clock64();
