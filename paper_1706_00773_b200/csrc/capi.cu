@@ -297,8 +297,14 @@ void finish(eigmod_b200_ctx* c, const double* q, const double* lam_in, int64_t c
     if (best_waste < 0 || waste < best_waste) best_waste = waste, best_w = w;
   }
   std::vector<int64_t> bstart;  // block boundaries in columns
-  for (int64_t a = 0; a < main_tiles; a += best_w) bstart.push_back(a * 128);
-  if (tail) bstart.push_back(main_tiles * 128);
+  if (ctiles < 16) {
+    // small problems: the copy is short and the GEMM takes microseconds; one
+    // block avoids the per-block launches (GEMM, sign rule, copy)
+    bstart.push_back(0);
+  } else {
+    for (int64_t a = 0; a < main_tiles; a += best_w) bstart.push_back(a * 128);
+    if (tail) bstart.push_back(main_tiles * 128);
+  }
   bstart.push_back(nc);
   const int64_t nb = (int64_t)bstart.size() - 1;
   while ((int64_t)c->blk_ev.size() < nb) {
