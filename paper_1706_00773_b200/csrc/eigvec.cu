@@ -953,7 +953,7 @@ struct XtmSmem {
 };
 
 template <int KP>
-__global__ void __launch_bounds__(256, 2) xt_mma_kernel(
+__global__ void __launch_bounds__(256, 3) xt_mma_kernel(
     ReducedView rp, int64_t n, const int* __restrict__ ckind, const int64_t* __restrict__ cpay,
     const int64_t* __restrict__ origin, const double* __restrict__ delta,
     const int* __restrict__ flags, const double* __restrict__ yall,
