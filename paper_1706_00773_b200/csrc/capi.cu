@@ -509,6 +509,8 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
       ctx->sopt.fpre_rel = value;
     } else if (std::string(key) == "spec_plan") {
       ctx->sopt.spec_plan = value != 0.0;
+    } else if (std::string(key) == "noise_c") {
+      ctx->sopt.noise_c = value;
     } else if (std::string(key) == "compact") {
       ctx->sopt.compact = value != 0.0 ? 1 : 0;
     } else if (std::string(key) == "fuse_alpha") {

@@ -116,6 +116,8 @@ struct SolveArgs {
   double fexit_rel, floor_rel, floor_ulps, stall_ratio;
   int geo_bisect;
   int compact;               // pack the slots of drained batches (tail passes on fewer m-tiles)
+  const double* un2;         // |u_i|^2 of the reduced rows (noise-floor stopping; nullptr: off)
+  double noise_c;            // converged when |sigma| <= noise_c eps (1 + sum |u_i|^2 |D_i|)
   int64_t trace_j;           // diagnostics (-1: off)
   double* trace;             // [kTraceRows][kTraceCols]
   const int64_t* f_o;        // f presolve per root [j0, j1) (nullptr: none): origin,
@@ -458,6 +460,15 @@ __global__ void __launch_bounds__(kFPreWarps * 32) fpresolve_kernel(FPreArgs a) 
     if (t < 32 && s.act[t] == 1) fpre_step(s, t, a);
     __syncthreads();
   }
+}
+
+__global__ void row_norm2_kernel(const double* __restrict__ u, int64_t n, int kp,
+                                 double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double v = 0.0;
+  for (int c = 0; c < kp; ++c) v = fma(u[i * kp + c], u[i * kp + c], v);
+  out[i] = v;
 }
 
 // A root-queue counter set on the stream (a pageable host-to-device copy of
@@ -1175,8 +1186,24 @@ __device__ void slot_post(SolveSmem& s, ParSmem<KP>& P, double* y, int b, const 
     if (o + 1 < N) gn = fmin(gn, fabs((d[o + 1] - s.dob[b]) - dl));
     far = fabs(step) <= 1e-10 * gn;
   }
+  // at the rounding floor of the S evaluation: |sigma| within the rounding
+  // error of the pole sum (LAPACK dlaed4's |f| <= eps erretm for S) -- the
+  // iterate is a root to working precision unless a neighbouring pole is
+  // within 1e10 times the implied uncertainty (clustered poles, where the
+  // vector needs delta to its own ulps)
+  bool nfloor = false;
+  if (!s.fmode[b] && a.noise_c > 0.0 && a.un2 && gp > 0.0) {
+    const double gnv = rb[C::IGN];
+    if (fabs(sigma) <= a.noise_c * DBL_EPSILON * (1.0 + gnv)) {
+      const int64_t o = s.o[b];
+      double gd = INFINITY;
+      if (o > 0) gd = fmin(gd, fabs((d[o - 1] - s.dob[b]) - dl));
+      if (o + 1 < N) gd = fmin(gd, fabs((d[o + 1] - s.dob[b]) - dl));
+      nfloor = fabs(sigma) / gp <= 1e-10 * gd;
+    }
+  }
   const bool sdone =
-      !s.fmode[b] && ((fabs(step) <= a.step_tol * DBL_EPSILON * fabs(dl)) ||
+      !s.fmode[b] && (nfloor || (fabs(step) <= a.step_tol * DBL_EPSILON * fabs(dl)) ||
                       (stalled && (fabs(step) <= a.floor_rel * fabs(dl) ||
                                    (far && fabs(step) <= a.floor_ulps * DBL_EPSILON *
                                                              fabs(s.dob[b] + dl)))));
@@ -1324,6 +1351,7 @@ __global__ void __launch_bounds__(kPassThreads, KP <= 16 ? 2 : 1) solve_roots_ke
   // a phase-A stage bisects on the count alone: no sigma' (g) and no f
   const double* alpha_pass = (a.alpha && !a.phase_a_only) ? a.alpha + plo : nullptr;
   o.alpha = alpha_pass;
+  o.un2 = (a.un2 && !a.phase_a_only && a.noise_c > 0.0) ? a.un2 + plo : nullptr;
   o.want_sigma = !a.phase_a_only;
   unsigned long long npass = 0, nact = 0;
   long long c_refill = 0, c_pass = 0, c_red = 0, c_step = 0;  // SM cycles (thread 0)
@@ -1729,7 +1757,7 @@ void launch_solve(const ReducedView& rp, const double* alpha, double* br_lo, dou
                   const double* f_delta, const int* f_state, const int64_t* order, int64_t j0,
                   int64_t j1, int64_t q_end, int phase_a_only, int* pa_evals, bool first_stage,
                   const RootRecords& out, const SolveOptions& opt, DeviceScratch& ws, int sms,
-                  cudaStream_t st) {
+                  cudaStream_t st, const double* un2) {
   SolveArgs<KP> a;
   a.phase_a_only = phase_a_only;
   a.pa_evals = pa_evals;
@@ -1765,6 +1793,8 @@ void launch_solve(const ReducedView& rp, const double* alpha, double* br_lo, dou
   a.stall_ratio = opt.stall_ratio;
   a.geo_bisect = opt.geo_bisect;
   a.compact = opt.compact;
+  a.noise_c = opt.noise_c;
+  a.un2 = un2;
   a.trace = ws.get_f64("solve_trace", (size_t)kTraceRows * kTraceCols);
   if (first_stage) {  // a split solve's second stage keeps the first stage's trace and profile
     if (opt.trace_root >= 0)
@@ -2254,9 +2284,15 @@ void solve_after_counts(const ReducedView& rp, const double* alpha, int64_t j0, 
                                                                   j0, cnt, order);
     EIGB_LAUNCH_CHECK();
   };
+  double* un2 = nullptr;  // |u_i|^2 per reduced row (noise-floor stopping)
+  if (opt.noise_c > 0.0 && rp.n > 0) {
+    un2 = ws.get_f64("solve_un2", rp.n);
+    row_norm2_kernel<<<(unsigned)cdiv(rp.n, 256), 256, 0, st>>>(rp.u, rp.n, rp.kp, un2);
+    EIGB_LAUNCH_CHECK();
+  }
 #define EIGB_SOLVE(K)                                                                          \
   launch_solve<K>(rp, alpha, br_lo, br_hi, br_ok, br_pl, br_ph, f_o, f_delta, f_state, order,   \
-                  j0, j1, q_end, phase_a_only, pa_evals, first_stage, out, opt, ws, sms, st)
+                  j0, j1, q_end, phase_a_only, pa_evals, first_stage, out, opt, ws, sms, st, un2)
   auto solve = [&](int64_t q_end, int phase_a_only, int* pa_evals, bool first_stage) {
     switch (rp.kp) {
       case 1: EIGB_SOLVE(1); break;

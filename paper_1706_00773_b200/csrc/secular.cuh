@@ -93,6 +93,8 @@ struct SolveOptions {
   double stall_ratio = 0.5;  // "no longer shrinking": |step| >= stall_ratio * |previous step|
   int geo_bisect = 1;       // geometric bisection of brackets spanning decades of delta
   int compact = 1;          // pack the slots of drained solver batches (tail passes)
+  // noise-floor stopping: converged when |sigma| <= noise_c eps (1 + sum |u_i|^2 |D_i|) (0: off)
+  double noise_c = 1.0;
   // scalar presolve: the f-root (K2 residues) of every isolated root before
   // the S solver, which then starts psi-Newton there. Used from kp = 16 up,
   // where an S evaluation costs ~10x an f evaluation (cfg4 n = 32768: solve

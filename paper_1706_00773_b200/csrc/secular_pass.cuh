@@ -70,14 +70,16 @@ struct PassCfg {
   __host__ __device__ static constexpr int pidx(int r, int c) {
     return r * KP - r * (r - 1) / 2 + (c - r);
   }
-  // reduced output per slot: P packed entries, then g, f, f'
-  static constexpr int OUT = P + 3;
-  static constexpr int IG = P, IF = P + 1, IFP = P + 2;
+  // reduced output per slot: P packed entries, then g, f, f', and the
+  // rounding scale sum_i |u_i|^2 |D_i| of the S evaluation (noise bound)
+  static constexpr int OUT = P + 4;
+  static constexpr int IG = P, IF = P + 1, IFP = P + 2, IGN = P + 3;
   // shared memory (doubles): tile = d, alpha, u rows
   // poles per tile: 128 (64 for KP = 32, whose reduction buffer is 136 KB;
   // 64 in MMA mode, 16 k-steps of 4 poles)
   static constexpr int T = MMA ? kPoleTile : ((KP >= 32) ? kPoleTile : 2 * kPoleTile);
-  static constexpr int TILE_DOUBLES = T * (LDU + 2);
+  // tile: d, alpha, |u|^2 (noise bound), then the u rows
+  static constexpr int TILE_DOUBLES = T * (LDU + 3);
   // D buffer: lane = slot order (DFMA), or A fragments per k-step (MMA)
   static constexpr int DBUF_MIN = MMA ? (T / 4) * DKS : T * 32;
   // the solver and K2 overlay their k x k factors (lower triangles, packed:
@@ -103,6 +105,7 @@ struct PassSlots {
 
 struct PassOpts {
   const double* alpha = nullptr;  // residues for f (nullptr: f not needed)
+  const double* un2 = nullptr;    // |u_i|^2 (nullptr: no rounding-scale sum)
   bool want_sigma = false;        // accumulate g_b along y_b
   bool exclude_zero = false;      // diff == 0 drops the term (no hit flag)
   double excl_gap = 0.0;          // > 0: drop poles with |d_i - dob| < excl_gap
@@ -112,18 +115,20 @@ template <int KP>
 __device__ __forceinline__ void load_pole_tile(double* tile, const double* __restrict__ d,
                                                const double* __restrict__ alpha,
                                                const double* __restrict__ u, int64_t i0,
-                                               int64_t n) {
-  // tile layout: [T] d, [T] alpha, then [T][KP] rows. Rows beyond n are zero
-  // with d = NaN (NaN difference => term skipped).
+                                               int64_t n, const double* __restrict__ un2 = nullptr) {
+  // tile layout: [T] d, [T] alpha, [T] |u|^2, then [T][LDU] rows. Rows beyond
+  // n are zero with d = NaN (NaN difference => term skipped).
   constexpr int T = PassCfg<KP>::T, LDU = PassCfg<KP>::LDU;
   double* td = tile;
   double* ta = tile + T;
-  double* tu = tile + 2 * T;
+  double* tn = tile + 2 * T;
+  double* tu = tile + 3 * T;
   const int tid = threadIdx.x;
   const int64_t cnt = (n - i0) < T ? (n - i0) : T;
   for (int t = tid; t < T; t += kPassThreads) {
     td[t] = (t < cnt) ? d[i0 + t] : __longlong_as_double(0x7ff8000000000000ll);
     ta[t] = (t < cnt && alpha) ? alpha[i0 + t] : 0.0;
+    tn[t] = (t < cnt && un2) ? un2[i0 + t] : 0.0;
   }
   if constexpr (KP >= 2) {
     constexpr int CH = KP / 2;  // 16-byte chunks per row
@@ -203,27 +208,29 @@ __device__ __forceinline__ void pass_body(const double* __restrict__ d, const do
   const bool act = slots.active[lane] != 0;
   const bool sig = o.want_sigma;
   const bool wf = o.alpha != nullptr;
+  const bool wn = o.un2 != nullptr;
   double yv[KP];
 #pragma unroll
   for (int c = 0; c < KP; ++c) yv[c] = sig ? slots.y[lane * KP + c] : 0.0;
   double acc[E > 0 ? E : 1];
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.0;
-  double gs = 0.0, fs = 0.0, fps = 0.0;
+  double gs = 0.0, fs = 0.0, fps = 0.0, gn = 0.0;
   int hit = 0;
 
   const int64_t ntiles = (n + C::T - 1) / C::T;
-  if (ntiles > 0) load_pole_tile<KP>(tiles, d, o.alpha, u, 0, n);
+  if (ntiles > 0) load_pole_tile<KP>(tiles, d, o.alpha, u, 0, n, o.un2);
   for (int64_t t = 0; t < ntiles; ++t) {
     const double* cur = tiles + (t & 1) * C::TILE_DOUBLES;
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();  // tile t landed; previous FMA phase done with dbuf
     if (t + 1 < ntiles)
       load_pole_tile<KP>(tiles + ((t + 1) & 1) * C::TILE_DOUBLES, d, o.alpha, u,
-                         (t + 1) * C::T, n);
+                         (t + 1) * C::T, n, o.un2);
     const double* td = cur;
     const double* ta = cur + C::T;
-    const double* tu = cur + 2 * C::T;
+    const double* tn = cur + 2 * C::T;
+    const double* tu = cur + 3 * C::T;
     // ---- D phase
 #pragma unroll 8
     for (int i = warp; i < C::T; i += kPassWarps) {
@@ -263,6 +270,7 @@ __device__ __forceinline__ void pass_body(const double* __restrict__ d, const do
         fs += aD;
         fps = fma(aD, D, fps);
       }
+      if (wn) gn = fma(tn[i], fabs(D), gn);
     }
     __syncthreads();  // D of this tile visible
     // ---- FMA phase
@@ -289,10 +297,12 @@ __device__ __forceinline__ void pass_body(const double* __restrict__ d, const do
         red[lane * OUT + C::IG] = gs;
         red[lane * OUT + C::IF] = fs;
         red[lane * OUT + C::IFP] = fps;
+        red[lane * OUT + C::IGN] = gn;
       } else {
         red[lane * OUT + C::IG] += gs;
         red[lane * OUT + C::IF] += fs;
         red[lane * OUT + C::IFP] += fps;
+        red[lane * OUT + C::IGN] += gn;
       }
     }
     __syncthreads();
@@ -423,6 +433,7 @@ __device__ __forceinline__ void pass_body_mma(const double* __restrict__ d,
   const bool act = slots.active[slot] != 0;
   const bool sig = o.want_sigma;
   const bool wf = o.alpha != nullptr;
+  const bool wn = o.un2 != nullptr;
   const bool exg = o.excl_gap > 0.0;
   const int64_t xr = (exg && slots.excl_row) ? slots.excl_row[slot] : -1;
   double yf[KC];
@@ -433,21 +444,22 @@ __device__ __forceinline__ void pass_body_mma(const double* __restrict__ d,
   for (int m = 0; m < 2; ++m)
 #pragma unroll
     for (int j = 0; j < NTL; ++j) acc[m][j][0] = acc[m][j][1] = 0.0;
-  double gs = 0.0, fs = 0.0, fps = 0.0;
+  double gs = 0.0, fs = 0.0, fps = 0.0, gn = 0.0;
   int hit = 0;
 
   const int64_t ntiles = (n + C::T - 1) / C::T;
-  if (ntiles > 0) load_pole_tile<KP>(tiles, d, o.alpha, u, 0, n);
+  if (ntiles > 0) load_pole_tile<KP>(tiles, d, o.alpha, u, 0, n, o.un2);
   for (int64_t t = 0; t < ntiles; ++t) {
     const double* cur = tiles + (t & 1) * C::TILE_DOUBLES;
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();  // tile t landed; previous MMA phase done with dbuf
     if (t + 1 < ntiles)
       load_pole_tile<KP>(tiles + ((t + 1) & 1) * C::TILE_DOUBLES, d, o.alpha, u,
-                         (t + 1) * C::T, n);
+                         (t + 1) * C::T, n, o.un2);
     const double* td = cur;
     const double* ta = cur + C::T;
-    const double* tu = cur + 2 * C::T;
+    const double* tn = cur + 2 * C::T;
+    const double* tu = cur + 3 * C::T;
     // ---- D phase (C-fragment layout: slot row g8, poles 8 nd + 2 t4 + h)
 #pragma unroll
     for (int jn = 0; jn < C::T / 16; ++jn) {
@@ -483,6 +495,7 @@ __device__ __forceinline__ void pass_body_mma(const double* __restrict__ d,
           fs += aD;
           fps = fma(aD, D, fps);
         }
+        if (wn) gn = fma(tn[i], fabs(D), gn);
       }
     }
     __syncthreads();  // D of this tile visible
@@ -534,6 +547,7 @@ __device__ __forceinline__ void pass_body_mma(const double* __restrict__ d,
     gs += __shfl_xor_sync(0xffffffffu, gs, o2);
     fs += __shfl_xor_sync(0xffffffffu, fs, o2);
     fps += __shfl_xor_sync(0xffffffffu, fps, o2);
+    gn += __shfl_xor_sync(0xffffffffu, gn, o2);
   }
   for (int q = 0; q < 2; ++q) {
     if ((warp >> 2) == q && t4 == 0) {
@@ -542,10 +556,12 @@ __device__ __forceinline__ void pass_body_mma(const double* __restrict__ d,
         rb[C::IG] = gs;
         rb[C::IF] = fs;
         rb[C::IFP] = fps;
+        rb[C::IGN] = gn;
       } else {
         rb[C::IG] += gs;
         rb[C::IF] += fs;
         rb[C::IFP] += fps;
+        rb[C::IGN] += gn;
       }
     }
     __syncthreads();
