@@ -59,7 +59,9 @@ int eigmod_b200_ctx_use_own_stream(eigmod_b200_ctx* ctx);
  * first solver stage before the scalar presolve), "fnewton" (1), "fpre" (1),
  * "fpre_min_kp", "fpre_iters", "cluster", "fexit_rel", "floor_rel",
  * "floor_ulps", "stall_ratio", "geo_bisect", "trace_root", "fpre_rel" (1e-6:
- * the presolve's stopping step relative to delta), "compact" (1: drained
+ * the presolve's stopping step relative to delta), "noise_c" (1: a root is
+ * converged when |sigma| <= noise_c eps (1 + sum_i |u_i|^2 |D_i|), the
+ * rounding level of the pole sum; 0 disables), "compact" (1: drained
  * solver batches pack their slots), "spec_plan" (1: one host round trip for
  * the one-shot plan), "fuse_alpha" (1:
  * one-shot updates in exact mode take the residues of the scalar presolve

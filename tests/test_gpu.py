@@ -277,7 +277,7 @@ def test_deterministic(api, ctx):
                                   {"fnewton": 0}, {"sweep_poles": 0},
                                   {"sweep_poles": 0, "pole_split": 0}, {"split_phase_a": 0},
                                   {"sweep": 0}, {"fuse_alpha": 0}, {"fpre_rel": 0},
-                                  {"compact": 0}, {"spec_plan": 0}])
+                                  {"compact": 0}, {"spec_plan": 0}, {"noise_c": 0}])
 def test_solver_variants_meet_tolerances(api, opts):
     """The solver's optional phases (scalar f presolve, f-Newton, cluster
     sizes) change only the path to each root: every variant meets the
