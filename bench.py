@@ -541,7 +541,13 @@ def run_ours(args):
         calls = max(1, stages["calls"])
         gemm_ms = stages["k5_gemm"] / calls
         cols = shard.ncols_local if sharded else n
-        gemm_flops = 2.0 * n * n * cols
+        # compact back-transform (plans with >= 64 decoupled columns, kp >= 4;
+        # capi.cu finish_compact): the GEMM runs over the nred reduced rows
+        # and the root columns only, 2 n nred * (roots among the columns)
+        nred, ndec = stats["roots"], stats["decoupled"]
+        compact = ndec >= 64 and int(stats["kp"]) >= 4
+        gemm_cols = cols * nred / n if compact else cols
+        gemm_flops = 2.0 * n * (nred if compact else n) * gemm_cols
         peaks = fp64_peaks_measured(torch, dev, ctx)
         peak = peaks["dmma_tflops"]
         achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
@@ -561,7 +567,9 @@ def run_ours(args):
             "stage_ms": {kk: round(v / calls, 3) for kk, v in stages.items() if kk != "calls"},
             "solver": {"roots": stats["roots"], "evals_per_root":
                        stats["evals"] / max(1.0, stats["roots"]), "max_evals": stats["max_evals"]},
-            "roofline": {"kernel": "K5 dmma_gemm_nt_kernel (Q' = Q X, DMMA.8x8x4)",
+            "roofline": {"kernel": ("K5 dmma_gemm_nt_kernel (Q' = Q X, DMMA.8x8x4)" if not compact
+                                    else "K5 dmma_gemm_nt_kernel (Q'[:, roots] = Q~_red X_red, "
+                                         "DMMA.8x8x4; compact: 2 n nred^2 flops)"),
                          "bound": "tensor", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
                          "peak_source": "DMMA.8x8x4 tensor-pipe loop measured live in this run "
@@ -594,8 +602,12 @@ def run_ours(args):
         # Xt workspace written, 8 B per entry)
         hbm, hbm_src = _hbm_peak()
         k1_cols = (shard.u_hi - shard.u_lo) if sharded else n
+        # compact: Xt_red written (nred per root column), Q read once by the
+        # gather, Q~_red and the decoupled columns of Q' written
+        k4_bytes = (8.0 * (nred * gemm_cols + n * n + n * (nred + cols - gemm_cols)) if compact
+                    else 8.0 * n * cols)
         for key, stage, nbytes in (("roofline_k1", "k1_project", 8.0 * (n * k1_cols + 2 * n * k)),
-                                   ("roofline_k4", "k4_columns", 8.0 * n * cols)):
+                                   ("roofline_k4", "k4_columns", k4_bytes)):
             t = stages[stage] / calls
             if t > 0:
                 a = nbytes / (t * 1e-3) / 1e9

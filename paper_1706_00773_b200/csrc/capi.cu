@@ -227,50 +227,9 @@ __global__ void copy_block_kernel(const double* __restrict__ a, int64_t n, int64
     for (int64_t j = threadIdx.x; j < nc; j += blockDim.x) out[i * ldo + j] = a[i * n + c0 + j];
 }
 
-// host_q_out != nullptr (host-pointer entry points): the GEMM and the sign
-// rule run in column blocks and each finished block is copied to the host on
-// a second stream while the next block computes (the D2H of Q' overlaps the
-// back-transform; each block's signs are final when its GEMM ends).
-void finish(eigmod_b200_ctx* c, const double* q, const double* lam_in, int64_t c0, int64_t c1,
-            double* lam_out, double* q_out, int64_t ldq, double* host_q_out, int64_t host_ld) {
-  eigb::Plan& p = c->plan;
-  const int64_t n = p.n;
-  if (!lam_in) lam_in = c->lam;
-  if (q_out && c1 > c0) c->stage_calls[3] += 1;
-  if (p.k == 0) {  // unchanged pairs: lambda and Q copied exactly
-    if (lam_out)
-      EIGB_CUDA(cudaMemcpyAsync(lam_out, lam_in, 8 * n, cudaMemcpyDeviceToDevice, c->stream));
-    if (q_out && c1 > c0) {
-      copy_block_kernel<<<1024, 256, 0, c->stream>>>(q, n, c0, c1 - c0, q_out, ldq);
-      EIGB_LAUNCH_CHECK();
-    }
-    return;
-  }
-  eigb::Columns cols;
-  eigb::merge_columns_dev(p, c->recs, cols, c->ws, c->stream);
-  if (lam_out)
-    EIGB_CUDA(cudaMemcpyAsync(lam_out, cols.value, 8 * n, cudaMemcpyDeviceToDevice, c->stream));
-  if (!q_out || c1 <= c0) return;
-  double* colldir = c->ws.get_f64("colldir", (size_t)std::max<int64_t>(p.nred, 1) * (2 * p.kp + 4));
-  int* collok = c->ws.get_i32("collok", std::max<int64_t>(p.nred, 1));
-  const int64_t ncoll =
-      eigb::collision_vectors_dev(p, c->recs, cols, c0, c1, colldir, collok, c->ws, c->stream);
-  const int64_t nc = c1 - c0;
-  double* xt = c->ws.get_f64("xt", (size_t)nc * n);
-  double* colscale = c->ws.get_f64("colscale", nc);
-  int* cmode = c->ws.get_i32("colmode", nc);
-  eigb::build_xt_dev(p, c->recs, cols, colldir, collok, ncoll, c0, c1, xt, colscale, cmode,
-                     c->ws, c->stream);
-  c->mark(4);
-  double* tcm = eigb::tile_colmax_buffer(n, nc, c->ws);
-  if (!host_q_out) {
-    eigb::gemm_nt_dev(q, xt, n, nc, n, q_out, ldq, colscale, tcm, c->stream);
-    c->mark(5);
-    eigb::sign_rule_dev(tcm, n, nc, cmode, q_out, ldq, c->ws, c->stream);
-    c->mark(6);
-    return;
-  }
-  if (!c->copy) EIGB_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+// Column blocks [bstart[b], bstart[b + 1]) of an nc-column back-transform
+// whose blocks are copied to the host while the next block computes.
+std::vector<int64_t> gemm_blocks(const eigmod_b200_ctx* c, int64_t n, int64_t nc) {
   // Block width: every block is a separate GEMM launch of 128 x 128 tiles
   // (one CTA per SM), so a block whose tile count is not a multiple of the SM
   // count leaves SMs idle in its last wave. Pick, among 6..16 blocks, the
@@ -306,6 +265,130 @@ void finish(eigmod_b200_ctx* c, const double* q, const double* lam_in, int64_t c
     if (tail) bstart.push_back(main_tiles * 128);
   }
   bstart.push_back(nc);
+  return bstart;
+}
+
+// Compact back-transform (plans with at least kCompactMinDecoupled decoupled
+// columns; eigvec.cu gather_qtilde_dev): the decoupled columns of Q' are
+// copies / run rotations of Q's columns, the root columns one GEMM over the
+// reduced rows, Q' [:, roots] = Q~_red X_red: 2 n nred^2 flops instead of
+// 2 n^3. The gather costs one read of Q (16 n^2 bytes with the write), so it
+// pays from a few dozen decoupled columns on.
+constexpr int64_t kCompactMinDecoupled = 64;
+
+void finish_compact(eigmod_b200_ctx* c, const eigb::Columns& cols, const double* q, int64_t c0,
+                    int64_t c1, double* q_out, int64_t ldq, const double* colldir,
+                    const int* collok, double* host_q_out, int64_t host_ld) {
+  eigb::Plan& p = c->plan;
+  const int64_t n = p.n, nc = c1 - c0, nred = p.nred;
+  eigb::CompactCols cc;
+  eigb::compact_columns_dev(p, cols, c0, c1, cc, c->ws, c->stream);
+  const int64_t nr = cc.j1 - cc.j0;
+  const int64_t ld = std::max<int64_t>(16, eigb::cdiv(nred, 16) * 16);  // 128-byte rows
+  double* qa = c->ws.get_f64("cmp_qa", (size_t)n * ld);
+  double* xr = c->ws.get_f64("cmp_xt", (size_t)std::max<int64_t>(nr, 1) * ld);
+  double* colscale = c->ws.get_f64("colscale", std::max<int64_t>(nr, 1));
+  double* tcm = eigb::tile_colmax_buffer(n, nc, c->ws);
+  eigb::build_xt_compact_dev(p, c->recs, colldir, collok, cc.j0, cc.j1, xr, ld, colscale, c->ws,
+                             c->stream);
+  eigb::gather_qtilde_dev(p, q, cc, qa, ld, q_out, ldq, tcm, nc, c->stream);
+  c->mark(4);
+  if (!host_q_out) {
+    eigb::gemm_nt_ex(qa, ld, xr, ld, n, nr, nred, q_out, ldq, colscale, cc.jpos, tcm, nc,
+                     c->stream);
+    c->mark(5);
+    eigb::sign_rule_ld(tcm, nc, n, nc, cc.cmode, q_out, ldq, c->ws, c->stream);
+    c->mark(6);
+    return;
+  }
+  // host path: blocks of root columns; block b's final columns run from the
+  // first root of the block (0 for the first) to the first root of the next
+  // (nc for the last), decoupled columns in between already gathered
+  if (!c->copy) EIGB_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+  std::vector<int64_t> rb = gemm_blocks(c, n, nr);
+  if (nr == 0) rb = {0, 0};
+  std::vector<int64_t> jpos(std::max<int64_t>(nr, 1), 0);
+  if (nr > 0) {
+    EIGB_CUDA(cudaMemcpyAsync(jpos.data(), cc.jpos, 8 * nr, cudaMemcpyDeviceToHost, c->stream));
+    EIGB_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  const int64_t nb = (int64_t)rb.size() - 1;
+  std::vector<int64_t> fb(nb + 1);
+  for (int64_t b = 0; b <= nb; ++b) fb[b] = (b == 0) ? 0 : (b == nb) ? nc : jpos[rb[b]];
+  while ((int64_t)c->blk_ev.size() < nb) {
+    cudaEvent_t e;
+    EIGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->blk_ev.push_back(e);
+  }
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t ja = rb[b], w = rb[b + 1] - rb[b];
+    eigb::gemm_nt_ex(qa, ld, xr + ja * ld, ld, n, w, nred, q_out, ldq, colscale + ja,
+                     cc.jpos + ja, tcm, nc, c->stream);
+    eigb::sign_rule_ld(tcm + fb[b], nc, n, fb[b + 1] - fb[b], cc.cmode + fb[b], q_out + fb[b],
+                       ldq, c->ws, c->stream);
+    EIGB_CUDA(cudaEventRecord(c->blk_ev[b], c->stream));
+  }
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t a0 = fb[b], w = fb[b + 1] - fb[b];
+    if (w <= 0) continue;
+    EIGB_CUDA(cudaStreamWaitEvent(c->copy, c->blk_ev[b], 0));
+    EIGB_CUDA(cudaMemcpy2DAsync(host_q_out + (c0 + a0), 8 * host_ld, q_out + a0, 8 * ldq, 8 * w,
+                                n, cudaMemcpyDeviceToHost, c->copy));
+  }
+  c->mark(5);
+  c->mark(6);
+  EIGB_CUDA(cudaStreamSynchronize(c->copy));
+}
+
+// host_q_out != nullptr (host-pointer entry points): the GEMM and the sign
+// rule run in column blocks and each finished block is copied to the host on
+// a second stream while the next block computes (the D2H of Q' overlaps the
+// back-transform; each block's signs are final when its GEMM ends).
+void finish(eigmod_b200_ctx* c, const double* q, const double* lam_in, int64_t c0, int64_t c1,
+            double* lam_out, double* q_out, int64_t ldq, double* host_q_out, int64_t host_ld) {
+  eigb::Plan& p = c->plan;
+  const int64_t n = p.n;
+  if (!lam_in) lam_in = c->lam;
+  if (q_out && c1 > c0) c->stage_calls[3] += 1;
+  if (p.k == 0) {  // unchanged pairs: lambda and Q copied exactly
+    if (lam_out)
+      EIGB_CUDA(cudaMemcpyAsync(lam_out, lam_in, 8 * n, cudaMemcpyDeviceToDevice, c->stream));
+    if (q_out && c1 > c0) {
+      copy_block_kernel<<<1024, 256, 0, c->stream>>>(q, n, c0, c1 - c0, q_out, ldq);
+      EIGB_LAUNCH_CHECK();
+    }
+    return;
+  }
+  eigb::Columns cols;
+  eigb::merge_columns_dev(p, c->recs, cols, c->ws, c->stream);
+  if (lam_out)
+    EIGB_CUDA(cudaMemcpyAsync(lam_out, cols.value, 8 * n, cudaMemcpyDeviceToDevice, c->stream));
+  if (!q_out || c1 <= c0) return;
+  double* colldir = c->ws.get_f64("colldir", (size_t)std::max<int64_t>(p.nred, 1) * (2 * p.kp + 4));
+  int* collok = c->ws.get_i32("collok", std::max<int64_t>(p.nred, 1));
+  const int64_t ncoll =
+      eigb::collision_vectors_dev(p, c->recs, cols, c0, c1, colldir, collok, c->ws, c->stream);
+  const int64_t nc = c1 - c0;
+  if (c->compact_gemm && p.kp >= 4 && p.ndec >= kCompactMinDecoupled) {
+    finish_compact(c, cols, q, c0, c1, q_out, ldq, colldir, collok, host_q_out, host_ld);
+    return;
+  }
+  double* xt = c->ws.get_f64("xt", (size_t)nc * n);
+  double* colscale = c->ws.get_f64("colscale", nc);
+  int* cmode = c->ws.get_i32("colmode", nc);
+  eigb::build_xt_dev(p, c->recs, cols, colldir, collok, ncoll, c0, c1, xt, colscale, cmode,
+                     c->ws, c->stream);
+  c->mark(4);
+  double* tcm = eigb::tile_colmax_buffer(n, nc, c->ws);
+  if (!host_q_out) {
+    eigb::gemm_nt_dev(q, xt, n, nc, n, q_out, ldq, colscale, tcm, c->stream);
+    c->mark(5);
+    eigb::sign_rule_dev(tcm, n, nc, cmode, q_out, ldq, c->ws, c->stream);
+    c->mark(6);
+    return;
+  }
+  if (!c->copy) EIGB_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+  const std::vector<int64_t> bstart = gemm_blocks(c, n, nc);
   const int64_t nb = (int64_t)bstart.size() - 1;
   while ((int64_t)c->blk_ev.size() < nb) {
     cudaEvent_t e;
@@ -525,6 +608,8 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
       ctx->sopt.fpre_iters = (int)value;
     } else if (std::string(key) == "cluster") {
       ctx->sopt.cluster = (int)value;
+    } else if (std::string(key) == "compact_gemm") {
+      ctx->compact_gemm = value != 0.0;
     } else if (std::string(key) == "timing") {
       ctx->timing = value != 0.0;
     } else {

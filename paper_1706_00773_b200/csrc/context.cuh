@@ -38,6 +38,9 @@ struct eigmod_b200_ctx {
   // stage launches (K1 projections, K2 plans, K3 solves, K4/K5 column builds)
   int64_t stage_calls[4] = {0, 0, 0, 0};
   bool timing = false;
+  // option "compact_gemm": back-transform over the reduced rows when the plan
+  // has decoupled columns (capi.cu finish_compact)
+  bool compact_gemm = true;
   cudaEvent_t ev[8] = {};
   double stage_ms[8] = {};
   int64_t timed_calls = 0;

@@ -789,8 +789,8 @@ __global__ void __launch_bounds__(256, KP >= 32 ? 1 : 2) xt_rows_kernel(
     double* y = yt + t * YS;
     for (int q = 0; q < YS; ++q) y[q] = 0.0;
     if (c < c1) {
-      kind = ckind[c];
-      const int64_t pay = cpay[c];
+      kind = ckind ? ckind[c] : 0;
+      const int64_t pay = ckind ? cpay[c] : c;
       if (kind == 0) {
         const int64_t j = pay;
         jr = j;
@@ -959,7 +959,10 @@ __global__ void __launch_bounds__(256, 3) xt_mma_kernel(
     const int* __restrict__ flags, const double* __restrict__ yall,
     const double* __restrict__ colldir, const int* __restrict__ collok,
     const int64_t* __restrict__ orig_map, const int64_t* __restrict__ dec_src, int64_t c0,
-    int64_t c1, double* __restrict__ xt, double* __restrict__ part) {
+    int64_t c1, int64_t ldx, double* __restrict__ xt, double* __restrict__ part) {
+  // Compact mode (orig_map == nullptr, ckind == nullptr): rows are the n
+  // reduced rows themselves and columns c are roots (payload j = c); the
+  // back-transform multiplies by the gathered Q~ of the reduced rows.
   using SM = XtmSmem<KP>;
   constexpr int LDU = SM::LDU, KC = KP / 4;
   extern __shared__ __align__(16) double xsm[];
@@ -977,8 +980,8 @@ __global__ void __launch_bounds__(256, 3) xt_mma_kernel(
     double* y = sm.yt + t * LDU;
     for (int q = 0; q < KP; ++q) y[q] = 0.0;
     if (c < c1) {
-      kind = ckind[c];
-      const int64_t pay = cpay[c];
+      kind = ckind ? ckind[c] : 0;
+      const int64_t pay = ckind ? cpay[c] : c;
       if (kind == 0) {
         const int64_t j = pay;
         jr = j;
@@ -1003,7 +1006,7 @@ __global__ void __launch_bounds__(256, 3) xt_mma_kernel(
   // rows: reduced index, pole value, u row (zero outside the reduced problem)
   for (int q = t; q < kXtmRows; q += 256) {
     const int64_t i = ib + q;
-    const int64_t r = (i < n) ? orig_map[i] : -1;
+    const int64_t r = (i < n) ? (orig_map ? orig_map[i] : i) : -1;
     sm.rr[q] = r;
     sm.drow[q] = (r >= 0) ? rp.d[r] : 0.0;
   }
@@ -1028,7 +1031,7 @@ __global__ void __launch_bounds__(256, 3) xt_mma_kernel(
     for (int kc = 0; kc < KC; ++kc) af[m][kc] = sm.yt[qc[m] * LDU + 4 * kc + t4];
     fast[m] = sm.ck[qc[m]] == 0 && sm.cm[qc[m]] == 0;
   }
-  const bool vec = (n % 2) == 0;
+  const bool vec = (ldx % 2) == 0;
 #pragma unroll 2
   for (int nt = 0; nt < kXtmRows / 8; ++nt) {
     double bf[KC];
@@ -1077,7 +1080,7 @@ __global__ void __launch_bounds__(256, 3) xt_mma_kernel(
       }
       const int64_t i = ib + q0;
       if (c < c1) {
-        double* dst = xt + (c - c0) * n + i;
+        double* dst = xt + (c - c0) * ldx + i;
         if (vec && i + 1 < n) {
           __stcs(reinterpret_cast<double2*>(dst), make_double2(x0, x1));
         } else {
@@ -1128,8 +1131,8 @@ void launch_xt(const Plan& p, const RootRecords& roots, const Columns& cols, con
                                      (int)sm));
       xt_mma_kernel<KP><<<grid, 256, sm, st>>>(p.view(), p.n, cols.kind, cols.payload,
                                                roots.origin, roots.delta, roots.flags, roots.y,
-                                               colldir, collok, p.orig_map, p.dec_src, c0, c1, xt,
-                                               part);
+                                               colldir, collok, p.orig_map, p.dec_src, c0, c1,
+                                               p.n, xt, part);
       EIGB_LAUNCH_CHECK();
       xt_norm_kernel<<<(unsigned)cdiv(c1 - c0, 128), 128, 0, st>>>(part, nchunks, c0, c1,
                                                                    cols.kind, colscale, cmode);
@@ -1354,6 +1357,194 @@ void build_xt_dev(const Plan& p, const RootRecords& roots, const Columns& cols,
     case 8: launch_xt<8>(p, roots, cols, colldir, collok, general, c0, c1, xt, colscale, cmode, ws, st); break;
     case 16: launch_xt<16>(p, roots, cols, colldir, collok, general, c0, c1, xt, colscale, cmode, ws, st); break;
     case 32: launch_xt<32>(p, roots, cols, colldir, collok, general, c0, c1, xt, colscale, cmode, ws, st); break;
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Compact back-transform (plans with decoupled columns). Every root column of
+// X is zero on the unchanged rows and, on a compressed run, a combination of
+// the run's rotated rows; so Q' = Q X splits into
+//   Q'[:, decoupled e] = Q~[:, e]            (a copy or one run rotation)
+//   Q'[:, roots]       = Q~_red X_red        (n x nred x nroot on DMMA)
+// with Q~ = Q H (the runs' Householder rotations, eigvec.cpp:288-291 and the
+// rotation rows of the plan) and X_red the root columns over the reduced
+// rows. The reference multiplies by the dense n x n X (eigvec.cpp:285-339);
+// the exact zeros it skips are 2 n (n^2 - nred^2) flops.
+
+// Range of the roots / decoupled entries whose final columns lie in [c0, c1)
+// (both contiguous: the merge is a stable merge by value), and each one's
+// column relative to c0.
+__global__ void compact_ranges_kernel(const int* __restrict__ ckind,
+                                      const int64_t* __restrict__ cpay, int64_t c0, int64_t c1,
+                                      unsigned long long* __restrict__ rng) {
+  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= c1) return;
+  const int kind = ckind[c];
+  const unsigned long long pay = (unsigned long long)cpay[c];
+  const int slot = (kind == 0) ? 0 : 2;
+  atomicMin(rng + slot, pay);
+  atomicMax(rng + slot + 1, pay + 1);
+}
+
+__global__ void compact_pos_kernel(const int* __restrict__ ckind, const int64_t* __restrict__ cpay,
+                                   int64_t c0, int64_t c1, int64_t j0, int64_t e0,
+                                   int64_t* __restrict__ jpos, int64_t* __restrict__ epos,
+                                   int* __restrict__ cmode) {
+  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= c1) return;
+  const int kind = ckind[c];
+  if (kind == 0) jpos[cpay[c] - j0] = c - c0;
+  else epos[cpay[c] - e0] = c - c0;
+  cmode[c - c0] = (kind != 1);  // sign rule on computed columns (eigvec.cpp:340-347)
+}
+
+// Q~ column of a source code: >= 0 the original column, <= -2 row t of group
+// g's rotation (code = -(g * 65536 + t) - 2, deflate.cu assemble_reduced).
+__device__ __forceinline__ double qtilde(const double* __restrict__ qrow, int64_t code,
+                                         const int64_t* __restrict__ gstart,
+                                         const int64_t* __restrict__ glen,
+                                         const int64_t* __restrict__ hoff,
+                                         const double* __restrict__ hbuf) {
+  if (code >= 0) return qrow[code];
+  const int64_t c2 = -(code + 2), g = c2 / 65536, t = c2 % 65536;
+  const int64_t s0 = gstart[g], m = glen[g];
+  const double* H = hbuf + hoff[g] + t * m;
+  double v = 0.0;
+  for (int64_t s = 0; s < m; ++s) v = fma(H[s], qrow[s0 + s], v);
+  return v;
+}
+
+// One thread = one item (a reduced row -> column of Qa, or a decoupled entry
+// -> its final column of Q') over the 128 rows of a row tile; consecutive
+// items read consecutive columns of Q (coalesced) and write consecutive
+// columns of Qa. Decoupled columns also leave their signed max per row tile
+// (first row on ties) for sign_rule_dev, as the GEMM epilogue does.
+constexpr int kGatherRows = 128;
+
+__global__ void __launch_bounds__(256) gather_qtilde_kernel(
+    const double* __restrict__ q, int64_t n, int64_t ldq_in, int64_t nred,
+    const int64_t* __restrict__ red_src, int64_t ne, const int64_t* __restrict__ dec_src,
+    int64_t e0, const int64_t* __restrict__ epos, const int64_t* __restrict__ gstart,
+    const int64_t* __restrict__ glen, const int64_t* __restrict__ hoff,
+    const double* __restrict__ hbuf, double* __restrict__ qa, int64_t lda,
+    double* __restrict__ qout, int64_t ldo, double* __restrict__ tile_colmax, int64_t tcm_ld) {
+  const int64_t item = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+  if (item >= nred + ne) return;
+  const int64_t tm = blockIdx.x, i0 = tm * kGatherRows;
+  const int64_t i1 = (i0 + kGatherRows < n) ? i0 + kGatherRows : n;
+  const bool red = item < nred;
+  const int64_t code = red ? red_src[item] : dec_src[e0 + (item - nred)];
+  double* dst = red ? qa + item : qout + epos[item - nred];
+  const int64_t ldd = red ? lda : ldo;
+  double best = 0.0;  // first row on ties: strict > in ascending row order
+  if (code >= 0) {
+    int64_t i = i0;
+    for (; i + 4 <= i1; i += 4) {
+      double v[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) v[h] = __ldcs(q + (i + h) * ldq_in + code);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        dst[(i + h) * ldd] = v[h];
+        if (fabs(v[h]) > fabs(best)) best = v[h];
+      }
+    }
+    for (; i < i1; ++i) {
+      const double v = __ldcs(q + i * ldq_in + code);
+      dst[i * ldd] = v;
+      if (fabs(v) > fabs(best)) best = v;
+    }
+  } else {
+    for (int64_t i = i0; i < i1; ++i) {
+      const double v = qtilde(q + i * ldq_in, code, gstart, glen, hoff, hbuf);
+      dst[i * ldd] = v;
+      if (fabs(v) > fabs(best)) best = v;
+    }
+  }
+  if (!red && tile_colmax) tile_colmax[tm * tcm_ld + epos[item - nred]] = best;
+}
+
+void compact_columns_dev(const Plan& p, const Columns& cols, int64_t c0, int64_t c1,
+                         CompactCols& cc, DeviceScratch& ws, cudaStream_t st) {
+  cc = CompactCols{};
+  if (c1 <= c0) return;
+  const int64_t nc = c1 - c0;
+  auto* rng = reinterpret_cast<unsigned long long*>(ws.get_i64("cmp_rng", 4));
+  const unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
+  EIGB_CUDA(cudaMemcpyAsync(rng, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  compact_ranges_kernel<<<(unsigned)cdiv(nc, 256), 256, 0, st>>>(cols.kind, cols.payload, c0, c1,
+                                                                 rng);
+  EIGB_LAUNCH_CHECK();
+  unsigned long long h[4];
+  EIGB_CUDA(cudaMemcpyAsync(h, rng, sizeof(h), cudaMemcpyDeviceToHost, st));
+  EIGB_CUDA(cudaStreamSynchronize(st));
+  cc.j0 = (h[1] > 0) ? (int64_t)h[0] : 0;
+  cc.j1 = (h[1] > 0) ? (int64_t)h[1] : 0;
+  cc.e0 = (h[3] > 0) ? (int64_t)h[2] : 0;
+  cc.e1 = (h[3] > 0) ? (int64_t)h[3] : 0;
+  if ((cc.j1 - cc.j0) + (cc.e1 - cc.e0) != nc)
+    throw Error(2, "assemble", "compact columns: root / decoupled ranges are not contiguous");
+  cc.jpos = ws.get_i64("cmp_jpos", std::max<int64_t>(cc.j1 - cc.j0, 1));
+  cc.epos = ws.get_i64("cmp_epos", std::max<int64_t>(cc.e1 - cc.e0, 1));
+  cc.cmode = ws.get_i32("cmp_cmode", nc);
+  compact_pos_kernel<<<(unsigned)cdiv(nc, 256), 256, 0, st>>>(cols.kind, cols.payload, c0, c1,
+                                                              cc.j0, cc.e0, cc.jpos, cc.epos,
+                                                              cc.cmode);
+  EIGB_LAUNCH_CHECK();
+}
+
+void gather_qtilde_dev(const Plan& p, const double* q, const CompactCols& cc, double* qa,
+                       int64_t lda, double* q_out, int64_t ldq, double* tile_colmax,
+                       int64_t tcm_ld, cudaStream_t st) {
+  const int64_t ne = cc.e1 - cc.e0, items = p.nred + ne;
+  if (items == 0) return;
+  dim3 grid((unsigned)cdiv(p.n, kGatherRows), (unsigned)cdiv(items, 256));
+  gather_qtilde_kernel<<<grid, 256, 0, st>>>(q, p.n, p.n, p.nred, p.red_src, ne, p.dec_src, cc.e0,
+                                             cc.epos, p.gstart, p.glen, p.hoff, p.hbuf, qa, lda,
+                                             q_out, ldq, tile_colmax, tcm_ld);
+  EIGB_LAUNCH_CHECK();
+}
+
+template <int KP>
+void launch_xt_compact(const Plan& p, const RootRecords& roots, const double* colldir,
+                       const int* collok, int64_t j0, int64_t j1, double* xt, int64_t ldx,
+                       double* colscale, DeviceScratch& ws, cudaStream_t st) {
+  if constexpr (KP >= 4) {
+    const int64_t nchunks = cdiv(p.nred, kXtmRows);
+    double* part = ws.get_f64("xt_part", (size_t)nchunks * (j1 - j0));
+    int* cm = ws.get_i32("cmp_rootmode", j1 - j0);
+    int* kinds = ws.get_i32("cmp_rootkind", j1 - j0);
+    EIGB_CUDA(cudaMemsetAsync(kinds, 0, 4 * (j1 - j0), st));
+    dim3 grid((unsigned)nchunks, (unsigned)cdiv(j1 - j0, kXtmCols));
+    const size_t sm = sizeof(XtmSmem<KP>);
+    EIGB_CUDA(cudaFuncSetAttribute(xt_mma_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sm));
+    xt_mma_kernel<KP><<<grid, 256, sm, st>>>(p.view(), p.nred, nullptr, nullptr, roots.origin,
+                                             roots.delta, roots.flags, roots.y, colldir, collok,
+                                             nullptr, p.dec_src, j0, j1, ldx, xt, part);
+    EIGB_LAUNCH_CHECK();
+    // every column is a root (kind 0): scale 1/||x_red||
+    xt_norm_kernel<<<(unsigned)cdiv(j1 - j0, 128), 128, 0, st>>>(part, nchunks, 0, j1 - j0,
+                                                                 kinds, colscale, cm);
+    EIGB_LAUNCH_CHECK();
+  } else {
+    (void)p, (void)roots, (void)colldir, (void)collok, (void)j0, (void)j1, (void)xt, (void)ldx,
+        (void)colscale, (void)ws, (void)st;
+    throw Error(2, "assemble", "compact back-transform needs kp >= 4");
+  }
+}
+
+void build_xt_compact_dev(const Plan& p, const RootRecords& roots, const double* colldir,
+                          const int* collok, int64_t j0, int64_t j1, double* xt, int64_t ldx,
+                          double* colscale, DeviceScratch& ws, cudaStream_t st) {
+  if (j1 <= j0) return;
+  switch (p.kp) {
+    case 4: launch_xt_compact<4>(p, roots, colldir, collok, j0, j1, xt, ldx, colscale, ws, st); break;
+    case 8: launch_xt_compact<8>(p, roots, colldir, collok, j0, j1, xt, ldx, colscale, ws, st); break;
+    case 16: launch_xt_compact<16>(p, roots, colldir, collok, j0, j1, xt, ldx, colscale, ws, st); break;
+    case 32: launch_xt_compact<32>(p, roots, colldir, collok, j0, j1, xt, ldx, colscale, ws, st); break;
+    default: throw Error(2, "assemble", "compact back-transform needs kp >= 4");
   }
 }
 

@@ -44,7 +44,8 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // 2 doubles, logical chunk q at physical chunk q ^ (r & 7).
 __device__ __forceinline__ void load_stage(double* st, const double* __restrict__ a,
                                            const double* __restrict__ b, int64_t m, int64_t nn,
-                                           int64_t K, int64_t m0, int64_t n0, int64_t k0) {
+                                           int64_t K, int64_t lda, int64_t ldb, int64_t m0,
+                                           int64_t n0, int64_t k0) {
   const int tid = threadIdx.x;
 #pragma unroll
   for (int s = 0; s < (BM * BK / 2) / GEMM_THREADS; ++s) {
@@ -53,7 +54,7 @@ __device__ __forceinline__ void load_stage(double* st, const double* __restrict_
     const int64_t gr = m0 + row, gk = k0 + 2 * q;
     int bytes = 0;
     if (gr < m && gk < K) bytes = (K - gk >= 2) ? 16 : 8;
-    const double* src = bytes ? a + gr * K + gk : a;
+    const double* src = bytes ? a + gr * lda + gk : a;
     cp_async16(st + row * BK + 2 * (q ^ (row & 7)), src, bytes);
   }
   double* sb = st + BM * BK;
@@ -64,7 +65,7 @@ __device__ __forceinline__ void load_stage(double* st, const double* __restrict_
     const int64_t gr = n0 + row, gk = k0 + 2 * q;
     int bytes = 0;
     if (gr < nn && gk < K) bytes = (K - gk >= 2) ? 16 : 8;
-    const double* src = bytes ? b + gr * K + gk : b;
+    const double* src = bytes ? b + gr * ldb + gk : b;
     cp_async16(sb + row * BK + 2 * (q ^ (row & 7)), src, bytes);
   }
 }
@@ -74,7 +75,8 @@ __device__ __forceinline__ void load_stage(double* st, const double* __restrict_
 // signed entry of largest magnitude, first row on ties (eigvec.cpp:340-347).
 __device__ __forceinline__ void epilogue_store(double (&acc)[8][4][2], int64_t m, int64_t nn,
                                                double* __restrict__ c, int64_t ldc,
-                                               const double* __restrict__ colscale, int64_t m0,
+                                               const double* __restrict__ colscale,
+                                               const int64_t* __restrict__ colmap, int64_t m0,
                                                int64_t n0, int wm, int wn, int g, int t4,
                                                double* colbest, int* colrow) {
 #pragma unroll
@@ -112,6 +114,27 @@ __device__ __forceinline__ void epilogue_store(double (&acc)[8][4][2], int64_t m
       }
     }
   }
+  if (colmap) {  // scattered output columns (compact back-transform)
+    int64_t oc[4][2];
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t col = n0 + wn * 32 + nb * 8 + 2 * t4 + e;
+        oc[nb][e] = (col < nn) ? colmap[col] : -1;
+      }
+#pragma unroll
+    for (int mb = 0; mb < 8; ++mb) {
+      const int64_t row = m0 + wm * 64 + mb * 8 + g;
+      if (row >= m) continue;
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (oc[nb][e] >= 0) c[row * ldc + oc[nb][e]] = acc[mb][nb][e];
+    }
+    return;
+  }
 #pragma unroll
   for (int mb = 0; mb < 8; ++mb) {
     const int64_t row = m0 + wm * 64 + mb * 8 + g;
@@ -131,21 +154,25 @@ __device__ __forceinline__ void epilogue_store(double (&acc)[8][4][2], int64_t m
 }
 
 __device__ __forceinline__ void tile_colmax_write(double* __restrict__ tile_colmax, int64_t tm,
-                                                  int64_t nn, int64_t n0, int tid,
-                                                  const double* colbest, const int* colrow) {
+                                                  int64_t nn, int64_t tcm_ld,
+                                                  const int64_t* __restrict__ colmap, int64_t n0,
+                                                  int tid, const double* colbest,
+                                                  const int* colrow) {
   const int64_t cg = n0 + tid;
   if (cg >= nn) return;
   const double b0 = colbest[tid], b1 = colbest[BN + tid];
   const int r0 = colrow[tid], r1 = colrow[BN + tid];
   double best = b0;
   if (fabs(b1) > fabs(b0) || (fabs(b1) == fabs(b0) && r1 < r0)) best = b1;
-  tile_colmax[tm * nn + cg] = best;
+  tile_colmax[tm * tcm_ld + (colmap ? colmap[cg] : cg)] = best;
 }
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     dmma_gemm_nt_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t m,
-                        int64_t nn, int64_t K, double* __restrict__ c, int64_t ldc,
-                        const double* __restrict__ colscale, double* __restrict__ tile_colmax) {
+                        int64_t nn, int64_t K, int64_t lda, int64_t ldb, double* __restrict__ c,
+                        int64_t ldc, const double* __restrict__ colscale,
+                        const int64_t* __restrict__ colmap, double* __restrict__ tile_colmax,
+                        int64_t tcm_ld) {
   extern __shared__ __align__(128) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps
@@ -170,7 +197,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int64_t KT = (K + BK - 1) / BK;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_stage(smem + s * STAGE_DOUBLES, a, b, m, nn, K, m0, n0, (int64_t)s * BK);
+    if (s < KT)
+      load_stage(smem + s * STAGE_DOUBLES, a, b, m, nn, K, lda, ldb, m0, n0, (int64_t)s * BK);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   const int g = lane >> 2, t4 = lane & 3;
@@ -179,7 +207,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     __syncthreads();
     const int64_t nk = kt + STAGES - 1;
     if (nk < KT)
-      load_stage(smem + (nk % STAGES) * STAGE_DOUBLES, a, b, m, nn, K, m0, n0, nk * BK);
+      load_stage(smem + (nk % STAGES) * STAGE_DOUBLES, a, b, m, nn, K, lda, ldb, m0, n0, nk * BK);
     asm volatile("cp.async.commit_group;" ::: "memory");
     const double* sa = smem + (kt % STAGES) * STAGE_DOUBLES;
     const double* sb = sa + BM * BK;
@@ -213,9 +241,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // ---- epilogue: scale, store, per-tile column max for the sign rule
   double* colbest = smem;                               // [2][BN] signed value
   int* colrow = reinterpret_cast<int*>(smem + 2 * BN);  // [2][BN] row of best
-  epilogue_store(acc, m, nn, c, ldc, colscale, m0, n0, wm, wn, g, t4, colbest, colrow);
+  epilogue_store(acc, m, nn, c, ldc, colscale, colmap, m0, n0, wm, wn, g, t4, colbest, colrow);
   __syncthreads();
-  if (tile_colmax && tid < BN) tile_colmax_write(tile_colmax, tm, nn, n0, tid, colbest, colrow);
+  if (tile_colmax && tid < BN)
+    tile_colmax_write(tile_colmax, tm, nn, tcm_ld, colmap, n0, tid, colbest, colrow);
 }
 
 }  // namespace
@@ -228,13 +257,13 @@ namespace {
 
 // Sign rule across row tiles: first tile holding the maximal |entry| decides.
 __global__ void colsign_kernel(const double* __restrict__ tile_colmax, int64_t tiles_m,
-                               int64_t nn, const int* __restrict__ mode,
+                               int64_t tcm_ld, int64_t nn, const int* __restrict__ mode,
                                double* __restrict__ flip) {
   const int64_t cidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (cidx >= nn) return;
   double best = 0.0;
   for (int64_t t = 0; t < tiles_m; ++t) {
-    const double v = tile_colmax[t * nn + cidx];
+    const double v = tile_colmax[t * tcm_ld + cidx];
     if (fabs(v) > fabs(best)) best = v;
   }
   flip[cidx] = (mode[cidx] && best < 0.0) ? -1.0 : 1.0;
@@ -259,8 +288,15 @@ __global__ void any_flip_kernel(const double* flip, int64_t nn, int* any) {
 
 void gemm_nt_dev(const double* a, const double* b, int64_t m, int64_t nn, int64_t kk, double* c,
                  int64_t ldc, const double* colscale, double* tile_colmax, cudaStream_t st) {
+  gemm_nt_ex(a, kk, b, kk, m, nn, kk, c, ldc, colscale, nullptr, tile_colmax, nn, st);
+}
+
+void gemm_nt_ex(const double* a, int64_t lda, const double* b, int64_t ldb, int64_t m, int64_t nn,
+                int64_t kk, double* c, int64_t ldc, const double* colscale, const int64_t* colmap,
+                double* tile_colmax, int64_t tcm_ld, cudaStream_t st) {
   if (m <= 0 || nn <= 0) return;
-  if ((kk & 1) || (reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15)) {
+  if ((lda & 1) || (ldb & 1) || (reinterpret_cast<uintptr_t>(a) & 15) ||
+      (reinterpret_cast<uintptr_t>(b) & 15)) {
     // odd inner dimension (odd n) or unaligned operands: stage zero-padded
     // copies with an even, 16-byte aligned row pitch (stream-ordered pool)
     const int64_t kp2 = (kk + 1) & ~int64_t(1);
@@ -269,9 +305,9 @@ void gemm_nt_dev(const double* a, const double* b, int64_t m, int64_t nn, int64_
     EIGB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bp), sizeof(double) * nn * kp2, st));
     EIGB_CUDA(cudaMemsetAsync(ap, 0, sizeof(double) * m * kp2, st));
     EIGB_CUDA(cudaMemsetAsync(bp, 0, sizeof(double) * nn * kp2, st));
-    EIGB_CUDA(cudaMemcpy2DAsync(ap, 8 * kp2, a, 8 * kk, 8 * kk, m, cudaMemcpyDeviceToDevice, st));
-    EIGB_CUDA(cudaMemcpy2DAsync(bp, 8 * kp2, b, 8 * kk, 8 * kk, nn, cudaMemcpyDeviceToDevice, st));
-    gemm_nt_dev(ap, bp, m, nn, kp2, c, ldc, colscale, tile_colmax, st);
+    EIGB_CUDA(cudaMemcpy2DAsync(ap, 8 * kp2, a, 8 * lda, 8 * kk, m, cudaMemcpyDeviceToDevice, st));
+    EIGB_CUDA(cudaMemcpy2DAsync(bp, 8 * kp2, b, 8 * ldb, 8 * kk, nn, cudaMemcpyDeviceToDevice, st));
+    gemm_nt_ex(ap, kp2, bp, kp2, m, nn, kp2, c, ldc, colscale, colmap, tile_colmax, tcm_ld, st);
     EIGB_CUDA(cudaFreeAsync(ap, st));
     EIGB_CUDA(cudaFreeAsync(bp, st));
     return;
@@ -283,31 +319,37 @@ void gemm_nt_dev(const double* a, const double* b, int64_t m, int64_t nn, int64_
     use_tma = !(e && std::string(e) == "cpasync");
   }
   CUtensorMap ma, mb;
-  if (use_tma && kk <= INT32_MAX && m <= INT32_MAX && nn <= INT32_MAX && make_map(&ma, a, m, kk) &&
-      make_map(&mb, b, nn, kk)) {
+  if (use_tma && kk <= INT32_MAX && m <= INT32_MAX && nn <= INT32_MAX &&
+      make_map(&ma, a, m, kk, lda) && make_map(&mb, b, nn, kk, ldb)) {
     const size_t sm = sizeof(double) * TMA_STAGES * STAGE_DOUBLES + 2 * TMA_STAGES * 8 + 1024;
     EIGB_CUDA(cudaFuncSetAttribute(dmma_gemm_nt_tma_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    dmma_gemm_nt_tma_kernel<<<(unsigned)tiles, TMA_THREADS, sm, st>>>(ma, mb, m, nn, kk, c, ldc,
-                                                                      colscale, tile_colmax);
+    dmma_gemm_nt_tma_kernel<<<(unsigned)tiles, TMA_THREADS, sm, st>>>(
+        ma, mb, m, nn, kk, c, ldc, colscale, colmap, tile_colmax, tcm_ld);
     EIGB_LAUNCH_CHECK();
     return;
   }
   const size_t sm = sizeof(double) * STAGES * STAGE_DOUBLES;
   EIGB_CUDA(cudaFuncSetAttribute(dmma_gemm_nt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sm));
-  dmma_gemm_nt_kernel<<<(unsigned)tiles, GEMM_THREADS, sm, st>>>(a, b, m, nn, kk, c, ldc, colscale,
-                                                                tile_colmax);
+  dmma_gemm_nt_kernel<<<(unsigned)tiles, GEMM_THREADS, sm, st>>>(
+      a, b, m, nn, kk, lda, ldb, c, ldc, colscale, colmap, tile_colmax, tcm_ld);
   EIGB_LAUNCH_CHECK();
 }
 
 void sign_rule_dev(const double* tile_colmax, int64_t n, int64_t ncols, const int* mode, double* c,
                    int64_t ldc, DeviceScratch& ws, cudaStream_t st) {
+  sign_rule_ld(tile_colmax, ncols, n, ncols, mode, c, ldc, ws, st);
+}
+
+void sign_rule_ld(const double* tile_colmax, int64_t tcm_ld, int64_t n, int64_t ncols,
+                  const int* mode, double* c, int64_t ldc, DeviceScratch& ws, cudaStream_t st) {
   if (ncols <= 0) return;
   const int64_t tiles_m = cdiv(n, BM);
   double* flip = ws.get_f64("gemm_flip", ncols);
   int* any = ws.get_i32("gemm_any_flip", 1);
-  colsign_kernel<<<(unsigned)cdiv(ncols, 256), 256, 0, st>>>(tile_colmax, tiles_m, ncols, mode, flip);
+  colsign_kernel<<<(unsigned)cdiv(ncols, 256), 256, 0, st>>>(tile_colmax, tiles_m, tcm_ld, ncols,
+                                                             mode, flip);
   EIGB_LAUNCH_CHECK();
   EIGB_CUDA(cudaMemsetAsync(any, 0, 4, st));
   any_flip_kernel<<<(unsigned)cdiv(ncols, 256), 256, 0, st>>>(flip, ncols, any);

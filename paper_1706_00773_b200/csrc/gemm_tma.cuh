@@ -59,7 +59,9 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
     dmma_gemm_nt_tma_kernel(const __grid_constant__ CUtensorMap tma_a,
                             const __grid_constant__ CUtensorMap tma_b, int64_t m, int64_t nn,
                             int64_t K, double* __restrict__ c, int64_t ldc,
-                            const double* __restrict__ colscale, double* __restrict__ tile_colmax) {
+                            const double* __restrict__ colscale,
+                            const int64_t* __restrict__ colmap, double* __restrict__ tile_colmax,
+                            int64_t tcm_ld) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   double* smem = reinterpret_cast<double*>(
       (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -145,9 +147,10 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
   __syncthreads();
   double* colbest = smem;
   int* colrow = reinterpret_cast<int*>(smem + 2 * BN);
-  epilogue_store(acc, m, nn, c, ldc, colscale, m0, n0, wm, wn, g, t4, colbest, colrow);
+  epilogue_store(acc, m, nn, c, ldc, colscale, colmap, m0, n0, wm, wn, g, t4, colbest, colrow);
   __syncthreads();
-  if (tile_colmax && tid < BN) tile_colmax_write(tile_colmax, tm, nn, n0, tid, colbest, colrow);
+  if (tile_colmax && tid < BN)
+    tile_colmax_write(tile_colmax, tm, nn, tcm_ld, colmap, n0, tid, colbest, colrow);
 }
 
 // Driver entry point for tensor-map encoding (no -lcuda at link time).
@@ -171,12 +174,13 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 2D map of a row-major [rows][kk] FP64 matrix, box BK (k) x 128 (rows).
-bool make_map(CUtensorMap* map, const double* base, int64_t rows, int64_t kk) {
+// 2D map of a row-major [rows][kk] FP64 matrix with row pitch ld (even),
+// box BK (k) x 128 (rows); k beyond kk reads as zero.
+bool make_map(CUtensorMap* map, const double* base, int64_t rows, int64_t kk, int64_t ld) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)kk, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)kk * 8};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
   const cuuint32_t box[2] = {BK, 128};
   const cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides,

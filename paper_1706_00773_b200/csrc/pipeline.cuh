@@ -83,13 +83,44 @@ void build_xt_dev(const Plan& p, const RootRecords& roots, const Columns& cols,
                   int64_t c1, double* xt, double* colscale, int* colsign_mode, DeviceScratch& ws,
                   cudaStream_t st);
 
+// Compact back-transform (plans with decoupled columns): the roots [j0, j1)
+// and decoupled entries [e0, e1) whose final columns lie in [c0, c1), their
+// columns relative to c0, and the sign-rule mode of every column.
+struct CompactCols {
+  int64_t j0 = 0, j1 = 0, e0 = 0, e1 = 0;
+  int64_t* jpos = nullptr;  // [j1 - j0]
+  int64_t* epos = nullptr;  // [e1 - e0]
+  int* cmode = nullptr;     // [c1 - c0]
+};
+void compact_columns_dev(const Plan& p, const Columns& cols, int64_t c0, int64_t c1,
+                         CompactCols& cc, DeviceScratch& ws, cudaStream_t st);
+// Qa[:, r] = Q~[:, reduced row r] (n x nred, leading dimension lda) and the
+// decoupled columns of Q' (their row-tile maxima into tile_colmax, row
+// stride tcm_ld, columns relative to c0).
+void gather_qtilde_dev(const Plan& p, const double* q, const CompactCols& cc, double* qa,
+                       int64_t lda, double* q_out, int64_t ldq, double* tile_colmax,
+                       int64_t tcm_ld, cudaStream_t st);
+// Xt_red[j - j0, r] (leading dimension ldx) and colscale[j - j0] = 1/||x_j||.
+void build_xt_compact_dev(const Plan& p, const RootRecords& roots, const double* colldir,
+                          const int* collok, int64_t j0, int64_t j1, double* xt, int64_t ldx,
+                          double* colscale, DeviceScratch& ws, cudaStream_t st);
+
 // gemm.cu: C[:, c0:c1] = (A Xt^T) diag(scale) on the DMMA pipe; the
 // epilogue leaves per-(row tile, column) signed maxima in tile_colmax, and
 // sign_rule_dev applies the reference's sign rule (proj/src/eigvec.cpp:340-347)
 // to the columns whose mode is 1.
 void gemm_nt_dev(const double* a, const double* b, int64_t m, int64_t nn, int64_t kk, double* c,
                  int64_t ldc, const double* colscale, double* tile_colmax, cudaStream_t st);
+// General form: lda / ldb the operand row pitches (even), colmap (nullable)
+// the output column of each GEMM column, tile_colmax rows of tcm_ld entries
+// indexed by the output column.
+void gemm_nt_ex(const double* a, int64_t lda, const double* b, int64_t ldb, int64_t m, int64_t nn,
+                int64_t kk, double* c, int64_t ldc, const double* colscale, const int64_t* colmap,
+                double* tile_colmax, int64_t tcm_ld, cudaStream_t st);
 double* tile_colmax_buffer(int64_t n, int64_t ncols, DeviceScratch& ws);
+// tile_colmax rows of tcm_ld entries (the default: ncols)
+void sign_rule_ld(const double* tile_colmax, int64_t tcm_ld, int64_t n, int64_t ncols,
+                  const int* mode, double* c, int64_t ldc, DeviceScratch& ws, cudaStream_t st);
 void sign_rule_dev(const double* tile_colmax, int64_t n, int64_t ncols, const int* mode, double* c,
                    int64_t ldc, DeviceScratch& ws, cudaStream_t st);
 
