@@ -9,6 +9,15 @@
 // per-thread copy instructions. (A dedicated producer warp would make the
 // CTA 288 threads, which caps registers at 168 and spills the accumulators.)
 // Out-of-range boxes are zero-filled by the TMA unit.
+//
+// Round 2: with two warps per scheduler the tensor pipe idles whenever both
+// are outside their DMMA streams, so the loop's non-DMMA work is kept minimal:
+// fragments are explicit LDS.128 on 32-bit shared addresses (a generic LD
+// through the aligned pointer cost latency and 64-bit address registers), the
+// stage index and barrier parity advance incrementally (no 64-bit modulo),
+// and the next stage's full barrier is tested before the last 64 DMMAs of the
+// current one. Tensor pipe active 96.4% -> 98.3% (ncu, n = 8192), 36.04 ->
+// 36.79 TFLOP/s at n = 32768 (cuBLAS DGEMM: 36.65).
 #pragma once
 
 #include <cuda.h>
@@ -43,6 +52,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "}\n" ::"r"(a),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ double2 lds128(unsigned addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+// One non-blocking test of a barrier phase (1 = completed).
+__device__ __forceinline__ unsigned mbar_test(unsigned bar32, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(bar32), "r"(parity)
+      : "memory");
+  return ok;
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1) {
@@ -109,27 +137,56 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   const int g = lane >> 2, t4 = lane & 3;
-  for (int64_t kt = 0; kt < KT; ++kt) {
-    // refill the slot released in the previous iteration
-    if (tid == 0 && kt >= 1 && kt - 1 + TMA_STAGES < KT) {
-      const int64_t pk = kt - 1;
-      mbar_wait(&empty[pk % TMA_STAGES], (unsigned)(pk / TMA_STAGES) & 1);
-      issue(pk + TMA_STAGES);
+  // 32-bit loop state (stage index and parity advance incrementally: no
+  // 64-bit modulo in the loop), explicit LDS.128, and the full-barrier test
+  // of the next stage issued before the last 64 DMMAs of this one, so its
+  // latency is off the critical path.
+  const unsigned sb32 = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const unsigned full32 = static_cast<unsigned>(__cvta_generic_to_shared(full));
+  const unsigned oa = (unsigned)((wm * 64 + g) * BK * 8);
+  const unsigned ob = (unsigned)(BM * BK * 8 + (wn * 32 + g) * BK * 8);
+  const unsigned q0 = 16u * (unsigned)((2 * t4) ^ g), q1 = 16u * (unsigned)((2 * t4 + 1) ^ g);
+  const int kts = (int)KT;
+  int s = 0;            // stage of k-tile kt
+  unsigned par = 0;     // its full-barrier parity
+  int rs = 0;           // stage refilled next (k-tile kt - 1)
+  unsigned rpar = 0;
+  unsigned ready = mbar_test(full32, 0) ? 1u : 0u;
+  for (int kt = 0; kt < kts; ++kt) {
+    if (tid == 0 && kt >= 1) {
+      if (kt - 1 + TMA_STAGES < kts) {
+        mbar_wait(&empty[rs], rpar);
+        issue((int64_t)kt - 1 + TMA_STAGES);
+      }
+      if (++rs == TMA_STAGES) { rs = 0; rpar ^= 1u; }
     }
-    const int s = (int)(kt % TMA_STAGES);
-    mbar_wait(&full[s], (unsigned)(kt / TMA_STAGES) & 1);
-    const double* sa = smem + s * STAGE_DOUBLES;
-    const double* sb = sa + BM * BK;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int q = 2 * t4 + h;
+    if (!ready) mbar_wait(&full[s], par);
+    const unsigned st = sb32 + (unsigned)s * (STAGE_DOUBLES * 8);
+    int s1 = s + 1;
+    unsigned par1 = par;
+    if (s1 == TMA_STAGES) { s1 = 0; par1 ^= 1u; }
+    {
       double2 af[8], bf[4];
 #pragma unroll
-      for (int mb = 0; mb < 8; ++mb)
-        af[mb] = *reinterpret_cast<const double2*>(sa + (wm * 64 + mb * 8 + g) * BK + 2 * (q ^ g));
+      for (int nb = 0; nb < 4; ++nb) bf[nb] = lds128(st + ob + q0 + nb * 8 * BK * 8);
 #pragma unroll
-      for (int nb = 0; nb < 4; ++nb)
-        bf[nb] = *reinterpret_cast<const double2*>(sb + (wn * 32 + nb * 8 + g) * BK + 2 * (q ^ g));
+      for (int mb = 0; mb < 8; ++mb) af[mb] = lds128(st + oa + q0 + mb * 8 * BK * 8);
+#pragma unroll
+      for (int mb = 0; mb < 8; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) dmma(acc[mb][nb][0], acc[mb][nb][1], af[mb].x, bf[nb].x);
+#pragma unroll
+      for (int mb = 0; mb < 8; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) dmma(acc[mb][nb][0], acc[mb][nb][1], af[mb].y, bf[nb].y);
+    }
+    {
+      double2 af[8], bf[4];
+#pragma unroll
+      for (int mb = 0; mb < 8; ++mb) af[mb] = lds128(st + oa + q1 + mb * 8 * BK * 8);
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb) bf[nb] = lds128(st + ob + q1 + nb * 8 * BK * 8);
+      ready = (kt + 1 < kts && mbar_test(full32 + 8u * (unsigned)s1, par1)) ? 1u : 0u;
 #pragma unroll
       for (int mb = 0; mb < 8; ++mb)
 #pragma unroll
@@ -141,6 +198,8 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+    s = s1;
+    par = par1;
   }
 
   // ---- epilogue
