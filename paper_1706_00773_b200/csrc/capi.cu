@@ -228,19 +228,76 @@ __global__ void copy_block_kernel(const double* __restrict__ a, int64_t n, int64
 }
 
 // Column blocks [bstart[b], bstart[b + 1]) of an nc-column back-transform
-// whose blocks are copied to the host while the next block computes.
-std::vector<int64_t> gemm_blocks(const eigmod_b200_ctx* c, int64_t n, int64_t nc) {
-  // Block width: every block is a separate GEMM launch of 128 x 128 tiles
-  // (one CTA per SM), so a block whose tile count is not a multiple of the SM
-  // count leaves SMs idle in its last wave. Pick, among 6..16 blocks, the
-  // width (in 128-column tiles) that wastes the fewest tile slots.
-  // The last block's copy is not overlapped: it is kept narrow (a few column
-  // tiles, its own launch).
+// (inner dimension kk) whose blocks are copied to the host while the next
+// blocks compute.
+std::vector<int64_t> gemm_blocks(const eigmod_b200_ctx* c, int64_t n, int64_t nc, int64_t kk) {
+  // Every block is a separate GEMM launch of 128 x 128 tiles (one CTA per
+  // SM): a block whose tile count is not a multiple of the SM count leaves SMs
+  // idle in its last wave, and every launch ends with a drain. The copy of a
+  // block must only finish under the GEMMs of the blocks after it, and a
+  // column copies rho times faster than it multiplies (rho = 2 x [8 n bytes at
+  // ~52 GB/s] / [2 n kk flops at ~36 TFLOP/s], the 2 a safety factor), so the
+  // blocks can shrink geometrically towards the end: at most four, the last
+  // (whose copy is exposed) 2-4 column tiles, each earlier one at most
+  // (columns after it) / rho, chosen by exhaustive search for the fewest idle
+  // tile slots (n = 32768: 185 + 37 + 30 + 4 column tiles, 185 and 37 being
+  // whole waves of 148 x 256 row tiles). EIGMOD_B200_BLOCKS=equal selects the
+  // round-1 scheme of 6-16 equal blocks.
   const int64_t tiles_m = eigb::cdiv(n, 128), ctiles = eigb::cdiv(nc, 128);
   auto waste_of = [&](int64_t w_tiles) {
     const int64_t t = tiles_m * w_tiles;
     return eigb::cdiv(t, c->sms) * c->sms - t;
   };
+  std::vector<int64_t> bstart;  // block boundaries in columns
+  if (ctiles < 16) {
+    // small problems: the copy is short and the GEMM takes microseconds; one
+    // block avoids the per-block launches (GEMM, sign rule, copy)
+    bstart = {0, nc};
+    return bstart;
+  }
+  static int equal = -1;
+  if (equal < 0) {
+    const char* e = std::getenv("EIGMOD_B200_BLOCKS");
+    equal = (e && std::string(e) == "equal");
+  }
+  const double rho = std::min(2.0, std::max(0.02, 2.0 * 2769.0 / (double)std::max<int64_t>(kk, 1)));
+  if (!equal) {
+    int64_t best[4] = {0, 0, 0, 0}, best_cost = -1;
+    // a launch costs about as much as 32 idle tile slots of a full-size tile
+    const int64_t launch_cost = 32;
+    for (int64_t t4 = 2; t4 <= 4; ++t4) {
+      const int64_t lim3 = std::min<int64_t>(ctiles - t4, (int64_t)(t4 / rho));
+      for (int64_t b3 = 0; b3 <= lim3; ++b3) {
+        const int64_t after2 = t4 + b3;
+        const int64_t lim2 = std::min<int64_t>(ctiles - after2, (int64_t)(after2 / rho));
+        for (int64_t b2 = 0; b2 <= lim2; ++b2) {
+          const int64_t b1 = ctiles - after2 - b2;
+          if (b1 < 0 || (double)b1 * rho > (double)(after2 + b2)) continue;
+          if (b3 == 0 && b2 > 0) continue;  // canonical order: empty blocks first
+          int64_t cost = waste_of(t4) + launch_cost;
+          for (int64_t w : {b3, b2, b1})
+            if (w > 0) cost += waste_of(w) + launch_cost;
+          if (best_cost < 0 || cost < best_cost) {
+            best_cost = cost;
+            best[0] = b1, best[1] = b2, best[2] = b3, best[3] = t4;
+          }
+        }
+      }
+    }
+    if (best_cost >= 0) {
+      int64_t a = 0;
+      bstart.push_back(0);
+      for (int i = 0; i < 4; ++i)
+        if (best[i] > 0) {
+          a += best[i];
+          bstart.push_back(std::min(a * 128, nc));
+        }
+      bstart.back() = nc;
+      return bstart;
+    }
+  }
+  // 6-16 equal blocks and a narrow last one (also the fallback when the copy
+  // is too slow relative to the GEMM for four geometric blocks)
   int64_t tail = 0;
   if (ctiles >= 32) {
     tail = 2;
@@ -255,15 +312,8 @@ std::vector<int64_t> gemm_blocks(const eigmod_b200_ctx* c, int64_t n, int64_t nc
     for (int64_t a = 0; a < main_tiles; a += w) waste += waste_of(std::min(w, main_tiles - a));
     if (best_waste < 0 || waste < best_waste) best_waste = waste, best_w = w;
   }
-  std::vector<int64_t> bstart;  // block boundaries in columns
-  if (ctiles < 16) {
-    // small problems: the copy is short and the GEMM takes microseconds; one
-    // block avoids the per-block launches (GEMM, sign rule, copy)
-    bstart.push_back(0);
-  } else {
-    for (int64_t a = 0; a < main_tiles; a += best_w) bstart.push_back(a * 128);
-    if (tail) bstart.push_back(main_tiles * 128);
-  }
+  for (int64_t a = 0; a < main_tiles; a += best_w) bstart.push_back(a * 128);
+  if (tail) bstart.push_back(main_tiles * 128);
   bstart.push_back(nc);
   return bstart;
 }
@@ -305,7 +355,7 @@ void finish_compact(eigmod_b200_ctx* c, const eigb::Columns& cols, const double*
   // first root of the block (0 for the first) to the first root of the next
   // (nc for the last), decoupled columns in between already gathered
   if (!c->copy) EIGB_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
-  std::vector<int64_t> rb = gemm_blocks(c, n, nr);
+  std::vector<int64_t> rb = gemm_blocks(c, n, nr, nred);
   if (nr == 0) rb = {0, 0};
   std::vector<int64_t> jpos(std::max<int64_t>(nr, 1), 0);
   if (nr > 0) {
@@ -388,7 +438,7 @@ void finish(eigmod_b200_ctx* c, const double* q, const double* lam_in, int64_t c
     return;
   }
   if (!c->copy) EIGB_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
-  const std::vector<int64_t> bstart = gemm_blocks(c, n, nc);
+  const std::vector<int64_t> bstart = gemm_blocks(c, n, nc, n);
   const int64_t nb = (int64_t)bstart.size() - 1;
   while ((int64_t)c->blk_ev.size() < nb) {
     cudaEvent_t e;
