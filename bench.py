@@ -426,10 +426,10 @@ def _hbm_peak():
 
 def _ncu_gemm_traffic(n):
     """dram__bytes_read.sum + dram__bytes_write.sum of one K5 launch from the
-    committed ncu --set full capture (profiles/ncu_full_cfg4_n32768_r01.json,
-    tools/profile_case.py --n 32768), when this run has that n; else None."""
+    committed ncu --set full capture (profiles/ncu_full_k5_cfg4_n32768_r02.json,
+    tools/gemm_one.py 32768), when this run has that n; else None."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                        "ncu_full_cfg4_n32768_r01.json")
+                        "ncu_full_k5_cfg4_n32768_r02.json")
     if n != 32768 or not os.path.exists(path):
         return None
     with open(path) as f:

@@ -65,8 +65,16 @@ int eigmod_b200_ctx_use_own_stream(eigmod_b200_ctx* ctx);
  * solver batches pack their slots), "spec_plan" (1: one host round trip for
  * the one-shot plan), "fuse_alpha" (1:
  * one-shot updates in exact mode take the residues of the scalar presolve
- * from the pole-limit count pass instead of a separate K2 pass). Unknown keys
- * fail with a message. */
+ * from the pole-limit count pass instead of a separate K2 pass),
+ * "compact_gemm" (1: plans with at least 64 decoupled pairs build those
+ * columns of Q' by copying / rotating Q's columns and multiply only the
+ * reduced rows, Q'[:, roots] = Q~_red X_red; 0: the reference's dense n x n
+ * product, eigvec.cpp:285-339). Environment (read once per process):
+ * EIGMOD_B200_GEMM=cpasync (the cp.async K5 kernel instead of TMA),
+ * EIGMOD_B200_GEMM_GROUP (row tiles per rasterization group of K5, 4),
+ * EIGMOD_B200_BLOCKS=equal (host path: 6-16 equal column blocks instead of
+ * at most four shrinking ones), EIGMOD_B200_XT=v1|v2|v3 (older K4 kernels).
+ * Unknown keys fail with a message. */
 int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value);
 const char* eigmod_b200_last_error(const eigmod_b200_ctx* ctx);
 const char* eigmod_b200_last_stage(const eigmod_b200_ctx* ctx);

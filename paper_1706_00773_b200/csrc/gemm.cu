@@ -324,8 +324,13 @@ void gemm_nt_ex(const double* a, int64_t lda, const double* b, int64_t ldb, int6
     const size_t sm = sizeof(double) * TMA_STAGES * STAGE_DOUBLES + 2 * TMA_STAGES * 8 + 1024;
     EIGB_CUDA(cudaFuncSetAttribute(dmma_gemm_nt_tma_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    static int group = 0;  // EIGMOD_B200_GEMM_GROUP: row tiles per rasterization group
+    if (group == 0) {
+      const char* e = std::getenv("EIGMOD_B200_GEMM_GROUP");
+      group = e ? std::max(1, std::atoi(e)) : 4;
+    }
     dmma_gemm_nt_tma_kernel<<<(unsigned)tiles, TMA_THREADS, sm, st>>>(
-        ma, mb, m, nn, kk, c, ldc, colscale, colmap, tile_colmax, tcm_ld);
+        ma, mb, m, nn, kk, c, ldc, colscale, colmap, tile_colmax, tcm_ld, group);
     EIGB_LAUNCH_CHECK();
     return;
   }

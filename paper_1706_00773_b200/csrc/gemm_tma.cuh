@@ -18,6 +18,14 @@
 // and the next stage's full barrier is tested before the last 64 DMMAs of the
 // current one. Tensor pipe active 96.4% -> 98.3% (ncu, n = 8192), 36.04 ->
 // 36.79 TFLOP/s at n = 32768 (cuBLAS DGEMM: 36.65).
+//
+// Rasterization: groups of `group_rows` row tiles sweep the column tiles, so
+// consecutive CTAs share a B panel. The CTAs of a launch drift apart in k
+// (tiles start whenever an SM frees up), and only CTAs a few launches apart
+// still find each other's panel slices in L2: DRAM reads per launch at
+// n = 32768 are 2.40 / 1.52 / 1.39 / 1.53 / 1.45 / 1.84 / 2.08 / 2.28 TB for
+// groups of 1 / 2 / 3 / 4 / 6 / 8 / 16 / 32 row tiles (ncu), the time the same
+// (tensor-bound) for all; 4 is the default (EIGMOD_B200_GEMM_GROUP).
 #pragma once
 
 #include <cuda.h>
@@ -89,7 +97,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
                             int64_t K, double* __restrict__ c, int64_t ldc,
                             const double* __restrict__ colscale,
                             const int64_t* __restrict__ colmap, double* __restrict__ tile_colmax,
-                            int64_t tcm_ld) {
+                            int64_t tcm_ld, int group_rows) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   double* smem = reinterpret_cast<double*>(
       (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -98,7 +106,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t tiles_m = cdiv_dev(m, BM), tiles_n = cdiv_dev(nn, BN);
   const int64_t pid = blockIdx.x;
-  const int64_t group = 8;
+  const int64_t group = group_rows;
   const int64_t per_group = group * tiles_n;
   const int64_t gidx = pid / per_group;
   const int64_t first_m = gidx * group;
