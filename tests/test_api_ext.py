@@ -231,7 +231,10 @@ def test_gemm_variants():
     from paper_1706_00773_b200 import capi
 
     rng = np.random.default_rng(4)
-    for m, nn, kk in ((1, 1, 1), (37, 5, 13), (130, 257, 64), (64, 64, 1)):
+    # kk = 97 .. 1000: 7 .. 63 k-tiles, the 6-stage TMA ring refills and its
+    # barrier parities wrap (the K5 main loop's incremental stage state)
+    for m, nn, kk in ((1, 1, 1), (37, 5, 13), (130, 257, 64), (64, 64, 1), (130, 140, 97),
+                      (129, 128, 200), (256, 130, 1000)):
         a = rng.standard_normal((m, kk))
         b = rng.standard_normal((kk, nn))
         assert np.abs(capi.gemm(a, b) - a @ b).max() <= 1e-12 * kk
