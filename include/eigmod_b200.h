@@ -63,7 +63,9 @@ int eigmod_b200_ctx_use_own_stream(eigmod_b200_ctx* ctx);
  * converged when |sigma| <= noise_c eps (1 + sum_i |u_i|^2 |D_i|), the
  * rounding level of the pole sum; 0 disables), "compact" (1: drained
  * solver batches pack their slots), "spec_plan" (1: one host round trip for
- * the one-shot plan), "fuse_alpha" (1:
+ * the one-shot plan), "plan_par" (-1: the plan's classification, reduced-
+ * problem assembly and clips run on many CTAs from n >= 8192 on; 0 never,
+ * 1 always), "fuse_alpha" (1:
  * one-shot updates in exact mode take the residues of the scalar presolve
  * from the pole-limit count pass instead of a separate K2 pass),
  * "compact_gemm" (1: plans with at least 64 decoupled pairs build those

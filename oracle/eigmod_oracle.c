@@ -1133,7 +1133,18 @@ int eo_update(const double* q, const double* lambda, const double* kmat, const i
           ++which;
       /* origin on a multiple pole: the shifted bordered system */
       const int64_t oj = rorig[j];
-      const int multi = (oj > 0 && d[oj - 1] == d[oj]) || (oj + 1 < N && d[oj + 1] == d[oj]);
+      int multi = (oj > 0 && d[oj - 1] == d[oj]) || (oj + 1 < N && d[oj + 1] == d[oj]);
+      if (multi && !rcol[j]) {
+        /* only next to the pole: |delta| below 1e-6 of the coupling of its
+         * rows; far roots take the formula (the bordered system loses ~1e-9
+         * at large delta) */
+        double ur2 = 0.0;
+        for (int64_t r = oj; r >= 0 && d[r] == d[oj]; --r)
+          for (int64_t c2 = 0; c2 < ke; ++c2) ur2 += ut[r * ke + c2] * ut[r * ke + c2];
+        for (int64_t r = oj + 1; r < N && d[r] == d[oj]; ++r)
+          for (int64_t c2 = 0; c2 < ke; ++c2) ur2 += ut[r * ke + c2] * ut[r * ke + c2];
+        multi = fabs(rdel[j]) < 1e-6 * ur2;
+      }
       if (rcol[j]) ok = collision_vector(d, ut, sg, N, ke, oj, 0.0, merge_gap, which, xr);
       else if (multi) ok = collision_vector(d, ut, sg, N, ke, oj, rdel[j], 0.0, 0, xr);
       if (rcol[j] && !ok) {

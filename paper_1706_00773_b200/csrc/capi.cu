@@ -66,6 +66,7 @@ void plan_from_u(eigmod_b200_ctx* c, const double* lam, const double* u, const i
       EIGB_CUDA(cudaMemsetAsync(p.alpha, 0, 8 * std::max<int64_t>(p.ng, 1), c->stream));
     else
       eigb::build_plan_weights(p, 0, p.ng, p.alpha, c->ws, c->stream);
+    p.par_mode = c->sopt.plan_par;
     eigb::build_plan_finish(p, c->lam, c->ws, c->stream);
     if (p.spec_failed) continue;
     c->have_plan = true;
@@ -642,6 +643,8 @@ int eigmod_b200_set_option(eigmod_b200_ctx* ctx, const char* key, double value) 
       ctx->sopt.fpre_rel = value;
     } else if (std::string(key) == "spec_plan") {
       ctx->sopt.spec_plan = value != 0.0;
+    } else if (std::string(key) == "plan_par") {
+      ctx->sopt.plan_par = (int)value;
     } else if (std::string(key) == "noise_c") {
       ctx->sopt.noise_c = value;
     } else if (std::string(key) == "compact") {
@@ -1074,6 +1077,7 @@ int eigmod_b200_plan_finish_device(eigmod_b200_ctx* ctx, const double* d_alpha_a
     if (d_alpha_all != p.alpha)
       EIGB_CUDA(cudaMemcpyAsync(p.alpha, d_alpha_all, 8 * p.ng, cudaMemcpyDeviceToDevice,
                                 ctx->stream));
+    p.par_mode = ctx->sopt.plan_par;
     eigb::build_plan_finish(p, ctx->lam, ctx->ws, ctx->stream);
     ctx->have_plan = true;
     *nred_out = p.nred;

@@ -414,6 +414,7 @@ __global__ void repack_kernel(const double* __restrict__ u, int64_t n, int kp, c
 // Single-CTA planning kernel: scale, run boundaries, groups, representatives.
 // groups are emitted in ascending order; rep_row[i] = representative of row i.
 constexpr int kPlanThreads = 1024;
+constexpr int64_t kPlanParMinN = 8192;  // parallel plan finish from here on (build_plan_finish)
 
 __device__ double block_max(double v, double* red) {
   v = warp_max(v);
@@ -793,6 +794,199 @@ __global__ void clips_kernel(const double* __restrict__ d, const double* __restr
   }
 }
 
+
+// ---- parallel plan finish (n >= kPlanParMinN): the single-CTA kernels above
+// take 0.3-0.8 ms each at n = 32768 (one SM's worth of latency-bound loops),
+// and every rank of a multi-GPU update repeats them. Same decisions per
+// group; the three sums (|alpha|, ||U||_F^2, the signed column masses of the
+// clips) are per-CTA partials over kPlanParBlocks fixed slices added in slice
+// order, so they are deterministic for a given n but round differently from
+// the single-CTA sums (they feed thresholds and the 1e-9-padded outer clips).
+constexpr int kPlanParBlocks = 64;
+constexpr int kPlanParThreads = 256;
+
+__global__ void __launch_bounds__(kPlanParThreads) plan_sums_kernel(
+    const double* __restrict__ u, int64_t n, int kp, int k, const double* __restrict__ alpha,
+    const int64_t* __restrict__ counts, double* __restrict__ part) {
+  __shared__ double red[32];
+  const int64_t ng = counts[0];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double am = 0.0, um = 0.0;
+  for (int64_t g = t0; g < ng; g += stride) am += fabs(alpha[g]);
+  for (int64_t i = t0; i < n; i += stride)
+    for (int r = 0; r < k; ++r) um = fma(u[i * kp + r], u[i * kp + r], um);
+  am = block_sum(am, red);
+  um = block_sum(um, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = am;
+    part[2 * blockIdx.x + 1] = um;
+  }
+}
+
+__global__ void __launch_bounds__(kPlanParThreads) classify_par_kernel(
+    const double* __restrict__ u, int kp, int k, const double* __restrict__ alpha,
+    const int64_t* __restrict__ gstart, const int64_t* __restrict__ glen,
+    const int64_t* __restrict__ counts, int exact, const double* __restrict__ part, int nparts,
+    int* __restrict__ kind, double* __restrict__ scal) {
+  __shared__ double sums[2];
+  if (threadIdx.x == 0) {
+    double am = 0.0, um = 0.0;
+    for (int b = 0; b < nparts; ++b) {
+      am += part[2 * b];
+      um += part[2 * b + 1];
+    }
+    sums[0] = am;
+    sums[1] = um;
+  }
+  __syncthreads();
+  const double alpha_mass = sums[0];
+  const double fn = sqrt(sums[1]);
+  const double u_mass = fn * fn;
+  const double drop = kWeightDeflationRel * (1.0 + alpha_mass);
+  const double scale = scal[0];
+  const int64_t ng = counts[0];
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < ng) {  // the rules of classify_kernel
+    int kd = 0;
+    if (exact) {
+      double row_mass = 0.0;
+      for (int64_t i = gstart[g]; i < gstart[g] + glen[g]; ++i)
+        for (int r = 0; r < k; ++r) row_mass += u[i * kp + r] * u[i * kp + r];
+      kd = (sqrt(row_mass) * fn <= kExactCouplingRel * scale) ? 1 : 0;
+    } else if (fabs(alpha[g]) <= drop) {
+      double row_mass = 0.0;
+      for (int64_t i = gstart[g]; i < gstart[g] + glen[g]; ++i)
+        for (int r = 0; r < k; ++r) row_mass += u[i * kp + r] * u[i * kp + r];
+      kd = (row_mass <= kRowMassRel * (1.0 + u_mass)) ? 1 : 2;
+    }
+    kind[g] = kd;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    scal[1] = alpha_mass;
+    scal[2] = u_mass;
+    scal[3] = fn;
+  }
+}
+
+__global__ void __launch_bounds__(kPlanParThreads) assemble_count_kernel(
+    const int64_t* __restrict__ glen, const int* __restrict__ kind,
+    const int64_t* __restrict__ rank, const int64_t* __restrict__ counts,
+    int64_t* __restrict__ tmp_a, int64_t* __restrict__ tmp_b) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= counts[0]) return;
+  const int64_t m = glen[g];
+  int64_t nr, nd;
+  if (kind[g] == 1) nr = 0, nd = m;
+  else if (m == 1) nr = 1, nd = 0;
+  else nr = rank[g], nd = m - rank[g];
+  tmp_a[g] = nr;
+  tmp_b[g] = nd;
+}
+
+__global__ void __launch_bounds__(kPlanThreads) assemble_scan_kernel(
+    const int64_t* __restrict__ tmp_a, const int64_t* __restrict__ tmp_b, int64_t* counts,
+    int64_t* __restrict__ off_red, int64_t* __restrict__ off_dec) {
+  __shared__ int64_t sh[kPlanThreads];
+  __shared__ int64_t nred, ndec;
+  const int64_t ng = counts[0];
+  block_exclusive_scan(tmp_a, off_red, ng, &nred, sh);
+  __syncthreads();
+  block_exclusive_scan(tmp_b, off_dec, ng, &ndec, sh);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    counts[1] = nred;
+    counts[2] = ndec;
+  }
+}
+
+// The scatter of assemble_reduced_kernel, one thread per group.
+__global__ void __launch_bounds__(kPlanParThreads) assemble_scatter_kernel(
+    const double* __restrict__ lam, const double* __restrict__ u, int kp,
+    const int64_t* __restrict__ gstart, const int64_t* __restrict__ glen,
+    const double* __restrict__ gval, const int* __restrict__ kind,
+    const int64_t* __restrict__ rank, const int64_t* __restrict__ roff,
+    const double* __restrict__ rbuf, const int64_t* __restrict__ counts,
+    const int64_t* __restrict__ off_red, const int64_t* __restrict__ off_dec,
+    const double* __restrict__ alpha, double* __restrict__ alpha_red, double* __restrict__ d,
+    double* __restrict__ ur, int64_t* __restrict__ red_src, double* __restrict__ dec_val,
+    int64_t* __restrict__ dec_src, int64_t* __restrict__ orig_map) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= counts[0]) return;
+  const int64_t m = glen[g], s0 = gstart[g];
+  const int64_t pr = off_red[g], pd = off_dec[g];
+  if (kind[g] == 1) {
+    for (int64_t i = 0; i < m; ++i) {
+      dec_val[pd + i] = lam[s0 + i];
+      dec_src[pd + i] = s0 + i;
+      orig_map[s0 + i] = -1;
+    }
+  } else if (m == 1) {
+    d[pr] = lam[s0];
+    alpha_red[pr] = alpha[g];
+    for (int c = 0; c < kp; ++c) ur[pr * kp + c] = u[s0 * kp + c];
+    red_src[pr] = s0;
+    orig_map[s0] = pr;
+  } else {
+    const int64_t r = rank[g];
+    const double* B = rbuf + roff[g];
+    for (int64_t t = 0; t < r; ++t) {
+      d[pr + t] = gval[g];
+      alpha_red[pr + t] = 0.0;
+      for (int c = 0; c < kp; ++c) ur[(pr + t) * kp + c] = B[t * kp + c];
+      red_src[pr + t] = -(g * 65536 + t) - 2;
+    }
+    for (int64_t t = r; t < m; ++t) {
+      dec_val[pd + t - r] = gval[g];
+      dec_src[pd + t - r] = -(g * 65536 + t) - 2;
+    }
+    for (int64_t i = 0; i < m; ++i) orig_map[s0 + i] = -2 - g;
+  }
+}
+
+__global__ void __launch_bounds__(kPlanParThreads) clips_part_kernel(
+    const double* __restrict__ d, const double* __restrict__ ur,
+    const int64_t* __restrict__ counts, int kp, int k, const int* __restrict__ sgn,
+    double* __restrict__ part) {
+  __shared__ double red[32];
+  const int64_t nr = counts[1];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double pos = 0.0, neg = 0.0, m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += stride) {
+    for (int c = 0; c < k; ++c) {
+      const double v = ur[i * kp + c] * ur[i * kp + c];
+      if (sgn[c] > 0) pos += v; else neg += v;
+    }
+    m = fmax(m, fabs(d[i]));
+  }
+  pos = block_sum(pos, red);
+  neg = block_sum(neg, red);
+  m = block_max(m, red);
+  if (threadIdx.x == 0) {
+    part[3 * blockIdx.x] = pos;
+    part[3 * blockIdx.x + 1] = neg;
+    part[3 * blockIdx.x + 2] = m;
+  }
+}
+
+__global__ void clips_final_kernel(const double* __restrict__ d,
+                                   const int64_t* __restrict__ counts,
+                                   const double* __restrict__ part, int nparts,
+                                   double* __restrict__ scal) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int64_t nr = counts[1];
+  double pos = 0.0, neg = 0.0, m = 0.0;
+  for (int b = 0; b < nparts; ++b) {
+    pos += part[3 * b];
+    neg += part[3 * b + 1];
+    m = fmax(m, part[3 * b + 2]);
+  }
+  m = fmax(m, pos + neg);
+  const double pad = 1e-9 * (m > 0.0 ? m : 1.0);
+  scal[4] = (nr > 0) ? d[0] - neg * (1.0 + 1e-12) - pad : 0.0;
+  scal[5] = (nr > 0) ? d[nr - 1] + pos * (1.0 + 1e-12) + pad : 0.0;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ host side
@@ -865,8 +1059,20 @@ void build_plan_finish(Plan& p, const double* lam, DeviceScratch& ws, cudaStream
   const int kp = p.kp, k = p.k;
   const int64_t n = p.n, ng = p.ng;
   p.kind = ws.get_i32("pl_kind", ng);
-  classify_kernel<<<1, kPlanThreads, 0, st>>>(p.u, n, kp, k, p.alpha, p.gstart, p.glen, p.counts,
-                                               p.exact ? 1 : 0, p.kind, p.scal);
+  const bool par = p.par_mode < 0 ? n >= kPlanParMinN : p.par_mode != 0;
+  const unsigned gblocks = (unsigned)cdiv(std::max<int64_t>(ng, 1), kPlanParThreads);
+  double* part = par ? ws.get_f64("pl_part", 3 * kPlanParBlocks) : nullptr;
+  if (par) {
+    plan_sums_kernel<<<kPlanParBlocks, kPlanParThreads, 0, st>>>(p.u, n, kp, k, p.alpha, p.counts,
+                                                                 part);
+    EIGB_LAUNCH_CHECK();
+    classify_par_kernel<<<gblocks, kPlanParThreads, 0, st>>>(p.u, kp, k, p.alpha, p.gstart, p.glen,
+                                                             p.counts, p.exact ? 1 : 0, part,
+                                                             kPlanParBlocks, p.kind, p.scal);
+  } else {
+    classify_kernel<<<1, kPlanThreads, 0, st>>>(p.u, n, kp, k, p.alpha, p.gstart, p.glen, p.counts,
+                                                 p.exact ? 1 : 0, p.kind, p.scal);
+  }
   EIGB_LAUNCH_CHECK();
 
   // multi-member runs (their count came back with ng): host-side offsets,
@@ -919,13 +1125,30 @@ void build_plan_finish(Plan& p, const double* lam, DeviceScratch& ws, cudaStream
   int64_t* tb = ws.get_i64("pl_tmpb", ng);
   p.off_red = ws.get_i64("pl_off_red", ng);
   p.off_dec = ws.get_i64("pl_off_dec", ng);
-  assemble_reduced_kernel<<<1, kPlanThreads, 0, st>>>(
-      lam, p.u, n, kp, p.gstart, p.glen, p.gval, p.kind, p.rank, p.roff, p.rbuf, p.counts, ta, tb,
-      p.off_red, p.off_dec, p.alpha, p.alpha_red, p.d, p.ur, p.red_src, p.dec_val, p.dec_src,
-      p.orig_map);
-  EIGB_LAUNCH_CHECK();
-  clips_kernel<<<1, kPlanThreads, 0, st>>>(p.d, p.ur, p.counts, kp, k, p.sgn, p.scal);
-  EIGB_LAUNCH_CHECK();
+  if (par) {
+    assemble_count_kernel<<<gblocks, kPlanParThreads, 0, st>>>(p.glen, p.kind, p.rank, p.counts, ta,
+                                                               tb);
+    EIGB_LAUNCH_CHECK();
+    assemble_scan_kernel<<<1, kPlanThreads, 0, st>>>(ta, tb, p.counts, p.off_red, p.off_dec);
+    EIGB_LAUNCH_CHECK();
+    assemble_scatter_kernel<<<gblocks, kPlanParThreads, 0, st>>>(
+        lam, p.u, kp, p.gstart, p.glen, p.gval, p.kind, p.rank, p.roff, p.rbuf, p.counts, p.off_red,
+        p.off_dec, p.alpha, p.alpha_red, p.d, p.ur, p.red_src, p.dec_val, p.dec_src, p.orig_map);
+    EIGB_LAUNCH_CHECK();
+    clips_part_kernel<<<kPlanParBlocks, kPlanParThreads, 0, st>>>(p.d, p.ur, p.counts, kp, k, p.sgn,
+                                                                  part);
+    EIGB_LAUNCH_CHECK();
+    clips_final_kernel<<<1, 32, 0, st>>>(p.d, p.counts, part, kPlanParBlocks, p.scal);
+    EIGB_LAUNCH_CHECK();
+  } else {
+    assemble_reduced_kernel<<<1, kPlanThreads, 0, st>>>(
+        lam, p.u, n, kp, p.gstart, p.glen, p.gval, p.kind, p.rank, p.roff, p.rbuf, p.counts, ta, tb,
+        p.off_red, p.off_dec, p.alpha, p.alpha_red, p.d, p.ur, p.red_src, p.dec_val, p.dec_src,
+        p.orig_map);
+    EIGB_LAUNCH_CHECK();
+    clips_kernel<<<1, kPlanThreads, 0, st>>>(p.d, p.ur, p.counts, kp, k, p.sgn, p.scal);
+    EIGB_LAUNCH_CHECK();
+  }
   // one round trip for the sizes, the scales and (with multi-member runs) the
   // run ranks and kinds; a speculative plan also learns its group count and
   // whether its assumptions held

@@ -336,7 +336,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) collision_kernel(
   }
 }
 
-// mark[j]: bit 0 collided (flag), bit 1 origin on a multiple pole, bit 2 the
+// mark[j]: bit 0 collided (flag), bit 1 origin on a multiple pole and the root
+// within 1e-6 of its rows' coupling, bit 2 the
 // root is so close to its pole that the formula's y loses the small
 // components (|delta| < 1e-6 |u_o|^2: S(lambda) has a term |u_o|^2/|delta|
 // above 1e6 times its O(1) part); which[j]: earlier collided roots on the
@@ -352,10 +353,23 @@ __global__ void bordered_mark_kernel(const double* __restrict__ d, const double*
   const int64_t o = origin[j];
   const double v = d[o];
   const bool coll = (flags[j] & 1) != 0;
-  const bool multi = allow_multi && ((o > 0 && d[o - 1] == v) || (o + 1 < N && d[o + 1] == v));
+  bool multi = allow_multi && ((o > 0 && d[o - 1] == v) || (o + 1 < N && d[o + 1] == v));
   double uo2 = 0.0;
   for (int c = 0; c < kp; ++c) uo2 += u[o * kp + c] * u[o * kp + c];
   const bool near = allow_multi && !coll && fabs(rdelta[j]) < 1e-6 * uo2;
+  if (multi && !coll) {
+    // the same rule for a multiple pole, with the coupling of all its rows: a
+    // root far from it (|delta| >= 1e-6 sum |u_r|^2, e.g. the outer roots of
+    // an update much larger than A) takes the formula, whose y is accurate
+    // there; the bordered system loses ~1e-9 at such delta
+    // (tests/test_stress.py::test_far_roots_of_a_clustered_spectrum)
+    double ur2 = uo2;
+    for (int64_t r = o - 1; r >= 0 && d[r] == v; --r)
+      for (int c = 0; c < kp; ++c) ur2 += u[r * kp + c] * u[r * kp + c];
+    for (int64_t r = o + 1; r < N && d[r] == v; ++r)
+      for (int c = 0; c < kp; ++c) ur2 += u[r * kp + c] * u[r * kp + c];
+    multi = fabs(rdelta[j]) < 1e-6 * ur2;
+  }
   mark[j] = (coll ? 1 : 0) | (multi ? 2 : 0) | (near ? 4 : 0);
   collok[j] = 0;
   int w = 0;

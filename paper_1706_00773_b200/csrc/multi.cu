@@ -157,6 +157,7 @@ void rank_update(eigmod_b200_multi* mg, int g, const double* q, const double* la
     if (g1 > g0) eigb::build_plan_weights(p, g0, g1, a_part, c->ws, st);
     EIGB_NCCL(nc, nc->AllGather(a_part, a_all, (size_t)gc, ncclDouble, comm, st));
     EIGB_CUDA(cudaMemcpyAsync(p.alpha, a_all, 8 * p.ng, cudaMemcpyDeviceToDevice, st));
+    p.par_mode = c->sopt.plan_par;
     eigb::build_plan_finish(p, c->lam, c->ws, st);
     c->have_plan = true;
   }

@@ -40,6 +40,7 @@ struct Plan {
   // verdict back with the plan's sizes (one host round trip for the plan).
   // spec_failed: an assumption failed, the caller rebuilds the plan.
   bool spec = false, spec_failed = false;
+  int par_mode = -1;  // plan finish on many CTAs: -1 from n >= 8192, 0 never, 1 always (option "plan_par")
   const double* norms_dev = nullptr;  // squared column norms of U (spec)
 
   ReducedView view() const {

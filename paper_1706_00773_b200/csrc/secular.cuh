@@ -113,6 +113,9 @@ struct SolveOptions {
   bool fuse_alpha = true;
   // fused one-shot plans: sizes and the column-drop decision read back once
   bool spec_plan = true;
+  // plan finish (classification, reduced-problem assembly, clips) on many
+  // CTAs: -1 from n >= 8192 on, 0 never, 1 always
+  int plan_par = -1;
 };
 
 // Diagnostics trace of one root: per evaluation kTraceCols doubles
