@@ -595,7 +595,18 @@ __device__ void slot_init(SolveSmem& s, double* y, int b, int64_t j, const Solve
   s.lo_ok[b] = lok;
   s.hi_ok[b] = hok;
   if (lok && hok && s.ph[b] == s.pl[b]) {
-    const int fs = a.f_state ? a.f_state[j - a.j0] : 0;
+    int fs = a.f_state ? a.f_state[j - a.j0] : 0;
+    if (fs != 0) {
+      // The presolved point is only trusted away from the bracket's ends: the
+      // scalar f (residues with rounding; values of 1e20 on spectra graded over
+      // many decades) can send its sign bisection into a pole, and an S
+      // evaluation at 1e-20 of the interval from a pole has no meaningful
+      // inertia (the pole's own term swamps the rest), so its count would
+      // collapse the bracket onto the pole (stress seeds 7306, 7477, 7666).
+      const double dob = d[a.f_o[j - a.j0]], fd = a.f_delta[j - a.j0];
+      const double margin = 1e-9 * (hi - lo);
+      if (!((dob - lo) + fd >= margin && (hi - dob) - fd >= margin)) fs = 0;
+    }
     if (fs != 0) enter_phase_b_at<KP>(s, b, a, a.f_o[j - a.j0], a.f_delta[j - a.j0], fs == 2);
     else enter_phase_b<KP>(s, b, a, 0.5 * (lo + hi));
   } else {

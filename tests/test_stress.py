@@ -175,6 +175,29 @@ def test_far_roots_of_a_clustered_spectrum(seed):
     assert np.abs(res.q.T @ res.q - np.eye(n)).max() <= 1e-9
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [7306, 7477, 7666])
+def test_graded_spectrum_presolve_guard(seed):
+    """Spectra graded over eight decades with k = 13 (padded to 16, where the
+    scalar f presolve runs): f reaches 1e20 and its sign bisection ran into a
+    pole; the S evaluation 1e-26 from that pole has no meaningful inertia and
+    its count collapsed the bracket onto the pole (a root 5% off, two equal
+    vectors). The solver now ignores a presolved point within 1e-9 of the
+    bracket from its ends (secular.cu refill). Found by tools/stress_sweep.py."""
+    from paper_1706_00773_b200 import capi
+
+    q, lam, kmat, signs, kind = _case(seed)
+    n = len(lam)
+    res = capi.update_decomposition(q, lam, kmat, signs, 1e-12)
+    a = (q * lam) @ q.T + (kmat * signs) @ kmat.T
+    a = 0.5 * (a + a.T)
+    ev = np.linalg.eigvalsh(a)
+    nrm = float(np.abs(ev).max())
+    assert np.abs(res.lam - ev).max() <= 1e-10 * nrm
+    assert residual(a, res.q, res.lam, nrm) <= 1e-10
+    assert np.abs(res.q.T @ res.q - np.eye(n)).max() <= 1e-9
+
+
 def test_oracle_far_roots_of_a_clustered_spectrum():
     """The same case through the CPU oracle (it shares the vector rules)."""
     q, lam, kmat, signs, kind = _case(7008)
